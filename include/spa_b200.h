@@ -1,0 +1,166 @@
+/*
+ * libspa_b200 -- C ABI of the B200-native SMC lambda-path sampler.
+ *
+ * The reference (`spa` 0.1.0) is pure Python/NumPy and has no FFI of its
+ * own.  Each entry point below replaces one reference
+ * function on the hot path (cited as reference file:line); the Python host
+ * package `paper_1106_0322_b200` binds them with ctypes and keeps the
+ * reference's public surface (`run_sampler`, `reweight`, `ess`,
+ * `systematic_resample_indices`, `smc_step`, ...).
+ *
+ * Conventions (all entry points):
+ *   - every pointer is a DEVICE pointer owned by the caller (no allocation
+ *     inside the library); `stream` is a cudaStream_t passed as void*;
+ *   - calls are stream-ordered and reentrant; the only process-global state
+ *     is one-time kernel attribute setup;
+ *   - return 0 on success, a cudaError_t value or an SPA_E* code otherwise;
+ *     spa_last_error() returns the calling thread's last message.
+ *   - particles are float32 rows with leading dimension `ldb` (elements).
+ */
+#ifndef SPA_B200_H_
+#define SPA_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPA_E_BAD_ARGUMENT 1001
+#define SPA_E_NOT_SUPPORTED 1002
+#define SPA_E_WORKSPACE 1003
+#define SPA_E_DRIVER 1004
+
+/* Design matrix in the layouts the kernels read (built once per dataset by
+ * the host from Dataset.X / Dataset.y; reference smc.py:106-123 make_design,
+ * including the optional unpenalised intercept column). */
+typedef struct spa_design {
+  int32_t n;          /* subjects */
+  int32_t q;          /* coordinates (p, +1 with intercept) */
+  int32_t coded;      /* 1: every column is x = alpha*g + gamma, g in {0,1,2} */
+  int32_t n_words;    /* 32-subject words per column in the bit planes */
+  const uint32_t* planes;   /* coded: [q][n_words][2] bit planes (g==1, g==2)  */
+  const float* xcols;       /* general: [q][n_words*32] float32 columns, 0-padded */
+  const float* xlev;        /* [q][4]  x value of code 0,1,2 (coded designs)   */
+  const double* sy;         /* [q]     X^T y                                    */
+  const double* alpha;      /* [q]     coded: x = alpha*g + gamma              */
+  const double* gamma;      /* [q]                                              */
+  const uint8_t* penalized; /* [q]     1 = prior applies (smc.py:266-270)      */
+  /* tensor-core operand of the batched likelihood (K1) */
+  const void* gemm_b;       /* bf16 B operand: coded -> G [n][kp] (0/1/2 and
+                               1 in the 3 offset columns q..q+2);
+                               general -> [Xhi | Xlo] [n][2*kp]              */
+  int32_t kp;               /* K per term, multiple of 64, >= q (+3 if coded) */
+  int32_t terms;            /* B terms: 1 (coded) or 2 (general); the A
+                               operand is always [beta hi | beta lo]          */
+} spa_design;
+
+/* Prior description: a > 0 (generalised t, model.py:78-81) or a = +inf
+ * (double-exponential limit, model.py:84-88). */
+
+const char* spa_last_error(void);
+int spa_version(void);
+
+/* ---- K6: Philox4x64-10 streams (smc.py:40-43) -------------------------- */
+/* Raw blocks first_block..first_block+count-1 of stream key (k0, k1):
+ * out[4*count] uint64 (device). Test hook for bit parity with NumPy. */
+int spa_philox_blocks(uint64_t k0, uint64_t k1, uint64_t first_block, int64_t count, uint64_t* out,
+                      void* stream);
+
+/* ---- K1: batched log-likelihood on tcgen05 tensor cores -----------------
+ * Replaces model.py:131-145 log_likelihood evaluated for many particles
+ * (batched as summary.py:154-170).  A = packed particles (spa_pack_particles),
+ * bf16 [m][terms*kp]; out_sp[m] = sum_i softplus(eta_ki) (float64).
+ * ws: workspace of spa_loglik_workspace_bytes(m, n) bytes. */
+size_t spa_loglik_workspace_bytes(int64_t m, int32_t n);
+int spa_loglik_softplus(const spa_design* d, const void* A, int64_t m, double* out_sp, void* ws, size_t ws_bytes,
+                        void* stream);
+
+/* Pack particle rows into the K1 A-operand and emit the exact linear term
+ * y.eta = beta . X^T y (float64).  Optionally (lp != NULL) also the log-prior
+ * sum at scale c (model.py:78-81 summed over penalised coordinates). */
+int spa_pack_particles(const spa_design* d, const float* beta, int64_t m, int32_t ldb, void* A, double* ylin,
+                       double a, double c, double* lp, void* stream);
+
+/* Full per-particle log-likelihood l_k = ylin_k - sp_k (float64): pack + K1.
+ * Convenience used by the parity tests and by the host between moves. */
+int spa_loglik_rows(const spa_design* d, const float* beta, int64_t m, int32_t ldb, void* A_ws, double* ylin_ws,
+                    double* out_ll, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- K2: generalised-t log-prior / incremental weights -----------------
+ * mode 0: out[k] = sum_j gt(beta_kj; a, c)             (model.py:78-81)
+ * mode 1: out[k] = sum_j gt(beta_kj; a, c) - gt(beta_kj; a, c_prev)
+ *         (smc.py:248-257 reweight increments, cancellation-free form). */
+int spa_prior_rows(const spa_design* d, const float* beta, int64_t m, int32_t ldb, double a, double c,
+                   double c_prev, int32_t mode, double* out, void* stream);
+
+/* ---- K3: log-sum-exp / ESS (smc.py:151-157, 171-174, 258-262) ----------
+ * Fixed 4096-particle chunks -> per-chunk (max, sum e^(x-max), sum e^(2(x-max)))
+ * of x = logw + lw; deterministic for any particle sharding. */
+int spa_lse_chunk_stats(const double* logw, const double* lw, int64_t m, double* stats /*[ceil(m/4096)][3]*/,
+                        void* stream);
+/* Combine chunk stats in fixed order: res[0] = log sum e^x, res[1] = ESS,
+ * res[2] = max.  Device pointer res[3]. */
+int spa_lse_combine(const double* stats, int64_t nchunks, double* res, void* stream);
+/* lw != NULL: logw <- logw + lw - res[0] and (w != NULL) w <- exp(logw)
+ *             (smc.py:258-262 renormalisation);
+ * lw == NULL: w <- exp(logw - res[0]), logw untouched (smc.py:151-154). */
+int spa_logw_apply(double* logw, const double* lw, int64_t m, const double* res, double* w, void* stream);
+
+/* ---- K4/K5: systematic resampling (smc.py:273-295) ----------------------
+ * Bit-exact with systematic_resample_indices(w, u): sequential float64
+ * cumsum, division by the last entry, cum[-1] = 1, positions u + k/N,
+ * searchsorted(side='right').  anc[k] for k in [k0, k0+count) of the N slots.
+ * ws: spa_resample_workspace_bytes(N). */
+size_t spa_resample_workspace_bytes(int64_t N);
+int spa_systematic_ancestors(const double* w, int64_t N, double u, int64_t k0, int64_t count, int64_t* anc,
+                             void* ws, size_t ws_bytes, void* stream);
+/* dst_rows[k] = src_rows[idx[k] - base] (float32 rows) and the per-particle
+ * float64 vectors (each may be NULL). */
+int spa_gather_rows(const float* src, int32_t ld_src, float* dst, int32_t ld_dst, int32_t q, const int64_t* idx,
+                    int64_t base, int64_t m, const double* v0, double* v0_out, const double* v1, double* v1_out,
+                    void* stream);
+
+/* ---- K7/K9: Metropolis-within-Gibbs coordinate moves --------------------
+ * smc.py:298-332 (_move_block) / smc.py:177-199 (mwg_sweep): `cycles` sweeps
+ * of single-coordinate random-walk updates with per-particle Philox streams
+ * keyed (seed, tag, t, i0+k); sweep s draws from block index s*q + j
+ * (Philox counter index + 1, the NumPy convention).
+ * Writes ll (log-likelihood) and lp (log-prior at c) of the final state,
+ * and adds the number of accepted updates to *accepted (device u64). */
+int spa_mwg_move(const spa_design* d, float* beta, int64_t m, int32_t ldb, double a, double c, double step_sd,
+                 int32_t cycles, uint64_t seed, int32_t tag, int64_t t, int64_t i0, int64_t sweep0, double* ll,
+                 double* lp, unsigned long long* accepted, void* stream);
+
+/* ---- K8: population random-walk moves (north-star kernel) --------------
+ * Weighted moments M1 = sum w beta, M2c = sum w (beta-mu)(beta-mu)^T (mu read
+ * from the accumulator, so call once with w to get M1, then again for M2c
+ * with phase = 1).  `partial` is an int64 fixed-point (2^-48) accumulator
+ * [q + q*q] zeroed by the caller; integer sums are order-independent, so the
+ * result is bit-identical for any CTA schedule or particle sharding. */
+int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const double* w, int32_t phase,
+                   int64_t* partial, void* stream);
+/* Covariance from the fixed-point moments, jitter, float64 Cholesky;
+ * L = s*chol(S) as float32 [q][q] row-major lower (s = scale/sqrt(q)) and as
+ * the bf16 proposal operand [q][kq] at ws + q*q doubles.
+ * ws >= 8*q*q + 2*q*kq bytes; *info = 0 or the failing column + 1. */
+int spa_rw_factor(const int64_t* partial, int32_t q, double scale, double jitter, float* L, double* ws, int* info,
+                  void* stream);
+/* prop = beta + L z, z ~ N(0, I) from stream (seed, 3, t, i0+k) blocks
+ * 1 + move*(ceil(q/4)+1) + j/4; then pack + ylin + lp at c as
+ * spa_pack_particles. */
+int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ldb, const void* Lb, uint64_t seed,
+                   int64_t t, int64_t i0, int32_t move, float* prop, void* A, double* ylin, double a, double c,
+                   double* lp, void* stream);
+/* Metropolis accept: d = (ylin' - sp' + lp') - (ll + lp); u from block
+ * 1 + move*(ceil(q/4)+1) + ceil(q/4) word 0; on accept copy the row and
+ * update ll, lp; adds accepted count to *accepted. */
+int spa_rw_accept(float* beta, int32_t ldb, const float* prop, int32_t q, int64_t m, const double* ylin_p,
+                  const double* sp_p, const double* lp_p, double* ll, double* lp, uint64_t seed, int64_t t,
+                  int64_t i0, int32_t move, unsigned long long* accepted, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPA_B200_H_ */

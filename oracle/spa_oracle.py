@@ -1,0 +1,258 @@
+"""CPU oracle for the SMC lambda-path hot path -- TEST INFRASTRUCTURE ONLY.
+
+This module is a NumPy restatement of the reference algorithm
+(`spa` 0.1.0, /root/reference/pkg/src/spa) used as the *checker* for the
+CUDA path.  Only `tests/`, `__graft_entry__.smoke()` and the `cpu_baseline`
+/ `--impl reference` legs of `bench.py` may import it.  The product package
+(`paper_1106_0322_b200`) never imports anything from `oracle/`; if the CUDA
+library is missing the product raises instead of falling back here.
+
+Parity pinning: every function below is checked in
+`tests/test_oracle_golden.py` against golden vectors produced by running the
+reference itself in the build container (`tests/golden/make_golden.py`).
+
+Each function cites the reference file:line it restates.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+# ---------------------------------------------------------------------------
+# Philox4x64-10 counter RNG (reference: smc.py:40-43 builds
+# np.random.Philox(key=[seed, tag<<58 | t<<34 | i]); NumPy's Philox4x64-10
+# emits block b (0-based) from counter value b+1, words in order 0..3).
+
+_PHILOX_M = (0xD2E7470EE14C6C93, 0xCA5A826395121157)
+_PHILOX_W = (0x9E3779B97F4A7C15, 0xBB67AE8584CAA73B)
+_U32 = np.uint64(0xFFFFFFFF)
+TAG_INIT, TAG_MOVE, TAG_RESAMPLE, TAG_RWMOVE = 0, 1, 2, 3
+
+
+def _mulhilo64(a: np.ndarray, b: int):
+    """Full 64x64->128 product of uint64 arrays by a constant, as (hi, lo)."""
+    a = a.astype(np.uint64)
+    b_lo, b_hi = np.uint64(b & 0xFFFFFFFF), np.uint64(b >> 32)
+    a_lo, a_hi = a & _U32, a >> np.uint64(32)
+    ll = a_lo * b_lo
+    lh = a_lo * b_hi
+    hl = a_hi * b_lo
+    hh = a_hi * b_hi
+    mid = (ll >> np.uint64(32)) + (lh & _U32) + (hl & _U32)
+    lo = (ll & _U32) | ((mid & _U32) << np.uint64(32))
+    hi = hh + (lh >> np.uint64(32)) + (hl >> np.uint64(32)) + (mid >> np.uint64(32))
+    return hi, lo
+
+
+def philox4x64_10(counters: np.ndarray, key) -> np.ndarray:
+    """Vectorised Philox4x64-10 bijection; counters [M,4] uint64 -> [M,4]."""
+    c = np.array(counters, dtype=np.uint64).reshape(-1, 4).T.copy()
+    k0, k1 = np.uint64(int(key[0]) & (2**64 - 1)), np.uint64(int(key[1]) & (2**64 - 1))
+    with np.errstate(over="ignore"):
+        for _ in range(10):
+            hi0, lo0 = _mulhilo64(c[0], _PHILOX_M[0])
+            hi1, lo1 = _mulhilo64(c[2], _PHILOX_M[1])
+            c = np.stack([hi1 ^ c[1] ^ k0, lo1, hi0 ^ c[3] ^ k1, lo0])
+            k0 = k0 + np.uint64(_PHILOX_W[0])
+            k1 = k1 + np.uint64(_PHILOX_W[1])
+    return c.T
+
+
+def stream_key(seed: int, tag: int, t: int = 0, i: int = 0):
+    """Key layout of smc.py:40-43: (seed, tag<<58 | t<<34 | i)."""
+    return (int(seed), (int(tag) << 58) | (int(t) << 34) | int(i))
+
+
+def stream_blocks(key, first_block: int, count: int) -> np.ndarray:
+    """Raw Philox blocks first_block..first_block+count-1 ([count,4] uint64)."""
+    ctr = np.zeros((count, 4), dtype=np.uint64)
+    ctr[:, 0] = np.arange(first_block + 1, first_block + 1 + count, dtype=np.uint64)
+    return philox4x64_10(ctr, key)
+
+
+def stream_raw(key, count: int) -> np.ndarray:
+    """The first `count` 64-bit draws of the stream, in NumPy's order."""
+    nb = -(-count // 4)
+    return stream_blocks(key, 0, nb).reshape(-1)[:count]
+
+
+def u53(raw) -> np.ndarray:
+    """NumPy's next_double: (raw >> 11) * 2^-53 (uniform in [0, 1))."""
+    return (np.asarray(raw, dtype=np.uint64) >> np.uint64(11)).astype(np.float64) * 2.0**-53
+
+
+def box_muller(w0, w1):
+    """Device normal generator restated (csrc/philox.cuh): one N(0,1) from
+    two raw words, u1 in (0,1], u2 in [0,1)."""
+    u1 = ((np.asarray(w0, np.uint64) >> np.uint64(11)).astype(np.float64) + 1.0) * 2.0**-53
+    u2 = u53(w1)
+    return np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2)
+
+
+def box_muller_pair(w0, w1):
+    u1 = ((np.asarray(w0, np.uint64) >> np.uint64(11)).astype(np.float64) + 1.0) * 2.0**-53
+    u2 = u53(w1)
+    r = np.sqrt(-2.0 * np.log(u1))
+    return r * np.cos(2.0 * np.pi * u2), r * np.sin(2.0 * np.pi * u2)
+
+
+# ---------------------------------------------------------------------------
+# Model (reference model.py)
+
+
+def gt_log_density(beta, a: float, c: float):
+    """model.py:78-81: -log(2c) - (a+1) log1p(|beta|/(a c))."""
+    x = np.abs(np.asarray(beta, dtype=np.float64))
+    return -math.log(2.0 * c) - (a + 1.0) * np.log1p(x / (a * c))
+
+
+def de_log_density(beta, c: float):
+    """model.py:84-88 (the a -> infinity limit)."""
+    return -math.log(2.0 * c) - np.abs(np.asarray(beta, dtype=np.float64)) / c
+
+
+def log_prior_rows(B, a: float, c: float, penalized=None):
+    """Per-particle sum of the log-prior over penalized coordinates
+    (model.py:166-169 prior part; smc.py:256, 266-270 for the mask)."""
+    B = np.asarray(B, dtype=np.float64)
+    dens = gt_log_density(B, a, c) if np.isfinite(a) else de_log_density(B, c)
+    if penalized is not None:
+        dens = dens[:, np.asarray(penalized, bool)]
+    return dens.sum(axis=1)
+
+
+def loglik_rows(X, y, B, block: int = 256):
+    """Per-particle Bernoulli-logit log-likelihood (model.py:131-145, batched
+    as in summary.py:154-170): sum_i y_i eta_i - logaddexp(0, eta_i)."""
+    X = np.asarray(X, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    B = np.atleast_2d(np.asarray(B, dtype=np.float64))
+    out = np.empty(B.shape[0])
+    for s in range(0, B.shape[0], block):
+        eta = B[s:s + block] @ X.T
+        out[s:s + block] = (eta * y).sum(axis=1) - np.logaddexp(0.0, eta).sum(axis=1)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Sampler building blocks (reference smc.py)
+
+
+def schedule_bs(b1: float, rho: float, T: int) -> np.ndarray:
+    """smc.py:62-64."""
+    return b1 * rho ** np.arange(T)
+
+
+def reweight_increments(B, a: float, c_t: float, c_prev: float, penalized=None):
+    """smc.py:248-263 incremental log-weights lw (before normalisation)."""
+    return log_prior_rows(B, a, c_t, penalized) - log_prior_rows(B, a, c_prev, penalized)
+
+
+def logsumexp(v) -> float:
+    v = np.asarray(v, dtype=np.float64)
+    m = np.max(v)
+    if not np.isfinite(m):
+        return float(m)
+    return float(m + np.log(np.sum(np.exp(v - m))))
+
+
+def normalise_log_weights(log_w, lw):
+    """smc.py:258-262: unnorm = logW + lw; inc = lse(unnorm); logW' = unnorm - inc."""
+    unnorm = np.asarray(log_w, np.float64) + np.asarray(lw, np.float64)
+    inc = logsumexp(unnorm)
+    return unnorm - inc, inc
+
+
+def weights_from_log(log_w):
+    """smc.py:151-154."""
+    w = np.exp(log_w - logsumexp(log_w))
+    return w / w.sum()
+
+
+def ess(w) -> float:
+    """smc.py:171-174."""
+    w = np.asarray(w, dtype=np.float64)
+    return float(1.0 / (w @ w))
+
+
+def systematic_ancestors(w, u: float) -> np.ndarray:
+    """smc.py:273-281: sequential cumsum, normalise by the last entry, pin it
+    to 1, positions u + k/N, searchsorted(side='right')."""
+    w = np.asarray(w, dtype=np.float64)
+    n = w.size
+    cum = np.cumsum(w)
+    cum = cum / cum[-1]
+    cum[-1] = 1.0
+    pos = u + np.arange(n) / n
+    return np.searchsorted(cum, pos, side="right")
+
+
+def resample_uniform(seed: int, t: int, n: int) -> float:
+    """smc.py:289 + smc.py:421: first uniform of stream (seed, 2, t) over N."""
+    return float(u53(stream_raw(stream_key(seed, TAG_RESAMPLE, t), 1))[0]) / n
+
+
+# ---------------------------------------------------------------------------
+# Move kernels
+
+
+def mwg_move_rows(B, eta, ll, X, y, a, c, sd, Z, U, penalized=None):
+    """Vectorised Metropolis-within-Gibbs cycles (smc.py:298-332 restated).
+
+    Z, U: [N, cycles, q] proposal normals / uniforms.  Mutates and returns
+    (B, eta, ll, accepted).  Used as the statistical checker of the GPU
+    coordinate kernel (which draws its own device-side normals)."""
+    B = np.array(B, dtype=np.float64)
+    eta = np.array(eta, dtype=np.float64)
+    ll = np.array(ll, dtype=np.float64)
+    N, cycles, q = Z.shape
+    pen = np.ones(q, bool) if penalized is None else np.asarray(penalized, bool)
+    acc_total = 0
+    with np.errstate(divide="ignore"):
+        for cyc in range(cycles):
+            for j in range(q):
+                old = B[:, j]
+                new = old + sd * Z[:, cyc, j]
+                eta_p = eta + np.outer(new - old, X[:, j])
+                ll_p = (eta_p * y).sum(axis=1) - np.logaddexp(0.0, eta_p).sum(axis=1)
+                d = ll_p - ll
+                if pen[j]:
+                    d = d + gt_log_density(new, a, c) - gt_log_density(old, a, c)
+                ok = (d >= 0.0) | (np.log(U[:, cyc, j]) < d)
+                B[ok, j] = new[ok]
+                eta[ok] = eta_p[ok]
+                ll[ok] = ll_p[ok]
+                acc_total += int(ok.sum())
+    return B, eta, ll, acc_total
+
+
+def rw_cov_factor(B, w, scale_const: float = 2.38, jitter: float = 1e-6):
+    """Population random-walk proposal factor for the north-star RW-cov move
+    (no reference counterpart; BASELINE.json north_star item 4): weighted
+    covariance of the particle cloud, Cholesky factor, scaled by 2.38/sqrt(q).
+    Restates csrc/rwmove.cu in float64."""
+    B = np.asarray(B, np.float64)
+    w = np.asarray(w, np.float64)
+    mu = w @ B
+    D = B - mu
+    S = (D * w[:, None]).T @ D
+    q = B.shape[1]
+    S = S + jitter * (np.trace(S) / q + 1e-300) * np.eye(q)
+    L = np.linalg.cholesky(S)
+    return L * (scale_const / math.sqrt(q)), mu, S
+
+
+def rw_move_rows(B, ll, lp, X, y, a, c, Ls, Z, U, penalized=None):
+    """One RW-cov Metropolis move for every row (float64 checker):
+    beta' = beta + Ls z; accept if log u < (ll'+lp') - (ll+lp)."""
+    B = np.asarray(B, np.float64)
+    prop = B + np.asarray(Z, np.float64) @ np.asarray(Ls, np.float64).T
+    ll_p = loglik_rows(X, y, prop)
+    lp_p = log_prior_rows(prop, a, c, penalized)
+    d = (ll_p + lp_p) - (ll + lp)
+    with np.errstate(divide="ignore"):
+        ok = (d >= 0.0) | (np.log(U) < d)
+    B2 = np.where(ok[:, None], prop, B)
+    return B2, np.where(ok, ll_p, ll), np.where(ok, lp_p, lp), ok

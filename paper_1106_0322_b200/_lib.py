@@ -1,0 +1,118 @@
+"""ctypes binding of libspa_b200.so (declarations: include/spa_b200.h).
+
+The library is the ONLY compute path: if it is missing or fails to load the
+package raises, there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_size_t, c_uint64, c_void_p
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libspa_b200.so")
+
+
+class SpaDesign(ctypes.Structure):
+    """Mirror of `spa_design` (include/spa_b200.h)."""
+
+    _fields_ = [
+        ("n", c_int32),
+        ("q", c_int32),
+        ("coded", c_int32),
+        ("n_words", c_int32),
+        ("planes", c_void_p),
+        ("xcols", c_void_p),
+        ("xlev", c_void_p),
+        ("sy", c_void_p),
+        ("alpha", c_void_p),
+        ("gamma", c_void_p),
+        ("penalized", c_void_p),
+        ("gemm_b", c_void_p),
+        ("kp", c_int32),
+        ("terms", c_int32),
+    ]
+
+
+# name -> (restype, argtypes); every symbol the header declares.
+_SIGNATURES = {
+    "spa_last_error": (c_char_p, []),
+    "spa_version": (c_int, []),
+    "spa_philox_blocks": (c_int, [c_uint64, c_uint64, c_uint64, c_int64, c_void_p, c_void_p]),
+    "spa_loglik_workspace_bytes": (c_size_t, [c_int64, c_int32]),
+    "spa_loglik_softplus": (c_int, [POINTER(SpaDesign), c_void_p, c_int64, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "spa_pack_particles": (c_int, [POINTER(SpaDesign), c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_double,
+                                   c_double, c_void_p, c_void_p]),
+    "spa_loglik_rows": (c_int, [POINTER(SpaDesign), c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p,
+                                c_void_p, c_size_t, c_void_p]),
+    "spa_prior_rows": (c_int, [POINTER(SpaDesign), c_void_p, c_int64, c_int32, c_double, c_double, c_double, c_int32,
+                               c_void_p, c_void_p]),
+    "spa_lse_chunk_stats": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
+    "spa_lse_combine": (c_int, [c_void_p, c_int64, c_void_p, c_void_p]),
+    "spa_logw_apply": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "spa_resample_workspace_bytes": (c_size_t, [c_int64]),
+    "spa_systematic_ancestors": (c_int, [c_void_p, c_int64, c_double, c_int64, c_int64, c_void_p, c_void_p, c_size_t,
+                                         c_void_p]),
+    "spa_gather_rows": (c_int, [c_void_p, c_int32, c_void_p, c_int32, c_int32, c_void_p, c_int64, c_int64, c_void_p,
+                                c_void_p, c_void_p, c_void_p, c_void_p]),
+    "spa_mwg_move": (c_int, [POINTER(SpaDesign), c_void_p, c_int64, c_int32, c_double, c_double, c_double, c_int32,
+                             c_uint64, c_int32, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "spa_rw_moments": (c_int, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_int32, c_void_p, c_void_p]),
+    "spa_rw_factor": (c_int, [c_void_p, c_int32, c_double, c_double, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "spa_rw_propose": (c_int, [POINTER(SpaDesign), c_void_p, c_int64, c_int32, c_void_p, c_uint64, c_int64, c_int64,
+                               c_int32, c_void_p, c_void_p, c_void_p, c_double, c_double, c_void_p, c_void_p]),
+    "spa_rw_accept": (c_int, [c_void_p, c_int32, c_void_p, c_int32, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                              c_void_p, c_uint64, c_int64, c_int64, c_int32, c_void_p, c_void_p]),
+}
+
+_lib = None
+
+
+class SpaLibraryError(RuntimeError):
+    """A libspa_b200 entry point returned a non-zero status."""
+
+
+def load(path: str = LIB_PATH):
+    """Load (once) and return the configured CDLL.  Raises if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"libspa_b200.so not found at {path}: build it with `make` (or __graft_entry__.build()); "
+            "there is no CPU fallback"
+        )
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def exported_symbols():
+    return list(_SIGNATURES)
+
+
+# kernels launched by one call of each entry point (for bench.py's
+# `gpu_launches`; csrc/*.cu are the source of truth)
+KERNELS_PER_CALL = {
+    "spa_philox_blocks": 1, "spa_loglik_softplus": 2, "spa_pack_particles": 1, "spa_loglik_rows": 3,
+    "spa_prior_rows": 1, "spa_lse_chunk_stats": 1, "spa_lse_combine": 1, "spa_logw_apply": 1,
+    "spa_systematic_ancestors": 2, "spa_gather_rows": 1, "spa_mwg_move": 1, "spa_rw_moments": 1,
+    "spa_rw_factor": 1, "spa_rw_propose": 3, "spa_rw_accept": 1,
+}
+launch_count = 0
+
+
+def call(name: str, *args) -> None:
+    """Invoke an int-returning entry point and raise on a non-zero status."""
+    global launch_count
+    lib = load()
+    launch_count += KERNELS_PER_CALL.get(name, 0)
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.spa_last_error().decode(errors="replace")
+        raise SpaLibraryError(f"{name} failed with status {rc}: {msg}")

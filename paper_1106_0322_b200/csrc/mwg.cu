@@ -1,0 +1,337 @@
+// K7/K9: Metropolis-within-Gibbs coordinate moves on the GPU.
+//
+// Reference: smc.py:298-332 (_move_block) and smc.py:177-199 (mwg_sweep):
+// for every particle, `cycles` sweeps over coordinates j = 0..q-1 of
+//   beta_j' = beta_j + sd * z_j,
+//   d = l(beta') - l(beta) + [gt(beta_j') - gt(beta_j)]  (penalised j only)
+//   accept if d >= 0 or log(u_j) < d.
+//
+// B200 formulation (one CTA per particle, the particle's subjects spread over
+// the CTA's threads, all state in registers):
+//   * the per-subject cache is sigma_i = logistic(eta_i) instead of eta_i;
+//   * with delta = beta_j' - beta_j and m_i = expm1(delta * x_ij),
+//       l(beta') - l(beta) = delta * (X^T y)_j - sum_i log(1 + m_i sigma_i),
+//     which is exact algebra (softplus(eta + d) - softplus(eta) =
+//     log1p(expm1(d) sigma)) and needs ONE transcendental (lg2) per subject;
+//   * on acceptance sigma_i <- sigma_i (1 + m_i) / (1 + m_i sigma_i);
+//   * integer-coded columns take only 3 values, so m_i is one of 3 per-
+//     coordinate constants selected from two genotype bit planes;
+//   * eta/sigma and the log-likelihood are re-materialised from beta at the
+//     start of every call, so float32 drift cannot accumulate across steps.
+// Proposal randomness: per-particle Philox stream keyed exactly like the
+// reference (seed, tag, t, i0 + k); sweep s uses block index s*q + j, i.e.
+// Philox counter s*q + j + 1 (normal from words 0,1 by Box-Muller, uniform
+// from word 2).
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "../../include/spa_b200.h"
+#include "common.cuh"
+#include "philox.cuh"
+
+namespace spa {
+
+struct MwgParams {
+  spa_design d;
+  float* beta;
+  int64_t m;
+  int ldb;
+  double a, c, sd;
+  int de;
+  int cycles;
+  uint64_t seed;
+  int tag;
+  int64_t t, i0, sweep0;
+  double* ll;
+  double* lp;
+  unsigned long long* accepted;
+};
+
+__device__ __forceinline__ double mwg_gt(double b, const MwgParams& P) {
+  const double x = fabs(b);
+  if (P.de) return -log(2.0 * P.c) - x / P.c;
+  return -log(2.0 * P.c) - (P.a + 1.0) * log1p(x / (P.a * P.c));
+}
+
+// Per-coordinate proposal data for one sweep (computed once per sweep:
+// within a sweep coordinate j is visited once, so beta_j at its visit is
+// its value at sweep start).
+struct CoordSlot {
+  double delta;   // beta_j' - beta_j (exact, float64)
+  double dlp;     // prior difference
+  double logu;    // log of the MH uniform
+  float newv;     // beta_j' (float32 state)
+  float m0, m1, m2;  // expm1(delta * x) for codes 0, 1, 2
+};
+
+// Genotype code from the two bit planes: (0,0)->0, (1,0)->1, (0,1)->2, and
+// (1,1) marks a padding subject whose factor m must be exactly 0.
+__device__ __forceinline__ float sel_m(uint32_t b1, uint32_t b2, const CoordSlot& cs) {
+  return (b2 & 1) ? ((b1 & 1) ? 0.0f : cs.m2) : ((b1 & 1) ? cs.m1 : cs.m0);
+}
+
+template <int S>
+__device__ __forceinline__ void load_bits(const spa_design& d, int j, int tid, uint32_t& p1, uint32_t& p2) {
+  if constexpr (S == 64) {
+    const uint2 a = reinterpret_cast<const uint2*>(d.planes)[(size_t)j * d.n_words + 2 * tid];
+    const uint2 b = reinterpret_cast<const uint2*>(d.planes)[(size_t)j * d.n_words + 2 * tid + 1];
+    p1 = a.x;
+    p2 = a.y;
+    (void)b;
+  } else {
+    const int bit0 = tid * S;
+    const uint2 a = reinterpret_cast<const uint2*>(d.planes)[(size_t)j * d.n_words + (bit0 >> 5)];
+    const int sh = bit0 & 31;
+    p1 = a.x >> sh;
+    p2 = a.y >> sh;
+  }
+}
+
+template <int S>
+__global__ void __launch_bounds__(512) mwg_kernel(MwgParams P) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int q = P.d.q;
+  CoordSlot* slot = reinterpret_cast<CoordSlot*>(sm);
+  float* bsh = reinterpret_cast<float*>(slot + q);
+  double* red = reinterpret_cast<double*>(bsh + ((q + 1) & ~1));  // [2][32]
+  float* fred = reinterpret_cast<float*>(red + 64);               // [2][32]
+
+  const int64_t row = blockIdx.x;
+  if (row >= P.m) return;
+  const int tid = threadIdx.x;
+  const int nthr = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5, nw = nthr >> 5;
+  float* brow = P.beta + row * P.ldb;
+  const Key2 key = stream_key(P.seed, (uint32_t)P.tag, (uint64_t)P.t, (uint64_t)(P.i0 + row));
+
+  for (int j = tid; j < q; j += nthr) bsh[j] = brow[j];
+  __syncthreads();
+
+  // ---- 1. materialise eta and sigma for this thread's subjects ------------
+  float eta[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) eta[s] = 0.0f;
+  const int sub0 = tid * S;
+  for (int j = 0; j < q; ++j) {
+    const float bj = bsh[j];
+    if (P.d.coded) {
+      const float4 lv = reinterpret_cast<const float4*>(P.d.xlev)[j];
+      const float v0 = lv.x * bj, v1 = lv.y * bj, v2 = lv.z * bj;
+      if constexpr (S == 64) {
+        const uint2 a = reinterpret_cast<const uint2*>(P.d.planes)[(size_t)j * P.d.n_words + 2 * tid];
+        const uint2 b = reinterpret_cast<const uint2*>(P.d.planes)[(size_t)j * P.d.n_words + 2 * tid + 1];
+#pragma unroll
+        for (int s = 0; s < 32; ++s) {
+          eta[s] += ((a.y >> s) & 1) ? v2 : (((a.x >> s) & 1) ? v1 : v0);
+          eta[s + 32] += ((b.y >> s) & 1) ? v2 : (((b.x >> s) & 1) ? v1 : v0);
+        }
+      } else {
+        uint32_t p1, p2;
+        load_bits<S>(P.d, j, tid, p1, p2);
+#pragma unroll
+        for (int s = 0; s < S; ++s) eta[s] += ((p2 >> s) & 1) ? v2 : (((p1 >> s) & 1) ? v1 : v0);
+      }
+    } else {
+      const float* xc = P.d.xcols + (size_t)j * P.d.n_words * 32 + sub0;
+#pragma unroll
+      for (int s = 0; s < S; ++s) eta[s] = fmaf(xc[s], bj, eta[s]);
+    }
+  }
+  float sig[S];
+  float sp_part = 0.0f;
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const bool valid = (sub0 + s) < P.d.n;
+    sig[s] = valid ? 1.0f / (1.0f + __expf(-eta[s])) : 0.0f;
+    if (valid) sp_part += fmaxf(eta[s], 0.0f) + log1pf(__expf(-fabsf(eta[s])));
+  }
+  double yl = 0.0, lp0 = 0.0;
+  for (int j = tid; j < q; j += nthr) {
+    yl += (double)bsh[j] * P.d.sy[j];
+    if (P.d.penalized[j]) lp0 += mwg_gt((double)bsh[j], P);
+  }
+  // block reduction of (sp, yl, lp0)
+  double v3[3] = {(double)sp_part, yl, lp0};
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v3[r] += __shfl_xor_sync(0xffffffffu, v3[r], o);
+  }
+  if (lane == 0) {
+    red[wid] = v3[0];
+    red[32 + wid] = v3[1];
+  }
+  __syncthreads();
+  double ll = 0.0, ylt = 0.0;
+  for (int w = 0; w < nw; ++w) {
+    ll -= red[w];
+    ylt += red[32 + w];
+  }
+  ll += ylt;
+  __syncthreads();
+  if (lane == 0) red[wid] = v3[2];
+  __syncthreads();
+  double lp = 0.0;
+  for (int w = 0; w < nw; ++w) lp += red[w];
+  __syncthreads();
+
+  unsigned long long acc = 0;
+  // ---- 2. sweeps -----------------------------------------------------------
+  for (int cyc = 0; cyc < P.cycles; ++cyc) {
+    const uint64_t blk0 = (uint64_t)(P.sweep0 + cyc) * (uint64_t)q;
+    for (int j = tid; j < q; j += nthr) {
+      uint64_t w[4];
+      philox_block(key, blk0 + j, w);  // block index sweep*q + j (Philox counter index + 1)
+      const double z = box_muller_cos(w[0], w[1]);
+      const double u = u53(w[2]);
+      const float old = bsh[j];
+      const float nv = __double2float_rn((double)old + P.sd * z);
+      CoordSlot cs;
+      cs.newv = nv;
+      cs.delta = (double)nv - (double)old;
+      cs.logu = log(u);
+      cs.dlp = P.d.penalized[j] ? (mwg_gt((double)nv, P) - mwg_gt((double)old, P)) : 0.0;
+      if (P.d.coded) {
+        const float4 lv = reinterpret_cast<const float4*>(P.d.xlev)[j];
+        const float df = (float)cs.delta;
+        cs.m0 = expm1f(df * lv.x);
+        cs.m1 = expm1f(df * lv.y);
+        cs.m2 = expm1f(df * lv.z);
+      } else {
+        cs.m0 = cs.m1 = cs.m2 = 0.0f;
+      }
+      slot[j] = cs;
+    }
+    __syncthreads();
+
+    for (int j = 0; j < q; ++j) {
+      const CoordSlot cs = slot[j];
+      float part = 0.0f;
+      float mloc[S];
+      if (P.d.coded) {
+        if constexpr (S == 64) {
+          const uint2 a = reinterpret_cast<const uint2*>(P.d.planes)[(size_t)j * P.d.n_words + 2 * tid];
+          const uint2 b = reinterpret_cast<const uint2*>(P.d.planes)[(size_t)j * P.d.n_words + 2 * tid + 1];
+#pragma unroll
+          for (int s = 0; s < 32; ++s) {
+            mloc[s] = sel_m(a.x >> s, a.y >> s, cs);
+            mloc[s + 32] = sel_m(b.x >> s, b.y >> s, cs);
+          }
+        } else {
+          uint32_t p1, p2;
+          load_bits<S>(P.d, j, tid, p1, p2);
+#pragma unroll
+          for (int s = 0; s < S; ++s) mloc[s] = sel_m(p1 >> s, p2 >> s, cs);
+        }
+      } else {
+        const float* xc = P.d.xcols + (size_t)j * P.d.n_words * 32 + sub0;
+        const float df = (float)cs.delta;
+#pragma unroll
+        for (int s = 0; s < S; ++s) mloc[s] = expm1f(df * xc[s]);
+      }
+#pragma unroll
+      for (int s = 0; s < S; ++s) part += fast_lg2(fmaxf(fmaf(mloc[s], sig[s], 1.0f), 1e-37f));
+      // block sum (double-buffered scratch: one barrier per coordinate)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      float tot = part;
+      if (nw > 1) {
+        float* buf = fred + (j & 1) * 32;
+        if (lane == 0) buf[wid] = part;
+        __syncthreads();
+        tot = 0.0f;
+        for (int w = 0; w < nw; ++w) tot += buf[w];
+      }
+      const double dll = cs.delta * P.d.sy[j] - 0.6931471805599453 * (double)tot;
+      const double d = dll + cs.dlp;
+      const bool ok = (d >= 0.0) || (cs.logu < d);
+      if (ok) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          const float mm = mloc[s];
+          sig[s] = sig[s] * (1.0f + mm) * __frcp_rn(fmaf(mm, sig[s], 1.0f));
+        }
+        ll += dll;
+        lp += cs.dlp;
+        ++acc;
+        if (tid == 0) bsh[j] = cs.newv;
+      }
+    }
+    __syncthreads();
+  }
+
+  for (int j = tid; j < q; j += nthr) brow[j] = bsh[j];
+  if (tid == 0) {
+    P.ll[row] = ll;
+    if (P.lp) P.lp[row] = lp;
+    atomicAdd(P.accepted, acc);
+  }
+}
+
+static int pick_s(int n) {
+  if (n <= 256) return 8;
+  if (n <= 512) return 16;
+  if (n <= 16384) return 32;
+  return 0;
+}
+
+}  // namespace spa
+
+using namespace spa;
+
+extern "C" int spa_mwg_move(const spa_design* d, float* beta, int64_t m, int32_t ldb, double a, double c,
+                            double step_sd, int32_t cycles, uint64_t seed, int32_t tag, int64_t t, int64_t i0,
+                            int64_t sweep0, double* ll, double* lp, unsigned long long* accepted, void* stream) {
+  SPA_REQUIRE(d && beta && ll && accepted && m >= 0 && cycles >= 0, kBadArgument, "spa_mwg_move: bad arguments");
+  SPA_REQUIRE(a > 0 && c > 0 && step_sd > 0, kBadArgument, "spa_mwg_move: a, c, step_sd must be positive");
+  SPA_REQUIRE(d->q >= 1 && d->q <= 2048, kNotSupported, "spa_mwg_move: q must lie in [1, 2048]");
+  const int S = pick_s(d->n);
+  SPA_REQUIRE(S > 0, kNotSupported, "spa_mwg_move: n > 16384 not supported");
+  SPA_REQUIRE(d->coded ? d->planes != nullptr : d->xcols != nullptr, kBadArgument, "spa_mwg_move: design arrays");
+  if (m == 0) return 0;
+  MwgParams P;
+  P.d = *d;
+  P.beta = beta;
+  P.m = m;
+  P.ldb = ldb;
+  P.a = a;
+  P.c = c;
+  P.sd = step_sd;
+  P.de = std::isinf(a) ? 1 : 0;
+  P.cycles = cycles;
+  P.seed = seed;
+  P.tag = tag;
+  P.t = t;
+  P.i0 = i0;
+  P.sweep0 = sweep0;
+  P.ll = ll;
+  P.lp = lp;
+  P.accepted = accepted;
+  const int nthr_raw = (d->n + S - 1) / S;
+  const int nthr = std::max(32, (nthr_raw + 31) / 32 * 32);
+  SPA_REQUIRE(nthr <= 1024, kNotSupported, "spa_mwg_move: too many subjects per particle");
+  SPA_REQUIRE(nthr * S <= d->n_words * 32, kBadArgument, "spa_mwg_move: n_words does not cover the thread layout");
+  const size_t smem = (size_t)d->q * sizeof(CoordSlot) + (size_t)((d->q + 1) & ~1) * sizeof(float) +
+                      64 * sizeof(double) + 64 * sizeof(float);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  switch (S) {
+    case 8:
+      SPA_CHECK_CUDA(cudaFuncSetAttribute(mwg_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      mwg_kernel<8><<<(unsigned)m, nthr, smem, st>>>(P);
+      break;
+    case 16:
+      SPA_CHECK_CUDA(cudaFuncSetAttribute(mwg_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      mwg_kernel<16><<<(unsigned)m, nthr, smem, st>>>(P);
+      break;
+    case 32:
+      SPA_REQUIRE(nthr <= 512, kNotSupported, "spa_mwg_move: n > 16384 not supported");
+      SPA_CHECK_CUDA(cudaFuncSetAttribute(mwg_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      mwg_kernel<32><<<(unsigned)m, nthr, smem, st>>>(P);
+      break;
+    default:
+      return fail(kNotSupported, "spa_mwg_move: n > 16384 not supported");
+  }
+  SPA_CHECK_LAUNCH();
+  return 0;
+}

@@ -1,0 +1,824 @@
+// libspa_b200: C-ABI entry points and the bandwidth-bound SMC kernels
+// (pack, prior/reweight, log-sum-exp/ESS, systematic resampling, gather,
+// RW-cov moments/factor/propose/accept) plus the tcgen05 likelihood launcher.
+//
+// Reference functions replaced are cited on each entry point (see also
+// include/spa_b200.h).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <mutex>
+#include <string>
+
+#include "../../include/spa_b200.h"
+#include "common.cuh"
+#include "philox.cuh"
+#include "tc_gemm.cuh"
+
+namespace spa {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------------------
+// TMA descriptor construction via the driver entry point (no -lcuda link).
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// bf16 matrix [rows][cols] row-major; box = 64 columns x box_rows rows, 128B swizzle.
+static int make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+  auto enc = tmap_encoder();
+  if (!enc) return fail(kDriverEntryPoint, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(kDriverEntryPoint, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return 0;
+}
+
+template <int TA, int TB, int BN, class Epi>
+static int launch_tc(const void* A, uint64_t a_cols, const void* B, uint64_t b_cols, uint64_t b_rows, TcArgs args,
+                     int units, Epi epi, cudaStream_t st) {
+  using S = TcShape<TA, TB, BN>;
+  CUtensorMap ta, tb;
+  int rc = make_tmap_bf16(&ta, A, a_cols, (uint64_t)args.m, kTcBM);
+  if (rc) return rc;
+  rc = make_tmap_bf16(&tb, B, b_cols, b_rows, BN);
+  if (rc) return rc;
+  auto kern = tc_gemm_kernel<TA, TB, BN, Epi>;
+  static bool attr_done = false;  // per template instantiation
+  if (!attr_done) {
+    SPA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kSmemBytes));
+    attr_done = true;
+  }
+  const int grid = args.m_tiles * units;
+  kern<<<grid, kTcThreads, S::kSmemBytes, st>>>(ta, tb, args, epi);
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Generalised-t prior pieces (reference model.py:78-88)
+struct PriorConst {
+  double a, c, c_prev;
+  int de;  // a = +inf: double exponential
+};
+
+__device__ __forceinline__ double gt_logpdf(double b, const PriorConst& p) {
+  const double x = fabs(b);
+  if (p.de) return -log(2.0 * p.c) - x / p.c;
+  return -log(2.0 * p.c) - (p.a + 1.0) * log1p(x / (p.a * p.c));
+}
+
+// gt(b; c) - gt(b; c_prev) without cancellation:
+//   log(c_prev/c) - (a+1) log1p( (x/a)(1/c - 1/c_prev) / (1 + x/(a c_prev)) )
+__device__ __forceinline__ double gt_logratio(double b, const PriorConst& p) {
+  const double x = fabs(b);
+  const double lr = log(p.c_prev / p.c);
+  if (p.de) return lr - x * (1.0 / p.c - 1.0 / p.c_prev);
+  const double num = (x / p.a) * (1.0 / p.c - 1.0 / p.c_prev);
+  return lr - (p.a + 1.0) * log1p(num / (1.0 + x / (p.a * p.c_prev)));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// Pack particle rows into the K1 A operand [m][2*kp] bf16 = [hi | lo] of the
+// scaled coefficients; coded designs carry the centring offset -o in three
+// bf16 columns q..q+2 of the hi block (the B operand holds 1 there).
+__global__ void pack_kernel(spa_design d, const float* __restrict__ beta, int64_t m, int ldb,
+                            __nv_bfloat16* __restrict__ A, double* __restrict__ ylin, PriorConst pc,
+                            double* __restrict__ lp) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= m) return;
+  const float* b = beta + row * ldb;
+  __nv_bfloat16* ah = A + row * (2 * (int64_t)d.kp);
+  __nv_bfloat16* al = ah + d.kp;
+  double yl = 0.0, off = 0.0, lps = 0.0;
+  for (int j = lane; j < d.kp; j += 32) {
+    __nv_bfloat16 h = __float2bfloat16(0.0f), l = __float2bfloat16(0.0f);
+    if (j < d.q) {
+      const double bj = (double)b[j];
+      yl += bj * d.sy[j];
+      if (lp != nullptr && d.penalized[j]) lps += gt_logpdf(bj, pc);
+      double bs = bj;
+      if (d.coded) {
+        bs = d.alpha[j] * bj;
+        off += d.gamma[j] * bj;
+      }
+      h = __double2bfloat16(bs);
+      l = __double2bfloat16(bs - (double)__bfloat162float(h));
+    }
+    ah[j] = h;
+    al[j] = l;
+  }
+  yl = warp_sum(yl);
+  off = warp_sum(off);
+  if (lp != nullptr) lps = warp_sum(lps);
+  if (lane == 0) {
+    ylin[row] = yl;
+    if (lp != nullptr) lp[row] = lps;
+    if (d.coded) {
+      const double o = -off;
+      const __nv_bfloat16 o1 = __double2bfloat16(o);
+      const double r1 = o - (double)__bfloat162float(o1);
+      const __nv_bfloat16 o2 = __double2bfloat16(r1);
+      const double r2 = r1 - (double)__bfloat162float(o2);
+      ah[d.q] = o1;
+      ah[d.q + 1] = o2;
+      ah[d.q + 2] = __double2bfloat16(r2);
+    }
+  }
+}
+
+__global__ void prior_kernel(spa_design d, const float* __restrict__ beta, int64_t m, int ldb, PriorConst pc,
+                             int mode, double* __restrict__ out) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= m) return;
+  const float* b = beta + row * ldb;
+  double s = 0.0;
+  for (int j = lane; j < d.q; j += 32) {
+    if (!d.penalized[j]) continue;
+    const double bj = (double)b[j];
+    s += mode == 0 ? gt_logpdf(bj, pc) : gt_logratio(bj, pc);
+  }
+  s = warp_sum(s);
+  if (lane == 0) out[row] = s;
+}
+
+// ---------------------------------------------------------------------------
+// K3: fixed-chunk log-sum-exp statistics
+constexpr int kChunk = 4096;
+
+__global__ void lse_stats_kernel(const double* __restrict__ logw, const double* __restrict__ lw, int64_t m,
+                                 double* __restrict__ stats) {
+  __shared__ double red[256];
+  const int64_t c0 = (int64_t)blockIdx.x * kChunk;
+  const int64_t c1 = min(m, c0 + kChunk);
+  double mx = -INFINITY;
+  bool nan = false;
+  for (int64_t k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
+    const double x = logw[k] + (lw ? lw[k] : 0.0);
+    if (x != x) nan = true;
+    mx = fmax(mx, x);
+  }
+  nan = __syncthreads_or(nan);
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  mx = red[0];
+  __syncthreads();
+  double s1 = 0.0, s2 = 0.0;
+  if (mx > -INFINITY) {
+    for (int64_t k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
+      const double e = exp(logw[k] + (lw ? lw[k] : 0.0) - mx);
+      s1 += e;
+      s2 += e * e;
+    }
+  }
+  red[threadIdx.x] = s1;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  s1 = red[0];
+  __syncthreads();
+  red[threadIdx.x] = s2;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    stats[3 * blockIdx.x + 0] = nan ? NAN : mx;
+    stats[3 * blockIdx.x + 1] = s1;
+    stats[3 * blockIdx.x + 2] = red[0];
+  }
+}
+
+__global__ void lse_combine_kernel(const double* __restrict__ stats, int64_t nchunks, double* __restrict__ res) {
+  if (threadIdx.x != 0) return;
+  double M = -INFINITY;
+  bool nan = false;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const double v = stats[3 * c];
+    if (v != v) nan = true;
+    M = fmax(M, v);
+  }
+  double s1 = 0.0, s2 = 0.0;
+  if (M > -INFINITY && !nan) {
+    for (int64_t c = 0; c < nchunks; ++c) {
+      const double mc = stats[3 * c];
+      if (mc == -INFINITY) continue;
+      const double f = exp(mc - M);
+      s1 += stats[3 * c + 1] * f;
+      s2 += stats[3 * c + 2] * f * f;
+    }
+  }
+  res[0] = nan ? NAN : (M > -INFINITY ? M + log(s1) : -INFINITY);
+  res[1] = nan ? NAN : s1 * s1 / s2;
+  res[2] = M;
+}
+
+__global__ void logw_apply_kernel(double* __restrict__ logw, const double* __restrict__ lw, int64_t m,
+                                  const double* __restrict__ res, double* __restrict__ w) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  if (lw) {
+    const double v = logw[k] + lw[k] - res[0];
+    logw[k] = v;
+    if (w) w[k] = exp(v);
+  } else if (w) {
+    w[k] = exp(logw[k] - res[0]);  // normalised weights, logw untouched
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4: systematic resampling, bit-exact with the reference (smc.py:273-281).
+// The reference cumsum is a strictly sequential float64 accumulation; it is
+// reproduced by one thread scanning smem-staged tiles (the other lanes stage
+// the next tile).  Ancestor search is parallel (one thread per slot).
+__global__ void seq_cumsum_kernel(const double* __restrict__ w, int64_t N, double* __restrict__ cum) {
+  // blockDim = 64: warp 1 stages tile t+1 into smem while lane 0 of warp 0
+  // runs the strictly sequential float64 accumulation over tile t.
+  __shared__ double tile[2][2048];
+  const int64_t ntiles = (N + 2047) / 2048;
+  if (threadIdx.x >= 32)
+    for (int i = threadIdx.x - 32; i < 2048; i += 32) tile[0][i] = (i < N) ? w[i] : 0.0;
+  __syncthreads();
+  double s = 0.0;
+  for (int64_t t = 0; t < ntiles; ++t) {
+    const int cur = (int)(t & 1);
+    if (threadIdx.x == 0) {
+      const int64_t base = t * 2048;
+      const int cnt = (int)(N - base < 2048 ? N - base : 2048);
+      const double* tl = tile[cur];
+      int i = 0;
+      for (; i + 4 <= cnt; i += 4) {
+        const double a0 = tl[i], a1 = tl[i + 1], a2 = tl[i + 2], a3 = tl[i + 3];
+        const double s0 = s + a0;  // same association as np.cumsum
+        const double s1 = s0 + a1;
+        const double s2 = s1 + a2;
+        const double s3 = s2 + a3;
+        cum[base + i] = s0;
+        cum[base + i + 1] = s1;
+        cum[base + i + 2] = s2;
+        cum[base + i + 3] = s3;
+        s = s3;
+      }
+      for (; i < cnt; ++i) {
+        s = s + tl[i];
+        cum[base + i] = s;
+      }
+    } else if (threadIdx.x >= 32 && t + 1 < ntiles) {
+      const int64_t base = (t + 1) * 2048;
+      for (int i = threadIdx.x - 32; i < 2048; i += 32) tile[cur ^ 1][i] = (base + i < N) ? w[base + i] : 0.0;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void ancestors_kernel(const double* __restrict__ cum, int64_t N, double u, int64_t k0, int64_t count,
+                                 int64_t* __restrict__ anc) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const int64_t k = k0 + i;
+  const double total = cum[N - 1];
+  const double pos = u + (double)k / (double)N;
+  // first index j with norm(j) > pos, norm(j) = cum[j]/total, norm(N-1) = 1
+  int64_t lo = 0, hi = N;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const double v = (mid == N - 1) ? 1.0 : __ddiv_rn(cum[mid], total);
+    if (v > pos)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  anc[i] = lo;
+}
+
+// K5: row gather (+ up to two per-particle float64 vectors)
+__global__ void gather_kernel(const float* __restrict__ src, int ld_src, float* __restrict__ dst, int ld_dst, int q,
+                              const int64_t* __restrict__ idx, int64_t base, int64_t m, const double* __restrict__ v0,
+                              double* __restrict__ v0o, const double* __restrict__ v1, double* __restrict__ v1o) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= m) return;
+  const int64_t s = idx[row] - base;
+  const float* a = src + s * ld_src;
+  float* o = dst + row * ld_dst;
+  if ((ld_src & 3) == 0 && (ld_dst & 3) == 0) {
+    const int q4 = q >> 2;
+    for (int j = lane; j < q4; j += 32) reinterpret_cast<float4*>(o)[j] = reinterpret_cast<const float4*>(a)[j];
+    for (int j = 4 * q4 + lane; j < q; j += 32) o[j] = a[j];
+  } else {
+    for (int j = lane; j < q; j += 32) o[j] = a[j];
+  }
+  if (lane == 0) {
+    if (v0) v0o[row] = v0[s];
+    if (v1) v1o[row] = v1[s];
+  }
+}
+
+__global__ void philox_blocks_kernel(Key2 k, uint64_t first, int64_t count, uint64_t* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  uint64_t w[4];
+  philox_block(k, first + (uint64_t)i, w);
+  for (int j = 0; j < 4; ++j) out[4 * i + j] = w[j];
+}
+
+__global__ void reduce_units_kernel(const double* __restrict__ partial, int units, int64_t m,
+                                    const double* __restrict__ ylin, double* __restrict__ out) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  double s = 0.0;
+  for (int u = 0; u < units; ++u) s += partial[(size_t)u * m + k];
+  out[k] = ylin ? ylin[k] - s : s;
+}
+
+// ---------------------------------------------------------------------------
+// K8: population random-walk moves.
+//
+// Moments: mu = sum_k w_k beta_k, then S = sum_k w_k (beta_k-mu)(beta_k-mu)^T,
+// each accumulated in float32 over fixed particle chunks / 64x64 tiles and
+// converted to 2^-48 fixed point before 64-bit integer atomics: integer sums
+// are associative, so the moments are bit-identical for any CTA order or GPU
+// count (the same property the reference guarantees for `threads`).
+constexpr double kFix = 281474976710656.0;  // 2^48
+constexpr int kMomChunk = 2048;
+
+__device__ __forceinline__ unsigned long long to_fix(double v) { return (unsigned long long)llrint(v * kFix); }
+__device__ __forceinline__ double from_fix(unsigned long long v) { return (double)(long long)v / kFix; }
+
+__global__ void rw_mean_kernel(const float* __restrict__ beta, int64_t m, int ldb, int q, const double* __restrict__ w,
+                               unsigned long long* __restrict__ acc) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= q) return;
+  const int64_t k0 = (int64_t)blockIdx.y * kMomChunk;
+  const int64_t k1 = min(m, k0 + kMomChunk);
+  double s = 0.0;
+  for (int64_t k = k0; k < k1; ++k) s += w[k] * (double)beta[k * ldb + j];
+  atomicAdd(&acc[j], to_fix(s));
+}
+
+__global__ void rw_moments_kernel(const float* __restrict__ beta, int64_t m, int ldb, int q,
+                                  const double* __restrict__ w, unsigned long long* __restrict__ acc) {
+  // block: 16x16 threads computing a 64x64 lower-triangle tile (4x4 per thread)
+  __shared__ float sa[32][64];
+  __shared__ float sb[32][64];
+  __shared__ float mu_i[64], mu_j[64];
+  const int tiles = (q + 63) / 64;
+  const int ti = blockIdx.x / tiles, tj = blockIdx.x % tiles;
+  if (tj > ti) return;
+  const int64_t k0 = (int64_t)blockIdx.y * kMomChunk;
+  const int64_t k1 = min(m, k0 + kMomChunk);
+  if (threadIdx.x < 64) {
+    const int gi = ti * 64 + threadIdx.x, gj = tj * 64 + threadIdx.x;
+    mu_i[threadIdx.x] = gi < q ? (float)from_fix(acc[gi]) : 0.f;
+    mu_j[threadIdx.x] = gj < q ? (float)from_fix(acc[gj]) : 0.f;
+  }
+  __syncthreads();
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float c[4][4] = {};
+  for (int64_t kb = k0; kb < k1; kb += 32) {
+    for (int e = threadIdx.x; e < 32 * 64; e += 256) {
+      const int r = e >> 6, col = e & 63;
+      const int64_t k = kb + r;
+      const int gi = ti * 64 + col, gj = tj * 64 + col;
+      const bool kin = k < k1;
+      const float wk = kin ? (float)w[k] : 0.f;
+      sa[r][col] = (kin && gi < q) ? wk * (beta[k * ldb + gi] - mu_i[col]) : 0.f;
+      sb[r][col] = (kin && gj < q) ? (beta[k * ldb + gj] - mu_j[col]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int r = 0; r < 32; ++r) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        av[i] = sa[r][ty * 4 + i];
+        bv[i] = sb[r][tx * 4 + i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) c[i][jj] = fmaf(av[i], bv[jj], c[i][jj]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gi = ti * 64 + ty * 4 + i;
+    if (gi >= q) continue;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int gj = tj * 64 + tx * 4 + jj;
+      if (gj >= q || gj > gi) continue;
+      atomicAdd(&acc[q + (size_t)gi * q + gj], to_fix((double)c[i][jj]));
+    }
+  }
+}
+
+// Single-CTA float64 Cholesky of S = M2 - M1 M1^T + jitter*I, blocked
+// right-looking with 32-column panels; L scaled by `scale`/sqrt(q) is written
+// as float32 and as the bf16 B operand [q][kq] of the proposal GEMM.
+__global__ void __launch_bounds__(1024) rw_factor_kernel(const unsigned long long* __restrict__ acc, int q,
+                                                         double scale, double jitter, double* __restrict__ S,
+                                                         float* __restrict__ L, __nv_bfloat16* __restrict__ Lb,
+                                                         int kq, int* info) {
+  __shared__ double diag[32][33];
+  __shared__ double tr;
+  const int tid = threadIdx.x;
+  // covariance (lower triangle, row-major S[i*q + j]) from the centred moments
+  for (int64_t e = tid; e < (int64_t)q * q; e += blockDim.x) {
+    const int i = (int)(e / q), j = (int)(e % q);
+    S[e] = (j > i) ? 0.0 : from_fix(acc[q + e]);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int i = 0; i < q; ++i) t += S[(size_t)i * q + i];
+    tr = t / q;
+    if (info) *info = 0;
+  }
+  __syncthreads();
+  for (int i = tid; i < q; i += blockDim.x) S[(size_t)i * q + i] += jitter * (tr > 0 ? tr : 1.0) + 1e-300;
+  __syncthreads();
+
+  for (int jb = 0; jb < q; jb += 32) {
+    const int nb = min(32, q - jb);
+    // 1. factor the diagonal block in smem
+    for (int e = tid; e < nb * nb; e += blockDim.x) {
+      const int i = e / nb, j = e % nb;
+      diag[i][j] = (j <= i) ? S[(size_t)(jb + i) * q + jb + j] : 0.0;
+    }
+    __syncthreads();
+    if (tid < 32) {
+      for (int j = 0; j < nb; ++j) {
+        if (tid == 0) {
+          double dj = diag[j][j];
+          if (!(dj > 0.0)) {
+            if (info && *info == 0) *info = jb + j + 1;
+            dj = 1e-300;
+          }
+          diag[j][j] = sqrt(dj);
+        }
+        __syncwarp();
+        const double djj = diag[j][j];
+        if (tid > j && tid < nb) diag[tid][j] /= djj;
+        __syncwarp();
+        for (int k = j + 1; k < nb; ++k)
+          if (tid >= k && tid < nb) diag[tid][k] -= diag[tid][j] * diag[k][j];
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < nb * nb; e += blockDim.x) {
+      const int i = e / nb, j = e % nb;
+      if (j <= i) S[(size_t)(jb + i) * q + jb + j] = diag[i][j];
+    }
+    // 2. panel solve: rows below, L21 = A21 L11^-T (one thread per row)
+    for (int i = jb + nb + tid; i < q; i += blockDim.x) {
+      double* r = S + (size_t)i * q + jb;
+      double x[32];
+      for (int j = 0; j < nb; ++j) {
+        double v = r[j];
+        for (int k = 0; k < j; ++k) v -= x[k] * diag[j][k];
+        x[j] = v / diag[j][j];
+      }
+      for (int j = 0; j < nb; ++j) r[j] = x[j];
+    }
+    __syncthreads();
+    // 3. trailing update A22 -= L21 L21^T (lower triangle)
+    const int rest = q - jb - nb;
+    const int64_t cnt = (int64_t)rest * (rest + 1) / 2;
+    for (int64_t e = tid; e < cnt; e += blockDim.x) {
+      // map linear index to (i, j) with j <= i
+      int i = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
+      while ((int64_t)(i + 1) * (i + 2) / 2 <= e) ++i;
+      while ((int64_t)i * (i + 1) / 2 > e) --i;
+      const int j = (int)(e - (int64_t)i * (i + 1) / 2);
+      const double* ri = S + (size_t)(jb + nb + i) * q + jb;
+      const double* rj = S + (size_t)(jb + nb + j) * q + jb;
+      double s = 0.0;
+      for (int k = 0; k < nb; ++k) s += ri[k] * rj[k];
+      S[(size_t)(jb + nb + i) * q + jb + nb + j] -= s;
+    }
+    __syncthreads();
+  }
+  const double f = scale / sqrt((double)q);
+  for (int64_t e = tid; e < (int64_t)q * kq; e += blockDim.x) {
+    const int i = (int)(e / kq), j = (int)(e % kq);
+    const double v = (j < q && j <= i) ? S[(size_t)i * q + j] * f : 0.0;
+    if (j < q) L[(size_t)i * q + j] = (float)v;
+    Lb[e] = __double2bfloat16(v);
+  }
+}
+
+// Proposal normals: Z[k][j] (bf16, [m][kq]) from stream (seed, 3, t, i0+k),
+// block index move*(B4+1) + j/4 (two Box-Muller pairs per block).
+__global__ void rw_normals_kernel(int64_t m, int q, int kq, uint64_t seed, int64_t t, int64_t i0, int move,
+                                  __nv_bfloat16* __restrict__ Z) {
+  const int b4 = (q + 3) / 4;
+  const int kq4 = kq / 4;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m * kq4) return;
+  const int64_t k = e / kq4;
+  const int jb = (int)(e % kq4);
+  __nv_bfloat16* z = Z + k * kq + 4 * jb;
+  if (jb >= b4) {
+    for (int i = 0; i < 4; ++i) z[i] = __float2bfloat16(0.0f);
+    return;
+  }
+  uint64_t w[4];
+  philox_block(stream_key(seed, 3, (uint64_t)t, (uint64_t)(i0 + k)), (uint64_t)move * (b4 + 1) + jb, w);
+  double z0, z1, z2, z3;
+  box_muller_pair(w[0], w[1], z0, z1);
+  box_muller_pair(w[2], w[3], z2, z3);
+  const double zz[4] = {z0, z1, z2, z3};
+  for (int i = 0; i < 4; ++i) z[i] = __double2bfloat16(4 * jb + i < q ? zz[i] : 0.0);
+}
+
+__global__ void rw_accept_kernel(float* __restrict__ beta, int ldb, const float* __restrict__ prop, int q, int64_t m,
+                                 const double* __restrict__ ylin_p, const double* __restrict__ sp_p,
+                                 const double* __restrict__ lp_p, double* __restrict__ ll, double* __restrict__ lp,
+                                 uint64_t seed, int64_t t, int64_t i0, int move, unsigned long long* accepted) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= m) return;
+  int ok = 0;
+  if (lane == 0) {
+    const int b4 = (q + 3) / 4;
+    uint64_t w[4];
+    philox_block(stream_key(seed, 3, (uint64_t)t, (uint64_t)(i0 + row)), (uint64_t)move * (b4 + 1) + b4, w);
+    const double u = u53(w[0]);
+    const double llp = ylin_p[row] - sp_p[row];
+    const double d = (llp + lp_p[row]) - (ll[row] + lp[row]);
+    ok = (d >= 0.0) || (log(u) < d);
+    if (ok) {
+      ll[row] = llp;
+      lp[row] = lp_p[row];
+      atomicAdd(accepted, 1ull);
+    }
+  }
+  ok = __shfl_sync(0xffffffffu, ok, 0);
+  if (ok) {
+    const float* s = prop + row * ldb;
+    float* o = beta + row * ldb;
+    for (int j = lane; j < q; j += 32) o[j] = s[j];
+  }
+}
+
+static inline unsigned cdiv(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
+
+// Likelihood work split: units of BN tiles so the grid covers several waves.
+static void loglik_split(int64_t m, int n, int& m_tiles, int& n_tiles, int& tpu, int& units) {
+  m_tiles = (int)((m + kTcBM - 1) / kTcBM);
+  n_tiles = (n + 255) / 256;
+  int want = (8 * 148 + m_tiles - 1) / m_tiles;
+  units = std::max(1, std::min(n_tiles, want));
+  tpu = (n_tiles + units - 1) / units;
+  units = (n_tiles + tpu - 1) / tpu;
+}
+
+}  // namespace spa
+
+using namespace spa;
+
+// ===========================================================================
+// C ABI
+extern "C" {
+
+const char* spa_last_error(void) { return g_last_error.c_str(); }
+int spa_version(void) { return 1; }
+
+int spa_philox_blocks(uint64_t k0, uint64_t k1, uint64_t first_block, int64_t count, uint64_t* out, void* stream) {
+  SPA_REQUIRE(count >= 0 && out, kBadArgument, "spa_philox_blocks: bad arguments");
+  if (count == 0) return 0;
+  philox_blocks_kernel<<<cdiv(count, 256), 256, 0, as_stream(stream)>>>(Key2{k0, k1}, first_block, count, out);
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+size_t spa_loglik_workspace_bytes(int64_t m, int32_t n) {
+  int mt, nt, tpu, units;
+  loglik_split(m, n, mt, nt, tpu, units);
+  return (size_t)units * (size_t)m * sizeof(double);
+}
+
+static int loglik_impl(const spa_design* d, const void* A, int64_t m, const double* ylin, double* out, void* ws,
+                       size_t ws_bytes, cudaStream_t st) {
+  SPA_REQUIRE(d && A && out && ws, kBadArgument, "spa_loglik: null argument");
+  SPA_REQUIRE(d->kp % 64 == 0 && d->kp > 0, kBadArgument, "spa_loglik: kp must be a positive multiple of 64");
+  SPA_REQUIRE(m > 0 && m < (1ll << 31), kBadArgument, "spa_loglik: m out of range");
+  SPA_REQUIRE(ws_bytes >= spa_loglik_workspace_bytes(m, d->n), kWorkspaceTooSmall, "spa_loglik: workspace too small");
+  SPA_REQUIRE(d->terms == 1 || d->terms == 2, kBadArgument, "spa_loglik: terms must be 1 or 2");
+  TcArgs args;
+  int units;
+  loglik_split(m, d->n, args.m_tiles, args.n_tiles, args.tiles_per_unit, units);
+  args.m = (int)m;
+  args.ncols = d->n;
+  args.kp = d->kp;
+  EpiSoftplusRowSum epi{reinterpret_cast<double*>(ws), 0.f, 0.0};
+  int rc;
+  if (d->terms == 1)
+    rc = launch_tc<2, 1, 256>(A, 2ull * d->kp, d->gemm_b, (uint64_t)d->kp, (uint64_t)d->n, args, units, epi, st);
+  else
+    rc = launch_tc<2, 2, 256>(A, 2ull * d->kp, d->gemm_b, 2ull * d->kp, (uint64_t)d->n, args, units, epi, st);
+  if (rc) return rc;
+  reduce_units_kernel<<<cdiv(m, 256), 256, 0, st>>>(reinterpret_cast<double*>(ws), units, m, ylin, out);
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+int spa_loglik_softplus(const spa_design* d, const void* A, int64_t m, double* out_sp, void* ws, size_t ws_bytes,
+                        void* stream) {
+  return loglik_impl(d, A, m, nullptr, out_sp, ws, ws_bytes, as_stream(stream));
+}
+
+static PriorConst make_prior(double a, double c, double c_prev) {
+  PriorConst p;
+  p.a = a;
+  p.c = c;
+  p.c_prev = c_prev;
+  p.de = std::isinf(a) ? 1 : 0;
+  return p;
+}
+
+int spa_pack_particles(const spa_design* d, const float* beta, int64_t m, int32_t ldb, void* A, double* ylin,
+                       double a, double c, double* lp, void* stream) {
+  SPA_REQUIRE(d && beta && A && ylin && m >= 0, kBadArgument, "spa_pack_particles: bad arguments");
+  SPA_REQUIRE(!d->coded || d->kp >= d->q + 3, kBadArgument, "spa_pack_particles: kp < q + 3");
+  if (m == 0) return 0;
+  pack_kernel<<<cdiv(m, 8), 256, 0, as_stream(stream)>>>(*d, beta, m, ldb, reinterpret_cast<__nv_bfloat16*>(A),
+                                                        ylin, make_prior(a, c, c), lp);
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+int spa_loglik_rows(const spa_design* d, const float* beta, int64_t m, int32_t ldb, void* A_ws, double* ylin_ws,
+                    double* out_ll, void* ws, size_t ws_bytes, void* stream) {
+  int rc = spa_pack_particles(d, beta, m, ldb, A_ws, ylin_ws, 1.0, 1.0, nullptr, stream);
+  if (rc) return rc;
+  return loglik_impl(d, A_ws, m, ylin_ws, out_ll, ws, ws_bytes, as_stream(stream));
+}
+
+int spa_prior_rows(const spa_design* d, const float* beta, int64_t m, int32_t ldb, double a, double c,
+                   double c_prev, int32_t mode, double* out, void* stream) {
+  SPA_REQUIRE(d && beta && out && m >= 0 && (mode == 0 || mode == 1), kBadArgument, "spa_prior_rows: bad arguments");
+  SPA_REQUIRE(a > 0 && c > 0 && c_prev > 0, kBadArgument, "spa_prior_rows: a, c must be positive");
+  if (m == 0) return 0;
+  prior_kernel<<<cdiv(m, 8), 256, 0, as_stream(stream)>>>(*d, beta, m, ldb, make_prior(a, c, c_prev), mode, out);
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+int spa_lse_chunk_stats(const double* logw, const double* lw, int64_t m, double* stats, void* stream) {
+  SPA_REQUIRE(logw && stats && m > 0, kBadArgument, "spa_lse_chunk_stats: bad arguments");
+  lse_stats_kernel<<<cdiv(m, kChunk), 256, 0, as_stream(stream)>>>(logw, lw, m, stats);
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+int spa_lse_combine(const double* stats, int64_t nchunks, double* res, void* stream) {
+  SPA_REQUIRE(stats && res && nchunks > 0, kBadArgument, "spa_lse_combine: bad arguments");
+  lse_combine_kernel<<<1, 32, 0, as_stream(stream)>>>(stats, nchunks, res);
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+int spa_logw_apply(double* logw, const double* lw, int64_t m, const double* res, double* w, void* stream) {
+  SPA_REQUIRE(logw && res && m > 0, kBadArgument, "spa_logw_apply: bad arguments");
+  logw_apply_kernel<<<cdiv(m, 256), 256, 0, as_stream(stream)>>>(logw, lw, m, res, w);
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+size_t spa_resample_workspace_bytes(int64_t N) { return (size_t)N * sizeof(double); }
+
+int spa_systematic_ancestors(const double* w, int64_t N, double u, int64_t k0, int64_t count, int64_t* anc,
+                             void* ws, size_t ws_bytes, void* stream) {
+  SPA_REQUIRE(w && anc && ws && N > 0 && k0 >= 0 && count >= 0 && k0 + count <= N, kBadArgument,
+              "spa_systematic_ancestors: bad arguments");
+  SPA_REQUIRE(ws_bytes >= spa_resample_workspace_bytes(N), kWorkspaceTooSmall,
+              "spa_systematic_ancestors: workspace too small");
+  cudaStream_t st = as_stream(stream);
+  double* cum = reinterpret_cast<double*>(ws);
+  seq_cumsum_kernel<<<1, 64, 0, st>>>(w, N, cum);
+  SPA_CHECK_LAUNCH();
+  if (count == 0) return 0;
+  ancestors_kernel<<<cdiv(count, 256), 256, 0, st>>>(cum, N, u, k0, count, anc);
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+int spa_gather_rows(const float* src, int32_t ld_src, float* dst, int32_t ld_dst, int32_t q, const int64_t* idx,
+                    int64_t base, int64_t m, const double* v0, double* v0_out, const double* v1, double* v1_out,
+                    void* stream) {
+  SPA_REQUIRE(src && dst && idx && m >= 0 && q > 0, kBadArgument, "spa_gather_rows: bad arguments");
+  if (m == 0) return 0;
+  gather_kernel<<<cdiv(m, 8), 256, 0, as_stream(stream)>>>(src, ld_src, dst, ld_dst, q, idx, base, m, v0, v0_out, v1,
+                                                          v1_out);
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const double* w, int32_t phase,
+                   int64_t* partial, void* stream) {
+  SPA_REQUIRE(beta && w && partial && m > 0 && q > 0 && (phase == 0 || phase == 1), kBadArgument,
+              "spa_rw_moments: bad arguments");
+  auto* acc = reinterpret_cast<unsigned long long*>(partial);
+  if (phase == 0) {
+    dim3 grid(cdiv(q, 128), cdiv(m, kMomChunk));
+    rw_mean_kernel<<<grid, 128, 0, as_stream(stream)>>>(beta, m, ldb, q, w, acc);
+  } else {
+    const int tiles = (q + 63) / 64;
+    dim3 grid(tiles * tiles, cdiv(m, kMomChunk));
+    rw_moments_kernel<<<grid, 256, 0, as_stream(stream)>>>(beta, m, ldb, q, w, acc);
+  }
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+int spa_rw_factor(const int64_t* partial, int32_t q, double scale, double jitter, float* L, double* ws, int* info,
+                  void* stream) {
+  SPA_REQUIRE(partial && L && ws && q > 0 && q <= 2048, kBadArgument, "spa_rw_factor: bad arguments");
+  const int kq = (q + 63) / 64 * 64;
+  __nv_bfloat16* Lb = reinterpret_cast<__nv_bfloat16*>(ws + (size_t)q * q);
+  rw_factor_kernel<<<1, 1024, 0, as_stream(stream)>>>(reinterpret_cast<const unsigned long long*>(partial), q, scale,
+                                                      jitter, ws, L, Lb, kq, info);
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ldb, const void* Lb, uint64_t seed,
+                   int64_t t, int64_t i0, int32_t move, float* prop, void* A, double* ylin, double a, double c,
+                   double* lp, void* stream) {
+  SPA_REQUIRE(d && beta && Lb && prop && A && ylin && m > 0, kBadArgument, "spa_rw_propose: bad arguments");
+  SPA_REQUIRE((ldb & 3) == 0, kBadArgument, "spa_rw_propose: ldb must be a multiple of 4");
+  cudaStream_t st = as_stream(stream);
+  const int q = d->q;
+  const int kq = (q + 63) / 64 * 64;
+  __nv_bfloat16* Z = reinterpret_cast<__nv_bfloat16*>(A);
+  rw_normals_kernel<<<cdiv(m * (kq / 4), 256), 256, 0, st>>>(m, q, kq, seed, t, i0, move, Z);
+  SPA_CHECK_LAUNCH();
+  TcArgs args;
+  args.m = (int)m;
+  args.ncols = q;
+  args.kp = kq;
+  args.m_tiles = (int)((m + kTcBM - 1) / kTcBM);
+  args.n_tiles = (q + 255) / 256;
+  args.tiles_per_unit = args.n_tiles;
+  EpiStoreAdd epi{beta, prop, ldb, (int)m};
+  int rc = launch_tc<1, 1, 256>(Z, (uint64_t)kq, Lb, (uint64_t)kq, (uint64_t)q, args, 1, epi, st);
+  if (rc) return rc;
+  return spa_pack_particles(d, prop, m, ldb, A, ylin, a, c, lp, stream);
+}
+
+int spa_rw_accept(float* beta, int32_t ldb, const float* prop, int32_t q, int64_t m, const double* ylin_p,
+                  const double* sp_p, const double* lp_p, double* ll, double* lp, uint64_t seed, int64_t t,
+                  int64_t i0, int32_t move, unsigned long long* accepted, void* stream) {
+  SPA_REQUIRE(beta && prop && ylin_p && sp_p && lp_p && ll && lp && accepted && m > 0, kBadArgument,
+              "spa_rw_accept: bad arguments");
+  rw_accept_kernel<<<cdiv(m, 8), 256, 0, as_stream(stream)>>>(beta, ldb, prop, q, m, ylin_p, sp_p, lp_p, ll, lp, seed,
+                                                             t, i0, move, accepted);
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // extern "C"

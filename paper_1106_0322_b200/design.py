@@ -1,0 +1,144 @@
+"""Device-resident design matrix (the layouts libspa_b200 reads).
+
+Built once per (dataset, intercept) from the host arrays the reference uses
+(reference smc.py:106-123 `make_design`: optional leading unpenalised column
+of ones).  Two representations:
+
+* coded (the genotype case): every column takes at most 3 equally spaced
+  values, x = alpha*g + gamma with g in {0,1,2} (standardised allele counts,
+  reference data.py:131-140, are exactly this).  The tensor-core operand is
+  G itself (exact in bf16) and the MwG kernel reads 2-bit codes from two bit
+  planes.
+* general: arbitrary float columns; the tensor-core operand is the bf16
+  hi/lo split [Xhi | Xlo] and the MwG kernel reads float32 columns.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from ._lib import SpaDesign
+
+K_ALIGN = 64
+
+
+def _round_up(x: int, m: int) -> int:
+    return -(-x // m) * m
+
+
+def mwg_words(n: int) -> int:
+    """32-subject words per column so that the MwG kernel's thread layout
+    (csrc/mwg.cu: S subjects per thread, >= 32 threads) is fully covered."""
+    S = 8 if n <= 256 else (16 if n <= 512 else 32)
+    nthr = max(32, _round_up(-(-n // S), 32))
+    return -(-(nthr * S) // 32)
+
+
+def _code_column(x: np.ndarray):
+    """Return (codes, alpha, gamma, levels) if x = alpha*g + gamma with
+    g in {0,1,2} (at most 3 equally spaced distinct values), else None."""
+    u = np.unique(x)
+    if u.size == 1:
+        return np.zeros(x.size, np.uint8), 0.0, float(u[0]), np.array([u[0], 0.0, 0.0])
+    if u.size > 3:
+        return None
+    step = float(u[1] - u[0])
+    if u.size == 3 and abs((u[2] - u[1]) - step) > 1e-9 * max(1.0, abs(step)):
+        return None
+    g = np.rint((x - u[0]) / step)
+    if np.max(np.abs(u[0] + step * g - x)) > 1e-12 * max(1.0, float(np.max(np.abs(x)))):
+        return None
+    lev = np.zeros(3)
+    lev[: u.size] = u
+    return g.astype(np.uint8), step, float(u[0]), lev
+
+
+@dataclass
+class DeviceDesign:
+    """Owns the device tensors behind one `spa_design` struct."""
+
+    n: int
+    q: int
+    coded: bool
+    kp: int
+    penalized: np.ndarray
+    tensors: dict
+    struct: SpaDesign
+
+    @property
+    def ptr(self):
+        return self.struct
+
+    @classmethod
+    def build(cls, X, y, intercept: bool = False, device=None) -> "DeviceDesign":
+        X = np.asarray(X, dtype=np.float64)
+        y = np.asarray(y, dtype=np.float64)
+        if intercept:
+            X = np.column_stack([np.ones(X.shape[0]), X])
+        n, q = X.shape
+        pen = np.ones(q, dtype=np.uint8)
+        if intercept:
+            pen[0] = 0
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        coded_cols = [_code_column(X[:, j]) for j in range(q)]
+        coded = all(c is not None for c in coded_cols)
+        n_words = mwg_words(n)
+        npad = n_words * 32
+        sy = X.T @ y
+        t = {}
+        if coded:
+            codes = np.stack([c[0] for c in coded_cols])  # [q][n]
+            alpha = np.array([c[1] for c in coded_cols])
+            gamma = np.array([c[2] for c in coded_cols])
+            lev = np.zeros((q, 4), np.float32)
+            lev[:, :3] = np.stack([c[3] for c in coded_cols])
+            b1 = np.zeros((q, npad), bool)
+            b2 = np.zeros((q, npad), bool)
+            b1[:, :n] = codes == 1
+            b2[:, :n] = codes == 2
+            b1[:, n:] = True  # padding subjects carry code (1,1)
+            b2[:, n:] = True
+            p1 = np.packbits(b1, axis=1, bitorder="little").view("<u4")
+            p2 = np.packbits(b2, axis=1, bitorder="little").view("<u4")
+            planes = np.stack([p1, p2], axis=-1).astype(np.uint32)  # [q][n_words][2]
+            kp = _round_up(q + 3, K_ALIGN)
+            G = np.zeros((n, kp), np.float32)
+            G[:, :q] = codes.T
+            G[:, q:q + 3] = 1.0
+            t["planes"] = torch.from_numpy(planes.view(np.int32).copy()).to(dev)
+            t["xlev"] = torch.from_numpy(lev).to(dev)
+            t["alpha"] = torch.from_numpy(alpha).to(dev)
+            t["gamma"] = torch.from_numpy(gamma).to(dev)
+            t["gemm_b"] = torch.from_numpy(G).to(dev).to(torch.bfloat16).contiguous()
+            terms = 1
+        else:
+            kp = _round_up(q, K_ALIGN)
+            xc = np.zeros((q, npad), np.float32)
+            xc[:, :n] = X.T
+            t["xcols"] = torch.from_numpy(xc).to(dev)
+            Xf = torch.zeros((n, kp), dtype=torch.float64)
+            Xf[:, :q] = torch.from_numpy(X)
+            hi = Xf.to(torch.bfloat16)
+            lo = (Xf - hi.to(torch.float64)).to(torch.bfloat16)
+            t["gemm_b"] = torch.cat([hi, lo], dim=1).contiguous().to(dev)
+            t["xlev"] = torch.zeros((q, 4), dtype=torch.float32, device=dev)
+            t["alpha"] = torch.ones(q, dtype=torch.float64, device=dev)
+            t["gamma"] = torch.zeros(q, dtype=torch.float64, device=dev)
+            terms = 2
+        t["sy"] = torch.from_numpy(sy).to(dev)
+        t["penalized"] = torch.from_numpy(pen).to(dev)
+        s = SpaDesign()
+        s.n, s.q, s.coded, s.n_words = n, q, int(coded), n_words
+        s.planes = t["planes"].data_ptr() if coded else None
+        s.xcols = None if coded else t["xcols"].data_ptr()
+        s.xlev = t["xlev"].data_ptr()
+        s.sy = t["sy"].data_ptr()
+        s.alpha = t["alpha"].data_ptr()
+        s.gamma = t["gamma"].data_ptr()
+        s.penalized = t["penalized"].data_ptr()
+        s.gemm_b = t["gemm_b"].data_ptr()
+        s.kp, s.terms = kp, terms
+        return cls(n, q, coded, kp, pen.astype(bool), t, s)

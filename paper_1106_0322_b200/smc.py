@@ -1,0 +1,666 @@
+"""Drop-in replacement for the reference sampler surface (`spa.smc`).
+
+Public API mirrors reference pkg/src/spa/smc.py:
+    Schedule, make_schedule, SmcConfig, StepRecord, SmcOutput, DegeneracyError,
+    ParticleSystem, init_particles, reweight, ess, systematic_resample_indices,
+    systematic_resample, smc_step, run_sampler, fixed_b_mcmc, save_run, load_run
+with the same argument meanings, output layout and error behaviour.  All
+arithmetic on particles runs in libspa_b200 (hand-written sm_100a kernels)
+through the C ABI; the host only orders launches, makes the ESS branch and
+copies snapshots out.
+
+Extra SmcConfig fields (defaults keep the reference's behaviour):
+    move_kernel  "mwg" (reference Metropolis-within-Gibbs, default) or "rw"
+                 (north-star population-covariance random walk on tcgen05)
+    moves        RW moves per step
+    rw_scale     RW proposal scale numerator (scale = rw_scale / sqrt(q))
+    init_chains  parallel MwG chains for initialisation (0 = auto)
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._philox_host import first_uniform
+from .design import DeviceDesign
+from .model import GtPrior
+
+TAG_INIT, TAG_MOVE, TAG_RESAMPLE, TAG_RWMOVE = 0, 1, 2, 3
+
+# Optional CUDA-event timer around the dominant kernel (bench.py sets it;
+# events are recorded on the launching stream).
+KERNEL_TIMER = None
+_CHUNK = 4096
+TRACE_COLUMNS = ("t", "b", "ess", "log_z_ratio_cum", "acceptance_rate")
+
+
+class DegeneracyError(RuntimeError):
+    """All particle weights collapsed to zero mass (reference smc.py:31-32)."""
+
+
+@dataclass(frozen=True)
+class Schedule:
+    """Geometric scale sequence b_t = b1 * rho^(t-1), t = 1..T (smc.py:46-64)."""
+
+    b1: float
+    rho: float
+    T: int
+
+    def __post_init__(self):
+        if not self.b1 > 0:
+            raise ValueError(f"b1 must be positive, got {self.b1}")
+        if not 0.0 < self.rho < 1.0:
+            raise ValueError(f"rho must lie in (0, 1) for a decreasing schedule, got {self.rho}")
+        if self.T < 1:
+            raise ValueError(f"T must be >= 1, got {self.T}")
+
+    @property
+    def bs(self) -> np.ndarray:
+        return self.b1 * self.rho ** np.arange(self.T)
+
+
+def make_schedule(b1: float, rho: float, T: int) -> Schedule:
+    return Schedule(b1, rho, T)
+
+
+@dataclass
+class SmcConfig:
+    """Sampler knobs (smc.py:71-103) plus the B200 extensions above."""
+
+    N: int = 8192
+    cycles: int = 5
+    step_sd: float = 0.5
+    ess_threshold_frac: float = 0.75
+    seed: int = 0
+    init_burn: int = 2000
+    init_thin: int = 5
+    snapshot_thin: int = 1
+    threads: int = 1
+    move_kernel: str = "mwg"
+    moves: int = 5
+    rw_scale: float = 2.38
+    init_chains: int = 0
+
+    def __post_init__(self):
+        if self.N < 2:
+            raise ValueError(f"need at least 2 particles, got N={self.N}")
+        if self.cycles < 1:
+            raise ValueError(f"cycles must be >= 1, got {self.cycles}")
+        if not self.step_sd > 0:
+            raise ValueError(f"step_sd must be positive, got {self.step_sd}")
+        if not 0.0 < self.ess_threshold_frac <= 1.0:
+            raise ValueError(f"ESS threshold fraction must lie in (0, 1], got {self.ess_threshold_frac}")
+        if self.seed < 0:
+            raise ValueError(f"seed must be nonnegative, got {self.seed}")
+        if self.init_burn < 0 or self.init_thin < 1 or self.snapshot_thin < 1 or self.threads < 1:
+            raise ValueError("init_burn >= 0, init_thin >= 1, snapshot_thin >= 1, threads >= 1 required")
+        if self.move_kernel not in ("mwg", "rw"):
+            raise ValueError(f"move_kernel must be 'mwg' or 'rw', got {self.move_kernel!r}")
+        if self.moves < 1 or self.init_chains < 0 or not self.rw_scale > 0:
+            raise ValueError("moves >= 1, init_chains >= 0, rw_scale > 0 required")
+
+
+@dataclass
+class StepRecord:
+    """Per-step trace entry with the particle snapshot when retained (smc.py:362-374)."""
+
+    t: int
+    b: float
+    ess: float
+    log_z_ratio_cum: float
+    acceptance: float
+    resampled: bool
+    weights: np.ndarray | None = None
+    particles: np.ndarray | None = None
+    logliks: np.ndarray | None = None
+
+
+@dataclass
+class SmcOutput:
+    """Configuration echo and per-step records (smc.py:377-394)."""
+
+    a: float
+    schedule: Schedule
+    config: SmcConfig
+    intercept: bool
+    names: list
+    steps: list
+    init_acceptance: float
+    timings: dict = field(default_factory=dict)
+
+    @property
+    def c_values(self) -> np.ndarray:
+        return self.schedule.bs / self.a
+
+    def step(self, t: int) -> StepRecord:
+        return self.steps[t - 1]
+
+
+# ---------------------------------------------------------------------------
+# device plumbing
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1106_0322_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
+    _lib.load()
+
+
+def _round_up(x, m):
+    return -(-x // m) * m
+
+
+class ParticleSystem:
+    """Device-resident particle state (reference smc.py:126-168).
+
+    beta [N][ldb] float32, loglik / logprior / log_weights [N] float64.
+    The reference's fp64 eta cache is not kept: the kernels rematerialise
+    eta (MwG) or never form it in HBM (tensor-core likelihood).
+    """
+
+    def __init__(self, design: DeviceDesign, N: int, prior_a: float, intercept: bool = False,
+                 rank_offset: int = 0, N_total: int | None = None):
+        self.design = design
+        self.N = int(N)
+        self.N_total = int(N_total if N_total is not None else N)
+        self.i0 = int(rank_offset)
+        self.q = design.q
+        self.ldb = _round_up(self.q, 4)
+        self.prior_a = float(prior_a)
+        self.intercept = bool(intercept)
+        self.t = 1
+        self.log_z_cum = 0.0
+        dev = design.tensors["sy"].device
+        self.device = dev
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.beta = torch.zeros((self.N, self.ldb), dtype=torch.float32, device=dev)
+        self.beta_alt = torch.empty_like(self.beta)
+        self.ll = torch.zeros(self.N, **f64)
+        self.lp = torch.zeros(self.N, **f64)
+        self.ll_alt = torch.empty_like(self.ll)
+        self.lp_alt = torch.empty_like(self.lp)
+        self.logw = torch.full((self.N,), -math.log(self.N_total), **f64)
+        self.lw = torch.empty(self.N, **f64)
+        self.w = torch.empty(self.N, **f64)
+        self.nchunks = -(-self.N // _CHUNK)
+        self.stats = torch.empty((self.nchunks, 3), **f64)
+        self.res = torch.empty(3, **f64)
+        self.counter = torch.zeros(1, dtype=torch.int64, device=dev)
+        self._rw = None
+        self._ll_ws = None
+
+    # --- reference-compatible host views -------------------------------
+    @property
+    def betas(self) -> np.ndarray:
+        return self.beta[:, : self.q].double().cpu().numpy()
+
+    @property
+    def logliks(self) -> np.ndarray:
+        return self.ll.cpu().numpy()
+
+    @property
+    def log_weights(self) -> np.ndarray:
+        return self.logw.cpu().numpy()
+
+    @log_weights.setter
+    def log_weights(self, v):
+        self.logw.copy_(torch.as_tensor(np.asarray(v, dtype=np.float64)))
+
+    @property
+    def weights(self) -> np.ndarray:
+        return self.device_weights().cpu().numpy()
+
+    def ess(self) -> float:
+        _lse(self, None)
+        return float(self.res[1].item())
+
+    def device_weights(self) -> torch.Tensor:
+        """Normalised weights exp(logw - lse(logw)) (smc.py:151-154), on device."""
+        _lse(self, None)
+        _lib.call("spa_logw_apply", _p(self.logw), None, self.N, _p(self.res), _p(self.w), _stream())
+        return self.w
+
+    def load_betas(self, B: np.ndarray):
+        B = np.asarray(B, dtype=np.float64)
+        self.beta.zero_()
+        self.beta[:, : self.q] = torch.from_numpy(B).to(self.beta.device, torch.float32)
+
+    # --- work buffers -----------------------------------------------------
+    def ll_workspace(self):
+        if self._ll_ws is None:
+            d = self.design
+            kq = _round_up(self.q, 64)
+            a_cols = max(2 * d.kp, kq)
+            nbytes = _lib.load().spa_loglik_workspace_bytes(self.N, d.n)
+            self._ll_ws = dict(
+                A=torch.empty((self.N, a_cols), dtype=torch.bfloat16, device=self.device),
+                ylin=torch.empty(self.N, dtype=torch.float64, device=self.device),
+                sp=torch.empty(self.N, dtype=torch.float64, device=self.device),
+                ws=torch.empty(max(nbytes, 8), dtype=torch.uint8, device=self.device),
+            )
+        return self._ll_ws
+
+    def rw_workspace(self):
+        if self._rw is None:
+            q = self.q
+            kq = _round_up(q, 64)
+            dev = self.device
+            self._rw = dict(
+                prop=torch.zeros((self.N, self.ldb), dtype=torch.float32, device=dev),
+                lp_p=torch.empty(self.N, dtype=torch.float64, device=dev),
+                acc=torch.zeros(q + q * q, dtype=torch.int64, device=dev),
+                L=torch.empty((q, q), dtype=torch.float32, device=dev),
+                fws=torch.empty(q * q + (q * kq + 3) // 4, dtype=torch.float64, device=dev),
+                info=torch.zeros(1, dtype=torch.int32, device=dev),
+            )
+        return self._rw
+
+    def factor_operand(self):
+        rw = self.rw_workspace()
+        return ctypes.c_void_p(rw["fws"].data_ptr() + 8 * self.q * self.q)
+
+
+def _lse(system: ParticleSystem, lw):
+    _lib.call("spa_lse_chunk_stats", _p(system.logw), _p(lw), system.N, _p(system.stats), _stream())
+    _lib.call("spa_lse_combine", _p(system.stats), system.nchunks, _p(system.res), _stream())
+
+
+# ---------------------------------------------------------------------------
+# reference building blocks
+
+
+def ess(weights) -> float:
+    """Effective sample size 1 / sum(W^2) of normalised weights (smc.py:171-174),
+    computed by the K3 chunk kernels: ESS = (sum w)^2 / sum w^2."""
+    _require_cuda()
+    w = torch.as_tensor(np.asarray(weights, dtype=np.float64)).cuda()
+    with np.errstate(divide="ignore"):
+        logw = torch.log(w)
+    m = w.numel()
+    nch = -(-m // _CHUNK)
+    stats = torch.empty((nch, 3), dtype=torch.float64, device=w.device)
+    res = torch.empty(3, dtype=torch.float64, device=w.device)
+    _lib.call("spa_lse_chunk_stats", _p(logw), None, m, _p(stats), _stream())
+    _lib.call("spa_lse_combine", _p(stats), nch, _p(res), _stream())
+    return float(res[1].item())
+
+
+def systematic_resample_indices(weights, u: float) -> np.ndarray:
+    """Ancestor indices for one systematic draw u in [0, 1/N) (smc.py:273-281),
+    bit-exact (K4 kernel: sequential float64 cumsum + parallel search)."""
+    _require_cuda()
+    w = torch.as_tensor(np.ascontiguousarray(weights, dtype=np.float64)).cuda()
+    N = w.numel()
+    anc = torch.empty(N, dtype=torch.int64, device=w.device)
+    ws = torch.empty(max(8 * N, 8), dtype=torch.uint8, device=w.device)
+    _lib.call("spa_systematic_ancestors", _p(w), N, float(u), 0, N, _p(anc), _p(ws), ws.numel(), _stream())
+    return anc.cpu().numpy()
+
+
+def _penalized_count(system):
+    return int(system.design.penalized.sum())
+
+
+def reweight(system: ParticleSystem, prior_t: GtPrior, prior_prev: GtPrior):
+    """Reweight toward the new scale; the likelihood cancels (smc.py:248-263).
+
+    Returns (incremental log-weights, log Z_t/Z_{t-1}) and leaves the
+    system's log-weights renormalised."""
+    if prior_t.a != prior_prev.a:
+        raise ValueError("consecutive targets must share the degrees of freedom")
+    inc = _reweight_device(system, prior_t, prior_prev)
+    return system.lw.cpu().numpy(), inc
+
+
+def _reweight_device(system: ParticleSystem, prior_t: GtPrior, prior_prev: GtPrior, group=None) -> float:
+    d = system.design
+    _lib.call("spa_prior_rows", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb, float(prior_t.a),
+              float(prior_t.c), float(prior_prev.c), 1, _p(system.lw), _stream())
+    _lib.call("spa_lse_chunk_stats", _p(system.logw), _p(system.lw), system.N, _p(system.stats), _stream())
+    stats = system.stats
+    nch = system.nchunks
+    if group is not None:
+        stats = group.all_gather_cat(system.stats)
+        nch = stats.shape[0]
+    _lib.call("spa_lse_combine", _p(stats), nch, _p(system.res), _stream())
+    res = system.res.cpu()
+    inc = float(res[0])
+    if not math.isfinite(inc):
+        raise DegeneracyError("all incremental weights vanished")
+    _lib.call("spa_logw_apply", _p(system.logw), _p(system.lw), system.N, _p(system.res), None, _stream())
+    system._ess_after_reweight = float(res[1])
+    return inc
+
+
+def systematic_resample(system: ParticleSystem, rng_or_u, group=None) -> np.ndarray:
+    """Resample in place with one uniform; weights reset to 1/N (smc.py:284-295).
+    `rng_or_u` is a float u in [0, 1) (the reference passes a Generator whose
+    first draw is u; pass `first_uniform(seed, 2, t)` to reproduce it)."""
+    u = float(rng_or_u.random()) if hasattr(rng_or_u, "random") else float(rng_or_u)
+    u = u / system.N_total
+    d_anc = _resample_device(system, u, group)
+    return d_anc.cpu().numpy()
+
+
+def _resample_device(system: ParticleSystem, u: float, group=None) -> torch.Tensor:
+    N = system.N_total
+    # normalised weights (smc.py:151-154) of this shard, gathered over shards
+    w = system.device_weights() if group is None else _global_weights(system, group)
+    w_full = w if group is None else group.all_gather_cat(w)
+    anc = torch.empty(N, dtype=torch.int64, device=system.device)
+    ws = torch.empty(8 * N, dtype=torch.uint8, device=system.device)
+    _lib.call("spa_systematic_ancestors", _p(w_full), N, u, 0, N, _p(anc), _p(ws), ws.numel(), _stream())
+    if group is None:
+        _lib.call("spa_gather_rows", _p(system.beta), system.ldb, _p(system.beta_alt), system.ldb, system.q, _p(anc),
+                  0, system.N, _p(system.ll), _p(system.ll_alt), _p(system.lp), _p(system.lp_alt), _stream())
+    else:
+        group.exchange_rows(system, anc)
+    system.beta, system.beta_alt = system.beta_alt, system.beta
+    system.ll, system.ll_alt = system.ll_alt, system.ll
+    system.lp, system.lp_alt = system.lp_alt, system.lp
+    system.logw.fill_(-math.log(N))
+    return anc
+
+
+# ---------------------------------------------------------------------------
+# moves
+
+
+def _mwg(system: ParticleSystem, prior: GtPrior, sd: float, cycles: int, seed: int, tag: int, t: int,
+         sweep0: int = 0) -> int:
+    d = system.design
+    system.counter.zero_()
+    _lib.call("spa_mwg_move", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb, float(prior.a),
+              float(prior.c), float(sd), int(cycles), int(seed), int(tag), int(t), int(system.i0), int(sweep0),
+              _p(system.ll), _p(system.lp), _p(system.counter), _stream())
+    return int(system.counter.item())
+
+
+def _loglik_device(system: ParticleSystem, out: torch.Tensor):
+    d = system.design
+    ws = system.ll_workspace()
+    _lib.call("spa_loglik_rows", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb, _p(ws["A"]),
+              _p(ws["ylin"]), _p(out), _p(ws["ws"]), ws["ws"].numel(), _stream())
+
+
+def _rw_factor(system: ParticleSystem, scale: float, group=None):
+    rw = system.rw_workspace()
+    w = system.device_weights() if group is None else _global_weights(system, group)
+    rw["acc"].zero_()
+    _lib.call("spa_rw_moments", _p(system.beta), system.N, system.ldb, system.q, _p(w), 0, _p(rw["acc"]), _stream())
+    if group is not None:
+        group.all_reduce_sum(rw["acc"])
+    _lib.call("spa_rw_moments", _p(system.beta), system.N, system.ldb, system.q, _p(w), 1, _p(rw["acc"]), _stream())
+    if group is not None:
+        group.all_reduce_sum(rw["acc"][system.q:])
+    _lib.call("spa_rw_factor", _p(rw["acc"]), system.q, float(scale), 1e-6, _p(rw["L"]), _p(rw["fws"]),
+              _p(rw["info"]), _stream())
+
+
+def _global_weights(system, group):
+    # weights normalised over all shards: logw is globally normalised already
+    _lib.call("spa_logw_apply", _p(system.logw), None, system.N, _p(group.zero_res(system)), _p(system.w), _stream())
+    return system.w
+
+
+def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int, group=None) -> int:
+    d = system.design
+    ws = system.ll_workspace()
+    rw = system.rw_workspace()
+    _rw_factor(system, config.rw_scale, group)
+    # log-prior of the current particles at the new scale
+    _lib.call("spa_prior_rows", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb, float(prior.a),
+              float(prior.c), float(prior.c), 0, _p(system.lp), _stream())
+    system.counter.zero_()
+    Lb = system.factor_operand()
+    for mv in range(config.moves):
+        _lib.call("spa_rw_propose", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb, Lb,
+                  int(config.seed), int(t), int(system.i0), mv, _p(rw["prop"]), _p(ws["A"]), _p(ws["ylin"]),
+                  float(prior.a), float(prior.c), _p(rw["lp_p"]), _stream())
+        if KERNEL_TIMER is not None:
+            KERNEL_TIMER.start("loglik")
+        _lib.call("spa_loglik_softplus", ctypes.byref(d.struct), _p(ws["A"]), system.N, _p(ws["sp"]), _p(ws["ws"]),
+                  ws["ws"].numel(), _stream())
+        if KERNEL_TIMER is not None:
+            KERNEL_TIMER.stop("loglik")
+        _lib.call("spa_rw_accept", _p(system.beta), system.ldb, _p(rw["prop"]), system.q, system.N, _p(ws["ylin"]),
+                  _p(ws["sp"]), _p(rw["lp_p"]), _p(system.ll), _p(system.lp), int(config.seed), int(t),
+                  int(system.i0), mv, _p(system.counter), _stream())
+    acc = system.counter if group is None else group.all_reduce_sum(system.counter.clone())
+    return int(acc.item())
+
+
+# ---------------------------------------------------------------------------
+# initialisation (reference smc.py:202-245, as parallel chains)
+
+
+def init_particles(data, prior_at_b1: GtPrior, config: SmcConfig, intercept: bool = False, design=None,
+                   group=None):
+    """Seed the particles from MwG chains targeting the first posterior.
+
+    The reference runs ONE chain (init_burn sweeps, then every init_thin-th
+    state).  Here K = config.init_chains (auto: min(N, 1024)) independent
+    chains run in parallel on the GPU, each burning init_burn sweeps and then
+    contributing every init_thin-th state; chain c keyed (seed, 0, 0, c).
+    Returns (system, acceptance_rate)."""
+    _require_cuda()
+    if design is None:
+        design = DeviceDesign.build(data.X, data.y, intercept)
+    N_total = config.N
+    shard, offset = (N_total, 0) if group is None else group.shard(N_total)
+    system = ParticleSystem(design, shard, prior_at_b1.a, intercept, rank_offset=offset, N_total=N_total)
+    K = config.init_chains or min(N_total, 1024)
+    K = max(1, min(K, N_total))
+    chains = ParticleSystem(design, K, prior_at_b1.a, intercept)
+    acc = _mwg(chains, prior_at_b1, config.step_sd, config.init_burn, config.seed, TAG_INIT, 0, 0) \
+        if config.init_burn > 0 else 0
+    rounds = -(-N_total // K)
+    sweeps = config.init_burn
+    lo_mine, hi_mine = offset, offset + shard
+    for r in range(rounds):
+        acc += _mwg(chains, prior_at_b1, config.step_sd, config.init_thin, config.seed, TAG_INIT, 0, sweeps)
+        sweeps += config.init_thin
+        # slots r*K .. r*K+K-1 take chain states 0..K-1 (only those in this shard)
+        s0, s1 = r * K, min(N_total, (r + 1) * K)
+        a, b = max(s0, lo_mine), min(s1, hi_mine)
+        if a < b:
+            system.beta[a - offset:b - offset].copy_(chains.beta[a - s0:b - s0])
+            system.ll[a - offset:b - offset].copy_(chains.ll[a - s0:b - s0])
+            system.lp[a - offset:b - offset].copy_(chains.lp[a - s0:b - s0])
+    total = K * (config.init_burn + rounds * config.init_thin) * design.q
+    return system, acc / max(total, 1)
+
+
+# ---------------------------------------------------------------------------
+# one lambda step (reference smc.py:397-424)
+
+
+def smc_step(system: ParticleSystem, data, schedule: Schedule, t: int, config: SmcConfig, group=None) -> StepRecord:
+    """Advance from step t-1 to t: reweight -> accumulate evidence -> ESS ->
+    resample if ESS < frac*N -> move with the invariant kernel at prior_t."""
+    if not 2 <= t <= schedule.T:
+        raise ValueError(f"step index {t} outside [2, {schedule.T}]")
+    if system.t != t - 1:
+        raise ValueError(f"system is at step {system.t}, cannot advance to {t}")
+    a = system.prior_a
+    bs = schedule.bs
+    prior_prev = GtPrior(a, bs[t - 2] / a)
+    prior_t = GtPrior(a, bs[t - 1] / a)
+    try:
+        inc = _reweight_device(system, prior_t, prior_prev, group)
+    except DegeneracyError as exc:
+        raise DegeneracyError(f"step {t}: {exc}") from None
+    system.log_z_cum += inc
+    step_ess = system._ess_after_reweight
+    resampled = step_ess < config.ess_threshold_frac * system.N_total
+    if resampled:
+        u = first_uniform(config.seed, TAG_RESAMPLE, t) / system.N_total
+        _resample_device(system, u, group)
+    if config.move_kernel == "mwg":
+        acc = _mwg(system, prior_t, config.step_sd, config.cycles, config.seed, TAG_MOVE, t, 0)
+        if group is not None:
+            acc = int(group.all_reduce_sum(torch.tensor([acc], dtype=torch.int64, device=system.device)).item())
+        acceptance = acc / (system.N_total * config.cycles * system.q)
+    else:
+        if t == 2 or not getattr(system, "_ll_from_k1", False):
+            _loglik_device(system, system.ll)  # keep ll on the K1 arithmetic the MH ratio uses
+            system._ll_from_k1 = True
+        acc = _rw_moves(system, prior_t, config, t, group)
+        acceptance = acc / (system.N_total * config.moves)
+    system.t = t
+    return StepRecord(t, float(bs[t - 1]), float(step_ess), system.log_z_cum, acceptance, bool(resampled))
+
+
+def _snapshot(system: ParticleSystem, record: StepRecord, group=None):
+    w = system.device_weights() if group is None else _global_weights(system, group)
+    beta = system.beta[:, : system.q]
+    ll = system.ll
+    if group is not None:
+        w, beta, ll = group.gather_to_all(w), group.gather_to_all(beta.contiguous()), group.gather_to_all(ll)
+    record.weights = w.cpu().numpy().copy()
+    record.weights /= record.weights.sum()
+    record.particles = beta.cpu().numpy().astype(np.float64)  # float32 state, float64 output layout
+    record.logliks = ll.cpu().numpy().copy()
+    return record
+
+
+def run_sampler(data, a: float, schedule: Schedule, config: SmcConfig, intercept: bool = False,
+                group=None) -> SmcOutput:
+    """Initialise at the most diffuse scale and sweep the whole schedule
+    (reference smc.py:427-449).  `group` (optional) is a
+    `paper_1106_0322_b200.dist.ParticleGroup` sharding particles over GPUs."""
+    _require_cuda()
+    import time
+
+    timings = {}
+    t0 = time.perf_counter()
+    design = DeviceDesign.build(data.X, data.y, intercept)
+    prior1 = GtPrior(a, schedule.bs[0] / a)
+    system, init_acc = init_particles(data, prior1, config, intercept, design=design, group=group)
+    torch.cuda.synchronize()
+    timings["init_s"] = time.perf_counter() - t0
+    names = (["intercept"] if intercept else []) + list(data.names)
+
+    def retained(t):
+        return t == 1 or t == schedule.T or (t - 1) % config.snapshot_thin == 0
+
+    def snap(rec):
+        return _snapshot(system, rec, group) if retained(rec.t) else rec
+
+    steps = [snap(StepRecord(1, float(schedule.bs[0]), float(config.N), 0.0, init_acc, False))]
+    t1 = time.perf_counter()
+    for t in range(2, schedule.T + 1):
+        steps.append(snap(smc_step(system, data, schedule, t, config, group)))
+    torch.cuda.synchronize()
+    timings["path_s"] = time.perf_counter() - t1
+    return SmcOutput(float(a), schedule, config, intercept, names, steps, init_acc, timings)
+
+
+def fixed_b_mcmc(data, prior: GtPrior, n_samples: int, burn: int = 2000, thin: int = 5, seed: int = 0,
+                 step_sd: float = 0.5, intercept: bool = False):
+    """Fixed-prior MwG validation chains (reference smc.py:452-476), run as
+    min(n_samples, 1024) parallel chains on the GPU."""
+    cfg = SmcConfig(N=max(2, n_samples), step_sd=step_sd, seed=seed, init_burn=burn, init_thin=thin)
+    system, acc = init_particles(data, prior, cfg, intercept)
+    return FixedBResult(system.betas[:n_samples], acc)
+
+
+@dataclass
+class FixedBResult:
+    samples: np.ndarray
+    acceptance: float
+
+
+# ---------------------------------------------------------------------------
+# run-directory persistence (reference smc.py:479-592, same files and format)
+
+
+def _fmt(v: float) -> str:
+    return f"{v:.17g}"
+
+
+def manifest_entries(output: SmcOutput) -> dict:
+    from . import __version__
+
+    cfg = output.config
+    return {
+        "a": _fmt(output.a), "b1": _fmt(output.schedule.b1), "rho": _fmt(output.schedule.rho),
+        "T": output.schedule.T, "N": cfg.N, "cycles": cfg.cycles, "step_sd": _fmt(cfg.step_sd),
+        "ess_frac": _fmt(cfg.ess_threshold_frac), "seed": cfg.seed, "init_burn": cfg.init_burn,
+        "init_thin": cfg.init_thin, "snapshot_thin": cfg.snapshot_thin, "threads": cfg.threads,
+        "intercept": str(output.intercept).lower(), "spa_version": __version__,
+        "numpy_version": np.__version__, "move_kernel": cfg.move_kernel, "moves": cfg.moves,
+    }
+
+
+def save_run(output: SmcOutput, outdir, extra: dict | None = None) -> None:
+    os.makedirs(outdir, exist_ok=True)
+    entries = manifest_entries(output)
+    if extra:
+        entries.update(extra)
+    with open(os.path.join(outdir, "manifest.txt"), "w") as fh:
+        for k, v in entries.items():
+            fh.write(f"{k} = {v}\n")
+    with open(os.path.join(outdir, "trace.csv"), "w") as fh:
+        fh.write(",".join(TRACE_COLUMNS) + "\n")
+        for s in output.steps:
+            fh.write(f"{s.t},{_fmt(s.b)},{_fmt(s.ess)},{_fmt(s.log_z_ratio_cum)},{_fmt(s.acceptance)}\n")
+    for s in output.steps:
+        if s.particles is None:
+            continue
+        with open(os.path.join(outdir, f"particles_t{s.t:04d}.csv"), "w") as fh:
+            fh.write("particle_index,weight," + ",".join(output.names) + "\n")
+            for i in range(s.particles.shape[0]):
+                fh.write(f"{i},{_fmt(s.weights[i])}," + ",".join(_fmt(v) for v in s.particles[i]) + "\n")
+
+
+def load_run(outdir) -> SmcOutput:
+    kv = {}
+    with open(os.path.join(outdir, "manifest.txt")) as fh:
+        for line in fh:
+            line = line.strip()
+            if line and not line.startswith("#"):
+                k, _, v = line.partition("=")
+                kv[k.strip()] = v.strip()
+    config = SmcConfig(N=int(kv["N"]), cycles=int(kv["cycles"]), step_sd=float(kv["step_sd"]),
+                       ess_threshold_frac=float(kv["ess_frac"]), seed=int(kv["seed"]),
+                       init_burn=int(kv["init_burn"]), init_thin=int(kv["init_thin"]),
+                       snapshot_thin=int(kv["snapshot_thin"]), threads=int(kv["threads"]),
+                       move_kernel=kv.get("move_kernel", "mwg"), moves=int(kv.get("moves", 5)))
+    schedule = Schedule(float(kv["b1"]), float(kv["rho"]), int(kv["T"]))
+    steps, names = [], []
+    with open(os.path.join(outdir, "trace.csv")) as fh:
+        header = fh.readline().strip().split(",")
+        if tuple(header) != TRACE_COLUMNS:
+            raise ValueError(f"{outdir}/trace.csv: unexpected columns {header}")
+        for line in fh:
+            t_s, b_s, e_s, z_s, a_s = line.strip().split(",")
+            e = float(e_s)
+            steps.append(StepRecord(int(t_s), float(b_s), e, float(z_s), float(a_s),
+                                    int(t_s) > 1 and e < config.ess_threshold_frac * config.N))
+    for rec in steps:
+        path = os.path.join(outdir, f"particles_t{rec.t:04d}.csv")
+        if not os.path.exists(path):
+            continue
+        with open(path) as fh:
+            names = fh.readline().strip().split(",")[2:]
+            block = np.loadtxt(fh, delimiter=",", ndmin=2)
+        rec.weights = block[:, 1]
+        rec.particles = block[:, 2:]
+    return SmcOutput(float(kv["a"]), schedule, config, kv.get("intercept", "false") == "true", names, steps,
+                     steps[0].acceptance if steps else 0.0)

@@ -1,0 +1,223 @@
+"""Per-kernel parity of the CUDA path against the golden vectors / oracle.
+
+Tolerances:
+  * Philox words, resampling ancestors: bit-exact;
+  * per-particle log-likelihood (K1, bf16 hi/lo split on tcgen05, fp32
+    accumulate): <= 1e-5 relative to the reference float64 values;
+  * log-prior / reweight increments (float64 kernels): <= 1e-12 relative;
+  * LSE / ESS: <= 1e-12 relative.
+"""
+
+import ctypes
+import hashlib
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import spa_oracle as orc  # noqa: E402
+from paper_1106_0322_b200 import _lib  # noqa: E402
+from paper_1106_0322_b200.design import DeviceDesign  # noqa: E402
+from paper_1106_0322_b200.smc import ParticleSystem, _p, _stream  # noqa: E402
+
+LL_RTOL = 1e-5
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def system_from(X, y, B, intercept=False, a=1.0):
+    d = DeviceDesign.build(X, y, intercept)
+    s = ParticleSystem(d, B.shape[0], a, intercept)
+    s.load_betas(B)
+    return d, s
+
+
+def gpu_loglik(X, y, B, intercept=False):
+    d, s = system_from(X, y, B, intercept)
+    out = torch.empty(s.N, dtype=torch.float64, device="cuda")
+    ws = s.ll_workspace()
+    _lib.call("spa_loglik_rows", ctypes.byref(d.struct), _p(s.beta), s.N, s.ldb, _p(ws["A"]), _p(ws["ylin"]),
+              _p(out), _p(ws["ws"]), ws["ws"].numel(), _stream())
+    return out.cpu().numpy()
+
+
+def test_philox_bits(gold_philox):
+    for key, raw in zip(gold_philox["keys"], gold_philox["raw"]):
+        k0, k1 = orc.stream_key(*(int(v) for v in key))
+        out = torch.empty(16, dtype=torch.int64, device="cuda")
+        _lib.call("spa_philox_blocks", k0, k1, 0, 4, _p(out), _stream())
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), raw)
+    # far counters agree with the oracle too
+    k = orc.stream_key(3, 1, 77, 12345)
+    out = torch.empty(4 * 64, dtype=torch.int64, device="cuda")
+    _lib.call("spa_philox_blocks", k[0], k[1], 10**9, 64, _p(out), _stream())
+    assert np.array_equal(out.cpu().numpy().view(np.uint64).reshape(64, 4), orc.stream_blocks(k, 10**9, 64))
+
+
+@pytest.mark.parametrize("s", [0.02, 0.1, 0.5])
+def test_loglik_c1_vs_reference(gold_loglik, s):
+    got = gpu_loglik(gold_loglik["c1_X"], gold_loglik["c1_y"], gold_loglik[f"c1_B_{s}"])
+    ref = gold_loglik[f"c1_ll_{s}"]
+    np.testing.assert_allclose(got, ref, rtol=LL_RTOL)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_loglik_large_shapes_vs_reference(gold_loglik, name):
+    from paper_1106_0322_b200.data import named_spec, simulate_dataset
+
+    d, _ = simulate_dataset(named_spec(name))
+    for s in (0.02, 0.1):
+        got = gpu_loglik(d.X, d.y, gold_loglik[f"{name}_B_{s}"])
+        np.testing.assert_allclose(got, gold_loglik[f"{name}_ll_{s}"], rtol=LL_RTOL)
+
+
+def test_loglik_intercept_design(gold_loglik):
+    got = gpu_loglik(gold_loglik["c1_X"], gold_loglik["c1_y"], gold_loglik["c1_Bi"], intercept=True)
+    np.testing.assert_allclose(got, gold_loglik["c1_lli"], rtol=LL_RTOL)
+
+
+def test_loglik_general_design(gold_loglik):
+    """Non-integer (Gaussian) X takes the 3-product split path."""
+    got = gpu_loglik(gold_loglik["g_X"], gold_loglik["g_y"], gold_loglik["g_B"])
+    np.testing.assert_allclose(got, gold_loglik["g_ll"], rtol=LL_RTOL)
+
+
+def test_loglik_many_particles_ragged_vs_oracle(gold_loglik):
+    """Ragged particle count (not a multiple of the 128-row tile), several
+    tiles and work units, against the float64 oracle."""
+    X, y = gold_loglik["c1_X"], gold_loglik["c1_y"]
+    B = np.random.default_rng(7).normal(0, 0.3, size=(1000 + 37, X.shape[1]))
+    np.testing.assert_allclose(gpu_loglik(X, y, B), orc.loglik_rows(X, y, B), rtol=LL_RTOL)
+
+
+def test_loglik_known_answers():
+    # beta = 0 -> n log(1/2) (test_model.py:131-136)
+    rng = np.random.default_rng(0)
+    X = rng.standard_normal((40, 3))
+    y = (rng.random(40) < 0.5).astype(float)
+    got = gpu_loglik(X, y, np.zeros((2, 3)))
+    np.testing.assert_allclose(got, 40 * np.log(0.5), rtol=1e-7)
+
+
+@pytest.mark.parametrize("s", [0.02, 0.5])
+def test_log_prior_rows(gold_loglik, s):
+    X, y, B = gold_loglik["c1_X"], gold_loglik["c1_y"], gold_loglik[f"c1_B_{s}"]
+    d, sysm = system_from(X, y, B)
+    out = torch.empty(sysm.N, dtype=torch.float64, device="cuda")
+    for (a, c) in ((1.0, 2.0), (4.0, 0.3), (0.5, 0.05)):
+        _lib.call("spa_prior_rows", ctypes.byref(d.struct), _p(sysm.beta), sysm.N, sysm.ldb, a, c, c, 0, _p(out),
+                  _stream())
+        # float32 particle storage: compare against the oracle on the stored values
+        Bf = B.astype(np.float32).astype(np.float64)
+        np.testing.assert_allclose(out.cpu().numpy(), orc.log_prior_rows(Bf, a, c), rtol=1e-12)
+        np.testing.assert_allclose(out.cpu().numpy(), gold_loglik[f"c1_lp_{s}_{a}_{c}"], rtol=1e-6)
+
+
+def test_reweight_and_ess(gold_reweight, gold_loglik):
+    from paper_1106_0322_b200 import GtPrior, ess, reweight
+
+    X, y = gold_loglik["c1_X"], gold_loglik["c1_y"]
+    for tag in ("a4", "a1", "a05"):
+        a, c_prev, c_t = (float(v) for v in gold_reweight[f"{tag}_params"])
+        B = gold_reweight[f"{tag}_B"]
+        d, s = system_from(X, y, B, a=a)
+        s.log_weights = gold_reweight[f"{tag}_lw0"]
+        lw, inc = reweight(s, GtPrior(a, c_t), GtPrior(a, c_prev))
+        Bf = B.astype(np.float32).astype(np.float64)
+        lw_ref = orc.reweight_increments(Bf, a, c_t, c_prev)
+        np.testing.assert_allclose(lw, lw_ref, rtol=1e-12, atol=1e-14)
+        np.testing.assert_allclose(lw, gold_reweight[f"{tag}_lw"], rtol=1e-6, atol=1e-7)
+        _, inc_ref = orc.normalise_log_weights(gold_reweight[f"{tag}_lw0"], lw_ref)
+        assert inc == pytest.approx(inc_ref, abs=1e-12)
+        w_ref = orc.weights_from_log(s.log_weights)
+        np.testing.assert_allclose(s.weights, w_ref, rtol=1e-12)
+        assert s.ess() == pytest.approx(orc.ess(w_ref), rel=1e-12)
+        assert ess(gold_reweight[f"{tag}_w"]) == pytest.approx(float(gold_reweight[f"{tag}_ess"]), rel=1e-12)
+
+
+def test_equal_scales_are_neutral(gold_loglik):
+    from paper_1106_0322_b200 import GtPrior, reweight
+
+    d, s = system_from(gold_loglik["c1_X"], gold_loglik["c1_y"], gold_loglik["c1_B_0.1"], a=4.0)
+    before = s.log_weights.copy()
+    lw, inc = reweight(s, GtPrior(4.0, 0.5), GtPrior(4.0, 0.5))
+    assert np.array_equal(lw, np.zeros(s.N))
+    assert inc == pytest.approx(0.0, abs=1e-12)
+    np.testing.assert_allclose(s.log_weights, before, atol=1e-12)
+
+
+def test_degenerate_weights_raise(gold_loglik):
+    from paper_1106_0322_b200 import DegeneracyError, GtPrior, reweight
+
+    d, s = system_from(gold_loglik["c1_X"], gold_loglik["c1_y"], gold_loglik["c1_B_0.1"], a=4.0)
+    s.log_weights = np.full(s.N, -np.inf)
+    with pytest.raises(DegeneracyError):
+        reweight(s, GtPrior(4.0, 0.4), GtPrior(4.0, 0.5))
+    with pytest.raises(ValueError):
+        reweight(s, GtPrior(3.0, 0.4), GtPrior(4.0, 0.5))
+
+
+def test_resample_ancestors_bit_exact(gold_resample):
+    from paper_1106_0322_b200 import systematic_resample_indices
+
+    for k, (N, alpha) in enumerate(gold_resample["cases"]):
+        N = int(N)
+        w = gold_resample[f"w_{k}"] if f"w_{k}" in gold_resample else \
+            np.random.default_rng(1000 + k).dirichlet(np.full(N, alpha))
+        assert sha(w) == str(gold_resample[f"wsha_{k}"])
+        got = systematic_resample_indices(w, float(gold_resample[f"u_{k}"]))
+        assert np.array_equal(got, gold_resample[f"idx_{k}"]), (N, alpha)
+
+
+def test_resample_edge_cases(gold_resample):
+    from paper_1106_0322_b200 import systematic_resample_indices
+
+    for e in range(4):
+        for j in range(3):
+            w, u = gold_resample[f"ew_{e}_{j}"], float(gold_resample[f"eu_{e}_{j}"])
+            assert np.array_equal(systematic_resample_indices(w, u), gold_resample[f"eidx_{e}_{j}"])
+
+
+def test_resample_many_random_trials_bit_exact():
+    """>= 1000 Dirichlet trials, alpha in [0.05, 2], N up to 2^16 (SURVEY 8(c) iii)."""
+    from paper_1106_0322_b200 import systematic_resample_indices
+
+    rng = np.random.default_rng(2024)
+    for trial in range(1000):
+        N = int(rng.choice([7, 100, 1024, 5000, 65536]) if trial % 50 else 65536)
+        alpha = float(rng.uniform(0.05, 2.0))
+        w = rng.dirichlet(np.full(N, alpha))
+        u = rng.random() / N
+        assert np.array_equal(systematic_resample_indices(w, u), orc.systematic_ancestors(w, u)), (trial, N, alpha)
+
+
+def test_resample_large_n_bit_exact():
+    from paper_1106_0322_b200 import systematic_resample_indices
+
+    rng = np.random.default_rng(5)
+    for N in (2**20,):
+        w = rng.dirichlet(np.full(N, 0.5))
+        u = rng.random() / N
+        assert np.array_equal(systematic_resample_indices(w, u), orc.systematic_ancestors(w, u))
+
+
+def test_gather_rows_and_system_resample(gold_loglik):
+    from paper_1106_0322_b200 import systematic_resample
+
+    X, y, B = gold_loglik["c1_X"], gold_loglik["c1_y"], gold_loglik["c1_B_0.5"]
+    d, s = system_from(X, y, B)
+    rng = np.random.default_rng(33)
+    s.log_weights = np.log(rng.dirichlet(np.ones(s.N)))
+    s.ll.copy_(torch.arange(s.N, dtype=torch.float64))
+    original = s.betas.copy()
+    idx = systematic_resample(s, 0.37)
+    np.testing.assert_allclose(s.weights, 1.0 / s.N)
+    np.testing.assert_array_equal(s.betas, original[idx])
+    np.testing.assert_array_equal(s.logliks, idx.astype(float))
