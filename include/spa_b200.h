@@ -143,8 +143,9 @@ int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const d
                    int64_t* partial, void* stream);
 /* Covariance from the fixed-point moments, jitter, float64 Cholesky;
  * L = s*chol(S) as float32 [q][q] row-major lower (s = scale/sqrt(q)) and as
- * the bf16 proposal operand [q][kq] at ws + q*q doubles.
- * ws >= 8*q*q + 2*q*kq bytes; *info = 0 or the failing column + 1. */
+ * the bf16 proposal operand [q][kq] at byte offset roundup(8*q*q, 256) of ws
+ * (kq = roundup(q, 64)); ws >= roundup(8*q*q, 256) + 2*q*kq bytes;
+ * *info = 0 or the failing column + 1. */
 int spa_rw_factor(const int64_t* partial, int32_t q, double scale, double jitter, float* L, double* ws, int* info,
                   void* stream);
 /* prop = beta + L z, z ~ N(0, I) from stream (seed, 3, t, i0+k) blocks
@@ -159,6 +160,13 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
 int spa_rw_accept(float* beta, int32_t ldb, const float* prop, int32_t q, int64_t m, const double* ylin_p,
                   const double* sp_p, const double* lp_p, double* ll, double* lp, uint64_t seed, int64_t t,
                   int64_t i0, int32_t move, unsigned long long* accepted, void* stream);
+
+/* ---- test hook: the raw tcgen05 GEMM engine --------------------------
+ * C[m][ldc] += sum_t A_t B^T for A = [A_0 | A_1] (terms_a bf16 blocks of kp
+ * columns, K-major) and B [rows_b][kp] bf16; float32 C.  Used by the GEMM
+ * unit tests (tests/test_gpu_kernels.py::test_tc_gemm_*). */
+int spa_tc_gemm_f32(const void* A, int64_t m, int32_t terms_a, const void* B, int32_t rows_b, int32_t kp, float* C,
+                    int32_t ldc, void* stream);
 
 #ifdef __cplusplus
 }

@@ -73,19 +73,67 @@ __device__ __forceinline__ float sel_m(uint32_t b1, uint32_t b2, const CoordSlot
 
 template <int S>
 __device__ __forceinline__ void load_bits(const spa_design& d, int j, int tid, uint32_t& p1, uint32_t& p2) {
-  if constexpr (S == 64) {
-    const uint2 a = reinterpret_cast<const uint2*>(d.planes)[(size_t)j * d.n_words + 2 * tid];
-    const uint2 b = reinterpret_cast<const uint2*>(d.planes)[(size_t)j * d.n_words + 2 * tid + 1];
-    p1 = a.x;
-    p2 = a.y;
-    (void)b;
-  } else {
-    const int bit0 = tid * S;
-    const uint2 a = reinterpret_cast<const uint2*>(d.planes)[(size_t)j * d.n_words + (bit0 >> 5)];
-    const int sh = bit0 & 31;
-    p1 = a.x >> sh;
-    p2 = a.y >> sh;
+  static_assert(S == 8 || S == 16 || S == 32, "subjects per thread");
+  const int bit0 = tid * S;
+  const uint2 a = reinterpret_cast<const uint2*>(d.planes)[(size_t)j * d.n_words + (bit0 >> 5)];
+  const int sh = bit0 & 31;
+  p1 = a.x >> sh;
+  p2 = a.y >> sh;
+}
+
+// eta_i = sum_j x_ij beta_j for this thread's S subjects (float32), then
+// l = sum_j beta_j (X^T y)_j - sum_i softplus(eta_i) (block-reduced, float64,
+// identical in every thread); optionally returns sigma_i = logistic(eta_i).
+template <int S>
+__device__ double materialise_ll(const MwgParams& P, const float* bsh, int tid, int nthr, int lane, int wid, int nw,
+                                 double* red, float* sig_out) {
+  const int q = P.d.q;
+  float eta[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) eta[s] = 0.0f;
+  const int sub0 = tid * S;
+  for (int j = 0; j < q; ++j) {
+    const float bj = bsh[j];
+    if (P.d.coded) {
+      const float4 lv = reinterpret_cast<const float4*>(P.d.xlev)[j];
+      const float v0 = lv.x * bj, v1 = lv.y * bj, v2 = lv.z * bj;
+      uint32_t p1, p2;
+      load_bits<S>(P.d, j, tid, p1, p2);
+#pragma unroll
+      for (int s = 0; s < S; ++s) eta[s] += ((p2 >> s) & 1) ? v2 : (((p1 >> s) & 1) ? v1 : v0);
+    } else {
+      const float* xc = P.d.xcols + (size_t)j * P.d.n_words * 32 + sub0;
+#pragma unroll
+      for (int s = 0; s < S; ++s) eta[s] = fmaf(xc[s], bj, eta[s]);
+    }
   }
+  float sp_part = 0.0f;
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const bool valid = (sub0 + s) < P.d.n;
+    if (sig_out) sig_out[s] = valid ? 1.0f / (1.0f + expf(-eta[s])) : 0.0f;
+    if (valid) sp_part += fmaxf(eta[s], 0.0f) + log1pf(expf(-fabsf(eta[s])));
+  }
+  double yl = 0.0;
+  for (int j = tid; j < q; j += nthr) yl += (double)bsh[j] * P.d.sy[j];
+  double v0 = (double)sp_part, v1 = yl;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+  }
+  if (lane == 0) {
+    red[wid] = v0;
+    red[32 + wid] = v1;
+  }
+  __syncthreads();
+  double sp = 0.0, ylt = 0.0;
+  for (int w = 0; w < nw; ++w) {
+    sp += red[w];
+    ylt += red[32 + w];
+  }
+  __syncthreads();
+  return ylt - sp;
 }
 
 template <int S>
@@ -108,75 +156,23 @@ __global__ void __launch_bounds__(512) mwg_kernel(MwgParams P) {
   for (int j = tid; j < q; j += nthr) bsh[j] = brow[j];
   __syncthreads();
 
-  // ---- 1. materialise eta and sigma for this thread's subjects ------------
-  float eta[S];
-#pragma unroll
-  for (int s = 0; s < S; ++s) eta[s] = 0.0f;
-  const int sub0 = tid * S;
-  for (int j = 0; j < q; ++j) {
-    const float bj = bsh[j];
-    if (P.d.coded) {
-      const float4 lv = reinterpret_cast<const float4*>(P.d.xlev)[j];
-      const float v0 = lv.x * bj, v1 = lv.y * bj, v2 = lv.z * bj;
-      if constexpr (S == 64) {
-        const uint2 a = reinterpret_cast<const uint2*>(P.d.planes)[(size_t)j * P.d.n_words + 2 * tid];
-        const uint2 b = reinterpret_cast<const uint2*>(P.d.planes)[(size_t)j * P.d.n_words + 2 * tid + 1];
-#pragma unroll
-        for (int s = 0; s < 32; ++s) {
-          eta[s] += ((a.y >> s) & 1) ? v2 : (((a.x >> s) & 1) ? v1 : v0);
-          eta[s + 32] += ((b.y >> s) & 1) ? v2 : (((b.x >> s) & 1) ? v1 : v0);
-        }
-      } else {
-        uint32_t p1, p2;
-        load_bits<S>(P.d, j, tid, p1, p2);
-#pragma unroll
-        for (int s = 0; s < S; ++s) eta[s] += ((p2 >> s) & 1) ? v2 : (((p1 >> s) & 1) ? v1 : v0);
-      }
-    } else {
-      const float* xc = P.d.xcols + (size_t)j * P.d.n_words * 32 + sub0;
-#pragma unroll
-      for (int s = 0; s < S; ++s) eta[s] = fmaf(xc[s], bj, eta[s]);
-    }
-  }
   float sig[S];
-  float sp_part = 0.0f;
-#pragma unroll
-  for (int s = 0; s < S; ++s) {
-    const bool valid = (sub0 + s) < P.d.n;
-    sig[s] = valid ? 1.0f / (1.0f + __expf(-eta[s])) : 0.0f;
-    if (valid) sp_part += fmaxf(eta[s], 0.0f) + log1pf(__expf(-fabsf(eta[s])));
-  }
-  double yl = 0.0, lp0 = 0.0;
-  for (int j = tid; j < q; j += nthr) {
-    yl += (double)bsh[j] * P.d.sy[j];
-    if (P.d.penalized[j]) lp0 += mwg_gt((double)bsh[j], P);
-  }
-  // block reduction of (sp, yl, lp0)
-  double v3[3] = {(double)sp_part, yl, lp0};
-#pragma unroll
-  for (int r = 0; r < 3; ++r) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v3[r] += __shfl_xor_sync(0xffffffffu, v3[r], o);
-  }
-  if (lane == 0) {
-    red[wid] = v3[0];
-    red[32 + wid] = v3[1];
-  }
-  __syncthreads();
-  double ll = 0.0, ylt = 0.0;
-  for (int w = 0; w < nw; ++w) {
-    ll -= red[w];
-    ylt += red[32 + w];
-  }
-  ll += ylt;
-  __syncthreads();
-  if (lane == 0) red[wid] = v3[2];
-  __syncthreads();
+  double ll = materialise_ll<S>(P, bsh, tid, nthr, lane, wid, nw, red, sig);
   double lp = 0.0;
-  for (int w = 0; w < nw; ++w) lp += red[w];
-  __syncthreads();
+  {
+    double lp0 = 0.0;
+    for (int j = tid; j < q; j += nthr)
+      if (P.d.penalized[j]) lp0 += mwg_gt((double)bsh[j], P);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lp0 += __shfl_xor_sync(0xffffffffu, lp0, o);
+    if (lane == 0) red[wid] = lp0;
+    __syncthreads();
+    for (int w = 0; w < nw; ++w) lp += red[w];
+    __syncthreads();
+  }
 
   unsigned long long acc = 0;
+  const int sub0 = tid * S;
   // ---- 2. sweeps -----------------------------------------------------------
   for (int cyc = 0; cyc < P.cycles; ++cyc) {
     const uint64_t blk0 = (uint64_t)(P.sweep0 + cyc) * (uint64_t)q;
@@ -210,28 +206,32 @@ __global__ void __launch_bounds__(512) mwg_kernel(MwgParams P) {
       float part = 0.0f;
       float mloc[S];
       if (P.d.coded) {
-        if constexpr (S == 64) {
-          const uint2 a = reinterpret_cast<const uint2*>(P.d.planes)[(size_t)j * P.d.n_words + 2 * tid];
-          const uint2 b = reinterpret_cast<const uint2*>(P.d.planes)[(size_t)j * P.d.n_words + 2 * tid + 1];
+        uint32_t p1, p2;
+        load_bits<S>(P.d, j, tid, p1, p2);
 #pragma unroll
-          for (int s = 0; s < 32; ++s) {
-            mloc[s] = sel_m(a.x >> s, a.y >> s, cs);
-            mloc[s + 32] = sel_m(b.x >> s, b.y >> s, cs);
-          }
-        } else {
-          uint32_t p1, p2;
-          load_bits<S>(P.d, j, tid, p1, p2);
-#pragma unroll
-          for (int s = 0; s < S; ++s) mloc[s] = sel_m(p1 >> s, p2 >> s, cs);
-        }
+        for (int s = 0; s < S; ++s) mloc[s] = sel_m(p1 >> s, p2 >> s, cs);
       } else {
         const float* xc = P.d.xcols + (size_t)j * P.d.n_words * 32 + sub0;
         const float df = (float)cs.delta;
 #pragma unroll
         for (int s = 0; s < S; ++s) mloc[s] = expm1f(df * xc[s]);
       }
+      // sum_s log2(1 + m_s sigma_s) as log2 of 8-term products: one MUFU per
+      // 8 subjects and fewer rounding errors; a product outside [1e-30, 1e30]
+      // (extreme proposals only) falls back to per-term logs.
 #pragma unroll
-      for (int s = 0; s < S; ++s) part += fast_lg2(fmaxf(fmaf(mloc[s], sig[s], 1.0f), 1e-37f));
+      for (int c8 = 0; c8 < S / 8; ++c8) {
+        float prod = 1.0f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) prod *= fmaf(mloc[8 * c8 + k], sig[8 * c8 + k], 1.0f);
+        if (prod >= 1e-30f && prod <= 1e30f) {
+          part += fast_lg2(prod);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            part += fast_lg2(fmaxf(fmaf(mloc[8 * c8 + k], sig[8 * c8 + k], 1.0f), 1e-37f));
+        }
+      }
       // block sum (double-buffered scratch: one barrier per coordinate)
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(512) mwg_kernel(MwgParams P) {
 #pragma unroll
         for (int s = 0; s < S; ++s) {
           const float mm = mloc[s];
-          sig[s] = sig[s] * (1.0f + mm) * __frcp_rn(fmaf(mm, sig[s], 1.0f));
+          sig[s] = __fdividef(sig[s] * (1.0f + mm), fmaf(mm, sig[s], 1.0f));
         }
         ll += dll;
         lp += cs.dlp;
@@ -261,7 +261,11 @@ __global__ void __launch_bounds__(512) mwg_kernel(MwgParams P) {
     __syncthreads();
   }
 
+  __syncthreads();
   for (int j = tid; j < q; j += nthr) brow[j] = bsh[j];
+  // rematerialise the final state's log-likelihood from beta (the running
+  // sum of float32 increments only drives the accept decisions)
+  ll = materialise_ll<S>(P, bsh, tid, nthr, lane, wid, nw, red, nullptr);
   if (tid == 0) {
     P.ll[row] = ll;
     if (P.lp) P.lp[row] = lp;

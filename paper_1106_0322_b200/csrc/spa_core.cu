@@ -110,8 +110,9 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // ---------------------------------------------------------------------------
 // Pack particle rows into the K1 A operand [m][2*kp] bf16 = [hi | lo] of the
-// scaled coefficients; coded designs carry the centring offset -o in three
-// bf16 columns q..q+2 of the hi block (the B operand holds 1 there).
+// scaled coefficients; coded designs carry the centring offset
+// o = sum_j gamma_j beta_j in three bf16 columns q..q+2 of the hi block (the
+// B operand holds 1 there), so the MMA yields eta directly.
 __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, int64_t m, int ldb,
                             __nv_bfloat16* __restrict__ A, double* __restrict__ ylin, PriorConst pc,
                             double* __restrict__ lp) {
@@ -146,7 +147,7 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, int64_
     ylin[row] = yl;
     if (lp != nullptr) lp[row] = lps;
     if (d.coded) {
-      const double o = -off;
+      const double o = off;  // eta = sum_j g_ij alpha_j beta_j + sum_j gamma_j beta_j
       const __nv_bfloat16 o1 = __double2bfloat16(o);
       const double r1 = o - (double)__bfloat162float(o1);
       const __nv_bfloat16 o2 = __double2bfloat16(r1);
@@ -779,7 +780,9 @@ int spa_rw_factor(const int64_t* partial, int32_t q, double scale, double jitter
                   void* stream) {
   SPA_REQUIRE(partial && L && ws && q > 0 && q <= 2048, kBadArgument, "spa_rw_factor: bad arguments");
   const int kq = (q + 63) / 64 * 64;
-  __nv_bfloat16* Lb = reinterpret_cast<__nv_bfloat16*>(ws + (size_t)q * q);
+  // bf16 operand after the float64 factor, 256-byte aligned for TMA
+  __nv_bfloat16* Lb =
+      reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<char*>(ws) + (((size_t)8 * q * q + 255) & ~size_t(255)));
   rw_factor_kernel<<<1, 1024, 0, as_stream(stream)>>>(reinterpret_cast<const unsigned long long*>(partial), q, scale,
                                                       jitter, ws, L, Lb, kq, info);
   SPA_CHECK_LAUNCH();
@@ -808,6 +811,23 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
   int rc = launch_tc<1, 1, 256>(Z, (uint64_t)kq, Lb, (uint64_t)kq, (uint64_t)q, args, 1, epi, st);
   if (rc) return rc;
   return spa_pack_particles(d, prop, m, ldb, A, ylin, a, c, lp, stream);
+}
+
+int spa_tc_gemm_f32(const void* A, int64_t m, int32_t terms_a, const void* B, int32_t rows_b, int32_t kp, float* C,
+                    int32_t ldc, void* stream) {
+  SPA_REQUIRE(A && B && C && m > 0 && rows_b > 0 && kp % 64 == 0 && (terms_a == 1 || terms_a == 2), kBadArgument,
+              "spa_tc_gemm_f32: bad arguments");
+  TcArgs args;
+  args.m = (int)m;
+  args.ncols = rows_b;
+  args.kp = kp;
+  args.m_tiles = (int)((m + kTcBM - 1) / kTcBM);
+  args.n_tiles = (rows_b + 255) / 256;
+  args.tiles_per_unit = args.n_tiles;
+  EpiStoreAdd epi{C, C, ldc, (int)m};
+  if (terms_a == 1)
+    return launch_tc<1, 1, 256>(A, (uint64_t)kp, B, (uint64_t)kp, (uint64_t)rows_b, args, 1, epi, as_stream(stream));
+  return launch_tc<2, 1, 256>(A, 2ull * kp, B, (uint64_t)kp, (uint64_t)rows_b, args, 1, epi, as_stream(stream));
 }
 
 int spa_rw_accept(float* beta, int32_t ldb, const float* prop, int32_t q, int64_t m, const double* ylin_p,

@@ -70,6 +70,13 @@ def make_schedule(b1: float, rho: float, T: int) -> Schedule:
     return Schedule(b1, rho, T)
 
 
+def prior_scale(a: float, b: float) -> float:
+    """Prior scale c_t = b_t / a (reference smc.py:410-411).  In the
+    double-exponential limit a = inf the schedule is read as c_t = b_t (the
+    reference would evaluate GtPrior(inf, 0) -> nan)."""
+    return float(b) if math.isinf(a) else float(b) / a
+
+
 @dataclass
 class SmcConfig:
     """Sampler knobs (smc.py:71-103) plus the B200 extensions above."""
@@ -137,7 +144,7 @@ class SmcOutput:
 
     @property
     def c_values(self) -> np.ndarray:
-        return self.schedule.bs / self.a
+        return self.schedule.bs if math.isinf(self.a) else self.schedule.bs / self.a
 
     def step(self, t: int) -> StepRecord:
         return self.steps[t - 1]
@@ -265,14 +272,14 @@ class ParticleSystem:
                 lp_p=torch.empty(self.N, dtype=torch.float64, device=dev),
                 acc=torch.zeros(q + q * q, dtype=torch.int64, device=dev),
                 L=torch.empty((q, q), dtype=torch.float32, device=dev),
-                fws=torch.empty(q * q + (q * kq + 3) // 4, dtype=torch.float64, device=dev),
+                fws=torch.empty((_round_up(8 * q * q, 256) + 2 * q * kq + 7) // 8, dtype=torch.float64, device=dev),
                 info=torch.zeros(1, dtype=torch.int32, device=dev),
             )
         return self._rw
 
     def factor_operand(self):
         rw = self.rw_workspace()
-        return ctypes.c_void_p(rw["fws"].data_ptr() + 8 * self.q * self.q)
+        return ctypes.c_void_p(rw["fws"].data_ptr() + _round_up(8 * self.q * self.q, 256))
 
 
 def _lse(system: ParticleSystem, lw):
@@ -499,8 +506,8 @@ def smc_step(system: ParticleSystem, data, schedule: Schedule, t: int, config: S
         raise ValueError(f"system is at step {system.t}, cannot advance to {t}")
     a = system.prior_a
     bs = schedule.bs
-    prior_prev = GtPrior(a, bs[t - 2] / a)
-    prior_t = GtPrior(a, bs[t - 1] / a)
+    prior_prev = GtPrior(a, prior_scale(a, bs[t - 2]))
+    prior_t = GtPrior(a, prior_scale(a, bs[t - 1]))
     try:
         inc = _reweight_device(system, prior_t, prior_prev, group)
     except DegeneracyError as exc:
@@ -550,7 +557,7 @@ def run_sampler(data, a: float, schedule: Schedule, config: SmcConfig, intercept
     timings = {}
     t0 = time.perf_counter()
     design = DeviceDesign.build(data.X, data.y, intercept)
-    prior1 = GtPrior(a, schedule.bs[0] / a)
+    prior1 = GtPrior(a, prior_scale(a, schedule.bs[0]))
     system, init_acc = init_particles(data, prior1, config, intercept, design=design, group=group)
     torch.cuda.synchronize()
     timings["init_s"] = time.perf_counter() - t0

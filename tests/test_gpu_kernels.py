@@ -103,7 +103,7 @@ def test_loglik_known_answers():
     X = rng.standard_normal((40, 3))
     y = (rng.random(40) < 0.5).astype(float)
     got = gpu_loglik(X, y, np.zeros((2, 3)))
-    np.testing.assert_allclose(got, 40 * np.log(0.5), rtol=1e-7)
+    np.testing.assert_allclose(got, 40 * np.log(0.5), rtol=1e-6)  # MUFU ex2/lg2
 
 
 @pytest.mark.parametrize("s", [0.02, 0.5])
@@ -221,3 +221,30 @@ def test_gather_rows_and_system_resample(gold_loglik):
     np.testing.assert_allclose(s.weights, 1.0 / s.N)
     np.testing.assert_array_equal(s.betas, original[idx])
     np.testing.assert_array_equal(s.logliks, idx.astype(float))
+
+
+def _tc_gemm(A, B, terms=1):
+    m = A.shape[0]
+    rows, kp = B.shape
+    At = torch.from_numpy(np.ascontiguousarray(A, np.float32)).cuda().to(torch.bfloat16).contiguous()
+    Bt = torch.from_numpy(np.ascontiguousarray(B, np.float32)).cuda().to(torch.bfloat16).contiguous()
+    C = torch.zeros((m, rows), dtype=torch.float32, device="cuda")
+    _lib.call("spa_tc_gemm_f32", _p(At), m, terms, _p(Bt), rows, kp, _p(C), rows, _stream())
+    return C.cpu().numpy()
+
+
+@pytest.mark.parametrize("m,rows,kp", [(128, 256, 64), (128, 256, 128), (300, 300, 192), (1, 20, 64)])
+def test_tc_gemm_exact_integers(m, rows, kp):
+    """The raw tcgen05 engine (TMA SW128 -> UMMA -> TMEM -> epilogue) on
+    exactly representable integer inputs: results must be exact."""
+    rng = np.random.default_rng(m + rows + kp)
+    A = np.zeros((m, kp), np.float32)
+    B = np.zeros((rows, kp), np.float32)
+    A[np.arange(m), np.arange(m) % kp] = 1
+    B[np.arange(rows), np.arange(rows) % kp] = 1
+    np.testing.assert_array_equal(_tc_gemm(A, B), A @ B.T)
+    A = rng.integers(-3, 4, (m, kp)).astype(np.float32)
+    B = rng.integers(0, 3, (rows, kp)).astype(np.float32)
+    np.testing.assert_array_equal(_tc_gemm(A, B), A @ B.T)
+    A2 = np.concatenate([A, rng.integers(-3, 4, (m, kp)).astype(np.float32)], 1)
+    np.testing.assert_array_equal(_tc_gemm(A2, B, 2), A2[:, :kp] @ B.T + A2[:, kp:] @ B.T)
