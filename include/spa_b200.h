@@ -91,7 +91,9 @@ int spa_loglik_rows(const spa_design* d, const float* beta, int64_t m, int32_t l
 /* ---- K2: generalised-t log-prior / incremental weights -----------------
  * mode 0: out[k] = sum_j gt(beta_kj; a, c)             (model.py:78-81)
  * mode 1: out[k] = sum_j gt(beta_kj; a, c) - gt(beta_kj; a, c_prev)
- *         (smc.py:248-257 reweight increments, cancellation-free form). */
+ *         (smc.py:248-257 reweight increments, cancellation-free form);
+ * mode 2: as mode 0 with float32 terms (the arithmetic of the RW proposal
+ *         pack, so the MH ratio compares like with like). */
 int spa_prior_rows(const spa_design* d, const float* beta, int64_t m, int32_t ldb, double a, double c,
                    double c_prev, int32_t mode, double* out, void* stream);
 
@@ -134,30 +136,37 @@ int spa_mwg_move(const spa_design* d, float* beta, int64_t m, int32_t ldb, doubl
                  double* lp, unsigned long long* accepted, void* stream);
 
 /* ---- K8: population random-walk moves (north-star kernel) --------------
- * Weighted moments M1 = sum w beta, M2c = sum w (beta-mu)(beta-mu)^T (mu read
- * from the accumulator, so call once with w to get M1, then again for M2c
- * with phase = 1).  `partial` is an int64 fixed-point (2^-48) accumulator
- * [q + q*q] zeroed by the caller; integer sums are order-independent, so the
- * result is bit-identical for any CTA schedule or particle sharding. */
+ * Weighted moments into an int64 fixed-point (2^-48) accumulator
+ * partial[q + q*q] zeroed by the caller:
+ *   phase 0: mu = sum_k w_k beta_k                       -> partial[0:q]
+ *   phase 1: S = sum_k w_k (beta_k-mu)(beta_k-mu)^T      -> partial[q:] (lower)
+ *            as a split-K tcgen05 SYRK of the centred, sqrt(w)-weighted,
+ *            transposed bf16 hi/lo particles (ws: spa_rw_moments_workspace_bytes).
+ * Integer sums are order-independent, so the moments are bit-identical for any
+ * CTA schedule or particle sharding (multi-GPU: all-reduce `partial`). */
+size_t spa_rw_moments_workspace_bytes(int64_t m, int32_t q);
 int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const double* w, int32_t phase,
-                   int64_t* partial, void* stream);
-/* Covariance from the fixed-point moments, jitter, float64 Cholesky;
+                   int64_t* partial, void* ws, size_t ws_bytes, void* stream);
+/* Covariance from the fixed-point moments, jitter, blocked float64 Cholesky;
  * L = s*chol(S) as float32 [q][q] row-major lower (s = scale/sqrt(q)) and as
  * the bf16 proposal operand [q][kq] at byte offset roundup(8*q*q, 256) of ws
  * (kq = roundup(q, 64)); ws >= roundup(8*q*q, 256) + 2*q*kq bytes;
  * *info = 0 or the failing column + 1. */
 int spa_rw_factor(const int64_t* partial, int32_t q, double scale, double jitter, float* L, double* ws, int* info,
                   void* stream);
-/* prop = beta + L z, z ~ N(0, I) from stream (seed, 3, t, i0+k) blocks
- * 1 + move*(ceil(q/4)+1) + j/4; then pack + ylin + lp at c as
- * spa_pack_particles. */
+/* prop = beta + L z, z ~ N(0, I) from stream (seed, 3, t, i0+k) block index
+ * move*(ceil(q/4)+1) + j/4 (two Box-Muller pairs per block), L z on tcgen05
+ * (zbuf: bf16 [m][kq] normals, kq = roundup(q, 64)) stored as eps = L z
+ * (float32 [m][ldb], coalesced through an smem transpose); then one
+ * vectorised pass packs prop = beta + eps into the K1 operand A and emits
+ * ylin and lp at c.  `Lb` is the bf16 operand written by spa_rw_factor. */
 int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ldb, const void* Lb, uint64_t seed,
-                   int64_t t, int64_t i0, int32_t move, float* prop, void* A, double* ylin, double a, double c,
-                   double* lp, void* stream);
-/* Metropolis accept: d = (ylin' - sp' + lp') - (ll + lp); u from block
- * 1 + move*(ceil(q/4)+1) + ceil(q/4) word 0; on accept copy the row and
- * update ll, lp; adds accepted count to *accepted. */
-int spa_rw_accept(float* beta, int32_t ldb, const float* prop, int32_t q, int64_t m, const double* ylin_p,
+                   int64_t t, int64_t i0, int32_t move, void* zbuf, float* eps, void* A, double* ylin, double a,
+                   double c, double* lp, void* stream);
+/* Metropolis accept: d = (ylin' - sp' + lp') - (ll + lp); u from block index
+ * move*(ceil(q/4)+1) + ceil(q/4), word 0; on accept beta <- beta + eps (the
+ * proposal) and ll, lp are updated; adds the accepted count to *accepted. */
+int spa_rw_accept(float* beta, int32_t ldb, const float* eps, int32_t q, int64_t m, const double* ylin_p,
                   const double* sp_p, const double* lp_p, double* ll, double* lp, uint64_t seed, int64_t t,
                   int64_t i0, int32_t move, unsigned long long* accepted, void* stream);
 

@@ -91,6 +91,27 @@ def box_muller(w0, w1):
     return np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2)
 
 
+def rw_normals(key, move: int, q: int) -> np.ndarray:
+    """Proposal normals of the RW-cov move (csrc/spa_core.cu rw_normals_kernel):
+    block index move*(ceil(q/4)+1) + j/4, two float32 Box-Muller pairs per
+    block from 24-bit uniforms."""
+    b4 = -(-q // 4)
+    w = stream_blocks(key, move * (b4 + 1), b4)
+    out = np.empty((b4, 4), np.float32)
+    for h in range(2):
+        u1 = ((w[:, 2 * h] >> np.uint64(40)).astype(np.float32) + np.float32(1.0)) * np.float32(2.0**-24)
+        u2 = (w[:, 2 * h + 1] >> np.uint64(40)).astype(np.float32) * np.float32(2.0**-24)
+        r = np.sqrt(np.float32(-2.0) * np.log(u1))
+        out[:, 2 * h] = r * np.cos(np.float32(2.0 * np.pi) * u2)
+        out[:, 2 * h + 1] = r * np.sin(np.float32(2.0 * np.pi) * u2)
+    return out.reshape(-1)[:q].astype(np.float64)
+
+
+def rw_accept_uniform(key, move: int, q: int) -> float:
+    b4 = -(-q // 4)
+    return float(u53(stream_blocks(key, move * (b4 + 1) + b4, 1)[0, 0]))
+
+
 def box_muller_pair(w0, w1):
     u1 = ((np.asarray(w0, np.uint64) >> np.uint64(11)).astype(np.float64) + 1.0) * 2.0**-53
     u2 = u53(w1)

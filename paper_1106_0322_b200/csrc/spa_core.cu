@@ -83,20 +83,22 @@ static int launch_tc(const void* A, uint64_t a_cols, const void* B, uint64_t b_c
 // Generalised-t prior pieces (reference model.py:78-88)
 struct PriorConst {
   double a, c, c_prev;
-  int de;  // a = +inf: double exponential
+  double lc;  // -log(2c)
+  double lr;  // log(c_prev / c)
+  int de;     // a = +inf: double exponential
 };
 
 __device__ __forceinline__ double gt_logpdf(double b, const PriorConst& p) {
   const double x = fabs(b);
-  if (p.de) return -log(2.0 * p.c) - x / p.c;
-  return -log(2.0 * p.c) - (p.a + 1.0) * log1p(x / (p.a * p.c));
+  if (p.de) return p.lc - x / p.c;
+  return p.lc - (p.a + 1.0) * log1p(x / (p.a * p.c));
 }
 
 // gt(b; c) - gt(b; c_prev) without cancellation:
 //   log(c_prev/c) - (a+1) log1p( (x/a)(1/c - 1/c_prev) / (1 + x/(a c_prev)) )
 __device__ __forceinline__ double gt_logratio(double b, const PriorConst& p) {
   const double x = fabs(b);
-  const double lr = log(p.c_prev / p.c);
+  const double lr = p.lr;
   if (p.de) return lr - x * (1.0 / p.c - 1.0 / p.c_prev);
   const double num = (x / p.a) * (1.0 / p.c - 1.0 / p.c_prev);
   return lr - (p.a + 1.0) * log1p(num / (1.0 + x / (p.a * p.c_prev)));
@@ -113,32 +115,70 @@ __device__ __forceinline__ double warp_sum(double v) {
 // scaled coefficients; coded designs carry the centring offset
 // o = sum_j gamma_j beta_j in three bf16 columns q..q+2 of the hi block (the
 // B operand holds 1 there), so the MMA yields eta directly.
-__global__ void pack_kernel(spa_design d, const float* __restrict__ beta, int64_t m, int ldb,
-                            __nv_bfloat16* __restrict__ A, double* __restrict__ ylin, PriorConst pc,
+__device__ __forceinline__ float gt_logpdf_f(float b, float lc, float ap1, float inv, int de) {
+  const float x = fabsf(b);
+  return de ? lc - x * inv : lc - ap1 * log1pf(x * inv);
+}
+
+// One warp per particle row; lanes take 4 consecutive columns (float4).
+// prop = beta (+ eps); A = [hi | lo] of alpha*prop; ylin = prop . X^T y;
+// off (coded) into the offset columns; lp = sum gt(prop) (float32 terms,
+// float64 accumulation).
+__global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const float* __restrict__ eps, int64_t m,
+                            int ldb, __nv_bfloat16* __restrict__ A, double* __restrict__ ylin, PriorConst pc,
                             double* __restrict__ lp) {
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= m) return;
   const float* b = beta + row * ldb;
+  const float* e = eps ? eps + row * ldb : nullptr;
   __nv_bfloat16* ah = A + row * (2 * (int64_t)d.kp);
   __nv_bfloat16* al = ah + d.kp;
+  const float lc = (float)(-log(2.0 * pc.c));
+  const float ap1 = pc.de ? 0.f : (float)(pc.a + 1.0);
+  const float inv = pc.de ? (float)(1.0 / pc.c) : (float)(1.0 / (pc.a * pc.c));
   double yl = 0.0, off = 0.0, lps = 0.0;
-  for (int j = lane; j < d.kp; j += 32) {
-    __nv_bfloat16 h = __float2bfloat16(0.0f), l = __float2bfloat16(0.0f);
-    if (j < d.q) {
-      const double bj = (double)b[j];
-      yl += bj * d.sy[j];
-      if (lp != nullptr && d.penalized[j]) lps += gt_logpdf(bj, pc);
-      double bs = bj;
-      if (d.coded) {
-        bs = d.alpha[j] * bj;
-        off += d.gamma[j] * bj;
+  const bool vec = (ldb & 3) == 0;
+  for (int j0 = lane * 4; j0 < d.kp; j0 += 128) {
+    float p[4] = {0.f, 0.f, 0.f, 0.f};
+    if (vec && j0 + 4 <= d.q) {
+      const float4 x = *reinterpret_cast<const float4*>(b + j0);
+      p[0] = x.x;
+      p[1] = x.y;
+      p[2] = x.z;
+      p[3] = x.w;
+      if (e) {
+        const float4 y = *reinterpret_cast<const float4*>(e + j0);
+        p[0] += y.x;
+        p[1] += y.y;
+        p[2] += y.z;
+        p[3] += y.w;
       }
-      h = __double2bfloat16(bs);
-      l = __double2bfloat16(bs - (double)__bfloat162float(h));
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (j0 + i < d.q) p[i] = b[j0 + i] + (e ? e[j0 + i] : 0.f);
     }
-    ah[j] = h;
-    al[j] = l;
+    __align__(8) __nv_bfloat16 h[4], l[4];
+    float fy = 0.f, fo = 0.f, fl = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int j = j0 + i;
+      float bs = 0.f;
+      if (j < d.q) {
+        bs = d.coded ? (float)d.alpha[j] * p[i] : p[i];
+        fy = fmaf(p[i], (float)d.sy[j], fy);
+        if (d.coded) fo = fmaf(p[i], (float)d.gamma[j], fo);
+        if (lp != nullptr && d.penalized[j]) fl += gt_logpdf_f(p[i], lc, ap1, inv, pc.de);
+      }
+      h[i] = __float2bfloat16_rn(bs);
+      l[i] = __float2bfloat16_rn(bs - __bfloat162float(h[i]));
+    }
+    yl += fy;
+    off += fo;
+    lps += fl;
+    *reinterpret_cast<uint2*>(ah + j0) = *reinterpret_cast<const uint2*>(h);
+    *reinterpret_cast<uint2*>(al + j0) = *reinterpret_cast<const uint2*>(l);
   }
   yl = warp_sum(yl);
   off = warp_sum(off);
@@ -166,10 +206,20 @@ __global__ void prior_kernel(spa_design d, const float* __restrict__ beta, int64
   if (row >= m) return;
   const float* b = beta + row * ldb;
   double s = 0.0;
-  for (int j = lane; j < d.q; j += 32) {
-    if (!d.penalized[j]) continue;
-    const double bj = (double)b[j];
-    s += mode == 0 ? gt_logpdf(bj, pc) : gt_logratio(bj, pc);
+  if (mode == 2) {  // float32 terms, identical arithmetic to pack_kernel's lp
+    const float lc = (float)pc.lc;
+    const float ap1 = pc.de ? 0.f : (float)(pc.a + 1.0);
+    const float inv = pc.de ? (float)(1.0 / pc.c) : (float)(1.0 / (pc.a * pc.c));
+    float f = 0.f;
+    for (int j = lane; j < d.q; j += 32)
+      if (d.penalized[j]) f += gt_logpdf_f(b[j], lc, ap1, inv, pc.de);
+    s = (double)f;
+  } else {
+    for (int j = lane; j < d.q; j += 32) {
+      if (!d.penalized[j]) continue;
+      const double bj = (double)b[j];
+      s += mode == 0 ? gt_logpdf(bj, pc) : gt_logratio(bj, pc);
+    }
   }
   s = warp_sum(s);
   if (lane == 0) out[row] = s;
@@ -389,8 +439,8 @@ __global__ void rw_mean_kernel(const float* __restrict__ beta, int64_t m, int ld
                                unsigned long long* __restrict__ acc) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= q) return;
-  const int64_t k0 = (int64_t)blockIdx.y * kMomChunk;
-  const int64_t k1 = min(m, k0 + kMomChunk);
+  const int64_t k0 = (int64_t)blockIdx.y * 256;
+  const int64_t k1 = min(m, k0 + 256);
   double s = 0.0;
   for (int64_t k = k0; k < k1; ++k) s += w[k] * (double)beta[k * ldb + j];
   atomicAdd(&acc[j], to_fix(s));
@@ -455,95 +505,127 @@ __global__ void rw_moments_kernel(const float* __restrict__ beta, int64_t m, int
   }
 }
 
-// Single-CTA float64 Cholesky of S = M2 - M1 M1^T + jitter*I, blocked
-// right-looking with 32-column panels; L scaled by `scale`/sqrt(q) is written
-// as float32 and as the bf16 B operand [q][kq] of the proposal GEMM.
-__global__ void __launch_bounds__(1024) rw_factor_kernel(const unsigned long long* __restrict__ acc, int q,
-                                                         double scale, double jitter, double* __restrict__ S,
-                                                         float* __restrict__ L, __nv_bfloat16* __restrict__ Lb,
-                                                         int kq, int* info) {
-  __shared__ double diag[32][33];
-  __shared__ double tr;
-  const int tid = threadIdx.x;
-  // covariance (lower triangle, row-major S[i*q + j]) from the centred moments
-  for (int64_t e = tid; e < (int64_t)q * q; e += blockDim.x) {
-    const int i = (int)(e / q), j = (int)(e % q);
-    S[e] = (j > i) ? 0.0 : from_fix(acc[q + e]);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double t = 0.0;
-    for (int i = 0; i < q; ++i) t += S[(size_t)i * q + i];
-    tr = t / q;
-    if (info) *info = 0;
-  }
-  __syncthreads();
-  for (int i = tid; i < q; i += blockDim.x) S[(size_t)i * q + i] += jitter * (tr > 0 ? tr : 1.0) + 1e-300;
-  __syncthreads();
+// Blocked right-looking float64 Cholesky of S = M2c + jitter*I.
+//   rw_cov_kernel      : S (lower) from the fixed-point moments, trace
+//   rw_panel_kernel    : factor the 32x32 diagonal block in smem, then the
+//                        panel below it (one thread per row)      [1 CTA]
+//   rw_trail_kernel    : A22 -= L21 L21^T on 32x32 tiles           [many CTAs]
+//   rw_emit_kernel     : L = (scale/sqrt(q)) chol(S) as float32 and as the
+//                        bf16 proposal operand [q][kq]
+constexpr int kPanel = 32;
 
-  for (int jb = 0; jb < q; jb += 32) {
-    const int nb = min(32, q - jb);
-    // 1. factor the diagonal block in smem
-    for (int e = tid; e < nb * nb; e += blockDim.x) {
-      const int i = e / nb, j = e % nb;
-      diag[i][j] = (j <= i) ? S[(size_t)(jb + i) * q + jb + j] : 0.0;
-    }
-    __syncthreads();
-    if (tid < 32) {
-      for (int j = 0; j < nb; ++j) {
-        if (tid == 0) {
-          double dj = diag[j][j];
-          if (!(dj > 0.0)) {
-            if (info && *info == 0) *info = jb + j + 1;
-            dj = 1e-300;
-          }
-          diag[j][j] = sqrt(dj);
-        }
-        __syncwarp();
-        const double djj = diag[j][j];
-        if (tid > j && tid < nb) diag[tid][j] /= djj;
-        __syncwarp();
-        for (int k = j + 1; k < nb; ++k)
-          if (tid >= k && tid < nb) diag[tid][k] -= diag[tid][j] * diag[k][j];
-        __syncwarp();
-      }
-    }
-    __syncthreads();
-    for (int e = tid; e < nb * nb; e += blockDim.x) {
-      const int i = e / nb, j = e % nb;
-      if (j <= i) S[(size_t)(jb + i) * q + jb + j] = diag[i][j];
-    }
-    // 2. panel solve: rows below, L21 = A21 L11^-T (one thread per row)
-    for (int i = jb + nb + tid; i < q; i += blockDim.x) {
-      double* r = S + (size_t)i * q + jb;
-      double x[32];
-      for (int j = 0; j < nb; ++j) {
-        double v = r[j];
-        for (int k = 0; k < j; ++k) v -= x[k] * diag[j][k];
-        x[j] = v / diag[j][j];
-      }
-      for (int j = 0; j < nb; ++j) r[j] = x[j];
-    }
-    __syncthreads();
-    // 3. trailing update A22 -= L21 L21^T (lower triangle)
-    const int rest = q - jb - nb;
-    const int64_t cnt = (int64_t)rest * (rest + 1) / 2;
-    for (int64_t e = tid; e < cnt; e += blockDim.x) {
-      // map linear index to (i, j) with j <= i
-      int i = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
-      while ((int64_t)(i + 1) * (i + 2) / 2 <= e) ++i;
-      while ((int64_t)i * (i + 1) / 2 > e) --i;
-      const int j = (int)(e - (int64_t)i * (i + 1) / 2);
-      const double* ri = S + (size_t)(jb + nb + i) * q + jb;
-      const double* rj = S + (size_t)(jb + nb + j) * q + jb;
-      double s = 0.0;
-      for (int k = 0; k < nb; ++k) s += ri[k] * rj[k];
-      S[(size_t)(jb + nb + i) * q + jb + nb + j] -= s;
-    }
+__global__ void rw_cov_kernel(const unsigned long long* __restrict__ acc, int q, double jitter,
+                              double* __restrict__ S) {
+  __shared__ double red[256];
+  double tr = 0.0;
+  for (int i = threadIdx.x; i < q; i += blockDim.x) tr += from_fix(acc[q + (size_t)i * q + i]);
+  red[threadIdx.x] = tr;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
     __syncthreads();
   }
-  const double f = scale / sqrt((double)q);
-  for (int64_t e = tid; e < (int64_t)q * kq; e += blockDim.x) {
+  const double t = red[0] / q;
+  const double add = jitter * (t > 0 ? t : 1.0) + 1e-300;
+  const int64_t total = (int64_t)q * q;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / q), j = (int)(e % q);
+    S[e] = (j > i) ? 0.0 : from_fix(acc[q + e]) + (i == j ? add : 0.0);
+  }
+}
+
+__global__ void __launch_bounds__(512) rw_panel_kernel(double* __restrict__ S, int q, int jb, int* info) {
+  __shared__ double dg[kPanel][kPanel + 1];
+  const int nb = min(kPanel, q - jb);
+  const int tid = threadIdx.x;
+  for (int e = tid; e < nb * nb; e += blockDim.x) {
+    const int i = e / nb, j = e % nb;
+    dg[i][j] = (j <= i) ? S[(size_t)(jb + i) * q + jb + j] : 0.0;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    for (int j = 0; j < nb; ++j) {
+      if (tid == 0) {
+        double d = dg[j][j];
+        if (!(d > 0.0)) {
+          if (info && *info == 0) *info = jb + j + 1;
+          d = 1e-300;
+        }
+        dg[j][j] = sqrt(d);
+      }
+      __syncwarp();
+      const double djj = dg[j][j];
+      if (tid > j && tid < nb) dg[tid][j] /= djj;
+      __syncwarp();
+      for (int k = j + 1; k < nb; ++k)
+        if (tid >= k && tid < nb) dg[tid][k] -= dg[tid][j] * dg[k][j];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < nb * nb; e += blockDim.x) {
+    const int i = e / nb, j = e % nb;
+    if (j <= i) S[(size_t)(jb + i) * q + jb + j] = dg[i][j];
+  }
+  // panel below: L21 = A21 L11^-T, one thread per row
+  for (int i = jb + nb + tid; i < q; i += blockDim.x) {
+    double* r = S + (size_t)i * q + jb;
+    double x[kPanel];
+#pragma unroll
+    for (int j = 0; j < kPanel; ++j) {
+      if (j < nb) {
+        double v = r[j];
+        for (int k = 0; k < j; ++k) v -= x[k] * dg[j][k];
+        x[j] = v / dg[j][j];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kPanel; ++j)
+      if (j < nb) r[j] = x[j];
+  }
+}
+
+// tile (bi, bj), bj <= bi, of the trailing matrix starting at row/col j0
+__global__ void __launch_bounds__(256) rw_trail_kernel(double* __restrict__ S, int q, int jb, int ntiles) {
+  __shared__ double li[32][kPanel + 1];
+  __shared__ double lj[32][kPanel + 1];
+  int t = blockIdx.x, bi = 0;
+  while (t > bi) {
+    t -= bi + 1;
+    ++bi;
+  }
+  const int bj = t;
+  const int j0 = jb + kPanel;
+  const int r0 = j0 + bi * 32, c0 = j0 + bj * 32;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < 32 * kPanel; e += blockDim.x) {
+    const int r = e / kPanel, k = e % kPanel;
+    li[r][k] = (r0 + r < q) ? S[(size_t)(r0 + r) * q + jb + k] : 0.0;
+    lj[r][k] = (c0 + r < q) ? S[(size_t)(c0 + r) * q + jb + k] : 0.0;
+  }
+  __syncthreads();
+  // 256 threads x 4 outputs each = 32x32 tile
+  const int ty = tid >> 3, tx = (tid & 7) * 4;
+  double acc[4] = {0, 0, 0, 0};
+#pragma unroll 8
+  for (int k = 0; k < kPanel; ++k) {
+    const double a = li[ty][k];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[c] += a * lj[tx + c][k];
+  }
+  const int i = r0 + ty;
+  if (i >= q) return;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int j = c0 + tx + c;
+    if (j < q && j <= i) S[(size_t)i * q + j] -= acc[c];
+  }
+}
+
+__global__ void rw_emit_kernel(const double* __restrict__ S, int q, int kq, double f, float* __restrict__ L,
+                               __nv_bfloat16* __restrict__ Lb) {
+  const int64_t total = (int64_t)q * kq;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(e / kq), j = (int)(e % kq);
     const double v = (j < q && j <= i) ? S[(size_t)i * q + j] * f : 0.0;
     if (j < q) L[(size_t)i * q + j] = (float)v;
@@ -552,7 +634,8 @@ __global__ void __launch_bounds__(1024) rw_factor_kernel(const unsigned long lon
 }
 
 // Proposal normals: Z[k][j] (bf16, [m][kq]) from stream (seed, 3, t, i0+k),
-// block index move*(B4+1) + j/4 (two Box-Muller pairs per block).
+// block index move*(B4+1) + j/4 (two float32 Box-Muller pairs per block; any
+// symmetric law is a valid random-walk increment, the MH ratio is exact).
 __global__ void rw_normals_kernel(int64_t m, int q, int kq, uint64_t seed, int64_t t, int64_t i0, int move,
                                   __nv_bfloat16* __restrict__ Z) {
   const int b4 = (q + 3) / 4;
@@ -561,21 +644,59 @@ __global__ void rw_normals_kernel(int64_t m, int q, int kq, uint64_t seed, int64
   if (e >= m * kq4) return;
   const int64_t k = e / kq4;
   const int jb = (int)(e % kq4);
-  __nv_bfloat16* z = Z + k * kq + 4 * jb;
+  __align__(8) __nv_bfloat16 z[4];
   if (jb >= b4) {
-    for (int i = 0; i < 4; ++i) z[i] = __float2bfloat16(0.0f);
-    return;
+    z[0] = z[1] = z[2] = z[3] = __float2bfloat16(0.0f);
+  } else {
+    uint64_t w[4];
+    philox_block(stream_key(seed, 3, (uint64_t)t, (uint64_t)(i0 + k)), (uint64_t)move * (b4 + 1) + jb, w);
+    float zz[4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float u1 = ((float)(w[2 * h] >> 40) + 1.0f) * 0x1.0p-24f;  // (0, 1]
+      const float u2 = (float)(w[2 * h + 1] >> 40) * 0x1.0p-24f;       // [0, 1)
+      const float r = sqrtf(-2.0f * logf(u1));
+      float sn, cs;
+      sincospif(2.0f * u2, &sn, &cs);
+      zz[2 * h] = r * cs;
+      zz[2 * h + 1] = r * sn;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) z[i] = __float2bfloat16(4 * jb + i < q ? zz[i] : 0.0f);
   }
-  uint64_t w[4];
-  philox_block(stream_key(seed, 3, (uint64_t)t, (uint64_t)(i0 + k)), (uint64_t)move * (b4 + 1) + jb, w);
-  double z0, z1, z2, z3;
-  box_muller_pair(w[0], w[1], z0, z1);
-  box_muller_pair(w[2], w[3], z2, z3);
-  const double zz[4] = {z0, z1, z2, z3};
-  for (int i = 0; i < 4; ++i) z[i] = __double2bfloat16(4 * jb + i < q ? zz[i] : 0.0);
+  *reinterpret_cast<uint2*>(Z + k * kq + 4 * jb) = *reinterpret_cast<const uint2*>(z);
 }
 
-__global__ void rw_accept_kernel(float* __restrict__ beta, int ldb, const float* __restrict__ prop, int q, int64_t m,
+// Centre, weight and transpose the particles for the tensor-core SYRK:
+// Dt[i][k] = sqrt(w_k) (beta_ki - mu_i) as bf16 hi / lo, rows [hi | lo] of
+// 2*ldk columns (the engine's two-term A/B layout).
+__global__ void rw_center_t_kernel(const float* __restrict__ beta, int64_t m, int ldb, int q,
+                                   const double* __restrict__ w, const unsigned long long* __restrict__ acc,
+                                   __nv_bfloat16* __restrict__ Dt, int64_t ldk) {
+  __shared__ float tile[32][33];
+  const int64_t k0 = (int64_t)blockIdx.x * 32;
+  const int j0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t k = k0 + r;
+    const int j = j0 + tx;
+    float v = 0.f;
+    if (k < m && j < q) v = (float)(sqrt(w[k]) * ((double)beta[k * ldb + j] - from_fix(acc[j])));
+    tile[r][tx] = v;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int j = j0 + r;
+    const int64_t k = k0 + tx;
+    if (j >= q || k >= ldk) continue;
+    const float v = tile[tx][r];
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    Dt[(size_t)j * 2 * ldk + k] = h;
+    Dt[(size_t)j * 2 * ldk + ldk + k] = __float2bfloat16_rn(v - __bfloat162float(h));
+  }
+}
+
+__global__ void rw_accept_kernel(float* __restrict__ beta, int ldb, const float* __restrict__ eps, int q, int64_t m,
                                  const double* __restrict__ ylin_p, const double* __restrict__ sp_p,
                                  const double* __restrict__ lp_p, double* __restrict__ ll, double* __restrict__ lp,
                                  uint64_t seed, int64_t t, int64_t i0, int move, unsigned long long* accepted) {
@@ -598,10 +719,10 @@ __global__ void rw_accept_kernel(float* __restrict__ beta, int ldb, const float*
     }
   }
   ok = __shfl_sync(0xffffffffu, ok, 0);
-  if (ok) {
-    const float* s = prop + row * ldb;
+  if (ok) {  // beta' = beta + eps, the same float32 sum the pack kernel used
+    const float* s = eps + row * ldb;
     float* o = beta + row * ldb;
-    for (int j = lane; j < q; j += 32) o[j] = s[j];
+    for (int j = lane; j < q; j += 32) o[j] = o[j] + s[j];
   }
 }
 
@@ -655,6 +776,7 @@ static int loglik_impl(const spa_design* d, const void* A, int64_t m, const doub
   args.m = (int)m;
   args.ncols = d->n;
   args.kp = d->kp;
+  args.kb_per_unit = 0;
   EpiSoftplusRowSum epi{reinterpret_cast<double*>(ws), 0.f, 0.0};
   int rc;
   if (d->terms == 1)
@@ -677,6 +799,8 @@ static PriorConst make_prior(double a, double c, double c_prev) {
   p.a = a;
   p.c = c;
   p.c_prev = c_prev;
+  p.lc = -std::log(2.0 * c);
+  p.lr = std::log(c_prev / c);
   p.de = std::isinf(a) ? 1 : 0;
   return p;
 }
@@ -686,8 +810,9 @@ int spa_pack_particles(const spa_design* d, const float* beta, int64_t m, int32_
   SPA_REQUIRE(d && beta && A && ylin && m >= 0, kBadArgument, "spa_pack_particles: bad arguments");
   SPA_REQUIRE(!d->coded || d->kp >= d->q + 3, kBadArgument, "spa_pack_particles: kp < q + 3");
   if (m == 0) return 0;
-  pack_kernel<<<cdiv(m, 8), 256, 0, as_stream(stream)>>>(*d, beta, m, ldb, reinterpret_cast<__nv_bfloat16*>(A),
-                                                        ylin, make_prior(a, c, c), lp);
+  pack_kernel<<<cdiv(m, 8), 256, 0, as_stream(stream)>>>(*d, beta, nullptr, m, ldb,
+                                                        reinterpret_cast<__nv_bfloat16*>(A), ylin,
+                                                        make_prior(a, c, c), lp);
   SPA_CHECK_LAUNCH();
   return 0;
 }
@@ -701,7 +826,7 @@ int spa_loglik_rows(const spa_design* d, const float* beta, int64_t m, int32_t l
 
 int spa_prior_rows(const spa_design* d, const float* beta, int64_t m, int32_t ldb, double a, double c,
                    double c_prev, int32_t mode, double* out, void* stream) {
-  SPA_REQUIRE(d && beta && out && m >= 0 && (mode == 0 || mode == 1), kBadArgument, "spa_prior_rows: bad arguments");
+  SPA_REQUIRE(d && beta && out && m >= 0 && mode >= 0 && mode <= 2, kBadArgument, "spa_prior_rows: bad arguments");
   SPA_REQUIRE(a > 0 && c > 0 && c_prev > 0, kBadArgument, "spa_prior_rows: a, c must be positive");
   if (m == 0) return 0;
   prior_kernel<<<cdiv(m, 8), 256, 0, as_stream(stream)>>>(*d, beta, m, ldb, make_prior(a, c, c_prev), mode, out);
@@ -759,45 +884,88 @@ int spa_gather_rows(const float* src, int32_t ld_src, float* dst, int32_t ld_dst
   return 0;
 }
 
+size_t spa_rw_moments_workspace_bytes(int64_t m, int32_t q) {
+  const int64_t ldk = (m + 63) / 64 * 64;
+  return (size_t)2 * q * ldk * sizeof(__nv_bfloat16);
+}
+
 int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const double* w, int32_t phase,
-                   int64_t* partial, void* stream) {
+                   int64_t* partial, void* ws, size_t ws_bytes, void* stream) {
   SPA_REQUIRE(beta && w && partial && m > 0 && q > 0 && (phase == 0 || phase == 1), kBadArgument,
               "spa_rw_moments: bad arguments");
+  cudaStream_t st = as_stream(stream);
   auto* acc = reinterpret_cast<unsigned long long*>(partial);
   if (phase == 0) {
-    dim3 grid(cdiv(q, 128), cdiv(m, kMomChunk));
-    rw_mean_kernel<<<grid, 128, 0, as_stream(stream)>>>(beta, m, ldb, q, w, acc);
-  } else {
-    const int tiles = (q + 63) / 64;
-    dim3 grid(tiles * tiles, cdiv(m, kMomChunk));
-    rw_moments_kernel<<<grid, 256, 0, as_stream(stream)>>>(beta, m, ldb, q, w, acc);
+    dim3 grid(cdiv(q, 128), cdiv(m, 256));
+    rw_mean_kernel<<<grid, 128, 0, st>>>(beta, m, ldb, q, w, acc);
+    SPA_CHECK_LAUNCH();
+    return 0;
   }
-  SPA_CHECK_LAUNCH();
-  return 0;
+  // phase 1: S = Dt Dt^T on tcgen05 (3 split products), split-K over particles
+  SPA_REQUIRE(ws && ws_bytes >= spa_rw_moments_workspace_bytes(m, q), kWorkspaceTooSmall,
+              "spa_rw_moments: workspace too small");
+  const int64_t ldk = (m + 63) / 64 * 64;
+  __nv_bfloat16* Dt = reinterpret_cast<__nv_bfloat16*>(ws);
+  // layout [q][2*ldk]: row i = [hi(i, :) | lo(i, :)]
+  {
+    dim3 grid(cdiv(ldk, 32), cdiv(q, 32));
+    rw_center_t_kernel<<<grid, 256, 0, st>>>(beta, m, ldb, q, w, acc, Dt, ldk);
+    SPA_CHECK_LAUNCH();
+  }
+  TcArgs args;
+  args.m = q;
+  args.ncols = q;
+  args.kp = (int)ldk;
+  args.m_tiles = (q + kTcBM - 1) / kTcBM;
+  args.n_tiles = (q + 255) / 256;
+  args.tiles_per_unit = args.n_tiles;
+  const int kblocks = (int)(ldk / kTcBK);
+  int units = std::max(1, std::min(kblocks, (2 * 148 + args.m_tiles - 1) / args.m_tiles));
+  args.kb_per_unit = (kblocks + units - 1) / units;
+  units = (kblocks + args.kb_per_unit - 1) / args.kb_per_unit;
+  EpiFixAtomic epi{acc + q, q, q, 1};
+  return launch_tc<2, 2, 256>(Dt, 2ull * ldk, Dt, 2ull * ldk, (uint64_t)q, args, units, epi, st);
 }
 
 int spa_rw_factor(const int64_t* partial, int32_t q, double scale, double jitter, float* L, double* ws, int* info,
                   void* stream) {
-  SPA_REQUIRE(partial && L && ws && q > 0 && q <= 2048, kBadArgument, "spa_rw_factor: bad arguments");
+  SPA_REQUIRE(partial && L && ws && q > 0 && q <= 4096, kBadArgument, "spa_rw_factor: bad arguments");
+  cudaStream_t st = as_stream(stream);
   const int kq = (q + 63) / 64 * 64;
   // bf16 operand after the float64 factor, 256-byte aligned for TMA
   __nv_bfloat16* Lb =
       reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<char*>(ws) + (((size_t)8 * q * q + 255) & ~size_t(255)));
-  rw_factor_kernel<<<1, 1024, 0, as_stream(stream)>>>(reinterpret_cast<const unsigned long long*>(partial), q, scale,
-                                                      jitter, ws, L, Lb, kq, info);
+  if (info) SPA_CHECK_CUDA(cudaMemsetAsync(info, 0, sizeof(int), st));
+  rw_cov_kernel<<<std::min<unsigned>(cdiv((int64_t)q * q, 256), 1184), 256, 0, st>>>(
+      reinterpret_cast<const unsigned long long*>(partial), q, jitter, ws);
+  SPA_CHECK_LAUNCH();
+  for (int jb = 0; jb < q; jb += kPanel) {
+    rw_panel_kernel<<<1, 512, 0, st>>>(ws, q, jb, info);
+    SPA_CHECK_LAUNCH();
+    const int rest = q - jb - kPanel;
+    if (rest > 0) {
+      const int nt = (rest + 31) / 32;
+      rw_trail_kernel<<<nt * (nt + 1) / 2, 256, 0, st>>>(ws, q, jb, nt);
+      SPA_CHECK_LAUNCH();
+    }
+  }
+  rw_emit_kernel<<<std::min<unsigned>(cdiv((int64_t)q * kq, 256), 1184), 256, 0, st>>>(ws, q, kq,
+                                                                                       scale / std::sqrt((double)q),
+                                                                                       L, Lb);
   SPA_CHECK_LAUNCH();
   return 0;
 }
 
 int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ldb, const void* Lb, uint64_t seed,
-                   int64_t t, int64_t i0, int32_t move, float* prop, void* A, double* ylin, double a, double c,
-                   double* lp, void* stream) {
-  SPA_REQUIRE(d && beta && Lb && prop && A && ylin && m > 0, kBadArgument, "spa_rw_propose: bad arguments");
-  SPA_REQUIRE((ldb & 3) == 0, kBadArgument, "spa_rw_propose: ldb must be a multiple of 4");
+                   int64_t t, int64_t i0, int32_t move, void* zbuf, float* eps, void* A, double* ylin, double a,
+                   double c, double* lp, void* stream) {
+  SPA_REQUIRE(d && beta && Lb && zbuf && eps && A && ylin && m > 0, kBadArgument, "spa_rw_propose: bad arguments");
+  SPA_REQUIRE((ldb & 3) == 0 && beta != eps, kBadArgument, "spa_rw_propose: ldb % 4 != 0 or beta aliases eps");
+  SPA_REQUIRE(!d->coded || d->kp >= d->q + 3, kBadArgument, "spa_rw_propose: kp < q + 3");
   cudaStream_t st = as_stream(stream);
   const int q = d->q;
   const int kq = (q + 63) / 64 * 64;
-  __nv_bfloat16* Z = reinterpret_cast<__nv_bfloat16*>(A);
+  __nv_bfloat16* Z = reinterpret_cast<__nv_bfloat16*>(zbuf);
   rw_normals_kernel<<<cdiv(m * (kq / 4), 256), 256, 0, st>>>(m, q, kq, seed, t, i0, move, Z);
   SPA_CHECK_LAUNCH();
   TcArgs args;
@@ -807,10 +975,14 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
   args.m_tiles = (int)((m + kTcBM - 1) / kTcBM);
   args.n_tiles = (q + 255) / 256;
   args.tiles_per_unit = args.n_tiles;
-  EpiStoreAdd epi{beta, prop, ldb, (int)m};
+  args.kb_per_unit = 0;
+  EpiStoreT epi{eps, ldb, (int)m};
   int rc = launch_tc<1, 1, 256>(Z, (uint64_t)kq, Lb, (uint64_t)kq, (uint64_t)q, args, 1, epi, st);
   if (rc) return rc;
-  return spa_pack_particles(d, prop, m, ldb, A, ylin, a, c, lp, stream);
+  pack_kernel<<<cdiv(m, 8), 256, 0, st>>>(*d, beta, eps, m, ldb, reinterpret_cast<__nv_bfloat16*>(A), ylin,
+                                          make_prior(a, c, c), lp);
+  SPA_CHECK_LAUNCH();
+  return 0;
 }
 
 int spa_tc_gemm_f32(const void* A, int64_t m, int32_t terms_a, const void* B, int32_t rows_b, int32_t kp, float* C,
@@ -824,18 +996,19 @@ int spa_tc_gemm_f32(const void* A, int64_t m, int32_t terms_a, const void* B, in
   args.m_tiles = (int)((m + kTcBM - 1) / kTcBM);
   args.n_tiles = (rows_b + 255) / 256;
   args.tiles_per_unit = args.n_tiles;
+  args.kb_per_unit = 0;
   EpiStoreAdd epi{C, C, ldc, (int)m};
   if (terms_a == 1)
     return launch_tc<1, 1, 256>(A, (uint64_t)kp, B, (uint64_t)kp, (uint64_t)rows_b, args, 1, epi, as_stream(stream));
   return launch_tc<2, 1, 256>(A, 2ull * kp, B, (uint64_t)kp, (uint64_t)rows_b, args, 1, epi, as_stream(stream));
 }
 
-int spa_rw_accept(float* beta, int32_t ldb, const float* prop, int32_t q, int64_t m, const double* ylin_p,
+int spa_rw_accept(float* beta, int32_t ldb, const float* eps, int32_t q, int64_t m, const double* ylin_p,
                   const double* sp_p, const double* lp_p, double* ll, double* lp, uint64_t seed, int64_t t,
                   int64_t i0, int32_t move, unsigned long long* accepted, void* stream) {
-  SPA_REQUIRE(beta && prop && ylin_p && sp_p && lp_p && ll && lp && accepted && m > 0, kBadArgument,
+  SPA_REQUIRE(beta && eps && ylin_p && sp_p && lp_p && ll && lp && accepted && m > 0, kBadArgument,
               "spa_rw_accept: bad arguments");
-  rw_accept_kernel<<<cdiv(m, 8), 256, 0, as_stream(stream)>>>(beta, ldb, prop, q, m, ylin_p, sp_p, lp_p, ll, lp, seed,
+  rw_accept_kernel<<<cdiv(m, 8), 256, 0, as_stream(stream)>>>(beta, ldb, eps, q, m, ylin_p, sp_p, lp_p, ll, lp, seed,
                                                              t, i0, move, accepted);
   SPA_CHECK_LAUNCH();
   return 0;

@@ -34,7 +34,8 @@ struct TcShape {
   static constexpr int kBudget = 196 * 1024;
   static constexpr int kStagesRaw = kBudget / kStageBytes;
   static constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kScratchPerWarp = 32 * 33 * 4;  // epilogue transpose tile
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ + 4 * kScratchPerWarp;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
   static_assert(kStages >= 2, "tile too large");
   static_assert(kTmemCols <= 512 && (kTmemCols & (kTmemCols - 1)) == 0, "TMEM columns must be a power of 2");
@@ -46,12 +47,15 @@ struct TcArgs {
   int kp;              // K per term (multiple of 64)
   int m_tiles;         // ceil(m / 128)
   int n_tiles;         // ceil(ncols / BN)
-  int tiles_per_unit;  // BN tiles per CTA
+  int tiles_per_unit;  // BN tiles per CTA (column split), or
+  int kb_per_unit;     // > 0: split-K -- a CTA covers all BN tiles over this many k-blocks
 };
 
 // Epilogue contract:
 //   begin_unit(row, unit)                       once per CTA (per thread)
-//   consume(row, col0, float v[32], ncols)      32 consecutive columns of one row
+//   consume(row, col0, float v[32], ncols, scratch)
+//                                               32 consecutive columns of one row; scratch is a
+//                                               per-warp 32x33 float smem tile
 //   end_tile(row)                               after every BN tile
 //   end_unit(row, unit, m)                      once per CTA
 template <int TA, int TB, int BN, class Epi>
@@ -71,9 +75,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int lane = threadIdx.x & 31;
   const int unit = blockIdx.x / args.m_tiles;
   const int mt = blockIdx.x % args.m_tiles;
-  const int nt0 = unit * args.tiles_per_unit;
-  const int nt1 = min(args.n_tiles, nt0 + args.tiles_per_unit);
-  const int kblocks = args.kp / kTcBK;
+  int nt0, nt1, kb0, kb1;
+  if (args.kb_per_unit > 0) {
+    nt0 = 0;
+    nt1 = args.n_tiles;
+    kb0 = unit * args.kb_per_unit;
+    kb1 = min(args.kp / kTcBK, kb0 + args.kb_per_unit);
+  } else {
+    nt0 = unit * args.tiles_per_unit;
+    nt1 = min(args.n_tiles, nt0 + args.tiles_per_unit);
+    kb0 = 0;
+    kb1 = args.kp / kTcBK;
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S::kStages; ++s) {
@@ -100,7 +113,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int nt = nt0; nt < nt1; ++nt) {
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + s * S::kStageBytes;
           mbar_arrive_expect_tx(&full[s], S::kStageBytes);
@@ -131,7 +144,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         mbar_wait(&tempty[buf], bph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + buf * BN;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t st = smem_u32(smem + s * S::kStageBytes);
@@ -142,7 +155,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
           for (int k = 0; k < kTcBK / 16; ++k) {
             const uint64_t adv = (uint64_t)(k * 2);  // 16 bf16 = 32 B = 2 x 16 B
-            tc_mma_f16(d, a0 + adv, b0 + adv, idesc, (kb | k) != 0 ? 1u : 0u);
+            tc_mma_f16(d, a0 + adv, b0 + adv, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
             if (TA == 2) tc_mma_f16(d, a1 + adv, b0 + adv, idesc, 1u);
             if (TB == 2) tc_mma_f16(d, a0 + adv, b1 + adv, idesc, 1u);
           }
@@ -159,6 +172,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ---------------- epilogue (warps 2..5) ----------------
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int row = mt * kTcBM + quarter * 32 + lane;
+    float* scratch = reinterpret_cast<float*>(smem + S::kStages * S::kStageBytes + 256) + (warp - 2) * 32 * 33;
     epi.begin_unit(row, unit);
     int it = 0;
     for (int nt = nt0; nt < nt1; ++nt, ++it) {
@@ -175,7 +189,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        epi.consume(row, nt * BN + c * 32, v, args.ncols);
+        epi.consume(row, nt * BN + c * 32, v, args.ncols, scratch);
       }
       tc_fence_before();
       __syncwarp();
@@ -205,7 +219,7 @@ struct EpiSoftplusRowSum {
     acc = 0.0;
     tile_acc = 0.0f;
   }
-  __device__ __forceinline__ void consume(int, int col0, const float (&v)[32], int ncols) {
+  __device__ __forceinline__ void consume(int, int col0, const float (&v)[32], int ncols, float*) {
     if (col0 + 32 <= ncols) {
       float s0 = 0.f, s1 = 0.f;
 #pragma unroll
@@ -236,7 +250,7 @@ struct EpiStoreAdd {
   int ld;
   int m;
   __device__ __forceinline__ void begin_unit(int, int) {}
-  __device__ __forceinline__ void consume(int row, int col0, const float (&v)[32], int ncols) {
+  __device__ __forceinline__ void consume(int row, int col0, const float (&v)[32], int ncols, float*) {
     if (row >= m) return;
     const float* b = base + (size_t)row * ld + col0;
     float* o = out + (size_t)row * ld + col0;
@@ -251,6 +265,51 @@ struct EpiStoreAdd {
       for (int i = 0; i < 32; ++i)
         if (col0 + i < ncols) o[i] = b[i] + v[i];
     }
+  }
+  __device__ __forceinline__ void end_tile(int) {}
+  __device__ __forceinline__ void end_unit(int, int, int) {}
+};
+
+// Split-K accumulation into a 2^-48 fixed-point int64 matrix with integer
+// atomics (order-independent => bit-deterministic for any schedule).
+struct EpiFixAtomic {
+  unsigned long long* acc;  // [m][ld]
+  int ld;
+  int m;
+  int lower_only;
+  __device__ __forceinline__ void begin_unit(int, int) {}
+  __device__ __forceinline__ void consume(int row, int col0, const float (&v)[32], int ncols, float*) {
+    if (row >= m) return;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int c = col0 + i;
+      if (c < ncols && (!lower_only || c <= row))
+        atomicAdd(&acc[(size_t)row * ld + c], (unsigned long long)llrint((double)v[i] * 281474976710656.0));
+    }
+  }
+  __device__ __forceinline__ void end_tile(int) {}
+  __device__ __forceinline__ void end_unit(int, int, int) {}
+};
+
+// Raw accumulator store through a per-warp smem transpose: lane = row in
+// TMEM, lane = column in the global store, so each store instruction writes
+// one contiguous 128-byte row segment.  out[row][col] = D for valid entries.
+struct EpiStoreT {
+  float* out;
+  int ld;
+  int m;
+  __device__ __forceinline__ void begin_unit(int, int) {}
+  __device__ __forceinline__ void consume(int row, int col0, const float (&v)[32], int ncols, float* tile) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) tile[lane * 33 + i] = v[i];
+    __syncwarp();
+    const int row0 = row - lane;
+    const int c = col0 + lane;
+#pragma unroll 4
+    for (int r = 0; r < 32; ++r)
+      if (row0 + r < m && c < ncols) out[(size_t)(row0 + r) * ld + c] = tile[r * 33 + lane];
+    __syncwarp();
   }
   __device__ __forceinline__ void end_tile(int) {}
   __device__ __forceinline__ void end_unit(int, int, int) {}

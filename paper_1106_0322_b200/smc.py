@@ -274,6 +274,9 @@ class ParticleSystem:
                 L=torch.empty((q, q), dtype=torch.float32, device=dev),
                 fws=torch.empty((_round_up(8 * q * q, 256) + 2 * q * kq + 7) // 8, dtype=torch.float64, device=dev),
                 info=torch.zeros(1, dtype=torch.int32, device=dev),
+                zbuf=torch.empty((self.N, kq), dtype=torch.bfloat16, device=dev),
+                mws=torch.empty(max(_lib.load().spa_rw_moments_workspace_bytes(self.N, q), 8), dtype=torch.uint8,
+                                device=dev),
             )
         return self._rw
 
@@ -409,14 +412,19 @@ def _rw_factor(system: ParticleSystem, scale: float, group=None):
     rw = system.rw_workspace()
     w = system.device_weights() if group is None else _global_weights(system, group)
     rw["acc"].zero_()
-    _lib.call("spa_rw_moments", _p(system.beta), system.N, system.ldb, system.q, _p(w), 0, _p(rw["acc"]), _stream())
+    _lib.call("spa_rw_moments", _p(system.beta), system.N, system.ldb, system.q, _p(w), 0, _p(rw["acc"]), None, 0,
+              _stream())
     if group is not None:
-        group.all_reduce_sum(rw["acc"])
-    _lib.call("spa_rw_moments", _p(system.beta), system.N, system.ldb, system.q, _p(w), 1, _p(rw["acc"]), _stream())
+        group.all_reduce_sum(rw["acc"][: system.q])
+    _lib.call("spa_rw_moments", _p(system.beta), system.N, system.ldb, system.q, _p(w), 1, _p(rw["acc"]),
+              _p(rw["mws"]), rw["mws"].numel(), _stream())
+    _lib.add_launches(1)  # phase 1 = transpose + tcgen05 SYRK
     if group is not None:
         group.all_reduce_sum(rw["acc"][system.q:])
     _lib.call("spa_rw_factor", _p(rw["acc"]), system.q, float(scale), 1e-6, _p(rw["L"]), _p(rw["fws"]),
               _p(rw["info"]), _stream())
+    panels = -(-system.q // 32)
+    _lib.add_launches(2 + panels + max(0, panels - 1))
 
 
 def _global_weights(system, group):
@@ -432,13 +440,13 @@ def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int,
     _rw_factor(system, config.rw_scale, group)
     # log-prior of the current particles at the new scale
     _lib.call("spa_prior_rows", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb, float(prior.a),
-              float(prior.c), float(prior.c), 0, _p(system.lp), _stream())
+              float(prior.c), float(prior.c), 2, _p(system.lp), _stream())
     system.counter.zero_()
     Lb = system.factor_operand()
     for mv in range(config.moves):
         _lib.call("spa_rw_propose", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb, Lb,
-                  int(config.seed), int(t), int(system.i0), mv, _p(rw["prop"]), _p(ws["A"]), _p(ws["ylin"]),
-                  float(prior.a), float(prior.c), _p(rw["lp_p"]), _stream())
+                  int(config.seed), int(t), int(system.i0), mv, _p(rw["zbuf"]), _p(rw["prop"]), _p(ws["A"]),
+                  _p(ws["ylin"]), float(prior.a), float(prior.c), _p(rw["lp_p"]), _stream())
         if KERNEL_TIMER is not None:
             KERNEL_TIMER.start("loglik")
         _lib.call("spa_loglik_softplus", ctypes.byref(d.struct), _p(ws["A"]), system.N, _p(ws["sp"]), _p(ws["ws"]),

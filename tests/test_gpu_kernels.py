@@ -248,3 +248,74 @@ def test_tc_gemm_exact_integers(m, rows, kp):
     np.testing.assert_array_equal(_tc_gemm(A, B), A @ B.T)
     A2 = np.concatenate([A, rng.integers(-3, 4, (m, kp)).astype(np.float32)], 1)
     np.testing.assert_array_equal(_tc_gemm(A2, B, 2), A2[:, :kp] @ B.T + A2[:, kp:] @ B.T)
+
+
+def _rw_setup(name="c1", N=1000, seed=3):
+    from paper_1106_0322_b200.data import named_spec, simulate_dataset
+
+    data, _ = simulate_dataset(named_spec(name))
+    rng = np.random.default_rng(seed)
+    C = rng.normal(size=(data.p, data.p)) * 0.05
+    B = rng.normal(size=(N, data.p)) @ C + rng.normal(0, 0.1, size=data.p)
+    d, s = system_from(data.X, data.y, B)
+    return data, d, s, B
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_rw_moments_and_factor(name):
+    """Fixed-point moments (tcgen05 SYRK) and the blocked Cholesky factor vs
+    the float64 oracle (weighted covariance, numpy Cholesky)."""
+    from paper_1106_0322_b200.smc import _rw_factor
+
+    data, d, s, B = _rw_setup(name)
+    s.log_weights = np.log(np.random.default_rng(1).dirichlet(np.ones(s.N) * 2.0))
+    _rw_factor(s, 2.38)
+    rw = s.rw_workspace()
+    assert int(rw["info"].item()) == 0
+    w = s.weights
+    Bf = B.astype(np.float32).astype(np.float64)
+    Ls_ref, mu_ref, S_ref = orc.rw_cov_factor(Bf, w)
+    acc = rw["acc"].cpu().numpy()
+    np.testing.assert_allclose(acc[: s.q] / 2.0**48, mu_ref, rtol=1e-6, atol=1e-9)
+    L = rw["L"].cpu().numpy().astype(np.float64)
+    np.testing.assert_allclose(L @ L.T, Ls_ref @ Ls_ref.T, rtol=2e-3, atol=2e-5 * np.abs(Ls_ref @ Ls_ref.T).max())
+    assert np.allclose(np.triu(L, 1), 0.0)
+
+
+def test_rw_propose_and_accept_vs_oracle():
+    """One RW move: proposal (Philox normals, L z on tcgen05, fused pack),
+    K1 likelihood of the proposal and the MH decision vs the oracle."""
+    from paper_1106_0322_b200 import GtPrior
+    from paper_1106_0322_b200.smc import _loglik_device, _rw_factor
+
+    data, d, s, B = _rw_setup("c1", N=777)
+    _rw_factor(s, 2.38)
+    rw, ws = s.rw_workspace(), s.ll_workspace()
+    a, c, seed, t, move = 1.0, 0.8, 11, 7, 2
+    _loglik_device(s, s.ll)
+    _lib.call("spa_prior_rows", ctypes.byref(d.struct), _p(s.beta), s.N, s.ldb, a, c, c, 2, _p(s.lp), _stream())
+    beta0, ll0, lp0 = s.betas.copy(), s.logliks.copy(), s.lp.cpu().numpy().copy()
+    np.testing.assert_allclose(lp0, orc.log_prior_rows(beta0, a, c), rtol=1e-6)
+    _lib.call("spa_rw_propose", ctypes.byref(d.struct), _p(s.beta), s.N, s.ldb, s.factor_operand(), seed, t, 0, move,
+              _p(rw["zbuf"]), _p(rw["prop"]), _p(ws["A"]), _p(ws["ylin"]), a, c, _p(rw["lp_p"]), _stream())
+    eps = rw["prop"][:, : s.q].cpu().numpy()  # eps = L z (float32)
+    prop = (s.beta[:, : s.q].cpu().numpy() + eps).astype(np.float64)
+    Lbf = torch.from_numpy(rw["L"].cpu().numpy()).to(torch.bfloat16).double().numpy()
+    Z = np.stack([orc.rw_normals(orc.stream_key(seed, 3, t, k), move, s.q) for k in range(s.N)])
+    Zb = torch.from_numpy(Z).to(torch.bfloat16).double().numpy()
+    np.testing.assert_allclose(prop, beta0 + Zb @ Lbf.T, rtol=0, atol=2e-5)
+    np.testing.assert_allclose(ws["ylin"].cpu().numpy(), prop @ (data.X.T @ data.y), rtol=1e-5, atol=1e-6)
+    np.testing.assert_allclose(rw["lp_p"].cpu().numpy(), orc.log_prior_rows(prop, a, c), rtol=1e-6)
+    _lib.call("spa_loglik_softplus", ctypes.byref(d.struct), _p(ws["A"]), s.N, _p(ws["sp"]), _p(ws["ws"]),
+              ws["ws"].numel(), _stream())
+    ll_p = ws["ylin"].cpu().numpy() - ws["sp"].cpu().numpy()
+    np.testing.assert_allclose(ll_p, orc.loglik_rows(data.X, data.y, prop), rtol=1e-5)
+    s.counter.zero_()
+    _lib.call("spa_rw_accept", _p(s.beta), s.ldb, _p(rw["prop"]), s.q, s.N, _p(ws["ylin"]), _p(ws["sp"]),
+              _p(rw["lp_p"]), _p(s.ll), _p(s.lp), seed, t, 0, move, _p(s.counter), _stream())
+    u = np.array([orc.rw_accept_uniform(orc.stream_key(seed, 3, t, k), move, s.q) for k in range(s.N)])
+    dlt = (ll_p + rw["lp_p"].cpu().numpy()) - (ll0 + lp0)
+    with np.errstate(divide="ignore"):
+        ok = (dlt >= 0) | (np.log(u) < dlt)
+    assert int(s.counter.item()) == int(ok.sum()) and 0 < ok.sum() < s.N
+    np.testing.assert_array_equal(s.betas, np.where(ok[:, None], prop, beta0))
