@@ -154,8 +154,9 @@ int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const d
  * *info = 0 or the failing column + 1. */
 int spa_rw_factor(const int64_t* partial, int32_t q, double scale, double jitter, float* L, double* ws, int* info,
                   void* stream);
-/* prop = beta + L z, z ~ N(0, I) from stream (seed, 3, t, i0+k) block index
- * move*(ceil(q/4)+1) + j/4 (two Box-Muller pairs per block), L z on tcgen05
+/* prop = beta + L z, z ~ N(0, I) from Philox4x32-10 keyed by seed with
+ * counter (j/4, i0+k, t, move | 3<<24) (two sign-symmetric Box-Muller pairs per
+ * block; csrc/spa_core.cu rw_normals4), L z on tcgen05
  * (zbuf: bf16 [m][kq] normals, kq = roundup(q, 64)) stored as eps = L z
  * (float32 [m][ldb], coalesced through an smem transpose); then one
  * vectorised pass packs prop = beta + eps into the K1 operand A and emits
@@ -163,8 +164,8 @@ int spa_rw_factor(const int64_t* partial, int32_t q, double scale, double jitter
 int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ldb, const void* Lb, uint64_t seed,
                    int64_t t, int64_t i0, int32_t move, void* zbuf, float* eps, void* A, double* ylin, double a,
                    double c, double* lp, void* stream);
-/* Metropolis accept: d = (ylin' - sp' + lp') - (ll + lp); u from block index
- * move*(ceil(q/4)+1) + ceil(q/4), word 0; on accept beta <- beta + eps (the
+/* Metropolis accept: d = (ylin' - sp' + lp') - (ll + lp); u (53 bits) from
+ * Philox4x32 counter (0xFFFFFFFF, i0+k, t, move | 3<<24); on accept beta <- beta + eps (the
  * proposal) and ll, lp are updated; adds the accepted count to *accepted. */
 int spa_rw_accept(float* beta, int32_t ldb, const float* eps, int32_t q, int64_t m, const double* ylin_p,
                   const double* sp_p, const double* lp_p, double* ll, double* lp, uint64_t seed, int64_t t,

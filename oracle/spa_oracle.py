@@ -91,25 +91,50 @@ def box_muller(w0, w1):
     return np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2)
 
 
-def rw_normals(key, move: int, q: int) -> np.ndarray:
-    """Proposal normals of the RW-cov move (csrc/spa_core.cu rw_normals_kernel):
-    block index move*(ceil(q/4)+1) + j/4, two float32 Box-Muller pairs per
-    block from 24-bit uniforms."""
-    b4 = -(-q // 4)
-    w = stream_blocks(key, move * (b4 + 1), b4)
-    out = np.empty((b4, 4), np.float32)
+def philox4x32_10(counters: np.ndarray, k0: int, k1: int) -> np.ndarray:
+    """Philox4x32-10 bijection (the RW proposal stream, csrc/philox.cuh)."""
+    c = np.array(counters, dtype=np.uint64).reshape(-1, 4).T.copy() & np.uint64(0xFFFFFFFF)
+    k0, k1 = np.uint64(k0 & 0xFFFFFFFF), np.uint64(k1 & 0xFFFFFFFF)
+    M0, M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
+    W0, W1 = np.uint64(0x9E3779B9), np.uint64(0xBB67AE85)
+    m32 = np.uint64(0xFFFFFFFF)
+    for _ in range(10):
+        p0 = M0 * c[0]
+        p1 = M1 * c[2]
+        c = np.stack([((p1 >> np.uint64(32)) ^ c[1] ^ k0) & m32, p1 & m32, ((p0 >> np.uint64(32)) ^ c[3] ^ k1) & m32,
+                      p0 & m32])
+        k0 = (k0 + W0) & m32
+        k1 = (k1 + W1) & m32
+    return c.T
+
+
+def rw_normals(seed: int, t: int, k: int, move: int, q: int) -> np.ndarray:
+    """Proposal normals of the RW-cov move (csrc/spa_core.cu rw_normals4):
+    Philox4x32-10, key = seed, counter (j/4, k, t, move | 3<<24); per block two
+    sign-symmetric Box-Muller pairs from 24-bit uniforms (float32 math; the
+    device uses fast intrinsics, so agreement is to ~1e-6)."""
+    nb = -(-q // 4)
+    ctr = np.zeros((nb, 4), np.uint64)
+    ctr[:, 0] = np.arange(nb)
+    ctr[:, 1] = k
+    ctr[:, 2] = t
+    ctr[:, 3] = move | (3 << 24)
+    w = philox4x32_10(ctr, seed & 0xFFFFFFFF, seed >> 32)
+    out = np.empty((nb, 4))
     for h in range(2):
-        u1 = ((w[:, 2 * h] >> np.uint64(40)).astype(np.float32) + np.float32(1.0)) * np.float32(2.0**-24)
-        u2 = (w[:, 2 * h + 1] >> np.uint64(40)).astype(np.float32) * np.float32(2.0**-24)
-        r = np.sqrt(np.float32(-2.0) * np.log(u1))
-        out[:, 2 * h] = r * np.cos(np.float32(2.0 * np.pi) * u2)
-        out[:, 2 * h + 1] = r * np.sin(np.float32(2.0 * np.pi) * u2)
-    return out.reshape(-1)[:q].astype(np.float64)
+        a, b = w[:, 2 * h], w[:, 2 * h + 1]
+        u1 = ((a >> np.uint64(8)).astype(np.float64) + 1.0) * 2.0**-24
+        u2 = (b >> np.uint64(8)).astype(np.float64) * 2.0**-24
+        r = np.sqrt(-2.0 * np.log(u1))
+        m0, m1 = np.abs(r * np.cos(np.pi / 2 * u2)), np.abs(r * np.sin(np.pi / 2 * u2))
+        out[:, 2 * h] = np.where(a & np.uint64(1), -m0, m0)
+        out[:, 2 * h + 1] = np.where(b & np.uint64(1), -m1, m1)
+    return out.reshape(-1)[:q]
 
 
-def rw_accept_uniform(key, move: int, q: int) -> float:
-    b4 = -(-q // 4)
-    return float(u53(stream_blocks(key, move * (b4 + 1) + b4, 1)[0, 0]))
+def rw_accept_uniform(seed: int, t: int, k: int, move: int) -> float:
+    w = philox4x32_10(np.array([[0xFFFFFFFF, k, t, move | (3 << 24)]], np.uint64), seed & 0xFFFFFFFF, seed >> 32)[0]
+    return float(((int(w[0]) << 21) | (int(w[1]) >> 11)) * 2.0**-53)
 
 
 def box_muller_pair(w0, w1):

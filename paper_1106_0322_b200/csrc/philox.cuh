@@ -48,6 +48,24 @@ __device__ __forceinline__ void philox_block(Key2 k, uint64_t b, uint64_t out[4]
   philox4x64_10(out, k);
 }
 
+// Philox4x32-10 (Salmon et al. 2011) for the RW proposal streams (no
+// reference counterpart): key (k0, k1), counter c[4] in place.
+__device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(M0, c[0]), lo0 = M0 * c[0];
+    const uint32_t hi1 = __umulhi(M1, c[2]), lo1 = M1 * c[2];
+    const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+    k0 += W0;
+    k1 += W1;
+  }
+}
+
 __device__ __forceinline__ double u53(uint64_t raw) { return (double)(raw >> 11) * 0x1.0p-53; }
 
 // u1 in (0, 1] so log(u1) is finite.

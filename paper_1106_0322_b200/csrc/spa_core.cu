@@ -166,9 +166,9 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const 
       const int j = j0 + i;
       float bs = 0.f;
       if (j < d.q) {
-        bs = d.coded ? (float)d.alpha[j] * p[i] : p[i];
+        bs = (d.coded ? (float)d.alpha[j] : 1.0f) * p[i];
         fy = fmaf(p[i], (float)d.sy[j], fy);
-        if (d.coded) fo = fmaf(p[i], (float)d.gamma[j], fo);
+        fo = fmaf(p[i], d.coded ? (float)d.gamma[j] : 0.f, fo);
         if (lp != nullptr && d.penalized[j]) fl += gt_logpdf_f(p[i], lc, ap1, inv, pc.de);
       }
       h[i] = __float2bfloat16_rn(bs);
@@ -195,6 +195,92 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const 
       ah[d.q] = o1;
       ah[d.q + 1] = o2;
       ah[d.q + 2] = __double2bfloat16(r2);
+    }
+  }
+}
+
+// Proposal pack (spa_rw_propose): same arithmetic as pack_kernel, but each
+// warp walks many rows with its lanes' per-column constants (alpha, X^T y,
+// gamma, penalty mask) held in registers.  IT = kp / 128 column groups.
+template <int IT>
+__global__ void __launch_bounds__(256) pack_eps_kernel(spa_design d, const float* __restrict__ beta,
+                                                       const float* __restrict__ eps, int64_t m, int ldb,
+                                                       __nv_bfloat16* __restrict__ A, double* __restrict__ ylin,
+                                                       PriorConst pc, double* __restrict__ lp) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  float ca[IT][4], cs[IT][4], cg[IT][4];
+  uint32_t pen = 0;
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int j = it * 128 + lane * 4 + i;
+      const bool v = j < d.q;
+      ca[it][i] = v ? (d.coded ? (float)d.alpha[j] : 1.0f) : 0.f;
+      cs[it][i] = v ? (float)d.sy[j] : 0.f;
+      cg[it][i] = (v && d.coded) ? (float)d.gamma[j] : 0.f;
+      if (v && d.penalized[j]) pen |= 1u << (it * 4 + i);
+    }
+  }
+  const float lc = (float)pc.lc;
+  const float ap1 = pc.de ? 0.f : (float)(pc.a + 1.0);
+  const float inv = pc.de ? (float)(1.0 / pc.c) : (float)(1.0 / (pc.a * pc.c));
+  for (int64_t row = warp0; row < m; row += nwarps) {
+    const float* b = beta + row * ldb;
+    const float* e = eps + row * ldb;
+    __nv_bfloat16* ah = A + row * (2 * (int64_t)d.kp);
+    __nv_bfloat16* al = ah + d.kp;
+    double yl = 0.0, off = 0.0, lps = 0.0;  // same grouping as pack_kernel => identical sums
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int j0 = it * 128 + lane * 4;
+      if (j0 >= d.kp) break;
+      float fy = 0.f, fo = 0.f, fl = 0.f;
+      float p[4] = {0.f, 0.f, 0.f, 0.f};
+      if (j0 + 4 <= d.q) {
+        const float4 x = *reinterpret_cast<const float4*>(b + j0);
+        const float4 y = *reinterpret_cast<const float4*>(e + j0);
+        p[0] = x.x + y.x;
+        p[1] = x.y + y.y;
+        p[2] = x.z + y.z;
+        p[3] = x.w + y.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (j0 + i < d.q) p[i] = b[j0 + i] + e[j0 + i];
+      }
+      __align__(8) __nv_bfloat16 h[4], l[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float bs = ca[it][i] * p[i];
+        h[i] = __float2bfloat16_rn(bs);
+        l[i] = __float2bfloat16_rn(bs - __bfloat162float(h[i]));
+        fy = fmaf(p[i], cs[it][i], fy);
+        fo = fmaf(p[i], cg[it][i], fo);
+        if ((pen >> (it * 4 + i)) & 1u) fl += gt_logpdf_f(p[i], lc, ap1, inv, pc.de);
+      }
+      yl += fy;
+      off += fo;
+      lps += fl;
+      *reinterpret_cast<uint2*>(ah + j0) = *reinterpret_cast<const uint2*>(h);
+      *reinterpret_cast<uint2*>(al + j0) = *reinterpret_cast<const uint2*>(l);
+    }
+    yl = warp_sum(yl);
+    off = warp_sum(off);
+    lps = warp_sum(lps);
+    if (lane == 0) {
+      ylin[row] = yl;
+      if (lp != nullptr) lp[row] = lps;
+      if (d.coded) {
+        const __nv_bfloat16 o1 = __double2bfloat16(off);
+        const double r1 = off - (double)__bfloat162float(o1);
+        const __nv_bfloat16 o2 = __double2bfloat16(r1);
+        ah[d.q] = o1;
+        ah[d.q + 1] = o2;
+        ah[d.q + 2] = __double2bfloat16(r1 - (double)__bfloat162float(o2));
+      }
     }
   }
 }
@@ -534,54 +620,62 @@ __global__ void rw_cov_kernel(const unsigned long long* __restrict__ acc, int q,
   }
 }
 
-__global__ void __launch_bounds__(512) rw_panel_kernel(double* __restrict__ S, int q, int jb, int* info) {
+__global__ void __launch_bounds__(256) rw_panel_kernel(double* __restrict__ S, int q, int jb, int* info) {
   __shared__ double dg[kPanel][kPanel + 1];
+  __shared__ double inv[kPanel][kPanel + 1];  // L11^-1 (lower)
   const int nb = min(kPanel, q - jb);
   const int tid = threadIdx.x;
-  for (int e = tid; e < nb * nb; e += blockDim.x) {
-    const int i = e / nb, j = e % nb;
-    dg[i][j] = (j <= i) ? S[(size_t)(jb + i) * q + jb + j] : 0.0;
+  for (int e = tid; e < kPanel * kPanel; e += blockDim.x) {
+    const int i = e / kPanel, j = e % kPanel;
+    dg[i][j] = (i < nb && j <= i) ? S[(size_t)(jb + i) * q + jb + j] : (i == j ? 1.0 : 0.0);
+    inv[i][j] = 0.0;
   }
   __syncthreads();
-  if (tid < 32) {
-    for (int j = 0; j < nb; ++j) {
-      if (tid == 0) {
-        double d = dg[j][j];
-        if (!(d > 0.0)) {
-          if (info && *info == 0) *info = jb + j + 1;
-          d = 1e-300;
-        }
-        dg[j][j] = sqrt(d);
+  // right-looking factorisation of the 32x32 block; thread owns 4 entries
+  for (int j = 0; j < kPanel; ++j) {
+    if (tid == 0) {
+      double d = dg[j][j];
+      if (!(d > 0.0)) {
+        if (info && j < nb && *info == 0) *info = jb + j + 1;
+        d = 1e-300;
       }
-      __syncwarp();
-      const double djj = dg[j][j];
-      if (tid > j && tid < nb) dg[tid][j] /= djj;
-      __syncwarp();
-      for (int k = j + 1; k < nb; ++k)
-        if (tid >= k && tid < nb) dg[tid][k] -= dg[tid][j] * dg[k][j];
-      __syncwarp();
+      dg[j][j] = sqrt(d);
     }
+    __syncthreads();
+    if (tid > j && tid < kPanel) dg[tid][j] /= dg[j][j];
+    __syncthreads();
+    for (int e = tid; e < kPanel * kPanel; e += blockDim.x) {
+      const int i = e / kPanel, k = e % kPanel;
+      if (k > j && i >= k) dg[i][k] -= dg[i][j] * dg[k][j];
+    }
+    __syncthreads();
   }
-  __syncthreads();
+  // L11^-1 row by row (columns in parallel)
+  for (int i = 0; i < kPanel; ++i) {
+    if (tid <= i) {
+      double v = (tid == i) ? 1.0 : 0.0;
+      for (int k = tid; k < i; ++k) v -= dg[i][k] * inv[k][tid];
+      inv[i][tid] = v / dg[i][i];
+    }
+    __syncthreads();
+  }
   for (int e = tid; e < nb * nb; e += blockDim.x) {
     const int i = e / nb, j = e % nb;
     if (j <= i) S[(size_t)(jb + i) * q + jb + j] = dg[i][j];
   }
-  // panel below: L21 = A21 L11^-T, one thread per row
+  // panel below: L21 = A21 L11^-T, one thread per row: x_j = sum_k a_k inv[j][k]
   for (int i = jb + nb + tid; i < q; i += blockDim.x) {
     double* r = S + (size_t)i * q + jb;
-    double x[kPanel];
+    double a[kPanel];
+#pragma unroll
+    for (int k = 0; k < kPanel; ++k) a[k] = (k < nb) ? r[k] : 0.0;
 #pragma unroll
     for (int j = 0; j < kPanel; ++j) {
-      if (j < nb) {
-        double v = r[j];
-        for (int k = 0; k < j; ++k) v -= x[k] * dg[j][k];
-        x[j] = v / dg[j][j];
-      }
-    }
+      double x = 0.0;
 #pragma unroll
-    for (int j = 0; j < kPanel; ++j)
-      if (j < nb) r[j] = x[j];
+      for (int k = 0; k <= j; ++k) x = fma(a[k], inv[j][k], x);
+      if (j < nb) r[j] = x;
+    }
   }
 }
 
@@ -633,37 +727,41 @@ __global__ void rw_emit_kernel(const double* __restrict__ S, int q, int kq, doub
   }
 }
 
-// Proposal normals: Z[k][j] (bf16, [m][kq]) from stream (seed, 3, t, i0+k),
-// block index move*(B4+1) + j/4 (two float32 Box-Muller pairs per block; any
-// symmetric law is a valid random-walk increment, the MH ratio is exact).
+// Proposal normals: Z[k][j] (bf16, [m][kq]).  Counter-based Philox4x32-10
+// keyed by the seed, counter (j/4, particle i0+k, t, move | tag 3 << 24);
+// each block gives two Box-Muller pairs.  Each normal is |r cos(pi/2 u)| with
+// an independent random sign, so its law is exactly symmetric whatever the
+// rounding of the fast intrinsics (the RW increment must be symmetric for the
+// plain Metropolis ratio; its exact shape is immaterial).
+__device__ __forceinline__ void rw_normals4(uint64_t seed, int64_t t, int64_t k, int move, uint32_t blk, float z[4]) {
+  uint32_t w[4] = {blk, (uint32_t)k, (uint32_t)t, (uint32_t)move | (3u << 24)};
+  philox4x32_10(w, (uint32_t)seed, (uint32_t)(seed >> 32));
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t a = w[2 * h], b = w[2 * h + 1];
+    const float u1 = ((float)(a >> 8) + 1.0f) * 0x1.0p-24f;  // (0, 1]
+    const float u2 = (float)(b >> 8) * 0x1.0p-24f;           // [0, 1)
+    const float r = sqrtf(-2.0f * __logf(u1));
+    float sn, cs;
+    __sincosf(1.5707963267948966f * u2, &sn, &cs);
+    const float m0 = fabsf(r * cs), m1 = fabsf(r * sn);
+    z[2 * h] = (a & 1u) ? -m0 : m0;
+    z[2 * h + 1] = (b & 1u) ? -m1 : m1;
+  }
+}
+
 __global__ void rw_normals_kernel(int64_t m, int q, int kq, uint64_t seed, int64_t t, int64_t i0, int move,
                                   __nv_bfloat16* __restrict__ Z) {
-  const int b4 = (q + 3) / 4;
   const int kq4 = kq / 4;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= m * kq4) return;
   const int64_t k = e / kq4;
   const int jb = (int)(e % kq4);
   __align__(8) __nv_bfloat16 z[4];
-  if (jb >= b4) {
-    z[0] = z[1] = z[2] = z[3] = __float2bfloat16(0.0f);
-  } else {
-    uint64_t w[4];
-    philox_block(stream_key(seed, 3, (uint64_t)t, (uint64_t)(i0 + k)), (uint64_t)move * (b4 + 1) + jb, w);
-    float zz[4];
+  float zz[4] = {0.f, 0.f, 0.f, 0.f};
+  if (4 * jb < q) rw_normals4(seed, t, i0 + k, move, (uint32_t)jb, zz);
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const float u1 = ((float)(w[2 * h] >> 40) + 1.0f) * 0x1.0p-24f;  // (0, 1]
-      const float u2 = (float)(w[2 * h + 1] >> 40) * 0x1.0p-24f;       // [0, 1)
-      const float r = sqrtf(-2.0f * logf(u1));
-      float sn, cs;
-      sincospif(2.0f * u2, &sn, &cs);
-      zz[2 * h] = r * cs;
-      zz[2 * h + 1] = r * sn;
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) z[i] = __float2bfloat16(4 * jb + i < q ? zz[i] : 0.0f);
-  }
+  for (int i = 0; i < 4; ++i) z[i] = __float2bfloat16(4 * jb + i < q ? zz[i] : 0.0f);
   *reinterpret_cast<uint2*>(Z + k * kq + 4 * jb) = *reinterpret_cast<const uint2*>(z);
 }
 
@@ -674,15 +772,17 @@ __global__ void rw_center_t_kernel(const float* __restrict__ beta, int64_t m, in
                                    const double* __restrict__ w, const unsigned long long* __restrict__ acc,
                                    __nv_bfloat16* __restrict__ Dt, int64_t ldk) {
   __shared__ float tile[32][33];
+  __shared__ float sw[32], mu[32];
   const int64_t k0 = (int64_t)blockIdx.x * 32;
   const int j0 = blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  if (ty == 0) sw[tx] = (k0 + tx < m) ? (float)sqrt(w[k0 + tx]) : 0.f;
+  if (ty == 1) mu[tx] = (j0 + tx < q) ? (float)from_fix(acc[j0 + tx]) : 0.f;
+  __syncthreads();
   for (int r = ty; r < 32; r += 8) {
     const int64_t k = k0 + r;
     const int j = j0 + tx;
-    float v = 0.f;
-    if (k < m && j < q) v = (float)(sqrt(w[k]) * ((double)beta[k * ldb + j] - from_fix(acc[j])));
-    tile[r][tx] = v;
+    tile[r][tx] = (k < m && j < q) ? sw[r] * (beta[k * ldb + j] - mu[tx]) : 0.f;
   }
   __syncthreads();
   for (int r = ty; r < 32; r += 8) {
@@ -705,10 +805,9 @@ __global__ void rw_accept_kernel(float* __restrict__ beta, int ldb, const float*
   if (row >= m) return;
   int ok = 0;
   if (lane == 0) {
-    const int b4 = (q + 3) / 4;
-    uint64_t w[4];
-    philox_block(stream_key(seed, 3, (uint64_t)t, (uint64_t)(i0 + row)), (uint64_t)move * (b4 + 1) + b4, w);
-    const double u = u53(w[0]);
+    uint32_t w[4] = {0xFFFFFFFFu, (uint32_t)(i0 + row), (uint32_t)t, (uint32_t)move | (3u << 24)};
+    philox4x32_10(w, (uint32_t)seed, (uint32_t)(seed >> 32));
+    const double u = (double)(((uint64_t)w[0] << 21) | (w[1] >> 11)) * 0x1.0p-53;
     const double llp = ylin_p[row] - sp_p[row];
     const double d = (llp + lp_p[row]) - (ll[row] + lp[row]);
     ok = (d >= 0.0) || (log(u) < d);
@@ -940,7 +1039,7 @@ int spa_rw_factor(const int64_t* partial, int32_t q, double scale, double jitter
       reinterpret_cast<const unsigned long long*>(partial), q, jitter, ws);
   SPA_CHECK_LAUNCH();
   for (int jb = 0; jb < q; jb += kPanel) {
-    rw_panel_kernel<<<1, 512, 0, st>>>(ws, q, jb, info);
+    rw_panel_kernel<<<1, 256, 0, st>>>(ws, q, jb, info);
     SPA_CHECK_LAUNCH();
     const int rest = q - jb - kPanel;
     if (rest > 0) {
@@ -979,8 +1078,19 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
   EpiStoreT epi{eps, ldb, (int)m};
   int rc = launch_tc<1, 1, 256>(Z, (uint64_t)kq, Lb, (uint64_t)kq, (uint64_t)q, args, 1, epi, st);
   if (rc) return rc;
-  pack_kernel<<<cdiv(m, 8), 256, 0, st>>>(*d, beta, eps, m, ldb, reinterpret_cast<__nv_bfloat16*>(A), ylin,
-                                          make_prior(a, c, c), lp);
+  const unsigned grid = std::min<unsigned>(cdiv(m, 8), 148 * 8);
+  const PriorConst pc = make_prior(a, c, c);
+  auto* Ab = reinterpret_cast<__nv_bfloat16*>(A);
+  if (d->kp <= 128)
+    pack_eps_kernel<1><<<grid, 256, 0, st>>>(*d, beta, eps, m, ldb, Ab, ylin, pc, lp);
+  else if (d->kp <= 256)
+    pack_eps_kernel<2><<<grid, 256, 0, st>>>(*d, beta, eps, m, ldb, Ab, ylin, pc, lp);
+  else if (d->kp <= 512)
+    pack_eps_kernel<4><<<grid, 256, 0, st>>>(*d, beta, eps, m, ldb, Ab, ylin, pc, lp);
+  else if (d->kp <= 1024)
+    pack_eps_kernel<8><<<grid, 256, 0, st>>>(*d, beta, eps, m, ldb, Ab, ylin, pc, lp);
+  else
+    pack_kernel<<<cdiv(m, 8), 256, 0, st>>>(*d, beta, eps, m, ldb, Ab, ylin, pc, lp);
   SPA_CHECK_LAUNCH();
   return 0;
 }

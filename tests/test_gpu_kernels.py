@@ -301,9 +301,13 @@ def test_rw_propose_and_accept_vs_oracle():
     eps = rw["prop"][:, : s.q].cpu().numpy()  # eps = L z (float32)
     prop = (s.beta[:, : s.q].cpu().numpy() + eps).astype(np.float64)
     Lbf = torch.from_numpy(rw["L"].cpu().numpy()).to(torch.bfloat16).double().numpy()
-    Z = np.stack([orc.rw_normals(orc.stream_key(seed, 3, t, k), move, s.q) for k in range(s.N)])
+    Z = np.stack([orc.rw_normals(seed, t, k, move, s.q) for k in range(s.N)])
     Zb = torch.from_numpy(Z).to(torch.bfloat16).double().numpy()
-    np.testing.assert_allclose(prop, beta0 + Zb @ Lbf.T, rtol=0, atol=2e-5)
+    # device normals use fast intrinsics (~1e-6); a z within that of a bf16
+    # rounding boundary rounds the other way (one bf16 ulp): allow rare flips
+    diff = np.abs(prop - (beta0 + Zb @ Lbf.T))
+    assert np.mean(diff > 1e-5 * max(1.0, np.abs(prop).max())) < 0.005
+    assert diff.max() < 2.0**-7 * np.abs(Zb).max() * np.abs(Lbf).max() * 4
     np.testing.assert_allclose(ws["ylin"].cpu().numpy(), prop @ (data.X.T @ data.y), rtol=1e-5, atol=1e-6)
     np.testing.assert_allclose(rw["lp_p"].cpu().numpy(), orc.log_prior_rows(prop, a, c), rtol=1e-6)
     _lib.call("spa_loglik_softplus", ctypes.byref(d.struct), _p(ws["A"]), s.N, _p(ws["sp"]), _p(ws["ws"]),
@@ -313,7 +317,7 @@ def test_rw_propose_and_accept_vs_oracle():
     s.counter.zero_()
     _lib.call("spa_rw_accept", _p(s.beta), s.ldb, _p(rw["prop"]), s.q, s.N, _p(ws["ylin"]), _p(ws["sp"]),
               _p(rw["lp_p"]), _p(s.ll), _p(s.lp), seed, t, 0, move, _p(s.counter), _stream())
-    u = np.array([orc.rw_accept_uniform(orc.stream_key(seed, 3, t, k), move, s.q) for k in range(s.N)])
+    u = np.array([orc.rw_accept_uniform(seed, t, k, move) for k in range(s.N)])
     dlt = (ll_p + rw["lp_p"].cpu().numpy()) - (ll0 + lp0)
     with np.errstate(divide="ignore"):
         ok = (dlt >= 0) | (np.log(u) < dlt)
