@@ -200,30 +200,28 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const 
 }
 
 // Proposal pack (spa_rw_propose): same arithmetic as pack_kernel, but each
-// warp walks many rows with its lanes' per-column constants (alpha, X^T y,
-// gamma, penalty mask) held in registers.  IT = kp / 128 column groups.
-template <int IT>
+// block stages the per-column constants (alpha, X^T y, gamma as float32, the
+// penalty flag) in shared memory once and its warps walk many rows.
 __global__ void __launch_bounds__(256) pack_eps_kernel(spa_design d, const float* __restrict__ beta,
                                                        const float* __restrict__ eps, int64_t m, int ldb,
                                                        __nv_bfloat16* __restrict__ A, double* __restrict__ ylin,
                                                        PriorConst pc, double* __restrict__ lp) {
+  extern __shared__ float4 csm[];  // [kp/4] x {alpha, sy, gamma, pen}
+  float* ca = reinterpret_cast<float*>(csm);
+  float* cs = ca + d.kp;
+  float* cg = cs + d.kp;
+  float* cp = cg + d.kp;
+  for (int j = threadIdx.x; j < d.kp; j += blockDim.x) {
+    const bool v = j < d.q;
+    ca[j] = v ? (d.coded ? (float)d.alpha[j] : 1.0f) : 0.f;
+    cs[j] = v ? (float)d.sy[j] : 0.f;
+    cg[j] = (v && d.coded) ? (float)d.gamma[j] : 0.f;
+    cp[j] = (v && d.penalized[j]) ? 1.f : 0.f;
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  float ca[IT][4], cs[IT][4], cg[IT][4];
-  uint32_t pen = 0;
-#pragma unroll
-  for (int it = 0; it < IT; ++it) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int j = it * 128 + lane * 4 + i;
-      const bool v = j < d.q;
-      ca[it][i] = v ? (d.coded ? (float)d.alpha[j] : 1.0f) : 0.f;
-      cs[it][i] = v ? (float)d.sy[j] : 0.f;
-      cg[it][i] = (v && d.coded) ? (float)d.gamma[j] : 0.f;
-      if (v && d.penalized[j]) pen |= 1u << (it * 4 + i);
-    }
-  }
   const float lc = (float)pc.lc;
   const float ap1 = pc.de ? 0.f : (float)(pc.a + 1.0);
   const float inv = pc.de ? (float)(1.0 / pc.c) : (float)(1.0 / (pc.a * pc.c));
@@ -233,10 +231,7 @@ __global__ void __launch_bounds__(256) pack_eps_kernel(spa_design d, const float
     __nv_bfloat16* ah = A + row * (2 * (int64_t)d.kp);
     __nv_bfloat16* al = ah + d.kp;
     double yl = 0.0, off = 0.0, lps = 0.0;  // same grouping as pack_kernel => identical sums
-#pragma unroll
-    for (int it = 0; it < IT; ++it) {
-      const int j0 = it * 128 + lane * 4;
-      if (j0 >= d.kp) break;
+    for (int j0 = lane * 4; j0 < d.kp; j0 += 128) {
       float fy = 0.f, fo = 0.f, fl = 0.f;
       float p[4] = {0.f, 0.f, 0.f, 0.f};
       if (j0 + 4 <= d.q) {
@@ -251,15 +246,21 @@ __global__ void __launch_bounds__(256) pack_eps_kernel(spa_design d, const float
         for (int i = 0; i < 4; ++i)
           if (j0 + i < d.q) p[i] = b[j0 + i] + e[j0 + i];
       }
+      const float4 va = *reinterpret_cast<const float4*>(ca + j0);
+      const float4 vs = *reinterpret_cast<const float4*>(cs + j0);
+      const float4 vg = *reinterpret_cast<const float4*>(cg + j0);
+      const float4 vp = *reinterpret_cast<const float4*>(cp + j0);
+      const float a4[4] = {va.x, va.y, va.z, va.w}, s4[4] = {vs.x, vs.y, vs.z, vs.w};
+      const float g4[4] = {vg.x, vg.y, vg.z, vg.w}, p4[4] = {vp.x, vp.y, vp.z, vp.w};
       __align__(8) __nv_bfloat16 h[4], l[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const float bs = ca[it][i] * p[i];
+        const float bs = a4[i] * p[i];
         h[i] = __float2bfloat16_rn(bs);
         l[i] = __float2bfloat16_rn(bs - __bfloat162float(h[i]));
-        fy = fmaf(p[i], cs[it][i], fy);
-        fo = fmaf(p[i], cg[it][i], fo);
-        if ((pen >> (it * 4 + i)) & 1u) fl += gt_logpdf_f(p[i], lc, ap1, inv, pc.de);
+        fy = fmaf(p[i], s4[i], fy);
+        fo = fmaf(p[i], g4[i], fo);
+        if (p4[i] != 0.f) fl += gt_logpdf_f(p[i], lc, ap1, inv, pc.de);
       }
       yl += fy;
       off += fo;
@@ -300,12 +301,35 @@ __global__ void prior_kernel(spa_design d, const float* __restrict__ beta, int64
     for (int j = lane; j < d.q; j += 32)
       if (d.penalized[j]) f += gt_logpdf_f(b[j], lc, ap1, inv, pc.de);
     s = (double)f;
-  } else {
+  } else if (pc.de) {
     for (int j = lane; j < d.q; j += 32) {
       if (!d.penalized[j]) continue;
       const double bj = (double)b[j];
       s += mode == 0 ? gt_logpdf(bj, pc) : gt_logratio(bj, pc);
     }
+  } else {
+    // float64: sum_j log1p(u_j) = log prod_j (1 + u_j) over groups of 8 terms
+    // (one log per 8 coordinates; every factor lies in [1, max(c_prev/c, 1 +
+    // |beta|/(a c))], products stay far from overflow; rel. error ~1e-15).
+    const double k1 = mode == 0 ? 1.0 / (pc.a * pc.c) : (1.0 / pc.c - 1.0 / pc.c_prev) / pc.a;
+    const double k2 = mode == 0 ? 0.0 : 1.0 / (pc.a * pc.c_prev);
+    const double cst = mode == 0 ? pc.lc : pc.lr;
+    double lsum = 0.0, prod = 1.0;
+    int cnt = 0, npen = 0;
+    for (int j = lane; j < d.q; j += 32) {
+      if (!d.penalized[j]) continue;
+      const double x = fabs((double)b[j]);
+      const double u = mode == 0 ? x * k1 : (x * k1) / (1.0 + x * k2);
+      prod *= 1.0 + u;
+      ++npen;
+      if (++cnt == 8 || !(prod < 1e250)) {
+        lsum += log(prod);
+        prod = 1.0;
+        cnt = 0;
+      }
+    }
+    lsum += log(prod);
+    s = (double)npen * cst - (pc.a + 1.0) * lsum;
   }
   s = warp_sum(s);
   if (lane == 0) out[row] = s;
@@ -650,12 +674,16 @@ __global__ void __launch_bounds__(256) rw_panel_kernel(double* __restrict__ S, i
     }
     __syncthreads();
   }
-  // L11^-1 row by row (columns in parallel)
-  for (int i = 0; i < kPanel; ++i) {
-    if (tid <= i) {
-      double v = (tid == i) ? 1.0 : 0.0;
-      for (int k = tid; k < i; ++k) v -= dg[i][k] * inv[k][tid];
-      inv[i][tid] = v / dg[i][i];
+  // L11^-1 by right-looking forward substitution on [L | I]: step k scales
+  // row k of the right-hand side, then eliminates it from the rows below.
+  for (int e = tid; e < kPanel * kPanel; e += blockDim.x) inv[e / kPanel][e % kPanel] = (e / kPanel == e % kPanel);
+  __syncthreads();
+  for (int k = 0; k < kPanel; ++k) {
+    if (tid < kPanel) inv[k][tid] /= dg[k][k];
+    __syncthreads();
+    for (int e = tid; e < kPanel * kPanel; e += blockDim.x) {
+      const int i = e / kPanel, cc = e % kPanel;
+      if (i > k) inv[i][cc] -= dg[i][k] * inv[k][cc];
     }
     __syncthreads();
   }
@@ -1078,19 +1106,9 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
   EpiStoreT epi{eps, ldb, (int)m};
   int rc = launch_tc<1, 1, 256>(Z, (uint64_t)kq, Lb, (uint64_t)kq, (uint64_t)q, args, 1, epi, st);
   if (rc) return rc;
-  const unsigned grid = std::min<unsigned>(cdiv(m, 8), 148 * 8);
-  const PriorConst pc = make_prior(a, c, c);
-  auto* Ab = reinterpret_cast<__nv_bfloat16*>(A);
-  if (d->kp <= 128)
-    pack_eps_kernel<1><<<grid, 256, 0, st>>>(*d, beta, eps, m, ldb, Ab, ylin, pc, lp);
-  else if (d->kp <= 256)
-    pack_eps_kernel<2><<<grid, 256, 0, st>>>(*d, beta, eps, m, ldb, Ab, ylin, pc, lp);
-  else if (d->kp <= 512)
-    pack_eps_kernel<4><<<grid, 256, 0, st>>>(*d, beta, eps, m, ldb, Ab, ylin, pc, lp);
-  else if (d->kp <= 1024)
-    pack_eps_kernel<8><<<grid, 256, 0, st>>>(*d, beta, eps, m, ldb, Ab, ylin, pc, lp);
-  else
-    pack_kernel<<<cdiv(m, 8), 256, 0, st>>>(*d, beta, eps, m, ldb, Ab, ylin, pc, lp);
+  const unsigned grid = std::min<unsigned>(cdiv(m, 8), 148 * 16);
+  pack_eps_kernel<<<grid, 256, (size_t)16 * d->kp, st>>>(*d, beta, eps, m, ldb, reinterpret_cast<__nv_bfloat16*>(A),
+                                                         ylin, make_prior(a, c, c), lp);
   SPA_CHECK_LAUNCH();
   return 0;
 }

@@ -73,8 +73,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int unit = blockIdx.x / args.m_tiles;
-  const int mt = blockIdx.x % args.m_tiles;
+  // units of the same A tile are adjacent in the grid, so they run together
+  // and share the A tile in L2 (one DRAM read of A per launch)
+  const int units = gridDim.x / args.m_tiles;
+  const int unit = blockIdx.x % units;
+  const int mt = blockIdx.x / units;
   int nt0, nt1, kb0, kb1;
   if (args.kb_per_unit > 0) {
     nt0 = 0;
