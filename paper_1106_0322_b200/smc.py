@@ -428,8 +428,12 @@ def _rw_factor(system: ParticleSystem, scale: float, group=None):
 
 
 def _global_weights(system, group):
-    # weights normalised over all shards: logw is globally normalised already
-    _lib.call("spa_logw_apply", _p(system.logw), None, system.N, _p(group.zero_res(system)), _p(system.w), _stream())
+    """Normalised weights exp(logw - lse(logw)) with the LSE over ALL shards
+    (same fixed-chunk combine as the single-process path => identical bits)."""
+    _lib.call("spa_lse_chunk_stats", _p(system.logw), None, system.N, _p(system.stats), _stream())
+    stats = group.all_gather_cat(system.stats)
+    _lib.call("spa_lse_combine", _p(stats), stats.shape[0], _p(system.res), _stream())
+    _lib.call("spa_logw_apply", _p(system.logw), None, system.N, _p(system.res), _p(system.w), _stream())
     return system.w
 
 
