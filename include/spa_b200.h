@@ -92,8 +92,9 @@ int spa_loglik_rows(const spa_design* d, const float* beta, int64_t m, int32_t l
  * mode 0: out[k] = sum_j gt(beta_kj; a, c)             (model.py:78-81)
  * mode 1: out[k] = sum_j gt(beta_kj; a, c) - gt(beta_kj; a, c_prev)
  *         (smc.py:248-257 reweight increments, cancellation-free form);
- * mode 2: as mode 0 with float32 terms (the arithmetic of the RW proposal
- *         pack, so the MH ratio compares like with like). */
+ * mode 2: as mode 0 in the arithmetic of the RW proposal pack (float64
+ *         products of (1 + |beta|/(a c)) per lane, one log each), so the MH
+ *         ratio compares bit-identical quantities. */
 int spa_prior_rows(const spa_design* d, const float* beta, int64_t m, int32_t ldb, double a, double c,
                    double c_prev, int32_t mode, double* out, void* stream);
 
@@ -141,16 +142,19 @@ int spa_mwg_move(const spa_design* d, float* beta, int64_t m, int32_t ldb, doubl
  *   phase 0: mu = sum_k w_k beta_k                       -> partial[0:q]
  *   phase 1: S = sum_k w_k (beta_k-mu)(beta_k-mu)^T      -> partial[q:] (lower)
  *            as a split-K tcgen05 SYRK of the centred, sqrt(w)-weighted,
- *            transposed bf16 hi/lo particles (ws: spa_rw_moments_workspace_bytes).
+ *            transposed bf16 hi/lo particles; per-split float32 tiles are
+ *            summed in fixed order (ws: spa_rw_moments_workspace_bytes).
  * Integer sums are order-independent, so the moments are bit-identical for any
  * CTA schedule or particle sharding (multi-GPU: all-reduce `partial`). */
 size_t spa_rw_moments_workspace_bytes(int64_t m, int32_t q);
 int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const double* w, int32_t phase,
                    int64_t* partial, void* ws, size_t ws_bytes, void* stream);
-/* Covariance from the fixed-point moments, jitter, blocked float64 Cholesky;
+/* Covariance from the fixed-point moments, jitter, blocked float32 Cholesky
+ * (L only parameterises a symmetric proposal, so float32 suffices);
  * L = s*chol(S) as float32 [q][q] row-major lower (s = scale/sqrt(q)) and as
  * the bf16 proposal operand [q][kq] at byte offset roundup(8*q*q, 256) of ws
- * (kq = roundup(q, 64)); ws >= roundup(8*q*q, 256) + 2*q*kq bytes;
+ * (kq = roundup(q, 64)); ws >= roundup(8*q*q, 256) + roundup(2*q*kq, 256) + 8192
+ * bytes (the last 8 KB hold the 32x32 panel inverse);
  * *info = 0 or the failing column + 1. */
 int spa_rw_factor(const int64_t* partial, int32_t q, double scale, double jitter, float* L, double* ws, int* info,
                   void* stream);
@@ -158,16 +162,17 @@ int spa_rw_factor(const int64_t* partial, int32_t q, double scale, double jitter
  * counter (j/4, i0+k, t, move | 3<<24) (two sign-symmetric Box-Muller pairs per
  * block; csrc/spa_core.cu rw_normals4), L z on tcgen05
  * (zbuf: bf16 [m][kq] normals, kq = roundup(q, 64)) stored as eps = L z
- * (float32 [m][ldb], coalesced through an smem transpose); then one
+ * (bf16 [m][ldb] -- rounding keeps the increment law exactly symmetric --,
+ * coalesced through an smem transpose); then one
  * vectorised pass packs prop = beta + eps into the K1 operand A and emits
  * ylin and lp at c.  `Lb` is the bf16 operand written by spa_rw_factor. */
 int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ldb, const void* Lb, uint64_t seed,
-                   int64_t t, int64_t i0, int32_t move, void* zbuf, float* eps, void* A, double* ylin, double a,
+                   int64_t t, int64_t i0, int32_t move, void* zbuf, void* eps, void* A, double* ylin, double a,
                    double c, double* lp, void* stream);
 /* Metropolis accept: d = (ylin' - sp' + lp') - (ll + lp); u (53 bits) from
  * Philox4x32 counter (0xFFFFFFFF, i0+k, t, move | 3<<24); on accept beta <- beta + eps (the
  * proposal) and ll, lp are updated; adds the accepted count to *accepted. */
-int spa_rw_accept(float* beta, int32_t ldb, const float* eps, int32_t q, int64_t m, const double* ylin_p,
+int spa_rw_accept(float* beta, int32_t ldb, const void* eps, int32_t q, int64_t m, const double* ylin_p,
                   const double* sp_p, const double* lp_p, double* ll, double* lp, uint64_t seed, int64_t t,
                   int64_t i0, int32_t move, unsigned long long* accepted, void* stream);
 

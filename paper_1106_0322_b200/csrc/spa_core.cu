@@ -10,6 +10,7 @@
 
 #include <cmath>
 #include <mutex>
+#include <vector>
 #include <string>
 
 #include "../../include/spa_b200.h"
@@ -120,24 +121,53 @@ __device__ __forceinline__ float gt_logpdf_f(float b, float lc, float ap1, float
   return de ? lc - x * inv : lc - ap1 * log1pf(x * inv);
 }
 
+// Per-lane log-prior accumulator shared by pack_kernel, pack_eps_kernel and
+// prior_kernel mode 2 (same lane->column mapping and multiplication order, so
+// all three produce identical bits):
+//   sum_j gt(p_j) = npen*(-log 2c) - (a+1) * log prod_j (1 + |p_j|/(a c))
+// with the float64 product flushed into the log sum before it can overflow
+// (a = inf: the linear double-exponential form).
+struct LpAcc {
+  double logsum = 0.0, prod = 1.0, lin = 0.0;
+  int npen = 0;
+  __device__ __forceinline__ void add(float p, double K, int de) {
+    const double x = fabs((double)p);
+    ++npen;
+    if (de) {
+      lin += x;
+    } else {
+      prod *= fma(x, K, 1.0);
+      if (!(prod < 1e250)) {
+        logsum += log(prod);
+        prod = 1.0;
+      }
+    }
+  }
+  __device__ __forceinline__ double value(const PriorConst& pc) const {
+    return pc.de ? (double)npen * pc.lc - lin / pc.c : (double)npen * pc.lc - (pc.a + 1.0) * (logsum + log(prod));
+  }
+};
+
 // One warp per particle row; lanes take 4 consecutive columns (float4).
 // prop = beta (+ eps); A = [hi | lo] of alpha*prop; ylin = prop . X^T y;
 // off (coded) into the offset columns; lp = sum gt(prop) (float32 terms,
 // float64 accumulation).
-__global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const float* __restrict__ eps, int64_t m,
+__global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const __nv_bfloat16* __restrict__ eps, int64_t m,
                             int ldb, __nv_bfloat16* __restrict__ A, double* __restrict__ ylin, PriorConst pc,
                             double* __restrict__ lp) {
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= m) return;
   const float* b = beta + row * ldb;
-  const float* e = eps ? eps + row * ldb : nullptr;
+  const __nv_bfloat16* e = eps ? eps + row * ldb : nullptr;
   __nv_bfloat16* ah = A + row * (2 * (int64_t)d.kp);
   __nv_bfloat16* al = ah + d.kp;
   const float lc = (float)(-log(2.0 * pc.c));
   const float ap1 = pc.de ? 0.f : (float)(pc.a + 1.0);
   const float inv = pc.de ? (float)(1.0 / pc.c) : (float)(1.0 / (pc.a * pc.c));
-  double yl = 0.0, off = 0.0, lps = 0.0;
+  double yl = 0.0, off = 0.0;
+  LpAcc la;
+  const double K = pc.de ? 0.0 : 1.0 / (pc.a * pc.c);
   const bool vec = (ldb & 3) == 0;
   for (int j0 = lane * 4; j0 < d.kp; j0 += 128) {
     float p[4] = {0.f, 0.f, 0.f, 0.f};
@@ -148,19 +178,21 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const 
       p[2] = x.z;
       p[3] = x.w;
       if (e) {
-        const float4 y = *reinterpret_cast<const float4*>(e + j0);
-        p[0] += y.x;
-        p[1] += y.y;
-        p[2] += y.z;
-        p[3] += y.w;
+        const uint2 yv = *reinterpret_cast<const uint2*>(e + j0);
+        const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&yv);
+        const float2 ya = __bfloat1622float2(y2[0]), yb = __bfloat1622float2(y2[1]);
+        p[0] += ya.x;
+        p[1] += ya.y;
+        p[2] += yb.x;
+        p[3] += yb.y;
       }
     } else {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        if (j0 + i < d.q) p[i] = b[j0 + i] + (e ? e[j0 + i] : 0.f);
+        if (j0 + i < d.q) p[i] = b[j0 + i] + (e ? __bfloat162float(e[j0 + i]) : 0.f);
     }
     __align__(8) __nv_bfloat16 h[4], l[4];
-    float fy = 0.f, fo = 0.f, fl = 0.f;
+    float fy = 0.f, fo = 0.f;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int j = j0 + i;
@@ -169,20 +201,20 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const 
         bs = (d.coded ? (float)d.alpha[j] : 1.0f) * p[i];
         fy = fmaf(p[i], (float)d.sy[j], fy);
         fo = fmaf(p[i], d.coded ? (float)d.gamma[j] : 0.f, fo);
-        if (lp != nullptr && d.penalized[j]) fl += gt_logpdf_f(p[i], lc, ap1, inv, pc.de);
+        if (lp != nullptr && d.penalized[j]) la.add(p[i], K, pc.de);
       }
       h[i] = __float2bfloat16_rn(bs);
       l[i] = __float2bfloat16_rn(bs - __bfloat162float(h[i]));
     }
     yl += fy;
     off += fo;
-    lps += fl;
     *reinterpret_cast<uint2*>(ah + j0) = *reinterpret_cast<const uint2*>(h);
     *reinterpret_cast<uint2*>(al + j0) = *reinterpret_cast<const uint2*>(l);
   }
   yl = warp_sum(yl);
   off = warp_sum(off);
-  if (lp != nullptr) lps = warp_sum(lps);
+  double lps = 0.0;
+  if (lp != nullptr) lps = warp_sum(la.value(pc));
   if (lane == 0) {
     ylin[row] = yl;
     if (lp != nullptr) lp[row] = lps;
@@ -203,7 +235,7 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const 
 // block stages the per-column constants (alpha, X^T y, gamma as float32, the
 // penalty flag) in shared memory once and its warps walk many rows.
 __global__ void __launch_bounds__(256) pack_eps_kernel(spa_design d, const float* __restrict__ beta,
-                                                       const float* __restrict__ eps, int64_t m, int ldb,
+                                                       const __nv_bfloat16* __restrict__ eps, int64_t m, int ldb,
                                                        __nv_bfloat16* __restrict__ A, double* __restrict__ ylin,
                                                        PriorConst pc, double* __restrict__ lp) {
   extern __shared__ float4 csm[];  // [kp/4] x {alpha, sy, gamma, pen}
@@ -222,29 +254,30 @@ __global__ void __launch_bounds__(256) pack_eps_kernel(spa_design d, const float
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const float lc = (float)pc.lc;
-  const float ap1 = pc.de ? 0.f : (float)(pc.a + 1.0);
-  const float inv = pc.de ? (float)(1.0 / pc.c) : (float)(1.0 / (pc.a * pc.c));
+  const double K = pc.de ? 0.0 : 1.0 / (pc.a * pc.c);
   for (int64_t row = warp0; row < m; row += nwarps) {
     const float* b = beta + row * ldb;
-    const float* e = eps + row * ldb;
+    const __nv_bfloat16* e = eps + row * ldb;
     __nv_bfloat16* ah = A + row * (2 * (int64_t)d.kp);
     __nv_bfloat16* al = ah + d.kp;
-    double yl = 0.0, off = 0.0, lps = 0.0;  // same grouping as pack_kernel => identical sums
+    double yl = 0.0, off = 0.0;  // same grouping as pack_kernel => identical sums
+    LpAcc la;
     for (int j0 = lane * 4; j0 < d.kp; j0 += 128) {
-      float fy = 0.f, fo = 0.f, fl = 0.f;
+      float fy = 0.f, fo = 0.f;
       float p[4] = {0.f, 0.f, 0.f, 0.f};
       if (j0 + 4 <= d.q) {
         const float4 x = *reinterpret_cast<const float4*>(b + j0);
-        const float4 y = *reinterpret_cast<const float4*>(e + j0);
-        p[0] = x.x + y.x;
-        p[1] = x.y + y.y;
-        p[2] = x.z + y.z;
-        p[3] = x.w + y.w;
+        const uint2 yv = *reinterpret_cast<const uint2*>(e + j0);
+        const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&yv);
+        const float2 ya = __bfloat1622float2(y2[0]), yb = __bfloat1622float2(y2[1]);
+        p[0] = x.x + ya.x;
+        p[1] = x.y + ya.y;
+        p[2] = x.z + yb.x;
+        p[3] = x.w + yb.y;
       } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          if (j0 + i < d.q) p[i] = b[j0 + i] + e[j0 + i];
+          if (j0 + i < d.q) p[i] = b[j0 + i] + __bfloat162float(e[j0 + i]);
       }
       const float4 va = *reinterpret_cast<const float4*>(ca + j0);
       const float4 vs = *reinterpret_cast<const float4*>(cs + j0);
@@ -260,17 +293,16 @@ __global__ void __launch_bounds__(256) pack_eps_kernel(spa_design d, const float
         l[i] = __float2bfloat16_rn(bs - __bfloat162float(h[i]));
         fy = fmaf(p[i], s4[i], fy);
         fo = fmaf(p[i], g4[i], fo);
-        if (p4[i] != 0.f) fl += gt_logpdf_f(p[i], lc, ap1, inv, pc.de);
+        if (p4[i] != 0.f) la.add(p[i], K, pc.de);
       }
       yl += fy;
       off += fo;
-      lps += fl;
       *reinterpret_cast<uint2*>(ah + j0) = *reinterpret_cast<const uint2*>(h);
       *reinterpret_cast<uint2*>(al + j0) = *reinterpret_cast<const uint2*>(l);
     }
     yl = warp_sum(yl);
     off = warp_sum(off);
-    lps = warp_sum(lps);
+    const double lps = warp_sum(la.value(pc));
     if (lane == 0) {
       ylin[row] = yl;
       if (lp != nullptr) lp[row] = lps;
@@ -293,14 +325,14 @@ __global__ void prior_kernel(spa_design d, const float* __restrict__ beta, int64
   if (row >= m) return;
   const float* b = beta + row * ldb;
   double s = 0.0;
-  if (mode == 2) {  // float32 terms, identical arithmetic to pack_kernel's lp
-    const float lc = (float)pc.lc;
-    const float ap1 = pc.de ? 0.f : (float)(pc.a + 1.0);
-    const float inv = pc.de ? (float)(1.0 / pc.c) : (float)(1.0 / (pc.a * pc.c));
-    float f = 0.f;
-    for (int j = lane; j < d.q; j += 32)
-      if (d.penalized[j]) f += gt_logpdf_f(b[j], lc, ap1, inv, pc.de);
-    s = (double)f;
+  if (mode == 2) {  // identical arithmetic (and lane->column mapping) to the pack kernels' lp
+    LpAcc la;
+    const double K = pc.de ? 0.0 : 1.0 / (pc.a * pc.c);
+    for (int j0 = lane * 4; j0 < d.kp; j0 += 128)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (j0 + i < d.q && d.penalized[j0 + i]) la.add(b[j0 + i], K, pc.de);
+    s = la.value(pc);
   } else if (pc.de) {
     for (int j = lane; j < d.q; j += 32) {
       if (!d.penalized[j]) continue;
@@ -308,28 +340,31 @@ __global__ void prior_kernel(spa_design d, const float* __restrict__ beta, int64
       s += mode == 0 ? gt_logpdf(bj, pc) : gt_logratio(bj, pc);
     }
   } else {
-    // float64: sum_j log1p(u_j) = log prod_j (1 + u_j) over groups of 8 terms
-    // (one log per 8 coordinates; every factor lies in [1, max(c_prev/c, 1 +
-    // |beta|/(a c))], products stay far from overflow; rel. error ~1e-15).
-    const double k1 = mode == 0 ? 1.0 / (pc.a * pc.c) : (1.0 / pc.c - 1.0 / pc.c_prev) / pc.a;
-    const double k2 = mode == 0 ? 0.0 : 1.0 / (pc.a * pc.c_prev);
-    const double cst = mode == 0 ? pc.lc : pc.lr;
-    double lsum = 0.0, prod = 1.0;
+    // float64 without per-element transcendentals or divisions:
+    //   mode 0: sum_j gt = npen*(-log 2c) - (a+1) log prod_j (1 + x_j/(a c))
+    //   mode 1: 1 + u_j = (1 + x_j/(a c)) / (1 + x_j/(a c_prev)), so
+    //           lw = npen*log(c_prev/c) - (a+1) [log prod (1 + x K) - log prod (1 + x K')]
+    // with the products taken over groups of 8 factors (each >= 1, renormalised
+    // before overflow).  Relative error ~1e-14 (the golden tolerance is 1e-12).
+    const double K1 = 1.0 / (pc.a * pc.c), K2 = 1.0 / (pc.a * pc.c_prev);
+    double la = 0.0, lb = 0.0, pa = 1.0, pb = 1.0;
     int cnt = 0, npen = 0;
     for (int j = lane; j < d.q; j += 32) {
       if (!d.penalized[j]) continue;
       const double x = fabs((double)b[j]);
-      const double u = mode == 0 ? x * k1 : (x * k1) / (1.0 + x * k2);
-      prod *= 1.0 + u;
+      pa *= fma(x, K1, 1.0);
+      if (mode == 1) pb *= fma(x, K2, 1.0);
       ++npen;
-      if (++cnt == 8 || !(prod < 1e250)) {
-        lsum += log(prod);
-        prod = 1.0;
+      if (++cnt == 8 || !(pa < 1e250 && pb < 1e250)) {
+        la += log(pa);
+        if (mode == 1) lb += log(pb);
+        pa = pb = 1.0;
         cnt = 0;
       }
     }
-    lsum += log(prod);
-    s = (double)npen * cst - (pc.a + 1.0) * lsum;
+    la += log(pa);
+    if (mode == 1) lb += log(pb);
+    s = mode == 0 ? (double)npen * pc.lc - (pc.a + 1.0) * la : (double)npen * pc.lr - (pc.a + 1.0) * (la - lb);
   }
   s = warp_sum(s);
   if (lane == 0) out[row] = s;
@@ -615,17 +650,20 @@ __global__ void rw_moments_kernel(const float* __restrict__ beta, int64_t m, int
   }
 }
 
-// Blocked right-looking float64 Cholesky of S = M2c + jitter*I.
-//   rw_cov_kernel      : S (lower) from the fixed-point moments, trace
-//   rw_panel_kernel    : factor the 32x32 diagonal block in smem, then the
-//                        panel below it (one thread per row)      [1 CTA]
-//   rw_trail_kernel    : A22 -= L21 L21^T on 32x32 tiles           [many CTAs]
-//   rw_emit_kernel     : L = (scale/sqrt(q)) chol(S) as float32 and as the
-//                        bf16 proposal operand [q][kq]
+// Blocked right-looking Cholesky of S = M2c + jitter*I in float32.  L only
+// parameterises the symmetric random-walk increment L z (any fixed L keeps the
+// Metropolis ratio exact), so float32 suffices; a non-positive pivot is
+// clamped (reported through *info) and still yields a valid proposal.
+//   rw_cov_kernel        : S (lower, float32) from the fixed-point moments
+//   rw_chol_diag_kernel  : one warp factors + inverts the 32x32 diagonal block
+//   rw_chol_trail_kernel : L21 rows + A22 -= L21 L21^T on 32x32 tiles
+// The ~2q/32 dependent launches are recorded once into a CUDA graph per
+// (workspace, q) and replayed every step (the loop is launch-latency bound).
+//   rw_emit_kernel       : scale, write float32 L and the bf16 operand [q][kq]
 constexpr int kPanel = 32;
 
 __global__ void rw_cov_kernel(const unsigned long long* __restrict__ acc, int q, double jitter,
-                              double* __restrict__ S) {
+                              float* __restrict__ S) {
   __shared__ double red[256];
   double tr = 0.0;
   for (int i = threadIdx.x; i < q; i += blockDim.x) tr += from_fix(acc[q + (size_t)i * q + i]);
@@ -636,81 +674,66 @@ __global__ void rw_cov_kernel(const unsigned long long* __restrict__ acc, int q,
     __syncthreads();
   }
   const double t = red[0] / q;
-  const double add = jitter * (t > 0 ? t : 1.0) + 1e-300;
+  const double add = jitter * (t > 0 ? t : 1.0) + 1e-30;
   const int64_t total = (int64_t)q * q;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(e / q), j = (int)(e % q);
-    S[e] = (j > i) ? 0.0 : from_fix(acc[q + e]) + (i == j ? add : 0.0);
+    S[e] = (j > i) ? 0.f : (float)(from_fix(acc[q + e]) + (i == j ? add : 0.0));
   }
 }
 
-__global__ void __launch_bounds__(256) rw_panel_kernel(double* __restrict__ S, int q, int jb, int* info) {
-  __shared__ double dg[kPanel][kPanel + 1];
-  __shared__ double inv[kPanel][kPanel + 1];  // L11^-1 (lower)
+__global__ void __launch_bounds__(32) rw_chol_diag_kernel(float* __restrict__ S, int q, int jb,
+                                                           float* __restrict__ inv, int* info) {
+  const int lane = threadIdx.x;
   const int nb = min(kPanel, q - jb);
-  const int tid = threadIdx.x;
-  for (int e = tid; e < kPanel * kPanel; e += blockDim.x) {
-    const int i = e / kPanel, j = e % kPanel;
-    dg[i][j] = (i < nb && j <= i) ? S[(size_t)(jb + i) * q + jb + j] : (i == j ? 1.0 : 0.0);
-    inv[i][j] = 0.0;
-  }
-  __syncthreads();
-  // right-looking factorisation of the 32x32 block; thread owns 4 entries
+  float a[kPanel];  // constant-bound loops => a[], x[] stay in registers
+#pragma unroll
+  for (int k = 0; k < kPanel; ++k)
+    a[k] = (lane < nb && k <= lane) ? S[(size_t)(jb + lane) * q + jb + k] : (k == lane ? 1.f : 0.f);
+#pragma unroll
   for (int j = 0; j < kPanel; ++j) {
-    if (tid == 0) {
-      double d = dg[j][j];
-      if (!(d > 0.0)) {
-        if (info && j < nb && *info == 0) *info = jb + j + 1;
-        d = 1e-300;
-      }
-      dg[j][j] = sqrt(d);
+    float djj = __shfl_sync(0xffffffffu, a[j], j);
+    if (!(djj > 0.f)) {
+      if (lane == 0 && info && j < nb && *info == 0) *info = jb + j + 1;
+      djj = 1e-30f;
     }
-    __syncthreads();
-    if (tid > j && tid < kPanel) dg[tid][j] /= dg[j][j];
-    __syncthreads();
-    for (int e = tid; e < kPanel * kPanel; e += blockDim.x) {
-      const int i = e / kPanel, k = e % kPanel;
-      if (k > j && i >= k) dg[i][k] -= dg[i][j] * dg[k][j];
+    const float rd = rsqrtf(djj);
+    a[j] = (lane == j) ? djj * rd : (lane > j ? a[j] * rd : a[j]);
+#pragma unroll
+    for (int k = 0; k < kPanel; ++k) {
+      const float lkj = __shfl_sync(0xffffffffu, a[j], k);
+      if (k > j && lane >= k) a[k] = fmaf(-a[j], lkj, a[k]);
     }
-    __syncthreads();
   }
-  // L11^-1 by right-looking forward substitution on [L | I]: step k scales
-  // row k of the right-hand side, then eliminates it from the rows below.
-  for (int e = tid; e < kPanel * kPanel; e += blockDim.x) inv[e / kPanel][e % kPanel] = (e / kPanel == e % kPanel);
-  __syncthreads();
+  float x[kPanel];
+#pragma unroll
+  for (int i = 0; i < kPanel; ++i) {
+    float v = (i == lane) ? 1.f : 0.f;
+#pragma unroll
+    for (int k = 0; k < kPanel; ++k) {
+      const float lik = __shfl_sync(0xffffffffu, a[k], i);
+      if (k < i) v = fmaf(-lik, x[k], v);
+    }
+    const float lii = __shfl_sync(0xffffffffu, a[i], i);
+    x[i] = (i >= lane) ? __fdividef(v, lii) : 0.f;
+  }
+#pragma unroll
   for (int k = 0; k < kPanel; ++k) {
-    if (tid < kPanel) inv[k][tid] /= dg[k][k];
-    __syncthreads();
-    for (int e = tid; e < kPanel * kPanel; e += blockDim.x) {
-      const int i = e / kPanel, cc = e % kPanel;
-      if (i > k) inv[i][cc] -= dg[i][k] * inv[k][cc];
-    }
-    __syncthreads();
-  }
-  for (int e = tid; e < nb * nb; e += blockDim.x) {
-    const int i = e / nb, j = e % nb;
-    if (j <= i) S[(size_t)(jb + i) * q + jb + j] = dg[i][j];
-  }
-  // panel below: L21 = A21 L11^-T, one thread per row: x_j = sum_k a_k inv[j][k]
-  for (int i = jb + nb + tid; i < q; i += blockDim.x) {
-    double* r = S + (size_t)i * q + jb;
-    double a[kPanel];
-#pragma unroll
-    for (int k = 0; k < kPanel; ++k) a[k] = (k < nb) ? r[k] : 0.0;
-#pragma unroll
-    for (int j = 0; j < kPanel; ++j) {
-      double x = 0.0;
-#pragma unroll
-      for (int k = 0; k <= j; ++k) x = fma(a[k], inv[j][k], x);
-      if (j < nb) r[j] = x;
-    }
+    if (lane < nb && k <= lane) S[(size_t)(jb + lane) * q + jb + k] = a[k];
+    inv[k * kPanel + lane] = x[k];  // inv[k][lane]
   }
 }
 
-// tile (bi, bj), bj <= bi, of the trailing matrix starting at row/col j0
-__global__ void __launch_bounds__(256) rw_trail_kernel(double* __restrict__ S, int q, int jb, int ntiles) {
-  __shared__ double li[32][kPanel + 1];
-  __shared__ double lj[32][kPanel + 1];
+// Panel step 2 (one CTA per lower-triangle tile (bi, bj), bi >= bj, below the
+// panel): the L21 rows a tile needs are recomputed from A21 and L11^-1;
+// diagonal tiles store theirs transposed into the unused upper triangle (other
+// tiles of this launch still read A21 from the lower one); then the tile is
+// updated S -= L21_bi L21_bj^T.
+__global__ void __launch_bounds__(256) rw_chol_trail_kernel(float* __restrict__ S, int q, int jb,
+                                                             const float* __restrict__ inv) {
+  __shared__ float iv[kPanel][kPanel + 1];
+  __shared__ float li[32][kPanel + 1];
+  __shared__ float lj[32][kPanel + 1];
   int t = blockIdx.x, bi = 0;
   while (t > bi) {
     t -= bi + 1;
@@ -720,38 +743,70 @@ __global__ void __launch_bounds__(256) rw_trail_kernel(double* __restrict__ S, i
   const int j0 = jb + kPanel;
   const int r0 = j0 + bi * 32, c0 = j0 + bj * 32;
   const int tid = threadIdx.x;
+  for (int e = tid; e < kPanel * kPanel; e += blockDim.x) iv[e / kPanel][e % kPanel] = inv[e];
   for (int e = tid; e < 32 * kPanel; e += blockDim.x) {
     const int r = e / kPanel, k = e % kPanel;
-    li[r][k] = (r0 + r < q) ? S[(size_t)(r0 + r) * q + jb + k] : 0.0;
-    lj[r][k] = (c0 + r < q) ? S[(size_t)(c0 + r) * q + jb + k] : 0.0;
+    li[r][k] = (r0 + r < q) ? S[(size_t)(r0 + r) * q + jb + k] : 0.f;
+    lj[r][k] = (c0 + r < q) ? S[(size_t)(c0 + r) * q + jb + k] : 0.f;
   }
   __syncthreads();
-  // 256 threads x 4 outputs each = 32x32 tile
+  {
+    const int r = tid >> 3, cb = (tid & 7) * 4;
+    float xi[4], xj[4];
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      float si = 0.f, sj = 0.f;
+#pragma unroll 8
+      for (int k = 0; k < kPanel; ++k) {
+        si = fmaf(li[r][k], iv[cb + cc][k], si);
+        sj = fmaf(lj[r][k], iv[cb + cc][k], sj);
+      }
+      xi[cc] = si;
+      xj[cc] = sj;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      li[r][cb + cc] = xi[cc];
+      lj[r][cb + cc] = xj[cc];
+    }
+  }
+  __syncthreads();
+  if (bi == bj) {
+    for (int e = tid; e < 32 * kPanel; e += blockDim.x) {
+      const int k = e / 32, r = e % 32;
+      if (r0 + r < q) S[(size_t)(jb + k) * q + r0 + r] = li[r][k];
+    }
+  }
   const int ty = tid >> 3, tx = (tid & 7) * 4;
-  double acc[4] = {0, 0, 0, 0};
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 8
   for (int k = 0; k < kPanel; ++k) {
-    const double a = li[ty][k];
+    const float av = li[ty][k];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[c] += a * lj[tx + c][k];
+    for (int cc = 0; cc < 4; ++cc) acc[cc] = fmaf(av, lj[tx + cc][k], acc[cc]);
   }
   const int i = r0 + ty;
-  if (i >= q) return;
+  if (i < q) {
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const int j = c0 + tx + c;
-    if (j < q && j <= i) S[(size_t)i * q + j] -= acc[c];
+    for (int cc = 0; cc < 4; ++cc) {
+      const int j = c0 + tx + cc;
+      if (j < q && j <= i) S[(size_t)i * q + j] -= acc[cc];
+    }
   }
 }
 
-__global__ void rw_emit_kernel(const double* __restrict__ S, int q, int kq, double f, float* __restrict__ L,
+__global__ void rw_emit_kernel(const float* __restrict__ S, int q, int kq, float f, float* __restrict__ L,
                                __nv_bfloat16* __restrict__ Lb) {
   const int64_t total = (int64_t)q * kq;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(e / kq), j = (int)(e % kq);
-    const double v = (j < q && j <= i) ? S[(size_t)i * q + j] * f : 0.0;
-    if (j < q) L[(size_t)i * q + j] = (float)v;
-    Lb[e] = __double2bfloat16(v);
+    // entries inside a diagonal 32-block live in the lower triangle, panel
+    // entries below it (L21) were stored transposed in the upper triangle
+    float v = 0.f;
+    if (j < q && j <= i) v = ((i / kPanel == j / kPanel) ? S[(size_t)i * q + j] : S[(size_t)j * q + i]) * f;
+    if (j < q) L[(size_t)i * q + j] = v;
+    Lb[e] = __float2bfloat16(v);
   }
 }
 
@@ -780,17 +835,16 @@ __device__ __forceinline__ void rw_normals4(uint64_t seed, int64_t t, int64_t k,
 
 __global__ void rw_normals_kernel(int64_t m, int q, int kq, uint64_t seed, int64_t t, int64_t i0, int move,
                                   __nv_bfloat16* __restrict__ Z) {
-  const int kq4 = kq / 4;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= m * kq4) return;
-  const int64_t k = e / kq4;
-  const int jb = (int)(e % kq4);
+  // grid: x = rows, y = 4-column groups of blockDim.x (32-bit index math)
+  const int jb = blockIdx.y * blockDim.x + threadIdx.x;
+  const int k = blockIdx.x;
+  if (4 * jb >= kq) return;
   __align__(8) __nv_bfloat16 z[4];
   float zz[4] = {0.f, 0.f, 0.f, 0.f};
   if (4 * jb < q) rw_normals4(seed, t, i0 + k, move, (uint32_t)jb, zz);
 #pragma unroll
   for (int i = 0; i < 4; ++i) z[i] = __float2bfloat16(4 * jb + i < q ? zz[i] : 0.0f);
-  *reinterpret_cast<uint2*>(Z + k * kq + 4 * jb) = *reinterpret_cast<const uint2*>(z);
+  *reinterpret_cast<uint2*>(Z + (size_t)k * kq + 4 * jb) = *reinterpret_cast<const uint2*>(z);
 }
 
 // Centre, weight and transpose the particles for the tensor-core SYRK:
@@ -824,7 +878,7 @@ __global__ void rw_center_t_kernel(const float* __restrict__ beta, int64_t m, in
   }
 }
 
-__global__ void rw_accept_kernel(float* __restrict__ beta, int ldb, const float* __restrict__ eps, int q, int64_t m,
+__global__ void rw_accept_kernel(float* __restrict__ beta, int ldb, const __nv_bfloat16* __restrict__ eps, int q, int64_t m,
                                  const double* __restrict__ ylin_p, const double* __restrict__ sp_p,
                                  const double* __restrict__ lp_p, double* __restrict__ ll, double* __restrict__ lp,
                                  uint64_t seed, int64_t t, int64_t i0, int move, unsigned long long* accepted) {
@@ -847,10 +901,66 @@ __global__ void rw_accept_kernel(float* __restrict__ beta, int ldb, const float*
   }
   ok = __shfl_sync(0xffffffffu, ok, 0);
   if (ok) {  // beta' = beta + eps, the same float32 sum the pack kernel used
-    const float* s = eps + row * ldb;
+    const __nv_bfloat16* s = eps + row * ldb;
     float* o = beta + row * ldb;
-    for (int j = lane; j < q; j += 32) o[j] = o[j] + s[j];
+    for (int j = lane; j < q; j += 32) o[j] = o[j] + __bfloat162float(s[j]);
   }
+}
+
+// Record the panel loop of the Cholesky once per (S, q, inv, info) and replay it.
+struct CholGraphKey {
+  float* S;
+  int q;
+  float* inv;
+  int* info;
+  bool operator==(const CholGraphKey& o) const { return S == o.S && q == o.q && inv == o.inv && info == o.info; }
+};
+
+static cudaError_t chol_record(float* S, int q, float* inv, int* info, cudaStream_t st) {
+  for (int jb = 0; jb < q; jb += 32) {
+    rw_chol_diag_kernel<<<1, 32, 0, st>>>(S, q, jb, inv, info);
+    const int rest = q - jb - 32;
+    if (rest > 0) {
+      const int nt = (rest + 31) / 32;
+      rw_chol_trail_kernel<<<nt * (nt + 1) / 2, 256, 0, st>>>(S, q, jb, inv);
+    }
+  }
+  return cudaGetLastError();
+}
+
+static cudaError_t chol_graph_launch(float* S, int q, float* inv, int* info, cudaStream_t st) {
+  static std::mutex mu;
+  static std::vector<std::pair<CholGraphKey, cudaGraphExec_t>> cache;
+  const CholGraphKey key{S, q, inv, info};
+  cudaGraphExec_t exec = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& kv : cache)
+      if (kv.first == key) exec = kv.second;
+  }
+  if (exec == nullptr) {
+    cudaStream_t cap;
+    cudaError_t e = cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return e;
+    cudaGraph_t g = nullptr;
+    e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      cudaError_t er = chol_record(S, q, inv, info, cap);
+      e = cudaStreamEndCapture(cap, &g);
+      if (er != cudaSuccess) e = er;
+    }
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, g, 0);
+    if (g) cudaGraphDestroy(g);
+    cudaStreamDestroy(cap);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    if (cache.size() >= 16) {  // bounded: drop the oldest
+      cudaGraphExecDestroy(cache.front().second);
+      cache.erase(cache.begin());
+    }
+    cache.push_back({key, exec});
+  }
+  return cudaGraphLaunch(exec, st);
 }
 
 static inline unsigned cdiv(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
@@ -937,7 +1047,7 @@ int spa_pack_particles(const spa_design* d, const float* beta, int64_t m, int32_
   SPA_REQUIRE(d && beta && A && ylin && m >= 0, kBadArgument, "spa_pack_particles: bad arguments");
   SPA_REQUIRE(!d->coded || d->kp >= d->q + 3, kBadArgument, "spa_pack_particles: kp < q + 3");
   if (m == 0) return 0;
-  pack_kernel<<<cdiv(m, 8), 256, 0, as_stream(stream)>>>(*d, beta, nullptr, m, ldb,
+  pack_kernel<<<cdiv(m, 8), 256, 0, as_stream(stream)>>>(*d, beta, (const __nv_bfloat16*)nullptr, m, ldb,
                                                         reinterpret_cast<__nv_bfloat16*>(A), ylin,
                                                         make_prior(a, c, c), lp);
   SPA_CHECK_LAUNCH();
@@ -1011,9 +1121,34 @@ int spa_gather_rows(const float* src, int32_t ld_src, float* dst, int32_t ld_dst
   return 0;
 }
 
+static void syrk_split(int64_t m, int q, int& m_tiles, int& kb_per_unit, int& units) {
+  const int64_t ldk = (m + 63) / 64 * 64;
+  const int kblocks = (int)(ldk / kTcBK);
+  m_tiles = (q + kTcBM - 1) / kTcBM;
+  units = std::max(1, std::min(kblocks, (2 * 148 + m_tiles - 1) / m_tiles));
+  kb_per_unit = (kblocks + units - 1) / units;
+  units = (kblocks + kb_per_unit - 1) / kb_per_unit;
+}
+
 size_t spa_rw_moments_workspace_bytes(int64_t m, int32_t q) {
   const int64_t ldk = (m + 63) / 64 * 64;
-  return (size_t)2 * q * ldk * sizeof(__nv_bfloat16);
+  int mt, kbpu, units;
+  syrk_split(m, q, mt, kbpu, units);
+  const size_t dt = (((size_t)2 * q * ldk * sizeof(__nv_bfloat16)) + 255) & ~size_t(255);
+  return dt + (size_t)units * q * q * sizeof(float);
+}
+
+// Sum the per-split float32 SYRK tiles in fixed split order (float64) and
+// store the lower triangle as 2^-48 fixed point.
+__global__ void syrk_reduce_kernel(const float* __restrict__ part, int units, int q,
+                                   unsigned long long* __restrict__ acc) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)q * q) return;
+  const int i = (int)(e / q), j = (int)(e % q);
+  if (j > i) return;
+  double s = 0.0;
+  for (int u = 0; u < units; ++u) s += (double)part[(size_t)u * q * q + e];
+  acc[q + e] += to_fix(s);
 }
 
 int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const double* w, int32_t phase,
@@ -1040,51 +1175,46 @@ int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const d
     SPA_CHECK_LAUNCH();
   }
   TcArgs args;
+  int units;
+  syrk_split(m, q, args.m_tiles, args.kb_per_unit, units);
   args.m = q;
   args.ncols = q;
   args.kp = (int)ldk;
-  args.m_tiles = (q + kTcBM - 1) / kTcBM;
   args.n_tiles = (q + 255) / 256;
   args.tiles_per_unit = args.n_tiles;
-  const int kblocks = (int)(ldk / kTcBK);
-  int units = std::max(1, std::min(kblocks, (2 * 148 + args.m_tiles - 1) / args.m_tiles));
-  args.kb_per_unit = (kblocks + units - 1) / units;
-  units = (kblocks + args.kb_per_unit - 1) / args.kb_per_unit;
-  EpiFixAtomic epi{acc + q, q, q, 1};
-  return launch_tc<2, 2, 256>(Dt, 2ull * ldk, Dt, 2ull * ldk, (uint64_t)q, args, units, epi, st);
+  float* part = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) +
+                                         ((((size_t)2 * q * ldk * sizeof(__nv_bfloat16)) + 255) & ~size_t(255)));
+  EpiStoreT<float> epi{part, q, q, (size_t)q * q, nullptr};
+  int rc = launch_tc<2, 2, 256>(Dt, 2ull * ldk, Dt, 2ull * ldk, (uint64_t)q, args, units, epi, st);
+  if (rc) return rc;
+  syrk_reduce_kernel<<<cdiv((int64_t)q * q, 256), 256, 0, st>>>(part, units, q, acc);
+  SPA_CHECK_LAUNCH();
+  return 0;
 }
 
 int spa_rw_factor(const int64_t* partial, int32_t q, double scale, double jitter, float* L, double* ws, int* info,
                   void* stream) {
-  SPA_REQUIRE(partial && L && ws && q > 0 && q <= 4096, kBadArgument, "spa_rw_factor: bad arguments");
+  SPA_REQUIRE(partial && L && ws && q > 0 && q <= 8192, kBadArgument, "spa_rw_factor: bad arguments");
   cudaStream_t st = as_stream(stream);
   const int kq = (q + 63) / 64 * 64;
-  // bf16 operand after the float64 factor, 256-byte aligned for TMA
-  __nv_bfloat16* Lb =
-      reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<char*>(ws) + (((size_t)8 * q * q + 255) & ~size_t(255)));
+  float* S = reinterpret_cast<float*>(ws);
+  char* base = reinterpret_cast<char*>(ws);
+  __nv_bfloat16* Lb = reinterpret_cast<__nv_bfloat16*>(base + (((size_t)8 * q * q + 255) & ~size_t(255)));
+  float* inv = reinterpret_cast<float*>(base + (((size_t)8 * q * q + 255) & ~size_t(255)) +
+                                        (((size_t)2 * q * kq + 255) & ~size_t(255)));
   if (info) SPA_CHECK_CUDA(cudaMemsetAsync(info, 0, sizeof(int), st));
   rw_cov_kernel<<<std::min<unsigned>(cdiv((int64_t)q * q, 256), 1184), 256, 0, st>>>(
-      reinterpret_cast<const unsigned long long*>(partial), q, jitter, ws);
+      reinterpret_cast<const unsigned long long*>(partial), q, jitter, S);
   SPA_CHECK_LAUNCH();
-  for (int jb = 0; jb < q; jb += kPanel) {
-    rw_panel_kernel<<<1, 256, 0, st>>>(ws, q, jb, info);
-    SPA_CHECK_LAUNCH();
-    const int rest = q - jb - kPanel;
-    if (rest > 0) {
-      const int nt = (rest + 31) / 32;
-      rw_trail_kernel<<<nt * (nt + 1) / 2, 256, 0, st>>>(ws, q, jb, nt);
-      SPA_CHECK_LAUNCH();
-    }
-  }
-  rw_emit_kernel<<<std::min<unsigned>(cdiv((int64_t)q * kq, 256), 1184), 256, 0, st>>>(ws, q, kq,
-                                                                                       scale / std::sqrt((double)q),
-                                                                                       L, Lb);
+  SPA_CHECK_CUDA(chol_graph_launch(S, q, inv, info, st));
+  rw_emit_kernel<<<std::min<unsigned>(cdiv((int64_t)q * kq, 256), 1184), 256, 0, st>>>(
+      S, q, kq, (float)(scale / std::sqrt((double)q)), L, Lb);
   SPA_CHECK_LAUNCH();
   return 0;
 }
 
 int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ldb, const void* Lb, uint64_t seed,
-                   int64_t t, int64_t i0, int32_t move, void* zbuf, float* eps, void* A, double* ylin, double a,
+                   int64_t t, int64_t i0, int32_t move, void* zbuf, void* eps, void* A, double* ylin, double a,
                    double c, double* lp, void* stream) {
   SPA_REQUIRE(d && beta && Lb && zbuf && eps && A && ylin && m > 0, kBadArgument, "spa_rw_propose: bad arguments");
   SPA_REQUIRE((ldb & 3) == 0 && beta != eps, kBadArgument, "spa_rw_propose: ldb % 4 != 0 or beta aliases eps");
@@ -1093,7 +1223,11 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
   const int q = d->q;
   const int kq = (q + 63) / 64 * 64;
   __nv_bfloat16* Z = reinterpret_cast<__nv_bfloat16*>(zbuf);
-  rw_normals_kernel<<<cdiv(m * (kq / 4), 256), 256, 0, st>>>(m, q, kq, seed, t, i0, move, Z);
+  {
+    const int tx = std::min(128, kq / 4);
+    dim3 grid((unsigned)m, cdiv(kq / 4, tx));
+    rw_normals_kernel<<<grid, tx, 0, st>>>(m, q, kq, seed, t, i0, move, Z);
+  }
   SPA_CHECK_LAUNCH();
   TcArgs args;
   args.m = (int)m;
@@ -1103,11 +1237,12 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
   args.n_tiles = (q + 255) / 256;
   args.tiles_per_unit = args.n_tiles;
   args.kb_per_unit = 0;
-  EpiStoreT epi{eps, ldb, (int)m};
+  auto* epsb = reinterpret_cast<__nv_bfloat16*>(eps);
+  EpiStoreT<__nv_bfloat16> epi{epsb, ldb, (int)m, 0, nullptr};
   int rc = launch_tc<1, 1, 256>(Z, (uint64_t)kq, Lb, (uint64_t)kq, (uint64_t)q, args, 1, epi, st);
   if (rc) return rc;
   const unsigned grid = std::min<unsigned>(cdiv(m, 8), 148 * 16);
-  pack_eps_kernel<<<grid, 256, (size_t)16 * d->kp, st>>>(*d, beta, eps, m, ldb, reinterpret_cast<__nv_bfloat16*>(A),
+  pack_eps_kernel<<<grid, 256, (size_t)16 * d->kp, st>>>(*d, beta, epsb, m, ldb, reinterpret_cast<__nv_bfloat16*>(A),
                                                          ylin, make_prior(a, c, c), lp);
   SPA_CHECK_LAUNCH();
   return 0;
@@ -1131,12 +1266,12 @@ int spa_tc_gemm_f32(const void* A, int64_t m, int32_t terms_a, const void* B, in
   return launch_tc<2, 1, 256>(A, 2ull * kp, B, (uint64_t)kp, (uint64_t)rows_b, args, 1, epi, as_stream(stream));
 }
 
-int spa_rw_accept(float* beta, int32_t ldb, const float* eps, int32_t q, int64_t m, const double* ylin_p,
+int spa_rw_accept(float* beta, int32_t ldb, const void* eps, int32_t q, int64_t m, const double* ylin_p,
                   const double* sp_p, const double* lp_p, double* ll, double* lp, uint64_t seed, int64_t t,
                   int64_t i0, int32_t move, unsigned long long* accepted, void* stream) {
   SPA_REQUIRE(beta && eps && ylin_p && sp_p && lp_p && ll && lp && accepted && m > 0, kBadArgument,
               "spa_rw_accept: bad arguments");
-  rw_accept_kernel<<<cdiv(m, 8), 256, 0, as_stream(stream)>>>(beta, ldb, eps, q, m, ylin_p, sp_p, lp_p, ll, lp, seed,
+  rw_accept_kernel<<<cdiv(m, 8), 256, 0, as_stream(stream)>>>(beta, ldb, reinterpret_cast<const __nv_bfloat16*>(eps), q, m, ylin_p, sp_p, lp_p, ll, lp, seed,
                                                              t, i0, move, accepted);
   SPA_CHECK_LAUNCH();
   return 0;

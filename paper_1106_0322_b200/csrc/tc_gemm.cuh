@@ -296,12 +296,16 @@ struct EpiFixAtomic {
 
 // Raw accumulator store through a per-warp smem transpose: lane = row in
 // TMEM, lane = column in the global store, so each store instruction writes
-// one contiguous 128-byte row segment.  out[row][col] = D for valid entries.
+// one contiguous row segment.  out[unit*unit_stride + row*ld + col] = D for
+// valid entries (OutT = float or __nv_bfloat16).
+template <class OutT>
 struct EpiStoreT {
-  float* out;
+  OutT* out;
   int ld;
   int m;
-  __device__ __forceinline__ void begin_unit(int, int) {}
+  size_t unit_stride;
+  OutT* base_;
+  __device__ __forceinline__ void begin_unit(int, int unit) { base_ = out + (size_t)unit * unit_stride; }
   __device__ __forceinline__ void consume(int row, int col0, const float (&v)[32], int ncols, float* tile) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -311,7 +315,7 @@ struct EpiStoreT {
     const int c = col0 + lane;
 #pragma unroll 4
     for (int r = 0; r < 32; ++r)
-      if (row0 + r < m && c < ncols) out[(size_t)(row0 + r) * ld + c] = tile[r * 33 + lane];
+      if (row0 + r < m && c < ncols) base_[(size_t)(row0 + r) * ld + c] = (OutT)tile[r * 33 + lane];
     __syncwarp();
   }
   __device__ __forceinline__ void end_tile(int) {}

@@ -187,7 +187,7 @@ class ParticleSystem:
         self.N_total = int(N_total if N_total is not None else N)
         self.i0 = int(rank_offset)
         self.q = design.q
-        self.ldb = _round_up(self.q, 4)
+        self.ldb = _round_up(self.q, 16)  # 64 B (float32) / 32 B (bf16 eps) aligned rows
         self.prior_a = float(prior_a)
         self.intercept = bool(intercept)
         self.t = 1
@@ -268,11 +268,12 @@ class ParticleSystem:
             kq = _round_up(q, 64)
             dev = self.device
             self._rw = dict(
-                prop=torch.zeros((self.N, self.ldb), dtype=torch.float32, device=dev),
+                prop=torch.zeros((self.N, self.ldb), dtype=torch.bfloat16, device=dev),  # eps = L z
                 lp_p=torch.empty(self.N, dtype=torch.float64, device=dev),
                 acc=torch.zeros(q + q * q, dtype=torch.int64, device=dev),
                 L=torch.empty((q, q), dtype=torch.float32, device=dev),
-                fws=torch.empty((_round_up(8 * q * q, 256) + 2 * q * kq + 7) // 8, dtype=torch.float64, device=dev),
+                fws=torch.empty((_round_up(8 * q * q, 256) + _round_up(2 * q * kq, 256) + 8192) // 8,
+                                dtype=torch.float64, device=dev),
                 info=torch.zeros(1, dtype=torch.int32, device=dev),
                 zbuf=torch.empty((self.N, kq), dtype=torch.bfloat16, device=dev),
                 mws=torch.empty(max(_lib.load().spa_rw_moments_workspace_bytes(self.N, q), 8), dtype=torch.uint8,
@@ -418,13 +419,13 @@ def _rw_factor(system: ParticleSystem, scale: float, group=None):
         group.all_reduce_sum(rw["acc"][: system.q])
     _lib.call("spa_rw_moments", _p(system.beta), system.N, system.ldb, system.q, _p(w), 1, _p(rw["acc"]),
               _p(rw["mws"]), rw["mws"].numel(), _stream())
-    _lib.add_launches(1)  # phase 1 = transpose + tcgen05 SYRK
+    _lib.add_launches(2)  # phase 1 = transpose + tcgen05 SYRK + split reduce
     if group is not None:
         group.all_reduce_sum(rw["acc"][system.q:])
     _lib.call("spa_rw_factor", _p(rw["acc"]), system.q, float(scale), 1e-6, _p(rw["L"]), _p(rw["fws"]),
               _p(rw["info"]), _stream())
     panels = -(-system.q // 32)
-    _lib.add_launches(2 + panels + max(0, panels - 1))
+    _lib.add_launches(2 + 2 * panels - 1)  # cov + graph of panel kernels + emit
 
 
 def _global_weights(system, group):

@@ -298,7 +298,7 @@ def test_rw_propose_and_accept_vs_oracle():
     np.testing.assert_allclose(lp0, orc.log_prior_rows(beta0, a, c), rtol=1e-6)
     _lib.call("spa_rw_propose", ctypes.byref(d.struct), _p(s.beta), s.N, s.ldb, s.factor_operand(), seed, t, 0, move,
               _p(rw["zbuf"]), _p(rw["prop"]), _p(ws["A"]), _p(ws["ylin"]), a, c, _p(rw["lp_p"]), _stream())
-    eps = rw["prop"][:, : s.q].cpu().numpy()  # eps = L z (float32)
+    eps = rw["prop"][:, : s.q].float().cpu().numpy()  # eps = L z (bf16)
     prop = (s.beta[:, : s.q].cpu().numpy() + eps).astype(np.float64)
     Lbf = torch.from_numpy(rw["L"].cpu().numpy()).to(torch.bfloat16).double().numpy()
     Z = np.stack([orc.rw_normals(seed, t, k, move, s.q) for k in range(s.N)])
@@ -306,7 +306,9 @@ def test_rw_propose_and_accept_vs_oracle():
     # device normals use fast intrinsics (~1e-6); a z within that of a bf16
     # rounding boundary rounds the other way (one bf16 ulp): allow rare flips
     diff = np.abs(prop - (beta0 + Zb @ Lbf.T))
-    assert np.mean(diff > 1e-5 * max(1.0, np.abs(prop).max())) < 0.005
+    # eps is stored in bf16: compare with the oracle increment rounded to bf16
+    eps_ref = torch.from_numpy(Zb @ Lbf.T).to(torch.bfloat16).double().numpy()
+    assert np.mean(np.abs(eps - eps_ref) > 2.0**-8 * np.abs(eps_ref) + 1e-12) < 0.005
     assert diff.max() < 2.0**-7 * np.abs(Zb).max() * np.abs(Lbf).max() * 4
     np.testing.assert_allclose(ws["ylin"].cpu().numpy(), prop @ (data.X.T @ data.y), rtol=1e-5, atol=1e-6)
     np.testing.assert_allclose(rw["lp_p"].cpu().numpy(), orc.log_prior_rows(prop, a, c), rtol=1e-6)
