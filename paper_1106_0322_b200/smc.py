@@ -547,24 +547,17 @@ def smc_step(system: ParticleSystem, data, schedule: Schedule, t: int, config: S
 
 
 def _snapshot(system: ParticleSystem, record: StepRecord, group=None):
-    """Copy the retained arrays out in the reference layout (float64 NumPy).
-    The float32 -> float64 widening runs on the device and lands in pinned
-    host memory (one D2H per array)."""
+    """Copy the retained arrays out in the reference layout (float64 NumPy);
+    the float32 -> float64 widening runs on the device."""
     w = system.device_weights() if group is None else _global_weights(system, group)
     beta = system.beta[:, : system.q]
     ll = system.ll
     if group is not None:
         w, beta, ll = group.gather_to_all(w), group.gather_to_all(beta.contiguous()), group.gather_to_all(ll)
-    out = []
-    for t in (w, beta.double(), ll):
-        h = torch.empty(t.shape, dtype=torch.float64, pin_memory=True)
-        h.copy_(t, non_blocking=True)
-        out.append(h)
-    torch.cuda.current_stream().synchronize()
-    record.weights = out[0].numpy()
+    record.weights = w.cpu().numpy().copy()
     record.weights /= record.weights.sum()
-    record.particles = out[1].numpy()
-    record.logliks = out[2].numpy()
+    record.particles = beta.double().cpu().numpy()
+    record.logliks = ll.cpu().numpy().copy()
     return record
 
 
