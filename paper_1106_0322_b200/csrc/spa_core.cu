@@ -74,7 +74,15 @@ static int launch_tc(const void* A, uint64_t a_cols, const void* B, uint64_t b_c
     SPA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kSmemBytes));
     attr_done = true;
   }
-  const int grid = args.m_tiles * units;
+  args.units = units;
+  // persistent: one CTA per SM (the ring uses ~200 KB of smem) over all items
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    SPA_CHECK_CUDA(cudaGetDevice(&dev));
+    SPA_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int grid = std::min(args.m_tiles * units, sms);
   kern<<<grid, kTcThreads, S::kSmemBytes, st>>>(ta, tb, args, epi);
   SPA_CHECK_LAUNCH();
   return 0;
@@ -967,11 +975,13 @@ static inline unsigned cdiv(int64_t a, int64_t b) { return (unsigned)((a + b - 1
 
 // Likelihood work split: units of BN tiles so the grid covers several waves.
 static void loglik_split(int64_t m, int n, int& m_tiles, int& n_tiles, int& tpu, int& units) {
+  // persistent kernel: items = (particle tile, subject-tile group); groups of
+  // ~4 subject tiles keep the partial-sum traffic small while leaving enough
+  // items (>= ~8 per SM) to balance the tail
   m_tiles = (int)((m + kTcBM - 1) / kTcBM);
   n_tiles = (n + 255) / 256;
-  int want = (8 * 148 + m_tiles - 1) / m_tiles;
-  units = std::max(1, std::min(n_tiles, want));
-  tpu = (n_tiles + units - 1) / units;
+  tpu = std::max(1, std::min(n_tiles, 4));
+  while (tpu > 1 && (int64_t)m_tiles * ((n_tiles + tpu - 1) / tpu) < 8 * 148) --tpu;
   units = (n_tiles + tpu - 1) / tpu;
 }
 

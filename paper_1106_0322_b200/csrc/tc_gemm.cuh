@@ -49,6 +49,7 @@ struct TcArgs {
   int n_tiles;         // ceil(ncols / BN)
   int tiles_per_unit;  // BN tiles per CTA (column split), or
   int kb_per_unit;     // > 0: split-K -- a CTA covers all BN tiles over this many k-blocks
+  int units;           // column (or K) units per A tile; work items = m_tiles * units
 };
 
 // Epilogue contract:
@@ -73,23 +74,28 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  // units of the same A tile are adjacent in the grid, so they run together
-  // and share the A tile in L2 (one DRAM read of A per launch)
-  const int units = gridDim.x / args.m_tiles;
-  const int unit = blockIdx.x % units;
-  const int mt = blockIdx.x / units;
-  int nt0, nt1, kb0, kb1;
-  if (args.kb_per_unit > 0) {
-    nt0 = 0;
-    nt1 = args.n_tiles;
-    kb0 = unit * args.kb_per_unit;
-    kb1 = min(args.kp / kTcBK, kb0 + args.kb_per_unit);
-  } else {
-    nt0 = unit * args.tiles_per_unit;
-    nt1 = min(args.n_tiles, nt0 + args.tiles_per_unit);
-    kb0 = 0;
-    kb1 = args.kp / kTcBK;
-  }
+  // Persistent: CTA b processes work items b, b + gridDim.x, ... where item
+  // w = (mt = w / units, unit = w % units); consecutive items share the A
+  // tile, and CTAs running concurrently hold consecutive items, so each A
+  // tile is read from DRAM once and re-used from L2.  The smem and TMEM
+  // pipelines (stage / accumulator phases) run on across items.
+  const int units = args.units;
+  const int items = args.m_tiles * units;
+  auto item_range = [&](int w, int& mt, int& unit, int& nt0, int& nt1, int& kb0, int& kb1) {
+    mt = w / units;
+    unit = w % units;
+    if (args.kb_per_unit > 0) {
+      nt0 = 0;
+      nt1 = args.n_tiles;
+      kb0 = unit * args.kb_per_unit;
+      kb1 = min(args.kp / kTcBK, kb0 + args.kb_per_unit);
+    } else {
+      nt0 = unit * args.tiles_per_unit;
+      nt1 = min(args.n_tiles, nt0 + args.tiles_per_unit);
+      kb0 = 0;
+      kb1 = args.kp / kTcBK;
+    }
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S::kStages; ++s) {
@@ -115,6 +121,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       prefetch_tmap(&tmb);
       int s = 0;
       uint32_t ph = 0;
+      for (int w = blockIdx.x; w < items; w += gridDim.x) {
+      int mt, unit, nt0, nt1, kb0, kb1;
+      item_range(w, mt, unit, nt0, nt1, kb0, kb1);
       for (int nt = nt0; nt < nt1; ++nt) {
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
@@ -133,6 +142,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
         }
       }
+      }
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -141,6 +151,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
+      for (int w = blockIdx.x; w < items; w += gridDim.x) {
+      int mt, unit, nt0, nt1, kb0, kb1;
+      item_range(w, mt, unit, nt0, nt1, kb0, kb1);
       for (int nt = nt0; nt < nt1; ++nt, ++it) {
         const int buf = it & 1;
         const uint32_t bph = (it >> 1) & 1;
@@ -170,14 +183,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         tc_commit(&tfull[buf]);  // accumulator ready for the epilogue
       }
+      }
     }
   } else {
     // ---------------- epilogue (warps 2..5) ----------------
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-    const int row = mt * kTcBM + quarter * 32 + lane;
     float* scratch = reinterpret_cast<float*>(smem + S::kStages * S::kStageBytes + 256) + (warp - 2) * 32 * 33;
-    epi.begin_unit(row, unit);
     int it = 0;
+    for (int w = blockIdx.x; w < items; w += gridDim.x) {
+    int mt, unit, nt0, nt1, kb0, kb1;
+    item_range(w, mt, unit, nt0, nt1, kb0, kb1);
+    (void)kb0;
+    (void)kb1;
+    const int row = mt * kTcBM + quarter * 32 + lane;
+    epi.begin_unit(row, unit);
     for (int nt = nt0; nt < nt1; ++nt, ++it) {
       const int buf = it & 1;
       const uint32_t bph = (it >> 1) & 1;
@@ -200,6 +219,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       epi.end_tile(row);
     }
     epi.end_unit(row, unit, args.m);
+    }
   }
 
   __syncthreads();
