@@ -241,7 +241,10 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const 
 
 // Proposal pack (spa_rw_propose): same arithmetic as pack_kernel, but each
 // block stages the per-column constants (alpha, X^T y, gamma as float32, the
-// penalty flag) in shared memory once and its warps walk many rows.
+// penalty flag) in shared memory once and its warps walk many rows; all of a
+// row's vector loads are issued before any arithmetic (IT = kp/128 groups of
+// 4 columns per lane) so every lane keeps IT x 24 bytes in flight.
+template <int IT>
 __global__ void __launch_bounds__(256) pack_eps_kernel(spa_design d, const float* __restrict__ beta,
                                                        const __nv_bfloat16* __restrict__ eps, int64_t m, int ldb,
                                                        __nv_bfloat16* __restrict__ A, double* __restrict__ ylin,
@@ -263,25 +266,37 @@ __global__ void __launch_bounds__(256) pack_eps_kernel(spa_design d, const float
   const int64_t warp0 = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const double K = pc.de ? 0.0 : 1.0 / (pc.a * pc.c);
+  const bool full = (d.q % 4 == 0);  // every 4-column group is either all-valid or all-padding
   for (int64_t row = warp0; row < m; row += nwarps) {
     const float* b = beta + row * ldb;
     const __nv_bfloat16* e = eps + row * ldb;
     __nv_bfloat16* ah = A + row * (2 * (int64_t)d.kp);
     __nv_bfloat16* al = ah + d.kp;
+    float4 xv[IT];
+    uint2 ev[IT];
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int j0 = it * 128 + lane * 4;
+      if (full && j0 + 4 <= d.q) {
+        xv[it] = __ldcs(reinterpret_cast<const float4*>(b + j0));
+        ev[it] = __ldcs(reinterpret_cast<const uint2*>(e + j0));
+      }
+    }
     double yl = 0.0, off = 0.0;  // same grouping as pack_kernel => identical sums
     LpAcc la;
-    for (int j0 = lane * 4; j0 < d.kp; j0 += 128) {
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int j0 = it * 128 + lane * 4;
+      if (j0 >= d.kp) break;
       float fy = 0.f, fo = 0.f;
       float p[4] = {0.f, 0.f, 0.f, 0.f};
-      if (j0 + 4 <= d.q) {
-        const float4 x = *reinterpret_cast<const float4*>(b + j0);
-        const uint2 yv = *reinterpret_cast<const uint2*>(e + j0);
-        const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&yv);
+      if (full && j0 + 4 <= d.q) {
+        const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&ev[it]);
         const float2 ya = __bfloat1622float2(y2[0]), yb = __bfloat1622float2(y2[1]);
-        p[0] = x.x + ya.x;
-        p[1] = x.y + ya.y;
-        p[2] = x.z + yb.x;
-        p[3] = x.w + yb.y;
+        p[0] = xv[it].x + ya.x;
+        p[1] = xv[it].y + ya.y;
+        p[2] = xv[it].z + yb.x;
+        p[3] = xv[it].w + yb.y;
       } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -305,8 +320,8 @@ __global__ void __launch_bounds__(256) pack_eps_kernel(spa_design d, const float
       }
       yl += fy;
       off += fo;
-      *reinterpret_cast<uint2*>(ah + j0) = *reinterpret_cast<const uint2*>(h);
-      *reinterpret_cast<uint2*>(al + j0) = *reinterpret_cast<const uint2*>(l);
+      __stcs(reinterpret_cast<uint2*>(ah + j0), *reinterpret_cast<const uint2*>(h));
+      __stcs(reinterpret_cast<uint2*>(al + j0), *reinterpret_cast<const uint2*>(l));
     }
     yl = warp_sum(yl);
     off = warp_sum(off);
@@ -352,18 +367,34 @@ __global__ void prior_kernel(spa_design d, const float* __restrict__ beta, int64
     //   mode 0: sum_j gt = npen*(-log 2c) - (a+1) log prod_j (1 + x_j/(a c))
     //   mode 1: 1 + u_j = (1 + x_j/(a c)) / (1 + x_j/(a c_prev)), so
     //           lw = npen*log(c_prev/c) - (a+1) [log prod (1 + x K) - log prod (1 + x K')]
-    // with the products taken over groups of 8 factors (each >= 1, renormalised
-    // before overflow).  Relative error ~1e-14 (the golden tolerance is 1e-12).
+    // Lanes own 4 consecutive columns (float4 loads); each lane's product is
+    // flushed into a log every 8 factors.  Relative error ~1e-14.
     const double K1 = 1.0 / (pc.a * pc.c), K2 = 1.0 / (pc.a * pc.c_prev);
     double la = 0.0, lb = 0.0, pa = 1.0, pb = 1.0;
     int cnt = 0, npen = 0;
-    for (int j = lane; j < d.q; j += 32) {
-      if (!d.penalized[j]) continue;
-      const double x = fabs((double)b[j]);
-      pa *= fma(x, K1, 1.0);
-      if (mode == 1) pb *= fma(x, K2, 1.0);
-      ++npen;
-      if (++cnt == 8 || !(pa < 1e250 && pb < 1e250)) {
+    const bool vec = (d.q % 4 == 0) && (ldb % 4 == 0);
+    for (int j0 = lane * 4; j0 < d.q; j0 += 128) {
+      float xv[4];
+      if (vec) {
+        const float4 x = __ldcs(reinterpret_cast<const float4*>(b + j0));
+        xv[0] = x.x;
+        xv[1] = x.y;
+        xv[2] = x.z;
+        xv[3] = x.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) xv[i] = (j0 + i < d.q) ? b[j0 + i] : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (j0 + i >= d.q || !d.penalized[j0 + i]) continue;
+        const double x = fabs((double)xv[i]);
+        pa *= fma(x, K1, 1.0);
+        if (mode == 1) pb *= fma(x, K2, 1.0);
+        ++npen;
+        ++cnt;
+      }
+      if (cnt >= 8 || !(pa < 1e250 && pb < 1e250)) {
         la += log(pa);
         if (mode == 1) lb += log(pb);
         pa = pb = 1.0;
@@ -594,9 +625,18 @@ __global__ void rw_mean_kernel(const float* __restrict__ beta, int64_t m, int ld
   if (j >= q) return;
   const int64_t k0 = (int64_t)blockIdx.y * 256;
   const int64_t k1 = min(m, k0 + 256);
-  double s = 0.0;
-  for (int64_t k = k0; k < k1; ++k) s += w[k] * (double)beta[k * ldb + j];
-  atomicAdd(&acc[j], to_fix(s));
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int64_t k = k0;
+  for (; k + 4 <= k1; k += 4) {  // 4 independent rows in flight per thread
+    const float b0 = beta[k * ldb + j], b1 = beta[(k + 1) * ldb + j];
+    const float b2 = beta[(k + 2) * ldb + j], b3 = beta[(k + 3) * ldb + j];
+    s0 += w[k] * (double)b0;
+    s1 += w[k + 1] * (double)b1;
+    s2 += w[k + 2] * (double)b2;
+    s3 += w[k + 3] * (double)b3;
+  }
+  for (; k < k1; ++k) s0 += w[k] * (double)beta[k * ldb + j];
+  atomicAdd(&acc[j], to_fix((s0 + s1) + (s2 + s3)));
 }
 
 __global__ void rw_moments_kernel(const float* __restrict__ beta, int64_t m, int ldb, int q,
@@ -861,35 +901,46 @@ __global__ void rw_normals_kernel(int64_t m, int q, int kq, uint64_t seed, int64
 __global__ void rw_center_t_kernel(const float* __restrict__ beta, int64_t m, int ldb, int q,
                                    const double* __restrict__ w, const unsigned long long* __restrict__ acc,
                                    __nv_bfloat16* __restrict__ Dt, int64_t ldk) {
-  __shared__ float tile[32][33];
-  __shared__ float sw[32], mu[32];
-  const int64_t k0 = (int64_t)blockIdx.x * 32;
+  // tile: 64 particles (k) x 32 columns (j); reads are row-coalesced, writes
+  // are 128-byte segments of Dt rows (bf16 pairs of consecutive particles)
+  __shared__ float tile[64][33];
+  __shared__ float sw[64], mu[32];
+  const int64_t k0 = (int64_t)blockIdx.x * 64;
   const int j0 = blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  if (ty == 0) sw[tx] = (k0 + tx < m) ? (float)sqrt(w[k0 + tx]) : 0.f;
-  if (ty == 1) mu[tx] = (j0 + tx < q) ? (float)from_fix(acc[j0 + tx]) : 0.f;
+  if (threadIdx.x < 64) sw[threadIdx.x] = (k0 + threadIdx.x < m) ? (float)sqrt(w[k0 + threadIdx.x]) : 0.f;
+  if (threadIdx.x >= 64 && threadIdx.x < 96)
+    mu[threadIdx.x - 64] = (j0 + threadIdx.x - 64 < q) ? (float)from_fix(acc[j0 + threadIdx.x - 64]) : 0.f;
   __syncthreads();
-  for (int r = ty; r < 32; r += 8) {
+#pragma unroll
+  for (int r = ty; r < 64; r += 8) {
     const int64_t k = k0 + r;
     const int j = j0 + tx;
     tile[r][tx] = (k < m && j < q) ? sw[r] * (beta[k * ldb + j] - mu[tx]) : 0.f;
   }
   __syncthreads();
-  for (int r = ty; r < 32; r += 8) {
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {  // r = column j0 + r; lane = particle pair
     const int j = j0 + r;
-    const int64_t k = k0 + tx;
+    const int64_t k = k0 + 2 * tx;
     if (j >= q || k >= ldk) continue;
-    const float v = tile[tx][r];
-    const __nv_bfloat16 h = __float2bfloat16_rn(v);
-    Dt[(size_t)j * 2 * ldk + k] = h;
-    Dt[(size_t)j * 2 * ldk + ldk + k] = __float2bfloat16_rn(v - __bfloat162float(h));
+    const float v0 = tile[2 * tx][r], v1 = tile[2 * tx + 1][r];
+    const __nv_bfloat162 h = __floats2bfloat162_rn(v0, v1);
+    const float2 hf = __bfloat1622float2(h);
+    const __nv_bfloat162 l = __floats2bfloat162_rn(v0 - hf.x, v1 - hf.y);
+    *reinterpret_cast<__nv_bfloat162*>(Dt + (size_t)j * 2 * ldk + k) = h;
+    *reinterpret_cast<__nv_bfloat162*>(Dt + (size_t)j * 2 * ldk + ldk + k) = l;
   }
 }
 
-__global__ void rw_accept_kernel(float* __restrict__ beta, int ldb, const __nv_bfloat16* __restrict__ eps, int q, int64_t m,
-                                 const double* __restrict__ ylin_p, const double* __restrict__ sp_p,
-                                 const double* __restrict__ lp_p, double* __restrict__ ll, double* __restrict__ lp,
-                                 uint64_t seed, int64_t t, int64_t i0, int move, unsigned long long* accepted) {
+__global__ void __launch_bounds__(256) rw_accept_kernel(float* __restrict__ beta, int ldb,
+                                                         const __nv_bfloat16* __restrict__ eps, int q, int64_t m,
+                                                         const double* __restrict__ ylin_p,
+                                                         const double* __restrict__ sp_p,
+                                                         const double* __restrict__ lp_p, double* __restrict__ ll,
+                                                         double* __restrict__ lp, uint64_t seed, int64_t t, int64_t i0,
+                                                         int move, unsigned long long* accepted) {
+  // one warp per particle: lane 0 decides, the warp applies beta += eps
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= m) return;
@@ -899,18 +950,32 @@ __global__ void rw_accept_kernel(float* __restrict__ beta, int ldb, const __nv_b
     philox4x32_10(w, (uint32_t)seed, (uint32_t)(seed >> 32));
     const double u = (double)(((uint64_t)w[0] << 21) | (w[1] >> 11)) * 0x1.0p-53;
     const double llp = ylin_p[row] - sp_p[row];
-    const double d = (llp + lp_p[row]) - (ll[row] + lp[row]);
+    const double lpp = lp_p[row];
+    const double d = (llp + lpp) - (ll[row] + lp[row]);
     ok = (d >= 0.0) || (log(u) < d);
     if (ok) {
       ll[row] = llp;
-      lp[row] = lp_p[row];
+      lp[row] = lpp;
       atomicAdd(accepted, 1ull);
     }
   }
   ok = __shfl_sync(0xffffffffu, ok, 0);
-  if (ok) {  // beta' = beta + eps, the same float32 sum the pack kernel used
-    const __nv_bfloat16* s = eps + row * ldb;
-    float* o = beta + row * ldb;
+  if (!ok) return;
+  float* o = beta + row * ldb;
+  const __nv_bfloat16* s = eps + row * ldb;
+  if ((q % 4 == 0) && (ldb % 4 == 0)) {  // beta' = beta + eps, the same float32 sum the pack used
+    for (int j = lane * 4; j < q; j += 128) {
+      float4 x = *reinterpret_cast<const float4*>(o + j);
+      const uint2 yv = *reinterpret_cast<const uint2*>(s + j);
+      const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&yv);
+      const float2 ya = __bfloat1622float2(y2[0]), yb = __bfloat1622float2(y2[1]);
+      x.x += ya.x;
+      x.y += ya.y;
+      x.z += yb.x;
+      x.w += yb.y;
+      *reinterpret_cast<float4*>(o + j) = x;
+    }
+  } else {
     for (int j = lane; j < q; j += 32) o[j] = o[j] + __bfloat162float(s[j]);
   }
 }
@@ -1180,7 +1245,7 @@ int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const d
   __nv_bfloat16* Dt = reinterpret_cast<__nv_bfloat16*>(ws);
   // layout [q][2*ldk]: row i = [hi(i, :) | lo(i, :)]
   {
-    dim3 grid(cdiv(ldk, 32), cdiv(q, 32));
+    dim3 grid(cdiv(ldk, 64), cdiv(q, 32));
     rw_center_t_kernel<<<grid, 256, 0, st>>>(beta, m, ldb, q, w, acc, Dt, ldk);
     SPA_CHECK_LAUNCH();
   }
@@ -1252,8 +1317,19 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
   int rc = launch_tc<1, 1, 256>(Z, (uint64_t)kq, Lb, (uint64_t)kq, (uint64_t)q, args, 1, epi, st);
   if (rc) return rc;
   const unsigned grid = std::min<unsigned>(cdiv(m, 8), 148 * 16);
-  pack_eps_kernel<<<grid, 256, (size_t)16 * d->kp, st>>>(*d, beta, epsb, m, ldb, reinterpret_cast<__nv_bfloat16*>(A),
-                                                         ylin, make_prior(a, c, c), lp);
+  const size_t sm = (size_t)16 * d->kp;
+  auto* Ab = reinterpret_cast<__nv_bfloat16*>(A);
+  const PriorConst pc = make_prior(a, c, c);
+  if (d->kp <= 128)
+    pack_eps_kernel<1><<<grid, 256, sm, st>>>(*d, beta, epsb, m, ldb, Ab, ylin, pc, lp);
+  else if (d->kp <= 256)
+    pack_eps_kernel<2><<<grid, 256, sm, st>>>(*d, beta, epsb, m, ldb, Ab, ylin, pc, lp);
+  else if (d->kp <= 512)
+    pack_eps_kernel<4><<<grid, 256, sm, st>>>(*d, beta, epsb, m, ldb, Ab, ylin, pc, lp);
+  else if (d->kp <= 1024)
+    pack_eps_kernel<8><<<grid, 256, sm, st>>>(*d, beta, epsb, m, ldb, Ab, ylin, pc, lp);
+  else
+    pack_kernel<<<cdiv(m, 8), 256, 0, st>>>(*d, beta, epsb, m, ldb, Ab, ylin, pc, lp);
   SPA_CHECK_LAUNCH();
   return 0;
 }
