@@ -546,18 +546,74 @@ def smc_step(system: ParticleSystem, data, schedule: Schedule, t: int, config: S
     return StepRecord(t, float(bs[t - 1]), float(step_ess), system.log_z_cum, acceptance, bool(resampled))
 
 
+class _SnapshotWriter:
+    """Copies retained steps out without stalling the step loop.
+
+    At snapshot time only device-side clones are taken (weights, float32
+    particles, log-likelihoods; ~0.1 ms) and an event is recorded; a
+    background thread then copies them through a reused pinned staging buffer
+    and widens to the reference's float64 NumPy layout on host threads."""
+
+    def __init__(self):
+        from concurrent.futures import ThreadPoolExecutor
+
+        self.pool = ThreadPoolExecutor(max_workers=1)
+        self.jobs = []
+        self.stream = None
+        self.stage = None
+
+    def submit(self, system: ParticleSystem, record: StepRecord, group=None):
+        w = system.device_weights() if group is None else _global_weights(system, group)
+        beta = system.beta[:, : system.q]
+        ll = system.ll
+        if group is not None:
+            w, beta, ll = group.gather_to_all(w), group.gather_to_all(beta.contiguous()), group.gather_to_all(ll)
+        clones = (w.clone(), beta.contiguous() if group is not None else beta.clone(), ll.clone())
+        ev = torch.cuda.Event()
+        ev.record()
+        dev = system.device
+        if len(self.jobs) >= 4:  # bound the device memory held by pending clones
+            self.jobs.pop(0).result()
+        self.jobs.append(self.pool.submit(self._finish, record, clones, ev, dev))
+        return record
+
+    def _finish(self, record, clones, ev, dev):
+        w, beta, ll = clones
+        with torch.cuda.device(dev):
+            if self.stream is None:
+                self.stream = torch.cuda.Stream(dev)
+            if self.stage is None or self.stage.numel() < beta.numel():
+                self.stage = torch.empty(beta.numel(), dtype=torch.float32, pin_memory=True)
+            st = self.stage[: beta.numel()].view(beta.shape)
+            self.stream.wait_event(ev)
+            with torch.cuda.stream(self.stream):
+                st.copy_(beta, non_blocking=True)
+                wh = w.to("cpu", non_blocking=False)
+                llh = ll.to("cpu", non_blocking=False)
+            self.stream.synchronize()
+        part = torch.empty(beta.shape, dtype=torch.float64)
+        part.copy_(st)  # float32 -> float64 on host threads
+        weights = wh.numpy().copy()
+        weights /= weights.sum()
+        record.weights = weights
+        record.particles = part.numpy()
+        record.logliks = llh.numpy().copy()
+        del clones
+
+    def close(self):
+        for j in self.jobs:
+            j.result()
+        self.jobs.clear()
+        self.pool.shutdown(wait=True)
+
+
 def _snapshot(system: ParticleSystem, record: StepRecord, group=None):
-    """Copy the retained arrays out in the reference layout (float64 NumPy);
-    the float32 -> float64 widening runs on the device."""
-    w = system.device_weights() if group is None else _global_weights(system, group)
-    beta = system.beta[:, : system.q]
-    ll = system.ll
-    if group is not None:
-        w, beta, ll = group.gather_to_all(w), group.gather_to_all(beta.contiguous()), group.gather_to_all(ll)
-    record.weights = w.cpu().numpy().copy()
-    record.weights /= record.weights.sum()
-    record.particles = beta.double().cpu().numpy()
-    record.logliks = ll.cpu().numpy().copy()
+    """Synchronous snapshot (reference layout: float64 NumPy arrays)."""
+    writer = _SnapshotWriter()
+    try:
+        writer.submit(system, record, group)
+    finally:
+        writer.close()
     return record
 
 
@@ -581,15 +637,29 @@ def run_sampler(data, a: float, schedule: Schedule, config: SmcConfig, intercept
     def retained(t):
         return t == 1 or t == schedule.T or (t - 1) % config.snapshot_thin == 0
 
-    def snap(rec):
-        return _snapshot(system, rec, group) if retained(rec.t) else rec
+    timings["snapshot_s"] = 0.0
+    writer = _SnapshotWriter()
 
-    steps = [snap(StepRecord(1, float(schedule.bs[0]), float(config.N), 0.0, init_acc, False))]
-    t1 = time.perf_counter()
-    for t in range(2, schedule.T + 1):
-        steps.append(snap(smc_step(system, data, schedule, t, config, group)))
-    torch.cuda.synchronize()
-    timings["path_s"] = time.perf_counter() - t1
+    def snap(rec):
+        if not retained(rec.t):
+            return rec
+        ts = time.perf_counter()
+        writer.submit(system, rec, group)
+        timings["snapshot_s"] += time.perf_counter() - ts
+        return rec
+
+    try:
+        steps = [snap(StepRecord(1, float(schedule.bs[0]), float(config.N), 0.0, init_acc, False))]
+        t1 = time.perf_counter()
+        for t in range(2, schedule.T + 1):
+            steps.append(snap(smc_step(system, data, schedule, t, config, group)))
+        torch.cuda.synchronize()
+        timings["path_s"] = time.perf_counter() - t1
+        ts = time.perf_counter()
+    finally:
+        writer.close()
+    timings["snapshot_drain_s"] = time.perf_counter() - ts
+    timings["resampling_steps"] = sum(1 for s in steps if s.resampled)
     return SmcOutput(float(a), schedule, config, intercept, names, steps, init_acc, timings)
 
 
