@@ -264,7 +264,7 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
-            rec = S.smc_step(system, data, sched, t, cfg, group)
+            rec = S.smc_step(system, data, sched, t, cfg, group, _defer=True)
             resampled += int(rec.resampled)
             t += 1
         e1.record()

@@ -158,14 +158,19 @@ int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const d
  * *info = 0 or the failing column + 1. */
 int spa_rw_factor(const int64_t* partial, int32_t q, double scale, double jitter, float* L, double* ws, int* info,
                   void* stream);
-/* prop = beta + L z, z ~ N(0, I) from Philox4x32-10 keyed by seed with
- * counter (j/4, i0+k, t, move | 3<<24) (two sign-symmetric Box-Muller pairs per
- * block; csrc/spa_core.cu rw_normals4), L z on tcgen05
- * (zbuf: bf16 [m][kq] normals, kq = roundup(q, 64)) stored as eps = L z
- * (bf16 [m][ldb] -- rounding keeps the increment law exactly symmetric --,
- * coalesced through an smem transpose); then one
+/* Proposal normals Z (bf16 [m][kq], kq = roundup(q, 64), zero padded) from
+ * Philox4x32-10 keyed by seed with counter (j/4, i0+k, t, move | 3<<24): two
+ * sign-symmetric Box-Muller pairs per block (csrc/spa_core.cu rw_normals4).
+ * Independent of the particle state, so all moves of a step can be drawn
+ * ahead, e.g. on a side stream while the covariance is factored. */
+int spa_rw_normals(int64_t m, int32_t q, uint64_t seed, int64_t t, int64_t i0, int32_t move, void* zbuf,
+                   void* stream);
+/* prop = beta + L z for the normals in zbuf (spa_rw_normals of this move): L z
+ * on tcgen05, stored as eps (bf16 [m][ldb] -- rounding keeps the increment law
+ * exactly symmetric --, coalesced through an smem transpose); then one
  * vectorised pass packs prop = beta + eps into the K1 operand A and emits
- * ylin and lp at c.  `Lb` is the bf16 operand written by spa_rw_factor. */
+ * ylin and lp at c.  `Lb` is the bf16 operand written by spa_rw_factor;
+ * seed/t/i0/move are unused (kept for ABI stability). */
 int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ldb, const void* Lb, uint64_t seed,
                    int64_t t, int64_t i0, int32_t move, void* zbuf, void* eps, void* A, double* ylin, double a,
                    double c, double* lp, void* stream);

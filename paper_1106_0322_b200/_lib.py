@@ -62,6 +62,7 @@ _SIGNATURES = {
     "spa_rw_moments": (c_int, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_int32, c_void_p, c_void_p, c_size_t,
                                c_void_p]),
     "spa_rw_factor": (c_int, [c_void_p, c_int32, c_double, c_double, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "spa_rw_normals": (c_int, [c_int64, c_int32, c_uint64, c_int64, c_int64, c_int32, c_void_p, c_void_p]),
     "spa_rw_propose": (c_int, [POINTER(SpaDesign), c_void_p, c_int64, c_int32, c_void_p, c_uint64, c_int64, c_int64,
                                c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_double, c_void_p,
                                c_void_p]),
@@ -82,6 +83,7 @@ def load(path: str = LIB_PATH):
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("SPA_B200_LIB", path)  # developer override (A/B builds)
     if not os.path.exists(path):
         raise RuntimeError(
             f"libspa_b200.so not found at {path}: build it with `make` (or __graft_entry__.build()); "
@@ -106,7 +108,7 @@ KERNELS_PER_CALL = {
     "spa_philox_blocks": 1, "spa_loglik_softplus": 2, "spa_pack_particles": 1, "spa_loglik_rows": 3,
     "spa_prior_rows": 1, "spa_lse_chunk_stats": 1, "spa_lse_combine": 1, "spa_logw_apply": 1,
     "spa_systematic_ancestors": 2, "spa_gather_rows": 1, "spa_mwg_move": 1, "spa_rw_moments": 1,
-    "spa_rw_factor": 0, "spa_rw_propose": 3, "spa_rw_accept": 1, "spa_tc_gemm_f32": 1,
+    "spa_rw_factor": 0, "spa_rw_propose": 2, "spa_rw_normals": 1, "spa_rw_accept": 1, "spa_tc_gemm_f32": 1,
 }
 launch_count = 0
 

@@ -133,22 +133,27 @@ __device__ __forceinline__ float gt_logpdf_f(float b, float lc, float ap1, float
 // prior_kernel mode 2 (same lane->column mapping and multiplication order, so
 // all three produce identical bits):
 //   sum_j gt(p_j) = npen*(-log 2c) - (a+1) * log prod_j (1 + |p_j|/(a c))
-// with the float64 product flushed into the log sum before it can overflow
-// (a = inf: the linear double-exponential form).
+// Columns arrive in groups of 4 with 0/1 penalty flags; the group factor is
+// formed branch-free (an unpenalised column contributes exactly 1) and the
+// float64 running product is flushed into the log sum, once per group,
+// before it could overflow (a = inf: the linear double-exponential form).
 struct LpAcc {
   double logsum = 0.0, prod = 1.0, lin = 0.0;
-  int npen = 0;
-  __device__ __forceinline__ void add(float p, double K, int de) {
-    const double x = fabs((double)p);
-    ++npen;
+  float npen = 0.f;
+  __device__ __forceinline__ void add4(const float (&p)[4], const float (&pen)[4], double K, int de) {
+    npen += (pen[0] + pen[1]) + (pen[2] + pen[3]);
     if (de) {
-      lin += x;
+      lin += (fabs((double)p[0]) * pen[0] + fabs((double)p[1]) * pen[1]) +
+             (fabs((double)p[2]) * pen[2] + fabs((double)p[3]) * pen[3]);
+      return;
+    }
+    const double g = fma(fabs((double)p[0]), K * pen[0], 1.0) * fma(fabs((double)p[1]), K * pen[1], 1.0) *
+                     (fma(fabs((double)p[2]), K * pen[2], 1.0) * fma(fabs((double)p[3]), K * pen[3], 1.0));
+    if (prod < 1e200 && g < 1e100) {
+      prod *= g;
     } else {
-      prod *= fma(x, K, 1.0);
-      if (!(prod < 1e250)) {
-        logsum += log(prod);
-        prod = 1.0;
-      }
+      logsum += log(prod) + log(g);
+      prod = 1.0;
     }
   }
   __device__ __forceinline__ double value(const PriorConst& pc) const {
@@ -209,10 +214,15 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const 
         bs = (d.coded ? (float)d.alpha[j] : 1.0f) * p[i];
         fy = fmaf(p[i], (float)d.sy[j], fy);
         fo = fmaf(p[i], d.coded ? (float)d.gamma[j] : 0.f, fo);
-        if (lp != nullptr && d.penalized[j]) la.add(p[i], K, pc.de);
       }
       h[i] = __float2bfloat16_rn(bs);
       l[i] = __float2bfloat16_rn(bs - __bfloat162float(h[i]));
+    }
+    if (lp != nullptr) {
+      float pen[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) pen[i] = (j0 + i < d.q && d.penalized[j0 + i]) ? 1.f : 0.f;
+      la.add4(p, pen, K, pc.de);
     }
     yl += fy;
     off += fo;
@@ -239,21 +249,33 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const 
   }
 }
 
-// Proposal pack (spa_rw_propose): same arithmetic as pack_kernel, but each
-// block stages the per-column constants (alpha, X^T y, gamma as float32, the
-// penalty flag) in shared memory once and its warps walk many rows; all of a
-// row's vector loads are issued before any arithmetic (IT = kp/128 groups of
-// 4 columns per lane) so every lane keeps IT x 24 bytes in flight.
+// Proposal pack (spa_rw_propose): same arithmetic as pack_kernel.  Each block
+// stages the per-column constants (alpha, X^T y, gamma as float32, the
+// penalty flag) in shared memory once; each warp then walks its rows through
+// a 2-slot shared-memory ring filled by 1-D bulk copies (beta row | eps row),
+// so the next row streams in while the current one is packed and no load
+// data lives in registers.  IT = kp/128 groups of 4 columns per lane.
+constexpr int kPackWarps = 8;
+
+__host__ __device__ inline size_t pack_eps_smem_bytes(int kp, int ldb) {
+  return (size_t)16 * kp + (size_t)kPackWarps * 2 * ((size_t)ldb * 6);
+}
+
 template <int IT>
-__global__ void __launch_bounds__(256) pack_eps_kernel(spa_design d, const float* __restrict__ beta,
-                                                       const __nv_bfloat16* __restrict__ eps, int64_t m, int ldb,
-                                                       __nv_bfloat16* __restrict__ A, double* __restrict__ ylin,
-                                                       PriorConst pc, double* __restrict__ lp) {
-  extern __shared__ float4 csm[];  // [kp/4] x {alpha, sy, gamma, pen}
+__global__ void __launch_bounds__(32 * kPackWarps) pack_eps_kernel(spa_design d, const float* __restrict__ beta,
+                                                                const __nv_bfloat16* __restrict__ eps, int64_t m,
+                                                                int ldb, __nv_bfloat16* __restrict__ A,
+                                                                double* __restrict__ ylin, PriorConst pc,
+                                                                double* __restrict__ lp) {
+  extern __shared__ float4 csm[];  // [kp] x {alpha, sy, gamma, pen}, then the row rings
+  __shared__ uint64_t bars[kPackWarps][2];
   float* ca = reinterpret_cast<float*>(csm);
   float* cs = ca + d.kp;
   float* cg = cs + d.kp;
   float* cp = cg + d.kp;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rowB = (uint32_t)ldb * 4, slotB = (uint32_t)ldb * 6;
+  uint8_t* ring = reinterpret_cast<uint8_t*>(cp + d.kp) + (size_t)warp * 2 * slotB;
   for (int j = threadIdx.x; j < d.kp; j += blockDim.x) {
     const bool v = j < d.q;
     ca[j] = v ? (d.coded ? (float)d.alpha[j] : 1.0f) : 0.f;
@@ -261,27 +283,36 @@ __global__ void __launch_bounds__(256) pack_eps_kernel(spa_design d, const float
     cg[j] = (v && d.coded) ? (float)d.gamma[j] : 0.f;
     cp[j] = (v && d.penalized[j]) ? 1.f : 0.f;
   }
+  if (lane == 0) {
+    mbar_init(&bars[warp][0], 1);
+    mbar_init(&bars[warp][1], 1);
+    fence_barrier_init();
+  }
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int64_t warp0 = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t warp0 = (int64_t)blockIdx.x * kPackWarps + warp;
+  const int64_t nwarps = (int64_t)gridDim.x * kPackWarps;
+  auto issue = [&](int64_t row, int s) {
+    if (row < m) {
+      mbar_arrive_expect_tx(&bars[warp][s], slotB);
+      bulk_g2s(ring + s * slotB, beta + row * ldb, rowB, &bars[warp][s]);
+      bulk_g2s(ring + s * slotB + rowB, eps + row * ldb, slotB - rowB, &bars[warp][s]);
+    }
+  };
+  if (lane == 0) {
+    issue(warp0, 0);
+    issue(warp0 + nwarps, 1);
+  }
   const double K = pc.de ? 0.0 : 1.0 / (pc.a * pc.c);
   const bool full = (d.q % 4 == 0);  // every 4-column group is either all-valid or all-padding
-  for (int64_t row = warp0; row < m; row += nwarps) {
-    const float* b = beta + row * ldb;
-    const __nv_bfloat16* e = eps + row * ldb;
+  uint32_t phase = 0;                // bit s = parity of slot s
+  int s = 0;
+  for (int64_t row = warp0; row < m; row += nwarps, s ^= 1) {
+    mbar_wait(&bars[warp][s], (phase >> s) & 1u);
+    phase ^= 1u << s;
+    const float* b = reinterpret_cast<const float*>(ring + s * slotB);
+    const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(ring + s * slotB + rowB);
     __nv_bfloat16* ah = A + row * (2 * (int64_t)d.kp);
     __nv_bfloat16* al = ah + d.kp;
-    float4 xv[IT];
-    uint2 ev[IT];
-#pragma unroll
-    for (int it = 0; it < IT; ++it) {
-      const int j0 = it * 128 + lane * 4;
-      if (full && j0 + 4 <= d.q) {
-        xv[it] = __ldcs(reinterpret_cast<const float4*>(b + j0));
-        ev[it] = __ldcs(reinterpret_cast<const uint2*>(e + j0));
-      }
-    }
     double yl = 0.0, off = 0.0;  // same grouping as pack_kernel => identical sums
     LpAcc la;
 #pragma unroll
@@ -291,12 +322,14 @@ __global__ void __launch_bounds__(256) pack_eps_kernel(spa_design d, const float
       float fy = 0.f, fo = 0.f;
       float p[4] = {0.f, 0.f, 0.f, 0.f};
       if (full && j0 + 4 <= d.q) {
-        const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&ev[it]);
+        const float4 xv = *reinterpret_cast<const float4*>(b + j0);
+        const uint2 ev = *reinterpret_cast<const uint2*>(e + j0);
+        const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&ev);
         const float2 ya = __bfloat1622float2(y2[0]), yb = __bfloat1622float2(y2[1]);
-        p[0] = xv[it].x + ya.x;
-        p[1] = xv[it].y + ya.y;
-        p[2] = xv[it].z + yb.x;
-        p[3] = xv[it].w + yb.y;
+        p[0] = xv.x + ya.x;
+        p[1] = xv.y + ya.y;
+        p[2] = xv.z + yb.x;
+        p[3] = xv.w + yb.y;
       } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -316,12 +349,17 @@ __global__ void __launch_bounds__(256) pack_eps_kernel(spa_design d, const float
         l[i] = __float2bfloat16_rn(bs - __bfloat162float(h[i]));
         fy = fmaf(p[i], s4[i], fy);
         fo = fmaf(p[i], g4[i], fo);
-        if (p4[i] != 0.f) la.add(p[i], K, pc.de);
       }
+      la.add4(p, p4, K, pc.de);
       yl += fy;
       off += fo;
       __stcs(reinterpret_cast<uint2*>(ah + j0), *reinterpret_cast<const uint2*>(h));
       __stcs(reinterpret_cast<uint2*>(al + j0), *reinterpret_cast<const uint2*>(l));
+    }
+    __syncwarp();  // every lane is done with slot s: refill it
+    if (lane == 0) {
+      fence_proxy_async_smem();
+      issue(row + 2 * nwarps, s);
     }
     yl = warp_sum(yl);
     off = warp_sum(off);
@@ -351,10 +389,16 @@ __global__ void prior_kernel(spa_design d, const float* __restrict__ beta, int64
   if (mode == 2) {  // identical arithmetic (and lane->column mapping) to the pack kernels' lp
     LpAcc la;
     const double K = pc.de ? 0.0 : 1.0 / (pc.a * pc.c);
-    for (int j0 = lane * 4; j0 < d.kp; j0 += 128)
+    for (int j0 = lane * 4; j0 < d.kp; j0 += 128) {
+      float x[4], pen[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (j0 + i < d.q && d.penalized[j0 + i]) la.add(b[j0 + i], K, pc.de);
+      for (int i = 0; i < 4; ++i) {
+        const bool v = j0 + i < d.q;
+        x[i] = v ? b[j0 + i] : 0.f;
+        pen[i] = (v && d.penalized[j0 + i]) ? 1.f : 0.f;
+      }
+      la.add4(x, pen, K, pc.de);
+    }
     s = la.value(pc);
   } else if (pc.de) {
     for (int j = lane; j < d.q; j += 32) {
@@ -872,7 +916,8 @@ __device__ __forceinline__ void rw_normals4(uint64_t seed, int64_t t, int64_t k,
     const uint32_t a = w[2 * h], b = w[2 * h + 1];
     const float u1 = ((float)(a >> 8) + 1.0f) * 0x1.0p-24f;  // (0, 1]
     const float u2 = (float)(b >> 8) * 0x1.0p-24f;           // [0, 1)
-    const float r = sqrtf(-2.0f * __logf(u1));
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-2.0f * __logf(u1)));
     float sn, cs;
     __sincosf(1.5707963267948966f * u2, &sn, &cs);
     const float m0 = fabsf(r * cs), m1 = fabsf(r * sn);
@@ -881,18 +926,25 @@ __device__ __forceinline__ void rw_normals4(uint64_t seed, int64_t t, int64_t k,
   }
 }
 
-__global__ void rw_normals_kernel(int64_t m, int q, int kq, uint64_t seed, int64_t t, int64_t i0, int move,
-                                  __nv_bfloat16* __restrict__ Z) {
-  // grid: x = rows, y = 4-column groups of blockDim.x (32-bit index math)
-  const int jb = blockIdx.y * blockDim.x + threadIdx.x;
-  const int k = blockIdx.x;
-  if (4 * jb >= kq) return;
-  __align__(8) __nv_bfloat16 z[4];
-  float zz[4] = {0.f, 0.f, 0.f, 0.f};
-  if (4 * jb < q) rw_normals4(seed, t, i0 + k, move, (uint32_t)jb, zz);
+__global__ void __launch_bounds__(256) rw_normals_kernel(int64_t m, int q, int kq, uint64_t seed, int64_t t,
+                                                          int64_t i0, int move, __nv_bfloat16* __restrict__ Z) {
+  // warp-stride over particle rows, lanes over 4-column groups (256 B
+  // contiguous stores per warp); a small grid so the kernel shares SMs with
+  // the latency-bound work it overlaps on the main stream
+  const int kq4 = kq / 4;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < m; k += nw) {
+    __nv_bfloat16* zr = Z + (size_t)k * kq;
+    for (int jb = lane; jb < kq4; jb += 32) {
+      __align__(8) __nv_bfloat16 z[4];
+      float zz[4] = {0.f, 0.f, 0.f, 0.f};
+      if (4 * jb < q) rw_normals4(seed, t, i0 + k, move, (uint32_t)jb, zz);
 #pragma unroll
-  for (int i = 0; i < 4; ++i) z[i] = __float2bfloat16(4 * jb + i < q ? zz[i] : 0.0f);
-  *reinterpret_cast<uint2*>(Z + (size_t)k * kq + 4 * jb) = *reinterpret_cast<const uint2*>(z);
+      for (int i = 0; i < 4; ++i) z[i] = __float2bfloat16(4 * jb + i < q ? zz[i] : 0.0f);
+      *reinterpret_cast<uint2*>(zr + 4 * jb) = *reinterpret_cast<const uint2*>(z);
+    }
+  }
 }
 
 // Centre, weight and transpose the particles for the tensor-core SYRK:
@@ -1288,6 +1340,17 @@ int spa_rw_factor(const int64_t* partial, int32_t q, double scale, double jitter
   return 0;
 }
 
+int spa_rw_normals(int64_t m, int32_t q, uint64_t seed, int64_t t, int64_t i0, int32_t move, void* zbuf,
+                   void* stream) {
+  SPA_REQUIRE(zbuf && m > 0 && q > 0, kBadArgument, "spa_rw_normals: bad arguments");
+  const int kq = (q + 63) / 64 * 64;
+  const unsigned grid = std::min<unsigned>(cdiv(m, 8), 4 * 148);
+  rw_normals_kernel<<<grid, 256, 0, as_stream(stream)>>>(m, q, kq, seed, t, i0, move,
+                                                          reinterpret_cast<__nv_bfloat16*>(zbuf));
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
 int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ldb, const void* Lb, uint64_t seed,
                    int64_t t, int64_t i0, int32_t move, void* zbuf, void* eps, void* A, double* ylin, double a,
                    double c, double* lp, void* stream) {
@@ -1298,12 +1361,10 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
   const int q = d->q;
   const int kq = (q + 63) / 64 * 64;
   __nv_bfloat16* Z = reinterpret_cast<__nv_bfloat16*>(zbuf);
-  {
-    const int tx = std::min(128, kq / 4);
-    dim3 grid((unsigned)m, cdiv(kq / 4, tx));
-    rw_normals_kernel<<<grid, tx, 0, st>>>(m, q, kq, seed, t, i0, move, Z);
-  }
-  SPA_CHECK_LAUNCH();
+  (void)seed;
+  (void)t;
+  (void)i0;
+  (void)move;
   TcArgs args;
   args.m = (int)m;
   args.ncols = q;
@@ -1316,20 +1377,26 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
   EpiStoreT<__nv_bfloat16> epi{epsb, ldb, (int)m, 0, nullptr};
   int rc = launch_tc<1, 1, 256>(Z, (uint64_t)kq, Lb, (uint64_t)kq, (uint64_t)q, args, 1, epi, st);
   if (rc) return rc;
-  const unsigned grid = std::min<unsigned>(cdiv(m, 8), 148 * 16);
-  const size_t sm = (size_t)16 * d->kp;
   auto* Ab = reinterpret_cast<__nv_bfloat16*>(A);
   const PriorConst pc = make_prior(a, c, c);
-  if (d->kp <= 128)
-    pack_eps_kernel<1><<<grid, 256, sm, st>>>(*d, beta, epsb, m, ldb, Ab, ylin, pc, lp);
-  else if (d->kp <= 256)
-    pack_eps_kernel<2><<<grid, 256, sm, st>>>(*d, beta, epsb, m, ldb, Ab, ylin, pc, lp);
-  else if (d->kp <= 512)
-    pack_eps_kernel<4><<<grid, 256, sm, st>>>(*d, beta, epsb, m, ldb, Ab, ylin, pc, lp);
-  else if (d->kp <= 1024)
-    pack_eps_kernel<8><<<grid, 256, sm, st>>>(*d, beta, epsb, m, ldb, Ab, ylin, pc, lp);
-  else
-    pack_kernel<<<cdiv(m, 8), 256, 0, st>>>(*d, beta, epsb, m, ldb, Ab, ylin, pc, lp);
+  const size_t sm = pack_eps_smem_bytes(d->kp, ldb);
+  auto run = [&](auto kern) -> int {
+    SPA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int per_sm = 0, dev = 0, nsm = 0;
+    SPA_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kPackWarps, sm));
+    SPA_CHECK_CUDA(cudaGetDevice(&dev));
+    SPA_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    SPA_REQUIRE(per_sm > 0, kNotSupported, "spa_rw_propose: pack ring does not fit in shared memory");
+    const unsigned grid = std::min<unsigned>(cdiv(m, kPackWarps), (unsigned)(per_sm * nsm));
+    kern<<<grid, 32 * kPackWarps, sm, st>>>(*d, beta, epsb, m, ldb, Ab, ylin, pc, lp);
+    SPA_CHECK_LAUNCH();
+    return 0;
+  };
+  if (d->kp <= 128) return run(pack_eps_kernel<1>);
+  if (d->kp <= 256) return run(pack_eps_kernel<2>);
+  if (d->kp <= 512) return run(pack_eps_kernel<4>);
+  if (d->kp <= 1024 && sm <= 200 * 1024) return run(pack_eps_kernel<8>);
+  pack_kernel<<<cdiv(m, 8), 256, 0, st>>>(*d, beta, epsb, m, ldb, Ab, ylin, pc, lp);
   SPA_CHECK_LAUNCH();
   return 0;
 }

@@ -17,6 +17,7 @@
 #pragma once
 
 #include <cuda.h>
+#include <cuda_bf16.h>
 
 #include "common.cuh"
 
@@ -65,7 +66,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                    Epi epi) {
   using S = TcShape<TA, TB, BN>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by pointer arithmetic on the shared array (keeps the shared
+  // address space visible to the compiler: LDS/STS, not generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kStages * S::kStageBytes);
   uint64_t* empty = full + S::kStages;
   uint64_t* tfull = empty + S::kStages;
@@ -332,10 +335,34 @@ struct EpiStoreT {
     for (int i = 0; i < 32; ++i) tile[lane * 33 + i] = v[i];
     __syncwarp();
     const int row0 = row - lane;
-    const int c = col0 + lane;
+    if constexpr (sizeof(OutT) == 2) {
+      // bf16 pairs: lanes 0-15 write row r, lanes 16-31 row r+1 (2 x 64 B per store)
+      const int half = lane >> 4, cl = (lane & 15) * 2;
+      const int c = col0 + cl;
+      OutT* p = base_ + (size_t)(row0 + half) * ld + c;
+      const float* tp = tile + half * 33 + cl;
+      const bool both = c + 1 < ncols, one = c < ncols;
 #pragma unroll 4
-    for (int r = 0; r < 32; ++r)
-      if (row0 + r < m && c < ncols) base_[(size_t)(row0 + r) * ld + c] = (OutT)tile[r * 33 + lane];
+      for (int r = 0; r < 32; r += 2) {
+        if (row0 + r + half < m) {
+          if (both)
+            *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(tp[0], tp[1]);
+          else if (one)
+            *p = (OutT)tp[0];
+        }
+        p += 2 * (size_t)ld;
+        tp += 66;
+      }
+    } else {
+      const int c = col0 + lane;
+      OutT* p = base_ + (size_t)row0 * ld + c;
+      const bool ok = c < ncols;
+#pragma unroll 4
+      for (int r = 0; r < 32; ++r) {
+        if (ok && row0 + r < m) *p = (OutT)tile[r * 33 + lane];
+        p += ld;
+      }
+    }
     __syncwarp();
   }
   __device__ __forceinline__ void end_tile(int) {}

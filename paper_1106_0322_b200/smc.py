@@ -275,11 +275,22 @@ class ParticleSystem:
                 fws=torch.empty((_round_up(8 * q * q, 256) + _round_up(2 * q * kq, 256) + 8192) // 8,
                                 dtype=torch.float64, device=dev),
                 info=torch.zeros(1, dtype=torch.int32, device=dev),
-                zbuf=torch.empty((self.N, kq), dtype=torch.bfloat16, device=dev),
                 mws=torch.empty(max(_lib.load().spa_rw_moments_workspace_bytes(self.N, q), 8), dtype=torch.uint8,
                                 device=dev),
             )
         return self._rw
+
+    def side_stream(self):
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(self.device)
+        return self._side
+
+    def z_buffers(self, moves: int):
+        kq = _round_up(self.q, 64)
+        zs = getattr(self, "_zs", None)
+        if zs is None or len(zs) < moves:
+            self._zs = zs = [torch.empty((self.N, kq), dtype=torch.bfloat16, device=self.device) for _ in range(moves)]
+        return zs
 
     def factor_operand(self):
         rw = self.rw_workspace()
@@ -349,11 +360,12 @@ def _reweight_device(system: ParticleSystem, prior_t: GtPrior, prior_prev: GtPri
         stats = group.all_gather_cat(system.stats)
         nch = stats.shape[0]
     _lib.call("spa_lse_combine", _p(stats), nch, _p(system.res), _stream())
+    # apply before the host read so the device is not idle across the sync
+    _lib.call("spa_logw_apply", _p(system.logw), _p(system.lw), system.N, _p(system.res), None, _stream())
     res = system.res.cpu()
     inc = float(res[0])
     if not math.isfinite(inc):
         raise DegeneracyError("all incremental weights vanished")
-    _lib.call("spa_logw_apply", _p(system.logw), _p(system.lw), system.N, _p(system.res), None, _stream())
     system._ess_after_reweight = float(res[1])
     return inc
 
@@ -438,11 +450,33 @@ def _global_weights(system, group):
     return system.w
 
 
-def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int, group=None) -> int:
+def _rw_normals_async(system: ParticleSystem, config: SmcConfig, t: int):
+    """The proposal normals of every move depend only on (seed, t, move,
+    particle): draw them on a side stream, launched at the top of the step so
+    they fill the device while the host waits on the reweight result and
+    while the covariance is estimated and factored.  Returns the ready event."""
+    main = torch.cuda.current_stream()
+    side = system.side_stream()
+    zs = system.z_buffers(config.moves)
+    side.wait_stream(main)  # previous step's proposals are done reading zs
+    with torch.cuda.stream(side):
+        for mv in range(config.moves):
+            _lib.call("spa_rw_normals", system.N, system.q, int(config.seed), int(t), int(system.i0), mv,
+                      _p(zs[mv]), ctypes.c_void_p(side.cuda_stream))
+    z_ready = torch.cuda.Event()
+    z_ready.record(side)
+    return z_ready
+
+
+def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int, group=None, z_ready=None):
     d = system.design
     ws = system.ll_workspace()
     rw = system.rw_workspace()
+    if z_ready is None:
+        z_ready = _rw_normals_async(system, config, t)
+    zs = system.z_buffers(config.moves)
     _rw_factor(system, config.rw_scale, group)
+    torch.cuda.current_stream().wait_event(z_ready)
     # log-prior of the current particles at the new scale
     _lib.call("spa_prior_rows", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb, float(prior.a),
               float(prior.c), float(prior.c), 2, _p(system.lp), _stream())
@@ -450,7 +484,7 @@ def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int,
     Lb = system.factor_operand()
     for mv in range(config.moves):
         _lib.call("spa_rw_propose", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb, Lb,
-                  int(config.seed), int(t), int(system.i0), mv, _p(rw["zbuf"]), _p(rw["prop"]), _p(ws["A"]),
+                  int(config.seed), int(t), int(system.i0), mv, _p(zs[mv]), _p(rw["prop"]), _p(ws["A"]),
                   _p(ws["ylin"]), float(prior.a), float(prior.c), _p(rw["lp_p"]), _stream())
         if KERNEL_TIMER is not None:
             KERNEL_TIMER.start("loglik")
@@ -461,8 +495,8 @@ def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int,
         _lib.call("spa_rw_accept", _p(system.beta), system.ldb, _p(rw["prop"]), system.q, system.N, _p(ws["ylin"]),
                   _p(ws["sp"]), _p(rw["lp_p"]), _p(system.ll), _p(system.lp), int(config.seed), int(t),
                   int(system.i0), mv, _p(system.counter), _stream())
-    acc = system.counter if group is None else group.all_reduce_sum(system.counter.clone())
-    return int(acc.item())
+    acc = system.counter.clone() if group is None else group.all_reduce_sum(system.counter.clone())
+    return acc  # device tensor: read lazily (no host sync inside the step)
 
 
 # ---------------------------------------------------------------------------
@@ -510,7 +544,18 @@ def init_particles(data, prior_at_b1: GtPrior, config: SmcConfig, intercept: boo
 # one lambda step (reference smc.py:397-424)
 
 
-def smc_step(system: ParticleSystem, data, schedule: Schedule, t: int, config: SmcConfig, group=None) -> StepRecord:
+class _LazyRate:
+    """Acceptance rate whose device-side counter is read on first use."""
+
+    def __init__(self, counter: torch.Tensor, denom: int):
+        self.counter, self.denom = counter, denom
+
+    def __float__(self):
+        return int(self.counter.item()) / self.denom
+
+
+def smc_step(system: ParticleSystem, data, schedule: Schedule, t: int, config: SmcConfig, group=None,
+             _defer: bool = False) -> StepRecord:
     """Advance from step t-1 to t: reweight -> accumulate evidence -> ESS ->
     resample if ESS < frac*N -> move with the invariant kernel at prior_t."""
     if not 2 <= t <= schedule.T:
@@ -521,6 +566,7 @@ def smc_step(system: ParticleSystem, data, schedule: Schedule, t: int, config: S
     bs = schedule.bs
     prior_prev = GtPrior(a, prior_scale(a, bs[t - 2]))
     prior_t = GtPrior(a, prior_scale(a, bs[t - 1]))
+    z_ready = _rw_normals_async(system, config, t) if config.move_kernel == "rw" else None
     try:
         inc = _reweight_device(system, prior_t, prior_prev, group)
     except DegeneracyError as exc:
@@ -540,10 +586,13 @@ def smc_step(system: ParticleSystem, data, schedule: Schedule, t: int, config: S
         if t == 2 or not getattr(system, "_ll_from_k1", False):
             _loglik_device(system, system.ll)  # keep ll on the K1 arithmetic the MH ratio uses
             system._ll_from_k1 = True
-        acc = _rw_moves(system, prior_t, config, t, group)
-        acceptance = acc / (system.N_total * config.moves)
+        acc = _rw_moves(system, prior_t, config, t, group, z_ready)
+        acceptance = _LazyRate(acc, system.N_total * config.moves)
     system.t = t
-    return StepRecord(t, float(bs[t - 1]), float(step_ess), system.log_z_cum, acceptance, bool(resampled))
+    rec = StepRecord(t, float(bs[t - 1]), float(step_ess), system.log_z_cum, acceptance, bool(resampled))
+    if not _defer:
+        rec.acceptance = float(rec.acceptance)
+    return rec
 
 
 class _SnapshotWriter:
@@ -652,7 +701,9 @@ def run_sampler(data, a: float, schedule: Schedule, config: SmcConfig, intercept
         steps = [snap(StepRecord(1, float(schedule.bs[0]), float(config.N), 0.0, init_acc, False))]
         t1 = time.perf_counter()
         for t in range(2, schedule.T + 1):
-            steps.append(snap(smc_step(system, data, schedule, t, config, group)))
+            steps.append(snap(smc_step(system, data, schedule, t, config, group, _defer=True)))
+        for s in steps:  # resolve the deferred acceptance counters (one sync)
+            s.acceptance = float(s.acceptance)
         torch.cuda.synchronize()
         timings["path_s"] = time.perf_counter() - t1
         ts = time.perf_counter()

@@ -296,8 +296,10 @@ def test_rw_propose_and_accept_vs_oracle():
     _lib.call("spa_prior_rows", ctypes.byref(d.struct), _p(s.beta), s.N, s.ldb, a, c, c, 2, _p(s.lp), _stream())
     beta0, ll0, lp0 = s.betas.copy(), s.logliks.copy(), s.lp.cpu().numpy().copy()
     np.testing.assert_allclose(lp0, orc.log_prior_rows(beta0, a, c), rtol=1e-6)
+    zb = s.z_buffers(1)[0]
+    _lib.call("spa_rw_normals", s.N, s.q, seed, t, 0, move, _p(zb), _stream())
     _lib.call("spa_rw_propose", ctypes.byref(d.struct), _p(s.beta), s.N, s.ldb, s.factor_operand(), seed, t, 0, move,
-              _p(rw["zbuf"]), _p(rw["prop"]), _p(ws["A"]), _p(ws["ylin"]), a, c, _p(rw["lp_p"]), _stream())
+              _p(zb), _p(rw["prop"]), _p(ws["A"]), _p(ws["ylin"]), a, c, _p(rw["lp_p"]), _stream())
     eps = rw["prop"][:, : s.q].float().cpu().numpy()  # eps = L z (bf16)
     prop = (s.beta[:, : s.q].cpu().numpy() + eps).astype(np.float64)
     Lbf = torch.from_numpy(rw["L"].cpu().numpy()).to(torch.bfloat16).double().numpy()

@@ -43,8 +43,10 @@ timeit("chol only", lambda: _lib.call("spa_rw_factor", _p(rw["acc"]), s.q, 2.38,
                                       _p(rw["info"]), _stream()))
 timeit("prior mode 2", lambda: _lib.call("spa_prior_rows", ctypes.byref(d.struct), _p(s.beta), s.N, s.ldb, 1.0,
                                          float(prior.c), float(prior.c), 2, _p(s.lp), _stream()))
-timeit("propose (normals+gemm+pack)", lambda: _lib.call(
-    "spa_rw_propose", ctypes.byref(d.struct), _p(s.beta), s.N, s.ldb, s.factor_operand(), 1, 4, 0, 0, _p(rw["zbuf"]),
+zb = s.z_buffers(1)[0]
+timeit("normals", lambda: _lib.call("spa_rw_normals", s.N, s.q, 1, 4, 0, 0, _p(zb), _stream()))
+timeit("propose (gemm+pack)", lambda: _lib.call(
+    "spa_rw_propose", ctypes.byref(d.struct), _p(s.beta), s.N, s.ldb, s.factor_operand(), 1, 4, 0, 0, _p(zb),
     _p(rw["prop"]), _p(ws["A"]), _p(ws["ylin"]), 1.0, float(prior.c), _p(rw["lp_p"]), _stream()))
 timeit("K1 loglik", lambda: _lib.call("spa_loglik_softplus", ctypes.byref(d.struct), _p(ws["A"]), s.N, _p(ws["sp"]),
                                       _p(ws["ws"]), ws["ws"].numel(), _stream()))
