@@ -457,53 +457,63 @@ __global__ void prior_kernel(spa_design d, const float* __restrict__ beta, int64
 // K3: fixed-chunk log-sum-exp statistics
 constexpr int kChunk = 4096;
 
-__global__ void lse_stats_kernel(const double* __restrict__ logw, const double* __restrict__ lw, int64_t m,
-                                 double* __restrict__ stats) {
-  __shared__ double red[256];
+// One 1024-thread block per fixed 4096-particle chunk; each thread keeps its
+// 4 values in registers across the max and sum passes.  The reduction tree is
+// fixed (shuffles, then one warp over the 32 warp results), so the chunk
+// statistics do not depend on how particles are sharded.
+constexpr int kLseThreads = 1024;
+
+__device__ __forceinline__ double block_reduce_1024(double v, double* red, bool is_max) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmax(v, u) : v + u;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  v = red[threadIdx.x & 31];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmax(v, u) : v + u;
+  }
+  __syncthreads();  // red reusable
+  return v;
+}
+
+__global__ void __launch_bounds__(kLseThreads) lse_stats_kernel(const double* __restrict__ logw,
+                                                                const double* __restrict__ lw, int64_t m,
+                                                                double* __restrict__ stats) {
+  __shared__ double red[32];
+  constexpr int kPer = kChunk / kLseThreads;
   const int64_t c0 = (int64_t)blockIdx.x * kChunk;
-  const int64_t c1 = min(m, c0 + kChunk);
+  double x[kPer];
   double mx = -INFINITY;
   bool nan = false;
-  for (int64_t k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
-    const double x = logw[k] + (lw ? lw[k] : 0.0);
-    if (x != x) nan = true;
-    mx = fmax(mx, x);
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int64_t k = c0 + threadIdx.x + i * kLseThreads;
+    x[i] = k < m ? logw[k] + (lw ? lw[k] : 0.0) : -INFINITY;
+    if (x[i] != x[i]) nan = true;
+    mx = fmax(mx, x[i]);
   }
   nan = __syncthreads_or(nan);
-  red[threadIdx.x] = mx;
-  __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
-    if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
-    __syncthreads();
-  }
-  mx = red[0];
-  __syncthreads();
+  mx = block_reduce_1024(mx, red, true);
   double s1 = 0.0, s2 = 0.0;
   if (mx > -INFINITY) {
-    for (int64_t k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
-      const double e = exp(logw[k] + (lw ? lw[k] : 0.0) - mx);
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const double e = exp(x[i] - mx);
       s1 += e;
       s2 += e * e;
     }
   }
-  red[threadIdx.x] = s1;
-  __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
-    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
-    __syncthreads();
-  }
-  s1 = red[0];
-  __syncthreads();
-  red[threadIdx.x] = s2;
-  __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
-    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
-    __syncthreads();
-  }
+  s1 = block_reduce_1024(s1, red, false);
+  s2 = block_reduce_1024(s2, red, false);
   if (threadIdx.x == 0) {
     stats[3 * blockIdx.x + 0] = nan ? NAN : mx;
     stats[3 * blockIdx.x + 1] = s1;
-    stats[3 * blockIdx.x + 2] = red[0];
+    stats[3 * blockIdx.x + 2] = s2;
   }
 }
 
@@ -1200,7 +1210,7 @@ int spa_prior_rows(const spa_design* d, const float* beta, int64_t m, int32_t ld
 
 int spa_lse_chunk_stats(const double* logw, const double* lw, int64_t m, double* stats, void* stream) {
   SPA_REQUIRE(logw && stats && m > 0, kBadArgument, "spa_lse_chunk_stats: bad arguments");
-  lse_stats_kernel<<<cdiv(m, kChunk), 256, 0, as_stream(stream)>>>(logw, lw, m, stats);
+  lse_stats_kernel<<<cdiv(m, kChunk), kLseThreads, 0, as_stream(stream)>>>(logw, lw, m, stats);
   SPA_CHECK_LAUNCH();
   return 0;
 }

@@ -317,10 +317,12 @@ struct EpiFixAtomic {
   __device__ __forceinline__ void end_unit(int, int, int) {}
 };
 
-// Raw accumulator store through a per-warp smem transpose: lane = row in
-// TMEM, lane = column in the global store, so each store instruction writes
-// one contiguous row segment.  out[unit*unit_stride + row*ld + col] = D for
-// valid entries (OutT = float or __nv_bfloat16).
+// Raw accumulator store: each thread owns one row and writes its 32
+// consecutive columns straight from registers with 16-byte stores (64 B of
+// bf16 / 128 B of fp32 per thread per chunk; a warp's 32 rows fill whole
+// sectors).  out[unit*unit_stride + row*ld + col] = D for valid entries
+// (OutT = float or __nv_bfloat16; ld * sizeof(OutT) must be a multiple of 16
+// for the vector path, otherwise element stores are used).
 template <class OutT>
 struct EpiStoreT {
   OutT* out;
@@ -329,41 +331,34 @@ struct EpiStoreT {
   size_t unit_stride;
   OutT* base_;
   __device__ __forceinline__ void begin_unit(int, int unit) { base_ = out + (size_t)unit * unit_stride; }
-  __device__ __forceinline__ void consume(int row, int col0, const float (&v)[32], int ncols, float* tile) {
-    const int lane = threadIdx.x & 31;
+  __device__ __forceinline__ void consume(int row, int col0, const float (&v)[32], int ncols, float*) {
+    if (row >= m) return;
+    OutT* p = base_ + (size_t)row * ld + col0;
+    const bool vec = col0 + 32 <= ncols && ((ld * sizeof(OutT)) & 15) == 0 &&
+                     ((reinterpret_cast<uintptr_t>(base_) & 15) == 0);
+    if (vec) {
+      if constexpr (sizeof(OutT) == 2) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) tile[lane * 33 + i] = v[i];
-    __syncwarp();
-    const int row0 = row - lane;
-    if constexpr (sizeof(OutT) == 2) {
-      // bf16 pairs: lanes 0-15 write row r, lanes 16-31 row r+1 (2 x 64 B per store)
-      const int half = lane >> 4, cl = (lane & 15) * 2;
-      const int c = col0 + cl;
-      OutT* p = base_ + (size_t)(row0 + half) * ld + c;
-      const float* tp = tile + half * 33 + cl;
-      const bool both = c + 1 < ncols, one = c < ncols;
-#pragma unroll 4
-      for (int r = 0; r < 32; r += 2) {
-        if (row0 + r + half < m) {
-          if (both)
-            *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(tp[0], tp[1]);
-          else if (one)
-            *p = (OutT)tp[0];
+        for (int i = 0; i < 32; i += 8) {
+          uint4 u;
+          __nv_bfloat162 h0 = __floats2bfloat162_rn(v[i], v[i + 1]), h1 = __floats2bfloat162_rn(v[i + 2], v[i + 3]);
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(v[i + 4], v[i + 5]), h3 = __floats2bfloat162_rn(v[i + 6], v[i + 7]);
+          u.x = *reinterpret_cast<uint32_t*>(&h0);
+          u.y = *reinterpret_cast<uint32_t*>(&h1);
+          u.z = *reinterpret_cast<uint32_t*>(&h2);
+          u.w = *reinterpret_cast<uint32_t*>(&h3);
+          *reinterpret_cast<uint4*>(p + i) = u;
         }
-        p += 2 * (size_t)ld;
-        tp += 66;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
       }
     } else {
-      const int c = col0 + lane;
-      OutT* p = base_ + (size_t)row0 * ld + c;
-      const bool ok = c < ncols;
-#pragma unroll 4
-      for (int r = 0; r < 32; ++r) {
-        if (ok && row0 + r < m) *p = (OutT)tile[r * 33 + lane];
-        p += ld;
-      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < ncols) p[i] = (OutT)v[i];
     }
-    __syncwarp();
   }
   __device__ __forceinline__ void end_tile(int) {}
   __device__ __forceinline__ void end_unit(int, int, int) {}

@@ -566,6 +566,8 @@ def smc_step(system: ParticleSystem, data, schedule: Schedule, t: int, config: S
     bs = schedule.bs
     prior_prev = GtPrior(a, prior_scale(a, bs[t - 2]))
     prior_t = GtPrior(a, prior_scale(a, bs[t - 1]))
+    # launched first: measured better than overlapping them with the Cholesky
+    # (they then slow its latency-bound panel kernels)
     z_ready = _rw_normals_async(system, config, t) if config.move_kernel == "rw" else None
     try:
         inc = _reweight_device(system, prior_t, prior_prev, group)
