@@ -98,6 +98,12 @@ int spa_loglik_rows(const spa_design* d, const float* beta, int64_t m, int32_t l
 int spa_prior_rows(const spa_design* d, const float* beta, int64_t m, int32_t ldb, double a, double c,
                    double c_prev, int32_t mode, double* out, void* stream);
 
+/* Fused reweight pass (smc.py:248-257 increments + model.py:78-81 at the new
+ * scale): lw[k] = sum_j gt(beta_kj; a, c) - gt(beta_kj; a, c_prev) and
+ * lp[k] = sum_j gt(beta_kj; a, c), lp bit-identical to mode 2 above. */
+int spa_prior_reweight(const spa_design* d, const float* beta, int64_t m, int32_t ldb, double a, double c,
+                       double c_prev, double* lw, double* lp, void* stream);
+
 /* ---- K3: log-sum-exp / ESS (smc.py:151-157, 171-174, 258-262) ----------
  * Fixed 4096-particle chunks -> per-chunk (max, sum e^(x-max), sum e^(2(x-max)))
  * of x = logw + lw; deterministic for any particle sharding. */
@@ -182,8 +188,9 @@ int spa_rw_accept(float* beta, int32_t ldb, const void* eps, int32_t q, int64_t 
                   int64_t i0, int32_t move, unsigned long long* accepted, void* stream);
 
 /* ---- test hook: the raw tcgen05 GEMM engine --------------------------
- * C[m][ldc] += sum_t A_t B^T for A = [A_0 | A_1] (terms_a bf16 blocks of kp
- * columns, K-major) and B [rows_b][kp] bf16; float32 C.  Used by the GEMM
+ * C[m][ldc] = sum_t A_t B^T for A = [A_0 | A_1] (terms_a bf16 blocks of kp
+ * columns, K-major) and B [rows_b][kp] bf16; float32 C (ldc % 4 == 0, TMA
+ * store epilogue).  Used by the GEMM
  * unit tests (tests/test_gpu_kernels.py::test_tc_gemm_*). */
 int spa_tc_gemm_f32(const void* A, int64_t m, int32_t terms_a, const void* B, int32_t rows_b, int32_t kp, float* C,
                     int32_t ldc, void* stream);

@@ -59,19 +59,44 @@ static int make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t cols, uint
   return 0;
 }
 
-template <int TA, int TB, int BN, class Epi>
+// Output map for EpiStoreT: [units][rows][cols] (OutT = float / bf16), row
+// stride ld, unit stride unit_stride elements; box 32 x 32 x 1 with the
+// swizzle matching the epilogue's staging layout (SW128 fp32, SW64 bf16).
+template <class OutT>
+static int make_tmap_out(CUtensorMap* map, void* ptr, uint64_t cols, uint64_t rows, uint64_t units, uint64_t ld,
+                         uint64_t unit_stride) {
+  auto enc = tmap_encoder();
+  if (!enc) return fail(kDriverEntryPoint, "cuTensorMapEncodeTiled unavailable");
+  constexpr bool f32 = sizeof(OutT) == 4;
+  if ((ld * sizeof(OutT)) % 16 || (unit_stride * sizeof(OutT)) % 16 || (reinterpret_cast<uintptr_t>(ptr) & 15))
+    return fail(kBadArgument, "TMA store: output rows must be 16-byte aligned");
+  cuuint64_t dims[3] = {cols, rows, units};
+  cuuint64_t strides[2] = {ld * sizeof(OutT), unit_stride * sizeof(OutT)};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, ptr, dims,
+                   strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(kDriverEntryPoint, "cuTensorMapEncodeTiled (store) failed: " + std::to_string((int)r));
+  return 0;
+}
+
+template <int TA, int TB, int BN, class Epi, int TM = 1>
 static int launch_tc(const void* A, uint64_t a_cols, const void* B, uint64_t b_cols, uint64_t b_rows, TcArgs args,
-                     int units, Epi epi, cudaStream_t st) {
-  using S = TcShape<TA, TB, BN>;
+                     int units, Epi epi, cudaStream_t st, const CUtensorMap* tmc_out = nullptr) {
+  constexpr int kSmem = tc_smem_bytes<TA, TB, BN, Epi, TM>();
   CUtensorMap ta, tb;
   int rc = make_tmap_bf16(&ta, A, a_cols, (uint64_t)args.m, kTcBM);
   if (rc) return rc;
   rc = make_tmap_bf16(&tb, B, b_cols, b_rows, BN);
   if (rc) return rc;
-  auto kern = tc_gemm_kernel<TA, TB, BN, Epi>;
+  SPA_REQUIRE(Epi::kScratchPerWarp == 0 || tmc_out != nullptr, kBadArgument, "launch_tc: store epilogue needs a map");
+  const CUtensorMap& tc = tmc_out ? *tmc_out : ta;  // unused by non-store epilogues
+  auto kern = tc_gemm_kernel<TA, TB, BN, Epi, TM>;
   static bool attr_done = false;  // per template instantiation
   if (!attr_done) {
-    SPA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kSmemBytes));
+    SPA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     attr_done = true;
   }
   args.units = units;
@@ -82,8 +107,8 @@ static int launch_tc(const void* A, uint64_t a_cols, const void* B, uint64_t b_c
     SPA_CHECK_CUDA(cudaGetDevice(&dev));
     SPA_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  const int grid = std::min(args.m_tiles * units, sms);
-  kern<<<grid, kTcThreads, S::kSmemBytes, st>>>(ta, tb, args, epi);
+  const int grid = std::min((args.m_tiles + TM - 1) / TM * units, sms);
+  kern<<<grid, kTcThreads, kSmem, st>>>(ta, tb, tc, args, epi);
   SPA_CHECK_LAUNCH();
   return 0;
 }
@@ -451,6 +476,48 @@ __global__ void prior_kernel(spa_design d, const float* __restrict__ beta, int64
   }
   s = warp_sum(s);
   if (lane == 0) out[row] = s;
+}
+
+// Reweight pass fused with the log-prior at the new scale: one read of the
+// particles gives both the incremental weights lw = sum_j gt(c) - gt(c_prev)
+// and lp = sum_j gt(c) in the LpAcc arithmetic of prior mode 2 / the pack
+// kernels (bit-identical to them), which the move kernels need next.
+__global__ void __launch_bounds__(256) prior_reweight_kernel(spa_design d, const float* __restrict__ beta, int64_t m,
+                                                             int ldb, PriorConst pc, double* __restrict__ lw,
+                                                             double* __restrict__ lp) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= m) return;
+  const float* b = beta + row * ldb;
+  const double K1 = pc.de ? 0.0 : 1.0 / (pc.a * pc.c), K2 = pc.de ? 0.0 : 1.0 / (pc.a * pc.c_prev);
+  const bool full = (d.q % 4 == 0) && (ldb % 4 == 0);
+  LpAcc la, lb;
+  for (int j0 = lane * 4; j0 < d.kp; j0 += 128) {
+    float x[4], pen[4];
+    if (full && j0 + 4 <= d.q) {
+      const float4 v = __ldcs(reinterpret_cast<const float4*>(b + j0));
+      x[0] = v.x;
+      x[1] = v.y;
+      x[2] = v.z;
+      x[3] = v.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) x[i] = j0 + i < d.q ? b[j0 + i] : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) pen[i] = (j0 + i < d.q && d.penalized[j0 + i]) ? 1.f : 0.f;
+    la.add4(x, pen, K1, pc.de);
+    if (!pc.de) lb.add4(x, pen, K2, 0);
+  }
+  const double lpv = la.value(pc);
+  const double lwv = pc.de ? (double)la.npen * pc.lr - la.lin * (1.0 / pc.c - 1.0 / pc.c_prev)
+                           : (double)la.npen * pc.lr -
+                                 (pc.a + 1.0) * ((la.logsum + log(la.prod)) - (lb.logsum + log(lb.prod)));
+  const double s_lp = warp_sum(lpv), s_lw = warp_sum(lwv);
+  if (lane == 0) {
+    lw[row] = s_lw;
+    lp[row] = s_lp;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1208,6 +1275,17 @@ int spa_prior_rows(const spa_design* d, const float* beta, int64_t m, int32_t ld
   return 0;
 }
 
+int spa_prior_reweight(const spa_design* d, const float* beta, int64_t m, int32_t ldb, double a, double c,
+                       double c_prev, double* lw, double* lp, void* stream) {
+  SPA_REQUIRE(d && beta && lw && lp && m >= 0, kBadArgument, "spa_prior_reweight: bad arguments");
+  SPA_REQUIRE(a > 0 && c > 0 && c_prev > 0, kBadArgument, "spa_prior_reweight: a, c must be positive");
+  if (m == 0) return 0;
+  prior_reweight_kernel<<<cdiv(m, 8), 256, 0, as_stream(stream)>>>(*d, beta, m, ldb, make_prior(a, c, c_prev), lw,
+                                                                   lp);
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
 int spa_lse_chunk_stats(const double* logw, const double* lw, int64_t m, double* stats, void* stream) {
   SPA_REQUIRE(logw && stats && m > 0, kBadArgument, "spa_lse_chunk_stats: bad arguments");
   lse_stats_kernel<<<cdiv(m, kChunk), kLseThreads, 0, as_stream(stream)>>>(logw, lw, m, stats);
@@ -1272,19 +1350,20 @@ size_t spa_rw_moments_workspace_bytes(int64_t m, int32_t q) {
   int mt, kbpu, units;
   syrk_split(m, q, mt, kbpu, units);
   const size_t dt = (((size_t)2 * q * ldk * sizeof(__nv_bfloat16)) + 255) & ~size_t(255);
-  return dt + (size_t)units * q * q * sizeof(float);
+  const size_t qp = (q + 3) / 4 * 4;  // 16-byte partial rows (TMA store)
+  return dt + (size_t)units * q * qp * sizeof(float);
 }
 
 // Sum the per-split float32 SYRK tiles in fixed split order (float64) and
 // store the lower triangle as 2^-48 fixed point.
-__global__ void syrk_reduce_kernel(const float* __restrict__ part, int units, int q,
+__global__ void syrk_reduce_kernel(const float* __restrict__ part, int units, int q, int qp,
                                    unsigned long long* __restrict__ acc) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)q * q) return;
   const int i = (int)(e / q), j = (int)(e % q);
   if (j > i) return;
   double s = 0.0;
-  for (int u = 0; u < units; ++u) s += (double)part[(size_t)u * q * q + e];
+  for (int u = 0; u < units; ++u) s += (double)part[((size_t)u * q + i) * qp + j];
   acc[q + e] += to_fix(s);
 }
 
@@ -1321,10 +1400,15 @@ int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const d
   args.tiles_per_unit = args.n_tiles;
   float* part = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) +
                                          ((((size_t)2 * q * ldk * sizeof(__nv_bfloat16)) + 255) & ~size_t(255)));
-  EpiStoreT<float> epi{part, q, q, (size_t)q * q, nullptr};
-  int rc = launch_tc<2, 2, 256>(Dt, 2ull * ldk, Dt, 2ull * ldk, (uint64_t)q, args, units, epi, st);
+  const int qp = (q + 3) / 4 * 4;
+  CUtensorMap tmc;
+  int rc = make_tmap_out<float>(&tmc, part, (uint64_t)q, (uint64_t)q, (uint64_t)units, (uint64_t)qp,
+                                (uint64_t)q * qp);
   if (rc) return rc;
-  syrk_reduce_kernel<<<cdiv((int64_t)q * q, 256), 256, 0, st>>>(part, units, q, acc);
+  EpiStoreT<float> epi{q, 0, 0};
+  rc = launch_tc<2, 2, 256>(Dt, 2ull * ldk, Dt, 2ull * ldk, (uint64_t)q, args, units, epi, st, &tmc);
+  if (rc) return rc;
+  syrk_reduce_kernel<<<cdiv((int64_t)q * q, 256), 256, 0, st>>>(part, units, q, qp, acc);
   SPA_CHECK_LAUNCH();
   return 0;
 }
@@ -1380,12 +1464,22 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
   args.ncols = q;
   args.kp = kq;
   args.m_tiles = (int)((m + kTcBM - 1) / kTcBM);
-  args.n_tiles = (q + 255) / 256;
+#ifndef SPA_PROP_TM
+#define SPA_PROP_TM 1
+#endif
+  // SPA_PROP_TM = 2: two 128-particle tiles per item share each L tile
+  // (halves the L2 -> SM traffic for L; measured slower, kept for A/B)
+  constexpr int kPropBN = SPA_PROP_TM == 1 ? 256 : 128;
+  args.n_tiles = (q + kPropBN - 1) / kPropBN;
   args.tiles_per_unit = args.n_tiles;
   args.kb_per_unit = 0;
   auto* epsb = reinterpret_cast<__nv_bfloat16*>(eps);
-  EpiStoreT<__nv_bfloat16> epi{epsb, ldb, (int)m, 0, nullptr};
-  int rc = launch_tc<1, 1, 256>(Z, (uint64_t)kq, Lb, (uint64_t)kq, (uint64_t)q, args, 1, epi, st);
+  CUtensorMap tmc;
+  int rc = make_tmap_out<__nv_bfloat16>(&tmc, epsb, (uint64_t)q, (uint64_t)m, 1, (uint64_t)ldb, (uint64_t)m * ldb);
+  if (rc) return rc;
+  EpiStoreT<__nv_bfloat16> epi{(int)m, 0, 0};
+  rc = launch_tc<1, 1, kPropBN, EpiStoreT<__nv_bfloat16>, SPA_PROP_TM>(Z, (uint64_t)kq, Lb, (uint64_t)kq, (uint64_t)q,
+                                                                      args, 1, epi, st, &tmc);
   if (rc) return rc;
   auto* Ab = reinterpret_cast<__nv_bfloat16*>(A);
   const PriorConst pc = make_prior(a, c, c);
@@ -1423,10 +1517,14 @@ int spa_tc_gemm_f32(const void* A, int64_t m, int32_t terms_a, const void* B, in
   args.n_tiles = (rows_b + 255) / 256;
   args.tiles_per_unit = args.n_tiles;
   args.kb_per_unit = 0;
-  EpiStoreAdd epi{C, C, ldc, (int)m};
+  CUtensorMap tmc;
+  int rc = make_tmap_out<float>(&tmc, C, (uint64_t)rows_b, (uint64_t)m, 1, (uint64_t)ldc, (uint64_t)m * ldc);
+  if (rc) return rc;
+  EpiStoreT<float> epi{(int)m, 0, 0};
   if (terms_a == 1)
-    return launch_tc<1, 1, 256>(A, (uint64_t)kp, B, (uint64_t)kp, (uint64_t)rows_b, args, 1, epi, as_stream(stream));
-  return launch_tc<2, 1, 256>(A, 2ull * kp, B, (uint64_t)kp, (uint64_t)rows_b, args, 1, epi, as_stream(stream));
+    return launch_tc<1, 1, 256>(A, (uint64_t)kp, B, (uint64_t)kp, (uint64_t)rows_b, args, 1, epi, as_stream(stream),
+                                &tmc);
+  return launch_tc<2, 1, 256>(A, 2ull * kp, B, (uint64_t)kp, (uint64_t)rows_b, args, 1, epi, as_stream(stream), &tmc);
 }
 
 int spa_rw_accept(float* beta, int32_t ldb, const void* eps, int32_t q, int64_t m, const double* ylin_p,

@@ -27,17 +27,16 @@ constexpr int kTcThreads = 192;
 constexpr int kTcBM = 128;
 constexpr int kTcBK = 64;  // bf16 elements per 128-byte swizzled row
 
-template <int TA, int TB, int BN>
+template <int TA, int TB, int BN, int TM = 1>
 struct TcShape {
-  static constexpr int kABytes = kTcBM * kTcBK * 2;  // 16 KB per A term
+  static constexpr int kABytes = kTcBM * kTcBK * 2;  // 16 KB per A term and m-tile
   static constexpr int kBBytes = BN * kTcBK * 2;     // per B term
-  static constexpr int kStageBytes = TA * kABytes + TB * kBBytes;
+  static constexpr int kStageBytes = TM * TA * kABytes + TB * kBBytes;
   static constexpr int kBudget = 196 * 1024;
   static constexpr int kStagesRaw = kBudget / kStageBytes;
   static constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
-  static constexpr int kScratchPerWarp = 32 * 33 * 4;  // epilogue transpose tile
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ + 4 * kScratchPerWarp;
-  static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
+  static constexpr int kRingBytes = kStages * kStageBytes;
+  static constexpr int kTmemCols = 2 * TM * BN;  // double-buffered accumulator(s)
   static_assert(kStages >= 2, "tile too large");
   static_assert(kTmemCols <= 512 && (kTmemCols & (kTmemCols - 1)) == 0, "TMEM columns must be a power of 2");
 };
@@ -53,23 +52,27 @@ struct TcArgs {
   int units;           // column (or K) units per A tile; work items = m_tiles * units
 };
 
-// Epilogue contract:
-//   begin_unit(row, unit)                       once per CTA (per thread)
-//   consume(row, col0, float v[32], ncols, scratch)
-//                                               32 consecutive columns of one row; scratch is a
-//                                               per-warp 32x33 float smem tile
-//   end_tile(row)                               after every BN tile
-//   end_unit(row, unit, m)                      once per CTA
-template <int TA, int TB, int BN, class Epi>
+// (the epilogue contract is documented with the epilogues below)
+// Dynamic shared memory: [stage ring][epilogue staging, 4 warps][barriers],
+// 1024-aligned (SW128 operands and swizzled store staging).
+template <int TA, int TB, int BN, class Epi, int TM = 1>
+constexpr int tc_smem_bytes() {
+  return TcShape<TA, TB, BN, TM>::kRingBytes + 4 * Epi::kScratchPerWarp + 1024 /*align*/ + 256 /*barriers*/;
+}
+
+template <int TA, int TB, int BN, class Epi, int TM = 1>
 __global__ void __launch_bounds__(kTcThreads, 1)
-    tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, TcArgs args,
-                   Epi epi) {
-  using S = TcShape<TA, TB, BN>;
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
+                   const __grid_constant__ CUtensorMap tmc, TcArgs args, Epi epi) {
+  using S = TcShape<TA, TB, BN, TM>;
+  static_assert(tc_smem_bytes<TA, TB, BN, Epi, TM>() <= 232448, "shared memory budget exceeded");
+  static_assert(TM == 1 || !Epi::kRowState, "TM > 1 interleaves rows: stateless epilogues only");
   extern __shared__ uint8_t smem_raw[];
   // align by pointer arithmetic on the shared array (keeps the shared
   // address space visible to the compiler: LDS/STS, not generic LD/ST)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kStages * S::kStageBytes);
+  uint8_t* staging = smem + S::kRingBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + 4 * Epi::kScratchPerWarp);
   uint64_t* empty = full + S::kStages;
   uint64_t* tfull = empty + S::kStages;
   uint64_t* tempty = tfull + 2;
@@ -82,10 +85,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   // tile, and CTAs running concurrently hold consecutive items, so each A
   // tile is read from DRAM once and re-used from L2.  The smem and TMEM
   // pipelines (stage / accumulator phases) run on across items.
+  // TM > 1: an item covers TM consecutive m-tiles that share every B tile
+  // loaded into shared memory (B traffic from L2 / TM).
   const int units = args.units;
-  const int items = args.m_tiles * units;
+  const int items = (args.m_tiles + TM - 1) / TM * units;
   auto item_range = [&](int w, int& mt, int& unit, int& nt0, int& nt1, int& kb0, int& kb1) {
-    mt = w / units;
+    mt = w / units * TM;
     unit = w % units;
     if (args.kb_per_unit > 0) {
       nt0 = 0;
@@ -133,11 +138,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           uint8_t* st = smem + s * S::kStageBytes;
           mbar_arrive_expect_tx(&full[s], S::kStageBytes);
 #pragma unroll
-          for (int t = 0; t < TA; ++t)
-            tma_load_2d(st + t * S::kABytes, &tma, &full[s], t * args.kp + kb * kTcBK, mt * kTcBM);
+          for (int tm = 0; tm < TM; ++tm)
+#pragma unroll
+            for (int t = 0; t < TA; ++t)
+              tma_load_2d(st + (tm * TA + t) * S::kABytes, &tma, &full[s], t * args.kp + kb * kTcBK,
+                          (mt + tm) * kTcBM);
 #pragma unroll
           for (int t = 0; t < TB; ++t)
-            tma_load_2d(st + TA * S::kABytes + t * S::kBBytes, &tmb, &full[s], t * args.kp + kb * kTcBK,
+            tma_load_2d(st + TM * TA * S::kABytes + t * S::kBBytes, &tmb, &full[s], t * args.kp + kb * kTcBK,
                         nt * BN);
           if (++s == S::kStages) {
             s = 0;
@@ -162,21 +170,24 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const uint32_t bph = (it >> 1) & 1;
         mbar_wait(&tempty[buf], bph ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem_base + buf * BN;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t st = smem_u32(smem + s * S::kStageBytes);
-          const uint64_t a0 = umma_desc_sw128(st);
-          const uint64_t a1 = umma_desc_sw128(st + S::kABytes);
-          const uint64_t b0 = umma_desc_sw128(st + TA * S::kABytes);
-          const uint64_t b1 = umma_desc_sw128(st + TA * S::kABytes + S::kBBytes);
+          const uint64_t b0 = umma_desc_sw128(st + TM * TA * S::kABytes);
+          const uint64_t b1 = umma_desc_sw128(st + TM * TA * S::kABytes + S::kBBytes);
 #pragma unroll
-          for (int k = 0; k < kTcBK / 16; ++k) {
-            const uint64_t adv = (uint64_t)(k * 2);  // 16 bf16 = 32 B = 2 x 16 B
-            tc_mma_f16(d, a0 + adv, b0 + adv, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
-            if (TA == 2) tc_mma_f16(d, a1 + adv, b0 + adv, idesc, 1u);
-            if (TB == 2) tc_mma_f16(d, a0 + adv, b1 + adv, idesc, 1u);
+          for (int tm = 0; tm < TM; ++tm) {
+            const uint32_t d = tmem_base + (buf * TM + tm) * BN;
+            const uint64_t a0 = umma_desc_sw128(st + tm * TA * S::kABytes);
+            const uint64_t a1 = umma_desc_sw128(st + (tm * TA + 1) * S::kABytes);
+#pragma unroll
+            for (int k = 0; k < kTcBK / 16; ++k) {
+              const uint64_t adv = (uint64_t)(k * 2);  // 16 bf16 = 32 B = 2 x 16 B
+              tc_mma_f16(d, a0 + adv, b0 + adv, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+              if (TA == 2) tc_mma_f16(d, a1 + adv, b0 + adv, idesc, 1u);
+              if (TB == 2) tc_mma_f16(d, a0 + adv, b1 + adv, idesc, 1u);
+            }
           }
           tc_commit(&empty[s]);  // frees the smem stage once these MMAs retire
           if (++s == S::kStages) {
@@ -191,7 +202,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   } else {
     // ---------------- epilogue (warps 2..5) ----------------
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-    float* scratch = reinterpret_cast<float*>(smem + S::kStages * S::kStageBytes + 256) + (warp - 2) * 32 * 33;
+    uint8_t* scratch = staging + (warp - 2) * Epi::kScratchPerWarp;
+    if (Epi::kScratchPerWarp > 0 && lane == 0) prefetch_tmap(&tmc);
     int it = 0;
     for (int w = blockIdx.x; w < items; w += gridDim.x) {
     int mt, unit, nt0, nt1, kb0, kb1;
@@ -205,16 +217,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const uint32_t bph = (it >> 1) & 1;
       mbar_wait(&tfull[buf], bph);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + buf * BN;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(taddr + c * 32, r);
-        tmem_ld_wait();
-        float v[32];
+      for (int tm = 0; tm < TM; ++tm) {
+        const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (buf * TM + tm) * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(taddr + c * 32, r);
+          tmem_ld_wait();
+          float v[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        epi.consume(row, nt * BN + c * 32, v, args.ncols, scratch);
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+          epi.consume(row + tm * kTcBM, nt * BN + c * 32, v, args.ncols, scratch, &tmc);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -223,6 +238,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     epi.end_unit(row, unit, args.m);
     }
+    epi.finish();
   }
 
   __syncthreads();
@@ -233,11 +249,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 }
 
 // ---- epilogues ------------------------------------------------------------
+// Contract (per epilogue thread; a warp's 32 threads hold 32 consecutive rows):
+//   kRowState, kScratchPerWarp (bytes of 1024-aligned smem per epilogue warp)
+//   begin_unit(row, unit) / end_tile(row) / end_unit(row, unit, m)
+//   consume(row, col0, v[32], ncols, scratch, tmc): columns col0..col0+31 of row
+//   finish()                                     once, after the last item
 
 // Likelihood: per row sum over valid columns of softplus(eta); eta never
 // leaves the SM.  Partial sums per unit are written to ws[unit][m] (float64)
 // and reduced in fixed unit order by a second kernel (deterministic).
 struct EpiSoftplusRowSum {
+  static constexpr bool kRowState = true;
+  static constexpr int kScratchPerWarp = 0;
   double* partial;
   float tile_acc;
   double acc;
@@ -245,7 +268,8 @@ struct EpiSoftplusRowSum {
     acc = 0.0;
     tile_acc = 0.0f;
   }
-  __device__ __forceinline__ void consume(int, int col0, const float (&v)[32], int ncols, float*) {
+  __device__ __forceinline__ void consume(int, int col0, const float (&v)[32], int ncols, uint8_t*,
+                                          const CUtensorMap*) {
     if (col0 + 32 <= ncols) {
       float s0 = 0.f, s1 = 0.f;
 #pragma unroll
@@ -267,101 +291,70 @@ struct EpiSoftplusRowSum {
   __device__ __forceinline__ void end_unit(int row, int unit, int m) {
     if (row < m) partial[(size_t)unit * m + row] = acc;
   }
+  __device__ __forceinline__ void finish() {}
 };
 
-// Proposal: out[row][col] = base[row][col] + v for valid rows / columns.
-struct EpiStoreAdd {
-  const float* base;
-  float* out;
-  int ld;
-  int m;
-  __device__ __forceinline__ void begin_unit(int, int) {}
-  __device__ __forceinline__ void consume(int row, int col0, const float (&v)[32], int ncols, float*) {
-    if (row >= m) return;
-    const float* b = base + (size_t)row * ld + col0;
-    float* o = out + (size_t)row * ld + col0;
-    if (col0 + 32 <= ncols && (ld & 3) == 0) {
-#pragma unroll
-      for (int i = 0; i < 32; i += 4) {
-        const float4 x = *reinterpret_cast<const float4*>(b + i);
-        *reinterpret_cast<float4*>(o + i) = make_float4(x.x + v[i], x.y + v[i + 1], x.z + v[i + 2], x.w + v[i + 3]);
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (col0 + i < ncols) o[i] = b[i] + v[i];
-    }
-  }
-  __device__ __forceinline__ void end_tile(int) {}
-  __device__ __forceinline__ void end_unit(int, int, int) {}
-};
-
-// Split-K accumulation into a 2^-48 fixed-point int64 matrix with integer
-// atomics (order-independent => bit-deterministic for any schedule).
-struct EpiFixAtomic {
-  unsigned long long* acc;  // [m][ld]
-  int ld;
-  int m;
-  int lower_only;
-  __device__ __forceinline__ void begin_unit(int, int) {}
-  __device__ __forceinline__ void consume(int row, int col0, const float (&v)[32], int ncols, float*) {
-    if (row >= m) return;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int c = col0 + i;
-      if (c < ncols && (!lower_only || c <= row))
-        atomicAdd(&acc[(size_t)row * ld + c], (unsigned long long)llrint((double)v[i] * 281474976710656.0));
-    }
-  }
-  __device__ __forceinline__ void end_tile(int) {}
-  __device__ __forceinline__ void end_unit(int, int, int) {}
-};
-
-// Raw accumulator store: each thread owns one row and writes its 32
-// consecutive columns straight from registers with 16-byte stores (64 B of
-// bf16 / 128 B of fp32 per thread per chunk; a warp's 32 rows fill whole
-// sectors).  out[unit*unit_stride + row*ld + col] = D for valid entries
-// (OutT = float or __nv_bfloat16; ld * sizeof(OutT) must be a multiple of 16
-// for the vector path, otherwise element stores are used).
+// Raw accumulator store through TMA: each thread writes its row's 32 columns
+// (64 B bf16 / 128 B fp32) into a per-warp swizzled staging tile (SW64 /
+// SW128: conflict-free 16-byte shared stores), then one lane issues a 3-D
+// bulk tensor store of the 32 x 32 box at (col0, row0, unit).  The tensor map
+// (tmc, built by the launcher) clips columns >= ncols, rows >= m and keeps
+// split-K units apart.  Two staging buffers per warp alternate; a buffer is
+// rewritten only after its previous store has finished reading it.
 template <class OutT>
 struct EpiStoreT {
-  OutT* out;
-  int ld;
+  static constexpr bool kRowState = false;
+  static constexpr int kBoxBytes = 32 * 32 * (int)sizeof(OutT);
+  static constexpr int kScratchPerWarp = 2 * kBoxBytes;
   int m;
-  size_t unit_stride;
-  OutT* base_;
-  __device__ __forceinline__ void begin_unit(int, int unit) { base_ = out + (size_t)unit * unit_stride; }
-  __device__ __forceinline__ void consume(int row, int col0, const float (&v)[32], int ncols, float*) {
-    if (row >= m) return;
-    OutT* p = base_ + (size_t)row * ld + col0;
-    const bool vec = col0 + 32 <= ncols && ((ld * sizeof(OutT)) & 15) == 0 &&
-                     ((reinterpret_cast<uintptr_t>(base_) & 15) == 0);
-    if (vec) {
-      if constexpr (sizeof(OutT) == 2) {
+  int unit_;
+  int nbuf_;
+  __device__ __forceinline__ void begin_unit(int, int unit) { unit_ = unit; }
+  __device__ __forceinline__ void consume(int row, int col0, const float (&v)[32], int, uint8_t* scratch,
+                                          const CUtensorMap* tmc) {
+    const int lane = threadIdx.x & 31;
+    const int row0 = row - lane;  // warp-uniform
+    if (row0 >= m) return;
+    uint8_t* buf = scratch + (nbuf_ & 1) * kBoxBytes;
+    ++nbuf_;
+    if (lane == 0) bulk_wait_read<1>();
+    __syncwarp();
+    if constexpr (sizeof(OutT) == 2) {
+      // 64-byte rows, SWIZZLE_64B: 16-byte chunk i of row r sits at chunk i ^ ((r >> 1) & 3)
+      const int sw = (lane >> 1) & 3;
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          uint4 u;
-          __nv_bfloat162 h0 = __floats2bfloat162_rn(v[i], v[i + 1]), h1 = __floats2bfloat162_rn(v[i + 2], v[i + 3]);
-          __nv_bfloat162 h2 = __floats2bfloat162_rn(v[i + 4], v[i + 5]), h3 = __floats2bfloat162_rn(v[i + 6], v[i + 7]);
-          u.x = *reinterpret_cast<uint32_t*>(&h0);
-          u.y = *reinterpret_cast<uint32_t*>(&h1);
-          u.z = *reinterpret_cast<uint32_t*>(&h2);
-          u.w = *reinterpret_cast<uint32_t*>(&h3);
-          *reinterpret_cast<uint4*>(p + i) = u;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      for (int i = 0; i < 4; ++i) {
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(v[8 * i], v[8 * i + 1]);
+        __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * i + 2], v[8 * i + 3]);
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * i + 4], v[8 * i + 5]);
+        __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * i + 6], v[8 * i + 7]);
+        uint4 u;
+        u.x = *reinterpret_cast<uint32_t*>(&h0);
+        u.y = *reinterpret_cast<uint32_t*>(&h1);
+        u.z = *reinterpret_cast<uint32_t*>(&h2);
+        u.w = *reinterpret_cast<uint32_t*>(&h3);
+        *reinterpret_cast<uint4*>(buf + lane * 64 + ((i ^ sw) << 4)) = u;
       }
     } else {
+      // 128-byte rows, SWIZZLE_128B: chunk i of row r sits at chunk i ^ (r & 7)
+      const int sw = lane & 7;
 #pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (col0 + i < ncols) p[i] = (OutT)v[i];
+      for (int i = 0; i < 8; ++i)
+        *reinterpret_cast<float4*>(buf + lane * 128 + ((i ^ sw) << 4)) =
+            make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_3d(tmc, buf, col0, row0, unit_);
+      bulk_commit();
     }
   }
   __device__ __forceinline__ void end_tile(int) {}
   __device__ __forceinline__ void end_unit(int, int, int) {}
+  __device__ __forceinline__ void finish() {
+    if ((threadIdx.x & 31) == 0) bulk_wait<0>();
+  }
 };
 
 }  // namespace spa

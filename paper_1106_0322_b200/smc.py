@@ -351,8 +351,9 @@ def reweight(system: ParticleSystem, prior_t: GtPrior, prior_prev: GtPrior):
 
 def _reweight_device(system: ParticleSystem, prior_t: GtPrior, prior_prev: GtPrior, group=None) -> float:
     d = system.design
-    _lib.call("spa_prior_rows", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb, float(prior_t.a),
-              float(prior_t.c), float(prior_prev.c), 1, _p(system.lw), _stream())
+    # one pass: increments lw and the log-prior lp at the new scale (the moves' lp)
+    _lib.call("spa_prior_reweight", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb,
+              float(prior_t.a), float(prior_t.c), float(prior_prev.c), _p(system.lw), _p(system.lp), _stream())
     _lib.call("spa_lse_chunk_stats", _p(system.logw), _p(system.lw), system.N, _p(system.stats), _stream())
     stats = system.stats
     nch = system.nchunks
@@ -477,9 +478,7 @@ def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int,
     zs = system.z_buffers(config.moves)
     _rw_factor(system, config.rw_scale, group)
     torch.cuda.current_stream().wait_event(z_ready)
-    # log-prior of the current particles at the new scale
-    _lib.call("spa_prior_rows", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb, float(prior.a),
-              float(prior.c), float(prior.c), 2, _p(system.lp), _stream())
+    # system.lp already holds the log-prior at the new scale (fused reweight pass)
     system.counter.zero_()
     Lb = system.factor_operand()
     for mv in range(config.moves):

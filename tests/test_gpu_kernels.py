@@ -120,6 +120,26 @@ def test_log_prior_rows(gold_loglik, s):
         np.testing.assert_allclose(out.cpu().numpy(), gold_loglik[f"c1_lp_{s}_{a}_{c}"], rtol=1e-6)
 
 
+@pytest.mark.parametrize("a", [4.0, 1.0, 0.5, float("inf")])
+def test_prior_reweight_fused(gold_loglik, a):
+    """spa_prior_reweight = prior mode 1 (increments) + mode 2 (lp at the new
+    scale, bit-identical: the MH ratio compares it with the pack kernels')."""
+    X, y, B = gold_loglik["c1_X"], gold_loglik["c1_y"], gold_loglik["c1_B_0.5"]
+    d, s = system_from(X, y, B, a=a)
+    c_prev, c = 0.9, 0.75
+    lw = torch.empty(s.N, dtype=torch.float64, device="cuda")
+    lp = torch.empty_like(lw)
+    m1, m2 = torch.empty_like(lw), torch.empty_like(lw)
+    _lib.call("spa_prior_reweight", ctypes.byref(d.struct), _p(s.beta), s.N, s.ldb, a, c, c_prev, _p(lw), _p(lp),
+              _stream())
+    _lib.call("spa_prior_rows", ctypes.byref(d.struct), _p(s.beta), s.N, s.ldb, a, c, c_prev, 1, _p(m1), _stream())
+    _lib.call("spa_prior_rows", ctypes.byref(d.struct), _p(s.beta), s.N, s.ldb, a, c, c, 2, _p(m2), _stream())
+    assert torch.equal(lp, m2)
+    np.testing.assert_allclose(lw.cpu().numpy(), m1.cpu().numpy(), rtol=1e-12, atol=1e-12)
+    Bf = B.astype(np.float32).astype(np.float64)
+    np.testing.assert_allclose(lw.cpu().numpy(), orc.reweight_increments(Bf, a, c, c_prev), rtol=1e-9, atol=1e-10)
+
+
 def test_reweight_and_ess(gold_reweight, gold_loglik):
     from paper_1106_0322_b200 import GtPrior, ess, reweight
 
