@@ -831,24 +831,28 @@ __global__ void rw_moments_kernel(const float* __restrict__ beta, int64_t m, int
 //   rw_emit_kernel       : scale, write float32 L and the bf16 operand [q][kq]
 constexpr int kPanel = 32;
 
-__global__ void rw_cov_kernel(const unsigned long long* __restrict__ acc, int q, double jitter,
-                              float* __restrict__ S) {
-  __shared__ double red[256];
-  double tr = 0.0;
-  for (int i = threadIdx.x; i < q; i += blockDim.x) tr += from_fix(acc[q + (size_t)i * q + i]);
-  red[threadIdx.x] = tr;
+// Fixed point -> float32 covariance with the trace-scaled jitter; one block
+// per row i (coalesced row writes).  Every block computes the trace with the
+// same warp-shuffle order, so all rows see the same jitter bits.
+__global__ void __launch_bounds__(256) rw_cov_kernel(const unsigned long long* __restrict__ acc, int q,
+                                                     double jitter, float* __restrict__ S) {
+  __shared__ double s_add;
+  const int i = blockIdx.x;
+  if (threadIdx.x < 32) {
+    double tr = 0.0;
+    for (int d = threadIdx.x; d < q; d += 32) tr += from_fix(acc[q + (size_t)d * q + d]);
+    tr = warp_sum(tr);
+    if (threadIdx.x == 0) {
+      const double t = tr / q;
+      s_add = jitter * (t > 0 ? t : 1.0) + 1e-30;
+    }
+  }
   __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-    __syncthreads();
-  }
-  const double t = red[0] / q;
-  const double add = jitter * (t > 0 ? t : 1.0) + 1e-30;
-  const int64_t total = (int64_t)q * q;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(e / q), j = (int)(e % q);
-    S[e] = (j > i) ? 0.f : (float)(from_fix(acc[q + e]) + (i == j ? add : 0.0));
-  }
+  const double add = s_add;
+  const unsigned long long* row = acc + q + (size_t)i * q;
+  float* out = S + (size_t)i * q;
+  for (int j = threadIdx.x; j < q; j += blockDim.x)
+    out[j] = (j > i) ? 0.f : (float)(from_fix(row[j]) + (i == j ? add : 0.0));
 }
 
 __global__ void __launch_bounds__(32) rw_chol_diag_kernel(float* __restrict__ S, int q, int jb,
@@ -1340,7 +1344,9 @@ static void syrk_split(int64_t m, int q, int& m_tiles, int& kb_per_unit, int& un
   const int64_t ldk = (m + 63) / 64 * 64;
   const int kblocks = (int)(ldk / kTcBK);
   m_tiles = (q + kTcBM - 1) / kTcBM;
-  units = std::max(1, std::min(kblocks, (2 * 148 + m_tiles - 1) / m_tiles));
+  // one wave of work items (m_tiles x units ~ 148): fewer split partials to
+  // write and reduce than two waves, same tensor work per CTA
+  units = std::max(1, std::min(kblocks, 148 / m_tiles));
   kb_per_unit = (kblocks + units - 1) / units;
   units = (kblocks + kb_per_unit - 1) / kb_per_unit;
 }
@@ -1424,7 +1430,7 @@ int spa_rw_factor(const int64_t* partial, int32_t q, double scale, double jitter
   float* inv = reinterpret_cast<float*>(base + (((size_t)8 * q * q + 255) & ~size_t(255)) +
                                         (((size_t)2 * q * kq + 255) & ~size_t(255)));
   if (info) SPA_CHECK_CUDA(cudaMemsetAsync(info, 0, sizeof(int), st));
-  rw_cov_kernel<<<std::min<unsigned>(cdiv((int64_t)q * q, 256), 1184), 256, 0, st>>>(
+  rw_cov_kernel<<<q, 256, 0, st>>>(
       reinterpret_cast<const unsigned long long*>(partial), q, jitter, S);
   SPA_CHECK_LAUNCH();
   SPA_CHECK_CUDA(chol_graph_launch(S, q, inv, info, st));

@@ -302,6 +302,41 @@ def test_rw_moments_and_factor(name):
     assert np.allclose(np.triu(L, 1), 0.0)
 
 
+@pytest.mark.parametrize("q", [5, 33, 100, 500, 512, 520, 700])
+def test_rw_factor_paths(q):
+    """spa_rw_factor (blocked Cholesky, graph of panel kernels) on a
+    fixed-point SPD matrix vs numpy, including partial panels and q > 512;
+    the scaled bf16 operand is L * scale/sqrt(q) with zero padding columns."""
+    from paper_1106_0322_b200.smc import _round_up
+
+    rng = np.random.default_rng(q)
+    G = rng.normal(size=(q, q + 8)) / np.sqrt(q)
+    S = G @ G.T + 0.05 * np.eye(q)
+    Sfix = np.rint(np.tril(S) * 2.0**48).astype(np.int64)
+    acc = torch.zeros(q + q * q, dtype=torch.int64)
+    acc[q:] = torch.from_numpy(Sfix.reshape(-1))
+    acc = acc.cuda()
+    kq = _round_up(q, 64)
+    L = torch.zeros((q, q), dtype=torch.float32, device="cuda")
+    fws = torch.zeros((_round_up(8 * q * q, 256) + _round_up(2 * q * kq, 256) + 8192) // 8 + 1, dtype=torch.float64,
+                      device="cuda")
+    info = torch.zeros(1, dtype=torch.int32, device="cuda")
+    jitter, scale = 1e-6, 2.38
+    _lib.call("spa_rw_factor", _p(acc), q, scale, jitter, _p(L), _p(fws), _p(info), _stream())
+    assert int(info.item()) == 0
+    Sref = np.tril(Sfix).astype(np.float64) / 2.0**48
+    Sref = Sref + np.tril(Sref, -1).T
+    Sref[np.diag_indices(q)] += jitter * np.trace(Sref) / q
+    Lref = np.linalg.cholesky(Sref) * (scale / np.sqrt(q))
+    Lg = L.cpu().numpy().astype(np.float64)
+    assert np.allclose(np.triu(Lg, 1), 0.0)
+    np.testing.assert_allclose(Lg, Lref, rtol=0, atol=2e-5 * np.abs(Lref).max())
+    off = _round_up(8 * q * q, 256)
+    Lb = fws.view(torch.uint8)[off: off + 2 * q * kq].view(torch.bfloat16).view(q, kq).float().cpu().numpy()
+    np.testing.assert_array_equal(Lb[:, :q], torch.from_numpy(L.cpu().numpy()).to(torch.bfloat16).float().numpy())
+    assert not Lb[:, q:].any()
+
+
 def test_rw_propose_and_accept_vs_oracle():
     """One RW move: proposal (Philox normals, L z on tcgen05, fused pack),
     K1 likelihood of the proposal and the MH decision vs the oracle."""
