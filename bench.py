@@ -241,7 +241,7 @@ def main():
 
     data, _ = simulate_dataset(named_spec(args.config))
     Ntot = args.particles * ws
-    cfg = S.SmcConfig(N=Ntot, move_kernel="rw", moves=MOVES, seed=0, init_burn=200, init_thin=5, init_chains=1024)
+    cfg = S.SmcConfig(N=Ntot, move_kernel="rw", moves=MOVES, seed=0, init_burn=200, init_thin=5)
     sched = S.make_schedule(*SCHED)
     assert args.warmup + args.steps + 1 <= sched.T
     design = DeviceDesign.build(data.X, data.y, False)
@@ -300,7 +300,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         cfg_e = S.SmcConfig(N=Ntot, move_kernel="rw", moves=MOVES, seed=1, init_burn=200, init_thin=5,
-                            init_chains=1024, snapshot_thin=10)
+                            snapshot_thin=10)
         sched_e = S.make_schedule(*SCHED)  # the full 100-step lambda path
         torch.cuda.synchronize()
         if group is not None:

@@ -137,10 +137,17 @@ int spa_gather_rows(const float* src, int32_t ld_src, float* dst, int32_t ld_dst
  * keyed (seed, tag, t, i0+k); sweep s draws from block index s*q + j
  * (Philox counter index + 1, the NumPy convention).
  * Writes ll (log-likelihood) and lp (log-prior at c) of the final state,
- * and adds the number of accepted updates to *accepted (device u64). */
+ * and adds the number of accepted updates to *accepted (device u64), or,
+ * with per_particle != 0, particle k's count to accepted[k]. */
+/* Chains (CTAs) of spa_mwg_move resident at once on the current device for
+ * this design (occupancy x SMs); init_particles sizes its parallel chains to
+ * one such wave (the reference's single init chain, smc.py:202-245, is
+ * replaced by parallel chains). */
+int spa_mwg_resident_chains(const spa_design* d, int64_t* chains);
+
 int spa_mwg_move(const spa_design* d, float* beta, int64_t m, int32_t ldb, double a, double c, double step_sd,
                  int32_t cycles, uint64_t seed, int32_t tag, int64_t t, int64_t i0, int64_t sweep0, double* ll,
-                 double* lp, unsigned long long* accepted, void* stream);
+                 double* lp, unsigned long long* accepted, int32_t per_particle, void* stream);
 
 /* ---- K8: population random-walk moves (north-star kernel) --------------
  * Weighted moments into an int64 fixed-point (2^-48) accumulator

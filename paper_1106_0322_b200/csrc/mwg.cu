@@ -46,6 +46,7 @@ struct MwgParams {
   double* ll;
   double* lp;
   unsigned long long* accepted;
+  int per_particle;  // accepted[row] instead of one total
 };
 
 __device__ __forceinline__ double mwg_gt(double b, const MwgParams& P) {
@@ -269,7 +270,10 @@ __global__ void __launch_bounds__(512) mwg_kernel(MwgParams P) {
   if (tid == 0) {
     P.ll[row] = ll;
     if (P.lp) P.lp[row] = lp;
-    atomicAdd(P.accepted, acc);
+    if (P.per_particle)
+      P.accepted[row] += acc;
+    else
+      atomicAdd(P.accepted, acc);
   }
 }
 
@@ -284,9 +288,30 @@ static int pick_s(int n) {
 
 using namespace spa;
 
+// Chains (one CTA each) resident at once on the current device: the
+// occupancy of the kernel variant spa_mwg_move would launch for this design
+// times the SM count.  Initialisation sizes its parallel chains to one wave.
+extern "C" int spa_mwg_resident_chains(const spa_design* d, int64_t* chains) {
+  SPA_REQUIRE(d && chains && d->q >= 1 && d->q <= 2048, kBadArgument, "spa_mwg_resident_chains: bad arguments");
+  const int S = pick_s(d->n);
+  SPA_REQUIRE(S > 0, kNotSupported, "spa_mwg_resident_chains: n > 16384 not supported");
+  const int nthr = std::max(32, ((d->n + S - 1) / S + 31) / 32 * 32);
+  const size_t smem = (size_t)d->q * sizeof(CoordSlot) + (size_t)((d->q + 1) & ~1) * sizeof(float) +
+                      64 * sizeof(double) + 64 * sizeof(float);
+  int per_sm = 0, dev = 0, nsm = 0;
+  const void* fn = S == 8 ? (const void*)mwg_kernel<8> : S == 16 ? (const void*)mwg_kernel<16> : (const void*)mwg_kernel<32>;
+  SPA_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SPA_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nthr, smem));
+  SPA_CHECK_CUDA(cudaGetDevice(&dev));
+  SPA_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  *chains = (int64_t)std::max(1, per_sm) * nsm;
+  return 0;
+}
+
 extern "C" int spa_mwg_move(const spa_design* d, float* beta, int64_t m, int32_t ldb, double a, double c,
                             double step_sd, int32_t cycles, uint64_t seed, int32_t tag, int64_t t, int64_t i0,
-                            int64_t sweep0, double* ll, double* lp, unsigned long long* accepted, void* stream) {
+                            int64_t sweep0, double* ll, double* lp, unsigned long long* accepted,
+                            int32_t per_particle, void* stream) {
   SPA_REQUIRE(d && beta && ll && accepted && m >= 0 && cycles >= 0, kBadArgument, "spa_mwg_move: bad arguments");
   SPA_REQUIRE(a > 0 && c > 0 && step_sd > 0, kBadArgument, "spa_mwg_move: a, c, step_sd must be positive");
   SPA_REQUIRE(d->q >= 1 && d->q <= 2048, kNotSupported, "spa_mwg_move: q must lie in [1, 2048]");
@@ -312,6 +337,7 @@ extern "C" int spa_mwg_move(const spa_design* d, float* beta, int64_t m, int32_t
   P.ll = ll;
   P.lp = lp;
   P.accepted = accepted;
+  P.per_particle = per_particle;
   const int nthr_raw = (d->n + S - 1) / S;
   const int nthr = std::max(32, (nthr_raw + 31) / 32 * 32);
   SPA_REQUIRE(nthr <= 1024, kNotSupported, "spa_mwg_move: too many subjects per particle");

@@ -406,13 +406,18 @@ def _resample_device(system: ParticleSystem, u: float, group=None) -> torch.Tens
 
 
 def _mwg(system: ParticleSystem, prior: GtPrior, sd: float, cycles: int, seed: int, tag: int, t: int,
-         sweep0: int = 0) -> int:
+         sweep0: int = 0, counts: torch.Tensor | None = None):
+    """`cycles` MwG sweeps; returns the accepted count (host int), or, given
+    a per-particle int64 `counts` tensor, adds each particle's count to it
+    on the device (no sync)."""
     d = system.design
-    system.counter.zero_()
+    if counts is None:
+        system.counter.zero_()
     _lib.call("spa_mwg_move", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb, float(prior.a),
               float(prior.c), float(sd), int(cycles), int(seed), int(tag), int(t), int(system.i0), int(sweep0),
-              _p(system.ll), _p(system.lp), _p(system.counter), _stream())
-    return int(system.counter.item())
+              _p(system.ll), _p(system.lp), _p(system.counter if counts is None else counts),
+              0 if counts is None else 1, _stream())
+    return None if counts is not None else int(system.counter.item())
 
 
 def _loglik_device(system: ParticleSystem, out: torch.Tensor):
@@ -502,40 +507,74 @@ def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int,
 # initialisation (reference smc.py:202-245, as parallel chains)
 
 
+def resident_chains(design: DeviceDesign) -> int:
+    """MwG chains (one CTA each) resident at once on this GPU for `design`."""
+    out = ctypes.c_int64(0)
+    _lib.call("spa_mwg_resident_chains", ctypes.byref(design.struct), ctypes.byref(out))
+    return int(out.value)
+
+
+def init_plan(N_total: int, init_chains: int, chains_auto: int) -> tuple[int, int]:
+    """(K chains, R slots per chain): chain c fills the contiguous slots
+    [c R, min((c+1) R, N)).  K = init_chains, else one resident wave per GPU
+    (`chains_auto`); R = ceil(N / K), then K = ceil(N / R)."""
+    K = max(1, min(N_total, init_chains or chains_auto))
+    R = -(-N_total // K)
+    return -(-N_total // R), R
+
+
 def init_particles(data, prior_at_b1: GtPrior, config: SmcConfig, intercept: bool = False, design=None,
                    group=None):
     """Seed the particles from MwG chains targeting the first posterior.
 
     The reference runs ONE chain (init_burn sweeps, then every init_thin-th
-    state).  Here K = config.init_chains (auto: min(N, 1024)) independent
-    chains run in parallel on the GPU, each burning init_burn sweeps and then
-    contributing every init_thin-th state; chain c keyed (seed, 0, 0, c).
+    state; smc.py:202-245).  Here K independent chains run in parallel, chain
+    c keyed (seed, 0, 0, c): each burns init_burn sweeps, then its state after
+    every further init_thin sweeps fills its next slot of the contiguous block
+    [c R, (c+1) R).  Total chain-sweeps K*init_burn + N*init_thin; K defaults
+    to one resident wave of chains per GPU (spa_mwg_resident_chains x ranks),
+    which minimises the wall time of these latency-bound sweeps.  A rank
+    simulates only the chains whose blocks meet its shard, so for a given K
+    the particles are identical for any number of GPUs.
     Returns (system, acceptance_rate)."""
     _require_cuda()
     if design is None:
         design = DeviceDesign.build(data.X, data.y, intercept)
     N_total = config.N
+    world = 1 if group is None else group.world
     shard, offset = (N_total, 0) if group is None else group.shard(N_total)
     system = ParticleSystem(design, shard, prior_at_b1.a, intercept, rank_offset=offset, N_total=N_total)
-    K = config.init_chains or min(N_total, 1024)
-    K = max(1, min(K, N_total))
-    chains = ParticleSystem(design, K, prior_at_b1.a, intercept)
-    acc = _mwg(chains, prior_at_b1, config.step_sd, config.init_burn, config.seed, TAG_INIT, 0, 0) \
-        if config.init_burn > 0 else 0
-    rounds = -(-N_total // K)
+    auto = 0 if config.init_chains else resident_chains(design) * world
+    K, R = init_plan(N_total, config.init_chains, auto)
+    lo, hi = offset, offset + shard
+    c0, c1 = lo // R, min(K, -(-hi // R))  # chains whose slot blocks meet [lo, hi)
+    chains = ParticleSystem(design, c1 - c0, prior_at_b1.a, intercept, rank_offset=c0)
+    Kl = c1 - c0
+    counts = torch.zeros(Kl, dtype=torch.int64, device=system.device)  # per chain, read once at the end
+    if config.init_burn > 0:
+        _mwg(chains, prior_at_b1, config.step_sd, config.init_burn, config.seed, TAG_INIT, 0, 0, counts=counts)
+    stage_b = torch.empty((Kl, R, system.ldb), dtype=torch.float32, device=system.device)
+    stage_l = torch.empty((Kl, R), dtype=torch.float64, device=system.device)
+    stage_p = torch.empty((Kl, R), dtype=torch.float64, device=system.device)
     sweeps = config.init_burn
-    lo_mine, hi_mine = offset, offset + shard
-    for r in range(rounds):
-        acc += _mwg(chains, prior_at_b1, config.step_sd, config.init_thin, config.seed, TAG_INIT, 0, sweeps)
+    for j in range(R):
+        _mwg(chains, prior_at_b1, config.step_sd, config.init_thin, config.seed, TAG_INIT, 0, sweeps, counts=counts)
         sweeps += config.init_thin
-        # slots r*K .. r*K+K-1 take chain states 0..K-1 (only those in this shard)
-        s0, s1 = r * K, min(N_total, (r + 1) * K)
-        a, b = max(s0, lo_mine), min(s1, hi_mine)
-        if a < b:
-            system.beta[a - offset:b - offset].copy_(chains.beta[a - s0:b - s0])
-            system.ll[a - offset:b - offset].copy_(chains.ll[a - s0:b - s0])
-            system.lp[a - offset:b - offset].copy_(chains.lp[a - s0:b - s0])
-    total = K * (config.init_burn + rounds * config.init_thin) * design.q
+        stage_b[:, j].copy_(chains.beta)
+        stage_l[:, j].copy_(chains.ll)
+        stage_p[:, j].copy_(chains.lp)
+    a, b = lo - c0 * R, hi - c0 * R  # this shard inside the staged slots [c0 R, c1 R)
+    system.beta.copy_(stage_b.view(Kl * R, system.ldb)[a:b])
+    system.ll.copy_(stage_l.view(-1)[a:b])
+    system.lp.copy_(stage_p.view(-1)[a:b])
+    del stage_b, stage_l, stage_p
+    # acceptance over the chains this rank owns (first slot in its shard), so
+    # every chain counts once for any number of ranks
+    own = torch.arange(c0, c1, device=system.device) * R >= lo
+    tally = torch.stack([counts[own].sum(), own.sum() * (config.init_burn + R * config.init_thin) * design.q])
+    if group is not None:
+        tally = group.all_reduce_sum(tally)
+    acc, total = (int(v) for v in tally.tolist())
     return system, acc / max(total, 1)
 
 

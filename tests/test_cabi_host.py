@@ -134,3 +134,21 @@ def test_persistence_round_trip(tmp_path):
         np.testing.assert_array_equal(s1.particles, s2.particles)
         np.testing.assert_array_equal(s1.weights, s2.weights)
     assert (tmp_path / "run" / "trace.csv").read_text().splitlines()[0] == "t,b,ess,log_z_ratio_cum,acceptance_rate"
+
+
+def test_init_plan_covers_slots_once():
+    """Chain c fills slots [c R, (c+1) R): every slot exactly once, K * R >= N,
+    and a rank's chain range covers its shard for any world size."""
+    from paper_1106_0322_b200.smc import init_plan
+
+    for N, chains, auto in [(65536, 0, 444), (8192, 300, 0), (1000, 0, 4096), (7, 0, 3), (1, 0, 5)]:
+        K, R = init_plan(N, chains, auto)
+        assert K * R >= N > (K - 1) * R
+        for world in (1, 2, 4):
+            if N % world:
+                continue
+            M = N // world
+            for r in range(world):
+                lo, hi = r * M, (r + 1) * M
+                c0, c1 = lo // R, min(K, -(-hi // R))
+                assert c0 * R <= lo and hi <= c1 * R

@@ -32,8 +32,10 @@ def _port():
 def _cfg(kernel):
     from paper_1106_0322_b200 import SmcConfig
 
+    # init_chains pinned (the automatic count scales with the number of GPUs);
+    # 293 chains x 28 slots: a chain's slot block straddles the shard boundary
     return SmcConfig(N=8192, cycles=2, moves=3, seed=5, init_burn=30, init_thin=1, move_kernel=kernel,
-                     ess_threshold_frac=0.9)
+                     ess_threshold_frac=0.9, init_chains=300)
 
 
 def _run(group, kernel):

@@ -12,7 +12,7 @@ from paper_1106_0322_b200.design import DeviceDesign  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 data, _ = simulate_dataset(named_spec(name))
 d = DeviceDesign.build(data.X, data.y)
-s = S.ParticleSystem(d, 1024, 1.0)
+s = S.ParticleSystem(d, int(sys.argv[2]) if len(sys.argv) > 2 else S.resident_chains(d), 1.0)
 S._mwg(s, S.GtPrior(1.0, 2.0), 0.5, 2, 0, 0, 0, 0)
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
