@@ -292,9 +292,14 @@ def main():
     tpath = os.path.join(ROOT, "profiles", "k1_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("bytes_per_launch")
+            tj = json.load(open(tpath))
+            # the ncu capture is per workload: only report it for the one it measured
+            if tj.get("workload", "c3") == args.config and int(tj.get("particles", 65536)) == args.particles:
+                traffic = tj.get("bytes_per_launch")
         except Exception:
             traffic = None
+    beta_mb = args.particles * system.ldb * 4 / 1e6
+    a_mb = args.particles * 2 * system.design.kp * 2 / 1e6
 
     # end to end through the public API (host Dataset in, host SmcOutput out)
     e2e = None
@@ -340,7 +345,7 @@ def main():
         "config": {"workload": f"{args.config}: n={n} p={p} N={args.particles}/GPU a={A_DOF} b_t=2*0.98^(t-1) "
                                f"moves={MOVES} (RW population covariance)",
                    "particles_total": Ntot, "lambda_steps_timed": f"t={t - args.steps}..{t - 1}",
-                   "resampling_steps_timed": resampled, "l2": "inputs larger than L2 (beta 131 MB + A 131 MB)",
+                   "resampling_steps_timed": resampled, "l2": f"inputs larger than L2 (beta {beta_mb:.0f} MB + A {a_mb:.0f} MB per GPU vs 126 MB L2)",
                    "init": "excluded (parallel MwG chains, 200 burn sweeps)", "parallelism": f"dp{ws} particles"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": "tc_gemm_kernel<2,1,256,Softplus> (K1)",

@@ -281,9 +281,10 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const 
 // so the next row streams in while the current one is packed and no load
 // data lives in registers.  IT = kp/128 groups of 4 columns per lane.
 constexpr int kPackWarps = 8;
+constexpr int kPackSlots = 3;  // rows in flight per warp (current + 2 ahead)
 
 __host__ __device__ inline size_t pack_eps_smem_bytes(int kp, int ldb) {
-  return (size_t)16 * kp + (size_t)kPackWarps * 2 * ((size_t)ldb * 6);
+  return (size_t)16 * kp + (size_t)kPackWarps * kPackSlots * ((size_t)ldb * 6);
 }
 
 template <int IT>
@@ -293,14 +294,14 @@ __global__ void __launch_bounds__(32 * kPackWarps) pack_eps_kernel(spa_design d,
                                                                 double* __restrict__ ylin, PriorConst pc,
                                                                 double* __restrict__ lp) {
   extern __shared__ float4 csm[];  // [kp] x {alpha, sy, gamma, pen}, then the row rings
-  __shared__ uint64_t bars[kPackWarps][2];
+  __shared__ uint64_t bars[kPackWarps][kPackSlots];
   float* ca = reinterpret_cast<float*>(csm);
   float* cs = ca + d.kp;
   float* cg = cs + d.kp;
   float* cp = cg + d.kp;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rowB = (uint32_t)ldb * 4, slotB = (uint32_t)ldb * 6;
-  uint8_t* ring = reinterpret_cast<uint8_t*>(cp + d.kp) + (size_t)warp * 2 * slotB;
+  uint8_t* ring = reinterpret_cast<uint8_t*>(cp + d.kp) + (size_t)warp * kPackSlots * slotB;
   for (int j = threadIdx.x; j < d.kp; j += blockDim.x) {
     const bool v = j < d.q;
     ca[j] = v ? (d.coded ? (float)d.alpha[j] : 1.0f) : 0.f;
@@ -309,8 +310,7 @@ __global__ void __launch_bounds__(32 * kPackWarps) pack_eps_kernel(spa_design d,
     cp[j] = (v && d.penalized[j]) ? 1.f : 0.f;
   }
   if (lane == 0) {
-    mbar_init(&bars[warp][0], 1);
-    mbar_init(&bars[warp][1], 1);
+    for (int sl = 0; sl < kPackSlots; ++sl) mbar_init(&bars[warp][sl], 1);
     fence_barrier_init();
   }
   __syncthreads();
@@ -323,15 +323,13 @@ __global__ void __launch_bounds__(32 * kPackWarps) pack_eps_kernel(spa_design d,
       bulk_g2s(ring + s * slotB + rowB, eps + row * ldb, slotB - rowB, &bars[warp][s]);
     }
   };
-  if (lane == 0) {
-    issue(warp0, 0);
-    issue(warp0 + nwarps, 1);
-  }
+  if (lane == 0)
+    for (int sl = 0; sl < kPackSlots; ++sl) issue(warp0 + sl * nwarps, sl);
   const double K = pc.de ? 0.0 : 1.0 / (pc.a * pc.c);
   const bool full = (d.q % 4 == 0);  // every 4-column group is either all-valid or all-padding
   uint32_t phase = 0;                // bit s = parity of slot s
   int s = 0;
-  for (int64_t row = warp0; row < m; row += nwarps, s ^= 1) {
+  for (int64_t row = warp0; row < m; row += nwarps, s = (s + 1 == kPackSlots) ? 0 : s + 1) {
     mbar_wait(&bars[warp][s], (phase >> s) & 1u);
     phase ^= 1u << s;
     const float* b = reinterpret_cast<const float*>(ring + s * slotB);
@@ -384,7 +382,7 @@ __global__ void __launch_bounds__(32 * kPackWarps) pack_eps_kernel(spa_design d,
     __syncwarp();  // every lane is done with slot s: refill it
     if (lane == 0) {
       fence_proxy_async_smem();
-      issue(row + 2 * nwarps, s);
+      issue(row + kPackSlots * nwarps, s);
     }
     yl = warp_sum(yl);
     off = warp_sum(off);
@@ -482,6 +480,7 @@ __global__ void prior_kernel(spa_design d, const float* __restrict__ beta, int64
 // particles gives both the incremental weights lw = sum_j gt(c) - gt(c_prev)
 // and lp = sum_j gt(c) in the LpAcc arithmetic of prior mode 2 / the pack
 // kernels (bit-identical to them), which the move kernels need next.
+template <int IT>
 __global__ void __launch_bounds__(256) prior_reweight_kernel(spa_design d, const float* __restrict__ beta, int64_t m,
                                                              int ldb, PriorConst pc, double* __restrict__ lw,
                                                              double* __restrict__ lp) {
@@ -491,15 +490,23 @@ __global__ void __launch_bounds__(256) prior_reweight_kernel(spa_design d, const
   const float* b = beta + row * ldb;
   const double K1 = pc.de ? 0.0 : 1.0 / (pc.a * pc.c), K2 = pc.de ? 0.0 : 1.0 / (pc.a * pc.c_prev);
   const bool full = (d.q % 4 == 0) && (ldb % 4 == 0);
+  float4 xv[IT];  // all of the row's loads in flight before any arithmetic
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const int j0 = it * 128 + lane * 4;
+    if (full && j0 + 4 <= d.q) xv[it] = __ldcs(reinterpret_cast<const float4*>(b + j0));
+  }
   LpAcc la, lb;
-  for (int j0 = lane * 4; j0 < d.kp; j0 += 128) {
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const int j0 = it * 128 + lane * 4;
+    if (j0 >= d.kp) break;
     float x[4], pen[4];
     if (full && j0 + 4 <= d.q) {
-      const float4 v = __ldcs(reinterpret_cast<const float4*>(b + j0));
-      x[0] = v.x;
-      x[1] = v.y;
-      x[2] = v.z;
-      x[3] = v.w;
+      x[0] = xv[it].x;
+      x[1] = xv[it].y;
+      x[2] = xv[it].z;
+      x[3] = xv[it].w;
     } else {
 #pragma unroll
       for (int i = 0; i < 4; ++i) x[i] = j0 + i < d.q ? b[j0 + i] : 0.f;
@@ -1073,12 +1080,16 @@ __global__ void __launch_bounds__(256) rw_accept_kernel(float* __restrict__ beta
                                                          const double* __restrict__ lp_p, double* __restrict__ ll,
                                                          double* __restrict__ lp, uint64_t seed, int64_t t, int64_t i0,
                                                          int move, unsigned long long* accepted) {
-  // one warp per particle: lane 0 decides, the warp applies beta += eps
-  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // one warp per 32 consecutive particles: lane l decides particle base + l
+  // (coalesced loads, Philox and the float64 log in parallel), then the warp
+  // walks the ballot of accepted rows applying beta += eps with vector
+  // accesses; one counter atomic per warp
+  const int64_t base = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
   const int lane = threadIdx.x & 31;
-  if (row >= m) return;
-  int ok = 0;
-  if (lane == 0) {
+  if (base >= m) return;
+  const int64_t row = base + lane;
+  bool ok = false;
+  if (row < m) {
     uint32_t w[4] = {0xFFFFFFFFu, (uint32_t)(i0 + row), (uint32_t)t, (uint32_t)move | (3u << 24)};
     philox4x32_10(w, (uint32_t)seed, (uint32_t)(seed >> 32));
     const double u = (double)(((uint64_t)w[0] << 21) | (w[1] >> 11)) * 0x1.0p-53;
@@ -1089,27 +1100,58 @@ __global__ void __launch_bounds__(256) rw_accept_kernel(float* __restrict__ beta
     if (ok) {
       ll[row] = llp;
       lp[row] = lpp;
-      atomicAdd(accepted, 1ull);
     }
   }
-  ok = __shfl_sync(0xffffffffu, ok, 0);
-  if (!ok) return;
-  float* o = beta + row * ldb;
-  const __nv_bfloat16* s = eps + row * ldb;
-  if ((q % 4 == 0) && (ldb % 4 == 0)) {  // beta' = beta + eps, the same float32 sum the pack used
-    for (int j = lane * 4; j < q; j += 128) {
-      float4 x = *reinterpret_cast<const float4*>(o + j);
-      const uint2 yv = *reinterpret_cast<const uint2*>(s + j);
-      const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&yv);
-      const float2 ya = __bfloat1622float2(y2[0]), yb = __bfloat1622float2(y2[1]);
-      x.x += ya.x;
-      x.y += ya.y;
-      x.z += yb.x;
-      x.w += yb.y;
-      *reinterpret_cast<float4*>(o + j) = x;
+  unsigned mask = __ballot_sync(0xffffffffu, ok);
+  if (lane == 0 && mask) atomicAdd(accepted, (unsigned long long)__popc(mask));
+  if ((q % 4 == 0) && (ldb % 4 == 0) && q <= 512) {
+    // beta' = beta + eps (the same float32 sum the pack used), accepted rows
+    // taken 4 at a time with all their loads in flight before any store
+    constexpr int kR = 4, kV = 4;  // rows per batch, float4 per lane per row (q <= 512)
+    while (mask) {
+      int rows[kR];
+#pragma unroll
+      for (int b = 0; b < kR; ++b) {
+        rows[b] = mask ? __ffs(mask) - 1 : -1;
+        if (mask) mask &= mask - 1;
+      }
+      float4 x[kR][kV];
+      uint2 y[kR][kV];
+#pragma unroll
+      for (int b = 0; b < kR; ++b)
+#pragma unroll
+        for (int v = 0; v < kV; ++v) {
+          const int j = (v * 32 + lane) * 4;
+          if (rows[b] >= 0 && j < q) {
+            x[b][v] = *reinterpret_cast<const float4*>(beta + (base + rows[b]) * ldb + j);
+            y[b][v] = *reinterpret_cast<const uint2*>(eps + (base + rows[b]) * ldb + j);
+          }
+        }
+#pragma unroll
+      for (int b = 0; b < kR; ++b)
+#pragma unroll
+        for (int v = 0; v < kV; ++v) {
+          const int j = (v * 32 + lane) * 4;
+          if (rows[b] >= 0 && j < q) {
+            const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&y[b][v]);
+            const float2 ya = __bfloat1622float2(y2[0]), yb = __bfloat1622float2(y2[1]);
+            float4 o = x[b][v];
+            o.x += ya.x;
+            o.y += ya.y;
+            o.z += yb.x;
+            o.w += yb.y;
+            *reinterpret_cast<float4*>(beta + (base + rows[b]) * ldb + j) = o;
+          }
+        }
     }
   } else {
-    for (int j = lane; j < q; j += 32) o[j] = o[j] + __bfloat162float(s[j]);
+    while (mask) {
+      const int r = __ffs(mask) - 1;
+      mask &= mask - 1;
+      float* o = beta + (base + r) * ldb;
+      const __nv_bfloat16* e = eps + (base + r) * ldb;
+      for (int j = lane; j < q; j += 32) o[j] = o[j] + __bfloat162float(e[j]);
+    }
   }
 }
 
@@ -1284,8 +1326,19 @@ int spa_prior_reweight(const spa_design* d, const float* beta, int64_t m, int32_
   SPA_REQUIRE(d && beta && lw && lp && m >= 0, kBadArgument, "spa_prior_reweight: bad arguments");
   SPA_REQUIRE(a > 0 && c > 0 && c_prev > 0, kBadArgument, "spa_prior_reweight: a, c must be positive");
   if (m == 0) return 0;
-  prior_reweight_kernel<<<cdiv(m, 8), 256, 0, as_stream(stream)>>>(*d, beta, m, ldb, make_prior(a, c, c_prev), lw,
-                                                                   lp);
+  const PriorConst pc = make_prior(a, c, c_prev);
+  cudaStream_t st = as_stream(stream);
+  const unsigned grid = (unsigned)cdiv(m, 8);
+  if (d->kp <= 128)
+    prior_reweight_kernel<1><<<grid, 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);
+  else if (d->kp <= 256)
+    prior_reweight_kernel<2><<<grid, 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);
+  else if (d->kp <= 512)
+    prior_reweight_kernel<4><<<grid, 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);
+  else if (d->kp <= 1024)
+    prior_reweight_kernel<8><<<grid, 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);
+  else
+    prior_reweight_kernel<32><<<grid, 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);
   SPA_CHECK_LAUNCH();
   return 0;
 }
@@ -1538,8 +1591,9 @@ int spa_rw_accept(float* beta, int32_t ldb, const void* eps, int32_t q, int64_t 
                   int64_t i0, int32_t move, unsigned long long* accepted, void* stream) {
   SPA_REQUIRE(beta && eps && ylin_p && sp_p && lp_p && ll && lp && accepted && m > 0, kBadArgument,
               "spa_rw_accept: bad arguments");
-  rw_accept_kernel<<<cdiv(m, 8), 256, 0, as_stream(stream)>>>(beta, ldb, reinterpret_cast<const __nv_bfloat16*>(eps), q, m, ylin_p, sp_p, lp_p, ll, lp, seed,
-                                                             t, i0, move, accepted);
+  rw_accept_kernel<<<cdiv(m, 256), 256, 0, as_stream(stream)>>>(beta, ldb, reinterpret_cast<const __nv_bfloat16*>(eps),
+                                                               q, m, ylin_p, sp_p, lp_p, ll, lp, seed, t, i0, move,
+                                                               accepted);
   SPA_CHECK_LAUNCH();
   return 0;
 }

@@ -37,6 +37,15 @@ def timeit(name, fn, reps=20):
     print(f"{name:28s} {e0.elapsed_time(e1) / reps * 1e3:9.1f} us")
 
 
+t0 = torch.cuda.Event(enable_timing=True)
+t1 = torch.cuda.Event(enable_timing=True)
+t0.record()
+for t in range(4, 14):
+    S.smc_step(s, data, sched, t, cfg)
+t1.record()
+torch.cuda.synchronize()
+print(f"{'smc_step (mean of 10)':28s} {t0.elapsed_time(t1) / 10 * 1e3:9.1f} us")
+
 timeit("reweight (prior mode 1+lse)", lambda: S._reweight_device(s, prior, S.GtPrior(1.0, sched.bs[2])), 5)
 timeit("rw_factor (moments+chol)", lambda: S._rw_factor(s, 2.38))
 timeit("chol only", lambda: _lib.call("spa_rw_factor", _p(rw["acc"]), s.q, 2.38, 1e-6, _p(rw["L"]), _p(rw["fws"]),
@@ -48,14 +57,9 @@ timeit("normals", lambda: _lib.call("spa_rw_normals", s.N, s.q, 1, 4, 0, 0, _p(z
 timeit("propose (gemm+pack)", lambda: _lib.call(
     "spa_rw_propose", ctypes.byref(d.struct), _p(s.beta), s.N, s.ldb, s.factor_operand(), 1, 4, 0, 0, _p(zb),
     _p(rw["prop"]), _p(ws["A"]), _p(ws["ylin"]), 1.0, float(prior.c), _p(rw["lp_p"]), _stream()))
+lw_t, lp_t = torch.empty_like(s.ll), torch.empty_like(s.ll)
+timeit("prior_reweight (fused)", lambda: _lib.call("spa_prior_reweight", ctypes.byref(d.struct), _p(s.beta), s.N, s.ldb,
+                                                    1.0, float(prior.c), float(sched.bs[2]), _p(lw_t), _p(lp_t),
+                                                    _stream()))
 timeit("K1 loglik", lambda: _lib.call("spa_loglik_softplus", ctypes.byref(d.struct), _p(ws["A"]), s.N, _p(ws["sp"]),
                                       _p(ws["ws"]), ws["ws"].numel(), _stream()))
-timeit("one smc_step", lambda: None)
-t0 = torch.cuda.Event(enable_timing=True)
-t1 = torch.cuda.Event(enable_timing=True)
-t0.record()
-for t in range(4, 14):
-    S.smc_step(s, data, sched, t, cfg)
-t1.record()
-torch.cuda.synchronize()
-print(f"{'smc_step (mean of 10)':28s} {t0.elapsed_time(t1) / 10 * 1e3:9.1f} us")
