@@ -257,19 +257,20 @@ def main():
     if group is not None:
         group.barrier()
     n_launch0 = _lib.launch_count
-    resampled = 0
     with ClockSampler(local) as clk:
         timer.enabled = True
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
+        recs = []
         for _ in range(args.steps):
-            rec = S.smc_step(system, data, sched, t, cfg, group, _defer=True)
-            resampled += int(rec.resampled)
+            recs.append(S.smc_step(system, data, sched, t, cfg, group, _defer=True))
             t += 1
         e1.record()
         torch.cuda.synchronize()
         timer.enabled = False
+    S.resolve_records(system, recs)  # device step records (ESS, resampled, acceptance), read once
+    resampled = sum(int(r.resampled) for r in recs)
     if group is not None:
         group.barrier()
     launches = _lib.launch_count - n_launch0
@@ -307,6 +308,11 @@ def main():
         cfg_e = S.SmcConfig(N=Ntot, move_kernel="rw", moves=MOVES, seed=1, init_burn=200, init_thin=5,
                             snapshot_thin=10)
         sched_e = S.make_schedule(*SCHED)  # the full 100-step lambda path
+        # untimed warm-up of the same shapes (pinned staging buffer, writer
+        # thread, first-call attribute setup), a 3-step path without burn-in
+        S.run_sampler(data, A_DOF, S.make_schedule(SCHED[0], SCHED[1], 3),
+                      S.SmcConfig(N=Ntot, move_kernel="rw", moves=MOVES, seed=2, init_burn=1, init_thin=1,
+                                  snapshot_thin=1), False, group)
         torch.cuda.synchronize()
         if group is not None:
             group.barrier()
@@ -325,7 +331,8 @@ def main():
                "lambda_path_s": out.timings.get("path_s"),
                "h2d_bytes_per_step": int(h2d / nsteps_e), "d2h_bytes_per_step": int(d2h_total / nsteps_e),
                "note": "full 100-step run_sampler(Dataset on host) -> SmcOutput on host: design upload, "
-                       "parallel-chain init (200 burn sweeps), 99 lambda steps, snapshots every 10th step"}
+                       "parallel-chain init (200 burn sweeps), 99 lambda steps, snapshots every 10th step; "
+                       "after an untimed 3-step warm-up run of the same shapes"}
 
     if rank != 0:
         return 0

@@ -131,6 +131,20 @@ int spa_gather_rows(const float* src, int32_t ld_src, float* dst, int32_t ld_dst
                     int64_t base, int64_t m, const double* v0, double* v0_out, const double* v1, double* v1_out,
                     void* stream);
 
+/* ---- device-decided resampling (no host sync inside a lambda step) -------
+ * smc.py:258-263 / 397-424: the ESS test and its consequences without a
+ * host round trip.  spa_step_record stores rec[t] = {log(Z_t/Z_t-1) = res[0],
+ * ESS = res[1], resampled = ESS < ess_threshold, log(Z_t/Z_1)} (running sum
+ * in step order) from a spa_lse_combine result; spa_resample_gated then runs
+ * the bit-exact systematic resampling (spa_systematic_ancestors) and gather
+ * for all N rows, commits them in place and resets logw to -log N -- every
+ * kernel returning immediately when *gate (rec[t][2]) is 0.  w = normalised
+ * weights, u = the step's uniform / N. */
+int spa_step_record(const double* res, double* rec, int64_t t, double ess_threshold, void* stream);
+int spa_resample_gated(const double* gate, const double* w, int64_t N, double u, float* beta, float* beta_alt,
+                       int32_t ldb, int32_t q, double* ll, double* ll_alt, double* lp, double* lp_alt, double* logw,
+                       int64_t* anc, void* ws, size_t ws_bytes, void* stream);
+
 /* ---- K7/K9: Metropolis-within-Gibbs coordinate moves --------------------
  * smc.py:298-332 (_move_block) / smc.py:177-199 (mwg_sweep): `cycles` sweeps
  * of single-coordinate random-walk updates with per-particle Philox streams

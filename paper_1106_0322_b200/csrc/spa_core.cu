@@ -167,13 +167,16 @@ struct LpAcc {
   float npen = 0.f;
   __device__ __forceinline__ void add4(const float (&p)[4], const float (&pen)[4], double K, int de) {
     npen += (pen[0] + pen[1]) + (pen[2] + pen[3]);
+    // an unpenalised column enters as x = 0 (factor exactly 1): a float32
+    // select instead of a float64 multiply by the 0/1 flag
+    double x[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[i] = (double)(pen[i] != 0.f ? fabsf(p[i]) : 0.f);
     if (de) {
-      lin += (fabs((double)p[0]) * pen[0] + fabs((double)p[1]) * pen[1]) +
-             (fabs((double)p[2]) * pen[2] + fabs((double)p[3]) * pen[3]);
+      lin += (x[0] + x[1]) + (x[2] + x[3]);
       return;
     }
-    const double g = fma(fabs((double)p[0]), K * pen[0], 1.0) * fma(fabs((double)p[1]), K * pen[1], 1.0) *
-                     (fma(fabs((double)p[2]), K * pen[2], 1.0) * fma(fabs((double)p[3]), K * pen[3], 1.0));
+    const double g = fma(x[0], K, 1.0) * fma(x[1], K, 1.0) * (fma(x[2], K, 1.0) * fma(x[3], K, 1.0));
     if (prod < 1e200 && g < 1e100) {
       prod *= g;
     } else {
@@ -484,6 +487,9 @@ template <int IT>
 __global__ void __launch_bounds__(256) prior_reweight_kernel(spa_design d, const float* __restrict__ beta, int64_t m,
                                                              int ldb, PriorConst pc, double* __restrict__ lw,
                                                              double* __restrict__ lp) {
+  __shared__ __align__(16) float pen_s[IT * 128];  // 0/1 penalty flags, padding columns 0
+  for (int j = threadIdx.x; j < IT * 128; j += blockDim.x) pen_s[j] = (j < d.q && d.penalized[j]) ? 1.f : 0.f;
+  __syncthreads();
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= m) return;
@@ -511,8 +517,11 @@ __global__ void __launch_bounds__(256) prior_reweight_kernel(spa_design d, const
 #pragma unroll
       for (int i = 0; i < 4; ++i) x[i] = j0 + i < d.q ? b[j0 + i] : 0.f;
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) pen[i] = (j0 + i < d.q && d.penalized[j0 + i]) ? 1.f : 0.f;
+    const float4 pv = *reinterpret_cast<const float4*>(pen_s + j0);
+    pen[0] = pv.x;
+    pen[1] = pv.y;
+    pen[2] = pv.z;
+    pen[3] = pv.w;
     la.add4(x, pen, K1, pc.de);
     if (!pc.de) lb.add4(x, pen, K2, 0);
   }
@@ -633,10 +642,16 @@ __global__ void logw_apply_kernel(double* __restrict__ logw, const double* __res
 // The reference cumsum is a strictly sequential float64 accumulation; it is
 // reproduced by one thread scanning smem-staged tiles (the other lanes stage
 // the next tile).  Ancestor search is parallel (one thread per slot).
-__global__ void seq_cumsum_kernel(const double* __restrict__ w, int64_t N, double* __restrict__ cum) {
+// gate: optional device flag (a step record's "resampled" field); kernels of
+// the device-decided resampling path return at once when it is 0.
+__device__ __forceinline__ bool gated_off(const double* gate) { return gate != nullptr && !(gate[0] != 0.0); }
+
+__global__ void seq_cumsum_kernel(const double* __restrict__ w, int64_t N, double* __restrict__ cum,
+                                  const double* __restrict__ gate) {
   // blockDim = 64: warp 1 stages tile t+1 into smem while lane 0 of warp 0
   // runs the strictly sequential float64 accumulation over tile t.
   __shared__ double tile[2][2048];
+  if (gated_off(gate)) return;
   const int64_t ntiles = (N + 2047) / 2048;
   if (threadIdx.x >= 32)
     for (int i = threadIdx.x - 32; i < 2048; i += 32) tile[0][i] = (i < N) ? w[i] : 0.0;
@@ -674,9 +689,9 @@ __global__ void seq_cumsum_kernel(const double* __restrict__ w, int64_t N, doubl
 }
 
 __global__ void ancestors_kernel(const double* __restrict__ cum, int64_t N, double u, int64_t k0, int64_t count,
-                                 int64_t* __restrict__ anc) {
+                                 int64_t* __restrict__ anc, const double* __restrict__ gate) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= count) return;
+  if (i >= count || gated_off(gate)) return;
   const int64_t k = k0 + i;
   const double total = cum[N - 1];
   const double pos = u + (double)k / (double)N;
@@ -696,10 +711,11 @@ __global__ void ancestors_kernel(const double* __restrict__ cum, int64_t N, doub
 // K5: row gather (+ up to two per-particle float64 vectors)
 __global__ void gather_kernel(const float* __restrict__ src, int ld_src, float* __restrict__ dst, int ld_dst, int q,
                               const int64_t* __restrict__ idx, int64_t base, int64_t m, const double* __restrict__ v0,
-                              double* __restrict__ v0o, const double* __restrict__ v1, double* __restrict__ v1o) {
+                              double* __restrict__ v0o, const double* __restrict__ v1, double* __restrict__ v1o,
+                              const double* __restrict__ gate) {
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (row >= m) return;
+  if (row >= m || gated_off(gate)) return;
   const int64_t s = idx[row] - base;
   const float* a = src + s * ld_src;
   float* o = dst + row * ld_dst;
@@ -713,6 +729,45 @@ __global__ void gather_kernel(const float* __restrict__ src, int ld_src, float* 
   if (lane == 0) {
     if (v0) v0o[row] = v0[s];
     if (v1) v1o[row] = v1[s];
+  }
+}
+
+// Step record (device-decided resampling): rec[t] = {inc, ESS, resampled,
+// log Z_t/Z_1}, the running log-evidence accumulated in step order (the same
+// float64 additions as the host loop).
+__global__ void step_record_kernel(const double* __restrict__ res, double* __restrict__ rec, int64_t t,
+                                   double ess_threshold) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double inc = res[0], e = res[1];
+  rec[4 * t + 0] = inc;
+  rec[4 * t + 1] = e;
+  rec[4 * t + 2] = (e < ess_threshold) ? 1.0 : 0.0;
+  rec[4 * t + 3] = rec[4 * (t - 1) + 3] + inc;
+}
+
+// Gated copy-back of the gathered rows (alt -> main) and log-weight reset to
+// -log N: what the host-decided path does with a buffer swap and a fill.
+__global__ void resample_commit_kernel(const float* __restrict__ beta_alt, float* __restrict__ beta, int ldb, int q,
+                                       const double* __restrict__ ll_alt, double* __restrict__ ll,
+                                       const double* __restrict__ lp_alt, double* __restrict__ lp,
+                                       double* __restrict__ logw, double logw0, int64_t m,
+                                       const double* __restrict__ gate) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= m || gated_off(gate)) return;
+  const float* a = beta_alt + row * ldb;
+  float* o = beta + row * ldb;
+  if ((ldb & 3) == 0) {
+    const int q4 = q >> 2;
+    for (int j = lane; j < q4; j += 32) reinterpret_cast<float4*>(o)[j] = reinterpret_cast<const float4*>(a)[j];
+    for (int j = 4 * q4 + lane; j < q; j += 32) o[j] = a[j];
+  } else {
+    for (int j = lane; j < q; j += 32) o[j] = a[j];
+  }
+  if (lane == 0) {
+    ll[row] = ll_alt[row];
+    lp[row] = lp_alt[row];
+    logw[row] = logw0;
   }
 }
 
@@ -742,89 +797,34 @@ __global__ void reduce_units_kernel(const double* __restrict__ partial, int unit
 // are associative, so the moments are bit-identical for any CTA order or GPU
 // count (the same property the reference guarantees for `threads`).
 constexpr double kFix = 281474976710656.0;  // 2^48
-constexpr int kMomChunk = 2048;
 
 __device__ __forceinline__ unsigned long long to_fix(double v) { return (unsigned long long)llrint(v * kFix); }
 __device__ __forceinline__ double from_fix(unsigned long long v) { return (double)(long long)v / kFix; }
 
-__global__ void rw_mean_kernel(const float* __restrict__ beta, int64_t m, int ldb, int q, const double* __restrict__ w,
-                               unsigned long long* __restrict__ acc) {
+// Weighted mean sum_k w_k beta_kj: thread = column j, block row = a
+// 256-particle chunk; 16 rows in flight per thread (latency), one fixed-point
+// atomic per (column, chunk) (order-independent => deterministic).
+__global__ void __launch_bounds__(128) rw_mean_kernel(const float* __restrict__ beta, int64_t m, int ldb, int q,
+                                                      const double* __restrict__ w,
+                                                      unsigned long long* __restrict__ acc) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= q) return;
   const int64_t k0 = (int64_t)blockIdx.y * 256;
   const int64_t k1 = min(m, k0 + 256);
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  constexpr int kU = 16;
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
   int64_t k = k0;
-  for (; k + 4 <= k1; k += 4) {  // 4 independent rows in flight per thread
-    const float b0 = beta[k * ldb + j], b1 = beta[(k + 1) * ldb + j];
-    const float b2 = beta[(k + 2) * ldb + j], b3 = beta[(k + 3) * ldb + j];
-    s0 += w[k] * (double)b0;
-    s1 += w[k + 1] * (double)b1;
-    s2 += w[k + 2] * (double)b2;
-    s3 += w[k + 3] * (double)b3;
+  for (; k + kU <= k1; k += kU) {
+    float b[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) b[u] = __ldcs(beta + (k + u) * ldb + j);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) s[u & 3] += w[k + u] * (double)b[u];
   }
-  for (; k < k1; ++k) s0 += w[k] * (double)beta[k * ldb + j];
-  atomicAdd(&acc[j], to_fix((s0 + s1) + (s2 + s3)));
+  for (; k < k1; ++k) s[0] += w[k] * (double)beta[k * ldb + j];
+  atomicAdd(&acc[j], to_fix((s[0] + s[1]) + (s[2] + s[3])));
 }
 
-__global__ void rw_moments_kernel(const float* __restrict__ beta, int64_t m, int ldb, int q,
-                                  const double* __restrict__ w, unsigned long long* __restrict__ acc) {
-  // block: 16x16 threads computing a 64x64 lower-triangle tile (4x4 per thread)
-  __shared__ float sa[32][64];
-  __shared__ float sb[32][64];
-  __shared__ float mu_i[64], mu_j[64];
-  const int tiles = (q + 63) / 64;
-  const int ti = blockIdx.x / tiles, tj = blockIdx.x % tiles;
-  if (tj > ti) return;
-  const int64_t k0 = (int64_t)blockIdx.y * kMomChunk;
-  const int64_t k1 = min(m, k0 + kMomChunk);
-  if (threadIdx.x < 64) {
-    const int gi = ti * 64 + threadIdx.x, gj = tj * 64 + threadIdx.x;
-    mu_i[threadIdx.x] = gi < q ? (float)from_fix(acc[gi]) : 0.f;
-    mu_j[threadIdx.x] = gj < q ? (float)from_fix(acc[gj]) : 0.f;
-  }
-  __syncthreads();
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  float c[4][4] = {};
-  for (int64_t kb = k0; kb < k1; kb += 32) {
-    for (int e = threadIdx.x; e < 32 * 64; e += 256) {
-      const int r = e >> 6, col = e & 63;
-      const int64_t k = kb + r;
-      const int gi = ti * 64 + col, gj = tj * 64 + col;
-      const bool kin = k < k1;
-      const float wk = kin ? (float)w[k] : 0.f;
-      sa[r][col] = (kin && gi < q) ? wk * (beta[k * ldb + gi] - mu_i[col]) : 0.f;
-      sb[r][col] = (kin && gj < q) ? (beta[k * ldb + gj] - mu_j[col]) : 0.f;
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (int r = 0; r < 32; ++r) {
-      float av[4], bv[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        av[i] = sa[r][ty * 4 + i];
-        bv[i] = sb[r][tx * 4 + i];
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) c[i][jj] = fmaf(av[i], bv[jj], c[i][jj]);
-      }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int gi = ti * 64 + ty * 4 + i;
-    if (gi >= q) continue;
-#pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-      const int gj = tj * 64 + tx * 4 + jj;
-      if (gj >= q || gj > gi) continue;
-      atomicAdd(&acc[q + (size_t)gi * q + gj], to_fix((double)c[i][jj]));
-    }
-  }
-}
 
 // Blocked right-looking Cholesky of S = M2c + jitter*I in float32.  L only
 // parameterises the symmetric random-walk increment L z (any fixed L keeps the
@@ -1325,6 +1325,7 @@ int spa_prior_reweight(const spa_design* d, const float* beta, int64_t m, int32_
                        double c_prev, double* lw, double* lp, void* stream) {
   SPA_REQUIRE(d && beta && lw && lp && m >= 0, kBadArgument, "spa_prior_reweight: bad arguments");
   SPA_REQUIRE(a > 0 && c > 0 && c_prev > 0, kBadArgument, "spa_prior_reweight: a, c must be positive");
+  SPA_REQUIRE(d->kp <= 32 * 128, kNotSupported, "spa_prior_reweight: q > 4093 not supported");
   if (m == 0) return 0;
   const PriorConst pc = make_prior(a, c, c_prev);
   cudaStream_t st = as_stream(stream);
@@ -1374,10 +1375,10 @@ int spa_systematic_ancestors(const double* w, int64_t N, double u, int64_t k0, i
               "spa_systematic_ancestors: workspace too small");
   cudaStream_t st = as_stream(stream);
   double* cum = reinterpret_cast<double*>(ws);
-  seq_cumsum_kernel<<<1, 64, 0, st>>>(w, N, cum);
+  seq_cumsum_kernel<<<1, 64, 0, st>>>(w, N, cum, nullptr);
   SPA_CHECK_LAUNCH();
   if (count == 0) return 0;
-  ancestors_kernel<<<cdiv(count, 256), 256, 0, st>>>(cum, N, u, k0, count, anc);
+  ancestors_kernel<<<cdiv(count, 256), 256, 0, st>>>(cum, N, u, k0, count, anc, nullptr);
   SPA_CHECK_LAUNCH();
   return 0;
 }
@@ -1388,7 +1389,35 @@ int spa_gather_rows(const float* src, int32_t ld_src, float* dst, int32_t ld_dst
   SPA_REQUIRE(src && dst && idx && m >= 0 && q > 0, kBadArgument, "spa_gather_rows: bad arguments");
   if (m == 0) return 0;
   gather_kernel<<<cdiv(m, 8), 256, 0, as_stream(stream)>>>(src, ld_src, dst, ld_dst, q, idx, base, m, v0, v0_out, v1,
-                                                          v1_out);
+                                                          v1_out, nullptr);
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+int spa_step_record(const double* res, double* rec, int64_t t, double ess_threshold, void* stream) {
+  SPA_REQUIRE(res && rec && t >= 1, kBadArgument, "spa_step_record: bad arguments");
+  step_record_kernel<<<1, 32, 0, as_stream(stream)>>>(res, rec, t, ess_threshold);
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+int spa_resample_gated(const double* gate, const double* w, int64_t N, double u, float* beta, float* beta_alt,
+                       int32_t ldb, int32_t q, double* ll, double* ll_alt, double* lp, double* lp_alt, double* logw,
+                       int64_t* anc, void* ws, size_t ws_bytes, void* stream) {
+  SPA_REQUIRE(gate && w && N > 0 && beta && beta_alt && ll && ll_alt && lp && lp_alt && logw && anc && ws && q > 0,
+              kBadArgument, "spa_resample_gated: bad arguments");
+  SPA_REQUIRE(ws_bytes >= spa_resample_workspace_bytes(N), kWorkspaceTooSmall,
+              "spa_resample_gated: workspace too small");
+  cudaStream_t st = as_stream(stream);
+  double* cum = reinterpret_cast<double*>(ws);
+  seq_cumsum_kernel<<<1, 64, 0, st>>>(w, N, cum, gate);
+  SPA_CHECK_LAUNCH();
+  ancestors_kernel<<<cdiv(N, 256), 256, 0, st>>>(cum, N, u, 0, N, anc, gate);
+  SPA_CHECK_LAUNCH();
+  gather_kernel<<<cdiv(N, 8), 256, 0, st>>>(beta, ldb, beta_alt, ldb, q, anc, 0, N, ll, ll_alt, lp, lp_alt, gate);
+  SPA_CHECK_LAUNCH();
+  resample_commit_kernel<<<cdiv(N, 8), 256, 0, st>>>(beta_alt, beta, ldb, q, ll_alt, ll, lp_alt, lp, logw,
+                                                      -std::log((double)N), N, gate);
   SPA_CHECK_LAUNCH();
   return 0;
 }

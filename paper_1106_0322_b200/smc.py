@@ -592,14 +592,96 @@ class _LazyRate:
         return int(self.counter.item()) / self.denom
 
 
+class _Pending:
+    """A StepRecord field held in the device step records (rec[t][col]),
+    filled in by resolve_records after the step loop."""
+
+    def __init__(self, t: int, col: int):
+        self.t, self.col = t, col
+
+
+def resolve_records(system: ParticleSystem, steps: list) -> None:
+    """Read the device step records once and fill the deferred StepRecord
+    fields (ESS, log Z_t/Z_1, resampled, acceptance).  Raises
+    DegeneracyError for the first step whose weights vanished, as the
+    host-decided path would have at that step."""
+    rec = system._records.cpu().numpy() if getattr(system, "_records", None) is not None else None
+    for s in steps:
+        for name in ("ess", "log_z_ratio_cum", "resampled"):
+            v = getattr(s, name)
+            if isinstance(v, _Pending):
+                if not math.isfinite(rec[v.t, 0]):
+                    raise DegeneracyError(f"step {v.t}: all incremental weights vanished")
+                val = rec[v.t, v.col]
+                setattr(s, name, bool(val != 0.0) if name == "resampled" else float(val))
+        if not isinstance(s.acceptance, float):
+            s.acceptance = float(s.acceptance)
+    if rec is not None and steps:
+        system.log_z_cum = float(rec[steps[-1].t, 3])
+
+
+def _smc_step_async(system: ParticleSystem, schedule: Schedule, t: int, config: SmcConfig) -> StepRecord:
+    """One lambda step with no host synchronisation (single process): the
+    ESS test runs on the device (spa_step_record) and resampling is gated on
+    its flag (spa_resample_gated), so the host only enqueues launches.  The
+    arithmetic is the host-decided path's (bit-identical particles, weights
+    and evidence); the record's ESS / evidence / resampled / acceptance are
+    resolved after the loop by resolve_records."""
+    a = system.prior_a
+    bs = schedule.bs
+    prior_prev = GtPrior(a, prior_scale(a, bs[t - 2]))
+    prior_t = GtPrior(a, prior_scale(a, bs[t - 1]))
+    z_ready = _rw_normals_async(system, config, t) if config.move_kernel == "rw" else None
+    d = system.design
+    N = system.N_total
+    if getattr(system, "_records", None) is None or system._records.shape[0] < schedule.T + 1:
+        system._records = torch.zeros((schedule.T + 1, 4), dtype=torch.float64, device=system.device)
+        system._records[:, 3] = system.log_z_cum
+        system._rs_ws = torch.empty(8 * system.N, dtype=torch.uint8, device=system.device)
+        system._anc = torch.empty(system.N, dtype=torch.int64, device=system.device)
+    rec = system._records
+    _lib.call("spa_prior_reweight", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb,
+              float(prior_t.a), float(prior_t.c), float(prior_prev.c), _p(system.lw), _p(system.lp), _stream())
+    _lib.call("spa_lse_chunk_stats", _p(system.logw), _p(system.lw), system.N, _p(system.stats), _stream())
+    _lib.call("spa_lse_combine", _p(system.stats), system.nchunks, _p(system.res), _stream())
+    _lib.call("spa_logw_apply", _p(system.logw), _p(system.lw), system.N, _p(system.res), None, _stream())
+    _lib.call("spa_step_record", _p(system.res), _p(rec), t, float(config.ess_threshold_frac * N), _stream())
+    w = system.device_weights()
+    u = first_uniform(config.seed, TAG_RESAMPLE, t) / N
+    gate = ctypes.c_void_p(rec.data_ptr() + (4 * t + 2) * 8)
+    _lib.call("spa_resample_gated", gate, _p(w), system.N, u, _p(system.beta), _p(system.beta_alt), system.ldb,
+              system.q, _p(system.ll), _p(system.ll_alt), _p(system.lp), _p(system.lp_alt), _p(system.logw),
+              _p(system._anc), _p(system._rs_ws), system._rs_ws.numel(), _stream())
+    if config.move_kernel == "mwg":
+        cnt = torch.zeros(1, dtype=torch.int64, device=system.device)
+        _lib.call("spa_mwg_move", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb, float(prior_t.a),
+                  float(prior_t.c), float(config.step_sd), int(config.cycles), int(config.seed), TAG_MOVE, int(t),
+                  int(system.i0), 0, _p(system.ll), _p(system.lp), _p(cnt), 0, _stream())
+        acceptance = _LazyRate(cnt, N * config.cycles * system.q)
+    else:
+        if t == 2 or not getattr(system, "_ll_from_k1", False):
+            _loglik_device(system, system.ll)
+            system._ll_from_k1 = True
+        acc = _rw_moves(system, prior_t, config, t, None, z_ready)
+        acceptance = _LazyRate(acc, N * config.moves)
+    system.t = t
+    return StepRecord(t, float(bs[t - 1]), _Pending(t, 1), _Pending(t, 3), acceptance, _Pending(t, 2))
+
+
 def smc_step(system: ParticleSystem, data, schedule: Schedule, t: int, config: SmcConfig, group=None,
              _defer: bool = False) -> StepRecord:
     """Advance from step t-1 to t: reweight -> accumulate evidence -> ESS ->
-    resample if ESS < frac*N -> move with the invariant kernel at prior_t."""
+    resample if ESS < frac*N -> move with the invariant kernel at prior_t.
+
+    _defer (internal; run_sampler and the bench): single-process steps run
+    without host synchronisation and return records with pending fields,
+    resolved by resolve_records."""
     if not 2 <= t <= schedule.T:
         raise ValueError(f"step index {t} outside [2, {schedule.T}]")
     if system.t != t - 1:
         raise ValueError(f"system is at step {system.t}, cannot advance to {t}")
+    if _defer and group is None:
+        return _smc_step_async(system, schedule, t, config)
     a = system.prior_a
     bs = schedule.bs
     prior_prev = GtPrior(a, prior_scale(a, bs[t - 2]))
@@ -742,8 +824,7 @@ def run_sampler(data, a: float, schedule: Schedule, config: SmcConfig, intercept
         t1 = time.perf_counter()
         for t in range(2, schedule.T + 1):
             steps.append(snap(smc_step(system, data, schedule, t, config, group, _defer=True)))
-        for s in steps:  # resolve the deferred acceptance counters (one sync)
-            s.acceptance = float(s.acceptance)
+        resolve_records(system, steps)  # one read of the deferred step records
         torch.cuda.synchronize()
         timings["path_s"] = time.perf_counter() - t1
         ts = time.perf_counter()
