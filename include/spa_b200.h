@@ -186,8 +186,9 @@ int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const d
 int spa_rw_factor(const int64_t* partial, int32_t q, double scale, double jitter, float* L, double* ws, int* info,
                   void* stream);
 /* Proposal normals Z (bf16 [m][kq], kq = roundup(q, 64), zero padded) from
- * Philox4x32-10 keyed by seed with counter (j/4, i0+k, t, move | 3<<24): two
- * sign-symmetric Box-Muller pairs per block (csrc/spa_core.cu rw_normals4).
+ * Philox4x32-10 keyed by seed with counter (j/8, i0+k, t, move | 3<<24): each
+ * 32-bit word gives one sign-symmetric Box-Muller pair from two 15-bit
+ * uniforms, 8 normals per block (csrc/spa_core.cu rw_normals8).
  * Independent of the particle state, so all moves of a step can be drawn
  * ahead, e.g. on a side stream while the covariance is factored. */
 int spa_rw_normals(int64_t m, int32_t q, uint64_t seed, int64_t t, int64_t i0, int32_t move, void* zbuf,

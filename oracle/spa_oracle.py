@@ -109,26 +109,28 @@ def philox4x32_10(counters: np.ndarray, k0: int, k1: int) -> np.ndarray:
 
 
 def rw_normals(seed: int, t: int, k: int, move: int, q: int) -> np.ndarray:
-    """Proposal normals of the RW-cov move (csrc/spa_core.cu rw_normals4):
-    Philox4x32-10, key = seed, counter (j/4, k, t, move | 3<<24); per block two
-    sign-symmetric Box-Muller pairs from 24-bit uniforms (float32 math; the
-    device uses fast intrinsics, so agreement is to ~1e-6)."""
-    nb = -(-q // 4)
+    """Proposal normals of the RW-cov move (csrc/spa_core.cu rw_normals8):
+    Philox4x32-10, key = seed, counter (j/8, k, t, move | 3<<24); each 32-bit
+    word w gives one sign-symmetric Box-Muller pair from two 15-bit uniforms,
+    u1 = (w>>1 & 0x7fff) + 1, u2 = w>>17 & 0x7fff (x 2^-15), signs = bits 0 and
+    16: z = (+-|r cos(pi/2 u2)|, +-|r sin(pi/2 u2)|).  Float32 math; the device
+    uses fast intrinsics, so agreement is to ~1e-6."""
+    nb = -(-q // 8)
     ctr = np.zeros((nb, 4), np.uint64)
     ctr[:, 0] = np.arange(nb)
     ctr[:, 1] = k
     ctr[:, 2] = t
     ctr[:, 3] = move | (3 << 24)
     w = philox4x32_10(ctr, seed & 0xFFFFFFFF, seed >> 32)
-    out = np.empty((nb, 4))
-    for h in range(2):
-        a, b = w[:, 2 * h], w[:, 2 * h + 1]
-        u1 = ((a >> np.uint64(8)).astype(np.float64) + 1.0) * 2.0**-24
-        u2 = (b >> np.uint64(8)).astype(np.float64) * 2.0**-24
+    out = np.empty((nb, 8))
+    for h in range(4):
+        a = w[:, h]
+        u1 = (((a >> np.uint64(1)) & np.uint64(0x7FFF)).astype(np.float64) + 1.0) * 2.0**-15
+        u2 = ((a >> np.uint64(17)) & np.uint64(0x7FFF)).astype(np.float64) * 2.0**-15
         r = np.sqrt(-2.0 * np.log(u1))
         m0, m1 = np.abs(r * np.cos(np.pi / 2 * u2)), np.abs(r * np.sin(np.pi / 2 * u2))
         out[:, 2 * h] = np.where(a & np.uint64(1), -m0, m0)
-        out[:, 2 * h + 1] = np.where(b & np.uint64(1), -m1, m1)
+        out[:, 2 * h + 1] = np.where((a >> np.uint64(16)) & np.uint64(1), -m1, m1)
     return out.reshape(-1)[:q]
 
 

@@ -991,46 +991,53 @@ __global__ void rw_emit_kernel(const float* __restrict__ S, int q, int kq, float
 }
 
 // Proposal normals: Z[k][j] (bf16, [m][kq]).  Counter-based Philox4x32-10
-// keyed by the seed, counter (j/4, particle i0+k, t, move | tag 3 << 24);
-// each block gives two Box-Muller pairs.  Each normal is |r cos(pi/2 u)| with
-// an independent random sign, so its law is exactly symmetric whatever the
-// rounding of the fast intrinsics (the RW increment must be symmetric for the
-// plain Metropolis ratio; its exact shape is immaterial).
-__device__ __forceinline__ void rw_normals4(uint64_t seed, int64_t t, int64_t k, int move, uint32_t blk, float z[4]) {
+// keyed by the seed, counter (j/8, particle i0+k, t, move | tag 3 << 24);
+// every 32-bit output word carries one Box-Muller pair: two 15-bit uniforms
+// (radius, angle) and two sign bits, so one Philox call gives 8 normals.
+// Each normal is |r cos(pi/2 u)| (resp. sin) with an independent random sign,
+// so the law is exactly symmetric whatever the rounding of the fast
+// intrinsics (the RW increment must be symmetric for the plain Metropolis
+// ratio; its exact shape is immaterial -- the radius tail stops at 4.56 sd).
+__device__ __forceinline__ void rw_normals8(uint64_t seed, int64_t t, int64_t k, int move, uint32_t blk, float z[8]) {
   uint32_t w[4] = {blk, (uint32_t)k, (uint32_t)t, (uint32_t)move | (3u << 24)};
   philox4x32_10(w, (uint32_t)seed, (uint32_t)(seed >> 32));
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const uint32_t a = w[2 * h], b = w[2 * h + 1];
-    const float u1 = ((float)(a >> 8) + 1.0f) * 0x1.0p-24f;  // (0, 1]
-    const float u2 = (float)(b >> 8) * 0x1.0p-24f;           // [0, 1)
+  for (int h = 0; h < 4; ++h) {
+    const uint32_t a = w[h];
+    const float u1 = (float)(((a >> 1) & 0x7FFFu) + 1u) * 0x1.0p-15f;  // (0, 1]
+    const float u2 = (float)((a >> 17) & 0x7FFFu) * 0x1.0p-15f;        // [0, 1)
     float r;
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-2.0f * __logf(u1)));
     float sn, cs;
     __sincosf(1.5707963267948966f * u2, &sn, &cs);
     const float m0 = fabsf(r * cs), m1 = fabsf(r * sn);
     z[2 * h] = (a & 1u) ? -m0 : m0;
-    z[2 * h + 1] = (b & 1u) ? -m1 : m1;
+    z[2 * h + 1] = (a & 0x10000u) ? -m1 : m1;
   }
 }
 
 __global__ void __launch_bounds__(256) rw_normals_kernel(int64_t m, int q, int kq, uint64_t seed, int64_t t,
                                                           int64_t i0, int move, __nv_bfloat16* __restrict__ Z) {
-  // warp-stride over particle rows, lanes over 4-column groups (256 B
-  // contiguous stores per warp); a small grid so the kernel shares SMs with
-  // the latency-bound work it overlaps on the main stream
-  const int kq4 = kq / 4;
+  // warp-stride over particle rows, lanes over 8-column groups (16-byte
+  // stores, 512 B per warp); a small grid so the kernel shares SMs with the
+  // latency-bound work it overlaps on the main stream
+  const int kq8 = kq / 8;
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < m; k += nw) {
     __nv_bfloat16* zr = Z + (size_t)k * kq;
-    for (int jb = lane; jb < kq4; jb += 32) {
-      __align__(8) __nv_bfloat16 z[4];
-      float zz[4] = {0.f, 0.f, 0.f, 0.f};
-      if (4 * jb < q) rw_normals4(seed, t, i0 + k, move, (uint32_t)jb, zz);
+    for (int jb = lane; jb < kq8; jb += 32) {
+      float zz[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (8 * jb < q) rw_normals8(seed, t, i0 + k, move, (uint32_t)jb, zz);
+      uint4 u;
+      uint32_t* up = reinterpret_cast<uint32_t*>(&u);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) z[i] = __float2bfloat16(4 * jb + i < q ? zz[i] : 0.0f);
-      *reinterpret_cast<uint2*>(zr + 4 * jb) = *reinterpret_cast<const uint2*>(z);
+      for (int i = 0; i < 4; ++i) {
+        const __nv_bfloat162 h2 = __floats2bfloat162_rn(8 * jb + 2 * i < q ? zz[2 * i] : 0.0f,
+                                                        8 * jb + 2 * i + 1 < q ? zz[2 * i + 1] : 0.0f);
+        up[i] = *reinterpret_cast<const uint32_t*>(&h2);
+      }
+      *reinterpret_cast<uint4*>(zr + 8 * jb) = u;
     }
   }
 }
