@@ -209,6 +209,10 @@ int spa_rw_accept(float* beta, int32_t ldb, const void* eps, int32_t q, int64_t 
                   const double* sp_p, const double* lp_p, double* ll, double* lp, uint64_t seed, int64_t t,
                   int64_t i0, int32_t move, unsigned long long* accepted, void* stream);
 
+/* Load every kernel of the library on the current device now (instead of
+ * lazily at first launch) -- run_sampler calls it during initialisation. */
+int spa_prepare(void);
+
 /* ---- test hook: the raw tcgen05 GEMM engine --------------------------
  * C[m][ldc] = sum_t A_t B^T for A = [A_0 | A_1] (terms_a bf16 blocks of kp
  * columns, K-major) and B [rows_b][kp] bf16; float32 C (ldc % 4 == 0, TMA

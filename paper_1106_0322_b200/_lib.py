@@ -58,6 +58,7 @@ _SIGNATURES = {
                                          c_void_p]),
     "spa_gather_rows": (c_int, [c_void_p, c_int32, c_void_p, c_int32, c_int32, c_void_p, c_int64, c_int64, c_void_p,
                                 c_void_p, c_void_p, c_void_p, c_void_p]),
+    "spa_prepare": (c_int, []),
     "spa_step_record": (c_int, [c_void_p, c_void_p, c_int64, c_double, c_void_p]),
     "spa_resample_gated": (c_int, [c_void_p, c_void_p, c_int64, c_double, c_void_p, c_void_p, c_int32, c_int32,
                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,

@@ -288,6 +288,16 @@ static int pick_s(int n) {
 
 using namespace spa;
 
+// internal (called by spa_prepare): load the MwG kernels
+extern "C" int spa_mwg_prepare_kernels(void) {
+  const void* fns[] = {(const void*)mwg_kernel<8>, (const void*)mwg_kernel<16>, (const void*)mwg_kernel<32>};
+  for (const void* f : fns) {
+    cudaFuncAttributes a;
+    SPA_CHECK_CUDA(cudaFuncGetAttributes(&a, f));
+  }
+  return 0;
+}
+
 // Chains (one CTA each) resident at once on the current device: the
 // occupancy of the kernel variant spa_mwg_move would launch for this design
 // times the SM count.  Initialisation sizes its parallel chains to one wave.

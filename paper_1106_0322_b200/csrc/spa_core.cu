@@ -1600,6 +1600,35 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
   return 0;
 }
 
+extern "C" int spa_mwg_prepare_kernels(void);  // mwg.cu
+
+// Load every hot-path kernel now (CUDA lazy module loading would otherwise
+// load each on its first launch inside the first lambda step) and apply the
+// shared-memory attributes; callable while other work runs on the device.
+int spa_prepare(void) {
+  const void* fns[] = {
+      (const void*)tc_gemm_kernel<2, 1, 256, EpiSoftplusRowSum>,
+      (const void*)tc_gemm_kernel<2, 2, 256, EpiSoftplusRowSum>,
+      (const void*)tc_gemm_kernel<1, 1, 256, EpiStoreT<__nv_bfloat16>>,
+      (const void*)tc_gemm_kernel<2, 2, 256, EpiStoreT<float>>,
+      (const void*)pack_kernel, (const void*)pack_eps_kernel<1>, (const void*)pack_eps_kernel<2>,
+      (const void*)pack_eps_kernel<4>, (const void*)pack_eps_kernel<8>, (const void*)prior_kernel,
+      (const void*)prior_reweight_kernel<1>, (const void*)prior_reweight_kernel<2>,
+      (const void*)prior_reweight_kernel<4>, (const void*)prior_reweight_kernel<8>,
+      (const void*)prior_reweight_kernel<32>, (const void*)lse_stats_kernel, (const void*)lse_combine_kernel,
+      (const void*)logw_apply_kernel, (const void*)seq_cumsum_kernel, (const void*)ancestors_kernel,
+      (const void*)gather_kernel, (const void*)step_record_kernel, (const void*)resample_commit_kernel,
+      (const void*)reduce_units_kernel, (const void*)rw_mean_kernel, (const void*)rw_cov_kernel,
+      (const void*)rw_chol_diag_kernel, (const void*)rw_chol_trail_kernel, (const void*)rw_emit_kernel,
+      (const void*)rw_normals_kernel, (const void*)rw_center_t_kernel, (const void*)rw_accept_kernel,
+      (const void*)syrk_reduce_kernel};
+  for (const void* f : fns) {
+    cudaFuncAttributes a;
+    SPA_CHECK_CUDA(cudaFuncGetAttributes(&a, f));
+  }
+  return spa_mwg_prepare_kernels();
+}
+
 int spa_tc_gemm_f32(const void* A, int64_t m, int32_t terms_a, const void* B, int32_t rows_b, int32_t kp, float* C,
                     int32_t ldc, void* stream) {
   SPA_REQUIRE(A && B && C && m > 0 && rows_b > 0 && kp % 64 == 0 && (terms_a == 1 || terms_a == 2), kBadArgument,

@@ -507,6 +507,21 @@ def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int,
 # initialisation (reference smc.py:202-245, as parallel chains)
 
 
+def _prepare_for_path(system: ParticleSystem, config: SmcConfig) -> None:
+    """One-time host work of the first lambda step, done while the GPU runs
+    the initialisation chains: load all kernels, allocate the step
+    workspaces and record the Cholesky's CUDA graph (a factor of the zeroed
+    moments, queued behind the chains; its result is discarded)."""
+    _lib.call("spa_prepare")
+    system.ll_workspace()
+    if config.move_kernel == "rw":
+        rw = system.rw_workspace()
+        system.z_buffers(config.moves)
+        system.side_stream()
+        _lib.call("spa_rw_factor", _p(rw["acc"]), system.q, float(config.rw_scale), 1e-6, _p(rw["L"]),
+                  _p(rw["fws"]), _p(rw["info"]), _stream())
+
+
 def resident_chains(design: DeviceDesign) -> int:
     """MwG chains (one CTA each) resident at once on this GPU for `design`."""
     out = ctypes.c_int64(0)
@@ -553,6 +568,7 @@ def init_particles(data, prior_at_b1: GtPrior, config: SmcConfig, intercept: boo
     counts = torch.zeros(Kl, dtype=torch.int64, device=system.device)  # per chain, read once at the end
     if config.init_burn > 0:
         _mwg(chains, prior_at_b1, config.step_sd, config.init_burn, config.seed, TAG_INIT, 0, 0, counts=counts)
+    _prepare_for_path(system, config)  # host work while the chains run
     stage_b = torch.empty((Kl, R, system.ldb), dtype=torch.float32, device=system.device)
     stage_l = torch.empty((Kl, R), dtype=torch.float64, device=system.device)
     stage_p = torch.empty((Kl, R), dtype=torch.float64, device=system.device)
