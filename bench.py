@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--particles", type=int, default=N_PER_GPU, help="particles per GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="bracket the timed steps with cudaProfilerStart/Stop (ncu --profile-from-start off)")
     return ap.parse_args()
 
 
@@ -263,11 +265,15 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         recs = []
+        if args.profile:
+            torch.cuda.profiler.start()
         for _ in range(args.steps):
             recs.append(S.smc_step(system, data, sched, t, cfg, group, _defer=True))
             t += 1
         e1.record()
         torch.cuda.synchronize()
+        if args.profile:
+            torch.cuda.profiler.stop()
         timer.enabled = False
     S.resolve_records(system, recs)  # device step records (ESS, resampled, acceptance), read once
     resampled = sum(int(r.resampled) for r in recs)

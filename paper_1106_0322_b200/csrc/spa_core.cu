@@ -203,9 +203,6 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const 
   const __nv_bfloat16* e = eps ? eps + row * ldb : nullptr;
   __nv_bfloat16* ah = A + row * (2 * (int64_t)d.kp);
   __nv_bfloat16* al = ah + d.kp;
-  const float lc = (float)(-log(2.0 * pc.c));
-  const float ap1 = pc.de ? 0.f : (float)(pc.a + 1.0);
-  const float inv = pc.de ? (float)(1.0 / pc.c) : (float)(1.0 / (pc.a * pc.c));
   double yl = 0.0, off = 0.0;
   LpAcc la;
   const double K = pc.de ? 0.0 : 1.0 / (pc.a * pc.c);
@@ -536,6 +533,66 @@ __global__ void __launch_bounds__(256) prior_reweight_kernel(spa_design d, const
   }
 }
 
+// Same pass with LPR lanes per particle row (32/LPR rows per warp): lane l
+// takes columns 4 (it LPR + l) .. +3, it < IT, all loads in flight first.
+// Fewer lanes per row amortise the two float64 logs and the shuffle
+// reduction of the per-lane products over 4 IT columns instead of 16.
+template <int LPR, int IT>
+__global__ void __launch_bounds__(256) prior_reweight_rows_kernel(spa_design d, const float* __restrict__ beta,
+                                                                  int64_t m, int ldb, PriorConst pc,
+                                                                  double* __restrict__ lw, double* __restrict__ lp) {
+  __shared__ __align__(16) float pen_s[LPR * IT * 4];  // 0/1 penalty flags, padding columns 0
+  for (int j = threadIdx.x; j < LPR * IT * 4; j += blockDim.x) pen_s[j] = (j < d.q && d.penalized[j]) ? 1.f : 0.f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, sub = lane % LPR;
+  const int64_t row = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (32 / LPR) + lane / LPR;
+  const bool live = row < m;
+  const float* b = beta + (live ? row : 0) * ldb;
+  const double K1 = pc.de ? 0.0 : 1.0 / (pc.a * pc.c), K2 = pc.de ? 0.0 : 1.0 / (pc.a * pc.c_prev);
+  const bool full = (d.q % 4 == 0) && (ldb % 4 == 0);
+  float4 xv[IT];
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const int j0 = (it * LPR + sub) * 4;
+    if (live && full && j0 + 4 <= d.q) xv[it] = __ldcs(reinterpret_cast<const float4*>(b + j0));
+  }
+  LpAcc la, lb;
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const int j0 = (it * LPR + sub) * 4;
+    float x[4], pen[4];
+    if (full && j0 + 4 <= d.q) {
+      x[0] = xv[it].x;
+      x[1] = xv[it].y;
+      x[2] = xv[it].z;
+      x[3] = xv[it].w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) x[i] = (live && j0 + i < d.q) ? b[j0 + i] : 0.f;
+    }
+    const float4 pv = *reinterpret_cast<const float4*>(pen_s + j0);
+    pen[0] = pv.x;
+    pen[1] = pv.y;
+    pen[2] = pv.z;
+    pen[3] = pv.w;
+    la.add4(x, pen, K1, pc.de);
+    if (!pc.de) lb.add4(x, pen, K2, 0);
+  }
+  double lpv = la.value(pc);
+  double lwv = pc.de ? (double)la.npen * pc.lr - la.lin * (1.0 / pc.c - 1.0 / pc.c_prev)
+                     : (double)la.npen * pc.lr -
+                           (pc.a + 1.0) * ((la.logsum + log(la.prod)) - (lb.logsum + log(lb.prod)));
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) {
+    lpv += __shfl_xor_sync(0xffffffffu, lpv, o);
+    lwv += __shfl_xor_sync(0xffffffffu, lwv, o);
+  }
+  if (live && sub == 0) {
+    lw[row] = lwv;
+    lp[row] = lpv;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K3: fixed-chunk log-sum-exp statistics
 constexpr int kChunk = 4096;
@@ -801,28 +858,60 @@ constexpr double kFix = 281474976710656.0;  // 2^48
 __device__ __forceinline__ unsigned long long to_fix(double v) { return (unsigned long long)llrint(v * kFix); }
 __device__ __forceinline__ double from_fix(unsigned long long v) { return (double)(long long)v / kFix; }
 
-// Weighted mean sum_k w_k beta_kj: thread = column j, block row = a
-// 256-particle chunk; 16 rows in flight per thread (latency), one fixed-point
-// atomic per (column, chunk) (order-independent => deterministic).
-__global__ void __launch_bounds__(128) rw_mean_kernel(const float* __restrict__ beta, int64_t m, int ldb, int q,
+// Weighted mean sum_k w_k beta_kj over a 128-particle block: row-major,
+// coalesced reads (warp w takes rows w, w+NW, ..; lane l columns 4 (l + 32 it)
+// .. +3), float64 per-lane column sums, a fixed-order reduction over the NW
+// warps in shared memory, then one fixed-point atomic per
+// (column, block) -- order-independent, so deterministic for any schedule
+// and, for shards that are multiples of 128 particles, any number of GPUs.
+constexpr int kMeanRows = 128;  // particles per block (one fixed-point atomic per column per block)
+
+template <int IT, int NW = (IT <= 4 ? 8 : 4)>
+__global__ void __launch_bounds__(256) rw_mean_kernel(const float* __restrict__ beta, int64_t m, int ldb, int q,
                                                       const double* __restrict__ w,
                                                       unsigned long long* __restrict__ acc) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= q) return;
-  const int64_t k0 = (int64_t)blockIdx.y * 256;
-  const int64_t k1 = min(m, k0 + 256);
-  constexpr int kU = 16;
-  double s[4] = {0.0, 0.0, 0.0, 0.0};
-  int64_t k = k0;
-  for (; k + kU <= k1; k += kU) {
-    float b[kU];
+  __shared__ double part[NW][IT * 128];  // NW warps per block (static smem <= 32 KB)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t k0 = (int64_t)blockIdx.x * kMeanRows;
+  const int64_t k1 = min(m, k0 + kMeanRows);
+  const bool vec = (q % 4 == 0) && (ldb % 4 == 0);
+  double s[IT][4];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) b[u] = __ldcs(beta + (k + u) * ldb + j);
+  for (int it = 0; it < IT; ++it)
 #pragma unroll
-    for (int u = 0; u < kU; ++u) s[u & 3] += w[k + u] * (double)b[u];
+    for (int i = 0; i < 4; ++i) s[it][i] = 0.0;
+  for (int64_t k = k0 + warp; k < k1; k += NW) {
+    const float* b = beta + k * ldb;
+    const double wk = w[k];
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int j0 = (lane + 32 * it) * 4;
+      float x[4] = {0.f, 0.f, 0.f, 0.f};
+      if (vec && j0 + 4 <= q) {
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(b + j0));
+        x[0] = v.x;
+        x[1] = v.y;
+        x[2] = v.z;
+        x[3] = v.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) x[i] = j0 + i < q ? b[j0 + i] : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) s[it][i] = fma(wk, (double)x[i], s[it][i]);
+    }
   }
-  for (; k < k1; ++k) s[0] += w[k] * (double)beta[k * ldb + j];
-  atomicAdd(&acc[j], to_fix((s[0] + s[1]) + (s[2] + s[3])));
+#pragma unroll
+  for (int it = 0; it < IT; ++it)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) part[warp][(lane + 32 * it) * 4 + i] = s[it][i];
+  __syncthreads();
+  for (int j = threadIdx.x; j < q; j += blockDim.x) {
+    double t = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < NW; ++ww) t += part[ww][j];
+    atomicAdd(&acc[j], to_fix(t));
+  }
 }
 
 
@@ -1338,13 +1427,15 @@ int spa_prior_reweight(const spa_design* d, const float* beta, int64_t m, int32_
   cudaStream_t st = as_stream(stream);
   const unsigned grid = (unsigned)cdiv(m, 8);
   if (d->kp <= 128)
-    prior_reweight_kernel<1><<<grid, 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);
+    prior_reweight_rows_kernel<8, 4><<<(unsigned)cdiv(m, 32), 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);
   else if (d->kp <= 256)
-    prior_reweight_kernel<2><<<grid, 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);
+    prior_reweight_rows_kernel<8, 8><<<(unsigned)cdiv(m, 32), 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);
   else if (d->kp <= 512)
-    prior_reweight_kernel<4><<<grid, 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);
+    prior_reweight_rows_kernel<16, 8><<<(unsigned)cdiv(m, 16), 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);
   else if (d->kp <= 1024)
-    prior_reweight_kernel<8><<<grid, 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);
+    prior_reweight_rows_kernel<16, 16><<<(unsigned)cdiv(m, 16), 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);
+  else if (d->kp <= 2048)
+    prior_reweight_rows_kernel<32, 16><<<grid, 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);
   else
     prior_reweight_kernel<32><<<grid, 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);
   SPA_CHECK_LAUNCH();
@@ -1469,8 +1560,18 @@ int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const d
   cudaStream_t st = as_stream(stream);
   auto* acc = reinterpret_cast<unsigned long long*>(partial);
   if (phase == 0) {
-    dim3 grid(cdiv(q, 128), cdiv(m, 256));
-    rw_mean_kernel<<<grid, 128, 0, st>>>(beta, m, ldb, q, w, acc);
+    const unsigned grid = (unsigned)cdiv(m, kMeanRows);
+    const int kq = (q + 127) / 128 * 128;
+    if (kq <= 128)
+      rw_mean_kernel<1><<<grid, 256, 0, st>>>(beta, m, ldb, q, w, acc);
+    else if (kq <= 256)
+      rw_mean_kernel<2><<<grid, 256, 0, st>>>(beta, m, ldb, q, w, acc);
+    else if (kq <= 512)
+      rw_mean_kernel<4><<<grid, 256, 0, st>>>(beta, m, ldb, q, w, acc);
+    else if (kq <= 1024)
+      rw_mean_kernel<8><<<grid, 128, 0, st>>>(beta, m, ldb, q, w, acc);
+    else
+      return fail(kNotSupported, "spa_rw_moments: q > 1024 not supported");
     SPA_CHECK_LAUNCH();
     return 0;
   }
@@ -1613,12 +1714,12 @@ int spa_prepare(void) {
       (const void*)tc_gemm_kernel<2, 2, 256, EpiStoreT<float>>,
       (const void*)pack_kernel, (const void*)pack_eps_kernel<1>, (const void*)pack_eps_kernel<2>,
       (const void*)pack_eps_kernel<4>, (const void*)pack_eps_kernel<8>, (const void*)prior_kernel,
-      (const void*)prior_reweight_kernel<1>, (const void*)prior_reweight_kernel<2>,
-      (const void*)prior_reweight_kernel<4>, (const void*)prior_reweight_kernel<8>,
-      (const void*)prior_reweight_kernel<32>, (const void*)lse_stats_kernel, (const void*)lse_combine_kernel,
+      (const void*)prior_reweight_rows_kernel<8, 4>, (const void*)prior_reweight_rows_kernel<8, 8>,
+      (const void*)prior_reweight_rows_kernel<16, 8>, (const void*)prior_reweight_rows_kernel<16, 16>,
+      (const void*)prior_reweight_rows_kernel<32, 16>, (const void*)prior_reweight_kernel<32>, (const void*)lse_stats_kernel, (const void*)lse_combine_kernel,
       (const void*)logw_apply_kernel, (const void*)seq_cumsum_kernel, (const void*)ancestors_kernel,
       (const void*)gather_kernel, (const void*)step_record_kernel, (const void*)resample_commit_kernel,
-      (const void*)reduce_units_kernel, (const void*)rw_mean_kernel, (const void*)rw_cov_kernel,
+      (const void*)reduce_units_kernel, (const void*)rw_mean_kernel<4>, (const void*)rw_cov_kernel,
       (const void*)rw_chol_diag_kernel, (const void*)rw_chol_trail_kernel, (const void*)rw_emit_kernel,
       (const void*)rw_normals_kernel, (const void*)rw_center_t_kernel, (const void*)rw_accept_kernel,
       (const void*)syrk_reduce_kernel};
