@@ -920,10 +920,11 @@ __global__ void __launch_bounds__(256) rw_mean_kernel(const float* __restrict__ 
 // Metropolis ratio exact), so float32 suffices; a non-positive pivot is
 // clamped (reported through *info) and still yields a valid proposal.
 //   rw_cov_kernel        : S (lower, float32) from the fixed-point moments
-//   rw_chol_diag_kernel  : one warp factors + inverts the 32x32 diagonal block
-//   rw_chol_trail_kernel : L21 rows + A22 -= L21 L21^T on 32x32 tiles
-// The ~2q/32 dependent launches are recorded once into a CUDA graph per
-// (workspace, q) and replayed every step (the loop is launch-latency bound).
+//   rw_chol_panel_kernel : per 32-column panel, one launch: the diagonal block
+//                          factor + inverse (one warp per CTA), then L21 rows
+//                          and A22 -= L21 L21^T on 32x32 tiles (one per CTA)
+// The q/32 dependent launches are recorded once into a CUDA graph per
+// (workspace, q) and replayed every step.
 //   rw_emit_kernel       : scale, write float32 L and the bf16 operand [q][kq]
 constexpr int kPanel = 32;
 
@@ -951,14 +952,16 @@ __global__ void __launch_bounds__(256) rw_cov_kernel(const unsigned long long* _
     out[j] = (j > i) ? 0.f : (float)(from_fix(row[j]) + (i == j ? add : 0.0));
 }
 
-__global__ void __launch_bounds__(32) rw_chol_diag_kernel(float* __restrict__ S, int q, int jb,
-                                                           float* __restrict__ inv, int* info) {
-  const int lane = threadIdx.x;
-  const int nb = min(kPanel, q - jb);
-  float a[kPanel];  // constant-bound loops => a[], x[] stay in registers
-#pragma unroll
-  for (int k = 0; k < kPanel; ++k)
-    a[k] = (lane < nb && k <= lane) ? S[(size_t)(jb + lane) * q + jb + k] : (k == lane ? 1.f : 0.f);
+// Factor one 32 x 32 diagonal block with one warp (lane = row, a[k] =
+// A[lane][k] for k <= lane; identity rows past nb) and form its inverse: on
+// return a[] holds the row of L11 and x[k] = (L11^-1)[k][lane].  Column j of
+// L is published once to shared memory (col) and read back as broadcast
+// float4s, the rows of L11 likewise (Ls) for the forward substitutions --
+// instead of one warp shuffle per element (the factor's critical path).
+// The substitution's dot products use 4 partial sums.  info records the first
+// non-positive pivot (1-based, offset jb).
+__device__ __forceinline__ void chol_block32(float (&a)[kPanel], float (&x)[kPanel], int lane, int nb, int jb,
+                                             int* info, float* col, float (*Ls)[kPanel + 4]) {
 #pragma unroll
   for (int j = 0; j < kPanel; ++j) {
     float djj = __shfl_sync(0xffffffffu, a[j], j);
@@ -968,56 +971,97 @@ __global__ void __launch_bounds__(32) rw_chol_diag_kernel(float* __restrict__ S,
     }
     const float rd = rsqrtf(djj);
     a[j] = (lane == j) ? djj * rd : (lane > j ? a[j] * rd : a[j]);
+    if (j + 1 < kPanel) {
+      col[lane] = a[j];  // column j of L (rows > j)
+      __syncwarp();
 #pragma unroll
-    for (int k = 0; k < kPanel; ++k) {
-      const float lkj = __shfl_sync(0xffffffffu, a[j], k);
-      if (k > j && lane >= k) a[k] = fmaf(-a[j], lkj, a[k]);
+      for (int c4 = ((j + 1) / 4) * 4; c4 < kPanel; c4 += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(col + c4);
+        const float lv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = c4 + u;
+          // no lane >= k test: entries above the diagonal (lane < k) are
+          // never read back, so they may absorb the update unconditionally
+          if (k > j) a[k] = fmaf(-a[j], lv[u], a[k]);
+        }
+      }
+      __syncwarp();
     }
   }
-  float x[kPanel];
+#pragma unroll
+  for (int k = 0; k < kPanel; k += 4)
+    *reinterpret_cast<float4*>(&Ls[lane][k]) = make_float4(a[k], a[k + 1], a[k + 2], a[k + 3]);
+  __syncwarp();
 #pragma unroll
   for (int i = 0; i < kPanel; ++i) {
-    float v = (i == lane) ? 1.f : 0.f;
+    float v[4] = {(i == lane) ? 1.f : 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int k = 0; k < kPanel; ++k) {
-      const float lik = __shfl_sync(0xffffffffu, a[k], i);
-      if (k < i) v = fmaf(-lik, x[k], v);
+    for (int k4 = 0; k4 < i; k4 += 4) {
+      const float4 r = *reinterpret_cast<const float4*>(&Ls[i][k4]);
+      const float rv[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k4 + u < i) v[u] = fmaf(-rv[u], x[k4 + u], v[u]);
     }
-    const float lii = __shfl_sync(0xffffffffu, a[i], i);
-    x[i] = (i >= lane) ? __fdividef(v, lii) : 0.f;
-  }
-#pragma unroll
-  for (int k = 0; k < kPanel; ++k) {
-    if (lane < nb && k <= lane) S[(size_t)(jb + lane) * q + jb + k] = a[k];
-    inv[k * kPanel + lane] = x[k];  // inv[k][lane]
+    x[i] = (i >= lane) ? __fdividef((v[0] + v[1]) + (v[2] + v[3]), Ls[i][i]) : 0.f;
   }
 }
 
-// Panel step 2 (one CTA per lower-triangle tile (bi, bj), bi >= bj, below the
-// panel): the L21 rows a tile needs are recomputed from A21 and L11^-1;
-// diagonal tiles store theirs transposed into the unused upper triangle (other
-// tiles of this launch still read A21 from the lower one); then the tile is
-// updated S -= L21_bi L21_bj^T.
-__global__ void __launch_bounds__(256) rw_chol_trail_kernel(float* __restrict__ S, int q, int jb,
-                                                             const float* __restrict__ inv) {
+
+
+// One launch per panel: every CTA's warp 0 factors the 32 x 32 diagonal
+// block and its inverse (chol_block32, redundantly per CTA, in parallel)
+// into shared memory; CTA 0 stores L11 and records pivot failures; then each
+// CTA owns one lower-triangle trailing tile (bi, bj), bi >= bj: the L21 rows
+// it needs are recomputed from A21 and L11^-1, diagonal tiles store theirs
+// transposed in the unused upper triangle (other CTAs still read A21 from
+// the lower one), and S -= L21_bi L21_bj^T.
+__global__ void __launch_bounds__(256) rw_chol_panel_kernel(float* __restrict__ S, int q, int jb, int* info) {
   __shared__ float iv[kPanel][kPanel + 1];
   __shared__ float li[32][kPanel + 1];
   __shared__ float lj[32][kPanel + 1];
-  int t = blockIdx.x, bi = 0;
-  while (t > bi) {
-    t -= bi + 1;
-    ++bi;
-  }
-  const int bj = t;
-  const int j0 = jb + kPanel;
-  const int r0 = j0 + bi * 32, c0 = j0 + bj * 32;
+  __shared__ __align__(16) float colb[kPanel];
+  __shared__ __align__(16) float Ls[kPanel][kPanel + 4];
   const int tid = threadIdx.x;
-  for (int e = tid; e < kPanel * kPanel; e += blockDim.x) iv[e / kPanel][e % kPanel] = inv[e];
-  for (int e = tid; e < 32 * kPanel; e += blockDim.x) {
-    const int r = e / kPanel, k = e % kPanel;
-    li[r][k] = (r0 + r < q) ? S[(size_t)(r0 + r) * q + jb + k] : 0.f;
-    lj[r][k] = (c0 + r < q) ? S[(size_t)(c0 + r) * q + jb + k] : 0.f;
+  const int j0 = jb + kPanel;
+  const int rest = q - j0;
+  int bi = 0, bj = 0, r0 = 0, c0 = 0;
+  if (rest > 0) {
+    int t = blockIdx.x;
+    while (t > bi) {
+      t -= bi + 1;
+      ++bi;
+    }
+    bj = t;
+    r0 = j0 + bi * 32;
+    c0 = j0 + bj * 32;
+    // the tile's A21 rows (read before CTA 0 overwrites the diagonal block:
+    // disjoint locations, so order does not matter)
+    for (int e = tid; e < 32 * kPanel; e += blockDim.x) {
+      const int r = e / kPanel, k = e % kPanel;
+      li[r][k] = (r0 + r < q) ? S[(size_t)(r0 + r) * q + jb + k] : 0.f;
+      lj[r][k] = (c0 + r < q) ? S[(size_t)(c0 + r) * q + jb + k] : 0.f;
+    }
   }
+  if (tid < 32) {
+    const int lane = tid;
+    const int nb = min(kPanel, q - jb);
+    float a[kPanel], x[kPanel];
+#pragma unroll
+    for (int k = 0; k < kPanel; ++k)
+      a[k] = (lane < nb && k <= lane) ? S[(size_t)(jb + lane) * q + jb + k] : (k == lane ? 1.f : 0.f);
+    __syncwarp();
+    chol_block32(a, x, lane, nb, jb, blockIdx.x == 0 ? info : nullptr, colb, Ls);
+#pragma unroll
+    for (int k = 0; k < kPanel; ++k) iv[k][lane] = x[k];
+    if (blockIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < kPanel; ++k)
+        if (lane < nb && k <= lane) S[(size_t)(jb + lane) * q + jb + k] = a[k];
+    }
+  }
+  if (rest <= 0) return;
   __syncthreads();
   {
     const int r = tid >> 3, cb = (tid & 7) * 4;
@@ -1064,6 +1108,7 @@ __global__ void __launch_bounds__(256) rw_chol_trail_kernel(float* __restrict__ 
     }
   }
 }
+
 
 __global__ void rw_emit_kernel(const float* __restrict__ S, int q, int kq, float f, float* __restrict__ L,
                                __nv_bfloat16* __restrict__ Lb) {
@@ -1261,13 +1306,11 @@ struct CholGraphKey {
 };
 
 static cudaError_t chol_record(float* S, int q, float* inv, int* info, cudaStream_t st) {
+  (void)inv;
   for (int jb = 0; jb < q; jb += 32) {
-    rw_chol_diag_kernel<<<1, 32, 0, st>>>(S, q, jb, inv, info);
     const int rest = q - jb - 32;
-    if (rest > 0) {
-      const int nt = (rest + 31) / 32;
-      rw_chol_trail_kernel<<<nt * (nt + 1) / 2, 256, 0, st>>>(S, q, jb, inv);
-    }
+    const int nt = rest > 0 ? (rest + 31) / 32 : 0;
+    rw_chol_panel_kernel<<<nt > 0 ? nt * (nt + 1) / 2 : 1, 256, 0, st>>>(S, q, jb, info);
   }
   return cudaGetLastError();
 }
@@ -1720,7 +1763,7 @@ int spa_prepare(void) {
       (const void*)logw_apply_kernel, (const void*)seq_cumsum_kernel, (const void*)ancestors_kernel,
       (const void*)gather_kernel, (const void*)step_record_kernel, (const void*)resample_commit_kernel,
       (const void*)reduce_units_kernel, (const void*)rw_mean_kernel<4>, (const void*)rw_cov_kernel,
-      (const void*)rw_chol_diag_kernel, (const void*)rw_chol_trail_kernel, (const void*)rw_emit_kernel,
+      (const void*)rw_chol_panel_kernel, (const void*)rw_emit_kernel,
       (const void*)rw_normals_kernel, (const void*)rw_center_t_kernel, (const void*)rw_accept_kernel,
       (const void*)syrk_reduce_kernel};
   for (const void* f : fns) {
