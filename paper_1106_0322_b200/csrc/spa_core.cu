@@ -84,15 +84,13 @@ static int make_tmap_out(CUtensorMap* map, void* ptr, uint64_t cols, uint64_t ro
 
 template <int TA, int TB, int BN, class Epi, int TM = 1>
 static int launch_tc(const void* A, uint64_t a_cols, const void* B, uint64_t b_cols, uint64_t b_rows, TcArgs args,
-                     int units, Epi epi, cudaStream_t st, const CUtensorMap* tmc_out = nullptr) {
+                     int units, const Epi& epi, cudaStream_t st) {
   constexpr int kSmem = tc_smem_bytes<TA, TB, BN, Epi, TM>();
   CUtensorMap ta, tb;
   int rc = make_tmap_bf16(&ta, A, a_cols, (uint64_t)args.m, kTcBM);
   if (rc) return rc;
   rc = make_tmap_bf16(&tb, B, b_cols, b_rows, BN);
   if (rc) return rc;
-  SPA_REQUIRE(Epi::kScratchPerWarp == 0 || tmc_out != nullptr, kBadArgument, "launch_tc: store epilogue needs a map");
-  const CUtensorMap& tc = tmc_out ? *tmc_out : ta;  // unused by non-store epilogues
   auto kern = tc_gemm_kernel<TA, TB, BN, Epi, TM>;
   static bool attr_done = false;  // per template instantiation
   if (!attr_done) {
@@ -108,7 +106,7 @@ static int launch_tc(const void* A, uint64_t a_cols, const void* B, uint64_t b_c
     SPA_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
   const int grid = std::min((args.m_tiles + TM - 1) / TM * units, sms);
-  kern<<<grid, kTcThreads, kSmem, st>>>(ta, tb, tc, args, epi);
+  kern<<<grid, kTcThreads, kSmem, st>>>(ta, tb, args, epi);
   SPA_CHECK_LAUNCH();
   return 0;
 }
@@ -1403,7 +1401,7 @@ static int loglik_impl(const spa_design* d, const void* A, int64_t m, const doub
   args.ncols = d->n;
   args.kp = d->kp;
   args.kb_per_unit = 0;
-  EpiSoftplusRowSum epi{reinterpret_cast<double*>(ws), 0.f, 0.0};
+  EpiSoftplusRowSum epi{reinterpret_cast<double*>(ws)};
   int rc;
   if (d->terms == 1)
     rc = launch_tc<2, 1, 256>(A, 2ull * d->kp, d->gemm_b, (uint64_t)d->kp, (uint64_t)d->n, args, units, epi, st);
@@ -1640,12 +1638,12 @@ int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const d
   float* part = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) +
                                          ((((size_t)2 * q * ldk * sizeof(__nv_bfloat16)) + 255) & ~size_t(255)));
   const int qp = (q + 3) / 4 * 4;
-  CUtensorMap tmc;
-  int rc = make_tmap_out<float>(&tmc, part, (uint64_t)q, (uint64_t)q, (uint64_t)units, (uint64_t)qp,
+  EpiStoreT<float> epi{};
+  int rc = make_tmap_out<float>(&epi.tmc, part, (uint64_t)q, (uint64_t)q, (uint64_t)units, (uint64_t)qp,
                                 (uint64_t)q * qp);
   if (rc) return rc;
-  EpiStoreT<float> epi{q, 0, 0};
-  rc = launch_tc<2, 2, 256>(Dt, 2ull * ldk, Dt, 2ull * ldk, (uint64_t)q, args, units, epi, st, &tmc);
+  epi.m = q;
+  rc = launch_tc<2, 2, 256>(Dt, 2ull * ldk, Dt, 2ull * ldk, (uint64_t)q, args, units, epi, st);
   if (rc) return rc;
   syrk_reduce_kernel<<<cdiv((int64_t)q * q, 256), 256, 0, st>>>(part, units, q, qp, acc);
   SPA_CHECK_LAUNCH();
@@ -1713,12 +1711,13 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
   args.tiles_per_unit = args.n_tiles;
   args.kb_per_unit = 0;
   auto* epsb = reinterpret_cast<__nv_bfloat16*>(eps);
-  CUtensorMap tmc;
-  int rc = make_tmap_out<__nv_bfloat16>(&tmc, epsb, (uint64_t)q, (uint64_t)m, 1, (uint64_t)ldb, (uint64_t)m * ldb);
+  EpiStoreT<__nv_bfloat16> epi{};
+  int rc = make_tmap_out<__nv_bfloat16>(&epi.tmc, epsb, (uint64_t)q, (uint64_t)m, 1, (uint64_t)ldb,
+                                        (uint64_t)m * ldb);
   if (rc) return rc;
-  EpiStoreT<__nv_bfloat16> epi{(int)m, 0, 0};
+  epi.m = (int)m;
   rc = launch_tc<1, 1, kPropBN, EpiStoreT<__nv_bfloat16>, SPA_PROP_TM>(Z, (uint64_t)kq, Lb, (uint64_t)kq, (uint64_t)q,
-                                                                      args, 1, epi, st, &tmc);
+                                                                      args, 1, epi, st);
   if (rc) return rc;
   auto* Ab = reinterpret_cast<__nv_bfloat16*>(A);
   const PriorConst pc = make_prior(a, c, c);
@@ -1785,14 +1784,13 @@ int spa_tc_gemm_f32(const void* A, int64_t m, int32_t terms_a, const void* B, in
   args.n_tiles = (rows_b + 255) / 256;
   args.tiles_per_unit = args.n_tiles;
   args.kb_per_unit = 0;
-  CUtensorMap tmc;
-  int rc = make_tmap_out<float>(&tmc, C, (uint64_t)rows_b, (uint64_t)m, 1, (uint64_t)ldc, (uint64_t)m * ldc);
+  EpiStoreT<float> epi{};
+  int rc = make_tmap_out<float>(&epi.tmc, C, (uint64_t)rows_b, (uint64_t)m, 1, (uint64_t)ldc, (uint64_t)m * ldc);
   if (rc) return rc;
-  EpiStoreT<float> epi{(int)m, 0, 0};
+  epi.m = (int)m;
   if (terms_a == 1)
-    return launch_tc<1, 1, 256>(A, (uint64_t)kp, B, (uint64_t)kp, (uint64_t)rows_b, args, 1, epi, as_stream(stream),
-                                &tmc);
-  return launch_tc<2, 1, 256>(A, 2ull * kp, B, (uint64_t)kp, (uint64_t)rows_b, args, 1, epi, as_stream(stream), &tmc);
+    return launch_tc<1, 1, 256>(A, (uint64_t)kp, B, (uint64_t)kp, (uint64_t)rows_b, args, 1, epi, as_stream(stream));
+  return launch_tc<2, 1, 256>(A, 2ull * kp, B, (uint64_t)kp, (uint64_t)rows_b, args, 1, epi, as_stream(stream));
 }
 
 int spa_rw_accept(float* beta, int32_t ldb, const void* eps, int32_t q, int64_t m, const double* ylin_p,

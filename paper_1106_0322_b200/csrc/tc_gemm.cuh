@@ -27,12 +27,16 @@ constexpr int kTcThreads = 192;
 constexpr int kTcBM = 128;
 constexpr int kTcBK = 64;  // bf16 elements per 128-byte swizzled row
 
-template <int TA, int TB, int BN, int TM = 1>
+constexpr int kTcSmemLimit = 232448;  // 227 KB dynamic shared memory per CTA
+
+// EpiBytes: shared memory the epilogue needs (its staging / tables); the
+// stage ring gets what remains (at most 6 stages).
+template <int TA, int TB, int BN, int TM = 1, int EpiBytes = 0>
 struct TcShape {
   static constexpr int kABytes = kTcBM * kTcBK * 2;  // 16 KB per A term and m-tile
   static constexpr int kBBytes = BN * kTcBK * 2;     // per B term
   static constexpr int kStageBytes = TM * TA * kABytes + TB * kBBytes;
-  static constexpr int kBudget = 196 * 1024;
+  static constexpr int kBudget = kTcSmemLimit - 1024 /*align*/ - 256 /*barriers*/ - EpiBytes;
   static constexpr int kStagesRaw = kBudget / kStageBytes;
   static constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
   static constexpr int kRingBytes = kStages * kStageBytes;
@@ -53,26 +57,30 @@ struct TcArgs {
 };
 
 // (the epilogue contract is documented with the epilogues below)
-// Dynamic shared memory: [stage ring][epilogue staging, 4 warps][barriers],
-// 1024-aligned (SW128 operands and swizzled store staging).
+// Dynamic shared memory: [stage ring][epilogue region (Epi::kSmemBytes)]
+// [barriers], 1024-aligned (SW128 operands, swizzled staging).
 template <int TA, int TB, int BN, class Epi, int TM = 1>
 constexpr int tc_smem_bytes() {
-  return TcShape<TA, TB, BN, TM>::kRingBytes + 4 * Epi::kScratchPerWarp + 1024 /*align*/ + 256 /*barriers*/;
+  return TcShape<TA, TB, BN, TM, Epi::kSmemBytes>::kRingBytes + Epi::kSmemBytes + 1024 /*align*/ +
+         256 /*barriers*/;
 }
 
+// The epilogue object is a __grid_constant__ parameter: its tensor maps stay
+// addressable in parameter space for TMA; per-thread mutable state lives in
+// Epi::State.
 template <int TA, int TB, int BN, class Epi, int TM = 1>
 __global__ void __launch_bounds__(kTcThreads, 1)
-    tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
-                   const __grid_constant__ CUtensorMap tmc, TcArgs args, Epi epi) {
-  using S = TcShape<TA, TB, BN, TM>;
-  static_assert(tc_smem_bytes<TA, TB, BN, Epi, TM>() <= 232448, "shared memory budget exceeded");
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, TcArgs args,
+                   const __grid_constant__ Epi epi) {
+  using S = TcShape<TA, TB, BN, TM, Epi::kSmemBytes>;
+  static_assert(tc_smem_bytes<TA, TB, BN, Epi, TM>() <= kTcSmemLimit, "shared memory budget exceeded");
   static_assert(TM == 1 || !Epi::kRowState, "TM > 1 interleaves rows: stateless epilogues only");
   extern __shared__ uint8_t smem_raw[];
   // align by pointer arithmetic on the shared array (keeps the shared
   // address space visible to the compiler: LDS/STS, not generic LD/ST)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* staging = smem + S::kRingBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(staging + 4 * Epi::kScratchPerWarp);
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + Epi::kSmemBytes);
   uint64_t* empty = full + S::kStages;
   uint64_t* tfull = empty + S::kStages;
   uint64_t* tempty = tfull + 2;
@@ -202,8 +210,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   } else {
     // ---------------- epilogue (warps 2..5) ----------------
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-    uint8_t* scratch = staging + (warp - 2) * Epi::kScratchPerWarp;
-    if (Epi::kScratchPerWarp > 0 && lane == 0) prefetch_tmap(&tmc);
+    typename Epi::State st;
+    epi.init(st, staging, warp - 2, args);
     int it = 0;
     for (int w = blockIdx.x; w < items; w += gridDim.x) {
     int mt, unit, nt0, nt1, kb0, kb1;
@@ -211,7 +219,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     (void)kb0;
     (void)kb1;
     const int row = mt * kTcBM + quarter * 32 + lane;
-    epi.begin_unit(row, unit);
+    epi.begin_unit(st, row, unit, nt0 * BN, nt1 * BN);
     for (int nt = nt0; nt < nt1; ++nt, ++it) {
       const int buf = it & 1;
       const uint32_t bph = (it >> 1) & 1;
@@ -228,17 +236,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          epi.consume(row + tm * kTcBM, nt * BN + c * 32, v, args.ncols, scratch, &tmc);
+          epi.consume(st, row + tm * kTcBM, nt * BN + c * 32, v, args.ncols);
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[buf]);
-      epi.end_tile(row);
+      epi.end_tile(st, row);
     }
-    epi.end_unit(row, unit, args.m);
+    epi.end_unit(st, row, unit, args.m);
     }
-    epi.finish();
+    epi.finish(st);
   }
 
   __syncthreads();
@@ -249,27 +257,32 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 }
 
 // ---- epilogues ------------------------------------------------------------
-// Contract (per epilogue thread; a warp's 32 threads hold 32 consecutive rows):
-//   kRowState, kScratchPerWarp (bytes of 1024-aligned smem per epilogue warp)
-//   begin_unit(row, unit) / end_tile(row) / end_unit(row, unit, m)
-//   consume(row, col0, v[32], ncols, scratch, tmc): columns col0..col0+31 of row
-//   finish()                                     once, after the last item
+// Contract (the epilogue object is read-only; per-thread state in State; a
+// warp's 32 threads hold 32 consecutive rows = one TMEM lane quarter):
+//   kRowState   true if State carries per-row sums across tiles
+//   kSmemBytes  shared memory of the epilogue region (1024-aligned base)
+//   init(st, smem, ew, args)               once per epilogue thread (ew = 0..3)
+//   begin_unit(st, row, unit, c0, c1)      per work item (columns [c0, c1))
+//   consume(st, row, col0, v[32], ncols)   32 consecutive columns of one row
+//   end_tile(st, row) / end_unit(st, row, unit, m) / finish(st)
 
 // Likelihood: per row sum over valid columns of softplus(eta); eta never
 // leaves the SM.  Partial sums per unit are written to ws[unit][m] (float64)
 // and reduced in fixed unit order by a second kernel (deterministic).
 struct EpiSoftplusRowSum {
   static constexpr bool kRowState = true;
-  static constexpr int kScratchPerWarp = 0;
+  static constexpr int kSmemBytes = 0;
   double* partial;
-  float tile_acc;
-  double acc;
-  __device__ __forceinline__ void begin_unit(int, int) {
-    acc = 0.0;
-    tile_acc = 0.0f;
+  struct State {
+    float tile_acc;
+    double acc;
+  };
+  __device__ __forceinline__ void init(State&, uint8_t*, int, const TcArgs&) const {}
+  __device__ __forceinline__ void begin_unit(State& s, int, int, int, int) const {
+    s.acc = 0.0;
+    s.tile_acc = 0.0f;
   }
-  __device__ __forceinline__ void consume(int, int col0, const float (&v)[32], int ncols, uint8_t*,
-                                          const CUtensorMap*) {
+  __device__ __forceinline__ void consume(State& s, int, int col0, const float (&v)[32], int ncols) const {
     if (col0 + 32 <= ncols) {
       float s0 = 0.f, s1 = 0.f;
 #pragma unroll
@@ -277,46 +290,55 @@ struct EpiSoftplusRowSum {
         s0 += softplus_f32(v[i]);
         s1 += softplus_f32(v[i + 1]);
       }
-      tile_acc += s0 + s1;
+      s.tile_acc += s0 + s1;
     } else {
 #pragma unroll
       for (int i = 0; i < 32; ++i)
-        if (col0 + i < ncols) tile_acc += softplus_f32(v[i]);
+        if (col0 + i < ncols) s.tile_acc += softplus_f32(v[i]);
     }
   }
-  __device__ __forceinline__ void end_tile(int) {
-    acc += (double)tile_acc;
-    tile_acc = 0.0f;
+  __device__ __forceinline__ void end_tile(State& s, int) const {
+    s.acc += (double)s.tile_acc;
+    s.tile_acc = 0.0f;
   }
-  __device__ __forceinline__ void end_unit(int row, int unit, int m) {
-    if (row < m) partial[(size_t)unit * m + row] = acc;
+  __device__ __forceinline__ void end_unit(State& s, int row, int unit, int m) const {
+    if (row < m) partial[(size_t)unit * m + row] = s.acc;
   }
-  __device__ __forceinline__ void finish() {}
+  __device__ __forceinline__ void finish(State&) const {}
 };
 
 // Raw accumulator store through TMA: each thread writes its row's 32 columns
 // (64 B bf16 / 128 B fp32) into a per-warp swizzled staging tile (SW64 /
 // SW128: conflict-free 16-byte shared stores), then one lane issues a 3-D
 // bulk tensor store of the 32 x 32 box at (col0, row0, unit).  The tensor map
-// (tmc, built by the launcher) clips columns >= ncols, rows >= m and keeps
+// tmc (built by the launcher) clips columns >= ncols, rows >= m and keeps
 // split-K units apart.  Two staging buffers per warp alternate; a buffer is
 // rewritten only after its previous store has finished reading it.
 template <class OutT>
 struct EpiStoreT {
   static constexpr bool kRowState = false;
   static constexpr int kBoxBytes = 32 * 32 * (int)sizeof(OutT);
-  static constexpr int kScratchPerWarp = 2 * kBoxBytes;
+  static constexpr int kSmemBytes = 4 * 2 * kBoxBytes;
+  CUtensorMap tmc;
   int m;
-  int unit_;
-  int nbuf_;
-  __device__ __forceinline__ void begin_unit(int, int unit) { unit_ = unit; }
-  __device__ __forceinline__ void consume(int row, int col0, const float (&v)[32], int, uint8_t* scratch,
-                                          const CUtensorMap* tmc) {
+  struct State {
+    uint8_t* scratch;
+    int unit;
+    int nbuf;
+  };
+  __device__ __forceinline__ void init(State& s, uint8_t* smem, int ew, const TcArgs&) const {
+    s.scratch = smem + ew * 2 * kBoxBytes;
+    s.unit = 0;
+    s.nbuf = 0;
+    if ((threadIdx.x & 31) == 0) prefetch_tmap(&tmc);
+  }
+  __device__ __forceinline__ void begin_unit(State& s, int, int unit, int, int) const { s.unit = unit; }
+  __device__ __forceinline__ void consume(State& s, int row, int col0, const float (&v)[32], int) const {
     const int lane = threadIdx.x & 31;
     const int row0 = row - lane;  // warp-uniform
     if (row0 >= m) return;
-    uint8_t* buf = scratch + (nbuf_ & 1) * kBoxBytes;
-    ++nbuf_;
+    uint8_t* buf = s.scratch + (s.nbuf & 1) * kBoxBytes;
+    ++s.nbuf;
     if (lane == 0) bulk_wait_read<1>();
     __syncwarp();
     if constexpr (sizeof(OutT) == 2) {
@@ -346,13 +368,13 @@ struct EpiStoreT {
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
-      tma_store_3d(tmc, buf, col0, row0, unit_);
+      tma_store_3d(&tmc, buf, col0, row0, s.unit);
       bulk_commit();
     }
   }
-  __device__ __forceinline__ void end_tile(int) {}
-  __device__ __forceinline__ void end_unit(int, int, int) {}
-  __device__ __forceinline__ void finish() {
+  __device__ __forceinline__ void end_tile(State&, int) const {}
+  __device__ __forceinline__ void end_unit(State&, int, int, int) const {}
+  __device__ __forceinline__ void finish(State&) const {
     if ((threadIdx.x & 31) == 0) bulk_wait<0>();
   }
 };
