@@ -209,6 +209,29 @@ int spa_rw_accept(float* beta, int32_t ldb, const void* eps, int32_t q, int64_t 
                   const double* sp_p, const double* lp_p, double* ll, double* lp, uint64_t seed, int64_t t,
                   int64_t i0, int32_t move, unsigned long long* accepted, void* stream);
 
+/* ---- f1: per-step weighted marginal summaries (summary.py:36-61) --------
+ * Weighted mean, weighted quantiles at nlev <= 4 levels ("smallest value whose
+ * cumulative weight reaches q", summary.py:36-45) and concentration
+ * V(delta) = mass outside (-delta, delta) for ndelta <= 4 deltas, per
+ * coordinate of beta [m][ldb] (q columns) with normalised weights w [m].
+ * All sums are exact integers (weights as 2^-62 fixed point), so the
+ * accumulators of shards may be added (all-reduce) between the calls:
+ *   pass 0..3: spa_summary_pass (pass 0 zero-initialised hist [1][q][256],
+ *              acc_mean [q], acc_in [ndelta][q], total [1]; pass p > 0 a
+ *              zeroed hist [nlev][q][256]), then spa_summary_select;
+ *   then spa_summary_finish -> out_mean [q], out_quant [nlev][q],
+ *   out_conc [ndelta][q] (float64). */
+int spa_summary_pass(const float* beta, int64_t m, int32_t ldb, int32_t q, const double* w, int32_t nlev,
+                     const double* levels, int32_t ndelta, const double* deltas, int32_t pass, const uint32_t* prefix,
+                     unsigned long long* hist, unsigned long long* acc_mean, unsigned long long* acc_in,
+                     unsigned long long* total, void* stream);
+int spa_summary_select(const unsigned long long* hist, int32_t q, int32_t nlev, const double* levels, int32_t pass,
+                       const unsigned long long* total, uint32_t* prefix, unsigned long long* below, void* stream);
+int spa_summary_finish(int32_t q, int32_t nlev, int32_t ndelta, const uint32_t* prefix,
+                       const unsigned long long* acc_mean, const unsigned long long* acc_in,
+                       const unsigned long long* total, double* out_mean, double* out_quant, double* out_conc,
+                       void* stream);
+
 /* Load every kernel of the library on the current device now (instead of
  * lazily at first launch) -- run_sampler calls it during initialisation. */
 int spa_prepare(void);

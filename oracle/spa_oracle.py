@@ -304,3 +304,33 @@ def rw_move_rows(B, ll, lp, X, y, a, c, Ls, Z, U, penalized=None):
         ok = (d >= 0.0) | (np.log(U) < d)
     B2 = np.where(ok[:, None], prop, B)
     return B2, np.where(ok, ll_p, ll), np.where(ok, lp_p, lp), ok
+
+
+# ---------------------------------------------------------------------------
+# Path summaries (reference summary.py:36-61) -- the per-step marginals the
+# device summary kernels (spa_summary_*) compute.
+
+
+def weighted_quantile(values, weights, q: float) -> float:
+    """summary.py:36-45: smallest value whose cumulative weight reaches q
+    (stable sort, sequential float64 cumsum, searchsorted left)."""
+    values = np.asarray(values, dtype=float)
+    weights = np.asarray(weights, dtype=float)
+    order = np.argsort(values, kind="stable")
+    cum = np.cumsum(weights[order])
+    idx = int(np.searchsorted(cum, q * cum[-1], side="left"))
+    return float(values[order][min(idx, values.size - 1)])
+
+
+def weighted_mean(values, weights) -> float:
+    """summary.py:48-51."""
+    values = np.asarray(values, dtype=float)
+    weights = np.asarray(weights, dtype=float)
+    return float(values @ weights / weights.sum())
+
+
+def concentration(samples, weights, delta: float) -> float:
+    """summary.py:54-61: weighted mass outside the open interval (-delta, delta)."""
+    samples = np.asarray(samples, dtype=float)
+    weights = np.asarray(weights, dtype=float)
+    return 1.0 - float(weights[np.abs(samples) < delta].sum() / weights.sum())

@@ -9,6 +9,7 @@ __version__ = "0.1.0+b200"
 
 from .data import Dataset, SimSpec, named_spec, simulate_dataset  # noqa: F401
 from .model import GtPrior  # noqa: F401
+from . import summary  # noqa: F401
 from .smc import (  # noqa: F401
     DegeneracyError,
     ParticleSystem,
@@ -21,6 +22,7 @@ from .smc import (  # noqa: F401
     init_particles,
     load_run,
     make_schedule,
+    marginal_summaries,
     reweight,
     run_sampler,
     save_run,

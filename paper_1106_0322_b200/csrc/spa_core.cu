@@ -152,6 +152,10 @@ __device__ __forceinline__ float gt_logpdf_f(float b, float lc, float ap1, float
   return de ? lc - x * inv : lc - ap1 * log1pf(x * inv);
 }
 
+constexpr double kFix = 281474976710656.0;  // 2^48
+
+__device__ __forceinline__ unsigned long long to_fix(double v) { return (unsigned long long)llrint(v * kFix); }
+__device__ __forceinline__ double from_fix(unsigned long long v) { return (double)(long long)v / kFix; }
 // Per-lane log-prior accumulator shared by pack_kernel, pack_eps_kernel and
 // prior_kernel mode 2 (same lane->column mapping and multiplication order, so
 // all three produce identical bits):
@@ -592,6 +596,242 @@ __global__ void __launch_bounds__(256) prior_reweight_rows_kernel(spa_design d, 
 }
 
 // ---------------------------------------------------------------------------
+// f1: per-step weighted marginal summaries (reference summary.py:36-61) on
+// the device -- weighted mean, weighted quantiles ("smallest value whose
+// cumulative weight reaches q") and concentration V(delta) per coordinate.
+// Weights are 2^-62 fixed point and every sum is an exact integer sum, so
+// results do not depend on the schedule or the number of GPUs (histograms
+// all-reduce exactly).  Quantiles by 4-pass radix select on order-preserving
+// 32-bit keys of the float32 particles: pass p histograms the p-th key byte
+// of the rows whose higher bytes match the level's prefix, a select step
+// picks the byte where the cumulative weight reaches q * total.
+constexpr int kSumMaxLev = 4, kSumMaxDelta = 4, kSumCols = 8, kSumRows = 2048, kSumTile = 256;
+constexpr double kWFix = 4611686018427387904.0;  // 2^62
+
+struct SumParams {
+  int nlev, ndelta;
+  double level[kSumMaxLev];
+  float delta[kSumMaxDelta];
+};
+
+__device__ __forceinline__ uint32_t sum_key(float x) {
+  const uint32_t u = __float_as_uint(x);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float sum_unkey(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+__device__ __forceinline__ unsigned long long sum_wfix(double w) {
+  return w > 0.0 ? (unsigned long long)llrint(w * kWFix) : 0ull;
+}
+
+// Shared-memory 64-bit bin counters as two native 32-bit atomics (a 64-bit
+// shared atomicAdd compiles to a CAS spin loop): the low-word add returns the
+// old value, so each adder knows its own carry exactly.
+__device__ __forceinline__ void sum_add64(uint32_t* h2, unsigned long long v) {
+  const uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
+  const uint32_t old = atomicAdd(h2, lo);
+  const uint32_t carry = (old + lo < old) ? 1u : 0u;
+  if (hi + carry) atomicAdd(h2 + 1, hi + carry);
+}
+
+// Warp-wide histogram add of (bin, v) for the lanes with `hit` (called by
+// all 32 lanes): up to kAgg distinct bins are summed in registers first
+// (ballot + __reduce_add_sync over 21-bit limbs) -- pass 0 keys (sign and
+// exponent) concentrate in few bins, which would otherwise serialise on one
+// counter -- the rest add directly (later passes: spread digits, kAgg = 0).
+template <int kAgg>
+__device__ __forceinline__ void sum_warp_add(uint32_t* h2, bool hit, uint32_t bin, unsigned long long v) {
+  const int lane = threadIdx.x & 31;
+  unsigned pending = __ballot_sync(0xffffffffu, hit);
+#pragma unroll 1
+  for (int it = 0; it < kAgg && pending; ++it) {
+    const int leader = __ffs(pending) - 1;
+    const uint32_t b = __shfl_sync(0xffffffffu, bin, leader);
+    const bool mine = hit && bin == b && ((pending >> lane) & 1u);
+    const unsigned grp = __ballot_sync(0xffffffffu, mine);
+    const uint32_t l0 = mine ? (uint32_t)(v & 0x1FFFFFull) : 0u;
+    const uint32_t l1 = mine ? (uint32_t)((v >> 21) & 0x1FFFFFull) : 0u;
+    const uint32_t l2 = mine ? (uint32_t)(v >> 42) : 0u;
+    const unsigned long long s = (unsigned long long)__reduce_add_sync(0xffffffffu, l0) +
+                                 ((unsigned long long)__reduce_add_sync(0xffffffffu, l1) << 21) +
+                                 ((unsigned long long)__reduce_add_sync(0xffffffffu, l2) << 42);
+    if (lane == leader) sum_add64(h2 + 2 * b, s);
+    pending &= ~grp;
+  }
+  if ((pending >> lane) & 1u) sum_add64(h2 + 2 * bin, v);
+}
+
+// Pass p over a block of kSumCols columns x kSumRows particles, staged per
+// kSumTile-row tile in shared memory; warp c owns column c0 + c.  Pass 0 also
+// accumulates the weighted mean (2^-48 fixed point), the mass inside
+// (-delta, delta) per delta and the total weight (2^-62 fixed point).
+__global__ void __launch_bounds__(256) summary_hist_kernel(const float* __restrict__ beta, int64_t m, int ldb, int q,
+                                                           const double* __restrict__ w, SumParams sp, int pass,
+                                                           const uint32_t* __restrict__ prefix,
+                                                           unsigned long long* __restrict__ hist,
+                                                           unsigned long long* __restrict__ acc_mean,
+                                                           unsigned long long* __restrict__ acc_in,
+                                                           unsigned long long* __restrict__ total) {
+  extern __shared__ uint32_t sh[];  // [nh][kSumCols][256] x {lo, hi} words
+  __shared__ float xs[kSumTile][kSumCols + 1];
+  __shared__ unsigned long long wf[kSumTile];
+  __shared__ double wd[kSumTile];
+  const int nh = pass == 0 ? 1 : sp.nlev;
+  for (int e = threadIdx.x; e < nh * kSumCols * 256 * 2; e += blockDim.x) sh[e] = 0u;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = blockIdx.x * kSumCols, col = c0 + warp;
+  const int64_t r0 = (int64_t)blockIdx.y * kSumRows;
+  uint32_t pre[kSumMaxLev];
+#pragma unroll
+  for (int l = 0; l < kSumMaxLev; ++l) pre[l] = (pass > 0 && l < sp.nlev && col < q) ? prefix[l * q + col] : 0u;
+  double smean = 0.0;
+  unsigned long long sin[kSumMaxDelta] = {0ull, 0ull, 0ull, 0ull}, stot = 0ull;
+  for (int64_t t0 = r0; t0 < min(m, r0 + kSumRows); t0 += kSumTile) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < kSumTile * kSumCols; e += blockDim.x) {
+      const int rr = e / kSumCols, cc = e % kSumCols;
+      const int64_t row = t0 + rr;
+      xs[rr][cc] = (row < m && c0 + cc < q) ? beta[row * ldb + c0 + cc] : 0.f;
+    }
+    for (int rr = threadIdx.x; rr < kSumTile; rr += blockDim.x) {
+      const int64_t row = t0 + rr;
+      const double wv = row < m ? w[row] : 0.0;
+      wd[rr] = wv;
+      wf[rr] = sum_wfix(wv);
+    }
+    __syncthreads();
+    if (col >= q) continue;
+    for (int rr = lane; rr < kSumTile; rr += 32) {
+      const bool live = t0 + rr < m;
+      const float x = xs[rr][warp];
+      const unsigned long long v = wf[rr];
+      const uint32_t key = sum_key(x);
+      if (pass == 0) {
+        if (live) {
+          smean = fma(wd[rr], (double)x, smean);
+#pragma unroll
+          for (int dd = 0; dd < kSumMaxDelta; ++dd)
+            if (dd < sp.ndelta && fabsf(x) < sp.delta[dd]) sin[dd] += v;
+          if (warp == 0) stot += v;
+        }
+        sum_warp_add<2>(sh + warp * 512, live && v != 0ull, key >> 24, v);
+      } else {
+        const int shift = 32 - 8 * pass;
+        const uint32_t top = key >> shift, dig = (key >> (shift - 8)) & 255u;
+        bool any = false;
+#pragma unroll
+        for (int l = 0; l < kSumMaxLev; ++l) any |= (l < sp.nlev) && top == pre[l];
+        any = any && live && v != 0ull;
+        if (__ballot_sync(0xffffffffu, any) == 0u) continue;  // most rows match no level's prefix
+#pragma unroll
+        for (int l = 0; l < kSumMaxLev; ++l) {
+          if (l >= sp.nlev) break;
+          sum_warp_add<0>(sh + (l * kSumCols + warp) * 512, any && top == pre[l], dig, v);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nh * kSumCols * 256; e += blockDim.x) {
+    const int l = e / (kSumCols * 256), cc = (e / 256) % kSumCols, bin = e % 256;
+    const unsigned long long v = (unsigned long long)sh[2 * e] | ((unsigned long long)sh[2 * e + 1] << 32);
+    if (v != 0ull && c0 + cc < q) atomicAdd(&hist[((size_t)l * q + c0 + cc) * 256 + bin], v);
+  }
+  if (pass == 0 && col < q) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) smean += __shfl_xor_sync(0xffffffffu, smean, o);
+#pragma unroll
+    for (int dd = 0; dd < kSumMaxDelta; ++dd) {
+      unsigned long long v = sin[dd];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && dd < sp.ndelta && v) atomicAdd(&acc_in[(size_t)dd * q + col], v);
+    }
+    if (lane == 0) atomicAdd(&acc_mean[col], to_fix(smean));
+    if (warp == 0) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) stot += __shfl_xor_sync(0xffffffffu, stot, o);
+      if (lane == 0 && blockIdx.x == 0) atomicAdd(total, stot);
+    }
+  }
+}
+
+// One warp per (level, column): lanes own 8 bins each; a shuffle scan of the
+// lane sums finds the byte whose cumulative weight reaches level * total,
+// then the prefix is extended and the weight below it carried.
+__global__ void summary_select_kernel(const unsigned long long* __restrict__ hist, int q, SumParams sp, int pass,
+                                      const unsigned long long* __restrict__ total, uint32_t* __restrict__ prefix,
+                                      unsigned long long* __restrict__ below) {
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= sp.nlev * q) return;  // warp-uniform
+  const int l = i / q, col = i % q;
+  const unsigned long long* h = hist + ((size_t)(pass == 0 ? 0 : l) * q + col) * 256 + lane * 8;
+  // target = ceil(level * total) in exact integer arithmetic (level as 2^-64 fixed point)
+  const unsigned long long qf = (unsigned long long)(sp.level[l] * 18446744073709551616.0);
+  const unsigned long long T = *total;
+  const unsigned long long target = __umul64hi(qf, T) + ((qf * T) != 0ull ? 1ull : 0ull);
+  const unsigned long long base = pass == 0 ? 0ull : below[i];
+  unsigned long long hv[8], ls = 0ull;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    hv[k] = h[k];
+    ls += hv[k];
+  }
+  unsigned long long incl = ls;  // inclusive scan over lanes
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  const unsigned long long excl = incl - ls;
+  const unsigned reach = __ballot_sync(0xffffffffu, base + incl >= target);
+  const unsigned nz = __ballot_sync(0xffffffffu, ls != 0ull);
+  int pick_lane, pick = -1;
+  unsigned long long acc = 0ull;
+  if (reach) {
+    pick_lane = __ffs(reach) - 1;
+    if (lane == pick_lane) {
+      acc = base + excl;
+      for (int k = 0; k < 8; ++k) {
+        if (hv[k] == 0ull) continue;
+        if (acc + hv[k] >= target) {
+          pick = lane * 8 + k;
+          break;
+        }
+        acc += hv[k];
+      }
+    }
+  } else {  // rounding left the target above the total: the largest value
+    pick_lane = 31 - __clz(nz);
+    if (lane == pick_lane) {
+      int kk = 7;
+      while (kk > 0 && hv[kk] == 0ull) --kk;
+      pick = lane * 8 + kk;
+      acc = base + incl - hv[kk];
+    }
+  }
+  if (lane == pick_lane) {
+    below[i] = acc;
+    prefix[i] = (pass == 0 ? 0u : prefix[i] << 8) | (uint32_t)pick;
+  }
+}
+
+__global__ void summary_finish_kernel(int q, SumParams sp, const uint32_t* __restrict__ prefix,
+                                      const unsigned long long* __restrict__ acc_mean,
+                                      const unsigned long long* __restrict__ acc_in,
+                                      const unsigned long long* __restrict__ total, double* __restrict__ out_mean,
+                                      double* __restrict__ out_quant, double* __restrict__ out_conc) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= q) return;
+  const double W = (double)*total / kWFix;
+  out_mean[j] = from_fix(acc_mean[j]) / W;
+  for (int l = 0; l < sp.nlev; ++l) out_quant[(size_t)l * q + j] = (double)sum_unkey(prefix[(size_t)l * q + j]);
+  for (int d = 0; d < sp.ndelta; ++d)
+    out_conc[(size_t)d * q + j] = 1.0 - (double)acc_in[(size_t)d * q + j] / (double)*total;
+}
+
+// ---------------------------------------------------------------------------
 // K3: fixed-chunk log-sum-exp statistics
 constexpr int kChunk = 4096;
 
@@ -851,10 +1091,6 @@ __global__ void reduce_units_kernel(const double* __restrict__ partial, int unit
 // converted to 2^-48 fixed point before 64-bit integer atomics: integer sums
 // are associative, so the moments are bit-identical for any CTA order or GPU
 // count (the same property the reference guarantees for `threads`).
-constexpr double kFix = 281474976710656.0;  // 2^48
-
-__device__ __forceinline__ unsigned long long to_fix(double v) { return (unsigned long long)llrint(v * kFix); }
-__device__ __forceinline__ double from_fix(unsigned long long v) { return (double)(long long)v / kFix; }
 
 // Weighted mean sum_k w_k beta_kj over a 128-particle block: row-major,
 // coalesced reads (warp w takes rows w, w+NW, ..; lane l columns 4 (l + 32 it)
@@ -1483,6 +1719,77 @@ int spa_prior_reweight(const spa_design* d, const float* beta, int64_t m, int32_
   return 0;
 }
 
+static int sum_params(int32_t nlev, const double* levels, int32_t ndelta, const double* deltas, SumParams* sp) {
+  SPA_REQUIRE(nlev >= 0 && nlev <= kSumMaxLev && ndelta >= 0 && ndelta <= kSumMaxDelta, kBadArgument,
+              "spa_summary: at most 4 levels and 4 deltas");
+  sp->nlev = nlev;
+  sp->ndelta = ndelta;
+  for (int i = 0; i < kSumMaxLev; ++i) sp->level[i] = i < nlev ? levels[i] : 0.5;
+  for (int i = 0; i < kSumMaxDelta; ++i) sp->delta[i] = i < ndelta ? (float)deltas[i] : 0.f;
+  for (int i = 0; i < nlev; ++i) SPA_REQUIRE(levels[i] > 0.0 && levels[i] < 1.0, kBadArgument, "spa_summary: level");
+  for (int i = 0; i < ndelta; ++i) SPA_REQUIRE(deltas[i] > 0.0, kBadArgument, "spa_summary: delta");
+  return 0;
+}
+
+int spa_summary_pass(const float* beta, int64_t m, int32_t ldb, int32_t q, const double* w, int32_t nlev,
+                     const double* levels, int32_t ndelta, const double* deltas, int32_t pass, const uint32_t* prefix,
+                     unsigned long long* hist, unsigned long long* acc_mean, unsigned long long* acc_in,
+                     unsigned long long* total, void* stream) {
+  SPA_REQUIRE(beta && w && hist && m >= 0 && q > 0 && pass >= 0 && pass < 4, kBadArgument,
+              "spa_summary_pass: bad arguments");
+  SPA_REQUIRE(pass == 0 ? (acc_mean && total && (ndelta == 0 || acc_in)) : prefix != nullptr, kBadArgument,
+              "spa_summary_pass: missing accumulators");
+  SumParams sp;
+  int rc = sum_params(nlev, levels, ndelta, deltas, &sp);
+  if (rc) return rc;
+  if (m == 0) return 0;
+  const int nh = pass == 0 ? 1 : nlev;
+  if (nh == 0) return 0;
+  const size_t smem = (size_t)nh * kSumCols * 256 * 2 * sizeof(uint32_t);
+  static bool attr = false;
+  if (!attr) {
+    SPA_CHECK_CUDA(cudaFuncSetAttribute(summary_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)(kSumMaxLev * kSumCols * 256 * sizeof(unsigned long long))));
+    attr = true;
+  }
+  dim3 grid((unsigned)cdiv(q, kSumCols), (unsigned)cdiv(m, kSumRows));
+  summary_hist_kernel<<<grid, 256, smem, as_stream(stream)>>>(beta, m, ldb, q, w, sp, pass, prefix, hist, acc_mean,
+                                                              acc_in, total);
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+int spa_summary_select(const unsigned long long* hist, int32_t q, int32_t nlev, const double* levels, int32_t pass,
+                       const unsigned long long* total, uint32_t* prefix, unsigned long long* below, void* stream) {
+  SPA_REQUIRE(hist && total && prefix && below && q > 0 && pass >= 0 && pass < 4, kBadArgument,
+              "spa_summary_select: bad arguments");
+  SumParams sp;
+  int rc = sum_params(nlev, levels, 0, nullptr, &sp);
+  if (rc) return rc;
+  if (nlev == 0) return 0;
+  summary_select_kernel<<<cdiv((int64_t)nlev * q * 32, 256), 256, 0, as_stream(stream)>>>(hist, q, sp, pass, total,
+                                                                                            prefix, below);
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+int spa_summary_finish(int32_t q, int32_t nlev, int32_t ndelta, const uint32_t* prefix,
+                       const unsigned long long* acc_mean, const unsigned long long* acc_in,
+                       const unsigned long long* total, double* out_mean, double* out_quant, double* out_conc,
+                       void* stream) {
+  SPA_REQUIRE(acc_mean && total && out_mean && q > 0, kBadArgument, "spa_summary_finish: bad arguments");
+  SPA_REQUIRE((nlev == 0 || (prefix && out_quant)) && (ndelta == 0 || (acc_in && out_conc)), kBadArgument,
+              "spa_summary_finish: missing outputs");
+  SumParams sp;
+  double lv[kSumMaxLev] = {0.5, 0.5, 0.5, 0.5}, dl[kSumMaxDelta] = {1.0, 1.0, 1.0, 1.0};
+  int rc = sum_params(nlev, lv, ndelta, dl, &sp);
+  if (rc) return rc;
+  summary_finish_kernel<<<cdiv(q, 128), 128, 0, as_stream(stream)>>>(q, sp, prefix, acc_mean, acc_in, total, out_mean,
+                                                                     out_quant, out_conc);
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
 int spa_lse_chunk_stats(const double* logw, const double* lw, int64_t m, double* stats, void* stream) {
   SPA_REQUIRE(logw && stats && m > 0, kBadArgument, "spa_lse_chunk_stats: bad arguments");
   lse_stats_kernel<<<cdiv(m, kChunk), kLseThreads, 0, as_stream(stream)>>>(logw, lw, m, stats);
@@ -1764,7 +2071,8 @@ int spa_prepare(void) {
       (const void*)reduce_units_kernel, (const void*)rw_mean_kernel<4>, (const void*)rw_cov_kernel,
       (const void*)rw_chol_panel_kernel, (const void*)rw_emit_kernel,
       (const void*)rw_normals_kernel, (const void*)rw_center_t_kernel, (const void*)rw_accept_kernel,
-      (const void*)syrk_reduce_kernel};
+      (const void*)syrk_reduce_kernel, (const void*)summary_hist_kernel, (const void*)summary_select_kernel,
+      (const void*)summary_finish_kernel};
   for (const void* f : fns) {
     cudaFuncAttributes a;
     SPA_CHECK_CUDA(cudaFuncGetAttributes(&a, f));

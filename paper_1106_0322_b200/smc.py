@@ -15,6 +15,9 @@ Extra SmcConfig fields (defaults keep the reference's behaviour):
     moves        RW moves per step
     rw_scale     RW proposal scale numerator (scale = rw_scale / sqrt(q))
     init_chains  parallel MwG chains for initialisation (0 = auto)
+    summary_levels / summary_deltas
+                 per-step weighted marginal summaries computed on the device
+                 (StepRecord.summary; see marginal_summaries)
 """
 
 from __future__ import annotations
@@ -94,6 +97,8 @@ class SmcConfig:
     moves: int = 5
     rw_scale: float = 2.38
     init_chains: int = 0
+    summary_levels: tuple = ()
+    summary_deltas: tuple = ()
 
     def __post_init__(self):
         if self.N < 2:
@@ -112,6 +117,10 @@ class SmcConfig:
             raise ValueError(f"move_kernel must be 'mwg' or 'rw', got {self.move_kernel!r}")
         if self.moves < 1 or self.init_chains < 0 or not self.rw_scale > 0:
             raise ValueError("moves >= 1, init_chains >= 0, rw_scale > 0 required")
+        if len(self.summary_levels) > 4 or not all(0.0 < float(v) < 1.0 for v in self.summary_levels):
+            raise ValueError("summary_levels: at most 4 quantile levels in (0, 1)")
+        if len(self.summary_deltas) > 4 or not all(float(v) > 0.0 for v in self.summary_deltas):
+            raise ValueError("summary_deltas: at most 4 positive deltas")
 
 
 @dataclass
@@ -127,6 +136,7 @@ class StepRecord:
     weights: np.ndarray | None = None
     particles: np.ndarray | None = None
     logliks: np.ndarray | None = None
+    summary: dict | None = None  # device marginal summaries (SmcConfig.summary_levels/deltas)
 
 
 @dataclass
@@ -733,6 +743,49 @@ def smc_step(system: ParticleSystem, data, schedule: Schedule, t: int, config: S
     return rec
 
 
+def marginal_summaries(system: ParticleSystem, levels=(0.05, 0.5, 0.95), deltas=(0.05, 0.1), group=None,
+                       out=None):
+    """Per-coordinate weighted marginals of the current weighted particle set
+    on the device (reference summary.py:36-61): weighted mean, weighted
+    quantiles at `levels` (smallest value whose cumulative weight reaches the
+    level; exact radix select) and concentration V(delta) = mass outside
+    (-delta, delta).  Sums are exact integers, so sharded runs all-reduce them
+    and get the same result for any number of GPUs.  Returns device float64
+    tensors {"mean": [q], "quantiles": [len(levels)][q], "concentration":
+    [len(deltas)][q]} (written into `out` when given)."""
+    q, dev = system.q, system.device
+    lv = (ctypes.c_double * max(1, len(levels)))(*[float(v) for v in levels])
+    dl = (ctypes.c_double * max(1, len(deltas)))(*[float(v) for v in deltas])
+    nl, nd = len(levels), len(deltas)
+    w = system.device_weights() if group is None else _global_weights(system, group)
+    u64 = dict(dtype=torch.int64, device=dev)
+    hist = torch.zeros((max(1, nl), q, 256), **u64)
+    acc_mean = torch.zeros(q, **u64)
+    acc_in = torch.zeros((max(1, nd), q), **u64)
+    total = torch.zeros(1, **u64)
+    prefix = torch.zeros((max(1, nl), q), dtype=torch.int32, device=dev)
+    below = torch.zeros((max(1, nl), q), **u64)
+    if out is None:
+        f64 = dict(dtype=torch.float64, device=dev)
+        out = {"mean": torch.empty(q, **f64), "quantiles": torch.empty((nl, q), **f64),
+               "concentration": torch.empty((nd, q), **f64)}
+    for ps in range(4 if nl else 1):
+        if ps:
+            hist.zero_()
+        _lib.call("spa_summary_pass", _p(system.beta), system.N, system.ldb, q, _p(w), nl, lv, nd, dl, ps,
+                  _p(prefix), _p(hist), _p(acc_mean), _p(acc_in), _p(total), _stream())
+        if group is not None:
+            group.all_reduce_sum(hist)
+            if ps == 0:
+                for t_ in (acc_mean, acc_in, total):
+                    group.all_reduce_sum(t_)
+        if nl:
+            _lib.call("spa_summary_select", _p(hist), q, nl, lv, ps, _p(total), _p(prefix), _p(below), _stream())
+    _lib.call("spa_summary_finish", q, nl, nd, _p(prefix), _p(acc_mean), _p(acc_in), _p(total), _p(out["mean"]),
+              _p(out["quantiles"]) if nl else None, _p(out["concentration"]) if nd else None, _stream())
+    return out
+
+
 class _SnapshotWriter:
     """Copies retained steps out without stalling the step loop.
 
@@ -827,7 +880,18 @@ def run_sampler(data, a: float, schedule: Schedule, config: SmcConfig, intercept
     timings["snapshot_s"] = 0.0
     writer = _SnapshotWriter()
 
+    summ = None
+    if config.summary_levels or config.summary_deltas:
+        f64 = dict(dtype=torch.float64, device=system.device)
+        q, T = system.q, schedule.T
+        summ = {"mean": torch.empty((T, q), **f64),
+                "quantiles": torch.empty((T, len(config.summary_levels), q), **f64),
+                "concentration": torch.empty((T, len(config.summary_deltas), q), **f64)}
+
     def snap(rec):
+        if summ is not None:  # every step, retained or not (no host sync)
+            marginal_summaries(system, config.summary_levels, config.summary_deltas, group,
+                               out={k: v[rec.t - 1] for k, v in summ.items()})
         if not retained(rec.t):
             return rec
         ts = time.perf_counter()
@@ -841,6 +905,13 @@ def run_sampler(data, a: float, schedule: Schedule, config: SmcConfig, intercept
         for t in range(2, schedule.T + 1):
             steps.append(snap(smc_step(system, data, schedule, t, config, group, _defer=True)))
         resolve_records(system, steps)  # one read of the deferred step records
+        if summ is not None:
+            host = {k: v.cpu().numpy() for k, v in summ.items()}
+            names_k = {"levels": tuple(float(v) for v in config.summary_levels),
+                       "deltas": tuple(float(v) for v in config.summary_deltas)}
+            for s in steps:
+                s.summary = {"mean": host["mean"][s.t - 1], "quantiles": host["quantiles"][s.t - 1],
+                             "concentration": host["concentration"][s.t - 1], **names_k}
         torch.cuda.synchronize()
         timings["path_s"] = time.perf_counter() - t1
         ts = time.perf_counter()

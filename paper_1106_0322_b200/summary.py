@@ -1,0 +1,84 @@
+"""Path summaries from the device marginal summaries (reference summary.py).
+
+`run_sampler` with `SmcConfig(summary_levels=..., summary_deltas=...)` stores
+per-step weighted marginals computed on the GPU in `StepRecord.summary`
+(`smc.marginal_summaries`), for every step whether or not its particles are
+retained.  These functions assemble the reference's path views from them,
+with the reference's names and shapes (summary.py:64-94, 113-122):
+
+    mean_path(out)              -> [T][q]   (summary.py:83-85)
+    quantile_path(out, q)       -> [T][q]   (summary.py:64-74), q one of the levels
+    abs_median_path(out)        -> [T][q]   (summary.py:77-79)
+    concentration_path(out, d)  -> [T][q]   (summary.py:88-97), d one of the deltas
+    c_posterior(out)            -> CPosterior (summary.py:113-122)
+
+Quantiles follow summary.py:36-45 exactly (smallest value whose cumulative
+weight reaches the level), the mean and V(delta) to float64 rounding.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+class SummaryError(ValueError):
+    """The run did not compute the requested device summary."""
+
+
+def _summaries(output):
+    recs = output.steps
+    if not recs or any(r.summary is None for r in recs):
+        raise SummaryError("no device summaries: run with SmcConfig(summary_levels=..., summary_deltas=...)")
+    return recs
+
+
+def mean_path(output) -> np.ndarray:
+    return np.stack([r.summary["mean"] for r in _summaries(output)])
+
+
+def quantile_path(output, q: float) -> np.ndarray:
+    recs = _summaries(output)
+    levels = recs[0].summary["levels"]
+    hits = [i for i, v in enumerate(levels) if abs(v - q) < 1e-12]
+    if not hits:
+        raise SummaryError(f"quantile level {q} was not computed (levels {levels})")
+    return np.stack([r.summary["quantiles"][hits[0]] for r in recs])
+
+
+def abs_median_path(output) -> np.ndarray:
+    return np.abs(quantile_path(output, 0.5))
+
+
+def concentration_path(output, delta: float) -> np.ndarray:
+    recs = _summaries(output)
+    deltas = recs[0].summary["deltas"]
+    hits = [i for i, v in enumerate(deltas) if abs(v - delta) < 1e-12]
+    if not hits:
+        raise SummaryError(f"delta {delta} was not computed (deltas {deltas})")
+    return np.stack([r.summary["concentration"][hits[0]] for r in recs])
+
+
+@dataclass
+class CPosterior:
+    """Discrete posterior over the scale grid {c_t = b_t / a} (summary.py:98-110)."""
+
+    c: np.ndarray
+    mass: np.ndarray
+
+    @property
+    def mode_index(self) -> int:
+        return int(np.argmax(self.mass))
+
+    @property
+    def mode(self) -> float:
+        return float(self.c[self.mode_index])
+
+
+def c_posterior(output) -> CPosterior:
+    """Evidence ratios normalised over the scale grid (summary.py:113-122)."""
+    log_z = np.array([s.log_z_ratio_cum for s in output.steps])
+    mass = np.exp(log_z - log_z.max())
+    mass /= mass.sum()
+    return CPosterior(output.c_values[: len(output.steps)], mass)

@@ -215,10 +215,45 @@ def gen_paths(name, a, b1, rho, T, N, cycles, seeds, fname):
     print(fname, "mean wall per path", float(out["wall"].mean()))
 
 
+def gen_summaries():
+    """Per-coordinate weighted mean / quantiles / concentration with the
+    reference's summary.py (36-61) on float32-representable particles (the
+    device keeps float32 particles): ties, zero weights, ragged N."""
+    from spa import summary as rsum
+
+    rng = np.random.default_rng(2024)
+    levels = np.array([0.05, 0.25, 0.5, 0.95])
+    deltas = np.array([0.05, 0.1])
+    cases = {
+        "normal": (rng.normal(0.0, 0.3, size=(1000, 13)), rng.dirichlet(np.ones(1000) * 0.7)),
+        "ties": (np.round(rng.normal(0.0, 0.3, size=(600, 7)), 1), rng.dirichlet(np.ones(600) * 0.3)),
+        "ragged": (rng.standard_t(3.0, size=(4097, 3)) * 0.1, rng.dirichlet(np.ones(4097))),
+        "equal": (rng.normal(0.0, 0.05, size=(512, 5)), np.full(512, 1.0 / 512)),
+    }
+    out = {"levels": levels, "deltas": deltas}
+    for name, (B, w) in cases.items():
+        B = B.astype(np.float32).astype(np.float64)
+        if name == "ties":
+            w[::7] = 0.0
+            w /= w.sum()
+        out[f"{name}_B"], out[f"{name}_w"] = B, w
+        out[f"{name}_mean"] = np.array([rsum.weighted_mean(B[:, j], w) for j in range(B.shape[1])])
+        out[f"{name}_quant"] = np.array([[rsum.weighted_quantile(B[:, j], w, q) for j in range(B.shape[1])]
+                                         for q in levels])
+        out[f"{name}_conc"] = np.array([[rsum.concentration(B[:, j], w, d) for j in range(B.shape[1])]
+                                        for d in deltas])
+    np.savez_compressed(os.path.join(HERE, "summaries.npz"), **out)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-paths", action="store_true")
+    ap.add_argument("--only", default=None, help="generate one fixture group (e.g. summaries)")
     args = ap.parse_args()
+    if args.only:
+        globals()[f"gen_{args.only}"]()
+        sys.exit(0)
+    gen_summaries()
     gen_philox()
     gen_data_hashes()
     gen_loglik_prior()

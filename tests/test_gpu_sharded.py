@@ -35,7 +35,8 @@ def _cfg(kernel):
     # init_chains pinned (the automatic count scales with the number of GPUs);
     # 293 chains x 28 slots: a chain's slot block straddles the shard boundary
     return SmcConfig(N=8192, cycles=2, moves=3, seed=5, init_burn=30, init_thin=1, move_kernel=kernel,
-                     ess_threshold_frac=0.9, init_chains=300)
+                     ess_threshold_frac=0.9, init_chains=300, summary_levels=(0.05, 0.5, 0.95),
+                     summary_deltas=(0.05,))
 
 
 def _run(group, kernel):
@@ -60,6 +61,8 @@ def _worker(rank, world, port, kernel, out):
             out["logz"] = [s.log_z_ratio_cum for s in res.steps]
             out["resampled"] = [s.resampled for s in res.steps]
             out["acc"] = [s.acceptance for s in res.steps]
+            out["summary"] = [(s.summary["mean"], s.summary["quantiles"], s.summary["concentration"])
+                              for s in res.steps]
     finally:
         dist.destroy_process_group()
 
@@ -75,3 +78,8 @@ def test_two_ranks_reproduce_single_process(kernel):
     np.testing.assert_array_equal(out["weights"], single.steps[-1].weights)
     assert out["logz"] == [s.log_z_ratio_cum for s in single.steps]
     assert out["acc"] == [s.acceptance for s in single.steps]
+    # device marginal summaries: exact integer sums all-reduced across shards
+    for (m2, q2, c2), s in zip(out["summary"], single.steps):
+        np.testing.assert_array_equal(m2, s.summary["mean"])
+        np.testing.assert_array_equal(q2, s.summary["quantiles"])
+        np.testing.assert_array_equal(c2, s.summary["concentration"])

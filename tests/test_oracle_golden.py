@@ -112,3 +112,17 @@ class TestDataGenerator:
         d, _ = simulate_dataset(named_spec(name))
         assert sha(d.X) == str(hashes[f"{name}_X"])
         assert sha(d.y) == str(hashes[f"{name}_y"])
+
+
+class TestSummaries:
+    @pytest.mark.parametrize("name", ["normal", "ties", "ragged", "equal"])
+    def test_marginal_summaries_match_reference(self, name):
+        """summary.py:36-61 weighted mean / quantile / concentration."""
+        g = golden("summaries.npz")
+        B, w = g[f"{name}_B"], g[f"{name}_w"]
+        q = B.shape[1]
+        assert np.array_equal([orc.weighted_mean(B[:, j], w) for j in range(q)], g[f"{name}_mean"])
+        assert np.array_equal([[orc.weighted_quantile(B[:, j], w, lv) for j in range(q)] for lv in g["levels"]],
+                              g[f"{name}_quant"])
+        assert np.array_equal([[orc.concentration(B[:, j], w, d) for j in range(q)] for d in g["deltas"]],
+                              g[f"{name}_conc"])

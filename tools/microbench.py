@@ -61,5 +61,6 @@ lw_t, lp_t = torch.empty_like(s.ll), torch.empty_like(s.ll)
 timeit("prior_reweight (fused)", lambda: _lib.call("spa_prior_reweight", ctypes.byref(d.struct), _p(s.beta), s.N, s.ldb,
                                                     1.0, float(prior.c), float(sched.bs[2]), _p(lw_t), _p(lp_t),
                                                     _stream()))
+timeit("marginal summaries (3 q, 2 d)", lambda: S.marginal_summaries(s, (0.05, 0.5, 0.95), (0.05, 0.1)))
 timeit("K1 loglik", lambda: _lib.call("spa_loglik_softplus", ctypes.byref(d.struct), _p(ws["A"]), s.N, _p(ws["sp"]),
                                       _p(ws["ws"]), ws["ws"].numel(), _stream()))
