@@ -232,6 +232,15 @@ int spa_summary_finish(int32_t q, int32_t nlev, int32_t ndelta, const uint32_t* 
                        const unsigned long long* total, double* out_mean, double* out_quant, double* out_conc,
                        void* stream);
 
+/* ---- f2: run-directory writer fast path (host, smc.py:532-549) -----------
+ * Rows "i,weight,p_0,...,p_{q-1}\n" for i = index0 .. index0+n-1 with every
+ * value as f"{v:.17g}" (byte-identical to the reference writer), formatted
+ * on `threads` host threads into buf (cap bytes; *used = bytes written, or
+ * needed when the status is the workspace-too-small code).  particles is
+ * float64 [n][q] row-major.  Needs no GPU. */
+int spa_format_particle_rows(const double* weights, const double* particles, int64_t n, int32_t q, int64_t index0,
+                             char* buf, size_t cap, size_t* used, int32_t threads);
+
 /* Load every kernel of the library on the current device now (instead of
  * lazily at first launch) -- run_sampler calls it during initialisation. */
 int spa_prepare(void);

@@ -65,6 +65,8 @@ _SIGNATURES = {
                                    c_void_p, c_void_p]),
     "spa_summary_finish": (c_int, [c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                    c_void_p, c_void_p, c_void_p]),
+    "spa_format_particle_rows": (c_int, [c_void_p, c_void_p, c_int64, c_int32, c_int64, c_void_p, c_size_t,
+                                         POINTER(c_size_t), c_int32]),
     "spa_prepare": (c_int, []),
     "spa_step_record": (c_int, [c_void_p, c_void_p, c_int64, c_double, c_void_p]),
     "spa_resample_gated": (c_int, [c_void_p, c_void_p, c_int64, c_double, c_void_p, c_void_p, c_int32, c_int32,

@@ -11,6 +11,8 @@
 #include <cmath>
 #include <mutex>
 #include <vector>
+#include <thread>
+#include <cstring>
 #include <string>
 
 #include "../../include/spa_b200.h"
@@ -2078,6 +2080,52 @@ int spa_prepare(void) {
     SPA_CHECK_CUDA(cudaFuncGetAttributes(&a, f));
   }
   return spa_mwg_prepare_kernels();
+}
+
+// ---------------------------------------------------------------------------
+// f2: run-directory writer fast path (host code).  Formats particle-file rows
+// "i,weight,p_0,...,p_{q-1}\n" exactly as smc.py:532-549 (f"{v:.17g}": glibc's
+// correctly rounded %.17g is byte-identical to Python's format for every
+// double), with the rows split over host threads.
+int spa_format_particle_rows(const double* weights, const double* particles, int64_t n, int32_t q, int64_t index0,
+                             char* buf, size_t cap, size_t* used, int32_t threads) {
+  SPA_REQUIRE(weights && particles && buf && used && n >= 0 && q >= 0, kBadArgument,
+              "spa_format_particle_rows: bad arguments");
+  const int nt = std::max<int>(1, std::min<int64_t>(threads > 0 ? threads : 1, std::max<int64_t>(1, n / 256)));
+  std::vector<std::string> parts((size_t)nt);
+  auto work = [&](int k) {
+    const int64_t r0 = n * k / nt, r1 = n * (k + 1) / nt;
+    std::string& out = parts[(size_t)k];
+    out.reserve((size_t)(r1 - r0) * (size_t)(q + 2) * 24);
+    char tmp[40];
+    for (int64_t i = r0; i < r1; ++i) {
+      int len = snprintf(tmp, sizeof(tmp), "%lld,", (long long)(index0 + i));
+      out.append(tmp, (size_t)len);
+      len = snprintf(tmp, sizeof(tmp), "%.17g", weights[i]);
+      out.append(tmp, (size_t)len);
+      const double* row = particles + (size_t)i * (size_t)q;
+      for (int32_t j = 0; j < q; ++j) {
+        tmp[0] = ',';
+        len = snprintf(tmp + 1, sizeof(tmp) - 1, "%.17g", row[j]);
+        out.append(tmp, (size_t)len + 1);
+      }
+      out.push_back('\n');
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int k = 1; k < nt; ++k) pool.emplace_back(work, k);
+  work(0);
+  for (auto& th : pool) th.join();
+  size_t total = 0;
+  for (const auto& p : parts) total += p.size();
+  *used = total;
+  SPA_REQUIRE(total <= cap, kWorkspaceTooSmall, "spa_format_particle_rows: buffer too small");
+  size_t off = 0;
+  for (const auto& p : parts) {
+    memcpy(buf + off, p.data(), p.size());
+    off += p.size();
+  }
+  return 0;
 }
 
 int spa_tc_gemm_f32(const void* A, int64_t m, int32_t terms_a, const void* B, int32_t rows_b, int32_t kp, float* C,

@@ -974,10 +974,29 @@ def save_run(output: SmcOutput, outdir, extra: dict | None = None) -> None:
     for s in output.steps:
         if s.particles is None:
             continue
-        with open(os.path.join(outdir, f"particles_t{s.t:04d}.csv"), "w") as fh:
-            fh.write("particle_index,weight," + ",".join(output.names) + "\n")
-            for i in range(s.particles.shape[0]):
-                fh.write(f"{i},{_fmt(s.weights[i])}," + ",".join(_fmt(v) for v in s.particles[i]) + "\n")
+        write_particles_csv(os.path.join(outdir, f"particles_t{s.t:04d}.csv"), output.names, s.weights, s.particles)
+
+
+def write_particles_csv(path, names, weights, particles, threads: int = 0, chunk: int = 16384) -> None:
+    """particles_tNNNN.csv of the reference run directory (smc.py:543-549),
+    byte-identical (every value as f"{v:.17g}"), formatted by
+    spa_format_particle_rows on host threads (the reference writer formats
+    ~1.5 M values/s in one Python loop)."""
+    P = np.ascontiguousarray(particles, dtype=np.float64)
+    W = np.ascontiguousarray(weights, dtype=np.float64)
+    n, q = P.shape
+    threads = threads or (os.cpu_count() or 1)
+    cap = chunk * (25 * (q + 1) + 24) + 64
+    buf = ctypes.create_string_buffer(cap)
+    view = memoryview(buf)
+    used = ctypes.c_size_t(0)
+    with open(path, "wb") as fh:
+        fh.write(("particle_index,weight," + ",".join(names) + "\n").encode())
+        for r0 in range(0, n, chunk):
+            m = min(chunk, n - r0)
+            _lib.call("spa_format_particle_rows", ctypes.c_void_p(W.ctypes.data + 8 * r0),
+                      ctypes.c_void_p(P.ctypes.data + 8 * r0 * q), m, q, r0, buf, cap, ctypes.byref(used), threads)
+            fh.write(view[:used.value])
 
 
 def load_run(outdir) -> SmcOutput:

@@ -152,3 +152,43 @@ def test_init_plan_covers_slots_once():
                 lo, hi = r * M, (r + 1) * M
                 c0, c1 = lo // R, min(K, -(-hi // R))
                 assert c0 * R <= lo and hi <= c1 * R
+
+
+def _py_rows(W, P, index0=0):
+    """The reference writer's row format (smc.py:546-549)."""
+    return "".join(f"{index0 + i},{W[i]:.17g}," + ",".join(f"{v:.17g}" for v in P[i]) + "\n"
+                   for i in range(P.shape[0]))
+
+
+def test_format_particle_rows_matches_python():
+    """f2 fast writer: byte-identical to f"{v:.17g}" rows, edge values included."""
+    import ctypes
+
+    from paper_1106_0322_b200 import _lib
+
+    rng = np.random.default_rng(9)
+    P = rng.normal(0, 0.3, size=(1500, 7)).astype(np.float32).astype(np.float64)
+    edge = [0.0, -0.0, 1e-300, -1e300, 5e-324, 2.2250738585072014e-308, 1 / 3, 0.1, 123456789.0, 1e16, 1e17,
+            -1e-5, 1e-4, 9.999999999999999e22, float("inf"), float("-inf"), float("nan")]
+    P[:3, :] = np.resize(np.array(edge), (3, 7))
+    W = rng.dirichlet(np.ones(P.shape[0]))
+    W[5] = 0.0
+    cap = 4 << 20
+    buf = ctypes.create_string_buffer(cap)
+    used = ctypes.c_size_t(0)
+    for threads in (1, 8):
+        _lib.call("spa_format_particle_rows", W.ctypes.data, P.ctypes.data, P.shape[0], P.shape[1], 10, buf, cap,
+                  ctypes.byref(used), threads)
+        assert buf.raw[:used.value].decode() == _py_rows(W, P, 10)
+
+
+def test_save_run_particles_byte_identical(tmp_path):
+    from paper_1106_0322_b200.smc import write_particles_csv
+
+    rng = np.random.default_rng(3)
+    P = rng.standard_t(2.0, size=(40000, 5)) * 0.1
+    W = rng.dirichlet(np.ones(P.shape[0]) * 0.5)
+    names = [f"snp{j}" for j in range(5)]
+    write_particles_csv(tmp_path / "p.csv", names, W, P, chunk=7000)
+    expect = "particle_index,weight," + ",".join(names) + "\n" + _py_rows(W, P)
+    assert (tmp_path / "p.csv").read_text() == expect
