@@ -241,6 +241,18 @@ int spa_summary_finish(int32_t q, int32_t nlev, int32_t ndelta, const uint32_t* 
 int spa_format_particle_rows(const double* weights, const double* particles, int64_t n, int32_t q, int64_t index0,
                              char* buf, size_t cap, size_t* used, int32_t threads);
 
+/* ---- f3: batched EM MAP (emmap.py:117-165; summary.py:173-211) ----------
+ * `problems` independent local-mode searches, problem k from seeds[k][q]
+ * (float64) under GtPrior(a[k], c[k]): EM with adaptive L1 weights
+ * (emmap.py:48-56) around weighted-L1 logistic solves by cyclic coordinate
+ * descent with curvature curv[j] = 0.25 sum_i x_ij^2 (emmap.py:69-108), all
+ * float64.  Outputs beta_out[k][q], the final log posterior, info[k] (bit 0
+ * EM converged, bit 1 every inner solve converged) and the EM iteration
+ * count.  Genotype-coded designs only. */
+int spa_em_map(const spa_design* d, int32_t problems, const double* seeds, const double* a, const double* c,
+               const double* curv, double tol, int32_t max_iter, double inner_tol, int32_t inner_max_sweeps,
+               double* beta_out, double* log_post, int32_t* info, int32_t* iters, void* stream);
+
 /* Load every kernel of the library on the current device now (instead of
  * lazily at first launch) -- run_sampler calls it during initialisation. */
 int spa_prepare(void);

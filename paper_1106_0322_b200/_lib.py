@@ -67,6 +67,8 @@ _SIGNATURES = {
                                    c_void_p, c_void_p, c_void_p]),
     "spa_format_particle_rows": (c_int, [c_void_p, c_void_p, c_int64, c_int32, c_int64, c_void_p, c_size_t,
                                          POINTER(c_size_t), c_int32]),
+    "spa_em_map": (c_int, [POINTER(SpaDesign), c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int32,
+                           c_double, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "spa_prepare": (c_int, []),
     "spa_step_record": (c_int, [c_void_p, c_void_p, c_int64, c_double, c_void_p]),
     "spa_resample_gated": (c_int, [c_void_p, c_void_p, c_int64, c_double, c_void_p, c_void_p, c_int32, c_int32,
@@ -127,7 +129,7 @@ KERNELS_PER_CALL = {
     "spa_prior_rows": 1, "spa_prior_reweight": 1, "spa_lse_chunk_stats": 1, "spa_lse_combine": 1, "spa_logw_apply": 1,
     "spa_systematic_ancestors": 2, "spa_gather_rows": 1, "spa_mwg_move": 1, "spa_rw_moments": 1,
     "spa_rw_factor": 0, "spa_mwg_resident_chains": 0, "spa_step_record": 1, "spa_resample_gated": 4, "spa_summary_pass": 1, "spa_summary_select": 1,
-    "spa_summary_finish": 1, "spa_rw_propose": 2, "spa_rw_normals": 1, "spa_rw_accept": 1, "spa_tc_gemm_f32": 1,
+    "spa_summary_finish": 1, "spa_em_map": 1, "spa_rw_propose": 2, "spa_rw_normals": 1, "spa_rw_accept": 1, "spa_tc_gemm_f32": 1,
 }
 launch_count = 0
 

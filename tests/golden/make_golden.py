@@ -245,6 +245,31 @@ def gen_summaries():
     np.savez_compressed(os.path.join(HERE, "summaries.npz"), **out)
 
 
+def gen_emmap():
+    """Reference em_map (emmap.py:117-165) on the C1 and C2 shapes from zero
+    and from perturbed seeds, several priors (with and without intercept)."""
+    from spa import emmap as rem
+
+    rng = np.random.default_rng(77)
+    out = {}
+    cases = [("c1", 1.0, 0.5, False), ("c1", 4.0, 0.05, True), ("c2", 1.0, 0.5, False), ("c2", 0.5, 0.2, False)]
+    for k, (name, a, c, icpt) in enumerate(cases):
+        ds = rdata.simulate_dataset(ref_spec(name))[0]
+        q = ds.X.shape[1] + (1 if icpt else 0)
+        seeds = [np.zeros(q), rng.normal(0, 0.2, size=q)]
+        for s, seed in enumerate(seeds):
+            r = rem.em_map(ds, rmodel.GtPrior(a, c), beta_init=seed, intercept=icpt)
+            key = f"{k}_{s}"
+            out[f"case_{key}"] = np.array([a, c, float(icpt)])
+            out[f"name_{key}"] = np.array(name)
+            out[f"seed_{key}"] = seed
+            out[f"beta_{key}"] = r.beta
+            out[f"lp_{key}"] = np.array(r.trace[-1].log_post)
+            out[f"conv_{key}"] = np.array([r.converged, r.inner_converged])
+            out[f"iters_{key}"] = np.array(len(r.trace) - 1)
+    np.savez_compressed(os.path.join(HERE, "emmap.npz"), **out)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-paths", action="store_true")
@@ -254,6 +279,7 @@ if __name__ == "__main__":
         globals()[f"gen_{args.only}"]()
         sys.exit(0)
     gen_summaries()
+    gen_emmap()
     gen_philox()
     gen_data_hashes()
     gen_loglik_prior()

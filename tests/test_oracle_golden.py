@@ -126,3 +126,22 @@ class TestSummaries:
                               g[f"{name}_quant"])
         assert np.array_equal([[orc.concentration(B[:, j], w, d) for j in range(q)] for d in g["deltas"]],
                               g[f"{name}_conc"])
+
+
+class TestEmMap:
+    @pytest.mark.parametrize("key", ["0_0", "0_1", "1_0", "1_1"])
+    def test_em_map_matches_reference(self, key):
+        """emmap.py:117-165 on C1 (C2 cases run in the GPU tests: slow in NumPy)."""
+        from paper_1106_0322_b200.data import named_spec, simulate_dataset
+
+        g = golden("emmap.npz")
+        a, c, icpt = (float(v) for v in g[f"case_{key}"])
+        d, _ = simulate_dataset(named_spec(str(g[f"name_{key}"])))
+        X = np.column_stack([np.ones(d.X.shape[0]), d.X]) if icpt else d.X
+        pen = np.ones(X.shape[1], bool)
+        if icpt:
+            pen[0] = False
+        beta, lp, conv, inner, iters = orc.em_map(X, d.y, a, c, g[f"seed_{key}"], pen)
+        np.testing.assert_allclose(beta, g[f"beta_{key}"], rtol=0, atol=1e-12)
+        assert abs(lp - float(g[f"lp_{key}"])) < 1e-9
+        assert [conv, inner] == list(g[f"conv_{key}"]) and iters == int(g[f"iters_{key}"])
