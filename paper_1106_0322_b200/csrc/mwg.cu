@@ -93,13 +93,15 @@ __device__ double materialise_ll(const MwgParams& P, const float* bsh, int tid, 
 #pragma unroll
   for (int s = 0; s < S; ++s) eta[s] = 0.0f;
   const int sub0 = tid * S;
+  uint32_t nb1 = 0, nb2 = 0;
+  if (P.d.coded) load_bits<S>(P.d, 0, tid, nb1, nb2);
   for (int j = 0; j < q; ++j) {
     const float bj = bsh[j];
     if (P.d.coded) {
       const float4 lv = reinterpret_cast<const float4*>(P.d.xlev)[j];
       const float v0 = lv.x * bj, v1 = lv.y * bj, v2 = lv.z * bj;
-      uint32_t p1, p2;
-      load_bits<S>(P.d, j, tid, p1, p2);
+      const uint32_t p1 = nb1, p2 = nb2;
+      if (j + 1 < q) load_bits<S>(P.d, j + 1, tid, nb1, nb2);
 #pragma unroll
       for (int s = 0; s < S; ++s) eta[s] += ((p2 >> s) & 1) ? v2 : (((p1 >> s) & 1) ? v1 : v0);
     } else {
@@ -202,13 +204,17 @@ __global__ void __launch_bounds__(512) mwg_kernel(MwgParams P) {
     }
     __syncthreads();
 
+    // genotype bits of coordinate j + 1 are loaded while j is processed
+    // (the load latency was the largest stall); same for the materialisation
+    uint32_t nb1 = 0, nb2 = 0;
+    if (P.d.coded) load_bits<S>(P.d, 0, tid, nb1, nb2);
     for (int j = 0; j < q; ++j) {
       const CoordSlot cs = slot[j];
       float part = 0.0f;
       float mloc[S];
       if (P.d.coded) {
-        uint32_t p1, p2;
-        load_bits<S>(P.d, j, tid, p1, p2);
+        const uint32_t p1 = nb1, p2 = nb2;
+        if (j + 1 < q) load_bits<S>(P.d, j + 1, tid, nb1, nb2);
 #pragma unroll
         for (int s = 0; s < S; ++s) mloc[s] = sel_m(p1 >> s, p2 >> s, cs);
       } else {
