@@ -171,6 +171,9 @@ int spa_mwg_move(const spa_design* d, float* beta, int64_t m, int32_t ldb, doubl
  *            as a split-K tcgen05 SYRK of the centred, sqrt(w)-weighted,
  *            transposed bf16 hi/lo particles; per-split float32 tiles are
  *            summed in fixed order (ws: spa_rw_moments_workspace_bytes).
+ *   phase 2: only the centring/transposition of phase 1 (the last read of
+ *            beta) into ws; phase 3: only its SYRK + reduce, from ws -- so
+ *            the particles may be modified once phase 2 has completed.
  * Integer sums are order-independent, so the moments are bit-identical for any
  * CTA schedule or particle sharding (multi-GPU: all-reduce `partial`). */
 size_t spa_rw_moments_workspace_bytes(int64_t m, int32_t q);

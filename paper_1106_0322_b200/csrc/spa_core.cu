@@ -1905,7 +1905,7 @@ __global__ void syrk_reduce_kernel(const float* __restrict__ part, int units, in
 
 int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const double* w, int32_t phase,
                    int64_t* partial, void* ws, size_t ws_bytes, void* stream) {
-  SPA_REQUIRE(beta && w && partial && m > 0 && q > 0 && (phase == 0 || phase == 1), kBadArgument,
+  SPA_REQUIRE(beta && w && partial && m > 0 && q > 0 && phase >= 0 && phase <= 3, kBadArgument,
               "spa_rw_moments: bad arguments");
   cudaStream_t st = as_stream(stream);
   auto* acc = reinterpret_cast<unsigned long long*>(partial);
@@ -1925,16 +1925,18 @@ int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const d
     SPA_CHECK_LAUNCH();
     return 0;
   }
-  // phase 1: S = Dt Dt^T on tcgen05 (3 split products), split-K over particles
+  // phase 1 = 2 then 3: centre/transpose (reads beta), then S = Dt Dt^T on
+  // tcgen05 (3 split products, split-K over particles) + fixed-order reduce
   SPA_REQUIRE(ws && ws_bytes >= spa_rw_moments_workspace_bytes(m, q), kWorkspaceTooSmall,
               "spa_rw_moments: workspace too small");
   const int64_t ldk = (m + 63) / 64 * 64;
   __nv_bfloat16* Dt = reinterpret_cast<__nv_bfloat16*>(ws);
   // layout [q][2*ldk]: row i = [hi(i, :) | lo(i, :)]
-  {
+  if (phase != 3) {
     dim3 grid(cdiv(ldk, 64), cdiv(q, 32));
     rw_center_t_kernel<<<grid, 256, 0, st>>>(beta, m, ldb, q, w, acc, Dt, ldk);
     SPA_CHECK_LAUNCH();
+    if (phase == 2) return 0;
   }
   TcArgs args;
   int units;

@@ -18,6 +18,10 @@ Extra SmcConfig fields (defaults keep the reference's behaviour):
     summary_levels / summary_deltas
                  per-step weighted marginal summaries computed on the device
                  (StepRecord.summary; see marginal_summaries)
+    rw_factor_lag
+                 RW: the first move of a step proposes with the previous step's
+                 covariance factor, so the new factor (SYRK + Cholesky) is
+                 computed on a side stream beside that move
 """
 
 from __future__ import annotations
@@ -99,6 +103,7 @@ class SmcConfig:
     init_chains: int = 0
     summary_levels: tuple = ()
     summary_deltas: tuple = ()
+    rw_factor_lag: bool = True
 
     def __post_init__(self):
         if self.N < 2:
@@ -284,6 +289,8 @@ class ParticleSystem:
                 L=torch.empty((q, q), dtype=torch.float32, device=dev),
                 fws=torch.empty((_round_up(8 * q * q, 256) + _round_up(2 * q * kq, 256) + 8192) // 8,
                                 dtype=torch.float64, device=dev),
+                fws2=torch.empty((_round_up(8 * q * q, 256) + _round_up(2 * q * kq, 256) + 8192) // 8,
+                                 dtype=torch.float64, device=dev),
                 info=torch.zeros(1, dtype=torch.int32, device=dev),
                 mws=torch.empty(max(_lib.load().spa_rw_moments_workspace_bytes(self.N, q), 8), dtype=torch.uint8,
                                 device=dev),
@@ -302,9 +309,16 @@ class ParticleSystem:
             self._zs = zs = [torch.empty((self.N, kq), dtype=torch.bfloat16, device=self.device) for _ in range(moves)]
         return zs
 
-    def factor_operand(self):
+    def factor_operand(self, buf: int | None = None):
+        """bf16 operand of factor buffer `buf` (default: the current one)."""
         rw = self.rw_workspace()
-        return ctypes.c_void_p(rw["fws"].data_ptr() + _round_up(8 * self.q * self.q, 256))
+        buf = getattr(self, "_fcur", 0) if buf is None else buf
+        return ctypes.c_void_p(rw["fws" if buf == 0 else "fws2"].data_ptr() + _round_up(8 * self.q * self.q, 256))
+
+    def factor_stream(self):
+        if getattr(self, "_fstream", None) is None:
+            self._fstream = torch.cuda.Stream(self.device)
+        return self._fstream
 
 
 def _lse(system: ParticleSystem, lw):
@@ -437,7 +451,11 @@ def _loglik_device(system: ParticleSystem, out: torch.Tensor):
               _p(ws["ylin"]), _p(out), _p(ws["ws"]), ws["ws"].numel(), _stream())
 
 
-def _rw_factor(system: ParticleSystem, scale: float, group=None):
+def _rw_factor(system: ParticleSystem, scale: float, group=None, buf: int = 0, centred=None):
+    """Population covariance (fixed-point moments, tcgen05 SYRK) and its
+    Cholesky factor into factor buffer `buf`, on the current stream.
+    `centred` (optional event) is recorded once the particles have been read
+    for the last time (after the centring pass)."""
     rw = system.rw_workspace()
     w = system.device_weights() if group is None else _global_weights(system, group)
     rw["acc"].zero_()
@@ -445,13 +463,17 @@ def _rw_factor(system: ParticleSystem, scale: float, group=None):
               _stream())
     if group is not None:
         group.all_reduce_sum(rw["acc"][: system.q])
-    _lib.call("spa_rw_moments", _p(system.beta), system.N, system.ldb, system.q, _p(w), 1, _p(rw["acc"]),
+    _lib.call("spa_rw_moments", _p(system.beta), system.N, system.ldb, system.q, _p(w), 2, _p(rw["acc"]),
               _p(rw["mws"]), rw["mws"].numel(), _stream())
-    _lib.add_launches(2)  # phase 1 = transpose + tcgen05 SYRK + split reduce
+    if centred is not None:
+        centred.record()
+    _lib.call("spa_rw_moments", _p(system.beta), system.N, system.ldb, system.q, _p(w), 3, _p(rw["acc"]),
+              _p(rw["mws"]), rw["mws"].numel(), _stream())
+    _lib.add_launches(1)  # phase 3 = tcgen05 SYRK + split reduce
     if group is not None:
         group.all_reduce_sum(rw["acc"][system.q:])
-    _lib.call("spa_rw_factor", _p(rw["acc"]), system.q, float(scale), 1e-6, _p(rw["L"]), _p(rw["fws"]),
-              _p(rw["info"]), _stream())
+    _lib.call("spa_rw_factor", _p(rw["acc"]), system.q, float(scale), 1e-6, _p(rw["L"]),
+              _p(rw["fws" if buf == 0 else "fws2"]), _p(rw["info"]), _stream())
     panels = -(-system.q // 32)
     _lib.add_launches(2 + 2 * panels - 1)  # cov + graph of panel kernels + emit
 
@@ -491,12 +513,33 @@ def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int,
     if z_ready is None:
         z_ready = _rw_normals_async(system, config, t)
     zs = system.z_buffers(config.moves)
-    _rw_factor(system, config.rw_scale, group)
-    torch.cuda.current_stream().wait_event(z_ready)
+    main = torch.cuda.current_stream()
+    cur = getattr(system, "_fcur", 0)
+    lag = config.rw_factor_lag and getattr(system, "_factor_ready", False) and config.moves > 1
+    centred = factored = None
+    if lag:
+        # the new factor is built on a side stream while move 0 proposes with
+        # the previous one; only move 0's accept (which writes beta) waits for
+        # the centring pass, and move 1 for the factor
+        nxt = 1 - cur
+        fs = system.factor_stream()
+        centred, factored = torch.cuda.Event(), torch.cuda.Event()
+        fs.wait_stream(main)
+        with torch.cuda.stream(fs):
+            _rw_factor(system, config.rw_scale, group, buf=nxt, centred=centred)
+            factored.record()
+    else:
+        _rw_factor(system, config.rw_scale, group, buf=cur)
+        nxt = cur
+        system._factor_ready = True
+    main.wait_event(z_ready)
     # system.lp already holds the log-prior at the new scale (fused reweight pass)
     system.counter.zero_()
-    Lb = system.factor_operand()
+    Lb = system.factor_operand(cur)
     for mv in range(config.moves):
+        if lag and mv == 1:
+            main.wait_event(factored)
+            Lb = system.factor_operand(nxt)
         _lib.call("spa_rw_propose", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb, Lb,
                   int(config.seed), int(t), int(system.i0), mv, _p(zs[mv]), _p(rw["prop"]), _p(ws["A"]),
                   _p(ws["ylin"]), float(prior.a), float(prior.c), _p(rw["lp_p"]), _stream())
@@ -506,9 +549,12 @@ def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int,
                   ws["ws"].numel(), _stream())
         if KERNEL_TIMER is not None:
             KERNEL_TIMER.stop("loglik")
+        if lag and mv == 0:
+            main.wait_event(centred)  # the factor stream has read the particles
         _lib.call("spa_rw_accept", _p(system.beta), system.ldb, _p(rw["prop"]), system.q, system.N, _p(ws["ylin"]),
                   _p(ws["sp"]), _p(rw["lp_p"]), _p(system.ll), _p(system.lp), int(config.seed), int(t),
                   int(system.i0), mv, _p(system.counter), _stream())
+    system._fcur = nxt
     acc = system.counter.clone() if group is None else group.all_reduce_sum(system.counter.clone())
     return acc  # device tensor: read lazily (no host sync inside the step)
 
@@ -528,8 +574,9 @@ def _prepare_for_path(system: ParticleSystem, config: SmcConfig) -> None:
         rw = system.rw_workspace()
         system.z_buffers(config.moves)
         system.side_stream()
-        _lib.call("spa_rw_factor", _p(rw["acc"]), system.q, float(config.rw_scale), 1e-6, _p(rw["L"]),
-                  _p(rw["fws"]), _p(rw["info"]), _stream())
+        for buf in ("fws", "fws2"):  # both factor buffers (the lagged factor alternates them)
+            _lib.call("spa_rw_factor", _p(rw["acc"]), system.q, float(config.rw_scale), 1e-6, _p(rw["L"]),
+                      _p(rw[buf]), _p(rw["info"]), _stream())
 
 
 def resident_chains(design: DeviceDesign) -> int:
