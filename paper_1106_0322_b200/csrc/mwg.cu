@@ -66,11 +66,17 @@ struct CoordSlot {
   float m0, m1, m2;  // expm1(delta * x) for codes 0, 1, 2
 };
 
-// Genotype code from the two bit planes: (0,0)->0, (1,0)->1, (0,1)->2, and
-// (1,1) marks a padding subject whose factor m must be exactly 0.
+// Genotype code from the two bit planes: (0,0)->0, (1,0)->1, (0,1)->2.  A
+// padding subject (1,1) gets m2: harmless, because its sigma is exactly 0 and
+// the m are kept finite (so 1 + m sigma = 1 and sigma stays 0 on acceptance).
+// Two predicate tests and two selects per subject.
 __device__ __forceinline__ float sel_m(uint32_t b1, uint32_t b2, const CoordSlot& cs) {
-  return (b2 & 1) ? ((b1 & 1) ? 0.0f : cs.m2) : ((b1 & 1) ? cs.m1 : cs.m0);
+  const float a = (b1 & 1) ? cs.m1 : cs.m0;
+  return (b2 & 1) ? cs.m2 : a;
 }
+
+// expm1 kept finite (|delta x| > 88 would need a ~40-sigma proposal)
+__device__ __forceinline__ float finite_expm1(float v) { return fminf(expm1f(v), 3.0e38f); }
 
 template <int S>
 __device__ __forceinline__ void load_bits(const spa_design& d, int j, int tid, uint32_t& p1, uint32_t& p2) {
@@ -85,7 +91,7 @@ __device__ __forceinline__ void load_bits(const spa_design& d, int j, int tid, u
 // eta_i = sum_j x_ij beta_j for this thread's S subjects (float32), then
 // l = sum_j beta_j (X^T y)_j - sum_i softplus(eta_i) (block-reduced, float64,
 // identical in every thread); optionally returns sigma_i = logistic(eta_i).
-template <int S>
+template <int S, bool CODED>
 __device__ double materialise_ll(const MwgParams& P, const float* bsh, int tid, int nthr, int lane, int wid, int nw,
                                  double* red, float* sig_out) {
   const int q = P.d.q;
@@ -94,10 +100,10 @@ __device__ double materialise_ll(const MwgParams& P, const float* bsh, int tid, 
   for (int s = 0; s < S; ++s) eta[s] = 0.0f;
   const int sub0 = tid * S;
   uint32_t nb1 = 0, nb2 = 0;
-  if (P.d.coded) load_bits<S>(P.d, 0, tid, nb1, nb2);
+  if (CODED) load_bits<S>(P.d, 0, tid, nb1, nb2);
   for (int j = 0; j < q; ++j) {
     const float bj = bsh[j];
-    if (P.d.coded) {
+    if (CODED) {
       const float4 lv = reinterpret_cast<const float4*>(P.d.xlev)[j];
       const float v0 = lv.x * bj, v1 = lv.y * bj, v2 = lv.z * bj;
       const uint32_t p1 = nb1, p2 = nb2;
@@ -139,7 +145,50 @@ __device__ double materialise_ll(const MwgParams& P, const float* bsh, int tid, 
   return ylt - sp;
 }
 
-template <int S>
+// sum_s log2(1 + m_s sigma_s) for one coordinate over this thread's S
+// subjects, as log2 of 8-term products (two independent 4-term chains): one
+// MUFU per 8 subjects and fewer rounding errors; a product outside
+// [1e-30, 1e30] (extreme proposals only) falls back to per-term logs.
+template <int S, bool CODED>
+__device__ __forceinline__ float coord_log2_sum(const float (&sig)[S], uint32_t p1, uint32_t p2, const CoordSlot& cs,
+                                                const float* xc, float df) {
+  float part = 0.0f;
+#pragma unroll
+  for (int c8 = 0; c8 < S / 8; ++c8) {
+    float fac[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int s = 8 * c8 + k;
+      const float mm = CODED ? sel_m(p1 >> s, p2 >> s, cs) : expm1f(df * xc[s]);
+      fac[k] = fmaf(mm, sig[s], 1.0f);
+    }
+    const float prod = ((fac[0] * fac[1]) * (fac[2] * fac[3])) * ((fac[4] * fac[5]) * (fac[6] * fac[7]));
+    if (prod >= 1e-30f && prod <= 1e30f) {
+      part += fast_lg2(prod);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) part += fast_lg2(fmaxf(fac[k], 1e-37f));
+    }
+  }
+  return part;
+}
+
+// sigma_s <- sigma_s (1 + m_s) / (1 + m_s sigma_s) after an accepted move
+template <int S, bool CODED>
+__device__ __forceinline__ void coord_accept(float (&sig)[S], uint32_t p1, uint32_t p2, const CoordSlot& cs,
+                                             const float* xc, float df) {
+  // opaque copies: otherwise the compiler keeps the 2 S code predicates of
+  // coord_log2_sum alive (in predicate and general registers) for this path
+  asm volatile("mov.b32 %0, %0;" : "+r"(p1));
+  asm volatile("mov.b32 %0, %0;" : "+r"(p2));
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const float mm = CODED ? sel_m(p1 >> s, p2 >> s, cs) : expm1f(df * xc[s]);
+    sig[s] = __fdividef(sig[s] * (1.0f + mm), fmaf(mm, sig[s], 1.0f));
+  }
+}
+
+template <int S, bool CODED>
 __global__ void __launch_bounds__(512) mwg_kernel(MwgParams P) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int q = P.d.q;
@@ -160,7 +209,7 @@ __global__ void __launch_bounds__(512) mwg_kernel(MwgParams P) {
   __syncthreads();
 
   float sig[S];
-  double ll = materialise_ll<S>(P, bsh, tid, nthr, lane, wid, nw, red, sig);
+  double ll = materialise_ll<S, CODED>(P, bsh, tid, nthr, lane, wid, nw, red, sig);
   double lp = 0.0;
   {
     double lp0 = 0.0;
@@ -191,12 +240,12 @@ __global__ void __launch_bounds__(512) mwg_kernel(MwgParams P) {
       cs.delta = (double)nv - (double)old;
       cs.logu = log(u);
       cs.dlp = P.d.penalized[j] ? (mwg_gt((double)nv, P) - mwg_gt((double)old, P)) : 0.0;
-      if (P.d.coded) {
+      if (CODED) {
         const float4 lv = reinterpret_cast<const float4*>(P.d.xlev)[j];
         const float df = (float)cs.delta;
-        cs.m0 = expm1f(df * lv.x);
-        cs.m1 = expm1f(df * lv.y);
-        cs.m2 = expm1f(df * lv.z);
+        cs.m0 = finite_expm1(df * lv.x);
+        cs.m1 = finite_expm1(df * lv.y);
+        cs.m2 = finite_expm1(df * lv.z);
       } else {
         cs.m0 = cs.m1 = cs.m2 = 0.0f;
       }
@@ -204,48 +253,33 @@ __global__ void __launch_bounds__(512) mwg_kernel(MwgParams P) {
     }
     __syncthreads();
 
-    // genotype bits of coordinate j + 1 are loaded while j is processed
-    // (the load latency was the largest stall); same for the materialisation
-    uint32_t nb1 = 0, nb2 = 0;
-    if (P.d.coded) load_bits<S>(P.d, 0, tid, nb1, nb2);
+    // genotype bits are prefetched two coordinates ahead (the L2 load latency
+    // was the largest stall); the per-subject factors m are re-selected from
+    // the bits on acceptance instead of being kept (32 registers fewer, so
+    // more chains are resident per SM)
+    uint32_t nb1 = 0, nb2 = 0, nn1 = 0, nn2 = 0;
+    if (CODED) {
+      load_bits<S>(P.d, 0, tid, nb1, nb2);
+      if (q > 1) load_bits<S>(P.d, 1, tid, nn1, nn2);
+    }
     for (int j = 0; j < q; ++j) {
       const CoordSlot cs = slot[j];
-      float part = 0.0f;
-      float mloc[S];
-      if (P.d.coded) {
-        const uint32_t p1 = nb1, p2 = nb2;
-        if (j + 1 < q) load_bits<S>(P.d, j + 1, tid, nb1, nb2);
-#pragma unroll
-        for (int s = 0; s < S; ++s) mloc[s] = sel_m(p1 >> s, p2 >> s, cs);
-      } else {
-        const float* xc = P.d.xcols + (size_t)j * P.d.n_words * 32 + sub0;
-        const float df = (float)cs.delta;
-#pragma unroll
-        for (int s = 0; s < S; ++s) mloc[s] = expm1f(df * xc[s]);
+      const uint32_t p1 = nb1, p2 = nb2;
+      if (CODED) {
+        nb1 = nn1;
+        nb2 = nn2;
+        if (j + 2 < q) load_bits<S>(P.d, j + 2, tid, nn1, nn2);
       }
-      // sum_s log2(1 + m_s sigma_s) as log2 of 8-term products: one MUFU per
-      // 8 subjects and fewer rounding errors; a product outside [1e-30, 1e30]
-      // (extreme proposals only) falls back to per-term logs.
-#pragma unroll
-      for (int c8 = 0; c8 < S / 8; ++c8) {
-        float prod = 1.0f;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) prod *= fmaf(mloc[8 * c8 + k], sig[8 * c8 + k], 1.0f);
-        if (prod >= 1e-30f && prod <= 1e30f) {
-          part += fast_lg2(prod);
-        } else {
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
-            part += fast_lg2(fmaxf(fmaf(mloc[8 * c8 + k], sig[8 * c8 + k], 1.0f), 1e-37f));
-        }
-      }
+      const float* xc = P.d.xcols + (size_t)j * P.d.n_words * 32 + sub0;
+      const float df = (float)cs.delta;
+      const float part = coord_log2_sum<S, CODED>(sig, p1, p2, cs, xc, df);
       // block sum (double-buffered scratch: one barrier per coordinate)
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
       float tot = part;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
       if (nw > 1) {
         float* buf = fred + (j & 1) * 32;
-        if (lane == 0) buf[wid] = part;
+        if (lane == 0) buf[wid] = tot;
         __syncthreads();
         tot = 0.0f;
         for (int w = 0; w < nw; ++w) tot += buf[w];
@@ -254,11 +288,7 @@ __global__ void __launch_bounds__(512) mwg_kernel(MwgParams P) {
       const double d = dll + cs.dlp;
       const bool ok = (d >= 0.0) || (cs.logu < d);
       if (ok) {
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-          const float mm = mloc[s];
-          sig[s] = __fdividef(sig[s] * (1.0f + mm), fmaf(mm, sig[s], 1.0f));
-        }
+        coord_accept<S, CODED>(sig, p1, p2, cs, xc, df);
         ll += dll;
         lp += cs.dlp;
         ++acc;
@@ -272,7 +302,7 @@ __global__ void __launch_bounds__(512) mwg_kernel(MwgParams P) {
   for (int j = tid; j < q; j += nthr) brow[j] = bsh[j];
   // rematerialise the final state's log-likelihood from beta (the running
   // sum of float32 increments only drives the accept decisions)
-  ll = materialise_ll<S>(P, bsh, tid, nthr, lane, wid, nw, red, nullptr);
+  ll = materialise_ll<S, CODED>(P, bsh, tid, nthr, lane, wid, nw, red, nullptr);
   if (tid == 0) {
     P.ll[row] = ll;
     if (P.lp) P.lp[row] = lp;
@@ -281,6 +311,15 @@ __global__ void __launch_bounds__(512) mwg_kernel(MwgParams P) {
     else
       atomicAdd(P.accepted, acc);
   }
+}
+
+template <int S>
+static const void* mwg_fn_s(bool coded) {
+  return coded ? (const void*)mwg_kernel<S, true> : (const void*)mwg_kernel<S, false>;
+}
+
+static const void* mwg_fn(int S, bool coded) {
+  return S == 8 ? mwg_fn_s<8>(coded) : S == 16 ? mwg_fn_s<16>(coded) : mwg_fn_s<32>(coded);
 }
 
 static int pick_s(int n) {
@@ -296,7 +335,9 @@ using namespace spa;
 
 // internal (called by spa_prepare): load the MwG kernels
 extern "C" int spa_mwg_prepare_kernels(void) {
-  const void* fns[] = {(const void*)mwg_kernel<8>, (const void*)mwg_kernel<16>, (const void*)mwg_kernel<32>};
+  const void* fns[] = {(const void*)mwg_kernel<8, true>,   (const void*)mwg_kernel<16, true>,
+                       (const void*)mwg_kernel<32, true>,  (const void*)mwg_kernel<8, false>,
+                       (const void*)mwg_kernel<16, false>, (const void*)mwg_kernel<32, false>};
   for (const void* f : fns) {
     cudaFuncAttributes a;
     SPA_CHECK_CUDA(cudaFuncGetAttributes(&a, f));
@@ -315,7 +356,7 @@ extern "C" int spa_mwg_resident_chains(const spa_design* d, int64_t* chains) {
   const size_t smem = (size_t)d->q * sizeof(CoordSlot) + (size_t)((d->q + 1) & ~1) * sizeof(float) +
                       64 * sizeof(double) + 64 * sizeof(float);
   int per_sm = 0, dev = 0, nsm = 0;
-  const void* fn = S == 8 ? (const void*)mwg_kernel<8> : S == 16 ? (const void*)mwg_kernel<16> : (const void*)mwg_kernel<32>;
+  const void* fn = mwg_fn(S, d->coded != 0);
   SPA_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   SPA_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nthr, smem));
   SPA_CHECK_CUDA(cudaGetDevice(&dev));
@@ -361,23 +402,11 @@ extern "C" int spa_mwg_move(const spa_design* d, float* beta, int64_t m, int32_t
   const size_t smem = (size_t)d->q * sizeof(CoordSlot) + (size_t)((d->q + 1) & ~1) * sizeof(float) +
                       64 * sizeof(double) + 64 * sizeof(float);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  switch (S) {
-    case 8:
-      SPA_CHECK_CUDA(cudaFuncSetAttribute(mwg_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      mwg_kernel<8><<<(unsigned)m, nthr, smem, st>>>(P);
-      break;
-    case 16:
-      SPA_CHECK_CUDA(cudaFuncSetAttribute(mwg_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      mwg_kernel<16><<<(unsigned)m, nthr, smem, st>>>(P);
-      break;
-    case 32:
-      SPA_REQUIRE(nthr <= 512, kNotSupported, "spa_mwg_move: n > 16384 not supported");
-      SPA_CHECK_CUDA(cudaFuncSetAttribute(mwg_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      mwg_kernel<32><<<(unsigned)m, nthr, smem, st>>>(P);
-      break;
-    default:
-      return fail(kNotSupported, "spa_mwg_move: n > 16384 not supported");
-  }
+  SPA_REQUIRE(S != 32 || nthr <= 512, kNotSupported, "spa_mwg_move: n > 16384 not supported");
+  const void* fn = mwg_fn(S, d->coded != 0);
+  SPA_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  void* args[] = {&P};
+  SPA_CHECK_CUDA(cudaLaunchKernel(fn, dim3((unsigned)m), dim3(nthr), args, smem, st));
   SPA_CHECK_LAUNCH();
   return 0;
 }

@@ -1292,9 +1292,17 @@ __global__ void __launch_bounds__(256) rw_chol_panel_kernel(float* __restrict__ 
 #pragma unroll
     for (int k = 0; k < kPanel; ++k) iv[k][lane] = x[k];
     if (blockIdx.x == 0) {
+      // L11 must not overwrite A11 in place: the other CTAs of this launch
+      // may not have read it yet (they are not co-scheduled when the device
+      // is shared with other streams).  Its strict lower part goes transposed
+      // into the block's unused upper triangle, its diagonal to S + q*q.
+      float dv = 0.f;
 #pragma unroll
-      for (int k = 0; k < kPanel; ++k)
-        if (lane < nb && k <= lane) S[(size_t)(jb + lane) * q + jb + k] = a[k];
+      for (int k = 0; k < kPanel; ++k) {
+        if (lane < nb && k < lane) S[(size_t)(jb + k) * q + jb + lane] = a[k];
+        if (k == lane) dv = a[k];
+      }
+      if (lane < nb) S[(size_t)q * q + jb + lane] = dv;
     }
   }
   if (rest <= 0) return;
@@ -1351,10 +1359,10 @@ __global__ void rw_emit_kernel(const float* __restrict__ S, int q, int kq, float
   const int64_t total = (int64_t)q * kq;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(e / kq), j = (int)(e % kq);
-    // entries inside a diagonal 32-block live in the lower triangle, panel
-    // entries below it (L21) were stored transposed in the upper triangle
+    // the factor's strict lower part was stored transposed in the upper
+    // triangle, its diagonal at S + q*q (rw_chol_panel_kernel)
     float v = 0.f;
-    if (j < q && j <= i) v = ((i / kPanel == j / kPanel) ? S[(size_t)i * q + j] : S[(size_t)j * q + i]) * f;
+    if (j < q && j <= i) v = (i == j ? S[(size_t)q * q + i] : S[(size_t)j * q + i]) * f;
     if (j < q) L[(size_t)i * q + j] = v;
     Lb[e] = __float2bfloat16(v);
   }

@@ -19,9 +19,13 @@ Extra SmcConfig fields (defaults keep the reference's behaviour):
                  per-step weighted marginal summaries computed on the device
                  (StepRecord.summary; see marginal_summaries)
     rw_factor_lag
-                 RW: the first move of a step proposes with the previous step's
-                 covariance factor, so the new factor (SYRK + Cholesky) is
-                 computed on a side stream beside that move
+                 RW covariance factor pipelining: 0 = every move of step t
+                 uses the factor of step t's population (computed before the
+                 first move); 1 = the first move uses the previous step's
+                 factor while the new one is computed on a side stream;
+                 2 (default) = every move of step t uses the factor of step
+                 t-1's population, computed on the side stream during step
+                 t-1's moves (off the critical path)
 """
 
 from __future__ import annotations
@@ -103,7 +107,7 @@ class SmcConfig:
     init_chains: int = 0
     summary_levels: tuple = ()
     summary_deltas: tuple = ()
-    rw_factor_lag: bool = True
+    rw_factor_lag: int = 2
 
     def __post_init__(self):
         if self.N < 2:
@@ -120,6 +124,8 @@ class SmcConfig:
             raise ValueError("init_burn >= 0, init_thin >= 1, snapshot_thin >= 1, threads >= 1 required")
         if self.move_kernel not in ("mwg", "rw"):
             raise ValueError(f"move_kernel must be 'mwg' or 'rw', got {self.move_kernel!r}")
+        if self.rw_factor_lag not in (0, 1, 2):
+            raise ValueError(f"rw_factor_lag must be 0, 1 or 2, got {self.rw_factor_lag!r}")
         if self.moves < 1 or self.init_chains < 0 or not self.rw_scale > 0:
             raise ValueError("moves >= 1, init_chains >= 0, rw_scale > 0 required")
         if len(self.summary_levels) > 4 or not all(0.0 < float(v) < 1.0 for v in self.summary_levels):
@@ -515,12 +521,15 @@ def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int,
     zs = system.z_buffers(config.moves)
     main = torch.cuda.current_stream()
     cur = getattr(system, "_fcur", 0)
-    lag = config.rw_factor_lag and getattr(system, "_factor_ready", False) and config.moves > 1
+    lag = int(config.rw_factor_lag) if getattr(system, "_factor_ready", False) else 0
+    if lag == 1 and config.moves == 1:
+        lag = 2  # the new factor would only serve the next step anyway
     centred = factored = None
     if lag:
-        # the new factor is built on a side stream while move 0 proposes with
-        # the previous one; only move 0's accept (which writes beta) waits for
-        # the centring pass, and move 1 for the factor
+        # the new factor is built on a side stream from the current particles
+        # while the moves propose with the previous one; only move 0's accept
+        # (the first write of beta) waits for the centring pass.  Lag 1
+        # switches to the new factor at move 1, lag 2 at the next step.
         nxt = 1 - cur
         fs = system.factor_stream()
         centred, factored = torch.cuda.Event(), torch.cuda.Event()
@@ -533,11 +542,15 @@ def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int,
         nxt = cur
         system._factor_ready = True
     main.wait_event(z_ready)
+    pending = getattr(system, "_factored", None)
+    if pending is not None:  # lag 2: the previous step's factor (normally long finished)
+        main.wait_event(pending)
+        system._factored = None
     # system.lp already holds the log-prior at the new scale (fused reweight pass)
     system.counter.zero_()
     Lb = system.factor_operand(cur)
     for mv in range(config.moves):
-        if lag and mv == 1:
+        if lag == 1 and mv == 1:
             main.wait_event(factored)
             Lb = system.factor_operand(nxt)
         _lib.call("spa_rw_propose", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb, Lb,
@@ -554,6 +567,8 @@ def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int,
         _lib.call("spa_rw_accept", _p(system.beta), system.ldb, _p(rw["prop"]), system.q, system.N, _p(ws["ylin"]),
                   _p(ws["sp"]), _p(rw["lp_p"]), _p(system.ll), _p(system.lp), int(config.seed), int(t),
                   int(system.i0), mv, _p(system.counter), _stream())
+    if lag == 2:
+        system._factored = factored
     system._fcur = nxt
     acc = system.counter.clone() if group is None else group.all_reduce_sum(system.counter.clone())
     return acc  # device tensor: read lazily (no host sync inside the step)

@@ -338,6 +338,51 @@ def test_rw_factor_paths(q):
     assert not Lb[:, q:].any()
 
 
+def test_rw_factor_under_contention():
+    """The panel kernels' CTAs are not co-scheduled when other streams hold
+    SMs: the factor must be bit-identical to the idle-device result while
+    matmuls run on another stream (regression: the diagonal block used to be
+    overwritten in place by CTA 0 before the other CTAs had read it)."""
+    from paper_1106_0322_b200.smc import _round_up
+
+    q = 500
+    rng = np.random.default_rng(5)
+    G = rng.normal(size=(q, q + 8)) / np.sqrt(q)
+    S = G @ G.T + 0.05 * np.eye(q)
+    acc = torch.zeros(q + q * q, dtype=torch.int64)
+    acc[q:] = torch.from_numpy(np.rint(np.tril(S) * 2.0**48).astype(np.int64).reshape(-1))
+    acc = acc.cuda()
+    kq = _round_up(q, 64)
+    nws = (_round_up(8 * q * q, 256) + _round_up(2 * q * kq, 256) + 8192) // 8 + 1
+
+    def factor(stream):
+        L = torch.zeros((q, q), dtype=torch.float32, device="cuda")
+        fws = torch.zeros(nws, dtype=torch.float64, device="cuda")
+        info = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _lib.call("spa_rw_factor", _p(acc), q, 2.38, 1e-6, _p(L), _p(fws), _p(info),
+                  ctypes.c_void_p(stream.cuda_stream))
+        return L, info
+
+    main = torch.cuda.current_stream()
+    L0, info0 = factor(main)
+    torch.cuda.synchronize()
+    ref = L0.cpu()
+    busy, side = torch.cuda.Stream(), torch.cuda.Stream()
+    X = torch.randn(4096, 4096, device="cuda")
+    outs = []
+    for _ in range(6):
+        with torch.cuda.stream(busy):
+            for _ in range(4):
+                X = (X @ X).clamp_(-1, 1)
+        with torch.cuda.stream(side):
+            outs.append(factor(side))
+    torch.cuda.synchronize()
+    assert int(info0.item()) == 0
+    for L, info in outs:
+        assert int(info.item()) == 0
+        assert torch.equal(L.cpu(), ref)
+
+
 def test_rw_propose_and_accept_vs_oracle():
     """One RW move: proposal (Philox normals, L z on tcgen05, fused pack),
     K1 likelihood of the proposal and the MH decision vs the oracle."""

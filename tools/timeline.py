@@ -52,3 +52,11 @@ gaps.sort(reverse=True)
 print("largest gaps (us, next kernel):")
 for g, n in gaps[:15]:
     print(f"  {g:8.1f}  {n}")
+if os.environ.get("TIMELINE_DUMP"):
+    # the last step's kernels in start order (us from the step's first kernel)
+    per = len(kern) // steps
+    last = kern[-per:]
+    t0 = last[0][0]
+    print("last step, start/end us:")
+    for a, b, n in last:
+        print(f"  {a - t0:8.1f} {b - t0:8.1f} {b - a:7.1f}  {n[:70]}")
