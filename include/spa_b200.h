@@ -166,28 +166,34 @@ int spa_mwg_move(const spa_design* d, float* beta, int64_t m, int32_t ldb, doubl
 /* ---- K8: population random-walk moves (north-star kernel) --------------
  * Weighted moments into an int64 fixed-point (2^-48) accumulator
  * partial[q + q*q] zeroed by the caller:
- *   phase 0: mu = sum_k w_k beta_k                       -> partial[0:q]
- *   phase 1: S = sum_k w_k (beta_k-mu)(beta_k-mu)^T      -> partial[q:] (lower)
- *            as a split-K tcgen05 SYRK of the centred, sqrt(w)-weighted,
- *            transposed bf16 hi/lo particles; per-split float32 tiles are
- *            summed in fixed order (ws: spa_rw_moments_workspace_bytes).
- *   phase 2: only the centring/transposition of phase 1 (the last read of
- *            beta) into ws; phase 3: only its SYRK + reduce, from ws -- so
- *            the particles may be modified once phase 2 has completed.
+ *   phase 0: partial[0:q] += sum_k w_k beta_k (the weighted mean; seeds the
+ *            centring point on the first call)
+ *   phase 2: one pass over beta: Dt = bf16(sqrt(w_k) (beta_k - c)) into ws
+ *            and partial[0:q] += sum_k w_k (beta_k - c) = mu - c, for the
+ *            caller's centring point c = center[q] (float32; normally the
+ *            previous population mean)
+ *   phase 3: partial[q:] (lower) += Dt Dt^T = sum_k w_k (beta_k-c)(beta_k-c)^T
+ *            as a split-K tcgen05 SYRK; per-split float32 tiles summed in
+ *            fixed order (ws: spa_rw_moments_workspace_bytes)
+ *   phase 1: 2 then 3.  The particles may be modified once phase 2 has
+ *            completed.
  * Integer sums are order-independent, so the moments are bit-identical for any
  * CTA schedule or particle sharding (multi-GPU: all-reduce `partial`). */
 size_t spa_rw_moments_workspace_bytes(int64_t m, int32_t q);
-int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const double* w, int32_t phase,
-                   int64_t* partial, void* ws, size_t ws_bytes, void* stream);
-/* Covariance from the fixed-point moments, jitter, blocked float32 Cholesky
- * (L only parameterises a symmetric proposal, so float32 suffices);
+int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const double* w, const float* center,
+                   int32_t phase, int64_t* partial, void* ws, size_t ws_bytes, void* stream);
+/* Covariance from the phase 1 moments: S = M - delta delta^T (delta =
+ * partial[0:q], M = partial[q:]) = the weighted covariance for any centring
+ * point, plus trace-scaled jitter; blocked float32 Cholesky (L only
+ * parameterises a symmetric proposal, so float32 suffices);
  * L = s*chol(S) as float32 [q][q] row-major lower (s = scale/sqrt(q)) and as
  * the bf16 proposal operand [q][kq] at byte offset roundup(8*q*q, 256) of ws
  * (kq = roundup(q, 64)); ws >= roundup(8*q*q, 256) + roundup(2*q*kq, 256) + 8192
  * bytes (the last 8 KB hold the 32x32 panel inverse);
- * *info = 0 or the failing column + 1. */
+ * *info = 0 or the failing column + 1.  center (optional, the point phase 2
+ * used) is moved to the mean: center += delta. */
 int spa_rw_factor(const int64_t* partial, int32_t q, double scale, double jitter, float* L, double* ws, int* info,
-                  void* stream);
+                  float* center, void* stream);
 /* Proposal normals Z (bf16 [m][kq], kq = roundup(q, 64), zero padded) from
  * Philox4x32-10 keyed by seed with counter (j/8, i0+k, t, move | 3<<24): each
  * 32-bit word gives one sign-symmetric Box-Muller pair from two 15-bit

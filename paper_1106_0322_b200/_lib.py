@@ -79,9 +79,10 @@ _SIGNATURES = {
                              c_uint64, c_int32, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_int32,
                              c_void_p]),
     "spa_rw_moments_workspace_bytes": (c_size_t, [c_int64, c_int32]),
-    "spa_rw_moments": (c_int, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_int32, c_void_p, c_void_p, c_size_t,
-                               c_void_p]),
-    "spa_rw_factor": (c_int, [c_void_p, c_int32, c_double, c_double, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "spa_rw_moments": (c_int, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p, c_int32, c_void_p, c_void_p,
+                                c_size_t, c_void_p]),
+    "spa_rw_factor": (c_int, [c_void_p, c_int32, c_double, c_double, c_void_p, c_void_p, c_void_p, c_void_p,
+                              c_void_p]),
     "spa_rw_normals": (c_int, [c_int64, c_int32, c_uint64, c_int64, c_int64, c_int32, c_void_p, c_void_p]),
     "spa_rw_propose": (c_int, [POINTER(SpaDesign), c_void_p, c_int64, c_int32, c_void_p, c_uint64, c_int64, c_int64,
                                c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_double, c_void_p,

@@ -1167,13 +1167,21 @@ constexpr int kPanel = 32;
 // Fixed point -> float32 covariance with the trace-scaled jitter; one block
 // per row i (coalesced row writes).  Every block computes the trace with the
 // same warp-shuffle order, so all rows see the same jitter bits.
+// S = M - delta delta^T with M = sum_k w_k (beta_k - c)(beta_k - c)^T and
+// delta = sum_k w_k (beta_k - c) = mu - c (weights sum to 1), i.e. the
+// weighted covariance for any centring point c.  Block i also moves the
+// centre to the mean (center[i] += delta_i) for the next call.
 __global__ void __launch_bounds__(256) rw_cov_kernel(const unsigned long long* __restrict__ acc, int q,
-                                                     double jitter, float* __restrict__ S) {
+                                                     double jitter, float* __restrict__ S,
+                                                     float* __restrict__ center) {
   __shared__ double s_add;
   const int i = blockIdx.x;
   if (threadIdx.x < 32) {
     double tr = 0.0;
-    for (int d = threadIdx.x; d < q; d += 32) tr += from_fix(acc[q + (size_t)d * q + d]);
+    for (int d = threadIdx.x; d < q; d += 32) {
+      const double dd = from_fix(acc[d]);
+      tr += from_fix(acc[q + (size_t)d * q + d]) - dd * dd;
+    }
     tr = warp_sum(tr);
     if (threadIdx.x == 0) {
       const double t = tr / q;
@@ -1181,11 +1189,12 @@ __global__ void __launch_bounds__(256) rw_cov_kernel(const unsigned long long* _
     }
   }
   __syncthreads();
-  const double add = s_add;
+  const double add = s_add, di = from_fix(acc[i]);
   const unsigned long long* row = acc + q + (size_t)i * q;
   float* out = S + (size_t)i * q;
   for (int j = threadIdx.x; j < q; j += blockDim.x)
-    out[j] = (j > i) ? 0.f : (float)(from_fix(row[j]) + (i == j ? add : 0.0));
+    out[j] = (j > i) ? 0.f : (float)(from_fix(row[j]) - di * from_fix(acc[j]) + (i == j ? add : 0.0));
+  if (center && threadIdx.x == 0) center[i] = (float)((double)center[i] + di);
 }
 
 // Factor one 32 x 32 diagonal block with one warp (lane = row, a[k] =
@@ -1420,41 +1429,71 @@ __global__ void __launch_bounds__(256) rw_normals_kernel(int64_t m, int q, int k
   }
 }
 
-// Centre, weight and transpose the particles for the tensor-core SYRK:
-// Dt[i][k] = sqrt(w_k) (beta_ki - mu_i) as bf16 hi / lo, rows [hi | lo] of
-// 2*ldk columns (the engine's two-term A/B layout).
-__global__ void rw_center_t_kernel(const float* __restrict__ beta, int64_t m, int ldb, int q,
-                                   const double* __restrict__ w, const unsigned long long* __restrict__ acc,
-                                   __nv_bfloat16* __restrict__ Dt, int64_t ldk) {
-  // tile: 64 particles (k) x 32 columns (j); reads are row-coalesced, writes
-  // are 128-byte segments of Dt rows (bf16 pairs of consecutive particles)
-  __shared__ float tile[64][33];
-  __shared__ float sw[64], mu[32];
-  const int64_t k0 = (int64_t)blockIdx.x * 64;
+// Centre (around c, the previous population mean), weight and transpose
+// the particles for the tensor-core SYRK -- Dt[j][k] = bf16(sqrt(w_k)
+// (beta_kj - c_j)), rows of ldk particles -- and accumulate the mean offset
+// delta_j = sum_k w_k (beta_kj - c_j) (float64 per block, one fixed-point
+// atomic per column and block).  One pass over the particles: the exact
+// covariance is M - delta delta^T (rw_cov_kernel).  bf16 is ample here: the
+// factor only scales a symmetric proposal.
+constexpr int kCtrRows = 128;
+__global__ void __launch_bounds__(256) rw_center_kernel(const float* __restrict__ beta, int64_t m, int ldb, int q,
+                                                        const double* __restrict__ w,
+                                                        const float* __restrict__ center,
+                                                        unsigned long long* __restrict__ acc,
+                                                        __nv_bfloat16* __restrict__ Dt, int64_t ldk) {
+  // tile: 128 particles (k) x 32 columns (j); row-coalesced 128-byte reads,
+  // writes of 128-byte segments of Dt rows (bf16 pairs of particles)
+  __shared__ float tile[kCtrRows][33];
+  __shared__ float sw[kCtrRows];
+  __shared__ double wk[kCtrRows], red[8][32];
+  __shared__ float cj[32];
+  const int64_t k0 = (int64_t)blockIdx.x * kCtrRows;
   const int j0 = blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  if (threadIdx.x < 64) sw[threadIdx.x] = (k0 + threadIdx.x < m) ? (float)sqrt(w[k0 + threadIdx.x]) : 0.f;
-  if (threadIdx.x >= 64 && threadIdx.x < 96)
-    mu[threadIdx.x - 64] = (j0 + threadIdx.x - 64 < q) ? (float)from_fix(acc[j0 + threadIdx.x - 64]) : 0.f;
-  __syncthreads();
-#pragma unroll
-  for (int r = ty; r < 64; r += 8) {
-    const int64_t k = k0 + r;
-    const int j = j0 + tx;
-    tile[r][tx] = (k < m && j < q) ? sw[r] * (beta[k * ldb + j] - mu[tx]) : 0.f;
+  if (threadIdx.x < kCtrRows) {
+    const double v = (k0 + threadIdx.x < m) ? w[k0 + threadIdx.x] : 0.0;
+    wk[threadIdx.x] = v;
+    sw[threadIdx.x] = (float)sqrt(v);
+  } else if (threadIdx.x < kCtrRows + 32) {
+    const int j = j0 + threadIdx.x - kCtrRows;
+    cj[threadIdx.x - kCtrRows] = j < q ? center[j] : 0.f;
   }
   __syncthreads();
+  const int j = j0 + tx;
+  float x[kCtrRows / 8];
 #pragma unroll
-  for (int r = ty; r < 32; r += 8) {  // r = column j0 + r; lane = particle pair
-    const int j = j0 + r;
-    const int64_t k = k0 + 2 * tx;
-    if (j >= q || k >= ldk) continue;
-    const float v0 = tile[2 * tx][r], v1 = tile[2 * tx + 1][r];
-    const __nv_bfloat162 h = __floats2bfloat162_rn(v0, v1);
-    const float2 hf = __bfloat1622float2(h);
-    const __nv_bfloat162 l = __floats2bfloat162_rn(v0 - hf.x, v1 - hf.y);
-    *reinterpret_cast<__nv_bfloat162*>(Dt + (size_t)j * 2 * ldk + k) = h;
-    *reinterpret_cast<__nv_bfloat162*>(Dt + (size_t)j * 2 * ldk + ldk + k) = l;
+  for (int r = 0; r < kCtrRows / 8; ++r) {
+    const int64_t k = k0 + ty + 8 * r;
+    x[r] = (k < m && j < q) ? __ldcs(beta + k * ldb + j) : 0.f;
+  }
+  double ds = 0.0;
+#pragma unroll
+  for (int r = 0; r < kCtrRows / 8; ++r) {
+    const int rr = ty + 8 * r;
+    const float v = (j < q) ? x[r] - cj[tx] : 0.f;
+    tile[rr][tx] = sw[rr] * v;
+    ds = fma(wk[rr], (double)v, ds);
+  }
+  red[ty][tx] = ds;
+  __syncthreads();
+  if (ty == 0 && j < q) {
+    double t = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < 8; ++ww) t += red[ww][tx];
+    atomicAdd(&acc[j], to_fix(t));
+  }
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {  // column j0 + r; lane = particle pairs
+    const int jj = j0 + r;
+    if (jj >= q) continue;
+#pragma unroll
+    for (int h = 0; h < kCtrRows / 64; ++h) {
+      const int64_t k = k0 + 64 * h + 2 * tx;
+      if (k >= ldk) continue;
+      const __nv_bfloat162 b2 = __floats2bfloat162_rn(tile[64 * h + 2 * tx][r], tile[64 * h + 2 * tx + 1][r]);
+      *reinterpret_cast<__nv_bfloat162*>(Dt + (size_t)jj * ldk + k) = b2;
+    }
   }
 }
 
@@ -1893,7 +1932,7 @@ size_t spa_rw_moments_workspace_bytes(int64_t m, int32_t q) {
   const int64_t ldk = (m + 63) / 64 * 64;
   int mt, kbpu, units;
   syrk_split(m, q, mt, kbpu, units);
-  const size_t dt = (((size_t)2 * q * ldk * sizeof(__nv_bfloat16)) + 255) & ~size_t(255);
+  const size_t dt = (((size_t)q * ldk * sizeof(__nv_bfloat16)) + 255) & ~size_t(255);
   const size_t qp = (q + 3) / 4 * 4;  // 16-byte partial rows (TMA store)
   return dt + (size_t)units * q * qp * sizeof(float);
 }
@@ -1911,8 +1950,8 @@ __global__ void syrk_reduce_kernel(const float* __restrict__ part, int units, in
   acc[q + e] += to_fix(s);
 }
 
-int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const double* w, int32_t phase,
-                   int64_t* partial, void* ws, size_t ws_bytes, void* stream) {
+int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const double* w, const float* center,
+                   int32_t phase, int64_t* partial, void* ws, size_t ws_bytes, void* stream) {
   SPA_REQUIRE(beta && w && partial && m > 0 && q > 0 && phase >= 0 && phase <= 3, kBadArgument,
               "spa_rw_moments: bad arguments");
   cudaStream_t st = as_stream(stream);
@@ -1933,16 +1972,17 @@ int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const d
     SPA_CHECK_LAUNCH();
     return 0;
   }
-  // phase 1 = 2 then 3: centre/transpose (reads beta), then S = Dt Dt^T on
-  // tcgen05 (3 split products, split-K over particles) + fixed-order reduce
+  // phase 1 = 2 then 3: centre/weight/transpose (the one read of beta, also
+  // accumulating delta), then M = Dt Dt^T on tcgen05 (split-K over
+  // particles) + fixed-order reduce
   SPA_REQUIRE(ws && ws_bytes >= spa_rw_moments_workspace_bytes(m, q), kWorkspaceTooSmall,
               "spa_rw_moments: workspace too small");
   const int64_t ldk = (m + 63) / 64 * 64;
-  __nv_bfloat16* Dt = reinterpret_cast<__nv_bfloat16*>(ws);
-  // layout [q][2*ldk]: row i = [hi(i, :) | lo(i, :)]
+  __nv_bfloat16* Dt = reinterpret_cast<__nv_bfloat16*>(ws);  // [q][ldk]
   if (phase != 3) {
-    dim3 grid(cdiv(ldk, 64), cdiv(q, 32));
-    rw_center_t_kernel<<<grid, 256, 0, st>>>(beta, m, ldb, q, w, acc, Dt, ldk);
+    SPA_REQUIRE(center, kBadArgument, "spa_rw_moments: phases 1 and 2 need the centring point");
+    dim3 grid(cdiv(ldk, kCtrRows), cdiv(q, 32));
+    rw_center_kernel<<<grid, 256, 0, st>>>(beta, m, ldb, q, w, center, acc, Dt, ldk);
     SPA_CHECK_LAUNCH();
     if (phase == 2) return 0;
   }
@@ -1955,14 +1995,14 @@ int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const d
   args.n_tiles = (q + 255) / 256;
   args.tiles_per_unit = args.n_tiles;
   float* part = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) +
-                                         ((((size_t)2 * q * ldk * sizeof(__nv_bfloat16)) + 255) & ~size_t(255)));
+                                         ((((size_t)q * ldk * sizeof(__nv_bfloat16)) + 255) & ~size_t(255)));
   const int qp = (q + 3) / 4 * 4;
   EpiStoreT<float> epi{};
   int rc = make_tmap_out<float>(&epi.tmc, part, (uint64_t)q, (uint64_t)q, (uint64_t)units, (uint64_t)qp,
                                 (uint64_t)q * qp);
   if (rc) return rc;
   epi.m = q;
-  rc = launch_tc<2, 2, 256>(Dt, 2ull * ldk, Dt, 2ull * ldk, (uint64_t)q, args, units, epi, st);
+  rc = launch_tc<1, 1, 256>(Dt, (uint64_t)ldk, Dt, (uint64_t)ldk, (uint64_t)q, args, units, epi, st);
   if (rc) return rc;
   syrk_reduce_kernel<<<cdiv((int64_t)q * q, 256), 256, 0, st>>>(part, units, q, qp, acc);
   SPA_CHECK_LAUNCH();
@@ -1970,7 +2010,7 @@ int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const d
 }
 
 int spa_rw_factor(const int64_t* partial, int32_t q, double scale, double jitter, float* L, double* ws, int* info,
-                  void* stream) {
+                  float* center, void* stream) {
   SPA_REQUIRE(partial && L && ws && q > 0 && q <= 8192, kBadArgument, "spa_rw_factor: bad arguments");
   cudaStream_t st = as_stream(stream);
   const int kq = (q + 63) / 64 * 64;
@@ -1980,8 +2020,7 @@ int spa_rw_factor(const int64_t* partial, int32_t q, double scale, double jitter
   float* inv = reinterpret_cast<float*>(base + (((size_t)8 * q * q + 255) & ~size_t(255)) +
                                         (((size_t)2 * q * kq + 255) & ~size_t(255)));
   if (info) SPA_CHECK_CUDA(cudaMemsetAsync(info, 0, sizeof(int), st));
-  rw_cov_kernel<<<q, 256, 0, st>>>(
-      reinterpret_cast<const unsigned long long*>(partial), q, jitter, S);
+  rw_cov_kernel<<<q, 256, 0, st>>>(reinterpret_cast<const unsigned long long*>(partial), q, jitter, S, center);
   SPA_CHECK_LAUNCH();
   SPA_CHECK_CUDA(chol_graph_launch(S, q, inv, info, st));
   rw_emit_kernel<<<std::min<unsigned>(cdiv((int64_t)q * kq, 256), 1184), 256, 0, st>>>(
@@ -2082,7 +2121,7 @@ int spa_prepare(void) {
       (const void*)gather_kernel, (const void*)step_record_kernel, (const void*)resample_commit_kernel,
       (const void*)reduce_units_kernel, (const void*)rw_mean_kernel<4>, (const void*)rw_cov_kernel,
       (const void*)rw_chol_panel_kernel, (const void*)rw_emit_kernel,
-      (const void*)rw_normals_kernel, (const void*)rw_center_t_kernel, (const void*)rw_accept_kernel,
+      (const void*)rw_normals_kernel, (const void*)rw_center_kernel, (const void*)rw_accept_kernel,
       (const void*)syrk_reduce_kernel, (const void*)summary_hist_kernel, (const void*)summary_select_kernel,
       (const void*)summary_finish_kernel};
   for (const void* f : fns) {

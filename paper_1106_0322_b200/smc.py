@@ -21,11 +21,11 @@ Extra SmcConfig fields (defaults keep the reference's behaviour):
     rw_factor_lag
                  RW covariance factor pipelining: 0 = every move of step t
                  uses the factor of step t's population (computed before the
-                 first move); 1 = the first move uses the previous step's
-                 factor while the new one is computed on a side stream;
-                 2 (default) = every move of step t uses the factor of step
+                 first move); 1 (default) = the first move uses the previous
+                 step's factor while the new one is computed on a side
+                 stream; 2 = every move of step t uses the factor of step
                  t-1's population, computed on the side stream during step
-                 t-1's moves (off the critical path)
+                 t-1's moves
 """
 
 from __future__ import annotations
@@ -107,7 +107,7 @@ class SmcConfig:
     init_chains: int = 0
     summary_levels: tuple = ()
     summary_deltas: tuple = ()
-    rw_factor_lag: int = 2
+    rw_factor_lag: int = 1
 
     def __post_init__(self):
         if self.N < 2:
@@ -298,6 +298,7 @@ class ParticleSystem:
                 fws2=torch.empty((_round_up(8 * q * q, 256) + _round_up(2 * q * kq, 256) + 8192) // 8,
                                  dtype=torch.float64, device=dev),
                 info=torch.zeros(1, dtype=torch.int32, device=dev),
+                ctr=torch.zeros(q, dtype=torch.float32, device=dev),  # centring point (previous mean)
                 mws=torch.empty(max(_lib.load().spa_rw_moments_workspace_bytes(self.N, q), 8), dtype=torch.uint8,
                                 device=dev),
             )
@@ -313,6 +314,7 @@ class ParticleSystem:
         zs = getattr(self, "_zs", None)
         if zs is None or len(zs) < moves:
             self._zs = zs = [torch.empty((self.N, kq), dtype=torch.bfloat16, device=self.device) for _ in range(moves)]
+            self._z_next = None  # normals drawn ahead went to the old buffers
         return zs
 
     def factor_operand(self, buf: int | None = None):
@@ -459,27 +461,33 @@ def _loglik_device(system: ParticleSystem, out: torch.Tensor):
 
 def _rw_factor(system: ParticleSystem, scale: float, group=None, buf: int = 0, centred=None):
     """Population covariance (fixed-point moments, tcgen05 SYRK) and its
-    Cholesky factor into factor buffer `buf`, on the current stream.
-    `centred` (optional event) is recorded once the particles have been read
-    for the last time (after the centring pass)."""
+    Cholesky factor into factor buffer `buf`, on the current stream.  The
+    particles are read once, centred on the previous population mean (the
+    exact covariance is recovered as M - delta delta^T); the first call
+    seeds that centre with a mean pass.  `centred` (optional event) is
+    recorded once the particles have been read for the last time."""
     rw = system.rw_workspace()
     w = system.device_weights() if group is None else _global_weights(system, group)
     rw["acc"].zero_()
-    _lib.call("spa_rw_moments", _p(system.beta), system.N, system.ldb, system.q, _p(w), 0, _p(rw["acc"]), None, 0,
-              _stream())
-    if group is not None:
-        group.all_reduce_sum(rw["acc"][: system.q])
-    _lib.call("spa_rw_moments", _p(system.beta), system.N, system.ldb, system.q, _p(w), 2, _p(rw["acc"]),
-              _p(rw["mws"]), rw["mws"].numel(), _stream())
+    if not getattr(system, "_ctr_ready", False):
+        _lib.call("spa_rw_moments", _p(system.beta), system.N, system.ldb, system.q, _p(w), None, 0, _p(rw["acc"]),
+                  None, 0, _stream())
+        if group is not None:
+            group.all_reduce_sum(rw["acc"][: system.q])
+        rw["ctr"].copy_(rw["acc"][: system.q].double() * 2.0**-48)
+        rw["acc"][: system.q].zero_()
+        system._ctr_ready = True
+    _lib.call("spa_rw_moments", _p(system.beta), system.N, system.ldb, system.q, _p(w), _p(rw["ctr"]), 2,
+              _p(rw["acc"]), _p(rw["mws"]), rw["mws"].numel(), _stream())
     if centred is not None:
         centred.record()
-    _lib.call("spa_rw_moments", _p(system.beta), system.N, system.ldb, system.q, _p(w), 3, _p(rw["acc"]),
+    _lib.call("spa_rw_moments", _p(system.beta), system.N, system.ldb, system.q, _p(w), None, 3, _p(rw["acc"]),
               _p(rw["mws"]), rw["mws"].numel(), _stream())
     _lib.add_launches(1)  # phase 3 = tcgen05 SYRK + split reduce
     if group is not None:
-        group.all_reduce_sum(rw["acc"][system.q:])
+        group.all_reduce_sum(rw["acc"])
     _lib.call("spa_rw_factor", _p(rw["acc"]), system.q, float(scale), 1e-6, _p(rw["L"]),
-              _p(rw["fws" if buf == 0 else "fws2"]), _p(rw["info"]), _stream())
+              _p(rw["fws" if buf == 0 else "fws2"]), _p(rw["info"]), _p(rw["ctr"]), _stream())
     panels = -(-system.q // 32)
     _lib.add_launches(2 + 2 * panels - 1)  # cov + graph of panel kernels + emit
 
@@ -494,22 +502,33 @@ def _global_weights(system, group):
     return system.w
 
 
-def _rw_normals_async(system: ParticleSystem, config: SmcConfig, t: int):
-    """The proposal normals of every move depend only on (seed, t, move,
-    particle): draw them on a side stream, launched at the top of the step so
-    they fill the device while the host waits on the reweight result and
-    while the covariance is estimated and factored.  Returns the ready event."""
+def _launch_normals(system: ParticleSystem, config: SmcConfig, t: int, mv: int):
+    """Proposal normals of (step t, move mv) into z buffer mv, on the side
+    stream after everything enqueued on the current stream so far (so the
+    buffer's previous reader is done).  Returns the ready event."""
     main = torch.cuda.current_stream()
     side = system.side_stream()
     zs = system.z_buffers(config.moves)
-    side.wait_stream(main)  # previous step's proposals are done reading zs
-    with torch.cuda.stream(side):
-        for mv in range(config.moves):
-            _lib.call("spa_rw_normals", system.N, system.q, int(config.seed), int(t), int(system.i0), mv,
-                      _p(zs[mv]), ctypes.c_void_p(side.cuda_stream))
-    z_ready = torch.cuda.Event()
-    z_ready.record(side)
-    return z_ready
+    side.wait_stream(main)
+    _lib.call("spa_rw_normals", system.N, system.q, int(config.seed), int(t), int(system.i0), mv, _p(zs[mv]),
+              ctypes.c_void_p(side.cuda_stream))
+    ev = torch.cuda.Event()
+    ev.record(side)
+    return ev
+
+
+def _rw_normals_async(system: ParticleSystem, config: SmcConfig, t: int):
+    """The proposal normals depend only on (seed, t, move, particle), so each
+    move's are drawn on a side stream beside the previous move's likelihood
+    kernel (tensor-bound, leaving the ALU/XU pipes to the Philox/Box-Muller
+    kernel); move 0's beside the previous step's last move.  Returns move 0's
+    ready event, drawing them now if the previous step did not."""
+    key = (int(config.seed), int(t), int(system.i0), system.N, system.q)
+    pre = getattr(system, "_z_next", None)
+    system._z_next = None
+    if pre is not None and pre[0] == key:
+        return pre[1]
+    return _launch_normals(system, config, t, 0)
 
 
 def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int, group=None, z_ready=None):
@@ -541,7 +560,6 @@ def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int,
         _rw_factor(system, config.rw_scale, group, buf=cur)
         nxt = cur
         system._factor_ready = True
-    main.wait_event(z_ready)
     pending = getattr(system, "_factored", None)
     if pending is not None:  # lag 2: the previous step's factor (normally long finished)
         main.wait_event(pending)
@@ -553,9 +571,17 @@ def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int,
         if lag == 1 and mv == 1:
             main.wait_event(factored)
             Lb = system.factor_operand(nxt)
+        main.wait_event(z_ready)
         _lib.call("spa_rw_propose", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb, Lb,
                   int(config.seed), int(t), int(system.i0), mv, _p(zs[mv]), _p(rw["prop"]), _p(ws["A"]),
                   _p(ws["ylin"]), float(prior.a), float(prior.c), _p(rw["lp_p"]), _stream())
+        # the next move's normals (the next step's move 0 after the last move)
+        # run beside this move's likelihood kernel
+        if mv + 1 < config.moves:
+            z_ready = _launch_normals(system, config, t, mv + 1)
+        else:
+            system._z_next = ((int(config.seed), int(t) + 1, int(system.i0), system.N, system.q),
+                              _launch_normals(system, config, t + 1, 0))
         if KERNEL_TIMER is not None:
             KERNEL_TIMER.start("loglik")
         _lib.call("spa_loglik_softplus", ctypes.byref(d.struct), _p(ws["A"]), system.N, _p(ws["sp"]), _p(ws["ws"]),
@@ -591,7 +617,7 @@ def _prepare_for_path(system: ParticleSystem, config: SmcConfig) -> None:
         system.side_stream()
         for buf in ("fws", "fws2"):  # both factor buffers (the lagged factor alternates them)
             _lib.call("spa_rw_factor", _p(rw["acc"]), system.q, float(config.rw_scale), 1e-6, _p(rw["L"]),
-                      _p(rw[buf]), _p(rw["info"]), _stream())
+                      _p(rw[buf]), _p(rw["info"]), None, _stream())
 
 
 def resident_chains(design: DeviceDesign) -> int:
@@ -774,8 +800,7 @@ def smc_step(system: ParticleSystem, data, schedule: Schedule, t: int, config: S
     bs = schedule.bs
     prior_prev = GtPrior(a, prior_scale(a, bs[t - 2]))
     prior_t = GtPrior(a, prior_scale(a, bs[t - 1]))
-    # launched first: measured better than overlapping them with the Cholesky
-    # (they then slow its latency-bound panel kernels)
+    # move 0's normals (normally drawn during the previous step)
     z_ready = _rw_normals_async(system, config, t) if config.move_kernel == "rw" else None
     try:
         inc = _reweight_device(system, prior_t, prior_prev, group)

@@ -290,17 +290,24 @@ def test_rw_moments_and_factor(name):
 
     data, d, s, B = _rw_setup(name)
     s.log_weights = np.log(np.random.default_rng(1).dirichlet(np.ones(s.N) * 2.0))
-    _rw_factor(s, 2.38)
     rw = s.rw_workspace()
-    assert int(rw["info"].item()) == 0
-    w = s.weights
-    Bf = B.astype(np.float32).astype(np.float64)
-    Ls_ref, mu_ref, S_ref = orc.rw_cov_factor(Bf, w)
-    acc = rw["acc"].cpu().numpy()
-    np.testing.assert_allclose(acc[: s.q] / 2.0**48, mu_ref, rtol=1e-6, atol=1e-9)
-    L = rw["L"].cpu().numpy().astype(np.float64)
-    np.testing.assert_allclose(L @ L.T, Ls_ref @ Ls_ref.T, rtol=2e-3, atol=2e-5 * np.abs(Ls_ref @ Ls_ref.T).max())
-    assert np.allclose(np.triu(L, 1), 0.0)
+    # first call: centred on the exact mean; second: on the previous mean
+    # after the population moved (covariance recovered as M - delta delta^T)
+    for shift in (0.0, 0.3):
+        B = B + shift * np.linspace(-1.0, 1.0, s.q)
+        s.load_betas(B)
+        _rw_factor(s, 2.38)
+        assert int(rw["info"].item()) == 0
+        w = s.weights
+        Bf = B.astype(np.float32).astype(np.float64)
+        Ls_ref, mu_ref, S_ref = orc.rw_cov_factor(Bf, w)
+        np.testing.assert_allclose(rw["ctr"].cpu().numpy(), mu_ref, rtol=1e-6, atol=1e-7)
+        L = rw["L"].cpu().numpy().astype(np.float64)
+        # bf16 SYRK operands (2^-9 relative per element): entries within
+        # 1e-3 of the largest variance
+        np.testing.assert_allclose(L @ L.T, Ls_ref @ Ls_ref.T, rtol=2e-3,
+                                   atol=1e-3 * np.abs(Ls_ref @ Ls_ref.T).max())
+        assert np.allclose(np.triu(L, 1), 0.0)
 
 
 @pytest.mark.parametrize("q", [5, 33, 100, 500, 512, 520, 700])
@@ -323,7 +330,7 @@ def test_rw_factor_paths(q):
                       device="cuda")
     info = torch.zeros(1, dtype=torch.int32, device="cuda")
     jitter, scale = 1e-6, 2.38
-    _lib.call("spa_rw_factor", _p(acc), q, scale, jitter, _p(L), _p(fws), _p(info), _stream())
+    _lib.call("spa_rw_factor", _p(acc), q, scale, jitter, _p(L), _p(fws), _p(info), None, _stream())
     assert int(info.item()) == 0
     Sref = np.tril(Sfix).astype(np.float64) / 2.0**48
     Sref = Sref + np.tril(Sref, -1).T
@@ -359,7 +366,7 @@ def test_rw_factor_under_contention():
         L = torch.zeros((q, q), dtype=torch.float32, device="cuda")
         fws = torch.zeros(nws, dtype=torch.float64, device="cuda")
         info = torch.zeros(1, dtype=torch.int32, device="cuda")
-        _lib.call("spa_rw_factor", _p(acc), q, 2.38, 1e-6, _p(L), _p(fws), _p(info),
+        _lib.call("spa_rw_factor", _p(acc), q, 2.38, 1e-6, _p(L), _p(fws), _p(info), None,
                   ctypes.c_void_p(stream.cuda_stream))
         return L, info
 

@@ -17,7 +17,7 @@ L = torch.zeros((q, q), dtype=torch.float32, device="cuda")
 fws = torch.zeros((_round_up(8 * q * q, 256) + _round_up(2 * q * kq, 256) + 8192) // 8 + 1, dtype=torch.float64,
                   device="cuda")
 info = torch.zeros(1, dtype=torch.int32, device="cuda")
-f = lambda: _lib.call("spa_rw_factor", _p(acc), q, 2.38, 1e-6, _p(L), _p(fws), _p(info), _stream())
+f = lambda: _lib.call("spa_rw_factor", _p(acc), q, 2.38, 1e-6, _p(L), _p(fws), _p(info), None, _stream())
 f(); torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()

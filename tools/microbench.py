@@ -49,7 +49,7 @@ print(f"{'smc_step (mean of 10)':28s} {t0.elapsed_time(t1) / 10 * 1e3:9.1f} us")
 timeit("reweight (prior mode 1+lse)", lambda: S._reweight_device(s, prior, S.GtPrior(1.0, sched.bs[2])), 5)
 timeit("rw_factor (moments+chol)", lambda: S._rw_factor(s, 2.38))
 timeit("chol only", lambda: _lib.call("spa_rw_factor", _p(rw["acc"]), s.q, 2.38, 1e-6, _p(rw["L"]), _p(rw["fws"]),
-                                      _p(rw["info"]), _stream()))
+                                      _p(rw["info"]), None, _stream()))
 timeit("prior mode 2", lambda: _lib.call("spa_prior_rows", ctypes.byref(d.struct), _p(s.beta), s.N, s.ldb, 1.0,
                                          float(prior.c), float(prior.c), 2, _p(s.lp), _stream()))
 zb = s.z_buffers(1)[0]
