@@ -1432,72 +1432,89 @@ __global__ void __launch_bounds__(256) rw_normals_kernel(int64_t m, int q, int k
 // Centre (around c, the previous population mean), weight and transpose
 // the particles for the tensor-core SYRK -- Dt[j][k] = bf16(sqrt(w_k)
 // (beta_kj - c_j)), rows of ldk particles -- and accumulate the mean offset
-// delta_j = sum_k w_k (beta_kj - c_j) (float64 per block, one fixed-point
-// atomic per column and block).  One pass over the particles: the exact
-// covariance is M - delta delta^T (rw_cov_kernel).  bf16 is ample here: the
-// factor only scales a symmetric proposal.
-constexpr int kCtrRows = 128;
+// delta_j = sum_k w_k (beta_kj - c_j) (one fixed-point atomic per column and
+// block).  One pass over the particles: the exact covariance is
+// M - delta delta^T (rw_cov_kernel).  bf16 is ample here: the factor only
+// scales a symmetric proposal.
+// Transposed in registers: lane (cq, pg) of warp w holds columns 4 cq .. +3
+// of the 8 particles 16 w + 8 pg .. +7, so loads are 256-byte row segments
+// and each column's 8 particles leave as one 16-byte store (a warp writes
+// 16 full 32-byte sectors).  Block: 64 columns x 128 particles.
+constexpr int kCtrRows = 128, kCtrCols = 64;
 __global__ void __launch_bounds__(256) rw_center_kernel(const float* __restrict__ beta, int64_t m, int ldb, int q,
                                                         const double* __restrict__ w,
                                                         const float* __restrict__ center,
                                                         unsigned long long* __restrict__ acc,
                                                         __nv_bfloat16* __restrict__ Dt, int64_t ldk) {
-  // tile: 128 particles (k) x 32 columns (j); row-coalesced 128-byte reads,
-  // writes of 128-byte segments of Dt rows (bf16 pairs of particles)
-  __shared__ float tile[kCtrRows][33];
-  __shared__ float sw[kCtrRows];
-  __shared__ double wk[kCtrRows], red[8][32];
-  __shared__ float cj[32];
-  const int64_t k0 = (int64_t)blockIdx.x * kCtrRows;
-  const int j0 = blockIdx.y * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  if (threadIdx.x < kCtrRows) {
-    const double v = (k0 + threadIdx.x < m) ? w[k0 + threadIdx.x] : 0.0;
-    wk[threadIdx.x] = v;
-    sw[threadIdx.x] = (float)sqrt(v);
-  } else if (threadIdx.x < kCtrRows + 32) {
-    const int j = j0 + threadIdx.x - kCtrRows;
-    cj[threadIdx.x - kCtrRows] = j < q ? center[j] : 0.f;
-  }
-  __syncthreads();
-  const int j = j0 + tx;
-  float x[kCtrRows / 8];
+  __shared__ float red[8][kCtrCols];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, cq = lane & 15, pg = lane >> 4;
+  const int j = blockIdx.y * kCtrCols + 4 * cq;
+  const int64_t kb = (int64_t)blockIdx.x * kCtrRows + 16 * warp + 8 * pg;
+  const bool vec = (q % 4 == 0) && (ldb % 4 == 0);
+  float x[8][4];
 #pragma unroll
-  for (int r = 0; r < kCtrRows / 8; ++r) {
-    const int64_t k = k0 + ty + 8 * r;
-    x[r] = (k < m && j < q) ? __ldcs(beta + k * ldb + j) : 0.f;
-  }
-  double ds = 0.0;
+  for (int r = 0; r < 8; ++r) {
+    const int64_t k = kb + r;
+    if (vec) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (k < m && j < q) v = __ldcs(reinterpret_cast<const float4*>(beta + k * ldb + j));
+      x[r][0] = v.x;
+      x[r][1] = v.y;
+      x[r][2] = v.z;
+      x[r][3] = v.w;
+    } else {
 #pragma unroll
-  for (int r = 0; r < kCtrRows / 8; ++r) {
-    const int rr = ty + 8 * r;
-    const float v = (j < q) ? x[r] - cj[tx] : 0.f;
-    tile[rr][tx] = sw[rr] * v;
-    ds = fma(wk[rr], (double)v, ds);
-  }
-  red[ty][tx] = ds;
-  __syncthreads();
-  if (ty == 0 && j < q) {
-    double t = 0.0;
-#pragma unroll
-    for (int ww = 0; ww < 8; ++ww) t += red[ww][tx];
-    atomicAdd(&acc[j], to_fix(t));
-  }
-#pragma unroll
-  for (int r = ty; r < 32; r += 8) {  // column j0 + r; lane = particle pairs
-    const int jj = j0 + r;
-    if (jj >= q) continue;
-#pragma unroll
-    for (int h = 0; h < kCtrRows / 64; ++h) {
-      const int64_t k = k0 + 64 * h + 2 * tx;
-      if (k >= ldk) continue;
-      const __nv_bfloat162 b2 = __floats2bfloat162_rn(tile[64 * h + 2 * tx][r], tile[64 * h + 2 * tx + 1][r]);
-      *reinterpret_cast<__nv_bfloat162*>(Dt + (size_t)jj * ldk + k) = b2;
+      for (int i = 0; i < 4; ++i) x[r][i] = (k < m && j + i < q) ? beta[k * ldb + j + i] : 0.f;
     }
+  }
+  float c[4], d[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) c[i] = (j + i < q) ? center[j + i] : 0.f;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const double wd = (kb + r < m) ? w[kb + r] : 0.0;
+    const float wf = (float)wd, sf = (float)sqrt(wd);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float v = x[r][i] - c[i];
+      d[i] = fmaf(wf, v, d[i]);
+      x[r][i] = sf * v;  // exactly 0 for padding particles and columns
+    }
+  }
+  if (kb < ldk) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (j + i >= q) break;
+      uint4 u;
+      uint32_t* up = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const __nv_bfloat162 b2 = __floats2bfloat162_rn(x[2 * h][i], x[2 * h + 1][i]);
+        up[h] = *reinterpret_cast<const uint32_t*>(&b2);
+      }
+      *reinterpret_cast<uint4*>(Dt + (size_t)(j + i) * ldk + kb) = u;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) d[i] += __shfl_xor_sync(0xffffffffu, d[i], 16);
+  if (pg == 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) red[warp][4 * cq + i] = d[i];
+  }
+  __syncthreads();
+  if (threadIdx.x < kCtrCols) {
+    const int jj = blockIdx.y * kCtrCols + threadIdx.x;
+    double s = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < 8; ++ww) s += (double)red[ww][threadIdx.x];
+    if (jj < q) atomicAdd(&acc[jj], to_fix(s));
   }
 }
 
-__global__ void __launch_bounds__(256) rw_accept_kernel(float* __restrict__ beta, int ldb,
+constexpr int kAcceptThreads = 128;  // 4 warps x 32 particles: all blocks resident in one wave
+
+template <int kR>
+__global__ void __launch_bounds__(kAcceptThreads) rw_accept_kernel(float* __restrict__ beta, int ldb,
                                                          const __nv_bfloat16* __restrict__ eps, int q, int64_t m,
                                                          const double* __restrict__ ylin_p,
                                                          const double* __restrict__ sp_p,
@@ -1530,8 +1547,8 @@ __global__ void __launch_bounds__(256) rw_accept_kernel(float* __restrict__ beta
   if (lane == 0 && mask) atomicAdd(accepted, (unsigned long long)__popc(mask));
   if ((q % 4 == 0) && (ldb % 4 == 0) && q <= 512) {
     // beta' = beta + eps (the same float32 sum the pack used), accepted rows
-    // taken 4 at a time with all their loads in flight before any store
-    constexpr int kR = 4, kV = 4;  // rows per batch, float4 per lane per row (q <= 512)
+    // taken kR at a time with all their loads in flight before any store
+    constexpr int kV = 4;  // float4 per lane per row (q <= 512)
     while (mask) {
       int rows[kR];
 #pragma unroll
@@ -1981,7 +1998,7 @@ int spa_rw_moments(const float* beta, int64_t m, int32_t ldb, int32_t q, const d
   __nv_bfloat16* Dt = reinterpret_cast<__nv_bfloat16*>(ws);  // [q][ldk]
   if (phase != 3) {
     SPA_REQUIRE(center, kBadArgument, "spa_rw_moments: phases 1 and 2 need the centring point");
-    dim3 grid(cdiv(ldk, kCtrRows), cdiv(q, 32));
+    dim3 grid(cdiv(ldk, kCtrRows), cdiv(q, kCtrCols));
     rw_center_kernel<<<grid, 256, 0, st>>>(beta, m, ldb, q, w, center, acc, Dt, ldk);
     SPA_CHECK_LAUNCH();
     if (phase == 2) return 0;
@@ -2121,7 +2138,7 @@ int spa_prepare(void) {
       (const void*)gather_kernel, (const void*)step_record_kernel, (const void*)resample_commit_kernel,
       (const void*)reduce_units_kernel, (const void*)rw_mean_kernel<4>, (const void*)rw_cov_kernel,
       (const void*)rw_chol_panel_kernel, (const void*)rw_emit_kernel,
-      (const void*)rw_normals_kernel, (const void*)rw_center_kernel, (const void*)rw_accept_kernel,
+      (const void*)rw_normals_kernel, (const void*)rw_center_kernel, (const void*)rw_accept_kernel<2>,
       (const void*)syrk_reduce_kernel, (const void*)summary_hist_kernel, (const void*)summary_select_kernel,
       (const void*)summary_finish_kernel};
   for (const void* f : fns) {
@@ -2203,7 +2220,8 @@ int spa_rw_accept(float* beta, int32_t ldb, const void* eps, int32_t q, int64_t 
                   int64_t i0, int32_t move, unsigned long long* accepted, void* stream) {
   SPA_REQUIRE(beta && eps && ylin_p && sp_p && lp_p && ll && lp && accepted && m > 0, kBadArgument,
               "spa_rw_accept: bad arguments");
-  rw_accept_kernel<<<cdiv(m, 256), 256, 0, as_stream(stream)>>>(beta, ldb, reinterpret_cast<const __nv_bfloat16*>(eps),
+  rw_accept_kernel<2><<<cdiv(m, kAcceptThreads), kAcceptThreads, 0, as_stream(stream)>>>(
+      beta, ldb, reinterpret_cast<const __nv_bfloat16*>(eps),
                                                                q, m, ylin_p, sp_p, lp_p, ll, lp, seed, t, i0, move,
                                                                accepted);
   SPA_CHECK_LAUNCH();

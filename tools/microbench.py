@@ -64,3 +64,14 @@ timeit("prior_reweight (fused)", lambda: _lib.call("spa_prior_reweight", ctypes.
 timeit("marginal summaries (3 q, 2 d)", lambda: S.marginal_summaries(s, (0.05, 0.5, 0.95), (0.05, 0.1)))
 timeit("K1 loglik", lambda: _lib.call("spa_loglik_softplus", ctypes.byref(d.struct), _p(ws["A"]), s.N, _p(ws["sp"]),
                                       _p(ws["ws"]), ws["ws"].numel(), _stream()))
+wts = s.device_weights()
+timeit("centre pass (moments phase 2)", lambda: _lib.call(
+    "spa_rw_moments", _p(s.beta), s.N, s.ldb, s.q, _p(wts), _p(rw["ctr"]), 2, _p(rw["acc"]), _p(rw["mws"]),
+    rw["mws"].numel(), _stream()))
+timeit("SYRK + reduce (phase 3)", lambda: _lib.call(
+    "spa_rw_moments", _p(s.beta), s.N, s.ldb, s.q, _p(wts), None, 3, _p(rw["acc"]), _p(rw["mws"]),
+    rw["mws"].numel(), _stream()))
+# last: the accept writes the particle state
+timeit("accept", lambda: _lib.call("spa_rw_accept", _p(s.beta), s.ldb, _p(rw["prop"]), s.q, s.N, _p(ws["ylin"]),
+                                   _p(ws["sp"]), _p(rw["lp_p"]), _p(s.ll), _p(s.lp), 1, 4, 0, 0, _p(s.counter),
+                                   _stream()))
