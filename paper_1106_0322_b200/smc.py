@@ -314,7 +314,7 @@ class ParticleSystem:
         zs = getattr(self, "_zs", None)
         if zs is None or len(zs) < moves:
             self._zs = zs = [torch.empty((self.N, kq), dtype=torch.bfloat16, device=self.device) for _ in range(moves)]
-            self._z_next = None  # normals drawn ahead went to the old buffers
+            self._z_pending = None  # normals drawn ahead went to the old buffers
         return zs
 
     def factor_operand(self, buf: int | None = None):
@@ -517,18 +517,44 @@ def _launch_normals(system: ParticleSystem, config: SmcConfig, t: int, mv: int):
     return ev
 
 
+_NORMALS_AHEAD = 2  # moves between a move's normals being drawn and used
+
+
+def _normals_key(system: ParticleSystem, config: SmcConfig, t: int, mv: int):
+    return (int(config.seed), int(t), int(mv), int(system.i0), system.N, system.q)
+
+
+def _normals_event(system: ParticleSystem, config: SmcConfig, t: int, mv: int):
+    """Ready event of the normals of (t, mv): drawn ahead by an earlier move,
+    else now."""
+    pending = getattr(system, "_z_pending", None)
+    ev = pending.pop(_normals_key(system, config, t, mv), None) if pending else None
+    return ev if ev is not None else _launch_normals(system, config, t, mv)
+
+
+def _normals_ahead(system: ParticleSystem, config: SmcConfig, t: int, mv: int):
+    """After move mv's accept: draw the normals _NORMALS_AHEAD moves ahead (of
+    this step or the next), on the side stream beside the following moves'
+    proposal GEMM and pack -- not beside K1, whose tensor-pipe time they
+    would stretch."""
+    g = mv + _NORMALS_AHEAD
+    tt, mm = (t, g) if g < config.moves else (t + 1, g - config.moves)
+    if mm >= config.moves:
+        return
+    if getattr(system, "_z_pending", None) is None:
+        system._z_pending = {}
+    system._z_pending[_normals_key(system, config, tt, mm)] = _launch_normals(system, config, tt, mm)
+
+
 def _rw_normals_async(system: ParticleSystem, config: SmcConfig, t: int):
-    """The proposal normals depend only on (seed, t, move, particle), so each
-    move's are drawn on a side stream beside the previous move's likelihood
-    kernel (tensor-bound, leaving the ALU/XU pipes to the Philox/Box-Muller
-    kernel); move 0's beside the previous step's last move.  Returns move 0's
-    ready event, drawing them now if the previous step did not."""
-    key = (int(config.seed), int(t), int(system.i0), system.N, system.q)
-    pre = getattr(system, "_z_next", None)
-    system._z_next = None
-    if pre is not None and pre[0] == key:
-        return pre[1]
-    return _launch_normals(system, config, t, 0)
+    """The proposal normals depend only on (seed, t, move, particle), so they
+    are drawn ahead on a side stream (see _normals_ahead); returns move 0's
+    ready event, drawing them now if no earlier move did."""
+    pending = getattr(system, "_z_pending", None)
+    if pending:  # drop draws for other steps / seeds (a step sequence changed)
+        for k in [k for k in pending if k[1] < t or k[0] != int(config.seed)]:
+            pending.pop(k)
+    return _normals_event(system, config, t, 0)
 
 
 def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int, group=None, z_ready=None):
@@ -571,17 +597,14 @@ def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int,
         if lag == 1 and mv == 1:
             main.wait_event(factored)
             Lb = system.factor_operand(nxt)
-        main.wait_event(z_ready)
+        main.wait_event(z_ready if mv == 0 else _normals_event(system, config, t, mv))
         _lib.call("spa_rw_propose", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb, Lb,
                   int(config.seed), int(t), int(system.i0), mv, _p(zs[mv]), _p(rw["prop"]), _p(ws["A"]),
                   _p(ws["ylin"]), float(prior.a), float(prior.c), _p(rw["lp_p"]), _stream())
-        # the next move's normals (the next step's move 0 after the last move)
-        # run beside this move's likelihood kernel
-        if mv + 1 < config.moves:
-            z_ready = _launch_normals(system, config, t, mv + 1)
-        else:
-            system._z_next = ((int(config.seed), int(t) + 1, int(system.i0), system.N, system.q),
-                              _launch_normals(system, config, t + 1, 0))
+        if mv == 0 and config.moves > 1:  # first step of a run: move 1's normals were not drawn ahead
+            pend = system._z_pending = getattr(system, "_z_pending", None) or {}
+            if _normals_key(system, config, t, 1) not in pend:
+                pend[_normals_key(system, config, t, 1)] = _launch_normals(system, config, t, 1)
         if KERNEL_TIMER is not None:
             KERNEL_TIMER.start("loglik")
         _lib.call("spa_loglik_softplus", ctypes.byref(d.struct), _p(ws["A"]), system.N, _p(ws["sp"]), _p(ws["ws"]),
@@ -593,6 +616,7 @@ def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int,
         _lib.call("spa_rw_accept", _p(system.beta), system.ldb, _p(rw["prop"]), system.q, system.N, _p(ws["ylin"]),
                   _p(ws["sp"]), _p(rw["lp_p"]), _p(system.ll), _p(system.lp), int(config.seed), int(t),
                   int(system.i0), mv, _p(system.counter), _stream())
+        _normals_ahead(system, config, t, mv)
     if lag == 2:
         system._factored = factored
     system._fcur = nxt
