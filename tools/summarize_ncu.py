@@ -58,7 +58,9 @@ def full(rep, out, traffic_json=None):
             wr = float(v[h.index("dram__bytes_write.sum")].replace(",", ""))
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
             b = rd * scale[units[h.index("dram__bytes_read.sum")]] + wr * scale[units[h.index("dram__bytes_write.sum")]]
-            json.dump({"bytes_per_launch": b, "source": rep, "kernel": name[:160]}, open(traffic_json, "w"), indent=1)
+            json.dump({"bytes_per_launch": b, "source": rep, "kernel": name[:160], "workload": "c3", "particles": 65536,
+                       "note": "dram__bytes_read.sum + dram__bytes_write.sum of one K1 launch "
+                               "(ncu --set full, bench.py --profile)"}, open(traffic_json, "w"), indent=1)
     open(out, "w").write("\n".join(lines) + "\n")
 
 
