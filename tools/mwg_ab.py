@@ -19,4 +19,7 @@ for K in (0, 444, 0, 444):
     t0 = time.perf_counter()
     s, acc = S.init_particles(data, S.GtPrior(1.0, 2.0), cfg)
     torch.cuda.synchronize()
-    print(f"  K={K or 'auto'}: init {time.perf_counter() - t0:.3f} s  acc {acc:.4f}  mean ll {s.ll.mean().item():.3f}")
+    import hashlib
+    h = hashlib.sha1(s.beta.cpu().numpy().tobytes() + s.ll.cpu().numpy().tobytes()).hexdigest()[:12]
+    print(f"  K={K or 'auto'}: init {time.perf_counter() - t0:.3f} s  acc {acc:.4f}  mean ll {s.ll.mean().item():.3f}"
+          f"  state {h}")
