@@ -162,6 +162,18 @@ int spa_mwg_resident_chains(const spa_design* d, int64_t* chains);
 int spa_mwg_move(const spa_design* d, float* beta, int64_t m, int32_t ldb, double a, double c, double step_sd,
                  int32_t cycles, uint64_t seed, int32_t tag, int64_t t, int64_t i0, int64_t sweep0, double* ll,
                  double* lp, unsigned long long* accepted, int32_t per_particle, void* stream);
+/* Initialisation chains in one launch: `slots` blocks of cycles_per_slot
+ * sweeps (sweep indices sweep0 ..), the state after block s stored in slot
+ * row*slots + s of slot_beta ([m*slots][ldb] float32), slot_ll and slot_lp;
+ * beta/ll/lp end at the last slot's state.  Bit-identical to `slots` calls of
+ * spa_mwg_move with sweep0 advanced by cycles_per_slot (one materialisation
+ * of the subject cache per slot instead of two, one launch instead of
+ * `slots`). */
+int spa_mwg_chain_slots(const spa_design* d, float* beta, int64_t m, int32_t ldb, double a, double c,
+                        double step_sd, int32_t cycles_per_slot, int32_t slots, uint64_t seed, int32_t tag,
+                        int64_t t, int64_t i0, int64_t sweep0, double* ll, double* lp, float* slot_beta,
+                        double* slot_ll, double* slot_lp, unsigned long long* accepted, int32_t per_particle,
+                        void* stream);
 
 /* ---- K8: population random-walk moves (north-star kernel) --------------
  * Weighted moments into an int64 fixed-point (2^-48) accumulator

@@ -47,6 +47,13 @@ struct MwgParams {
   double* lp;
   unsigned long long* accepted;
   int per_particle;  // accepted[row] instead of one total
+  // chain-slot mode (initialisation): slots > 0 runs `slots` blocks of
+  // `cycles` sweeps and stores the state after each block in slot
+  // row * slots + s of slot_beta ([.][ldb]), slot_ll and slot_lp
+  int slots;
+  float* slot_beta;
+  double* slot_ll;
+  double* slot_lp;
 };
 
 __device__ __forceinline__ double mwg_gt(double b, const MwgParams& P) {
@@ -210,6 +217,12 @@ __global__ void __launch_bounds__(512) mwg_kernel(MwgParams P) {
 
   float sig[S];
   double ll = materialise_ll<S, CODED>(P, bsh, tid, nthr, lane, wid, nw, red, sig);
+  unsigned long long acc = 0;
+  const int sub0 = tid * S;
+  const int nslots = P.slots > 0 ? P.slots : 1;
+  for (int sl = 0; sl < nslots; ++sl) {
+  // the log-prior restarts from beta for every block of sweeps (as a fresh
+  // call would), so chain-slot mode is bit-identical to one call per slot
   double lp = 0.0;
   {
     double lp0 = 0.0;
@@ -223,11 +236,9 @@ __global__ void __launch_bounds__(512) mwg_kernel(MwgParams P) {
     __syncthreads();
   }
 
-  unsigned long long acc = 0;
-  const int sub0 = tid * S;
   // ---- 2. sweeps -----------------------------------------------------------
   for (int cyc = 0; cyc < P.cycles; ++cyc) {
-    const uint64_t blk0 = (uint64_t)(P.sweep0 + cyc) * (uint64_t)q;
+    const uint64_t blk0 = (uint64_t)(P.sweep0 + (int64_t)sl * P.cycles + cyc) * (uint64_t)q;
     for (int j = tid; j < q; j += nthr) {
       uint64_t w[4];
       philox_block(key, blk0 + j, w);  // block index sweep*q + j (Philox counter index + 1)
@@ -299,13 +310,27 @@ __global__ void __launch_bounds__(512) mwg_kernel(MwgParams P) {
   }
 
   __syncthreads();
-  for (int j = tid; j < q; j += nthr) brow[j] = bsh[j];
-  // rematerialise the final state's log-likelihood from beta (the running
-  // sum of float32 increments only drives the accept decisions)
-  ll = materialise_ll<S, CODED>(P, bsh, tid, nthr, lane, wid, nw, red, nullptr);
+  const bool last = sl + 1 == nslots;
+  if (last)
+    for (int j = tid; j < q; j += nthr) brow[j] = bsh[j];
+  if (P.slots > 0)
+    for (int j = tid; j < q; j += nthr) P.slot_beta[(row * P.slots + sl) * P.ldb + j] = bsh[j];
+  // rematerialise the state's log-likelihood from beta (the running sum of
+  // float32 increments only drives the accept decisions); between slots
+  // this also refreshes sigma, exactly as the next call's entry would
+  ll = materialise_ll<S, CODED>(P, bsh, tid, nthr, lane, wid, nw, red, last ? nullptr : sig);
   if (tid == 0) {
-    P.ll[row] = ll;
-    if (P.lp) P.lp[row] = lp;
+    if (P.slots > 0) {
+      P.slot_ll[row * P.slots + sl] = ll;
+      P.slot_lp[row * P.slots + sl] = lp;
+    }
+    if (last) {
+      P.ll[row] = ll;
+      if (P.lp) P.lp[row] = lp;
+    }
+  }
+  }  // slots
+  if (tid == 0) {
     if (P.per_particle)
       P.accepted[row] += acc;
     else
@@ -365,10 +390,10 @@ extern "C" int spa_mwg_resident_chains(const spa_design* d, int64_t* chains) {
   return 0;
 }
 
-extern "C" int spa_mwg_move(const spa_design* d, float* beta, int64_t m, int32_t ldb, double a, double c,
-                            double step_sd, int32_t cycles, uint64_t seed, int32_t tag, int64_t t, int64_t i0,
-                            int64_t sweep0, double* ll, double* lp, unsigned long long* accepted,
-                            int32_t per_particle, void* stream) {
+static int mwg_launch(const spa_design* d, float* beta, int64_t m, int32_t ldb, double a, double c, double step_sd,
+                      int32_t cycles, uint64_t seed, int32_t tag, int64_t t, int64_t i0, int64_t sweep0, double* ll,
+                      double* lp, unsigned long long* accepted, int32_t per_particle, int32_t slots,
+                      float* slot_beta, double* slot_ll, double* slot_lp, void* stream) {
   SPA_REQUIRE(d && beta && ll && accepted && m >= 0 && cycles >= 0, kBadArgument, "spa_mwg_move: bad arguments");
   SPA_REQUIRE(a > 0 && c > 0 && step_sd > 0, kBadArgument, "spa_mwg_move: a, c, step_sd must be positive");
   SPA_REQUIRE(d->q >= 1 && d->q <= 2048, kNotSupported, "spa_mwg_move: q must lie in [1, 2048]");
@@ -395,6 +420,10 @@ extern "C" int spa_mwg_move(const spa_design* d, float* beta, int64_t m, int32_t
   P.lp = lp;
   P.accepted = accepted;
   P.per_particle = per_particle;
+  P.slots = slots;
+  P.slot_beta = slot_beta;
+  P.slot_ll = slot_ll;
+  P.slot_lp = slot_lp;
   const int nthr_raw = (d->n + S - 1) / S;
   const int nthr = std::max(32, (nthr_raw + 31) / 32 * 32);
   SPA_REQUIRE(nthr <= 1024, kNotSupported, "spa_mwg_move: too many subjects per particle");
@@ -409,4 +438,23 @@ extern "C" int spa_mwg_move(const spa_design* d, float* beta, int64_t m, int32_t
   SPA_CHECK_CUDA(cudaLaunchKernel(fn, dim3((unsigned)m), dim3(nthr), args, smem, st));
   SPA_CHECK_LAUNCH();
   return 0;
+}
+
+extern "C" int spa_mwg_move(const spa_design* d, float* beta, int64_t m, int32_t ldb, double a, double c,
+                            double step_sd, int32_t cycles, uint64_t seed, int32_t tag, int64_t t, int64_t i0,
+                            int64_t sweep0, double* ll, double* lp, unsigned long long* accepted,
+                            int32_t per_particle, void* stream) {
+  return mwg_launch(d, beta, m, ldb, a, c, step_sd, cycles, seed, tag, t, i0, sweep0, ll, lp, accepted, per_particle,
+                    0, nullptr, nullptr, nullptr, stream);
+}
+
+extern "C" int spa_mwg_chain_slots(const spa_design* d, float* beta, int64_t m, int32_t ldb, double a, double c,
+                                   double step_sd, int32_t cycles_per_slot, int32_t slots, uint64_t seed,
+                                   int32_t tag, int64_t t, int64_t i0, int64_t sweep0, double* ll, double* lp,
+                                   float* slot_beta, double* slot_ll, double* slot_lp,
+                                   unsigned long long* accepted, int32_t per_particle, void* stream) {
+  SPA_REQUIRE(slots >= 1 && slot_beta && slot_ll && slot_lp && cycles_per_slot >= 1, kBadArgument,
+              "spa_mwg_chain_slots: bad slot arguments");
+  return mwg_launch(d, beta, m, ldb, a, c, step_sd, cycles_per_slot, seed, tag, t, i0, sweep0, ll, lp, accepted,
+                    per_particle, slots, slot_beta, slot_ll, slot_lp, stream);
 }

@@ -694,13 +694,13 @@ def init_particles(data, prior_at_b1: GtPrior, config: SmcConfig, intercept: boo
     stage_b = torch.empty((Kl, R, system.ldb), dtype=torch.float32, device=system.device)
     stage_l = torch.empty((Kl, R), dtype=torch.float64, device=system.device)
     stage_p = torch.empty((Kl, R), dtype=torch.float64, device=system.device)
-    sweeps = config.init_burn
-    for j in range(R):
-        _mwg(chains, prior_at_b1, config.step_sd, config.init_thin, config.seed, TAG_INIT, 0, sweeps, counts=counts)
-        sweeps += config.init_thin
-        stage_b[:, j].copy_(chains.beta)
-        stage_l[:, j].copy_(chains.ll)
-        stage_p[:, j].copy_(chains.lp)
+    # all R thinning blocks in one launch (slot j = the state after init_burn
+    # + (j+1)*init_thin sweeps; bit-identical to one spa_mwg_move per slot)
+    d = chains.design
+    _lib.call("spa_mwg_chain_slots", ctypes.byref(d.struct), _p(chains.beta), chains.N, chains.ldb,
+              float(prior_at_b1.a), float(prior_at_b1.c), float(config.step_sd), int(config.init_thin), int(R),
+              int(config.seed), TAG_INIT, 0, int(chains.i0), int(config.init_burn), _p(chains.ll), _p(chains.lp),
+              _p(stage_b), _p(stage_l), _p(stage_p), _p(counts), 1, _stream())
     a, b = lo - c0 * R, hi - c0 * R  # this shard inside the staged slots [c0 R, c1 R)
     system.beta.copy_(stage_b.view(Kl * R, system.ldb)[a:b])
     system.ll.copy_(stage_l.view(-1)[a:b])
