@@ -56,6 +56,39 @@ def _code_column(x: np.ndarray):
     return g.astype(np.uint8), step, float(u[0]), lev
 
 
+def _code_columns(X: np.ndarray, dev) -> list:
+    """_code_column for every column at once, on the device (float64; the
+    per-column np.unique sorts took ~40 ms at n=5000, p=500).  Division and
+    rint are exactly rounded, so the codes, steps and levels are identical
+    to the host function's."""
+    n, q = X.shape
+    XT = torch.from_numpy(np.ascontiguousarray(X.T)).to(dev)
+    mn, mx = XT.min(dim=1).values, XT.max(dim=1).values
+    inf = torch.tensor(float("inf"), dtype=XT.dtype, device=dev)
+    u1 = torch.where(XT > mn[:, None], XT, inf).min(dim=1).values  # second smallest distinct value
+    const = mn == mx
+    in_set = ((XT == mn[:, None]) | (XT == u1[:, None]) | (XT == mx[:, None])).all(dim=1) | const
+    step = torch.where(const, torch.ones_like(mn), u1 - mn)
+    three = (u1 < mx) & ~const
+    spaced = ~three | ((mx - u1 - step).abs() <= 1e-9 * torch.clamp(step.abs(), min=1.0))
+    G = torch.round((XT - mn[:, None]) / step[:, None])  # round half to even, as np.rint
+    err = (mn[:, None] + step[:, None] * G - XT).abs().max(dim=1).values
+    exact = err <= 1e-12 * torch.clamp(XT.abs().max(dim=1).values, min=1.0)
+    ok = (in_set & (const | (spaced & exact))).cpu().numpy()
+    codes = torch.where(const[:, None], torch.zeros_like(G), G).to(torch.uint8).cpu().numpy()
+    mn, u1, mx, step = (v.cpu().numpy() for v in (mn, u1, mx, step))
+    const, three = const.cpu().numpy(), three.cpu().numpy()
+    out = [None] * q
+    for j in np.flatnonzero(ok):
+        if const[j]:
+            out[j] = (codes[j], 0.0, float(mn[j]), np.array([mn[j], 0.0, 0.0]))
+        else:
+            lev = np.zeros(3)
+            lev[: 3 if three[j] else 2] = (mn[j], u1[j], mx[j]) if three[j] else (mn[j], u1[j])
+            out[j] = (codes[j], float(step[j]), float(mn[j]), lev)
+    return out
+
+
 @dataclass
 class DeviceDesign:
     """Owns the device tensors behind one `spa_design` struct."""
@@ -83,7 +116,7 @@ class DeviceDesign:
         if intercept:
             pen[0] = 0
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        coded_cols = [_code_column(X[:, j]) for j in range(q)]
+        coded_cols = _code_columns(X, dev)
         coded = all(c is not None for c in coded_cols)
         n_words = mwg_words(n)
         npad = n_words * 32

@@ -435,3 +435,25 @@ def test_rw_propose_and_accept_vs_oracle():
         ok = (dlt >= 0) | (np.log(u) < dlt)
     assert int(s.counter.item()) == int(ok.sum()) and 0 < ok.sum() < s.N
     np.testing.assert_array_equal(s.betas, np.where(ok[:, None], prop, beta0))
+
+
+def test_code_columns_on_device_match_host():
+    """The device column coder (used by DeviceDesign.build) reproduces the
+    host _code_column exactly: constant, 2-level, 3-level and continuous
+    columns, including standardised genotypes."""
+    from paper_1106_0322_b200.data import named_spec, simulate_dataset
+    from paper_1106_0322_b200.design import _code_column, _code_columns
+
+    data, _ = simulate_dataset(named_spec("c2"))
+    X = np.asarray(data.X, dtype=np.float64)
+    rng = np.random.default_rng(0)
+    X = np.column_stack([np.ones(X.shape[0]), X, rng.normal(size=X.shape[0]),
+                         np.where(X[:, 0] > X[:, 0].min(), 1.5, -0.25), np.full(X.shape[0], -3.0),
+                         rng.integers(0, 3, X.shape[0]) * 0.7 - 0.1])
+    host = [_code_column(X[:, j]) for j in range(X.shape[1])]
+    dev = _code_columns(X, torch.device("cuda"))
+    assert sum(h is None for h in host) == 1
+    for h, d in zip(host, dev):
+        assert (h is None) == (d is None)
+        if h is not None:
+            assert np.array_equal(h[0], d[0]) and h[1] == d[1] and h[2] == d[2] and np.array_equal(h[3], d[3])
