@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(256) prior_reweight_kernel(spa_design d, const
 // Fewer lanes per row amortise the two float64 logs and the shuffle
 // reduction of the per-lane products over 4 IT columns instead of 16.
 template <int LPR, int IT>
-__global__ void __launch_bounds__(256) prior_reweight_rows_kernel(spa_design d, const float* __restrict__ beta,
+__global__ void __launch_bounds__(256, 4) prior_reweight_rows_kernel(spa_design d, const float* __restrict__ beta,
                                                                   int64_t m, int ldb, PriorConst pc,
                                                                   double* __restrict__ lw, double* __restrict__ lp) {
   __shared__ __align__(16) float pen_s[LPR * IT * 4];  // 0/1 penalty flags, padding columns 0

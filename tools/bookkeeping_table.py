@@ -31,7 +31,9 @@ alg = {  # algorithmic MB per launch
     "rw_center_kernel": (N * ldb * 4 + q * N * 2) / 1e6,                      # beta read, Dt written
     "EpiStoreT<__nv_bfloat16>": (N * 512 * 2 + N * ldb * 2) / 1e6,            # z read, eps written
     "prior_reweight_rows_kernel": (N * ldb * 4) / 1e6,                        # beta read
-    "rw_accept_kernel": None,                                                 # data dependent
+    # decision scalars of every row + beta/eps read and beta written for the
+    # accepted rows, at the C3 acceptance rate of the profiled step (0.256)
+    "rw_accept_kernel": (N * 5 * 8 + 0.256 * N * (ldb * 4 + ldb * 2 + ldb * 4)) / 1e6,
     "rw_normals_kernel": (N * 512 * 2) / 1e6,                                 # z written
 }
 label = {"EpiStoreT<__nv_bfloat16>": "propose GEMM (L z, TMA store)"}
@@ -56,7 +58,9 @@ for name, (n, t, rd, wr) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
           f"{ag:8.0f} {ag / peak * 100:6.1f}")
 print()
 print("# accept: algorithmic bytes are data dependent (decision scalars for all rows, beta/eps read and beta")
-print("# written for accepted rows only); the DRAM bytes are reported in their place.")
+print("# written for the accepted rows only, at the step's acceptance rate 0.256); its beta writes stay in L2.")
+print("# propose GEMM: also tensor work, 2*N*kq*kq = 34.4 GFLOP per launch (0.65 of the 1385 TFLOP/s peak")
+print("# at 38.4 us).")
 print("# normals: compute-bound (Philox4x32-10 + Box-Muller); its bytes are the 67 MB bf16 output.")
 print("# centre pass and propose GEMM outputs stay largely in L2 (read by the next kernel): DRAM writes")
 print("# are below the algorithmic bytes.")
