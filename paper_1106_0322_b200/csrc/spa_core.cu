@@ -144,20 +144,12 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// ---------------------------------------------------------------------------
-// Pack particle rows into the K1 A operand [m][2*kp] bf16 = [hi | lo] of the
-// scaled coefficients; coded designs carry the centring offset
-// o = sum_j gamma_j beta_j in three bf16 columns q..q+2 of the hi block (the
-// B operand holds 1 there), so the MMA yields eta directly.
-__device__ __forceinline__ float gt_logpdf_f(float b, float lc, float ap1, float inv, int de) {
-  const float x = fabsf(b);
-  return de ? lc - x * inv : lc - ap1 * log1pf(x * inv);
-}
-
+// 2^-48 fixed point for the order-independent moment sums
 constexpr double kFix = 281474976710656.0;  // 2^48
 
 __device__ __forceinline__ unsigned long long to_fix(double v) { return (unsigned long long)llrint(v * kFix); }
 __device__ __forceinline__ double from_fix(unsigned long long v) { return (double)(long long)v / kFix; }
+
 // Per-lane log-prior accumulator shared by pack_kernel, pack_eps_kernel and
 // prior_kernel mode 2 (same lane->column mapping and multiplication order, so
 // all three produce identical bits):
@@ -193,6 +185,11 @@ struct LpAcc {
   }
 };
 
+// ---------------------------------------------------------------------------
+// Pack particle rows into the K1 A operand [m][2*kp] bf16 = [hi | lo] of the
+// scaled coefficients; coded designs carry the centring offset
+// o = sum_j gamma_j beta_j in three bf16 columns q..q+2 of the hi block (the
+// B operand holds 1 there), so the MMA yields eta directly.
 // One warp per particle row; lanes take 4 consecutive columns (float4).
 // prop = beta (+ eps); A = [hi | lo] of alpha*prop; ylin = prop . X^T y;
 // off (coded) into the offset columns; lp = sum gt(prop) (float32 terms,
