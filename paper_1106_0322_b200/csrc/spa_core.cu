@@ -683,50 +683,67 @@ __global__ void __launch_bounds__(256) summary_hist_kernel(const float* __restri
   const int64_t r0 = (int64_t)blockIdx.y * kSumRows;
   uint32_t pre[kSumMaxLev];
 #pragma unroll
-  for (int l = 0; l < kSumMaxLev; ++l) pre[l] = (pass > 0 && l < sp.nlev && col < q) ? prefix[l * q + col] : 0u;
+  // levels past nlev get a prefix no key can have (tops are at most 24 bits)
+  for (int l = 0; l < kSumMaxLev; ++l) pre[l] = (pass > 0 && l < sp.nlev && col < q) ? prefix[l * q + col] : ~0u;
   double smean = 0.0;
   unsigned long long sin[kSumMaxDelta] = {0ull, 0ull, 0ull, 0ull}, stot = 0ull;
-  for (int64_t t0 = r0; t0 < min(m, r0 + kSumRows); t0 += kSumTile) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < kSumTile * kSumCols; e += blockDim.x) {
-      const int rr = e / kSumCols, cc = e % kSumCols;
+  // the next tile's particles and weights are loaded into registers while
+  // the current tile is histogrammed (the one-tile-at-a-time form spent
+  // most of its time waiting on the loads)
+  constexpr int kPer = kSumTile * kSumCols / 256;  // elements per thread (blockDim 256)
+  static_assert(kSumTile == 256, "one weight per thread");
+  const int64_t r1 = min(m, r0 + kSumRows);
+  float px[kPer];
+  double pw = 0.0;
+  auto load_tile = [&](int64_t t0) {
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int e = threadIdx.x + k * 256, rr = e / kSumCols, cc = e % kSumCols;
       const int64_t row = t0 + rr;
-      xs[rr][cc] = (row < m && c0 + cc < q) ? beta[row * ldb + c0 + cc] : 0.f;
+      px[k] = (row < m && c0 + cc < q) ? __ldcs(beta + row * ldb + c0 + cc) : 0.f;
     }
-    for (int rr = threadIdx.x; rr < kSumTile; rr += blockDim.x) {
-      const int64_t row = t0 + rr;
-      const double wv = row < m ? w[row] : 0.0;
-      wd[rr] = wv;
-      wf[rr] = sum_wfix(wv);
-    }
+    pw = (t0 + threadIdx.x < m) ? w[t0 + threadIdx.x] : 0.0;
+  };
+  load_tile(r0);
+  for (int64_t t0 = r0; t0 < r1; t0 += kSumTile) {
     __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int e = threadIdx.x + k * 256;
+      xs[e / kSumCols][e % kSumCols] = px[k];
+    }
+    wd[threadIdx.x] = pw;
+    wf[threadIdx.x] = sum_wfix(pw);
+    __syncthreads();
+    if (t0 + kSumTile < r1) load_tile(t0 + kSumTile);
     if (col >= q) continue;
-    for (int rr = lane; rr < kSumTile; rr += 32) {
-      const bool live = t0 + rr < m;
-      const float x = xs[rr][warp];
-      const unsigned long long v = wf[rr];
-      const uint32_t key = sum_key(x);
-      if (pass == 0) {
-        if (live) {
-          smean = fma(wd[rr], (double)x, smean);
+    // rows past m carry weight 0 (wd = wf = 0): no liveness tests needed
+    if (pass == 0) {
+#pragma unroll 2
+      for (int rr = lane; rr < kSumTile; rr += 32) {
+        const float x = xs[rr][warp];
+        const unsigned long long v = wf[rr];
+        smean = fma(wd[rr], (double)x, smean);
 #pragma unroll
-          for (int dd = 0; dd < kSumMaxDelta; ++dd)
-            if (dd < sp.ndelta && fabsf(x) < sp.delta[dd]) sin[dd] += v;
-          if (warp == 0) stot += v;
-        }
-        sum_warp_add<2>(sh + warp * 512, live && v != 0ull, key >> 24, v);
-      } else {
-        const int shift = 32 - 8 * pass;
-        const uint32_t top = key >> shift, dig = (key >> (shift - 8)) & 255u;
-        bool any = false;
-#pragma unroll
-        for (int l = 0; l < kSumMaxLev; ++l) any |= (l < sp.nlev) && top == pre[l];
-        any = any && live && v != 0ull;
+        for (int dd = 0; dd < kSumMaxDelta; ++dd)
+          if (dd < sp.ndelta && fabsf(x) < sp.delta[dd]) sin[dd] += v;
+        stot += v;
+        sum_warp_add<2>(sh + warp * 512, v != 0ull, sum_key(x) >> 24, v);
+      }
+    } else {
+      const int shift = 32 - 8 * pass;
+#pragma unroll 4
+      for (int rr = lane; rr < kSumTile; rr += 32) {
+        const uint32_t key = sum_key(xs[rr][warp]);
+        const uint32_t top = key >> shift;
+        const bool any = (top == pre[0]) | (top == pre[1]) | (top == pre[2]) | (top == pre[3]);
         if (__ballot_sync(0xffffffffu, any) == 0u) continue;  // most rows match no level's prefix
+        const unsigned long long v = any ? wf[rr] : 0ull;
+        const uint32_t dig = (key >> (shift - 8)) & 255u;
 #pragma unroll
         for (int l = 0; l < kSumMaxLev; ++l) {
           if (l >= sp.nlev) break;
-          sum_warp_add<0>(sh + (l * kSumCols + warp) * 512, any && top == pre[l], dig, v);
+          sum_warp_add<0>(sh + (l * kSumCols + warp) * 512, v != 0ull && top == pre[l], dig, v);
         }
       }
     }
