@@ -390,6 +390,31 @@ def test_rw_factor_under_contention():
         assert torch.equal(L.cpu(), ref)
 
 
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_rw_propose_eps_multi_tile(name):
+    """eps = L z of spa_rw_propose at q = 200 / 500 (several K blocks and
+    column tiles of the tcgen05 GEMM) equals the float32 product of the same
+    bf16 operands to bf16 output rounding."""
+    from paper_1106_0322_b200.smc import _round_up
+
+    data, d, s, B = _rw_setup(name, N=1536)
+    from paper_1106_0322_b200.smc import _rw_factor
+
+    _rw_factor(s, 2.38)
+    rw, ws = s.rw_workspace(), s.ll_workspace()
+    zb = s.z_buffers(1)[0]
+    _lib.call("spa_rw_normals", s.N, s.q, 3, 5, 0, 1, _p(zb), _stream())
+    _lib.call("spa_rw_propose", ctypes.byref(d.struct), _p(s.beta), s.N, s.ldb, s.factor_operand(), 3, 5, 0, 1,
+              _p(zb), _p(rw["prop"]), _p(ws["A"]), _p(ws["ylin"]), 1.0, 0.9, _p(rw["lp_p"]), _stream())
+    q, kq = s.q, _round_up(s.q, 64)
+    off = _round_up(8 * q * q, 256)
+    L = rw["fws"].view(torch.uint8)[off: off + 2 * q * kq].view(torch.bfloat16).view(q, kq).float()
+    ref = zb.float() @ L.T
+    got = rw["prop"][:, :q].float()
+    np.testing.assert_allclose(got.cpu().numpy(), ref.cpu().numpy(), rtol=1e-2, atol=2e-3 * ref.abs().max().item())
+    assert not rw["prop"][:, q:].float().any()
+
+
 def test_rw_propose_and_accept_vs_oracle():
     """One RW move: proposal (Philox normals, L z on tcgen05, fused pack),
     K1 likelihood of the proposal and the MH decision vs the oracle."""
