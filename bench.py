@@ -60,7 +60,8 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi SM clock / throttle-reason sampling during the timed region."""
+    """SM clock / throttle-reason sampling during the timed region (NVML,
+    falling back to the nvidia-smi CLI)."""
 
     QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -72,7 +73,32 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def _run_nvml(self):
+        """NVML (the library behind nvidia-smi) every ~2 ms: a short timed
+        region still gets many samples.  Rows in nvidia-smi's column layout."""
+        import pynvml
+
+        pynvml.nvmlInit()
+        try:
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            bits = (pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                flags = ["Active" if r & b else "Not Active" for b in bits]
+                self.rows.append([str(self.gpu), str(sm), str(mx), "", hex(r)] + flags)
+                self._stop.wait(0.002)
+        finally:
+            pynvml.nvmlShutdown()
+
     def _run(self):
+        try:
+            self._run_nvml()
+            return
+        except Exception:
+            self.rows.clear()
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.QUERY}",
