@@ -1035,8 +1035,10 @@ def run_sampler(data, a: float, schedule: Schedule, config: SmcConfig, intercept
 
 def fixed_b_mcmc(data, prior: GtPrior, n_samples: int, burn: int = 2000, thin: int = 5, seed: int = 0,
                  step_sd: float = 0.5, intercept: bool = False):
-    """Fixed-prior MwG validation chains (reference smc.py:452-476), run as
-    min(n_samples, 1024) parallel chains on the GPU."""
+    """Fixed-prior MwG validation chains (reference smc.py:452-476): the
+    reference's one chain (burn, then every thin-th state) run as parallel
+    chains on the GPU (init_particles: one resident wave of chains, each
+    filling a contiguous block of the n_samples slots)."""
     cfg = SmcConfig(N=max(2, n_samples), step_sd=step_sd, seed=seed, init_burn=burn, init_thin=thin)
     system, acc = init_particles(data, prior, cfg, intercept)
     return FixedBResult(system.betas[:n_samples], acc)
