@@ -73,34 +73,32 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
-    def _run_nvml(self):
-        """NVML (the library behind nvidia-smi) every ~2 ms: a short timed
-        region still gets many samples.  Rows in nvidia-smi's column layout."""
+    def _nvml_open(self):
         import pynvml
 
         pynvml.nvmlInit()
-        try:
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
-            bits = (pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
-                    pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap)
-            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
-            while not self._stop.is_set():
-                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                flags = ["Active" if r & b else "Not Active" for b in bits]
-                self.rows.append([str(self.gpu), str(sm), str(mx), "", hex(r)] + flags)
-                self._stop.wait(0.002)
-        finally:
-            pynvml.nvmlShutdown()
+        self._nvml = pynvml
+        self._h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+        self._bits = (pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                      pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap)
+        self._mx = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+
+    def _nvml_sample(self):
+        nv = self._nvml
+        sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        flags = ["Active" if r & b else "Not Active" for b in self._bits]
+        self.rows.append([str(self.gpu), str(sm), str(self._mx), "", hex(r)] + flags)
 
     def _run(self):
-        try:
-            self._run_nvml()
-            return
-        except Exception:
-            self.rows.clear()
+        """NVML (the library behind nvidia-smi) every ~2 ms, so a short timed
+        region still gets several samples; else the nvidia-smi CLI."""
         while not self._stop.is_set():
             try:
+                if self._nvml is not None:
+                    self._nvml_sample()
+                    self._stop.wait(0.002)
+                    continue
                 out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.QUERY}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
                 if out.returncode == 0 and out.stdout.strip():
@@ -110,6 +108,12 @@ class ClockSampler:
             self._stop.wait(0.2)
 
     def __enter__(self):
+        self._nvml = None
+        try:  # opened before the timed region (NVML init takes tens of ms)
+            self._nvml_open()
+            self._nvml_sample()
+        except Exception:
+            self._nvml = None
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
@@ -117,6 +121,12 @@ class ClockSampler:
     def __exit__(self, *exc):
         self._stop.set()
         self._t.join(timeout=10)
+        if self._nvml is not None:
+            try:
+                self._nvml_sample()  # the region's last instant
+                self._nvml.nvmlShutdown()
+            except Exception:
+                pass
 
     def summary(self):
         if not self.rows:

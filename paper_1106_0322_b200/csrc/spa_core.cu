@@ -282,14 +282,14 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const 
 // so the next row streams in while the current one is packed and no load
 // data lives in registers.  IT = kp/128 groups of 4 columns per lane.
 constexpr int kPackWarps = 8;
-constexpr int kPackSlots = 3;  // rows in flight per warp (current + 2 ahead)
+constexpr int kPackSlots = 2;  // rows in flight per warp (current + 1 ahead; 3 blocks per SM)
 
 __host__ __device__ inline size_t pack_eps_smem_bytes(int kp, int ldb) {
   return (size_t)16 * kp + (size_t)kPackWarps * kPackSlots * ((size_t)ldb * 6);
 }
 
 template <int IT>
-__global__ void __launch_bounds__(32 * kPackWarps) pack_eps_kernel(spa_design d, const float* __restrict__ beta,
+__global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design d, const float* __restrict__ beta,
                                                                 const __nv_bfloat16* __restrict__ eps, int64_t m,
                                                                 int ldb, __nv_bfloat16* __restrict__ A,
                                                                 double* __restrict__ ylin, PriorConst pc,
