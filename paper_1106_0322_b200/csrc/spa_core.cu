@@ -2090,12 +2090,9 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
   args.ncols = q;
   args.kp = kq;
   args.m_tiles = (int)((m + kTcBM - 1) / kTcBM);
-#ifndef SPA_PROP_TM
-#define SPA_PROP_TM 1
-#endif
-  // SPA_PROP_TM = 2: two 128-particle tiles per item share each L tile
-  // (halves the L2 -> SM traffic for L; measured slower, kept for A/B)
-  constexpr int kPropBN = SPA_PROP_TM == 1 ? 256 : 128;
+  // (two 128-particle tiles per item sharing each L tile, resident L, and one
+  // column tile per item were measured no faster: DESIGN.md section 9)
+  constexpr int kPropBN = 256;
   args.n_tiles = (q + kPropBN - 1) / kPropBN;
   args.tiles_per_unit = args.n_tiles;
   args.kb_per_unit = 0;
@@ -2105,8 +2102,8 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
                                         (uint64_t)m * ldb);
   if (rc) return rc;
   epi.m = (int)m;
-  rc = launch_tc<1, 1, kPropBN, EpiStoreT<__nv_bfloat16>, SPA_PROP_TM>(Z, (uint64_t)kq, Lb, (uint64_t)kq, (uint64_t)q,
-                                                                      args, 1, epi, st);
+  rc = launch_tc<1, 1, kPropBN, EpiStoreT<__nv_bfloat16>>(Z, (uint64_t)kq, Lb, (uint64_t)kq, (uint64_t)q, args, 1,
+                                                          epi, st);
   if (rc) return rc;
   auto* Ab = reinterpret_cast<__nv_bfloat16*>(A);
   const PriorConst pc = make_prior(a, c, c);
