@@ -67,6 +67,7 @@ __device__ __forceinline__ double mwg_gt(double b, const MwgParams& P) {
 // its value at sweep start).
 struct CoordSlot {
   double delta;   // beta_j' - beta_j (exact, float64)
+  double dsy;     // delta * (X^T y)_j (formed with the slot: off the per-coordinate critical path)
   double dlp;     // prior difference
   double logu;    // log of the MH uniform
   float newv;     // beta_j' (float32 state)
@@ -249,6 +250,7 @@ __global__ void __launch_bounds__(512) mwg_kernel(MwgParams P) {
       CoordSlot cs;
       cs.newv = nv;
       cs.delta = (double)nv - (double)old;
+      cs.dsy = cs.delta * P.d.sy[j];
       cs.logu = log(u);
       cs.dlp = P.d.penalized[j] ? (mwg_gt((double)nv, P) - mwg_gt((double)old, P)) : 0.0;
       if (CODED) {
@@ -295,7 +297,7 @@ __global__ void __launch_bounds__(512) mwg_kernel(MwgParams P) {
         tot = 0.0f;
         for (int w = 0; w < nw; ++w) tot += buf[w];
       }
-      const double dll = cs.delta * P.d.sy[j] - 0.6931471805599453 * (double)tot;
+      const double dll = cs.dsy - 0.6931471805599453 * (double)tot;
       const double d = dll + cs.dlp;
       const bool ok = (d >= 0.0) || (cs.logu < d);
       if (ok) {
