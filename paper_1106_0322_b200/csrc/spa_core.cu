@@ -594,6 +594,102 @@ __global__ void __launch_bounds__(256, 4) prior_reweight_rows_kernel(spa_design 
   }
 }
 
+// The rows kernel for the vector layout (q % 4 == 0, ldb % 4 == 0), lean:
+// no per-chunk overflow branch (the float64 running product of a lane's
+// factors 1 + |x| K >= 1 can only overflow to +inf, which one check per
+// lane at the end catches and recomputes as a sum of logs), the penalty flag
+// applied as a float32 multiply, and the per-lane penalised-column count and
+// the scale reciprocals formed once per block.  Same lane -> column map and
+// product order as the rows kernel: bit-identical to it whenever its
+// overflow branch does not fire (every product below 1e200).
+template <int LPR, int IT>
+__global__ void __launch_bounds__(256, IT >= 16 ? 3 : 4) prior_reweight_lean_kernel(spa_design d, const float* __restrict__ beta,
+                                                                  int64_t m, int ldb, PriorConst pc,
+                                                                  double* __restrict__ lw, double* __restrict__ lp) {
+  __shared__ __align__(16) float pen_s[LPR * IT * 4];  // 0/1 penalty flags, padding columns 0
+  __shared__ float npen_s[LPR];
+  __shared__ double k_s[2];
+  const int lane = threadIdx.x & 31, sub = lane % LPR;
+  const int64_t row = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (32 / LPR) + lane / LPR;
+  const bool live = row < m;
+  const float* b = beta + (live ? row : 0) * ldb;
+  // the row's loads go out first: their latency covers the block preamble
+  float4 xv[IT];
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const int j0 = (it * LPR + sub) * 4;
+    xv[it] = (live && j0 < d.q) ? __ldcs(reinterpret_cast<const float4*>(b + j0)) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (int j = threadIdx.x; j < LPR * IT * 4; j += blockDim.x) pen_s[j] = (j < d.q && d.penalized[j]) ? 1.f : 0.f;
+  if (threadIdx.x == 32) {
+    k_s[0] = pc.de ? 0.0 : 1.0 / (pc.a * pc.c);
+    k_s[1] = pc.de ? 0.0 : 1.0 / (pc.a * pc.c_prev);
+  }
+  __syncthreads();
+  if (threadIdx.x < LPR) {  // penalised columns of each lane slot (exact small-integer float sums)
+    float c = 0.f;
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const float4 pv = *reinterpret_cast<const float4*>(pen_s + (it * LPR + threadIdx.x) * 4);
+      c += (pv.x + pv.y) + (pv.z + pv.w);
+    }
+    npen_s[threadIdx.x] = c;
+  }
+  __syncthreads();
+  const double K1 = k_s[0], K2 = k_s[1];
+  const float npen = npen_s[sub];
+  double lpv, lwv;
+  if (pc.de) {
+    double lin = 0.0;
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const float4 pv = *reinterpret_cast<const float4*>(pen_s + (it * LPR + sub) * 4);
+      lin += ((double)(fabsf(xv[it].x) * pv.x) + (double)(fabsf(xv[it].y) * pv.y)) +
+             ((double)(fabsf(xv[it].z) * pv.z) + (double)(fabsf(xv[it].w) * pv.w));
+    }
+    lpv = (double)npen * pc.lc - lin / pc.c;
+    lwv = (double)npen * pc.lr - lin * (1.0 / pc.c - 1.0 / pc.c_prev);
+  } else {
+    double pa = 1.0, pb = 1.0;
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const float4 pv = *reinterpret_cast<const float4*>(pen_s + (it * LPR + sub) * 4);
+      const double x0 = (double)(fabsf(xv[it].x) * pv.x), x1 = (double)(fabsf(xv[it].y) * pv.y);
+      const double x2 = (double)(fabsf(xv[it].z) * pv.z), x3 = (double)(fabsf(xv[it].w) * pv.w);
+      pa *= fma(x0, K1, 1.0) * fma(x1, K1, 1.0) * (fma(x2, K1, 1.0) * fma(x3, K1, 1.0));
+      pb *= fma(x0, K2, 1.0) * fma(x1, K2, 1.0) * (fma(x2, K2, 1.0) * fma(x3, K2, 1.0));
+    }
+    double la, lb;
+    if (pa < 1e200 && pb < 1e200) {
+      la = log(pa);
+      lb = log(pb);
+    } else {  // a huge |beta|: the same factors as a sum of logs (row re-read)
+      la = lb = 0.0;
+#pragma unroll 1
+      for (int it = 0; it < IT; ++it) {
+#pragma unroll 1
+        for (int i = 0; i < 4; ++i) {
+          const int j = (it * LPR + sub) * 4 + i;
+          const double x = j < d.q ? (double)(fabsf(b[j]) * pen_s[j]) : 0.0;
+          la += log(fma(x, K1, 1.0));
+          lb += log(fma(x, K2, 1.0));
+        }
+      }
+    }
+    lpv = (double)npen * pc.lc - (pc.a + 1.0) * la;
+    lwv = (double)npen * pc.lr - (pc.a + 1.0) * (la - lb);
+  }
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) {
+    lpv += __shfl_xor_sync(0xffffffffu, lpv, o);
+    lwv += __shfl_xor_sync(0xffffffffu, lwv, o);
+  }
+  if (live && sub == 0) {
+    lw[row] = lwv;
+    lp[row] = lpv;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // f1: per-step weighted marginal summaries (reference summary.py:36-61) on
 // the device -- weighted mean, weighted quantiles ("smallest value whose
@@ -1783,7 +1879,16 @@ int spa_prior_reweight(const spa_design* d, const float* beta, int64_t m, int32_
   const PriorConst pc = make_prior(a, c, c_prev);
   cudaStream_t st = as_stream(stream);
   const unsigned grid = (unsigned)cdiv(m, 8);
-  if (d->kp <= 128)
+  if (d->q % 4 == 0 && ldb % 4 == 0 && d->kp <= 1024) {
+    if (d->kp <= 128)
+      prior_reweight_lean_kernel<8, 4><<<(unsigned)cdiv(m, 32), 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);
+    else if (d->kp <= 256)
+      prior_reweight_lean_kernel<8, 8><<<(unsigned)cdiv(m, 32), 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);
+    else if (d->kp <= 512)
+      prior_reweight_lean_kernel<16, 8><<<(unsigned)cdiv(m, 16), 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);
+    else
+      prior_reweight_lean_kernel<16, 16><<<(unsigned)cdiv(m, 16), 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);
+  } else if (d->kp <= 128)
     prior_reweight_rows_kernel<8, 4><<<(unsigned)cdiv(m, 32), 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);
   else if (d->kp <= 256)
     prior_reweight_rows_kernel<8, 8><<<(unsigned)cdiv(m, 32), 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);

@@ -141,6 +141,34 @@ def test_prior_reweight_fused(gold_loglik, a):
     np.testing.assert_allclose(lw.cpu().numpy(), orc.reweight_increments(Bf, a, c, c_prev), rtol=1e-9, atol=1e-10)
 
 
+@pytest.mark.parametrize("q", [20, 200, 500, 1000])
+def test_prior_reweight_wide_and_huge(q):
+    """The vector-layout reweight kernels (one per q band) against the oracle,
+    with rows of huge |beta| whose per-lane float64 product overflows and
+    takes the sum-of-logs path (smc.py:248-263 semantics either way)."""
+    from paper_1106_0322_b200.design import DeviceDesign
+    from paper_1106_0322_b200.smc import ParticleSystem
+
+    rng = np.random.default_rng(q)
+    n, N, a, c, c_prev = 64, 96, 1.0, 0.6, 0.7
+    X = rng.integers(0, 3, size=(n, q)).astype(np.float64)
+    X = (X - X.mean(0)) / np.where(X.std(0) > 0, X.std(0), 1.0)
+    y = (rng.random(n) < 0.5).astype(np.float64)
+    B = rng.normal(0.0, 0.3, size=(N, q))
+    B[::7] *= 1e12  # factors ~1e12: a lane's product overflows past 1e200
+    B[3, :5] = 3e38
+    d = DeviceDesign.build(X, y, False)
+    s = ParticleSystem(d, N, a, False)
+    s.load_betas(B)
+    lw = torch.empty(N, dtype=torch.float64, device="cuda")
+    lp = torch.empty_like(lw)
+    _lib.call("spa_prior_reweight", ctypes.byref(d.struct), _p(s.beta), N, s.ldb, a, c, c_prev, _p(lw), _p(lp),
+              _stream())
+    Bf = B.astype(np.float32).astype(np.float64)
+    np.testing.assert_allclose(lw.cpu().numpy(), orc.reweight_increments(Bf, a, c, c_prev), rtol=1e-11, atol=1e-9)
+    np.testing.assert_allclose(lp.cpu().numpy(), orc.log_prior_rows(Bf, a, c), rtol=1e-12)
+
+
 def test_reweight_and_ess(gold_reweight, gold_loglik):
     from paper_1106_0322_b200 import GtPrior, ess, reweight
 
