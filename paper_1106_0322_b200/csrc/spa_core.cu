@@ -2201,6 +2201,7 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
   args.n_tiles = (q + kPropBN - 1) / kPropBN;
   args.tiles_per_unit = args.n_tiles;
   args.kb_per_unit = 0;
+  args.tri_b = 1;  // L is lower triangular: column tile nt needs k < (nt + 1) BN only
   auto* epsb = reinterpret_cast<__nv_bfloat16*>(eps);
   EpiStoreT<__nv_bfloat16> epi{};
   int rc = make_tmap_out<__nv_bfloat16>(&epi.tmc, epsb, (uint64_t)q, (uint64_t)m, 1, (uint64_t)ldb,

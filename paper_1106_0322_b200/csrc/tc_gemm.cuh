@@ -54,6 +54,8 @@ struct TcArgs {
   int tiles_per_unit;  // BN tiles per CTA (column split), or
   int kb_per_unit;     // > 0: split-K -- a CTA covers all BN tiles over this many k-blocks
   int units;           // column (or K) units per A tile; work items = m_tiles * units
+  int tri_b = 0;       // 1: B[n][k] is lower triangular (k <= n), so column tile nt stops at
+                       // k-block ceil((nt + 1) BN / BK) -- the zero upper part is never loaded
 };
 
 // (the epilogue contract is documented with the epilogues below)
@@ -141,7 +143,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       int mt, unit, nt0, nt1, kb0, kb1;
       item_range(w, mt, unit, nt0, nt1, kb0, kb1);
       for (int nt = nt0; nt < nt1; ++nt) {
-        for (int kb = kb0; kb < kb1; ++kb) {
+        const int kbe = args.tri_b ? min(kb1, ((nt + 1) * BN + kTcBK - 1) / kTcBK) : kb1;
+        for (int kb = kb0; kb < kbe; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + s * S::kStageBytes;
           mbar_arrive_expect_tx(&full[s], S::kStageBytes);
@@ -178,7 +181,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const uint32_t bph = (it >> 1) & 1;
         mbar_wait(&tempty[buf], bph ^ 1);
         tc_fence_after();
-        for (int kb = kb0; kb < kb1; ++kb) {
+        const int kbe = args.tri_b ? min(kb1, ((nt + 1) * BN + kTcBK - 1) / kTcBK) : kb1;
+        for (int kb = kb0; kb < kbe; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t st = smem_u32(smem + s * S::kStageBytes);
