@@ -338,7 +338,11 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
     __nv_bfloat16* ah = A + row * (2 * (int64_t)d.kp);
     __nv_bfloat16* al = ah + d.kp;
     double yl = 0.0, off = 0.0;  // same grouping as pack_kernel => identical sums
-    LpAcc la;
+    // log-prior: the LpAcc product order without its per-chunk overflow
+    // branch (factors are >= 1, so the running product can only overflow
+    // upwards; one check per lane below), the flag applied as a multiply
+    double prod = 1.0, lin = 0.0;
+    float npen = 0.f;
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
       const int j0 = it * 128 + lane * 4;
@@ -374,11 +378,38 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
         fy = fmaf(p[i], s4[i], fy);
         fo = fmaf(p[i], g4[i], fo);
       }
-      la.add4(p, p4, K, pc.de);
+      {
+        npen += (p4[0] + p4[1]) + (p4[2] + p4[3]);
+        const double x0 = (double)(fabsf(p[0]) * p4[0]), x1 = (double)(fabsf(p[1]) * p4[1]);
+        const double x2 = (double)(fabsf(p[2]) * p4[2]), x3 = (double)(fabsf(p[3]) * p4[3]);
+        if (pc.de)
+          lin += (x0 + x1) + (x2 + x3);
+        else
+          prod *= fma(x0, K, 1.0) * fma(x1, K, 1.0) * (fma(x2, K, 1.0) * fma(x3, K, 1.0));
+      }
       yl += fy;
       off += fo;
       __stcs(reinterpret_cast<uint2*>(ah + j0), *reinterpret_cast<const uint2*>(h));
       __stcs(reinterpret_cast<uint2*>(al + j0), *reinterpret_cast<const uint2*>(l));
+    }
+    double lpl;
+    if (pc.de) {
+      lpl = (double)npen * pc.lc - lin / pc.c;
+    } else {
+      double lsum;
+      if (prod < 1e200) {
+        lsum = log(prod);
+      } else {  // a huge |beta + eps|: the same factors as a sum of logs
+        lsum = 0.0;
+#pragma unroll 1
+        for (int j = lane * 4; j < d.q; j += 128)
+#pragma unroll 1
+          for (int i = j; i < j + 4 && i < d.q; ++i) {
+            const double x = (double)(fabsf(b[i] + __bfloat162float(e[i])) * cp[i]);
+            lsum += log(fma(x, K, 1.0));
+          }
+      }
+      lpl = (double)npen * pc.lc - (pc.a + 1.0) * lsum;
     }
     __syncwarp();  // every lane is done with slot s: refill it
     if (lane == 0) {
@@ -387,7 +418,7 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
     }
     yl = warp_sum(yl);
     off = warp_sum(off);
-    const double lps = warp_sum(la.value(pc));
+    const double lps = warp_sum(lpl);
     if (lane == 0) {
       ylin[row] = yl;
       if (lp != nullptr) lp[row] = lps;
