@@ -434,6 +434,166 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
   }
 }
 
+// pack_eps with R = 32 / LPR particle rows per warp iteration (LPR lanes per
+// row, lane l of a row takes columns 4 (it LPR + l) .. +3): the per-row
+// overhead -- the ring wait, three reductions, the log, the row's scalar
+// stores -- is shared by R rows, which halves it at LPR = 16.  A hi/lo are
+// the same bits as pack_eps_kernel; ylin / lp / the offset are summed in a
+// different order (float64 rounding).
+template <int IT, int LPR>
+__global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
+    spa_design d, const float* __restrict__ beta, const __nv_bfloat16* __restrict__ eps, int64_t m, int ldb,
+    __nv_bfloat16* __restrict__ A, double* __restrict__ ylin, PriorConst pc, double* __restrict__ lp) {
+  constexpr int R = 32 / LPR;
+  extern __shared__ float4 csm[];  // [kp] x {alpha, sy, gamma, pen}, then the row rings
+  __shared__ uint64_t bars[kPackWarps][kPackSlots];
+  float* ca = reinterpret_cast<float*>(csm);
+  float* cs = ca + d.kp;
+  float* cg = cs + d.kp;
+  float* cp = cg + d.kp;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, sub = lane % LPR, rsub = lane / LPR;
+  const uint32_t rowB = (uint32_t)ldb * 4, slotB = (uint32_t)ldb * 6, groupB = slotB * R;
+  uint8_t* ring = reinterpret_cast<uint8_t*>(cp + d.kp) + (size_t)warp * kPackSlots * groupB;
+  for (int j = threadIdx.x; j < d.kp; j += blockDim.x) {
+    const bool v = j < d.q;
+    ca[j] = v ? (d.coded ? (float)d.alpha[j] : 1.0f) : 0.f;
+    cs[j] = v ? (float)d.sy[j] : 0.f;
+    cg[j] = (v && d.coded) ? (float)d.gamma[j] : 0.f;
+    cp[j] = (v && d.penalized[j]) ? 1.f : 0.f;
+  }
+  if (lane == 0) {
+    for (int sl = 0; sl < kPackSlots; ++sl) mbar_init(&bars[warp][sl], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int64_t ngroups = (m + R - 1) / R;
+  const int64_t warp0 = (int64_t)blockIdx.x * kPackWarps + warp;
+  const int64_t nwarps = (int64_t)gridDim.x * kPackWarps;
+  auto issue = [&](int64_t g, int s) {
+    if (g < ngroups) {
+      const int nr = (m - g * R) < R ? (int)(m - g * R) : R;
+      mbar_arrive_expect_tx(&bars[warp][s], slotB * nr);
+      for (int r = 0; r < nr; ++r) {
+        const int64_t row = g * R + r;
+        uint8_t* dst = ring + s * groupB + r * slotB;
+        bulk_g2s(dst, beta + row * ldb, rowB, &bars[warp][s]);
+        bulk_g2s(dst + rowB, eps + row * ldb, slotB - rowB, &bars[warp][s]);
+      }
+    }
+  };
+  if (lane == 0)
+    for (int sl = 0; sl < kPackSlots; ++sl) issue(warp0 + sl * nwarps, sl);
+  const double K = pc.de ? 0.0 : 1.0 / (pc.a * pc.c);
+  const bool full = (d.q % 4 == 0);  // every 4-column group is either all-valid or all-padding
+  uint32_t phase = 0;                // bit s = parity of slot s
+  int s = 0;
+  for (int64_t g = warp0; g < ngroups; g += nwarps, s = (s + 1 == kPackSlots) ? 0 : s + 1) {
+    mbar_wait(&bars[warp][s], (phase >> s) & 1u);
+    phase ^= 1u << s;
+    const int64_t row = g * R + rsub;
+    const bool live = row < m;
+    const float* b = reinterpret_cast<const float*>(ring + s * groupB + rsub * slotB);
+    const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(ring + s * groupB + rsub * slotB + rowB);
+    __nv_bfloat16* ah = A + (live ? row : 0) * (2 * (int64_t)d.kp);
+    __nv_bfloat16* al = ah + d.kp;
+    double yl = 0.0, off = 0.0, prod = 1.0, lin = 0.0;
+    float npen = 0.f;
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int j0 = (it * LPR + sub) * 4;
+      if (j0 >= d.kp) break;
+      float fy = 0.f, fo = 0.f;
+      float p[4] = {0.f, 0.f, 0.f, 0.f};
+      if (live) {
+        if (full && j0 + 4 <= d.q) {
+          const float4 xv = *reinterpret_cast<const float4*>(b + j0);
+          const uint2 ev = *reinterpret_cast<const uint2*>(e + j0);
+          const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&ev);
+          const float2 ya = __bfloat1622float2(y2[0]), yb = __bfloat1622float2(y2[1]);
+          p[0] = xv.x + ya.x;
+          p[1] = xv.y + ya.y;
+          p[2] = xv.z + yb.x;
+          p[3] = xv.w + yb.y;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (j0 + i < d.q) p[i] = b[j0 + i] + __bfloat162float(e[j0 + i]);
+        }
+      }
+      const float4 va = *reinterpret_cast<const float4*>(ca + j0);
+      const float4 vs = *reinterpret_cast<const float4*>(cs + j0);
+      const float4 vg = *reinterpret_cast<const float4*>(cg + j0);
+      const float4 vp = *reinterpret_cast<const float4*>(cp + j0);
+      const float a4[4] = {va.x, va.y, va.z, va.w}, s4[4] = {vs.x, vs.y, vs.z, vs.w};
+      const float g4[4] = {vg.x, vg.y, vg.z, vg.w}, p4[4] = {vp.x, vp.y, vp.z, vp.w};
+      __align__(8) __nv_bfloat16 h[4], l[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float bs = a4[i] * p[i];
+        h[i] = __float2bfloat16_rn(bs);
+        l[i] = __float2bfloat16_rn(bs - __bfloat162float(h[i]));
+        fy = fmaf(p[i], s4[i], fy);
+        fo = fmaf(p[i], g4[i], fo);
+      }
+      npen += (p4[0] + p4[1]) + (p4[2] + p4[3]);
+      const double x0 = (double)(fabsf(p[0]) * p4[0]), x1 = (double)(fabsf(p[1]) * p4[1]);
+      const double x2 = (double)(fabsf(p[2]) * p4[2]), x3 = (double)(fabsf(p[3]) * p4[3]);
+      if (pc.de)
+        lin += (x0 + x1) + (x2 + x3);
+      else
+        prod *= fma(x0, K, 1.0) * fma(x1, K, 1.0) * (fma(x2, K, 1.0) * fma(x3, K, 1.0));
+      yl += fy;
+      off += fo;
+      if (live) {
+        __stcs(reinterpret_cast<uint2*>(ah + j0), *reinterpret_cast<const uint2*>(h));
+        __stcs(reinterpret_cast<uint2*>(al + j0), *reinterpret_cast<const uint2*>(l));
+      }
+    }
+    double lpl;
+    if (pc.de) {
+      lpl = (double)npen * pc.lc - lin / pc.c;
+    } else {
+      double lsum;
+      if (prod < 1e200) {
+        lsum = log(prod);
+      } else {  // a huge |beta + eps|: the same factors as a sum of logs
+        lsum = 0.0;
+#pragma unroll 1
+        for (int j = sub * 4; j < d.q; j += LPR * 4)
+#pragma unroll 1
+          for (int i = j; i < j + 4 && i < d.q; ++i) {
+            const double x = (double)(fabsf(b[i] + __bfloat162float(e[i])) * cp[i]);
+            lsum += log(fma(x, K, 1.0));
+          }
+      }
+      lpl = (double)npen * pc.lc - (pc.a + 1.0) * lsum;
+    }
+    __syncwarp();  // every lane is done with slot s: refill it
+    if (lane == 0) {
+      fence_proxy_async_smem();
+      issue(g + kPackSlots * nwarps, s);
+    }
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) {
+      yl += __shfl_xor_sync(0xffffffffu, yl, o);
+      off += __shfl_xor_sync(0xffffffffu, off, o);
+      lpl += __shfl_xor_sync(0xffffffffu, lpl, o);
+    }
+    if (live && sub == 0) {
+      ylin[row] = yl;
+      if (lp != nullptr) lp[row] = lpl;
+      if (d.coded) {
+        const __nv_bfloat16 o1 = __double2bfloat16(off);
+        const double r1 = off - (double)__bfloat162float(o1);
+        const __nv_bfloat16 o2 = __double2bfloat16(r1);
+        ah[d.q] = o1;
+        ah[d.q + 1] = o2;
+        ah[d.q + 2] = __double2bfloat16(r1 - (double)__bfloat162float(o2));
+      }
+    }
+  }
+}
+
 __global__ void prior_kernel(spa_design d, const float* __restrict__ beta, int64_t m, int ldb, PriorConst pc,
                              int mode, double* __restrict__ out) {
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -2257,6 +2417,22 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
     SPA_CHECK_LAUNCH();
     return 0;
   };
+  // 2 rows per warp iteration where the doubled ring still fits 2 blocks per SM
+  if (d->kp > 128 && d->kp <= 512) {
+    const size_t sm2 = (size_t)16 * d->kp + (size_t)kPackWarps * kPackSlots * 2 * ((size_t)ldb * 6);
+    auto kern = d->kp <= 256 ? pack_eps_rows_kernel<4, 16> : pack_eps_rows_kernel<8, 16>;
+    SPA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+    int per_sm = 0, dev = 0, nsm = 0;
+    SPA_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kPackWarps, sm2));
+    SPA_CHECK_CUDA(cudaGetDevice(&dev));
+    SPA_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    if (per_sm > 0) {
+      const unsigned grid = std::min<unsigned>(cdiv(cdiv(m, 2), kPackWarps), (unsigned)(per_sm * nsm));
+      kern<<<grid, 32 * kPackWarps, sm2, st>>>(*d, beta, epsb, m, ldb, Ab, ylin, pc, lp);
+      SPA_CHECK_LAUNCH();
+      return 0;
+    }
+  }
   if (d->kp <= 128) return run(pack_eps_kernel<1>);
   if (d->kp <= 256) return run(pack_eps_kernel<2>);
   if (d->kp <= 512) return run(pack_eps_kernel<4>);
