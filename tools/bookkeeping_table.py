@@ -27,16 +27,17 @@ for i, m in per.items():
         a[idx] += v * scale[u] / 1e6
 N, q, ldb, kp = 65536, 500, 512, 512
 alg = {  # algorithmic MB per launch
-    "pack_eps_kernel": (N * ldb * 4 + N * ldb * 2 + N * 2 * kp * 2) / 1e6,   # beta + eps read, A hi/lo written
+    "pack_eps": (N * ldb * 4 + N * ldb * 2 + N * 2 * kp * 2) / 1e6,   # beta + eps read, A hi/lo written
     "rw_center_kernel": (N * ldb * 4 + q * N * 2) / 1e6,                      # beta read, Dt written
     "EpiStoreT<__nv_bfloat16>": (N * 512 * 2 + N * ldb * 2) / 1e6,            # z read, eps written
-    "prior_reweight_rows_kernel": (N * ldb * 4) / 1e6,                        # beta read
+    "prior_reweight": (N * ldb * 4) / 1e6,                                    # beta read
     # decision scalars of every row + beta/eps read and beta written for the
     # accepted rows, at the C3 acceptance rate of the profiled step (0.256)
     "rw_accept_kernel": (N * 5 * 8 + 0.256 * N * (ldb * 4 + ldb * 2 + ldb * 4)) / 1e6,
     "rw_normals_kernel": (N * 512 * 2) / 1e6,                                 # z written
 }
-label = {"EpiStoreT<__nv_bfloat16>": "propose GEMM (L z, TMA store)"}
+label = {"EpiStoreT<__nv_bfloat16>": "propose GEMM (L z, TMA store)", "pack_eps": "pack_eps_rows",
+         "prior_reweight": "prior_reweight_lean"}
 peak = 6556.0
 print("# Bookkeeping / bandwidth kernels of one C3 lambda step (bench.py --profile --steps 1, ncu")
 print("# gpu__time_duration.sum + dram__bytes_read/write.sum, --clock-control none; serialised, cold cache).")
@@ -59,8 +60,8 @@ for name, (n, t, rd, wr) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
 print()
 print("# accept: algorithmic bytes are data dependent (decision scalars for all rows, beta/eps read and beta")
 print("# written for the accepted rows only, at the step's acceptance rate 0.256); its beta writes stay in L2.")
-print("# propose GEMM: also tensor work, 2*N*kq*kq = 34.4 GFLOP per launch (0.65 of the 1385 TFLOP/s peak")
-print("# at 38.4 us).")
+print("# propose GEMM: also tensor work, the lower triangle of L only: 0.75 * 2*N*kq*kq = 25.8 GFLOP per")
+print("# launch at q = 500 (0.55 of the 1385 TFLOP/s peak at 34 us).")
 print("# normals: compute-bound (Philox4x32-10 + Box-Muller); its bytes are the 67 MB bf16 output.")
 print("# centre pass and propose GEMM outputs stay largely in L2 (read by the next kernel): DRAM writes")
 print("# are below the algorithmic bytes.")
