@@ -1771,10 +1771,19 @@ __global__ void __launch_bounds__(256) rw_center_kernel(const float* __restrict_
   float c[4], d[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int i = 0; i < 4; ++i) c[i] = (j + i < q) ? center[j + i] : 0.f;
+  // lane cq < 8 of each half-warp forms the weight scalars of particle kb + cq
+  // once (the float64 sqrt is the costly part); shuffles hand them to the
+  // 16 lanes of the half-warp
+  float wf_own = 0.f, sf_own = 0.f;
+  if (cq < 8) {
+    const double wd = (kb + cq < m) ? w[kb + cq] : 0.0;
+    wf_own = (float)wd;
+    sf_own = (float)sqrt(wd);
+  }
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
-    const double wd = (kb + r < m) ? w[kb + r] : 0.0;
-    const float wf = (float)wd, sf = (float)sqrt(wd);
+    const float wf = __shfl_sync(0xffffffffu, wf_own, 16 * pg + r);
+    const float sf = __shfl_sync(0xffffffffu, sf_own, 16 * pg + r);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const float v = x[r][i] - c[i];
