@@ -120,6 +120,7 @@ struct PriorConst {
   double lc;  // -log(2c)
   double lr;  // log(c_prev / c)
   int de;     // a = +inf: double exponential
+  double k, k_prev;  // 1 / (a c), 1 / (a c_prev) (0 for de); the same IEEE division as on the device
 };
 
 __device__ __forceinline__ double gt_logpdf(double b, const PriorConst& p) {
@@ -785,58 +786,59 @@ __global__ void __launch_bounds__(256, 4) prior_reweight_rows_kernel(spa_design 
   }
 }
 
-// The rows kernel for the vector layout (q % 4 == 0, ldb % 4 == 0), lean:
-// no per-chunk overflow branch (the float64 running product of a lane's
-// factors 1 + |x| K >= 1 can only overflow to +inf, which one check per
-// lane at the end catches and recomputes as a sum of logs), the penalty flag
-// applied as a float32 multiply, and the per-lane penalised-column count and
-// the scale reciprocals formed once per block.  Same lane -> column map and
-// product order as the rows kernel: bit-identical to it whenever its
-// overflow branch does not fire (every product below 1e200).
+// The rows kernel for the vector layout (q % 4 == 0, ldb % 4 == 0, a
+// 4-byte aligned penalty mask), lean: no per-chunk overflow branch (the
+// float64 running product of a lane's factors 1 + |x| K >= 1 can only
+// overflow to +inf, which one check per lane at the end catches and
+// recomputes as a sum of logs), and no block preamble -- each lane reads the
+// 0/1 penalty bytes of its 4 columns as one word (a byte-replicated mask
+// zeroes unpenalised columns; popc counts the penalised ones) and the scale
+// reciprocals come from the host.  Same lane -> column map and product order
+// as the rows kernel: bit-identical to it whenever its overflow branch does
+// not fire (every product below 1e200).
 template <int LPR, int IT>
 __global__ void __launch_bounds__(256, IT >= 16 ? 3 : 4) prior_reweight_lean_kernel(spa_design d, const float* __restrict__ beta,
                                                                   int64_t m, int ldb, PriorConst pc,
                                                                   double* __restrict__ lw, double* __restrict__ lp) {
-  __shared__ __align__(16) float pen_s[LPR * IT * 4];  // 0/1 penalty flags, padding columns 0
-  __shared__ float npen_s[LPR];
-  __shared__ double k_s[2];
   const int lane = threadIdx.x & 31, sub = lane % LPR;
   const int64_t row = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (32 / LPR) + lane / LPR;
   const bool live = row < m;
   const float* b = beta + (live ? row : 0) * ldb;
-  // the row's loads go out first: their latency covers the block preamble
+  // the mask words are loaded with the row when registers allow (IT <= 8),
+  // else next to their use (L1 hits after the first warps)
+  constexpr bool kEager = IT <= 8;
   float4 xv[IT];
+  uint32_t pw[kEager ? IT : 1];
+  auto mask_word = [&](int it) -> uint32_t {
+    const int j0 = (it * LPR + sub) * 4;
+    return j0 < d.q ? __ldg(reinterpret_cast<const uint32_t*>(d.penalized + j0)) : 0u;
+  };
 #pragma unroll
   for (int it = 0; it < IT; ++it) {
     const int j0 = (it * LPR + sub) * 4;
-    xv[it] = (live && j0 < d.q) ? __ldcs(reinterpret_cast<const float4*>(b + j0)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool v = live && j0 < d.q;
+    xv[it] = v ? __ldcs(reinterpret_cast<const float4*>(b + j0)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (kEager) pw[kEager ? it : 0] = mask_word(it);
   }
-  for (int j = threadIdx.x; j < LPR * IT * 4; j += blockDim.x) pen_s[j] = (j < d.q && d.penalized[j]) ? 1.f : 0.f;
-  if (threadIdx.x == 32) {
-    k_s[0] = pc.de ? 0.0 : 1.0 / (pc.a * pc.c);
-    k_s[1] = pc.de ? 0.0 : 1.0 / (pc.a * pc.c_prev);
-  }
-  __syncthreads();
-  if (threadIdx.x < LPR) {  // penalised columns of each lane slot (exact small-integer float sums)
-    float c = 0.f;
-#pragma unroll
-    for (int it = 0; it < IT; ++it) {
-      const float4 pv = *reinterpret_cast<const float4*>(pen_s + (it * LPR + threadIdx.x) * 4);
-      c += (pv.x + pv.y) + (pv.z + pv.w);
-    }
-    npen_s[threadIdx.x] = c;
-  }
-  __syncthreads();
-  const double K1 = k_s[0], K2 = k_s[1];
-  const float npen = npen_s[sub];
+  const double K1 = pc.k, K2 = pc.k_prev;
+  int npen = 0;
   double lpv, lwv;
+  auto masked = [&](const float4& x, uint32_t w, double (&o)[4]) {
+    const uint32_t mk = (w * 0xffu);  // 0x01 -> 0xff per byte (flags are 0/1: no carries)
+    o[0] = (double)__uint_as_float(__float_as_uint(fabsf(x.x)) & __byte_perm(mk, 0, 0x8888));
+    o[1] = (double)__uint_as_float(__float_as_uint(fabsf(x.y)) & __byte_perm(mk, 0, 0x9999));
+    o[2] = (double)__uint_as_float(__float_as_uint(fabsf(x.z)) & __byte_perm(mk, 0, 0xaaaa));
+    o[3] = (double)__uint_as_float(__float_as_uint(fabsf(x.w)) & __byte_perm(mk, 0, 0xbbbb));
+  };
   if (pc.de) {
     double lin = 0.0;
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
-      const float4 pv = *reinterpret_cast<const float4*>(pen_s + (it * LPR + sub) * 4);
-      lin += ((double)(fabsf(xv[it].x) * pv.x) + (double)(fabsf(xv[it].y) * pv.y)) +
-             ((double)(fabsf(xv[it].z) * pv.z) + (double)(fabsf(xv[it].w) * pv.w));
+      double x[4];
+      const uint32_t w = kEager ? pw[kEager ? it : 0] : mask_word(it);
+      masked(xv[it], w, x);
+      npen += __popc(w);
+      lin += (x[0] + x[1]) + (x[2] + x[3]);
     }
     lpv = (double)npen * pc.lc - lin / pc.c;
     lwv = (double)npen * pc.lr - lin * (1.0 / pc.c - 1.0 / pc.c_prev);
@@ -844,11 +846,12 @@ __global__ void __launch_bounds__(256, IT >= 16 ? 3 : 4) prior_reweight_lean_ker
     double pa = 1.0, pb = 1.0;
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
-      const float4 pv = *reinterpret_cast<const float4*>(pen_s + (it * LPR + sub) * 4);
-      const double x0 = (double)(fabsf(xv[it].x) * pv.x), x1 = (double)(fabsf(xv[it].y) * pv.y);
-      const double x2 = (double)(fabsf(xv[it].z) * pv.z), x3 = (double)(fabsf(xv[it].w) * pv.w);
-      pa *= fma(x0, K1, 1.0) * fma(x1, K1, 1.0) * (fma(x2, K1, 1.0) * fma(x3, K1, 1.0));
-      pb *= fma(x0, K2, 1.0) * fma(x1, K2, 1.0) * (fma(x2, K2, 1.0) * fma(x3, K2, 1.0));
+      double x[4];
+      const uint32_t w = kEager ? pw[kEager ? it : 0] : mask_word(it);
+      masked(xv[it], w, x);
+      npen += __popc(w);
+      pa *= fma(x[0], K1, 1.0) * fma(x[1], K1, 1.0) * (fma(x[2], K1, 1.0) * fma(x[3], K1, 1.0));
+      pb *= fma(x[0], K2, 1.0) * fma(x[1], K2, 1.0) * (fma(x[2], K2, 1.0) * fma(x[3], K2, 1.0));
     }
     double la, lb;
     if (pa < 1e200 && pb < 1e200) {
@@ -861,7 +864,7 @@ __global__ void __launch_bounds__(256, IT >= 16 ? 3 : 4) prior_reweight_lean_ker
 #pragma unroll 1
         for (int i = 0; i < 4; ++i) {
           const int j = (it * LPR + sub) * 4 + i;
-          const double x = j < d.q ? (double)(fabsf(b[j]) * pen_s[j]) : 0.0;
+          const double x = (j < d.q && d.penalized[j]) ? (double)fabsf(b[j]) : 0.0;
           la += log(fma(x, K1, 1.0));
           lb += log(fma(x, K2, 1.0));
         }
@@ -2038,6 +2041,8 @@ static PriorConst make_prior(double a, double c, double c_prev) {
   p.lc = -std::log(2.0 * c);
   p.lr = std::log(c_prev / c);
   p.de = std::isinf(a) ? 1 : 0;
+  p.k = p.de ? 0.0 : 1.0 / (a * c);
+  p.k_prev = p.de ? 0.0 : 1.0 / (a * c_prev);
   return p;
 }
 
@@ -2079,7 +2084,7 @@ int spa_prior_reweight(const spa_design* d, const float* beta, int64_t m, int32_
   const PriorConst pc = make_prior(a, c, c_prev);
   cudaStream_t st = as_stream(stream);
   const unsigned grid = (unsigned)cdiv(m, 8);
-  if (d->q % 4 == 0 && ldb % 4 == 0 && d->kp <= 1024) {
+  if (d->q % 4 == 0 && ldb % 4 == 0 && d->kp <= 1024 && ((uintptr_t)d->penalized & 3) == 0) {
     if (d->kp <= 128)
       prior_reweight_lean_kernel<8, 4><<<(unsigned)cdiv(m, 32), 256, 0, st>>>(*d, beta, m, ldb, pc, lw, lp);
     else if (d->kp <= 256)
