@@ -219,7 +219,8 @@ int spa_rw_normals(int64_t m, int32_t q, uint64_t seed, int64_t t, int64_t i0, i
  * exactly symmetric --, coalesced through an smem transpose); then one
  * vectorised pass packs prop = beta + eps into the K1 operand A and emits
  * ylin and lp at c.  `Lb` is the bf16 operand written by spa_rw_factor
- * (lower triangular: its upper part is never read);
+ * (lower triangular with zeros above the diagonal, as that call writes it: K blocks
+ * wholly above a 256-column output tile are skipped);
  * seed/t/i0/move are unused (kept for ABI stability). */
 int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ldb, const void* Lb, uint64_t seed,
                    int64_t t, int64_t i0, int32_t move, void* zbuf, void* eps, void* A, double* ylin, double a,
