@@ -1314,9 +1314,12 @@ __global__ void gather_kernel(const float* __restrict__ src, int ld_src, float* 
                               const int64_t* __restrict__ idx, int64_t base, int64_t m, const double* __restrict__ v0,
                               double* __restrict__ v0o, const double* __restrict__ v1, double* __restrict__ v1o,
                               const double* __restrict__ gate) {
-  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // grid-stride over rows with a capped grid: a gated-off launch (most
+  // steps) retires a few hundred blocks instead of one per 8 rows
+  if (gated_off(gate)) return;
   const int lane = threadIdx.x & 31;
-  if (row >= m || gated_off(gate)) return;
+  const int64_t stride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < m; row += stride) {
   const int64_t s = idx[row] - base;
   const float* a = src + s * ld_src;
   float* o = dst + row * ld_dst;
@@ -1330,6 +1333,7 @@ __global__ void gather_kernel(const float* __restrict__ src, int ld_src, float* 
   if (lane == 0) {
     if (v0) v0o[row] = v0[s];
     if (v1) v1o[row] = v1[s];
+  }
   }
 }
 
@@ -1353,9 +1357,10 @@ __global__ void resample_commit_kernel(const float* __restrict__ beta_alt, float
                                        const double* __restrict__ lp_alt, double* __restrict__ lp,
                                        double* __restrict__ logw, double logw0, int64_t m,
                                        const double* __restrict__ gate) {
-  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (gated_off(gate)) return;
   const int lane = threadIdx.x & 31;
-  if (row >= m || gated_off(gate)) return;
+  const int64_t stride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < m; row += stride) {
   const float* a = beta_alt + row * ldb;
   float* o = beta + row * ldb;
   if ((ldb & 3) == 0) {
@@ -1369,6 +1374,7 @@ __global__ void resample_commit_kernel(const float* __restrict__ beta_alt, float
     ll[row] = ll_alt[row];
     lp[row] = lp_alt[row];
     logw[row] = logw0;
+  }
   }
 }
 
@@ -2224,7 +2230,7 @@ int spa_gather_rows(const float* src, int32_t ld_src, float* dst, int32_t ld_dst
                     void* stream) {
   SPA_REQUIRE(src && dst && idx && m >= 0 && q > 0, kBadArgument, "spa_gather_rows: bad arguments");
   if (m == 0) return 0;
-  gather_kernel<<<cdiv(m, 8), 256, 0, as_stream(stream)>>>(src, ld_src, dst, ld_dst, q, idx, base, m, v0, v0_out, v1,
+  gather_kernel<<<std::min<unsigned>(cdiv(m, 8), 8 * 148), 256, 0, as_stream(stream)>>>(src, ld_src, dst, ld_dst, q, idx, base, m, v0, v0_out, v1,
                                                           v1_out, nullptr);
   SPA_CHECK_LAUNCH();
   return 0;
@@ -2250,9 +2256,9 @@ int spa_resample_gated(const double* gate, const double* w, int64_t N, double u,
   SPA_CHECK_LAUNCH();
   ancestors_kernel<<<cdiv(N, 256), 256, 0, st>>>(cum, N, u, 0, N, anc, gate);
   SPA_CHECK_LAUNCH();
-  gather_kernel<<<cdiv(N, 8), 256, 0, st>>>(beta, ldb, beta_alt, ldb, q, anc, 0, N, ll, ll_alt, lp, lp_alt, gate);
+  gather_kernel<<<std::min<unsigned>(cdiv(N, 8), 8 * 148), 256, 0, st>>>(beta, ldb, beta_alt, ldb, q, anc, 0, N, ll, ll_alt, lp, lp_alt, gate);
   SPA_CHECK_LAUNCH();
-  resample_commit_kernel<<<cdiv(N, 8), 256, 0, st>>>(beta_alt, beta, ldb, q, ll_alt, ll, lp_alt, lp, logw,
+  resample_commit_kernel<<<std::min<unsigned>(cdiv(N, 8), 8 * 148), 256, 0, st>>>(beta_alt, beta, ldb, q, ll_alt, ll, lp_alt, lp, logw,
                                                       -std::log((double)N), N, gate);
   SPA_CHECK_LAUNCH();
   return 0;
