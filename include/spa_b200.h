@@ -44,13 +44,14 @@ typedef struct spa_design {
   const float* xcols;       /* general: [q][n_words*32] float32 columns, 0-padded */
   const float* xlev;        /* [q][4]  x value of code 0,1,2 (coded designs)   */
   const double* sy;         /* [q]     X^T y                                    */
-  const double* alpha;      /* [q]     coded: x = alpha*g + gamma              */
+  const double* alpha;      /* [q]     coded: x = alpha*g + gamma; general: the
+                               power-of-two column scale of gemm_b (X = alpha*Xs) */
   const double* gamma;      /* [q]                                              */
   const uint8_t* penalized; /* [q]     1 = prior applies (smc.py:266-270)      */
   /* tensor-core operand of the batched likelihood (K1) */
-  const void* gemm_b;       /* bf16 B operand: coded -> G [n][kp] (0/1/2 and
+  const void* gemm_b;       /* fp16 B operand: coded -> G [n][kp] (0/1/2 and
                                1 in the 3 offset columns q..q+2);
-                               general -> [Xhi | Xlo] [n][2*kp]              */
+                               general -> [Xshi | Xslo] [n][2*kp], Xs = X/alpha */
   int32_t kp;               /* K per term, multiple of 64, >= q (+3 if coded) */
   int32_t terms;            /* B terms: 1 (coded) or 2 (general); the A
                                operand is always [beta hi | beta lo]          */
@@ -71,7 +72,8 @@ int spa_philox_blocks(uint64_t k0, uint64_t k1, uint64_t first_block, int64_t co
 /* ---- K1: batched log-likelihood on tcgen05 tensor cores -----------------
  * Replaces model.py:131-145 log_likelihood evaluated for many particles
  * (batched as summary.py:154-170).  A = packed particles (spa_pack_particles),
- * bf16 [m][terms*kp]; out_sp[m] = sum_i softplus(eta_ki) (float64).
+ * fp16 [m][2*kp] = [hi | lo] (22 significant bits of alpha*beta);
+ * out_sp[m] = sum_i softplus(eta_ki) (float64).
  * ws: workspace of spa_loglik_workspace_bytes(m, n) bytes. */
 size_t spa_loglik_workspace_bytes(int64_t m, int32_t n);
 int spa_loglik_softplus(const spa_design* d, const void* A, int64_t m, double* out_sp, void* ws, size_t ws_bytes,
@@ -121,8 +123,17 @@ int spa_logw_apply(double* logw, const double* lw, int64_t m, const double* res,
  * Bit-exact with systematic_resample_indices(w, u): sequential float64
  * cumsum, division by the last entry, cum[-1] = 1, positions u + k/N,
  * searchsorted(side='right').  anc[k] for k in [k0, k0+count) of the N slots.
+ * The cumsum is np.cumsum's strictly sequential chain reproduced by a
+ * parallel binade-segmented scan (csrc/resample.cu; speculative, verified,
+ * sequential fallback inside the same launches).
  * ws: spa_resample_workspace_bytes(N). */
 size_t spa_resample_workspace_bytes(int64_t N);
+/* Test hook: cum[i] = np.cumsum(w)[i] bit for bit (smc.py:276) into the
+ * device array cum (N doubles); *mode (device int32) = 0 if the parallel
+ * fast path produced it, else the sequential fallback did (the value is the
+ * first failed check, csrc/resample.cu chain_block). */
+int spa_exact_cumsum(const double* w, int64_t N, double* cum, int32_t* mode, void* ws, size_t ws_bytes,
+                     void* stream);
 int spa_systematic_ancestors(const double* w, int64_t N, double u, int64_t k0, int64_t count, int64_t* anc,
                              void* ws, size_t ws_bytes, void* stream);
 /* dst_rows[k] = src_rows[idx[k] - base] (float32 rows) and the per-particle

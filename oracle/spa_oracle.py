@@ -280,7 +280,8 @@ def rw_cov_factor(B, w, scale_const: float = 2.38, jitter: float = 1e-6):
     """Population random-walk proposal factor for the north-star RW-cov move
     (no reference counterpart; BASELINE.json north_star item 4): weighted
     covariance of the particle cloud, Cholesky factor, scaled by 2.38/sqrt(q).
-    Restates csrc/rwmove.cu in float64."""
+    Restates the K8 factor path (csrc/spa_core.cu: rw_center_kernel, the split-K
+    SYRK, rw_cov_kernel, rw_chol_panel_kernel, rw_emit_kernel) in float64."""
     B = np.asarray(B, np.float64)
     w = np.asarray(w, np.float64)
     mu = w @ B

@@ -6,6 +6,7 @@
 // include/spa_b200.h).
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include <cmath>
@@ -18,6 +19,7 @@
 #include "../../include/spa_b200.h"
 #include "common.cuh"
 #include "philox.cuh"
+#include "resample.cuh"
 #include "tc_gemm.cuh"
 
 namespace spa {
@@ -46,15 +48,17 @@ static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   return fn;
 }
 
-// bf16 matrix [rows][cols] row-major; box = 64 columns x box_rows rows, 128B swizzle.
-static int make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+// 16-bit (bf16 / fp16) matrix [rows][cols] row-major; box = 64 columns x
+// box_rows rows, 128B swizzle.
+static int make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t cols, uint64_t rows, uint32_t box_rows,
+                          bool f16 = false) {
   auto enc = tmap_encoder();
   if (!enc) return fail(kDriverEntryPoint, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
   cuuint32_t box[2] = {64, box_rows};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+  CUresult r = enc(map, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(kDriverEntryPoint, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
@@ -84,16 +88,16 @@ static int make_tmap_out(CUtensorMap* map, void* ptr, uint64_t cols, uint64_t ro
   return 0;
 }
 
-template <int TA, int TB, int BN, class Epi, int TM = 1>
+template <int TA, int TB, int BN, class Epi, int TM = 1, bool F16 = false>
 static int launch_tc(const void* A, uint64_t a_cols, const void* B, uint64_t b_cols, uint64_t b_rows, TcArgs args,
                      int units, const Epi& epi, cudaStream_t st) {
   constexpr int kSmem = tc_smem_bytes<TA, TB, BN, Epi, TM>();
   CUtensorMap ta, tb;
-  int rc = make_tmap_bf16(&ta, A, a_cols, (uint64_t)args.m, kTcBM);
+  int rc = make_tmap_bf16(&ta, A, a_cols, (uint64_t)args.m, kTcBM, F16);
   if (rc) return rc;
-  rc = make_tmap_bf16(&tb, B, b_cols, b_rows, BN);
+  rc = make_tmap_bf16(&tb, B, b_cols, b_rows, BN, F16);
   if (rc) return rc;
-  auto kern = tc_gemm_kernel<TA, TB, BN, Epi, TM>;
+  auto kern = tc_gemm_kernel<TA, TB, BN, Epi, TM, F16>;
   static bool attr_done = false;  // per template instantiation
   if (!attr_done) {
     SPA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
@@ -187,24 +191,50 @@ struct LpAcc {
 };
 
 // ---------------------------------------------------------------------------
-// Pack particle rows into the K1 A operand [m][2*kp] bf16 = [hi | lo] of the
+// K1 operand element: fp16 hi/lo split.  hi = fp16(x), lo = fp16(x - hi)
+// carries 22 significant bits (bf16 hi/lo: 16, which left 1e-5-relative
+// log-likelihood errors on diffuse particles: tests/test_gpu_bench_shapes.py);
+// the MMA rate of kind::f16 is the same for fp16 and bf16.  fp16 has a finite
+// range: a row with |alpha_j beta_j| >= 65504 (|beta| ~ 4e4) cannot be packed
+// and gets a NaN linear term (its log-likelihood is NaN: an MH proposal with
+// NaN log-ratio is rejected; the reference's value there is ~ -1e4 * n).
+constexpr float kOpMax = 65504.f;
+__device__ __forceinline__ void split_op(float x, __half& h, __half& l, float& flag_into) {
+  h = __float2half_rn(x);
+  l = __float2half_rn(x - __half2float(h));
+  if (!(fabsf(x) < kOpMax)) flag_into = __int_as_float(0x7fc00000);
+}
+// Coded designs: the centring offset o = sum_j gamma_j beta_j rides in three
+// fp16 limbs (B holds 1 in those columns); |o| >= 65504 -> NaN linear term.
+__device__ __forceinline__ void offset_limbs(double o, __half* dst, double* ylin_row) {
+  const __half o1 = __double2half(o);
+  const double r1 = o - (double)__half2float(o1);
+  const __half o2 = __double2half(r1);
+  dst[0] = o1;
+  dst[1] = o2;
+  dst[2] = __double2half(r1 - (double)__half2float(o2));
+  if (!(fabs(o) < (double)kOpMax)) *ylin_row = __longlong_as_double(0x7ff8000000000000ll);
+}
+
+// ---------------------------------------------------------------------------
+// Pack particle rows into the K1 A operand [m][2*kp] fp16 = [hi | lo] of the
 // scaled coefficients; coded designs carry the centring offset
-// o = sum_j gamma_j beta_j in three bf16 columns q..q+2 of the hi block (the
+// o = sum_j gamma_j beta_j in three fp16 columns q..q+2 of the hi block (the
 // B operand holds 1 there), so the MMA yields eta directly.
 // One warp per particle row; lanes take 4 consecutive columns (float4).
 // prop = beta (+ eps); A = [hi | lo] of alpha*prop; ylin = prop . X^T y;
 // off (coded) into the offset columns; lp = sum gt(prop) (float32 terms,
 // float64 accumulation).
 __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const __nv_bfloat16* __restrict__ eps, int64_t m,
-                            int ldb, __nv_bfloat16* __restrict__ A, double* __restrict__ ylin, PriorConst pc,
+                            int ldb, __half* __restrict__ A, double* __restrict__ ylin, PriorConst pc,
                             double* __restrict__ lp) {
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= m) return;
   const float* b = beta + row * ldb;
   const __nv_bfloat16* e = eps ? eps + row * ldb : nullptr;
-  __nv_bfloat16* ah = A + row * (2 * (int64_t)d.kp);
-  __nv_bfloat16* al = ah + d.kp;
+  __half* ah = A + row * (2 * (int64_t)d.kp);
+  __half* al = ah + d.kp;
   double yl = 0.0, off = 0.0;
   LpAcc la;
   const double K = pc.de ? 0.0 : 1.0 / (pc.a * pc.c);
@@ -231,19 +261,18 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const 
       for (int i = 0; i < 4; ++i)
         if (j0 + i < d.q) p[i] = b[j0 + i] + (e ? __bfloat162float(e[j0 + i]) : 0.f);
     }
-    __align__(8) __nv_bfloat16 h[4], l[4];
+    __align__(8) __half h[4], l[4];
     float fy = 0.f, fo = 0.f;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int j = j0 + i;
       float bs = 0.f;
       if (j < d.q) {
-        bs = (d.coded ? (float)d.alpha[j] : 1.0f) * p[i];
+        bs = (float)d.alpha[j] * p[i];
         fy = fmaf(p[i], (float)d.sy[j], fy);
         fo = fmaf(p[i], d.coded ? (float)d.gamma[j] : 0.f, fo);
       }
-      h[i] = __float2bfloat16_rn(bs);
-      l[i] = __float2bfloat16_rn(bs - __bfloat162float(h[i]));
+      split_op(bs, h[i], l[i], fy);
     }
     if (lp != nullptr) {
       float pen[4];
@@ -260,18 +289,13 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const 
   off = warp_sum(off);
   double lps = 0.0;
   if (lp != nullptr) lps = warp_sum(la.value(pc));
+  __syncwarp();  // orders every lane's zero stores to columns q..q+2 before lane 0's offset limbs
   if (lane == 0) {
     ylin[row] = yl;
     if (lp != nullptr) lp[row] = lps;
     if (d.coded) {
-      const double o = off;  // eta = sum_j g_ij alpha_j beta_j + sum_j gamma_j beta_j
-      const __nv_bfloat16 o1 = __double2bfloat16(o);
-      const double r1 = o - (double)__bfloat162float(o1);
-      const __nv_bfloat16 o2 = __double2bfloat16(r1);
-      const double r2 = r1 - (double)__bfloat162float(o2);
-      ah[d.q] = o1;
-      ah[d.q + 1] = o2;
-      ah[d.q + 2] = __double2bfloat16(r2);
+      // eta = sum_j g_ij alpha_j beta_j + sum_j gamma_j beta_j
+      offset_limbs(off, ah + d.q, ylin + row);
     }
   }
 }
@@ -292,7 +316,7 @@ __host__ __device__ inline size_t pack_eps_smem_bytes(int kp, int ldb) {
 template <int IT>
 __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design d, const float* __restrict__ beta,
                                                                 const __nv_bfloat16* __restrict__ eps, int64_t m,
-                                                                int ldb, __nv_bfloat16* __restrict__ A,
+                                                                int ldb, __half* __restrict__ A,
                                                                 double* __restrict__ ylin, PriorConst pc,
                                                                 double* __restrict__ lp) {
   extern __shared__ float4 csm[];  // [kp] x {alpha, sy, gamma, pen}, then the row rings
@@ -306,7 +330,7 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
   uint8_t* ring = reinterpret_cast<uint8_t*>(cp + d.kp) + (size_t)warp * kPackSlots * slotB;
   for (int j = threadIdx.x; j < d.kp; j += blockDim.x) {
     const bool v = j < d.q;
-    ca[j] = v ? (d.coded ? (float)d.alpha[j] : 1.0f) : 0.f;
+    ca[j] = v ? (float)d.alpha[j] : 0.f;
     cs[j] = v ? (float)d.sy[j] : 0.f;
     cg[j] = (v && d.coded) ? (float)d.gamma[j] : 0.f;
     cp[j] = (v && d.penalized[j]) ? 1.f : 0.f;
@@ -336,8 +360,8 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
     phase ^= 1u << s;
     const float* b = reinterpret_cast<const float*>(ring + s * slotB);
     const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(ring + s * slotB + rowB);
-    __nv_bfloat16* ah = A + row * (2 * (int64_t)d.kp);
-    __nv_bfloat16* al = ah + d.kp;
+    __half* ah = A + row * (2 * (int64_t)d.kp);
+    __half* al = ah + d.kp;
     double yl = 0.0, off = 0.0;  // same grouping as pack_kernel => identical sums
     // log-prior: the LpAcc product order without its per-chunk overflow
     // branch (factors are >= 1, so the running product can only overflow
@@ -370,14 +394,13 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
       const float4 vp = *reinterpret_cast<const float4*>(cp + j0);
       const float a4[4] = {va.x, va.y, va.z, va.w}, s4[4] = {vs.x, vs.y, vs.z, vs.w};
       const float g4[4] = {vg.x, vg.y, vg.z, vg.w}, p4[4] = {vp.x, vp.y, vp.z, vp.w};
-      __align__(8) __nv_bfloat16 h[4], l[4];
+      __align__(8) __half h[4], l[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const float bs = a4[i] * p[i];
-        h[i] = __float2bfloat16_rn(bs);
-        l[i] = __float2bfloat16_rn(bs - __bfloat162float(h[i]));
         fy = fmaf(p[i], s4[i], fy);
         fo = fmaf(p[i], g4[i], fo);
+        split_op(bs, h[i], l[i], fy);
       }
       {
         npen += (p4[0] + p4[1]) + (p4[2] + p4[3]);
@@ -424,12 +447,7 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
       ylin[row] = yl;
       if (lp != nullptr) lp[row] = lps;
       if (d.coded) {
-        const __nv_bfloat16 o1 = __double2bfloat16(off);
-        const double r1 = off - (double)__bfloat162float(o1);
-        const __nv_bfloat16 o2 = __double2bfloat16(r1);
-        ah[d.q] = o1;
-        ah[d.q + 1] = o2;
-        ah[d.q + 2] = __double2bfloat16(r1 - (double)__bfloat162float(o2));
+        offset_limbs(off, ah + d.q, ylin + row);
       }
     }
   }
@@ -444,7 +462,7 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
 template <int IT, int LPR>
 __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
     spa_design d, const float* __restrict__ beta, const __nv_bfloat16* __restrict__ eps, int64_t m, int ldb,
-    __nv_bfloat16* __restrict__ A, double* __restrict__ ylin, PriorConst pc, double* __restrict__ lp) {
+    __half* __restrict__ A, double* __restrict__ ylin, PriorConst pc, double* __restrict__ lp) {
   constexpr int R = 32 / LPR;
   extern __shared__ float4 csm[];  // [kp] x {alpha, sy, gamma, pen}, then the row rings
   __shared__ uint64_t bars[kPackWarps][kPackSlots];
@@ -457,7 +475,7 @@ __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
   uint8_t* ring = reinterpret_cast<uint8_t*>(cp + d.kp) + (size_t)warp * kPackSlots * groupB;
   for (int j = threadIdx.x; j < d.kp; j += blockDim.x) {
     const bool v = j < d.q;
-    ca[j] = v ? (d.coded ? (float)d.alpha[j] : 1.0f) : 0.f;
+    ca[j] = v ? (float)d.alpha[j] : 0.f;
     cs[j] = v ? (float)d.sy[j] : 0.f;
     cg[j] = (v && d.coded) ? (float)d.gamma[j] : 0.f;
     cp[j] = (v && d.penalized[j]) ? 1.f : 0.f;
@@ -495,8 +513,8 @@ __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
     const bool live = row < m;
     const float* b = reinterpret_cast<const float*>(ring + s * groupB + rsub * slotB);
     const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(ring + s * groupB + rsub * slotB + rowB);
-    __nv_bfloat16* ah = A + (live ? row : 0) * (2 * (int64_t)d.kp);
-    __nv_bfloat16* al = ah + d.kp;
+    __half* ah = A + (live ? row : 0) * (2 * (int64_t)d.kp);
+    __half* al = ah + d.kp;
     double yl = 0.0, off = 0.0, prod = 1.0, lin = 0.0;
     float npen = 0.f;
 #pragma unroll
@@ -527,14 +545,13 @@ __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
       const float4 vp = *reinterpret_cast<const float4*>(cp + j0);
       const float a4[4] = {va.x, va.y, va.z, va.w}, s4[4] = {vs.x, vs.y, vs.z, vs.w};
       const float g4[4] = {vg.x, vg.y, vg.z, vg.w}, p4[4] = {vp.x, vp.y, vp.z, vp.w};
-      __align__(8) __nv_bfloat16 h[4], l[4];
+      __align__(8) __half h[4], l[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const float bs = a4[i] * p[i];
-        h[i] = __float2bfloat16_rn(bs);
-        l[i] = __float2bfloat16_rn(bs - __bfloat162float(h[i]));
         fy = fmaf(p[i], s4[i], fy);
         fo = fmaf(p[i], g4[i], fo);
+        split_op(bs, h[i], l[i], fy);
       }
       npen += (p4[0] + p4[1]) + (p4[2] + p4[3]);
       const double x0 = (double)(fabsf(p[0]) * p4[0]), x1 = (double)(fabsf(p[1]) * p4[1]);
@@ -584,12 +601,7 @@ __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
       ylin[row] = yl;
       if (lp != nullptr) lp[row] = lpl;
       if (d.coded) {
-        const __nv_bfloat16 o1 = __double2bfloat16(off);
-        const double r1 = off - (double)__bfloat162float(o1);
-        const __nv_bfloat16 o2 = __double2bfloat16(r1);
-        ah[d.q] = o1;
-        ah[d.q + 1] = o2;
-        ah[d.q + 2] = __double2bfloat16(r1 - (double)__bfloat162float(o2));
+        offset_limbs(off, ah + d.q, ylin + row);
       }
     }
   }
@@ -1241,67 +1253,25 @@ __global__ void logw_apply_kernel(double* __restrict__ logw, const double* __res
 // ---------------------------------------------------------------------------
 // K4: systematic resampling, bit-exact with the reference (smc.py:273-281).
 // The reference cumsum is a strictly sequential float64 accumulation; it is
-// reproduced by one thread scanning smem-staged tiles (the other lanes stage
-// the next tile).  Ancestor search is parallel (one thread per slot).
+// reproduced by the parallel binade-segmented scan of resample.cu.  Ancestor
+// search is parallel (one thread per slot, binary search on cum / cum[N-1]).
 // gate: optional device flag (a step record's "resampled" field); kernels of
 // the device-decided resampling path return at once when it is 0.
 __device__ __forceinline__ bool gated_off(const double* gate) { return gate != nullptr && !(gate[0] != 0.0); }
 
-__global__ void seq_cumsum_kernel(const double* __restrict__ w, int64_t N, double* __restrict__ cum,
-                                  const double* __restrict__ gate) {
-  // blockDim = 64: warp 1 stages tile t+1 into smem while lane 0 of warp 0
-  // runs the strictly sequential float64 accumulation over tile t.
-  __shared__ double tile[2][2048];
-  if (gated_off(gate)) return;
-  const int64_t ntiles = (N + 2047) / 2048;
-  if (threadIdx.x >= 32)
-    for (int i = threadIdx.x - 32; i < 2048; i += 32) tile[0][i] = (i < N) ? w[i] : 0.0;
-  __syncthreads();
-  double s = 0.0;
-  for (int64_t t = 0; t < ntiles; ++t) {
-    const int cur = (int)(t & 1);
-    if (threadIdx.x == 0) {
-      const int64_t base = t * 2048;
-      const int cnt = (int)(N - base < 2048 ? N - base : 2048);
-      const double* tl = tile[cur];
-      int i = 0;
-      for (; i + 4 <= cnt; i += 4) {
-        const double a0 = tl[i], a1 = tl[i + 1], a2 = tl[i + 2], a3 = tl[i + 3];
-        const double s0 = s + a0;  // same association as np.cumsum
-        const double s1 = s0 + a1;
-        const double s2 = s1 + a2;
-        const double s3 = s2 + a3;
-        cum[base + i] = s0;
-        cum[base + i + 1] = s1;
-        cum[base + i + 2] = s2;
-        cum[base + i + 3] = s3;
-        s = s3;
-      }
-      for (; i < cnt; ++i) {
-        s = s + tl[i];
-        cum[base + i] = s;
-      }
-    } else if (threadIdx.x >= 32 && t + 1 < ntiles) {
-      const int64_t base = (t + 1) * 2048;
-      for (int i = threadIdx.x - 32; i < 2048; i += 32) tile[cur ^ 1][i] = (base + i < N) ? w[base + i] : 0.0;
-    }
-    __syncthreads();
-  }
-}
-
-__global__ void ancestors_kernel(const double* __restrict__ cum, int64_t N, double u, int64_t k0, int64_t count,
+// cumn = cum / cum[N-1] with cumn[N-1] = 1 (written by the exact scan):
+// anc = searchsorted(cumn, u + k/N, side='right') for slots k0.. (smc.py:279-281)
+__global__ void ancestors_kernel(const double* __restrict__ cumn, int64_t N, double u, int64_t k0, int64_t count,
                                  int64_t* __restrict__ anc, const double* __restrict__ gate) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count || gated_off(gate)) return;
   const int64_t k = k0 + i;
-  const double total = cum[N - 1];
   const double pos = u + (double)k / (double)N;
-  // first index j with norm(j) > pos, norm(j) = cum[j]/total, norm(N-1) = 1
+  // first index j with cumn[j] > pos
   int64_t lo = 0, hi = N;
   while (lo < hi) {
     const int64_t mid = (lo + hi) >> 1;
-    const double v = (mid == N - 1) ? 1.0 : __ddiv_rn(cum[mid], total);
-    if (v > pos)
+    if (__ldg(cumn + mid) > pos)
       hi = mid;
     else
       lo = mid + 1;
@@ -2025,9 +1995,11 @@ static int loglik_impl(const spa_design* d, const void* A, int64_t m, const doub
   EpiSoftplusRowSum epi{reinterpret_cast<double*>(ws)};
   int rc;
   if (d->terms == 1)
-    rc = launch_tc<2, 1, 256>(A, 2ull * d->kp, d->gemm_b, (uint64_t)d->kp, (uint64_t)d->n, args, units, epi, st);
+    rc = launch_tc<2, 1, 256, EpiSoftplusRowSum, 1, true>(A, 2ull * d->kp, d->gemm_b, (uint64_t)d->kp,
+                                                          (uint64_t)d->n, args, units, epi, st);
   else
-    rc = launch_tc<2, 2, 256>(A, 2ull * d->kp, d->gemm_b, 2ull * d->kp, (uint64_t)d->n, args, units, epi, st);
+    rc = launch_tc<2, 2, 256, EpiSoftplusRowSum, 1, true>(A, 2ull * d->kp, d->gemm_b, 2ull * d->kp,
+                                                          (uint64_t)d->n, args, units, epi, st);
   if (rc) return rc;
   reduce_units_kernel<<<cdiv(m, 256), 256, 0, st>>>(reinterpret_cast<double*>(ws), units, m, ylin, out);
   SPA_CHECK_LAUNCH();
@@ -2058,7 +2030,7 @@ int spa_pack_particles(const spa_design* d, const float* beta, int64_t m, int32_
   SPA_REQUIRE(!d->coded || d->kp >= d->q + 3, kBadArgument, "spa_pack_particles: kp < q + 3");
   if (m == 0) return 0;
   pack_kernel<<<cdiv(m, 8), 256, 0, as_stream(stream)>>>(*d, beta, (const __nv_bfloat16*)nullptr, m, ldb,
-                                                        reinterpret_cast<__nv_bfloat16*>(A), ylin,
+                                                        reinterpret_cast<__half*>(A), ylin,
                                                         make_prior(a, c, c), lp);
   SPA_CHECK_LAUNCH();
   return 0;
@@ -2121,7 +2093,13 @@ static int sum_params(int32_t nlev, const double* levels, int32_t ndelta, const 
   sp->nlev = nlev;
   sp->ndelta = ndelta;
   for (int i = 0; i < kSumMaxLev; ++i) sp->level[i] = i < nlev ? levels[i] : 0.5;
-  for (int i = 0; i < kSumMaxDelta; ++i) sp->delta[i] = i < ndelta ? (float)deltas[i] : 0.f;
+  // float32 threshold t = the smallest float >= delta, so that for float32
+  // particles |x| < t  <=>  |x| < delta in float64 (summary.py:54-61)
+  for (int i = 0; i < kSumMaxDelta; ++i) {
+    float t = i < ndelta ? (float)deltas[i] : 0.f;
+    if (i < ndelta && (double)t < deltas[i]) t = std::nextafter(t, INFINITY);
+    sp->delta[i] = t;
+  }
   for (int i = 0; i < nlev; ++i) SPA_REQUIRE(levels[i] > 0.0 && levels[i] < 1.0, kBadArgument, "spa_summary: level");
   for (int i = 0; i < ndelta; ++i) SPA_REQUIRE(deltas[i] > 0.0, kBadArgument, "spa_summary: delta");
   return 0;
@@ -2207,7 +2185,7 @@ int spa_logw_apply(double* logw, const double* lw, int64_t m, const double* res,
   return 0;
 }
 
-size_t spa_resample_workspace_bytes(int64_t N) { return (size_t)N * sizeof(double); }
+size_t spa_resample_workspace_bytes(int64_t N) { return exact_cumsum_ws_bytes(N); }
 
 int spa_systematic_ancestors(const double* w, int64_t N, double u, int64_t k0, int64_t count, int64_t* anc,
                              void* ws, size_t ws_bytes, void* stream) {
@@ -2216,12 +2194,32 @@ int spa_systematic_ancestors(const double* w, int64_t N, double u, int64_t k0, i
   SPA_REQUIRE(ws_bytes >= spa_resample_workspace_bytes(N), kWorkspaceTooSmall,
               "spa_systematic_ancestors: workspace too small");
   cudaStream_t st = as_stream(stream);
-  double* cum = reinterpret_cast<double*>(ws);
-  seq_cumsum_kernel<<<1, 64, 0, st>>>(w, N, cum, nullptr);
-  SPA_CHECK_LAUNCH();
+  const double* cumn = reinterpret_cast<const double*>(reinterpret_cast<char*>(ws) + exact_cumsum_norm_offset(N));
+  WSrc src{};
+  src.p[0] = w;
+  src.len = N;
+  src.nparts = 1;
+  int rc = exact_cumsum(src, N, ws, nullptr, st);
+  if (rc) return rc;
   if (count == 0) return 0;
-  ancestors_kernel<<<cdiv(count, 256), 256, 0, st>>>(cum, N, u, k0, count, anc, nullptr);
+  ancestors_kernel<<<cdiv(count, 256), 256, 0, st>>>(cumn, N, u, k0, count, anc, nullptr);
   SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+int spa_exact_cumsum(const double* w, int64_t N, double* cum, int32_t* mode, void* ws, size_t ws_bytes,
+                     void* stream) {
+  SPA_REQUIRE(w && cum && ws && N > 0, kBadArgument, "spa_exact_cumsum: bad arguments");
+  SPA_REQUIRE(ws_bytes >= spa_resample_workspace_bytes(N), kWorkspaceTooSmall, "spa_exact_cumsum: workspace too small");
+  cudaStream_t st = as_stream(stream);
+  WSrc src{};
+  src.p[0] = w;
+  src.len = N;
+  src.nparts = 1;
+  int rc = exact_cumsum(src, N, ws, nullptr, st);
+  if (rc) return rc;
+  SPA_CHECK_CUDA(cudaMemcpyAsync(cum, ws, (size_t)N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (mode) return exact_cumsum_mode(N, ws, mode, st);
   return 0;
 }
 
@@ -2251,10 +2249,14 @@ int spa_resample_gated(const double* gate, const double* w, int64_t N, double u,
   SPA_REQUIRE(ws_bytes >= spa_resample_workspace_bytes(N), kWorkspaceTooSmall,
               "spa_resample_gated: workspace too small");
   cudaStream_t st = as_stream(stream);
-  double* cum = reinterpret_cast<double*>(ws);
-  seq_cumsum_kernel<<<1, 64, 0, st>>>(w, N, cum, gate);
-  SPA_CHECK_LAUNCH();
-  ancestors_kernel<<<cdiv(N, 256), 256, 0, st>>>(cum, N, u, 0, N, anc, gate);
+  const double* cumn = reinterpret_cast<const double*>(reinterpret_cast<char*>(ws) + exact_cumsum_norm_offset(N));
+  WSrc src{};
+  src.p[0] = w;
+  src.len = N;
+  src.nparts = 1;
+  int rc = exact_cumsum(src, N, ws, gate, st);
+  if (rc) return rc;
+  ancestors_kernel<<<cdiv(N, 256), 256, 0, st>>>(cumn, N, u, 0, N, anc, gate);
   SPA_CHECK_LAUNCH();
   gather_kernel<<<std::min<unsigned>(cdiv(N, 8), 8 * 148), 256, 0, st>>>(beta, ldb, beta_alt, ldb, q, anc, 0, N, ll, ll_alt, lp, lp_alt, gate);
   SPA_CHECK_LAUNCH();
@@ -2422,7 +2424,7 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
   rc = launch_tc<1, 1, kPropBN, EpiStoreT<__nv_bfloat16>>(Z, (uint64_t)kq, Lb, (uint64_t)kq, (uint64_t)q, args, 1,
                                                           epi, st);
   if (rc) return rc;
-  auto* Ab = reinterpret_cast<__nv_bfloat16*>(A);
+  auto* Ab = reinterpret_cast<__half*>(A);
   const PriorConst pc = make_prior(a, c, c);
   const size_t sm = pack_eps_smem_bytes(d->kp, ldb);
   auto run = [&](auto kern) -> int {
@@ -2469,8 +2471,8 @@ extern "C" int spa_mwg_prepare_kernels(void);  // mwg.cu
 // shared-memory attributes; callable while other work runs on the device.
 int spa_prepare(void) {
   const void* fns[] = {
-      (const void*)tc_gemm_kernel<2, 1, 256, EpiSoftplusRowSum>,
-      (const void*)tc_gemm_kernel<2, 2, 256, EpiSoftplusRowSum>,
+      (const void*)tc_gemm_kernel<2, 1, 256, EpiSoftplusRowSum, 1, true>,
+      (const void*)tc_gemm_kernel<2, 2, 256, EpiSoftplusRowSum, 1, true>,
       (const void*)tc_gemm_kernel<1, 1, 256, EpiStoreT<__nv_bfloat16>>,
       (const void*)tc_gemm_kernel<2, 2, 256, EpiStoreT<float>>,
       (const void*)pack_kernel, (const void*)pack_eps_kernel<1>, (const void*)pack_eps_kernel<2>,
@@ -2478,7 +2480,7 @@ int spa_prepare(void) {
       (const void*)prior_reweight_rows_kernel<8, 4>, (const void*)prior_reweight_rows_kernel<8, 8>,
       (const void*)prior_reweight_rows_kernel<16, 8>, (const void*)prior_reweight_rows_kernel<16, 16>,
       (const void*)prior_reweight_rows_kernel<32, 16>, (const void*)prior_reweight_kernel<32>, (const void*)lse_stats_kernel, (const void*)lse_combine_kernel,
-      (const void*)logw_apply_kernel, (const void*)seq_cumsum_kernel, (const void*)ancestors_kernel,
+      (const void*)logw_apply_kernel, (const void*)ancestors_kernel,
       (const void*)gather_kernel, (const void*)step_record_kernel, (const void*)resample_commit_kernel,
       (const void*)reduce_units_kernel, (const void*)rw_mean_kernel<4>, (const void*)rw_cov_kernel,
       (const void*)rw_chol_panel_kernel, (const void*)rw_emit_kernel,

@@ -1,6 +1,6 @@
 // Warp-specialised tcgen05 GEMM engine for sm_100a with fused epilogues.
 //
-//   D[128 x BN] = sum_terms A_t[128 x K] * B_t[BN x K]^T   (bf16 in, fp32 TMEM accumulate)
+//   D[128 x BN] = sum_terms A_t[128 x K] * B_t[BN x K]^T   (bf16 or fp16 in, fp32 TMEM accumulate)
 //
 // One CTA owns one 128-row A tile (particles) and walks a contiguous range of
 // BN-column tiles (subjects for the likelihood, coordinates for the proposal).
@@ -70,7 +70,8 @@ constexpr int tc_smem_bytes() {
 // The epilogue object is a __grid_constant__ parameter: its tensor maps stay
 // addressable in parameter space for TMA; per-thread mutable state lives in
 // Epi::State.
-template <int TA, int TB, int BN, class Epi, int TM = 1>
+// F16: operands are fp16 (the K1 likelihood's hi/lo split), else bf16.
+template <int TA, int TB, int BN, class Epi, int TM = 1, bool F16 = false>
 __global__ void __launch_bounds__(kTcThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, TcArgs args,
                    const __grid_constant__ Epi epi) {
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
-      constexpr uint32_t idesc = idesc_bf16_f32(kTcBM, BN);
+      constexpr uint32_t idesc = F16 ? idesc_f16_f32(kTcBM, BN) : idesc_bf16_f32(kTcBM, BN);
       int s = 0;
       uint32_t ph = 0;
       int it = 0;

@@ -145,20 +145,27 @@ class DeviceDesign:
             t["xlev"] = torch.from_numpy(lev).to(dev)
             t["alpha"] = torch.from_numpy(alpha).to(dev)
             t["gamma"] = torch.from_numpy(gamma).to(dev)
-            t["gemm_b"] = torch.from_numpy(G).to(dev).to(torch.bfloat16).contiguous()
+            t["gemm_b"] = torch.from_numpy(G).to(dev).to(torch.float16).contiguous()  # 0/1/2 exact
             terms = 1
         else:
             kp = _round_up(q, K_ALIGN)
             xc = np.zeros((q, npad), np.float32)
             xc[:, :n] = X.T
             t["xcols"] = torch.from_numpy(xc).to(dev)
+            # fp16 hi/lo operand of X scaled per column by a power of two
+            # (max |X_j| / 2^s_j in [2, 8)); the pack multiplies beta_j by
+            # alpha_j = 2^s_j, so the product is unchanged and both fp16
+            # terms stay in their normal range
+            mx = np.max(np.abs(X), axis=0) if n else np.zeros(q)
+            sh = np.where(mx > 0, np.round(np.log2(np.where(mx > 0, mx, 1.0))) - 2, 0).astype(np.int64)
+            scale = np.ldexp(1.0, sh)
             Xf = torch.zeros((n, kp), dtype=torch.float64)
-            Xf[:, :q] = torch.from_numpy(X)
-            hi = Xf.to(torch.bfloat16)
-            lo = (Xf - hi.to(torch.float64)).to(torch.bfloat16)
+            Xf[:, :q] = torch.from_numpy(X / scale)
+            hi = Xf.to(torch.float16)
+            lo = (Xf - hi.to(torch.float64)).to(torch.float16)
             t["gemm_b"] = torch.cat([hi, lo], dim=1).contiguous().to(dev)
             t["xlev"] = torch.zeros((q, 4), dtype=torch.float32, device=dev)
-            t["alpha"] = torch.ones(q, dtype=torch.float64, device=dev)
+            t["alpha"] = torch.from_numpy(scale).to(dev)  # K1 column scale (general designs)
             t["gamma"] = torch.zeros(q, dtype=torch.float64, device=dev)
             terms = 2
         t["sy"] = torch.from_numpy(sy).to(dev)

@@ -276,7 +276,7 @@ class ParticleSystem:
             a_cols = max(2 * d.kp, kq)
             nbytes = _lib.load().spa_loglik_workspace_bytes(self.N, d.n)
             self._ll_ws = dict(
-                A=torch.empty((self.N, a_cols), dtype=torch.bfloat16, device=self.device),
+                A=torch.empty((self.N, a_cols), dtype=torch.float16, device=self.device),  # K1 operand (fp16 hi|lo)
                 ylin=torch.empty(self.N, dtype=torch.float64, device=self.device),
                 sp=torch.empty(self.N, dtype=torch.float64, device=self.device),
                 ws=torch.empty(max(nbytes, 8), dtype=torch.uint8, device=self.device),
@@ -356,12 +356,13 @@ def ess(weights) -> float:
 
 def systematic_resample_indices(weights, u: float) -> np.ndarray:
     """Ancestor indices for one systematic draw u in [0, 1/N) (smc.py:273-281),
-    bit-exact (K4 kernel: sequential float64 cumsum + parallel search)."""
+    bit-exact (K4: np.cumsum's sequential float64 sums by a parallel exact
+    scan, csrc/resample.cu, + parallel search)."""
     _require_cuda()
     w = torch.as_tensor(np.ascontiguousarray(weights, dtype=np.float64)).cuda()
     N = w.numel()
     anc = torch.empty(N, dtype=torch.int64, device=w.device)
-    ws = torch.empty(max(8 * N, 8), dtype=torch.uint8, device=w.device)
+    ws = torch.empty(_lib.load().spa_resample_workspace_bytes(N), dtype=torch.uint8, device=w.device)
     _lib.call("spa_systematic_ancestors", _p(w), N, float(u), 0, N, _p(anc), _p(ws), ws.numel(), _stream())
     return anc.cpu().numpy()
 
@@ -419,7 +420,7 @@ def _resample_device(system: ParticleSystem, u: float, group=None) -> torch.Tens
     w = system.device_weights() if group is None else _global_weights(system, group)
     w_full = w if group is None else group.all_gather_cat(w)
     anc = torch.empty(N, dtype=torch.int64, device=system.device)
-    ws = torch.empty(8 * N, dtype=torch.uint8, device=system.device)
+    ws = torch.empty(_lib.load().spa_resample_workspace_bytes(N), dtype=torch.uint8, device=system.device)
     _lib.call("spa_systematic_ancestors", _p(w_full), N, u, 0, N, _p(anc), _p(ws), ws.numel(), _stream())
     if group is None:
         _lib.call("spa_gather_rows", _p(system.beta), system.ldb, _p(system.beta_alt), system.ldb, system.q, _p(anc),
@@ -775,7 +776,8 @@ def _smc_step_async(system: ParticleSystem, schedule: Schedule, t: int, config: 
     if getattr(system, "_records", None) is None or system._records.shape[0] < schedule.T + 1:
         system._records = torch.zeros((schedule.T + 1, 4), dtype=torch.float64, device=system.device)
         system._records[:, 3] = system.log_z_cum
-        system._rs_ws = torch.empty(8 * system.N, dtype=torch.uint8, device=system.device)
+        system._rs_ws = torch.empty(_lib.load().spa_resample_workspace_bytes(system.N), dtype=torch.uint8,
+                                    device=system.device)
         system._anc = torch.empty(system.N, dtype=torch.int64, device=system.device)
     rec = system._records
     _lib.call("spa_prior_reweight", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb,

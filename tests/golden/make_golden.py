@@ -118,6 +118,24 @@ def gen_loglik_prior():
     np.savez_compressed(os.path.join(HERE, "loglik_prior.npz"), **out)
 
 
+def gen_loglik_c5():
+    """C5 shapes (n=10000, p=1000; BASELINE configs[4]): reference
+    log_likelihood (model.py:131-145) and prior sums for a in {0.5, 1, 4}
+    plus the double-exponential limit de_log_density (model.py:84-88), on a
+    few particles (the dataset is regenerated from its spec in the test)."""
+    out = {}
+    dd, _ = rdata.simulate_dataset(ref_spec("c5"))
+    r = np.random.default_rng(55)
+    for s in (0.02, 0.1):
+        B = r.normal(0.0, s, size=(6, dd.p))
+        out[f"c5_B_{s}"] = B
+        out[f"c5_ll_{s}"] = np.array([rmodel.log_likelihood(dd, b)[0] for b in B])
+        for a in (0.5, 1.0, 4.0):
+            out[f"c5_lp_{s}_{a}"] = rmodel.gt_log_density(B, rmodel.GtPrior(a, 0.3)).sum(axis=1)
+        out[f"c5_lp_{s}_de"] = rmodel.de_log_density(B, 0.3).sum(axis=1)
+    np.savez_compressed(os.path.join(HERE, "loglik_c5.npz"), **out)
+
+
 def gen_reweight():
     out = {}
     d, _ = rdata.simulate_dataset(ref_spec("c1"))
@@ -283,6 +301,7 @@ if __name__ == "__main__":
     gen_philox()
     gen_data_hashes()
     gen_loglik_prior()
+    gen_loglik_c5()
     gen_reweight()
     gen_resample()
     if not args.skip_paths:

@@ -257,6 +257,72 @@ def test_resample_large_n_bit_exact():
         assert np.array_equal(systematic_resample_indices(w, u), orc.systematic_ancestors(w, u))
 
 
+def _exact_cumsum(w):
+    wd = torch.from_numpy(np.ascontiguousarray(w, dtype=np.float64)).cuda()
+    N = wd.numel()
+    cum = torch.empty(N, dtype=torch.float64, device="cuda")
+    mode = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+    ws = torch.empty(_lib.load().spa_resample_workspace_bytes(N), dtype=torch.uint8, device="cuda")
+    _lib.call("spa_exact_cumsum", _p(wd), N, _p(cum), _p(mode), _p(ws), ws.numel(), _stream())
+    return cum.cpu().numpy(), int(mode.item())
+
+
+def _cumsum_families():
+    """(name, weights, fast-path expected) covering ties, zeros, ragged
+    tiles, many binade changes per tile and the fallback triggers."""
+    rng = np.random.default_rng(99)
+    out = []
+    for N in (1, 2, 7, 2047, 2048, 2049, 65536, 65539, 1 << 20):
+        for alpha in (0.3, 1.0, 2.0):
+            out.append((f"dirichlet{alpha}_{N}", rng.dirichlet(np.full(N, alpha)), True))
+    N = 65536
+    out.append(("uniform", np.full(N, 1.0 / N), True))                      # every add a power-of-two pattern
+    out.append(("uniform_3", np.full(N, 1.0 / 3.0), True))                  # sums > 1
+    out.append(("exact_ints", rng.integers(0, 4, N) * 2.0**-20, True))      # exactly representable sums
+    w = rng.choice([1.0, 3.0, 5.0], N) * 2.0**-53
+    w[0] = 1.5
+    out.append(("ties", w, True))                                           # every add an exact half-ulp tie
+    w = w.copy()
+    w[0] = 1.0
+    out.append(("ties_at_power_of_two", w, False))                          # all prefixes ambiguous: fallback
+    # multiples of 1e-3 land within rounding distance of 4: the float64 chain
+    # sits below 4 where the fixed-point prefix is above, with nonzero weights
+    # following -> the verified fallback (either path must give np.cumsum)
+    out.append(("half_ulps", (rng.integers(1, 3, N) * 2.0**-60) + np.where(np.arange(N) % 5 == 0, 1e-3, 0.0), None))
+    w = rng.random(N)
+    w[:100] = 0.0
+    out.append(("leading_zeros", w / w.sum(), True))
+    w = rng.random(N)
+    w[::3] = 0.0
+    out.append(("interior_zeros", w, True))
+    out.append(("single_one", np.eye(1, N, 4321).ravel(), True))
+    out.append(("geometric_heads", np.geomspace(1e-28, 1.0, 4096), True))   # a binade change every ~30 elements
+    out.append(("dense_heads", 2.0 ** np.arange(-90, -90 + 2048 * 3) .clip(-90, 20), False))  # > kHMax per tile
+    w = rng.dirichlet(np.full(N, 0.05))
+    out.append(("dirichlet0.05", w, None))                                   # tiny leading prefixes: either path
+    w = rng.random(N)
+    w[0] = 1e-310                                                            # denormal first prefix: fallback
+    out.append(("denormal_start", w, False))
+    out.append(("huge", rng.random(N) * 1e30, False))                        # >= 2^27: fallback
+    w = rng.random(N)
+    w[17] = np.nan
+    out.append(("nan", w, False))
+    return out
+
+
+def test_exact_cumsum_matches_numpy_bit_for_bit():
+    """The parallel binade-segmented scan equals np.cumsum (the reference's
+    strictly sequential float64 chain, smc.py:276) on every element, and the
+    realistic weight vectors take the parallel fast path."""
+    for name, w, fast in _cumsum_families():
+        cum, mode = _exact_cumsum(w)
+        ref = np.cumsum(w)
+        same = (cum == ref) | (np.isnan(cum) & np.isnan(ref))
+        assert same.all(), (name, int(np.argmin(same)))
+        if fast is not None:  # mode: 0 = parallel fast path, > 0 = the fallback's reason code
+            assert (mode == 0) == fast, (name, mode)
+
+
 def test_gather_rows_and_system_resample(gold_loglik):
     from paper_1106_0322_b200 import systematic_resample
 

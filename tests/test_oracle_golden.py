@@ -50,6 +50,20 @@ class TestModel:
             for (a, c) in ((1.0, 2.0), (4.0, 0.3), (0.5, 0.05)):
                 np.testing.assert_allclose(orc.log_prior_rows(B, a, c), gold_loglik[f"c1_lp_{s}_{a}_{c}"], rtol=1e-13)
 
+    def test_c5_shapes(self):
+        """n=10000, p=1000 (BASELINE configs[4]): log-lik and the prior sums
+        for a in {0.5, 1, 4} and the double-exponential limit."""
+        from paper_1106_0322_b200.data import named_spec, simulate_dataset
+
+        g = golden("loglik_c5.npz")
+        d, _ = simulate_dataset(named_spec("c5"))
+        for s in (0.02, 0.1):
+            B = g[f"c5_B_{s}"]
+            np.testing.assert_allclose(orc.loglik_rows(d.X, d.y, B), g[f"c5_ll_{s}"], rtol=1e-12)
+            for a in (0.5, 1.0, 4.0):
+                np.testing.assert_allclose(orc.log_prior_rows(B, a, 0.3), g[f"c5_lp_{s}_{a}"], rtol=1e-13)
+            np.testing.assert_allclose(orc.log_prior_rows(B, float("inf"), 0.3), g[f"c5_lp_{s}_de"], rtol=1e-13)
+
     def test_gaussian_design(self, gold_loglik):
         got = orc.loglik_rows(gold_loglik["g_X"], gold_loglik["g_y"], gold_loglik["g_B"])
         np.testing.assert_allclose(got, gold_loglik["g_ll"], rtol=1e-12)
