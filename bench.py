@@ -35,6 +35,7 @@ N_PER_GPU = 65536
 A_DOF = 1.0
 SCHED = (2.0, 0.98, 100)
 MOVES = 5
+REF_SAMPLE = 256  # particles per reference-arm step (the reference's MwG step at C3: several s on 16 cores)
 
 
 def parse():
@@ -174,46 +175,70 @@ def measured_peaks():
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the oracle port (oracle/spa_oracle.py) of the same lambda step
+# CPU baseline: the reference's own lambda step (reweight -> ESS -> systematic
+# resampling -> MwG cycles over particle blocks on a thread pool, smc.py:
+# 248-295, 298-359, 397-424) restated in oracle/spa_oracle.py (numpy, the
+# reference's vectorised _move_block arithmetic); the reference package
+# itself cannot travel to the GPU box.
 
 
-def cpu_rw_step(X, y, B, ll, lp, logw, a, c_prev, c_t, moves, rng, orc):
+def ref_lambda_step(X, y, B, eta, ll, logw, a, c_prev, c_t, cycles, rng, orc, threads, frac=0.75, sd=0.5):
     import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
 
     lw = orc.reweight_increments(B, a, c_t, c_prev)
     logw, inc = orc.normalise_log_weights(logw, lw)
     w = orc.weights_from_log(logw)
     n = B.shape[0]
-    if orc.ess(w) < 0.75 * n:
+    if orc.ess(w) < frac * n:
         idx = orc.systematic_ancestors(w, rng.random() / n)
-        B, ll = B[idx], ll[idx]
+        B, eta, ll = B[idx], eta[idx], ll[idx]
         logw = np.full(n, -math.log(n))
-        w = np.full(n, 1.0 / n)
-    Ls, _, _ = orc.rw_cov_factor(B, w)
-    lp = orc.log_prior_rows(B, a, c_t)
-    for _ in range(moves):
-        Z = rng.standard_normal(B.shape)
-        U = rng.random(n)
-        B, ll, lp, _ = orc.rw_move_rows(B, ll, lp, X, y, a, c_t, Ls, Z, U)
-    return B, ll, lp, logw
+    q = B.shape[1]
+    Z = rng.standard_normal((n, cycles, q))
+    U = rng.random((n, cycles, q))
+    bounds = np.linspace(0, n, threads + 1, dtype=int)
+
+    def block(lo, hi):
+        return orc.mwg_move_rows(B[lo:hi], eta[lo:hi], ll[lo:hi], X, y, a, c_t, sd, Z[lo:hi], U[lo:hi])
+
+    with ThreadPoolExecutor(max_workers=threads) as pool:  # smc.py:335-359 (threads = host cores)
+        parts = list(pool.map(lambda lh: block(*lh), [(lo, hi) for lo, hi in zip(bounds[:-1], bounds[1:]) if hi > lo]))
+    B = np.concatenate([p[0] for p in parts])
+    eta = np.concatenate([p[1] for p in parts])
+    ll = np.concatenate([p[2] for p in parts])
+    return B, eta, ll, logw
 
 
-def run_cpu_baseline(data, n_sub, steps, orc):
-    """Times `steps` oracle lambda steps on n_sub particles (host threads)."""
+def run_cpu_baseline(data, n_sub, steps, orc, threads):
+    """Times `steps` reference lambda steps (MwG, cycles = MOVES) on n_sub
+    particles with `threads` host threads; returns (evals/s, seconds) with
+    one eval = one n x p sweep of a particle (the unit of our RW move)."""
     import numpy as np
 
     rng = np.random.default_rng(0)
     B = rng.normal(0.0, 0.05, size=(n_sub, data.p))
+    eta = B @ data.X.T
     ll = orc.loglik_rows(data.X, data.y, B)
-    lp = np.zeros(n_sub)
     logw = np.full(n_sub, -math.log(n_sub))
     bs = SCHED[0] * SCHED[1] ** np.arange(SCHED[2])
     t0 = time.perf_counter()
     for k in range(steps):
-        B, ll, lp, logw = cpu_rw_step(data.X, data.y, B, ll, lp, logw, A_DOF, bs[k] / A_DOF, bs[k + 1] / A_DOF, MOVES,
-                                      rng, orc)
+        B, eta, ll, logw = ref_lambda_step(data.X, data.y, B, eta, ll, logw, A_DOF, bs[k] / A_DOF,
+                                           bs[k + 1] / A_DOF, MOVES, rng, orc, threads)
     dt = time.perf_counter() - t0
     return n_sub * MOVES * steps / dt, dt
+
+
+def batched_loglik_rate(data, orc, n_sub=2048):
+    """The reference's batched full log-likelihood (summary.py:154-170
+    pattern: block GEMM + logaddexp) in particle evals/s."""
+    import numpy as np
+
+    B = np.random.default_rng(1).normal(0.0, 0.05, size=(n_sub, data.p))
+    t0 = time.perf_counter()
+    orc.loglik_rows(data.X, data.y, B)
+    return n_sub / (time.perf_counter() - t0)
 
 
 def cores():
@@ -231,20 +256,24 @@ def reference_arm(args):
     from paper_1106_0322_b200.data import named_spec, simulate_dataset
 
     data, _ = simulate_dataset(named_spec(args.config))
-    n_sub = 1024
+    n_sub, thr = REF_SAMPLE, cores()
     for _ in range(max(0, min(args.warmup, 1))):
-        run_cpu_baseline(data, n_sub, 1, orc)
-    val, dt = run_cpu_baseline(data, n_sub, args.steps, orc)
+        run_cpu_baseline(data, 64, 1, orc, thr)
+    val, dt = run_cpu_baseline(data, n_sub, args.steps, orc, thr)
+    bl = batched_loglik_rate(data, orc)
     line = {
-        "impl": "reference", "metric": "particle log-lik evals/s (SMC lambda-path, RW-cov moves, n x p)",
+        "impl": "reference", "metric": "particle log-lik evals/s (SMC lambda-path, n x p)",
         "value": val, "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: n=5000 p=500 a=1 moves=5 (N={n_sub} particle sample per step)",
+        "config": {"workload": f"{args.config}: n={data.n} p={data.p} a={A_DOF} b_t=2*0.98^(t-1); the reference's "
+                               f"lambda step with {MOVES} MwG cycles (N={n_sub} particle sample per step)",
                    "particles_sampled": n_sub},
-        "cpu_baseline": {"value": val, "unit": "evals/s", "cores": cores(), "kind": "port",
-                         "sample": f"{args.steps} lambda steps x {n_sub} particles (oracle/spa_oracle.py numpy port,"
-                                   f" BLAS on all host threads)"},
+        "cpu_baseline": {"value": val, "unit": "evals/s", "cores": thr, "kind": "port",
+                         "sample": f"{args.steps} reference lambda steps (reweight, ESS, systematic resampling, "
+                                   f"{MOVES} MwG cycles = smc.py:397-424) x {n_sub} particles, oracle/spa_oracle.py "
+                                   f"numpy restatement, particle blocks on {thr} threads (SmcConfig.threads)",
+                         "batched_loglik_evals_per_s": bl},
         "e2e": {"value": val, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -254,14 +283,33 @@ def reference_arm(args):
 # ---------------------------------------------------------------------------
 
 
+def relaunch(args):
+    """`bench.py --gpus N` without a torchrun environment: start N ranks (one
+    per GPU, NCCL) with torch.distributed.run on this node; rank 0 prints
+    the JSON line."""
+    import socket
+
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return reference_arm(args)
+    ws, rank, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
+    if args.gpus != ws:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
     import numpy as np
     import torch
 
-    ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     group = None
     if ws > 1:
@@ -286,9 +334,11 @@ def main():
     prior1 = S.GtPrior(A_DOF, sched.bs[0] / A_DOF)
     system, _ = S.init_particles(data, prior1, cfg, False, design=design, group=group)
     t = 2
+    warm = []
     for _ in range(args.warmup):
-        S.smc_step(system, data, sched, t, cfg, group)
+        warm.append(S.smc_step(system, data, sched, t, cfg, group, _defer=True))
         t += 1
+    S.resolve_records(system, warm)
     timer = EventTimer(torch)
     S.KERNEL_TIMER = timer
     torch.cuda.synchronize()
@@ -390,10 +440,12 @@ def main():
     if not args.no_cpu:
         from oracle import spa_oracle as orc
 
-        n_sub = 1024
-        cval, cdt = run_cpu_baseline(data, n_sub, 2, orc)
-        cpu = {"value": cval, "unit": "evals/s", "cores": cores(), "kind": "port",
-               "sample": f"2 lambda steps x {n_sub} particles of the same workload (numpy port, {cdt:.1f} s)"}
+        n_sub, thr = REF_SAMPLE, cores()
+        cval, cdt = run_cpu_baseline(data, n_sub, 1, orc, thr)
+        cpu = {"value": cval, "unit": "evals/s", "cores": thr, "kind": "port",
+               "sample": f"1 reference lambda step ({MOVES} MwG cycles, smc.py:397-424) x {n_sub} particles of the "
+                         f"same workload (oracle numpy restatement on {thr} threads, {cdt:.1f} s)",
+               "batched_loglik_evals_per_s": batched_loglik_rate(data, orc)}
     line = {
         "metric": "particle log-lik evals/s (SMC lambda-path, RW-cov moves, n x p)",
         "value": value, "unit": "evals/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,

@@ -156,6 +156,34 @@ int spa_resample_gated(const double* gate, const double* w, int64_t N, double u,
                        int32_t ldb, int32_t q, double* ll, double* ll_alt, double* lp, double* lp_alt, double* logw,
                        int64_t* anc, void* ws, size_t ws_bytes, void* stream);
 
+/* ---- sharded particles: peer memory and the exchange --------------------
+ * One process per GPU; rank r owns global particles [r M, (r+1) M) (the
+ * reference's partition-invariant particle blocks, smc.py:335-359).
+ * spa_ipc_export: CUDA-IPC handle (64 bytes) of the allocation holding ptr
+ * and ptr's byte offset in it; spa_ipc_open / spa_ipc_close map a peer's
+ * allocation into this process (its base pointer).
+ * spa_resample_sharded: the device-decided systematic resampling of the
+ * global particle set (smc.py:273-295) for this rank's M slots -- every rank
+ * scans the global normalised weights through the peer pointers w_parts[r]
+ * (exact scan, bit-identical to np.cumsum on the concatenation), searches
+ * its own slots and gathers the ancestor rows (beta, ll, lp) straight from
+ * their owners' buffers into the *_alt buffers (P2P loads); all kernels
+ * return at once when *gate == 0.  The caller fences the ranks before (all
+ * weights / rows written) and after (all reads done, before the owners'
+ * spa_resample_commit overwrites them).  ws: spa_resample_workspace_bytes(nparts*M).
+ * spa_resample_commit: gated copy *_alt -> live buffers and logw = logw0. */
+int spa_ipc_export(const void* ptr, void* handle, uint64_t* offset);
+int spa_ipc_open(const void* handle, void** base);
+int spa_ipc_close(void* base);
+int spa_copy_async(void* dst, const void* src, size_t bytes, void* stream);
+int spa_resample_sharded(const double* gate, const double* const* w_parts, int32_t nparts, int64_t M, double u,
+                         int32_t rank, const float* const* beta_parts, const double* const* ll_parts,
+                         const double* const* lp_parts, int32_t ldb, int32_t q, float* beta_alt, double* ll_alt,
+                         double* lp_alt, int64_t* anc, void* ws, size_t ws_bytes, void* stream);
+int spa_resample_commit(const double* gate, float* beta, const float* beta_alt, int32_t ldb, int32_t q, double* ll,
+                        const double* ll_alt, double* lp, const double* lp_alt, double* logw, double logw0, int64_t M,
+                        void* stream);
+
 /* ---- K7/K9: Metropolis-within-Gibbs coordinate moves --------------------
  * smc.py:298-332 (_move_block) / smc.py:177-199 (mwg_sweep): `cycles` sweeps
  * of single-coordinate random-walk updates with per-particle Philox streams

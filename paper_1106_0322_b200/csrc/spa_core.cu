@@ -48,6 +48,20 @@ static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   return fn;
 }
 
+typedef CUresult (*PFN_memGetAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+static PFN_memGetAddressRange mem_range_fn() {
+  static PFN_memGetAddressRange fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_memGetAddressRange>(p);
+  });
+  return fn;
+}
+
 // 16-bit (bf16 / fp16) matrix [rows][cols] row-major; box = 64 columns x
 // box_rows rows, 128B swizzle.
 static int make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t cols, uint64_t rows, uint32_t box_rows,
@@ -1290,7 +1304,7 @@ __global__ void gather_kernel(const float* __restrict__ src, int ld_src, float* 
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < m; row += stride) {
-  const int64_t s = idx[row] - base;
+  const int64_t s = idx[row] - base;  // (callers pass ancestors < N; see peer_gather_kernel for j = N)
   const float* a = src + s * ld_src;
   float* o = dst + row * ld_dst;
   if ((ld_src & 3) == 0 && (ld_dst & 3) == 0) {
@@ -1345,6 +1359,40 @@ __global__ void resample_commit_kernel(const float* __restrict__ beta_alt, float
     lp[row] = lp_alt[row];
     logw[row] = logw0;
   }
+  }
+}
+
+// Sharded resampling (K5 over NVLink): slot row i of this rank takes global
+// ancestor j = anc[i], owned by rank j / M at row j % M, read straight from
+// the owner's particle buffers through CUDA-IPC peer pointers (P2P loads).
+// j = N (a position that rounded to 1.0: the reference's searchsorted
+// returns N and its gather raises) reads the last row instead of out of
+// bounds.
+struct PeerRows {
+  const float* beta[8];
+  const double* ll[8];
+  const double* lp[8];
+};
+__global__ void peer_gather_kernel(const __grid_constant__ PeerRows src, int64_t M, int64_t N, int ldb, int q,
+                                   const int64_t* __restrict__ anc, float* __restrict__ beta_alt,
+                                   double* __restrict__ ll_alt, double* __restrict__ lp_alt,
+                                   const double* __restrict__ gate) {
+  if (gated_off(gate)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < M; row += stride) {
+    const int64_t j = min(anc[row], N - 1);
+    const int r = (int)(j / M);
+    const int64_t off = j - (int64_t)r * M;
+    const float* a = src.beta[r] + off * ldb;
+    float* o = beta_alt + row * ldb;
+    const int q4 = q >> 2;  // ldb % 4 == 0 (checked by the caller)
+    for (int c = lane; c < q4; c += 32) reinterpret_cast<float4*>(o)[c] = reinterpret_cast<const float4*>(a)[c];
+    for (int c = 4 * q4 + lane; c < q; c += 32) o[c] = a[c];
+    if (lane == 0) {
+      ll_alt[row] = src.ll[r][off];
+      lp_alt[row] = src.lp[r][off];
+    }
   }
 }
 
@@ -2244,7 +2292,8 @@ int spa_step_record(const double* res, double* rec, int64_t t, double ess_thresh
 int spa_resample_gated(const double* gate, const double* w, int64_t N, double u, float* beta, float* beta_alt,
                        int32_t ldb, int32_t q, double* ll, double* ll_alt, double* lp, double* lp_alt, double* logw,
                        int64_t* anc, void* ws, size_t ws_bytes, void* stream) {
-  SPA_REQUIRE(gate && w && N > 0 && beta && beta_alt && ll && ll_alt && lp && lp_alt && logw && anc && ws && q > 0,
+  SPA_REQUIRE(gate && w && N > 0 && beta && beta_alt && ll && ll_alt && lp && lp_alt && logw && anc && ws && q > 0 &&
+                  (ldb & 3) == 0,
               kBadArgument, "spa_resample_gated: bad arguments");
   SPA_REQUIRE(ws_bytes >= spa_resample_workspace_bytes(N), kWorkspaceTooSmall,
               "spa_resample_gated: workspace too small");
@@ -2258,7 +2307,12 @@ int spa_resample_gated(const double* gate, const double* w, int64_t N, double u,
   if (rc) return rc;
   ancestors_kernel<<<cdiv(N, 256), 256, 0, st>>>(cumn, N, u, 0, N, anc, gate);
   SPA_CHECK_LAUNCH();
-  gather_kernel<<<std::min<unsigned>(cdiv(N, 8), 8 * 148), 256, 0, st>>>(beta, ldb, beta_alt, ldb, q, anc, 0, N, ll, ll_alt, lp, lp_alt, gate);
+  PeerRows rows{};  // one part: the local buffers (clamps an ancestor index N like the sharded path)
+  rows.beta[0] = beta;
+  rows.ll[0] = ll;
+  rows.lp[0] = lp;
+  peer_gather_kernel<<<std::min<unsigned>(cdiv(N, 8), 8 * 148), 256, 0, st>>>(rows, N, N, ldb, q, anc, beta_alt,
+                                                                             ll_alt, lp_alt, gate);
   SPA_CHECK_LAUNCH();
   resample_commit_kernel<<<std::min<unsigned>(cdiv(N, 8), 8 * 148), 256, 0, st>>>(beta_alt, beta, ldb, q, ll_alt, ll, lp_alt, lp, logw,
                                                       -std::log((double)N), N, gate);
@@ -2482,6 +2536,7 @@ int spa_prepare(void) {
       (const void*)prior_reweight_rows_kernel<32, 16>, (const void*)prior_reweight_kernel<32>, (const void*)lse_stats_kernel, (const void*)lse_combine_kernel,
       (const void*)logw_apply_kernel, (const void*)ancestors_kernel,
       (const void*)gather_kernel, (const void*)step_record_kernel, (const void*)resample_commit_kernel,
+      (const void*)peer_gather_kernel,
       (const void*)reduce_units_kernel, (const void*)rw_mean_kernel<4>, (const void*)rw_cov_kernel,
       (const void*)rw_chol_panel_kernel, (const void*)rw_emit_kernel,
       (const void*)rw_normals_kernel, (const void*)rw_center_kernel, (const void*)rw_accept_kernel<2>,
@@ -2570,6 +2625,94 @@ int spa_rw_accept(float* beta, int32_t ldb, const void* eps, int32_t q, int64_t 
       beta, ldb, reinterpret_cast<const __nv_bfloat16*>(eps),
                                                                q, m, ylin_p, sp_p, lp_p, ll, lp, seed, t, i0, move,
                                                                accepted);
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Peer memory for the sharded sampler (one process per GPU).  A rank exports
+// CUDA-IPC handles of its particle buffers; every other rank opens them once
+// and the gated resampling kernels read remote rows directly (P2P loads over
+// NVLink / NVSwitch), so no host round trip decides or sizes the exchange.
+int spa_ipc_export(const void* ptr, void* handle, uint64_t* offset) {
+  SPA_REQUIRE(ptr && handle && offset, kBadArgument, "spa_ipc_export: bad arguments");
+  auto range = mem_range_fn();
+  SPA_REQUIRE(range != nullptr, kDriverEntryPoint, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  CUresult r = range(&base, &size, (CUdeviceptr)ptr);
+  SPA_REQUIRE(r == CUDA_SUCCESS, kBadArgument, "spa_ipc_export: not a device allocation");
+  cudaIpcMemHandle_t h;
+  SPA_CHECK_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  memcpy(handle, &h, sizeof(h));
+  *offset = (uint64_t)((CUdeviceptr)ptr - base);
+  return 0;
+}
+
+int spa_ipc_open(const void* handle, void** base) {
+  SPA_REQUIRE(handle && base, kBadArgument, "spa_ipc_open: bad arguments");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  SPA_CHECK_CUDA(cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess));
+  return 0;
+}
+
+int spa_ipc_close(void* base) {
+  SPA_REQUIRE(base, kBadArgument, "spa_ipc_close: bad arguments");
+  SPA_CHECK_CUDA(cudaIpcCloseMemHandle(base));
+  return 0;
+}
+
+int spa_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
+  SPA_REQUIRE(dst && src, kBadArgument, "spa_copy_async: bad arguments");
+  if (bytes) SPA_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, as_stream(stream)));
+  return 0;
+}
+
+int spa_resample_sharded(const double* gate, const double* const* w_parts, int32_t nparts, int64_t M, double u,
+                         int32_t rank, const float* const* beta_parts, const double* const* ll_parts,
+                         const double* const* lp_parts, int32_t ldb, int32_t q, float* beta_alt, double* ll_alt,
+                         double* lp_alt, int64_t* anc, void* ws, size_t ws_bytes, void* stream) {
+  SPA_REQUIRE(gate && w_parts && beta_parts && ll_parts && lp_parts && beta_alt && ll_alt && lp_alt && anc && ws,
+              kBadArgument, "spa_resample_sharded: null argument");
+  SPA_REQUIRE(nparts >= 1 && nparts <= 8 && rank >= 0 && rank < nparts && M > 0 && q > 0 && (ldb & 3) == 0,
+              kBadArgument, "spa_resample_sharded: bad shape");
+  const int64_t N = (int64_t)nparts * M;
+  SPA_REQUIRE(ws_bytes >= spa_resample_workspace_bytes(N), kWorkspaceTooSmall,
+              "spa_resample_sharded: workspace too small");
+  cudaStream_t st = as_stream(stream);
+  WSrc src{};
+  PeerRows rows{};
+  for (int r = 0; r < nparts; ++r) {
+    SPA_REQUIRE(w_parts[r] && beta_parts[r] && ll_parts[r] && lp_parts[r], kBadArgument,
+                "spa_resample_sharded: null peer pointer");
+    src.p[r] = w_parts[r];
+    rows.beta[r] = beta_parts[r];
+    rows.ll[r] = ll_parts[r];
+    rows.lp[r] = lp_parts[r];
+  }
+  src.len = M;
+  src.nparts = nparts;
+  // every rank scans the global weights (read over the peer pointers) with
+  // the exact scan, then searches only its own slots
+  int rc = exact_cumsum(src, N, ws, gate, st);
+  if (rc) return rc;
+  const double* cumn = reinterpret_cast<const double*>(reinterpret_cast<char*>(ws) + exact_cumsum_norm_offset(N));
+  ancestors_kernel<<<cdiv(M, 256), 256, 0, st>>>(cumn, N, u, (int64_t)rank * M, M, anc, gate);
+  SPA_CHECK_LAUNCH();
+  peer_gather_kernel<<<std::min<unsigned>(cdiv(M, 8), 8 * 148), 256, 0, st>>>(rows, M, N, ldb, q, anc, beta_alt,
+                                                                             ll_alt, lp_alt, gate);
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+int spa_resample_commit(const double* gate, float* beta, const float* beta_alt, int32_t ldb, int32_t q, double* ll,
+                        const double* ll_alt, double* lp, const double* lp_alt, double* logw, double logw0, int64_t M,
+                        void* stream) {
+  SPA_REQUIRE(gate && beta && beta_alt && ll && ll_alt && lp && lp_alt && logw && M > 0 && q > 0, kBadArgument,
+              "spa_resample_commit: bad arguments");
+  resample_commit_kernel<<<std::min<unsigned>(cdiv(M, 8), 8 * 148), 256, 0, as_stream(stream)>>>(
+      beta_alt, beta, ldb, q, ll_alt, ll, lp_alt, lp, logw, logw0, M, gate);
   SPA_CHECK_LAUNCH();
   return 0;
 }

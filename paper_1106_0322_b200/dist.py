@@ -8,89 +8,89 @@ shards is made partition-invariant by construction:
 
 * RNG streams are keyed by the absolute particle index (smc.py:40-43);
 * log-sum-exp / ESS: per fixed 4096-particle chunk statistics are
-  all-gathered and combined in global chunk order (needs M % 4096 == 0 for
-  bit-identity across world sizes; otherwise still correct, order = rank order);
-* systematic resampling: the normalised weights are all-gathered and every
-  rank runs the bit-exact sequential-cumsum ancestor kernel on the full
-  vector, so all ranks agree on every ancestor; rows whose ancestor lives on
-  another rank are exchanged with one all-to-all (ancestors are monotone in
-  the slot index, so each rank sends one contiguous row range per peer);
-* RW-cov moments are 2^-48 fixed-point integers: the all-reduce SUM is
-  exact and order-independent.
+  all-gathered and combined in global chunk order (bit-identical for any
+  world size when M % 4096 == 0; otherwise still correct);
+* systematic resampling reads the other ranks' memory directly: every rank
+  maps its peers' weight and particle buffers once (CUDA IPC), scans the
+  global weight vector with the exact scan (np.cumsum's bits), searches the
+  ancestors of its own slots and loads those rows from their owners over
+  NVLink (spa_resample_sharded) -- gated on the device-side ESS decision, so
+  a lambda step issues only fixed-size, stream-ordered collectives and never
+  waits on the host;
+* RW-cov moments are 2^-48 fixed-point integers: the all-reduce SUM is exact
+  and order-independent;
+* snapshots are assembled on rank 0 only (peer copies), not all-gathered.
 
-The exchange plan (`resample_plan`) is pure index arithmetic and is tested on
-CPU with the gloo backend (tests/test_dist_gloo.py).
+Collectives run on the caller's current stream (NCCL orders them with the
+surrounding kernels), the covariance-factor stream uses a second process
+group so its all-reduces never interleave with the main stream's.
+`stage_host=True` routes every collective through host copies (gloo): the
+test harness runs several ranks on one GPU that way, where no kernel may
+wait on another rank.
 """
 
 from __future__ import annotations
 
 import ctypes
+import math
 
-import numpy as np
 import torch
 import torch.distributed as dist
 
 
-def resample_plan(anc: np.ndarray, rank: int, world: int, shard: int):
-    """Row-exchange plan for one systematic resampling step.
+def shard_layout(N: int, world: int):
+    """(M, [(rank, first global index)]) of the contiguous particle blocks."""
+    if N % world:
+        raise ValueError(f"N={N} is not divisible by the {world} ranks")
+    M = N // world
+    return M, [(r, r * M) for r in range(world)]
 
-    anc: global ancestors [N] (monotone non-decreasing, identical on all ranks).
-    Returns dict with
-      send_rows[d]  : local source rows (contiguous range) this rank sends to d
-      recv_counts[s]: rows received from s (concatenated in rank order)
-      gather_idx    : for each local slot, its row in the receive buffer
-    """
-    anc = np.asarray(anc, dtype=np.int64)
-    N = anc.size
-    assert N == shard * world
-    owner = anc // shard
-    send_rows = []
-    recv_counts = np.zeros(world, dtype=np.int64)
-    # what does destination d need from me (rank)?
-    for d in range(world):
-        a = anc[d * shard:(d + 1) * shard]
-        mine = a[(a // shard) == rank]
-        if mine.size:
-            lo, hi = int(mine.min()), int(mine.max())
-            send_rows.append(np.arange(lo - rank * shard, hi - rank * shard + 1, dtype=np.int64))
-        else:
-            send_rows.append(np.zeros(0, dtype=np.int64))
-    a = anc[rank * shard:(rank + 1) * shard]
-    o = owner[rank * shard:(rank + 1) * shard]
-    base = np.zeros(world, dtype=np.int64)
-    lo_src = np.zeros(world, dtype=np.int64)
-    for s in range(world):
-        sel = a[o == s]
-        if sel.size:
-            lo_src[s] = sel.min()
-            recv_counts[s] = sel.max() - sel.min() + 1
-    base[1:] = np.cumsum(recv_counts)[:-1]
-    gather_idx = base[o] + (a - lo_src[o])
-    return {"send_rows": send_rows, "recv_counts": recv_counts, "gather_idx": gather_idx}
+
+def owner_of(j: int, M: int):
+    """(rank, local row) of global particle j (the P2P gather's addressing)."""
+    return j // M, j % M
 
 
 class ParticleGroup:
-    """Collectives used by the sampler when particles are sharded."""
+    """Collectives and peer memory used by the sampler when particles are sharded."""
 
-    def __init__(self, pg=None, stage_host: bool = False):
-        """stage_host: run the collectives on host copies (gloo backend; used
-        to test the sharded path with several ranks on one GPU, where no
-        kernel may wait on another rank)."""
+    def __init__(self, pg=None, stage_host: bool = False, _side: bool = True):
         self.pg = pg if pg is not None else dist.group.WORLD
         self.rank = dist.get_rank(self.pg)
         self.world = dist.get_world_size(self.pg)
         self.stage_host = stage_host
+        self._peers = {}  # id(system) -> pointer tables
+        self._opened = {}  # (rank, handle bytes) -> mapped base pointer
+        self._bar = None
+        # the covariance factor is built on a side stream: its collectives
+        # get their own communicator (created collectively, same order on all ranks)
+        self.side = None
+        if _side:
+            pg_side = dist.new_group(ranks=list(range(self.world)))
+            self.side = ParticleGroup(pg_side, stage_host, _side=False)
 
     # -- layout ----------------------------------------------------------
     def shard(self, N: int):
-        if N % self.world:
-            raise ValueError(f"N={N} is not divisible by the {self.world} ranks")
-        M = N // self.world
-        return M, self.rank * M
+        M, blocks = shard_layout(N, self.world)
+        return M, blocks[self.rank][1]
 
     # -- collectives -----------------------------------------------------
     def barrier(self):
         dist.barrier(self.pg)
+
+    def stream_barrier(self):
+        """All ranks' work enqueued before this point on their current
+        streams has finished before anything enqueued after it runs (a
+        stream-ordered one-element all-reduce; a host barrier in stage_host
+        mode)."""
+        if self.stage_host:
+            if torch.cuda.is_available():
+                torch.cuda.synchronize()
+            dist.barrier(self.pg)
+            return
+        if self._bar is None:
+            self._bar = torch.zeros(1, dtype=torch.int32, device=self._dev())
+        dist.all_reduce(self._bar, group=self.pg)
 
     def all_gather_cat(self, t: torch.Tensor) -> torch.Tensor:
         src = t.contiguous().cpu() if self.stage_host else t.contiguous()
@@ -112,57 +112,109 @@ class ParticleGroup:
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.pg)
         return float(t.item())
 
-    def gather_to_all(self, t: torch.Tensor) -> torch.Tensor:
-        return self.all_gather_cat(t)
-
-    def zero_res(self, system):
-        """res vector with lse = 0: log-weights are globally normalised."""
-        r = torch.zeros(3, dtype=torch.float64, device=system.device)
-        return r
-
     def destroy(self):
+        from . import _lib
+
+        for base in self._opened.values():
+            _lib.call("spa_ipc_close", ctypes.c_void_p(base))
+        self._opened.clear()
+        self._peers.clear()
         if dist.is_initialized():
             dist.destroy_process_group()
 
     def _dev(self):
         return torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu")
 
-    # -- resampling row exchange -------------------------------------------
-    def exchange_rows(self, system, anc: torch.Tensor) -> None:
-        """Fill system.beta_alt / ll_alt / lp_alt with the rows of this rank's
-        slots' ancestors, fetching remote rows with one all-to-all."""
+    # -- peer memory ---------------------------------------------------------
+    def _export(self, t: torch.Tensor):
+        from . import _lib
+
+        h = (ctypes.c_uint8 * 64)()
+        off = ctypes.c_uint64(0)
+        _lib.call("spa_ipc_export", ctypes.c_void_p(t.data_ptr()), h, ctypes.byref(off))
+        return bytes(h), int(off.value)
+
+    def _open(self, rank: int, handle: bytes, offset: int) -> int:
+        from . import _lib
+
+        key = (rank, handle)
+        if key not in self._opened:
+            base = ctypes.c_void_p(0)
+            _lib.call("spa_ipc_open", ctypes.create_string_buffer(handle, 64), ctypes.byref(base))
+            self._opened[key] = int(base.value)
+        return self._opened[key] + offset
+
+    def setup_peers(self, system) -> None:
+        """Map every rank's weight / particle buffers (system.w, beta, ll,
+        lp -- fixed allocations for the life of the system) into this
+        process: the pointer tables of spa_resample_sharded / snapshots."""
+        names = ("w", "beta", "ll", "lp")
+        mine = [self._export(getattr(system, n)) for n in names]
+        blob = torch.zeros((len(names), 72), dtype=torch.uint8)
+        for i, (h, off) in enumerate(mine):
+            blob[i, :64] = torch.frombuffer(bytearray(h), dtype=torch.uint8)
+            blob[i, 64:] = torch.tensor(list(int(off).to_bytes(8, "little")), dtype=torch.uint8)
+        dev_blob = blob.to(self._dev()) if not self.stage_host else blob
+        allb = self.all_gather_cat(dev_blob.view(1, len(names), 72)).cpu()
+        tables = {n: (ctypes.c_void_p * self.world)() for n in names}
+        for r in range(self.world):
+            for i, n in enumerate(names):
+                if r == self.rank:
+                    tables[n][r] = getattr(system, n).data_ptr()
+                else:
+                    row = bytes(allb[r, i].numpy().tobytes())
+                    tables[n][r] = self._open(r, row[:64], int.from_bytes(row[64:], "little"))
+        tables["ptrs"] = {n: getattr(system, n).data_ptr() for n in names}
+        self._peers[id(system)] = tables
+
+    def peer_tables(self, system):
+        t = self._peers.get(id(system))
+        if t is None:
+            raise RuntimeError("ParticleGroup.setup_peers(system) was not called")
+        for n, p in t["ptrs"].items():  # the mapped buffers must not have moved
+            if getattr(system, n).data_ptr() != p:
+                raise RuntimeError(f"sharded particle buffer '{n}' was reallocated after setup_peers")
+        return t
+
+    # -- the exchange ----------------------------------------------------------
+    def resample(self, system, gate: ctypes.c_void_p, u: float, ws: torch.Tensor, anc: torch.Tensor) -> None:
+        """Device-decided global systematic resampling of the sharded set
+        (gated on *gate): fence, exact global scan + own-slot ancestors + P2P
+        row gather, fence, commit.  system.w must hold the globally
+        normalised weights."""
         from . import _lib
         from .smc import _p, _stream
 
-        M = system.N
-        plan = resample_plan(anc.cpu().numpy(), self.rank, self.world, M)
-        dev = system.device
-        send_idx = torch.from_numpy(np.concatenate(plan["send_rows"])).to(dev)
-        send_counts = [int(r.size) for r in plan["send_rows"]]
-        recv_counts = [int(c) for c in plan["recv_counts"]]
-        nsend, nrecv = int(sum(send_counts)), int(sum(recv_counts))
-        W = system.ldb + 4  # row payload: beta (ldb floats) + ll, lp (2 doubles as 4 floats)
-        sendbuf = torch.empty((max(nsend, 1), W), dtype=torch.float32, device=dev)
-        recvbuf = torch.empty((max(nrecv, 1), W), dtype=torch.float32, device=dev)
-        if nsend:
-            sb64 = sendbuf.view(torch.float64)  # [n, W/2] doubles view of the same storage
-            ll_col = torch.empty(nsend, dtype=torch.float64, device=dev)
-            lp_col = torch.empty(nsend, dtype=torch.float64, device=dev)
-            _lib.call("spa_gather_rows", _p(system.beta), system.ldb, _p(sendbuf), W, system.q, _p(send_idx), 0, nsend,
-                      _p(system.ll), _p(ll_col), _p(system.lp), _p(lp_col), _stream())
-            sb64[:nsend, system.ldb // 2] = ll_col
-            sb64[:nsend, system.ldb // 2 + 1] = lp_col
-        if self.stage_host:
-            rh = torch.empty((nrecv, W), dtype=torch.float32)
-            dist.all_to_all_single(rh, sendbuf[:nsend].cpu(), output_split_sizes=recv_counts,
-                                   input_split_sizes=send_counts, group=self.pg)
-            recvbuf[:nrecv].copy_(rh)
-        else:
-            dist.all_to_all_single(recvbuf[:nrecv], sendbuf[:nsend], output_split_sizes=recv_counts,
-                                   input_split_sizes=send_counts, group=self.pg)
-        rb64 = recvbuf.view(torch.float64)
-        gidx = torch.from_numpy(plan["gather_idx"]).to(dev)
-        ll_in = rb64[:, system.ldb // 2].contiguous()
-        lp_in = rb64[:, system.ldb // 2 + 1].contiguous()
-        _lib.call("spa_gather_rows", _p(recvbuf), W, _p(system.beta_alt), system.ldb, system.q, _p(gidx), 0, M,
-                  _p(ll_in), _p(system.ll_alt), _p(lp_in), _p(system.lp_alt), _stream())
+        tb = self.peer_tables(system)
+        self.stream_barrier()  # every rank's weights and rows are final
+        _lib.call("spa_resample_sharded", gate, tb["w"], self.world, system.N, float(u), self.rank, tb["beta"],
+                  tb["ll"], tb["lp"], system.ldb, system.q, _p(system.beta_alt), _p(system.ll_alt),
+                  _p(system.lp_alt), _p(anc), _p(ws), ws.numel(), _stream())
+        self.stream_barrier()  # every rank has read its ancestors' rows
+        _lib.call("spa_resample_commit", gate, _p(system.beta), _p(system.beta_alt), system.ldb, system.q,
+                  _p(system.ll), _p(system.ll_alt), _p(system.lp), _p(system.lp_alt), _p(system.logw),
+                  -math.log(system.N_total), system.N, _stream())
+
+    def snapshot_to_rank0(self, system, w: torch.Tensor):
+        """Rank 0 assembles the global (weights, particles [N][q], ll) from
+        the peers' buffers; other ranks return None.  w: this rank's globally
+        normalised weights (system.w)."""
+        from . import _lib
+        from .smc import _stream
+
+        tb = self.peer_tables(system)
+        self.stream_barrier()
+        out = None
+        if self.rank == 0:
+            M, ldb, q = system.N, system.ldb, system.q
+            dev = system.device
+            W = torch.empty(M * self.world, dtype=torch.float64, device=dev)
+            B = torch.empty((M * self.world, ldb), dtype=torch.float32, device=dev)
+            LL = torch.empty(M * self.world, dtype=torch.float64, device=dev)
+            for r in range(self.world):
+                for dst, src, nb in ((W, tb["w"][r], 8 * M), (B, tb["beta"][r], 4 * M * ldb), (LL, tb["ll"][r], 8 * M)):
+                    _lib.call("spa_copy_async", ctypes.c_void_p(dst.data_ptr() + r * nb), ctypes.c_void_p(src), nb,
+                              _stream())
+            out = (W, B[:, :q], LL)
+        self.stream_barrier()  # the peers keep their buffers until rank 0 has copied
+        return out

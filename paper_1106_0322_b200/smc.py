@@ -18,6 +18,10 @@ Extra SmcConfig fields (defaults keep the reference's behaviour):
     summary_levels / summary_deltas
                  per-step weighted marginal summaries computed on the device
                  (StepRecord.summary; see marginal_summaries)
+    summary_pooled
+                 also the pooled posterior's marginals over all steps
+                 (summary.py:126-140; SmcOutput.pooled), from every step's
+                 particles kept on the device -- no snapshots needed
     rw_factor_lag
                  RW covariance factor pipelining: 0 = every move of step t
                  uses the factor of step t's population (computed before the
@@ -48,6 +52,16 @@ TAG_INIT, TAG_MOVE, TAG_RESAMPLE, TAG_RWMOVE = 0, 1, 2, 3
 # Optional CUDA-event timer around the dominant kernel (bench.py sets it;
 # events are recorded on the launching stream).
 KERNEL_TIMER = None
+
+
+def _nvtx_push(name: str) -> None:
+    """NVTX range around a phase of the lambda step (reweight, resample,
+    cov, move, snapshot) for timelines / `ncu --nvtx`."""
+    torch.cuda.nvtx.range_push(name)
+
+
+def _nvtx_pop() -> None:
+    torch.cuda.nvtx.range_pop()
 _CHUNK = 4096
 TRACE_COLUMNS = ("t", "b", "ess", "log_z_ratio_cum", "acceptance_rate")
 
@@ -108,6 +122,7 @@ class SmcConfig:
     summary_levels: tuple = ()
     summary_deltas: tuple = ()
     rw_factor_lag: int = 1
+    summary_pooled: bool = False
 
     def __post_init__(self):
         if self.N < 2:
@@ -132,6 +147,8 @@ class SmcConfig:
             raise ValueError("summary_levels: at most 4 quantile levels in (0, 1)")
         if len(self.summary_deltas) > 4 or not all(float(v) > 0.0 for v in self.summary_deltas):
             raise ValueError("summary_deltas: at most 4 positive deltas")
+        if self.summary_pooled and not (self.summary_levels or self.summary_deltas):
+            raise ValueError("summary_pooled needs summary_levels and/or summary_deltas")
 
 
 @dataclass
@@ -162,6 +179,7 @@ class SmcOutput:
     steps: list
     init_acceptance: float
     timings: dict = field(default_factory=dict)
+    pooled: dict | None = None  # SmcConfig.summary_pooled: pooled-posterior marginals (summary.pooled_marginals)
 
     @property
     def c_values(self) -> np.ndarray:
@@ -299,10 +317,26 @@ class ParticleSystem:
                                  dtype=torch.float64, device=dev),
                 info=torch.zeros(1, dtype=torch.int32, device=dev),
                 ctr=torch.zeros(q, dtype=torch.float32, device=dev),  # centring point (previous mean)
+                wf=torch.empty(self.N, dtype=torch.float64, device=dev),  # the factor's normalised weights
+                statsf=torch.empty((self.nchunks, 3), dtype=torch.float64, device=dev),
+                resf=torch.empty(3, dtype=torch.float64, device=dev),
                 mws=torch.empty(max(_lib.load().spa_rw_moments_workspace_bytes(self.N, q), 8), dtype=torch.uint8,
                                 device=dev),
             )
         return self._rw
+
+    def resample_buffers(self):
+        """(exact-scan workspace for the global N, this shard's ancestor slots)."""
+        if getattr(self, "_rs_ws", None) is None:
+            self._rs_ws = torch.empty(_lib.load().spa_resample_workspace_bytes(self.N_total), dtype=torch.uint8,
+                                      device=self.device)
+            self._anc = torch.empty(self.N, dtype=torch.int64, device=self.device)
+        return self._rs_ws, self._anc
+
+    def gate_one(self):
+        if getattr(self, "_one", None) is None:
+            self._one = torch.ones(1, dtype=torch.float64, device=self.device)
+        return self._one
 
     def side_stream(self):
         if getattr(self, "_side", None) is None:
@@ -415,18 +449,23 @@ def systematic_resample(system: ParticleSystem, rng_or_u, group=None) -> np.ndar
 
 
 def _resample_device(system: ParticleSystem, u: float, group=None) -> torch.Tensor:
+    """Systematic resampling now (host-decided).  Sharded: the ancestors of
+    this rank's slots (global indices), rows fetched from their owners over
+    peer memory, buffers updated in place."""
     N = system.N_total
-    # normalised weights (smc.py:151-154) of this shard, gathered over shards
-    w = system.device_weights() if group is None else _global_weights(system, group)
-    w_full = w if group is None else group.all_gather_cat(w)
+    if group is not None:
+        _global_weights(system, group)
+        ws, anc = system.resample_buffers()
+        one = system.gate_one()
+        group.resample(system, ctypes.c_void_p(one.data_ptr()), u, ws, anc)
+        return anc
+    # normalised weights (smc.py:151-154)
+    w = system.device_weights()
     anc = torch.empty(N, dtype=torch.int64, device=system.device)
     ws = torch.empty(_lib.load().spa_resample_workspace_bytes(N), dtype=torch.uint8, device=system.device)
-    _lib.call("spa_systematic_ancestors", _p(w_full), N, u, 0, N, _p(anc), _p(ws), ws.numel(), _stream())
-    if group is None:
-        _lib.call("spa_gather_rows", _p(system.beta), system.ldb, _p(system.beta_alt), system.ldb, system.q, _p(anc),
-                  0, system.N, _p(system.ll), _p(system.ll_alt), _p(system.lp), _p(system.lp_alt), _stream())
-    else:
-        group.exchange_rows(system, anc)
+    _lib.call("spa_systematic_ancestors", _p(w), N, u, 0, N, _p(anc), _p(ws), ws.numel(), _stream())
+    _lib.call("spa_gather_rows", _p(system.beta), system.ldb, _p(system.beta_alt), system.ldb, system.q, _p(anc),
+              0, system.N, _p(system.ll), _p(system.ll_alt), _p(system.lp), _p(system.lp_alt), _stream())
     system.beta, system.beta_alt = system.beta_alt, system.beta
     system.ll, system.ll_alt = system.ll_alt, system.ll
     system.lp, system.lp_alt = system.lp_alt, system.lp
@@ -468,7 +507,9 @@ def _rw_factor(system: ParticleSystem, scale: float, group=None, buf: int = 0, c
     seeds that centre with a mean pass.  `centred` (optional event) is
     recorded once the particles have been read for the last time."""
     rw = system.rw_workspace()
-    w = system.device_weights() if group is None else _global_weights(system, group)
+    # normalised weights into the factor's own buffers (this may run on a
+    # side stream beside the main stream's use of system.w / stats / res)
+    w = _normalised_weights(system, group, (rw["wf"], rw["statsf"], rw["resf"]))
     rw["acc"].zero_()
     if not getattr(system, "_ctr_ready", False):
         _lib.call("spa_rw_moments", _p(system.beta), system.N, system.ldb, system.q, _p(w), None, 0, _p(rw["acc"]),
@@ -493,14 +534,22 @@ def _rw_factor(system: ParticleSystem, scale: float, group=None, buf: int = 0, c
     _lib.add_launches(2 + 2 * panels - 1)  # cov + graph of panel kernels + emit
 
 
+def _normalised_weights(system, group=None, out=None):
+    """Normalised weights exp(logw - lse(logw)) (smc.py:151-154) into
+    out = (w, stats, res) (default: the system's buffers); sharded, the LSE
+    runs over ALL shards with the same fixed-chunk combine as one process
+    (identical bits)."""
+    w, stats, res = out if out is not None else (system.w, system.stats, system.res)
+    _lib.call("spa_lse_chunk_stats", _p(system.logw), None, system.N, _p(stats), _stream())
+    allst = stats if group is None else group.all_gather_cat(stats)
+    _lib.call("spa_lse_combine", _p(allst), allst.shape[0], _p(res), _stream())
+    _lib.call("spa_logw_apply", _p(system.logw), None, system.N, _p(res), _p(w), _stream())
+    return w
+
+
 def _global_weights(system, group):
-    """Normalised weights exp(logw - lse(logw)) with the LSE over ALL shards
-    (same fixed-chunk combine as the single-process path => identical bits)."""
-    _lib.call("spa_lse_chunk_stats", _p(system.logw), None, system.N, _p(system.stats), _stream())
-    stats = group.all_gather_cat(system.stats)
-    _lib.call("spa_lse_combine", _p(stats), stats.shape[0], _p(system.res), _stream())
-    _lib.call("spa_logw_apply", _p(system.logw), None, system.N, _p(system.res), _p(system.w), _stream())
-    return system.w
+    """system.w = the globally normalised weights of this shard."""
+    return _normalised_weights(system, group)
 
 
 def _launch_normals(system: ParticleSystem, config: SmcConfig, t: int, mv: int):
@@ -581,7 +630,9 @@ def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int,
         centred, factored = torch.cuda.Event(), torch.cuda.Event()
         fs.wait_stream(main)
         with torch.cuda.stream(fs):
-            _rw_factor(system, config.rw_scale, group, buf=nxt, centred=centred)
+            _nvtx_push("cov")
+            _rw_factor(system, config.rw_scale, None if group is None else group.side, buf=nxt, centred=centred)
+            _nvtx_pop()
             factored.record()
     else:
         _rw_factor(system, config.rw_scale, group, buf=cur)
@@ -714,6 +765,8 @@ def init_particles(data, prior_at_b1: GtPrior, config: SmcConfig, intercept: boo
     if group is not None:
         tally = group.all_reduce_sum(tally)
     acc, total = (int(v) for v in tally.tolist())
+    if group is not None:
+        group.setup_peers(system)  # map the peers' particle buffers (the resampling exchange reads them)
     return system, acc / max(total, 1)
 
 
@@ -759,10 +812,12 @@ def resolve_records(system: ParticleSystem, steps: list) -> None:
         system.log_z_cum = float(rec[steps[-1].t, 3])
 
 
-def _smc_step_async(system: ParticleSystem, schedule: Schedule, t: int, config: SmcConfig) -> StepRecord:
-    """One lambda step with no host synchronisation (single process): the
-    ESS test runs on the device (spa_step_record) and resampling is gated on
-    its flag (spa_resample_gated), so the host only enqueues launches.  The
+def _smc_step_async(system: ParticleSystem, schedule: Schedule, t: int, config: SmcConfig,
+                    group=None) -> StepRecord:
+    """One lambda step with no host synchronisation: the ESS test runs on
+    the device (spa_step_record) and resampling is gated on its flag
+    (spa_resample_gated; sharded: group.resample, peer-memory exchange), so
+    the host only enqueues launches and fixed-size collectives.  The
     arithmetic is the host-decided path's (bit-identical particles, weights
     and evidence); the record's ESS / evidence / resampled / acceptance are
     resolved after the loop by resolve_records."""
@@ -776,34 +831,45 @@ def _smc_step_async(system: ParticleSystem, schedule: Schedule, t: int, config: 
     if getattr(system, "_records", None) is None or system._records.shape[0] < schedule.T + 1:
         system._records = torch.zeros((schedule.T + 1, 4), dtype=torch.float64, device=system.device)
         system._records[:, 3] = system.log_z_cum
-        system._rs_ws = torch.empty(_lib.load().spa_resample_workspace_bytes(system.N), dtype=torch.uint8,
-                                    device=system.device)
-        system._anc = torch.empty(system.N, dtype=torch.int64, device=system.device)
     rec = system._records
+    ws, anc = system.resample_buffers()
+    _nvtx_push("reweight")
     _lib.call("spa_prior_reweight", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb,
               float(prior_t.a), float(prior_t.c), float(prior_prev.c), _p(system.lw), _p(system.lp), _stream())
     _lib.call("spa_lse_chunk_stats", _p(system.logw), _p(system.lw), system.N, _p(system.stats), _stream())
-    _lib.call("spa_lse_combine", _p(system.stats), system.nchunks, _p(system.res), _stream())
+    stats = system.stats if group is None else group.all_gather_cat(system.stats)
+    _lib.call("spa_lse_combine", _p(stats), stats.shape[0], _p(system.res), _stream())
     _lib.call("spa_logw_apply", _p(system.logw), _p(system.lw), system.N, _p(system.res), None, _stream())
     _lib.call("spa_step_record", _p(system.res), _p(rec), t, float(config.ess_threshold_frac * N), _stream())
-    w = system.device_weights()
+    _nvtx_pop()
+    _nvtx_push("resample")
     u = first_uniform(config.seed, TAG_RESAMPLE, t) / N
     gate = ctypes.c_void_p(rec.data_ptr() + (4 * t + 2) * 8)
-    _lib.call("spa_resample_gated", gate, _p(w), system.N, u, _p(system.beta), _p(system.beta_alt), system.ldb,
-              system.q, _p(system.ll), _p(system.ll_alt), _p(system.lp), _p(system.lp_alt), _p(system.logw),
-              _p(system._anc), _p(system._rs_ws), system._rs_ws.numel(), _stream())
+    if group is None:
+        w = system.device_weights()
+        _lib.call("spa_resample_gated", gate, _p(w), system.N, u, _p(system.beta), _p(system.beta_alt), system.ldb,
+                  system.q, _p(system.ll), _p(system.ll_alt), _p(system.lp), _p(system.lp_alt), _p(system.logw),
+                  _p(anc), _p(ws), ws.numel(), _stream())
+    else:
+        _global_weights(system, group)
+        group.resample(system, gate, u, ws, anc)
+    _nvtx_pop()
+    _nvtx_push("move")
     if config.move_kernel == "mwg":
         cnt = torch.zeros(1, dtype=torch.int64, device=system.device)
         _lib.call("spa_mwg_move", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb, float(prior_t.a),
                   float(prior_t.c), float(config.step_sd), int(config.cycles), int(config.seed), TAG_MOVE, int(t),
                   int(system.i0), 0, _p(system.ll), _p(system.lp), _p(cnt), 0, _stream())
+        if group is not None:
+            group.all_reduce_sum(cnt)
         acceptance = _LazyRate(cnt, N * config.cycles * system.q)
     else:
         if t == 2 or not getattr(system, "_ll_from_k1", False):
             _loglik_device(system, system.ll)
             system._ll_from_k1 = True
-        acc = _rw_moves(system, prior_t, config, t, None, z_ready)
+        acc = _rw_moves(system, prior_t, config, t, group, z_ready)
         acceptance = _LazyRate(acc, N * config.moves)
+    _nvtx_pop()
     system.t = t
     return StepRecord(t, float(bs[t - 1]), _Pending(t, 1), _Pending(t, 3), acceptance, _Pending(t, 2))
 
@@ -813,15 +879,15 @@ def smc_step(system: ParticleSystem, data, schedule: Schedule, t: int, config: S
     """Advance from step t-1 to t: reweight -> accumulate evidence -> ESS ->
     resample if ESS < frac*N -> move with the invariant kernel at prior_t.
 
-    _defer (internal; run_sampler and the bench): single-process steps run
-    without host synchronisation and return records with pending fields,
+    _defer (internal; run_sampler and the bench): steps run without host
+    synchronisation (also sharded) and return records with pending fields,
     resolved by resolve_records."""
     if not 2 <= t <= schedule.T:
         raise ValueError(f"step index {t} outside [2, {schedule.T}]")
     if system.t != t - 1:
         raise ValueError(f"system is at step {system.t}, cannot advance to {t}")
-    if _defer and group is None:
-        return _smc_step_async(system, schedule, t, config)
+    if _defer:
+        return _smc_step_async(system, schedule, t, config, group)
     a = system.prior_a
     bs = schedule.bs
     prior_prev = GtPrior(a, prior_scale(a, bs[t - 2]))
@@ -866,11 +932,16 @@ def marginal_summaries(system: ParticleSystem, levels=(0.05, 0.5, 0.95), deltas=
     and get the same result for any number of GPUs.  Returns device float64
     tensors {"mean": [q], "quantiles": [len(levels)][q], "concentration":
     [len(deltas)][q]} (written into `out` when given)."""
-    q, dev = system.q, system.device
+    w = system.device_weights() if group is None else _global_weights(system, group)
+    return _weighted_marginals(system.beta, system.N, system.ldb, system.q, w, levels, deltas, group, out)
+
+
+def _weighted_marginals(beta, m, ldb, q, w, levels, deltas, group=None, out=None):
+    """The summary kernels on rows beta[m][ldb] (float32) with weights w[m]."""
+    dev = beta.device
     lv = (ctypes.c_double * max(1, len(levels)))(*[float(v) for v in levels])
     dl = (ctypes.c_double * max(1, len(deltas)))(*[float(v) for v in deltas])
     nl, nd = len(levels), len(deltas)
-    w = system.device_weights() if group is None else _global_weights(system, group)
     u64 = dict(dtype=torch.int64, device=dev)
     hist = torch.zeros((max(1, nl), q, 256), **u64)
     acc_mean = torch.zeros(q, **u64)
@@ -885,7 +956,7 @@ def marginal_summaries(system: ParticleSystem, levels=(0.05, 0.5, 0.95), deltas=
     for ps in range(4 if nl else 1):
         if ps:
             hist.zero_()
-        _lib.call("spa_summary_pass", _p(system.beta), system.N, system.ldb, q, _p(w), nl, lv, nd, dl, ps,
+        _lib.call("spa_summary_pass", _p(beta), m, ldb, q, _p(w), nl, lv, nd, dl, ps,
                   _p(prefix), _p(hist), _p(acc_mean), _p(acc_in), _p(total), _stream())
         if group is not None:
             group.all_reduce_sum(hist)
@@ -897,6 +968,39 @@ def marginal_summaries(system: ParticleSystem, levels=(0.05, 0.5, 0.95), deltas=
     _lib.call("spa_summary_finish", q, nl, nd, _p(prefix), _p(acc_mean), _p(acc_in), _p(total), _p(out["mean"]),
               _p(out["quantiles"]) if nl else None, _p(out["concentration"]) if nd else None, _stream())
     return out
+
+
+class _PooledStore:
+    """Every step's particles and normalised weights kept on the device
+    (SmcConfig.summary_pooled) for the pooled posterior of
+    summary.py:126-140: all particles of all steps, particle k of step t
+    weighted by the c-posterior mass of t (Z_t/Z_1 normalised over the
+    grid, summary.py:113-122) times its normalised weight.  The pooled
+    marginals run the same exact-sum summary kernels over the T*N rows."""
+
+    def __init__(self, system: ParticleSystem, T: int):
+        self.beta = torch.empty((T, system.N, system.ldb), dtype=torch.float32, device=system.device)
+        self.w = torch.empty((T, system.N), dtype=torch.float64, device=system.device)
+        self.system = system
+
+    def add(self, t: int, group=None):
+        s = self.system
+        w = s.device_weights() if group is None else _global_weights(s, group)
+        self.w[t - 1].copy_(w)
+        self.beta[t - 1].copy_(s.beta)
+
+    def summarise(self, steps, levels, deltas, group=None):
+        log_z = np.array([st.log_z_ratio_cum for st in steps])
+        mass = np.exp(log_z - log_z.max())
+        mass /= mass.sum()
+        T = len(steps)
+        s = self.system
+        wp = (torch.from_numpy(mass).to(s.device)[:, None] * self.w[:T]).reshape(-1)
+        out = _weighted_marginals(self.beta[:T].reshape(T * s.N, s.ldb), T * s.N, s.ldb, s.q, wp, levels, deltas,
+                                  group)
+        res = {k: v.cpu().numpy() for k, v in out.items()}
+        res.update(levels=tuple(float(v) for v in levels), deltas=tuple(float(v) for v in deltas), mass=mass)
+        return res
 
 
 class _SnapshotWriter:
@@ -916,12 +1020,14 @@ class _SnapshotWriter:
         self.stage = None
 
     def submit(self, system: ParticleSystem, record: StepRecord, group=None):
-        w = system.device_weights() if group is None else _global_weights(system, group)
-        beta = system.beta[:, : system.q]
-        ll = system.ll
-        if group is not None:
-            w, beta, ll = group.gather_to_all(w), group.gather_to_all(beta.contiguous()), group.gather_to_all(ll)
-        clones = (w.clone(), beta.contiguous() if group is not None else beta.clone(), ll.clone())
+        if group is None:
+            w = system.device_weights()
+            clones = (w.clone(), system.beta[:, : system.q].clone(), system.ll.clone())
+        else:  # rank 0 assembles the global arrays from the peers' buffers; the others keep none
+            got = group.snapshot_to_rank0(system, _global_weights(system, group))
+            if got is None:
+                return record
+            clones = (got[0], got[1].contiguous(), got[2])
         ev = torch.cuda.Event()
         ev.record()
         dev = system.device
@@ -1001,7 +1107,11 @@ def run_sampler(data, a: float, schedule: Schedule, config: SmcConfig, intercept
                 "quantiles": torch.empty((T, len(config.summary_levels), q), **f64),
                 "concentration": torch.empty((T, len(config.summary_deltas), q), **f64)}
 
+    pool = _PooledStore(system, schedule.T) if config.summary_pooled else None
+
     def snap(rec):
+        if pool is not None:
+            pool.add(rec.t, group)
         if summ is not None:  # every step, retained or not (no host sync)
             marginal_summaries(system, config.summary_levels, config.summary_deltas, group,
                                out={k: v[rec.t - 1] for k, v in summ.items()})
@@ -1025,6 +1135,10 @@ def run_sampler(data, a: float, schedule: Schedule, config: SmcConfig, intercept
             for s in steps:
                 s.summary = {"mean": host["mean"][s.t - 1], "quantiles": host["quantiles"][s.t - 1],
                              "concentration": host["concentration"][s.t - 1], **names_k}
+        pooled = None
+        if pool is not None:
+            pooled = pool.summarise(steps, config.summary_levels, config.summary_deltas, group)
+            del pool
         torch.cuda.synchronize()
         timings["path_s"] = time.perf_counter() - t1
         ts = time.perf_counter()
@@ -1032,7 +1146,7 @@ def run_sampler(data, a: float, schedule: Schedule, config: SmcConfig, intercept
         writer.close()
     timings["snapshot_drain_s"] = time.perf_counter() - ts
     timings["resampling_steps"] = sum(1 for s in steps if s.resampled)
-    return SmcOutput(float(a), schedule, config, intercept, names, steps, init_acc, timings)
+    return SmcOutput(float(a), schedule, config, intercept, names, steps, init_acc, timings, pooled)
 
 
 def fixed_b_mcmc(data, prior: GtPrior, n_samples: int, burn: int = 2000, thin: int = 5, seed: int = 0,

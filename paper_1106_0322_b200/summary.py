@@ -11,6 +11,9 @@ with the reference's names and shapes (summary.py:64-94, 113-122):
     abs_median_path(out)        -> [T][q]   (summary.py:77-79)
     concentration_path(out, d)  -> [T][q]   (summary.py:88-97), d one of the deltas
     c_posterior(out)            -> CPosterior (summary.py:113-122)
+    pooled_posterior(out)       -> PooledPosterior from snapshots (summary.py:126-140)
+    pooled_marginals(out)       -> the pooled posterior's mean / quantiles / V(delta)
+                                   computed on the device (SmcConfig.summary_pooled)
 
 Quantiles follow summary.py:36-45 exactly (smallest value whose cumulative
 weight reaches the level), the mean and V(delta) to float64 rounding.
@@ -82,3 +85,32 @@ def c_posterior(output) -> CPosterior:
     mass = np.exp(log_z - log_z.max())
     mass /= mass.sum()
     return CPosterior(output.c_values[: len(output.steps)], mass)
+
+
+@dataclass
+class PooledPosterior:
+    """All particles from all steps, weighted by evidence and local weight (summary.py:126-130)."""
+
+    samples: np.ndarray
+    weights: np.ndarray
+
+
+def pooled_posterior(output) -> PooledPosterior:
+    """summary.py:133-140 on retained snapshots (every step must be kept)."""
+    if any(s.particles is None for s in output.steps):
+        raise SummaryError("pooled_posterior needs every step's particles (snapshot_thin=1); "
+                           "use SmcConfig(summary_pooled=True) and pooled_marginals for the device version")
+    mass = c_posterior(output).mass
+    samples = np.concatenate([s.particles for s in output.steps], axis=0)
+    weights = np.concatenate([m * s.weights for m, s in zip(mass, output.steps)])
+    return PooledPosterior(samples, weights / weights.sum())
+
+
+def pooled_marginals(output) -> dict:
+    """Weighted mean, quantiles at the configured levels and V(delta) of the
+    pooled posterior (summary.py:126-140 marginals), computed on the device
+    over every step's particles: {"mean": [q], "quantiles": [L][q],
+    "concentration": [D][q], "levels", "deltas", "mass"}."""
+    if getattr(output, "pooled", None) is None:
+        raise SummaryError("no pooled summaries: run with SmcConfig(summary_pooled=True, summary_levels=...)")
+    return output.pooled
