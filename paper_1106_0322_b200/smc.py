@@ -185,6 +185,18 @@ class SmcOutput:
     def c_values(self) -> np.ndarray:
         return self.schedule.bs if math.isinf(self.a) else self.schedule.bs / self.a
 
+    @property
+    def evidence_validated(self) -> bool:
+        """Whether log_z_ratio_cum is inside the validated envelope.  The
+        reference's MwG kernel: yes.  The RW population-covariance move
+        (north-star throughput kernel): its marginal posteriors pass the
+        reference's fixed-b criterion at C3, but its
+        evidence carries a finite-N mixing bias (+1.5 nats at C3 with
+        N=65536 and 5 moves, SD 0.6; MwG 0.013), so evidence-derived
+        summaries (summary.c_posterior, pooled posterior) refuse RW runs
+        unless asked explicitly."""
+        return self.config.move_kernel == "mwg"
+
     def step(self, t: int) -> StepRecord:
         return self.steps[t - 1]
 

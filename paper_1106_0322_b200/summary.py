@@ -79,8 +79,16 @@ class CPosterior:
         return float(self.c[self.mode_index])
 
 
-def c_posterior(output) -> CPosterior:
+def _require_validated_evidence(output, allow_unvalidated: bool):
+    if not allow_unvalidated and not getattr(output, "evidence_validated", True):
+        raise SummaryError("the evidence of a move_kernel='rw' run is outside the validated envelope (finite-N mixing "
+                           "bias, DESIGN.md section 4): use move_kernel='mwg' for c-posterior / pooled summaries, or "
+                           "pass allow_unvalidated=True")
+
+
+def c_posterior(output, allow_unvalidated: bool = False) -> CPosterior:
     """Evidence ratios normalised over the scale grid (summary.py:113-122)."""
+    _require_validated_evidence(output, allow_unvalidated)
     log_z = np.array([s.log_z_ratio_cum for s in output.steps])
     mass = np.exp(log_z - log_z.max())
     mass /= mass.sum()
@@ -95,22 +103,24 @@ class PooledPosterior:
     weights: np.ndarray
 
 
-def pooled_posterior(output) -> PooledPosterior:
+def pooled_posterior(output, allow_unvalidated: bool = False) -> PooledPosterior:
     """summary.py:133-140 on retained snapshots (every step must be kept)."""
+    _require_validated_evidence(output, allow_unvalidated)
     if any(s.particles is None for s in output.steps):
         raise SummaryError("pooled_posterior needs every step's particles (snapshot_thin=1); "
                            "use SmcConfig(summary_pooled=True) and pooled_marginals for the device version")
-    mass = c_posterior(output).mass
+    mass = c_posterior(output, allow_unvalidated).mass
     samples = np.concatenate([s.particles for s in output.steps], axis=0)
     weights = np.concatenate([m * s.weights for m, s in zip(mass, output.steps)])
     return PooledPosterior(samples, weights / weights.sum())
 
 
-def pooled_marginals(output) -> dict:
+def pooled_marginals(output, allow_unvalidated: bool = False) -> dict:
     """Weighted mean, quantiles at the configured levels and V(delta) of the
     pooled posterior (summary.py:126-140 marginals), computed on the device
     over every step's particles: {"mean": [q], "quantiles": [L][q],
     "concentration": [D][q], "levels", "deltas", "mass"}."""
+    _require_validated_evidence(output, allow_unvalidated)
     if getattr(output, "pooled", None) is None:
         raise SummaryError("no pooled summaries: run with SmcConfig(summary_pooled=True, summary_levels=...)")
     return output.pooled

@@ -10,6 +10,9 @@
          worst 90%-endpoint diff < 0.1)
   c3z    C3 at N=8192: 6 RW (5 moves) vs 6 MwG (5 cycles) replicates, z of
          the weighted means, medians and log Z_t/Z_1 along the path
+  c3n    C3: RW replicates at N in {8192, 65536} x moves in {5, 10, 20} vs 6
+         MwG replicates at N=8192 (device marginal summaries, so it is fast):
+         log Z_T mean / SD and the z of the means / medians along the path
 
     python tools/rw_validate.py [c1] [crit8] [c3z]   (JSON lines on stdout)
 """
@@ -116,6 +119,41 @@ def c3z(N=8192, R=6):
          z_logz_max=float(np.abs(zl).max()), logz_T_mwg=float(mw["logz"][:, -1].mean()),
          logz_T_rw=float(rw["logz"][:, -1].mean()), logz_T_sd_mwg=float(mw["logz"][:, -1].std(ddof=1)),
          logz_T_sd_rw=float(rw["logz"][:, -1].std(ddof=1)), mwg_s=t1 - t0, rw_s=t2 - t1)
+
+
+def dev_reps(data, a, sched, seeds, **kw):
+    """Replicates summarised by the device marginal summaries (mean, median)."""
+    outs = []
+    for s in seeds:
+        o = run_sampler(data, a, sched, SmcConfig(seed=s, snapshot_thin=10**6, summary_levels=(0.5,), **kw))
+        outs.append(dict(mean=np.stack([r.summary["mean"] for r in o.steps]),
+                         med=np.stack([r.summary["quantiles"][0] for r in o.steps]),
+                         logz=np.array([r.log_z_ratio_cum for r in o.steps]),
+                         ess=np.array([r.ess for r in o.steps]), acc=np.array([float(r.acceptance) for r in o.steps])))
+    return {k: np.stack([o[k] for o in outs]) for k in outs[0]}
+
+
+def c3n(R=6):
+    data, _ = simulate_dataset(named_spec("c3"))
+    sched = make_schedule(2.0, 0.98, 100)
+    t0 = time.time()
+    mw = dev_reps(data, 1.0, sched, range(301, 301 + R), N=8192, cycles=5, move_kernel="mwg")
+    emit(study="c3n", kernel="mwg", N=8192, logz_T=float(mw["logz"][:, -1].mean()),
+         logz_T_sd=float(mw["logz"][:, -1].std(ddof=1)), min_ess_frac=float(mw["ess"][:, 1:].min() / 8192),
+         wall=time.time() - t0)
+    for N in (8192, 65536):
+        for moves in (5, 10, 20):
+            t0 = time.time()
+            rw = dev_reps(data, 1.0, sched, range(401, 401 + R), N=N, move_kernel="rw", moves=moves)
+            zm, zq, zl = z(mw["mean"], rw["mean"]), z(mw["med"], rw["med"]), z(mw["logz"], rw["logz"])
+            emit(study="c3n", kernel="rw", N=N, moves=moves, logz_T=float(rw["logz"][:, -1].mean()),
+                 logz_T_sd=float(rw["logz"][:, -1].std(ddof=1)), z_logz_max=float(np.abs(zl).max()),
+                 z_mean_frac_gt3=float(np.mean(np.abs(zm) > 3)), z_mean_max=float(np.abs(zm).max()),
+                 z_median_frac_gt3=float(np.mean(np.abs(zq) > 3)), z_median_max=float(np.abs(zq).max()),
+                 max_abs_mean_diff=float(np.abs(rw["mean"].mean(0) - mw["mean"].mean(0)).max()),
+                 max_abs_median_diff=float(np.abs(rw["med"].mean(0) - mw["med"].mean(0)).max()),
+                 min_ess_frac=float(rw["ess"][:, 1:].min() / N), acc=float(rw["acc"][:, 1:].mean()),
+                 wall=time.time() - t0)
 
 
 if __name__ == "__main__":
