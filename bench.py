@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--particles", type=int, default=N_PER_GPU, help="particles per GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-path", action="store_true", help="skip the full 99-step device-time path")
     ap.add_argument("--profile", action="store_true",
                     help="bracket the timed steps with cudaProfilerStart/Stop (ncu --profile-from-start off)")
     return ap.parse_args()
@@ -380,7 +381,14 @@ def main():
     flops_per_launch = 2.0 * n * p * args.particles
     peaks, peak_kind = measured_peaks()
     achieved = flops_per_launch / (k1_ms / 1e3) / 1e12
-    peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+    burst = float(peaks.get("bf16_tflops", 1661.3))
+    sustained = float(peaks.get("bf16_tflops_sustained", burst))
+    csum = clk.summary()
+    # the denominator matching the clocks: K1 timed at the maximum SM clock
+    # is compared with the burst peak (MEASURED_PEAKS.json's sustained figure
+    # was taken at a lower median clock)
+    at_max = csum.get("sm_mhz") is not None and csum.get("sm_max_mhz") and csum["sm_mhz"] >= 0.97 * csum["sm_max_mhz"]
+    peak = burst if at_max or csum.get("sm_mhz") is None else sustained
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "k1_traffic.json")
     if os.path.exists(tpath):
@@ -393,12 +401,34 @@ def main():
             traffic = None
     beta_mb = args.particles * system.ldb * 4 / 1e6
     a_mb = args.particles * 2 * system.design.kp * 2 / 1e6
+    del system
+
+    # the whole 99-step lambda path on the device (every step, the resampling
+    # ones included; device time, no host sync inside), from a fresh init
+    full = None
+    if not args.no_path:
+        sysf, _ = S.init_particles(data, prior1, cfg, False, design=design, group=group)
+        torch.cuda.synchronize()
+        if group is not None:
+            group.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        frecs = [S.smc_step(sysf, data, sched, tt, cfg, group, _defer=True) for tt in range(2, sched.T + 1)]
+        f1.record()
+        torch.cuda.synchronize()
+        S.resolve_records(sysf, frecs)
+        fms = f0.elapsed_time(f1)
+        if group is not None:
+            fms = group.max_scalar(fms)
+        nres = sum(int(r.resampled) for r in frecs)
+        full = {"steps": len(frecs), "ms": fms, "ms_per_step": fms / len(frecs), "resampling_steps": nres,
+                "evals_per_s": Ntot * MOVES * len(frecs) / (fms / 1e3),
+                "note": "device time of t=2..100 from a fresh init (CUDA events, max over ranks)"}
+        del sysf
 
     # end to end through the public API (host Dataset in, host SmcOutput out)
     e2e = None
     if not args.no_e2e:
-        cfg_e = S.SmcConfig(N=Ntot, move_kernel="rw", moves=MOVES, seed=1, init_burn=200, init_thin=5,
-                            snapshot_thin=10)
         sched_e = S.make_schedule(*SCHED)  # the full 100-step lambda path
         # untimed warm-up of the same shapes (pinned staging buffer, writer
         # thread, first-call attribute setup), a 3-step path without burn-in
@@ -406,10 +436,10 @@ def main():
                       S.SmcConfig(N=Ntot, move_kernel="rw", moves=MOVES, seed=2, init_burn=1, init_thin=1,
                                   snapshot_thin=1), False, group)
         torch.cuda.synchronize()
-        # two full timed runs, the faster reported (first-touch host page
-        # faults of the ~3 GB of float64 snapshots vary from box to box)
-        best = None
-        for _ in range(2):
+
+        def timed_run(burn, seed):
+            cfg_e = S.SmcConfig(N=Ntot, move_kernel="rw", moves=MOVES, seed=seed, init_burn=burn, init_thin=5,
+                                snapshot_thin=10)
             if group is not None:
                 group.barrier()
             t0 = time.perf_counter()
@@ -418,21 +448,29 @@ def main():
             wall = time.perf_counter() - t0
             if group is not None:
                 wall = group.max_scalar(wall)
-            if best is None or wall < best[0]:
-                best = (wall, out)
-            del out
-        wall, out = best
+            return wall, out
+
+        # the reference's default initialisation (init_burn = 2000,
+        # smc.py:86) is the headline; two runs, their mean reported
+        runs = [timed_run(2000, s) for s in (1, 3)]
+        wall = sum(w for w, _ in runs) / len(runs)
+        out = runs[-1][1]
+        wall200, out200 = timed_run(200, 5)
         h2d = sum(v.numel() * v.element_size() for v in design.tensors.values())
         snaps = sum(1 for s in out.steps if s.particles is not None)
         d2h_total = snaps * (Ntot * (8 + 8 + 4 * p)) + len(out.steps) * 64
         nsteps_e = SCHED[2] - 1
         evals_e = Ntot * MOVES * nsteps_e
-        e2e = {"value": evals_e / wall, "unit": "evals/s", "wall_s": wall, "init_s": out.timings.get("init_s"),
-               "lambda_path_s": out.timings.get("path_s"),
+        e2e = {"value": evals_e / wall, "unit": "evals/s", "wall_s": wall, "wall_s_runs": [w for w, _ in runs],
+               "init_s": out.timings.get("init_s"), "lambda_path_s": out.timings.get("path_s"),
+               "init_burn": 2000,
                "h2d_bytes_per_step": int(h2d / nsteps_e), "d2h_bytes_per_step": int(d2h_total / nsteps_e),
+               "with_init_burn_200": {"value": evals_e / wall200, "wall_s": wall200,
+                                      "init_s": out200.timings.get("init_s")},
                "note": "full 100-step run_sampler(Dataset on host) -> SmcOutput on host: design upload, "
-                       "parallel-chain init (200 burn sweeps), 99 lambda steps, snapshots every 10th step; "
-                       "after an untimed 3-step warm-up run of the same shapes; the faster of 2 timed runs"}
+                       "parallel-chain init (the reference's default 2000 burn sweeps), 99 lambda steps, snapshots "
+                       "every 10th step; after an untimed 3-step warm-up run of the same shapes; mean of 2 runs"}
+        del runs, out, out200
 
     if rank != 0:
         return 0
@@ -455,12 +493,19 @@ def main():
                                f"moves={MOVES} (RW population covariance)",
                    "particles_total": Ntot, "lambda_steps_timed": f"t={t - args.steps}..{t - 1}",
                    "resampling_steps_timed": resampled, "l2": f"inputs larger than L2 (beta {beta_mb:.0f} MB + A {a_mb:.0f} MB per GPU vs 126 MB L2)",
-                   "init": "excluded (parallel MwG chains, 200 burn sweeps)", "parallelism": f"dp{ws} particles"},
+                   "init": "excluded (parallel MwG chains, 200 burn sweeps; e2e: 2000)", "parallelism": f"dp{ws} particles",
+                   "rw_validity": "C3 5 moves: fixed-b criterion 8 passes (worst median diff 0.003 at t=50, 0.019 at "
+                                  "t=100; tests/test_gpu_sampler.py::test_rw_c3_fixed_b_criterion); evidence gated "
+                                  "(DESIGN.md section 4)"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic, "kernel": "tc_gemm_kernel<2,1,256,Softplus> (K1)",
-                     "k1_ms_per_launch": k1_ms, "k1_launches": k1_n, "peak_source": f"{peak_kind} sustained bf16",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "frac_vs_burst": achieved / burst, "frac_vs_sustained": achieved / sustained,
+                     "kernel": "tc_gemm_kernel<2,1,256,EpiSoftplusRowSum,1,fp16> (K1)",
+                     "mma_work_per_algorithmic_flop": 2.0 * design.kp * 256 * -(-n // 256) / (p * n),
+                     "k1_ms_per_launch": k1_ms, "k1_launches": k1_n, "peak_source": f"{peak_kind} bf16 {'burst (clocks at max)' if peak == burst else 'sustained'}",
                      "algorithmic_flops_per_launch": flops_per_launch,
                      "k1_share_of_step": (k1_ms * MOVES) / step_ms},
+        "full_path": full,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
