@@ -1293,6 +1293,28 @@ __global__ void ancestors_kernel(const double* __restrict__ cumn, int64_t N, dou
   anc[i] = lo;
 }
 
+// One warp copies one float32 row of q values (16-byte aligned rows): all of
+// a lane's float4 loads are issued before its stores (4 in flight per lane
+// for q <= 512), so a warp-per-row copy keeps enough bytes in flight to run
+// at HBM speed.
+__device__ __forceinline__ void warp_copy_row(float* __restrict__ o, const float* __restrict__ a, int q, int lane) {
+  const int q4 = q >> 2;
+  for (int base = 0; base < q4; base += 128) {
+    float4 r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = base + u * 32 + lane;
+      if (c < q4) r[u] = __ldcs(reinterpret_cast<const float4*>(a) + c);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = base + u * 32 + lane;
+      if (c < q4) reinterpret_cast<float4*>(o)[c] = r[u];
+    }
+  }
+  for (int c = 4 * q4 + lane; c < q; c += 32) o[c] = a[c];
+}
+
 // K5: row gather (+ up to two per-particle float64 vectors)
 __global__ void gather_kernel(const float* __restrict__ src, int ld_src, float* __restrict__ dst, int ld_dst, int q,
                               const int64_t* __restrict__ idx, int64_t base, int64_t m, const double* __restrict__ v0,
@@ -1308,9 +1330,7 @@ __global__ void gather_kernel(const float* __restrict__ src, int ld_src, float* 
   const float* a = src + s * ld_src;
   float* o = dst + row * ld_dst;
   if ((ld_src & 3) == 0 && (ld_dst & 3) == 0) {
-    const int q4 = q >> 2;
-    for (int j = lane; j < q4; j += 32) reinterpret_cast<float4*>(o)[j] = reinterpret_cast<const float4*>(a)[j];
-    for (int j = 4 * q4 + lane; j < q; j += 32) o[j] = a[j];
+    warp_copy_row(o, a, q, lane);
   } else {
     for (int j = lane; j < q; j += 32) o[j] = a[j];
   }
@@ -1348,9 +1368,7 @@ __global__ void resample_commit_kernel(const float* __restrict__ beta_alt, float
   const float* a = beta_alt + row * ldb;
   float* o = beta + row * ldb;
   if ((ldb & 3) == 0) {
-    const int q4 = q >> 2;
-    for (int j = lane; j < q4; j += 32) reinterpret_cast<float4*>(o)[j] = reinterpret_cast<const float4*>(a)[j];
-    for (int j = 4 * q4 + lane; j < q; j += 32) o[j] = a[j];
+    warp_copy_row(o, a, q, lane);
   } else {
     for (int j = lane; j < q; j += 32) o[j] = a[j];
   }
@@ -1386,9 +1404,7 @@ __global__ void peer_gather_kernel(const __grid_constant__ PeerRows src, int64_t
     const int64_t off = j - (int64_t)r * M;
     const float* a = src.beta[r] + off * ldb;
     float* o = beta_alt + row * ldb;
-    const int q4 = q >> 2;  // ldb % 4 == 0 (checked by the caller)
-    for (int c = lane; c < q4; c += 32) reinterpret_cast<float4*>(o)[c] = reinterpret_cast<const float4*>(a)[c];
-    for (int c = 4 * q4 + lane; c < q; c += 32) o[c] = a[c];
+    warp_copy_row(o, a, q, lane);  // ldb % 4 == 0 (checked by the caller)
     if (lane == 0) {
       ll_alt[row] = src.ll[r][off];
       lp_alt[row] = src.lp[r][off];
@@ -1991,13 +2007,28 @@ static inline unsigned cdiv(int64_t a, int64_t b) { return (unsigned)((a + b - 1
 
 // Likelihood work split: units of BN tiles so the grid covers several waves.
 static void loglik_split(int64_t m, int n, int& m_tiles, int& n_tiles, int& tpu, int& units) {
-  // persistent kernel: items = (particle tile, subject-tile group); groups of
-  // ~4 subject tiles keep the partial-sum traffic small while leaving enough
-  // items (>= ~8 per SM) to balance the tail
+  // persistent kernel: items = (particle tile, group of tpu subject tiles),
+  // CTA b takes items b, b + 148, ...  The group size minimises the makespan
+  // in subject-tile times, ceil(items / 148) * tpu, plus a small per-item
+  // cost (epilogue drain, partial-sum write, pipeline ramp) -- e.g. C3
+  // (512 x 20 tiles): tpu = 10, 7 rounds of 10 (the 4-tile groups of round 1
+  // took 18 rounds of 4: 72 vs 70 tile times)
+  constexpr int kSms = 148;
   m_tiles = (int)((m + kTcBM - 1) / kTcBM);
   n_tiles = (n + 255) / 256;
-  tpu = std::max(1, std::min(n_tiles, 4));
-  while (tpu > 1 && (int64_t)m_tiles * ((n_tiles + tpu - 1) / tpu) < 8 * 148) --tpu;
+  double best = 1e300;
+  tpu = 1;
+  for (int g = 1; g <= n_tiles; ++g) {
+    const int u = (n_tiles + g - 1) / g;
+    if (g > 1 && (u - 1) * g >= n_tiles) continue;  // same units as a smaller group
+    const int64_t items = (int64_t)m_tiles * u;
+    const int64_t rounds = (items + kSms - 1) / kSms;
+    const double cost = (double)rounds * g + 0.1 * (double)rounds;
+    if (cost < best - 1e-9) {
+      best = cost;
+      tpu = g;
+    }
+  }
   units = (n_tiles + tpu - 1) / tpu;
 }
 
@@ -2497,11 +2528,33 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
   if (d->kp > 128 && d->kp <= 512) {
     const size_t sm2 = (size_t)16 * d->kp + (size_t)kPackWarps * kPackSlots * 2 * ((size_t)ldb * 6);
     auto kern = d->kp <= 256 ? pack_eps_rows_kernel<4, 16> : pack_eps_rows_kernel<8, 16>;
-    SPA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
-    int per_sm = 0, dev = 0, nsm = 0;
-    SPA_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kPackWarps, sm2));
-    SPA_CHECK_CUDA(cudaGetDevice(&dev));
-    SPA_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    // the attribute / occupancy queries once per (kernel, smem size): the
+    // move loop calls this 5 times per step
+    struct Geo {
+      const void* k;
+      size_t sm;
+      int per_sm, nsm;
+    };
+    static thread_local Geo geo[4] = {};
+    Geo* g = nullptr;
+    for (auto& e : geo)
+      if (e.k == (const void*)kern && e.sm == sm2) g = &e;
+    if (!g) {
+      int per_sm = 0, dev = 0, nsm = 0;
+      SPA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+      SPA_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kPackWarps, sm2));
+      SPA_CHECK_CUDA(cudaGetDevice(&dev));
+      SPA_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+      for (auto& e : geo)
+        if (e.k == nullptr) {
+          e = Geo{(const void*)kern, sm2, per_sm, nsm};
+          g = &e;
+          break;
+        }
+      if (!g) g = &geo[0];
+      *g = Geo{(const void*)kern, sm2, per_sm, nsm};
+    }
+    const int per_sm = g->per_sm, nsm = g->nsm;
     if (per_sm > 0) {
       const unsigned grid = std::min<unsigned>(cdiv(cdiv(m, 2), kPackWarps), (unsigned)(per_sm * nsm));
       kern<<<grid, 32 * kPackWarps, sm2, st>>>(*d, beta, epsb, m, ldb, Ab, ylin, pc, lp);

@@ -20,6 +20,11 @@ from paper_1106_0322_b200.smc import _p, _stream  # noqa: E402
 def kernel_us(fn, reps=10):
     fn()
     torch.cuda.synchronize()
+    if os.environ.get("SPA_NO_PROFILER"):  # under ncu: plain launches only
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        return {}
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for _ in range(reps):
             fn()
