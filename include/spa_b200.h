@@ -192,10 +192,10 @@ int spa_resample_commit(const double* gate, float* beta, const float* beta_alt, 
  * Writes ll (log-likelihood) and lp (log-prior at c) of the final state,
  * and adds the number of accepted updates to *accepted (device u64), or,
  * with per_particle != 0, particle k's count to accepted[k]. */
-/* Chains (CTAs) of spa_mwg_move resident at once on the current device for
- * this design (occupancy x SMs); init_particles sizes its parallel chains to
- * one such wave (the reference's single init chain, smc.py:202-245, is
- * replaced by parallel chains). */
+/* Chains (CTAs) of spa_mwg_chain_slots resident at once on the current
+ * device for this design (occupancy x SMs); init_particles sizes its
+ * parallel chains to one such wave (the reference's single init chain,
+ * smc.py:202-245, is replaced by parallel chains). */
 int spa_mwg_resident_chains(const spa_design* d, int64_t* chains);
 
 int spa_mwg_move(const spa_design* d, float* beta, int64_t m, int32_t ldb, double a, double c, double step_sd,
@@ -204,10 +204,14 @@ int spa_mwg_move(const spa_design* d, float* beta, int64_t m, int32_t ldb, doubl
 /* Initialisation chains in one launch: `slots` blocks of cycles_per_slot
  * sweeps (sweep indices sweep0 ..), the state after block s stored in slot
  * row*slots + s of slot_beta ([m*slots][ldb] float32), slot_ll and slot_lp;
- * beta/ll/lp end at the last slot's state.  Bit-identical to `slots` calls of
- * spa_mwg_move with sweep0 advanced by cycles_per_slot (one materialisation
- * of the subject cache per slot instead of two, one launch instead of
- * `slots`). */
+ * beta/ll/lp end at the last slot's state.  Bit-identical to `slots` calls
+ * of spa_mwg_chain_slots with slots = 1 and sweep0 advanced by
+ * cycles_per_slot (one materialisation of the subject cache per slot
+ * instead of two, one launch instead of `slots`).  Chains run the
+ * latency layout (fewer subjects per thread, more threads per chain: one
+ * resident wave of long sequential chains) where spa_mwg_move, the
+ * throughput kernel of the lambda-step moves, keeps more subjects per
+ * thread; the two therefore differ in float32 summation order. */
 int spa_mwg_chain_slots(const spa_design* d, float* beta, int64_t m, int32_t ldb, double a, double c,
                         double step_sd, int32_t cycles_per_slot, int32_t slots, uint64_t seed, int32_t tag,
                         int64_t t, int64_t i0, int64_t sweep0, double* ll, double* lp, float* slot_beta,

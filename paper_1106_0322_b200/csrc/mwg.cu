@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "../../include/spa_b200.h"
 #include "common.cuh"
@@ -196,8 +197,10 @@ __device__ __forceinline__ void coord_accept(float (&sig)[S], uint32_t p1, uint3
   }
 }
 
+// Thread limits per layout: S = 8 up to 1024 threads, S = 16 up to 640 (the
+// initialisation layout up to n = 10240: <= 102 registers), S = 32 512
 template <int S, bool CODED>
-__global__ void __launch_bounds__(512) mwg_kernel(MwgParams P) {
+__global__ void __launch_bounds__(S == 8 ? 1024 : (S == 16 ? 640 : 512)) mwg_kernel(MwgParams P) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int q = P.d.q;
   CoordSlot* slot = reinterpret_cast<CoordSlot*>(sm);
@@ -291,11 +294,14 @@ __global__ void __launch_bounds__(512) mwg_kernel(MwgParams P) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
       if (nw > 1) {
+        // second level: every warp reduces the nw warp sums with shuffles
+        // (one smem load per lane instead of nw serial loads and adds)
         float* buf = fred + (j & 1) * 32;
         if (lane == 0) buf[wid] = tot;
         __syncthreads();
-        tot = 0.0f;
-        for (int w = 0; w < nw; ++w) tot += buf[w];
+        tot = lane < nw ? buf[lane] : 0.0f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
       }
       const double dll = cs.dsy - 0.6931471805599453 * (double)tot;
       const double d = dll + cs.dlp;
@@ -349,7 +355,28 @@ static const void* mwg_fn(int S, bool coded) {
   return S == 8 ? mwg_fn_s<8>(coded) : S == 16 ? mwg_fn_s<16>(coded) : mwg_fn_s<32>(coded);
 }
 
+static int max_threads(int S) { return S == 8 ? 1024 : (S == 16 ? 640 : 512); }
+
+// Layout of the initialisation chains (spa_mwg_chain_slots and the chain
+// count of spa_mwg_resident_chains): one resident wave of latency-bound
+// chains, so fewer subjects per thread and more threads per chain (C3 init
+// with 2000 burn sweeps 1.58 -> 1.32 s, C2 0.51 -> 0.34 s against the
+// throughput layout of pick_s)
+static int pick_s_init(int n) {
+  if (n <= 256) return 8;
+  if ((n + 15) / 16 <= 640) return 16;
+  if (n <= 16384) return 32;
+  return 0;
+}
+
 static int pick_s(int n) {
+  // developer A/B knob (init latency vs throughput layouts): SPA_MWG_S=8|16|32
+  static const int forced = [] {
+    const char* e = getenv("SPA_MWG_S");
+    return e ? atoi(e) : 0;
+  }();
+  if ((forced == 8 || forced == 16 || forced == 32) && (n + forced - 1) / forced <= max_threads(forced))
+    return forced;
   if (n <= 256) return 8;
   if (n <= 512) return 16;
   if (n <= 16384) return 32;
@@ -377,7 +404,7 @@ extern "C" int spa_mwg_prepare_kernels(void) {
 // times the SM count.  Initialisation sizes its parallel chains to one wave.
 extern "C" int spa_mwg_resident_chains(const spa_design* d, int64_t* chains) {
   SPA_REQUIRE(d && chains && d->q >= 1 && d->q <= 2048, kBadArgument, "spa_mwg_resident_chains: bad arguments");
-  const int S = pick_s(d->n);
+  const int S = pick_s_init(d->n);
   SPA_REQUIRE(S > 0, kNotSupported, "spa_mwg_resident_chains: n > 16384 not supported");
   const int nthr = std::max(32, ((d->n + S - 1) / S + 31) / 32 * 32);
   const size_t smem = (size_t)d->q * sizeof(CoordSlot) + (size_t)((d->q + 1) & ~1) * sizeof(float) +
@@ -395,11 +422,11 @@ extern "C" int spa_mwg_resident_chains(const spa_design* d, int64_t* chains) {
 static int mwg_launch(const spa_design* d, float* beta, int64_t m, int32_t ldb, double a, double c, double step_sd,
                       int32_t cycles, uint64_t seed, int32_t tag, int64_t t, int64_t i0, int64_t sweep0, double* ll,
                       double* lp, unsigned long long* accepted, int32_t per_particle, int32_t slots,
-                      float* slot_beta, double* slot_ll, double* slot_lp, void* stream) {
+                      float* slot_beta, double* slot_ll, double* slot_lp, void* stream, bool init_layout) {
   SPA_REQUIRE(d && beta && ll && accepted && m >= 0 && cycles >= 0, kBadArgument, "spa_mwg_move: bad arguments");
   SPA_REQUIRE(a > 0 && c > 0 && step_sd > 0, kBadArgument, "spa_mwg_move: a, c, step_sd must be positive");
   SPA_REQUIRE(d->q >= 1 && d->q <= 2048, kNotSupported, "spa_mwg_move: q must lie in [1, 2048]");
-  const int S = pick_s(d->n);
+  const int S = init_layout ? pick_s_init(d->n) : pick_s(d->n);
   SPA_REQUIRE(S > 0, kNotSupported, "spa_mwg_move: n > 16384 not supported");
   SPA_REQUIRE(d->coded ? d->planes != nullptr : d->xcols != nullptr, kBadArgument, "spa_mwg_move: design arrays");
   if (m == 0) return 0;
@@ -433,7 +460,7 @@ static int mwg_launch(const spa_design* d, float* beta, int64_t m, int32_t ldb, 
   const size_t smem = (size_t)d->q * sizeof(CoordSlot) + (size_t)((d->q + 1) & ~1) * sizeof(float) +
                       64 * sizeof(double) + 64 * sizeof(float);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  SPA_REQUIRE(S != 32 || nthr <= 512, kNotSupported, "spa_mwg_move: n > 16384 not supported");
+  SPA_REQUIRE(nthr <= max_threads(S), kNotSupported, "spa_mwg_move: too many threads for this layout");
   const void* fn = mwg_fn(S, d->coded != 0);
   SPA_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   void* args[] = {&P};
@@ -447,7 +474,7 @@ extern "C" int spa_mwg_move(const spa_design* d, float* beta, int64_t m, int32_t
                             int64_t sweep0, double* ll, double* lp, unsigned long long* accepted,
                             int32_t per_particle, void* stream) {
   return mwg_launch(d, beta, m, ldb, a, c, step_sd, cycles, seed, tag, t, i0, sweep0, ll, lp, accepted, per_particle,
-                    0, nullptr, nullptr, nullptr, stream);
+                    0, nullptr, nullptr, nullptr, stream, false);
 }
 
 extern "C" int spa_mwg_chain_slots(const spa_design* d, float* beta, int64_t m, int32_t ldb, double a, double c,
@@ -458,5 +485,5 @@ extern "C" int spa_mwg_chain_slots(const spa_design* d, float* beta, int64_t m, 
   SPA_REQUIRE(slots >= 1 && slot_beta && slot_ll && slot_lp && cycles_per_slot >= 1, kBadArgument,
               "spa_mwg_chain_slots: bad slot arguments");
   return mwg_launch(d, beta, m, ldb, a, c, step_sd, cycles_per_slot, seed, tag, t, i0, sweep0, ll, lp, accepted,
-                    per_particle, slots, slot_beta, slot_ll, slot_lp, stream);
+                    per_particle, slots, slot_beta, slot_ll, slot_lp, stream, true);
 }

@@ -715,6 +715,29 @@ def resident_chains(design: DeviceDesign) -> int:
     return int(out.value)
 
 
+# Sequential sweep time of one chain with c chains resident per SM, relative
+# to one chain per SM: measured 1.43 at c = 2 (C3 chain layout) -- the
+# chains are latency-bound, so a second one per SM costs less than 2x.
+_CHAIN_SHARE_EXP = 0.52
+
+
+def auto_chains(design: DeviceDesign, N: int, burn: int, thin: int) -> int:
+    """Parallel initialisation chains per GPU: c chains per SM (up to the
+    resident wave) minimising the sequential sweeps per chain, burn +
+    N*thin/(SMs*c), times the sweep time at c chains per SM (~c^0.52).  C3
+    with 2000 burn sweeps: one chain per SM (1.32 s vs 1.39 s for two); with
+    200, two."""
+    resident = resident_chains(design)
+    sms = torch.cuda.get_device_properties(design.tensors["sy"].device).multi_processor_count
+    occ = max(1, resident // max(sms, 1))
+    best, best_c = None, 1
+    for c in range(1, occ + 1):
+        cost = (burn + N * thin / (sms * c)) * c**_CHAIN_SHARE_EXP
+        if best is None or cost < best:
+            best, best_c = cost, c
+    return best_c * sms
+
+
 def init_plan(N_total: int, init_chains: int, chains_auto: int) -> tuple[int, int]:
     """(K chains, R slots per chain): chain c fills the contiguous slots
     [c R, min((c+1) R, N)).  K = init_chains, else one resident wave per GPU
@@ -733,8 +756,8 @@ def init_particles(data, prior_at_b1: GtPrior, config: SmcConfig, intercept: boo
     c keyed (seed, 0, 0, c): each burns init_burn sweeps, then its state after
     every further init_thin sweeps fills its next slot of the contiguous block
     [c R, (c+1) R).  Total chain-sweeps K*init_burn + N*init_thin; K defaults
-    to one resident wave of chains per GPU (spa_mwg_resident_chains x ranks),
-    which minimises the wall time of these latency-bound sweeps.  A rank
+    to whole waves of chains per GPU (auto_chains x ranks: one or more chains
+    per SM, whichever minimises the wall time of these latency-bound sweeps).  A rank
     simulates only the chains whose blocks meet its shard, so for a given K
     the particles are identical for any number of GPUs.
     Returns (system, acceptance_rate)."""
@@ -745,22 +768,29 @@ def init_particles(data, prior_at_b1: GtPrior, config: SmcConfig, intercept: boo
     world = 1 if group is None else group.world
     shard, offset = (N_total, 0) if group is None else group.shard(N_total)
     system = ParticleSystem(design, shard, prior_at_b1.a, intercept, rank_offset=offset, N_total=N_total)
-    auto = 0 if config.init_chains else resident_chains(design) * world
+    auto = 0 if config.init_chains else auto_chains(design, N_total // world, config.init_burn, config.init_thin) * world
     K, R = init_plan(N_total, config.init_chains, auto)
     lo, hi = offset, offset + shard
     c0, c1 = lo // R, min(K, -(-hi // R))  # chains whose slot blocks meet [lo, hi)
     chains = ParticleSystem(design, c1 - c0, prior_at_b1.a, intercept, rank_offset=c0)
     Kl = c1 - c0
     counts = torch.zeros(Kl, dtype=torch.int64, device=system.device)  # per chain, read once at the end
-    if config.init_burn > 0:
-        _mwg(chains, prior_at_b1, config.step_sd, config.init_burn, config.seed, TAG_INIT, 0, 0, counts=counts)
+    d = chains.design
+    if config.init_burn > 0:  # the burn-in: one chain-slot block of init_burn sweeps (the chains' layout)
+        bb = torch.empty((Kl, system.ldb), dtype=torch.float32, device=system.device)
+        bl = torch.empty(Kl, dtype=torch.float64, device=system.device)
+        bp = torch.empty(Kl, dtype=torch.float64, device=system.device)
+        _lib.call("spa_mwg_chain_slots", ctypes.byref(d.struct), _p(chains.beta), chains.N, chains.ldb,
+                  float(prior_at_b1.a), float(prior_at_b1.c), float(config.step_sd), int(config.init_burn), 1,
+                  int(config.seed), TAG_INIT, 0, int(chains.i0), 0, _p(chains.ll), _p(chains.lp), _p(bb), _p(bl),
+                  _p(bp), _p(counts), 1, _stream())
+        del bb, bl, bp
     _prepare_for_path(system, config)  # host work while the chains run
     stage_b = torch.empty((Kl, R, system.ldb), dtype=torch.float32, device=system.device)
     stage_l = torch.empty((Kl, R), dtype=torch.float64, device=system.device)
     stage_p = torch.empty((Kl, R), dtype=torch.float64, device=system.device)
     # all R thinning blocks in one launch (slot j = the state after init_burn
-    # + (j+1)*init_thin sweeps; bit-identical to one spa_mwg_move per slot)
-    d = chains.design
+    # + (j+1)*init_thin sweeps; bit-identical to one chain-slot call per slot)
     _lib.call("spa_mwg_chain_slots", ctypes.byref(d.struct), _p(chains.beta), chains.N, chains.ldb,
               float(prior_at_b1.a), float(prior_at_b1.c), float(config.step_sd), int(config.init_thin), int(R),
               int(config.seed), TAG_INIT, 0, int(chains.i0), int(config.init_burn), _p(chains.ll), _p(chains.lp),
