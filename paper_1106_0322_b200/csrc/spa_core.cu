@@ -1735,8 +1735,11 @@ __device__ __forceinline__ void rw_normals8(uint64_t seed, int64_t t, int64_t k,
 #pragma unroll
   for (int h = 0; h < 4; ++h) {
     const uint32_t a = w[h];
-    const float u1 = (float)(((a >> 1) & 0x7FFFu) + 1u) * 0x1.0p-15f;  // (0, 1]
-    const float u2 = (float)((a >> 17) & 0x7FFFu) * 0x1.0p-15f;        // [0, 1)
+    // 15-bit uniforms without int -> float conversions (those issue on the
+    // XU pipe beside the log / sqrt / sincos): the bits become the top of a
+    // float mantissa in [1, 2); subtracting 1 is exact
+    const float u2 = __uint_as_float(0x3F800000u | ((a >> 17) & 0x7FFFu) << 8) - 1.0f;       // [0, 1)
+    const float u1 = (__uint_as_float(0x3F800000u | ((a >> 1) & 0x7FFFu) << 8) - 1.0f) + 0x1.0p-15f;  // (0, 1]
     float r;
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-2.0f * __logf(u1)));
     float sn, cs;

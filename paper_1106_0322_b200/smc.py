@@ -25,11 +25,11 @@ Extra SmcConfig fields (defaults keep the reference's behaviour):
     rw_factor_lag
                  RW covariance factor pipelining: 0 = every move of step t
                  uses the factor of step t's population (computed before the
-                 first move); 1 (default) = the first move uses the previous
-                 step's factor while the new one is computed on a side
-                 stream; 2 = every move of step t uses the factor of step
+                 first move); 1 = the first move uses the previous step's
+                 factor while the new one is computed on a side stream;
+                 2 (default) = every move of step t uses the factor of step
                  t-1's population, computed on the side stream during step
-                 t-1's moves
+                 t-1's moves (never on the critical path)
 """
 
 from __future__ import annotations
@@ -121,7 +121,7 @@ class SmcConfig:
     init_chains: int = 0
     summary_levels: tuple = ()
     summary_deltas: tuple = ()
-    rw_factor_lag: int = 1
+    rw_factor_lag: int = 2
     summary_pooled: bool = False
 
     def __post_init__(self):
@@ -191,8 +191,8 @@ class SmcOutput:
         reference's MwG kernel: yes.  The RW population-covariance move
         (north-star throughput kernel): its marginal posteriors pass the
         reference's fixed-b criterion at C3, but its
-        evidence carries a finite-N mixing bias (+1.5 nats at C3 with
-        N=65536 and 5 moves, SD 0.6; MwG 0.013), so evidence-derived
+        evidence carries a finite-N mixing bias (+1.4 nats at C3 with
+        N=65536 and 5 moves, SD 0.5; MwG 0.014), so evidence-derived
         summaries (summary.c_posterior, pooled posterior) refuse RW runs
         unless asked explicitly."""
         return self.config.move_kernel == "mwg"
