@@ -19,6 +19,7 @@ global resampling / ancestor exchange and the covariance moments.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import math
 import os
@@ -35,6 +36,13 @@ N_PER_GPU = 65536
 A_DOF = 1.0
 SCHED = (2.0, 0.98, 100)
 MOVES = 5
+def k1_kernel_name(design) -> str:
+    """The K1 kernel spa_loglik_softplus launches for this design (csrc/spa_core.cu loglik_impl)."""
+    if not design.coded:
+        return "tc_gemm_kernel<2,2,256,EpiSoftplusRowSum,1,fp16> (K1, fp16 hi/lo)"
+    if design.kp <= 512:
+        return "k1_i8_pair_kernel (K1, int8 byte planes, CTA pairs, resident particle tiles)"
+    return "k1_i8_kernel (K1, int8 byte planes, streaming)"
 REF_SAMPLE = 256  # particles per reference-arm step (the reference's MwG step at C3: several s on 16 cores)
 
 
@@ -400,7 +408,7 @@ def main():
         except Exception:
             traffic = None
     beta_mb = args.particles * system.ldb * 4 / 1e6
-    a_mb = args.particles * 2 * system.design.kp * 2 / 1e6
+    a_mb = _lib.load().spa_k1_operand_bytes(ctypes.byref(system.design.struct), args.particles) / 1e6
     del system
 
     # the whole 99-step lambda path on the device (every step, the resampling
@@ -488,7 +496,7 @@ def main():
         "metric": "particle log-lik evals/s (SMC lambda-path, RW-cov moves, n x p)",
         "value": value, "unit": "evals/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "bf16x2->f32 (likelihood), f32 state, f64 weights", "data": "synthetic",
+        "dtype": ("i8x3->s32 (likelihood, 22-bit fixed point)" if design.coded else "f16x2->f32 (likelihood)") + ", f32 state, f64 weights", "data": "synthetic",
         "config": {"workload": f"{args.config}: n={n} p={p} N={args.particles}/GPU a={A_DOF} b_t=2*0.98^(t-1) "
                                f"moves={MOVES} (RW population covariance)",
                    "particles_total": Ntot, "lambda_steps_timed": f"t={t - args.steps}..{t - 1}",
@@ -500,8 +508,10 @@ def main():
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "frac_vs_burst": achieved / burst, "frac_vs_sustained": achieved / sustained,
-                     "kernel": "tc_gemm_kernel<2,1,256,EpiSoftplusRowSum,1,fp16> (K1)",
-                     "mma_work_per_algorithmic_flop": 2.0 * design.kp * 256 * -(-n // 256) / (p * n),
+                     "kernel": k1_kernel_name(design),
+                     # tensor-core work in bf16-equivalent MACs (an int8 MMA counts half)
+                     "mma_work_per_algorithmic_flop": (1.5 * design.kp * 128 * -(-n // 128) if design.coded else
+                                                       2.0 * design.kp * 256 * -(-n // 256)) / (p * n),
                      "k1_ms_per_launch": k1_ms, "k1_launches": k1_n, "peak_source": f"{peak_kind} bf16 {'burst (clocks at max)' if peak == burst else 'sustained'}",
                      "algorithmic_flops_per_launch": flops_per_launch,
                      "k1_share_of_step": (k1_ms * MOVES) / step_ms},

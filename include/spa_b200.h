@@ -49,12 +49,11 @@ typedef struct spa_design {
   const double* gamma;      /* [q]                                              */
   const uint8_t* penalized; /* [q]     1 = prior applies (smc.py:266-270)      */
   /* tensor-core operand of the batched likelihood (K1) */
-  const void* gemm_b;       /* fp16 B operand: coded -> G [n][kp] (0/1/2 and
-                               1 in the 3 offset columns q..q+2);
-                               general -> [Xshi | Xslo] [n][2*kp], Xs = X/alpha */
-  int32_t kp;               /* K per term, multiple of 64, >= q (+3 if coded) */
-  int32_t terms;            /* B terms: 1 (coded) or 2 (general); the A
-                               operand is always [beta hi | beta lo]          */
+  const void* gemm_b;       /* B operand: coded -> uint8 [n][2*kp] = [G | 64 G]
+                               (int8 K1); general -> fp16 [Xshi | Xslo]
+                               [n][2*kp], Xs = X/alpha                        */
+  int32_t kp;               /* K per plane, multiple of 64, >= q (<= 1024 coded) */
+  int32_t terms;            /* general designs: 2 B terms; coded: 1 (unused) */
 } spa_design;
 
 /* Prior description: a > 0 (generalised t, model.py:78-81) or a = +inf
@@ -72,9 +71,14 @@ int spa_philox_blocks(uint64_t k0, uint64_t k1, uint64_t first_block, int64_t co
 /* ---- K1: batched log-likelihood on tcgen05 tensor cores -----------------
  * Replaces model.py:131-145 log_likelihood evaluated for many particles
  * (batched as summary.py:154-170).  A = packed particles (spa_pack_particles),
- * fp16 [m][2*kp] = [hi | lo] (22 significant bits of alpha*beta);
+ * spa_k1_operand_bytes(d, m) bytes:
+ *   coded designs  -- int8 tensor cores: three byte planes [hi | mid | lo]
+ *                     [m][3*kp] of the 22-bit per-row fixed point of
+ *                     alpha*beta, then {scale, offset} float2 [m];
+ *   general        -- fp16 [m][2*kp] = [hi | lo] (22 significant bits).
  * out_sp[m] = sum_i softplus(eta_ki) (float64).
  * ws: workspace of spa_loglik_workspace_bytes(m, n) bytes. */
+size_t spa_k1_operand_bytes(const spa_design* d, int64_t m);
 size_t spa_loglik_workspace_bytes(int64_t m, int32_t n);
 int spa_loglik_softplus(const spa_design* d, const void* A, int64_t m, double* out_sp, void* ws, size_t ws_bytes,
                         void* stream);

@@ -41,6 +41,7 @@ _SIGNATURES = {
     "spa_version": (c_int, []),
     "spa_philox_blocks": (c_int, [c_uint64, c_uint64, c_uint64, c_int64, c_void_p, c_void_p]),
     "spa_loglik_workspace_bytes": (c_size_t, [c_int64, c_int32]),
+    "spa_k1_operand_bytes": (c_size_t, [POINTER(SpaDesign), c_int64]),
     "spa_loglik_softplus": (c_int, [POINTER(SpaDesign), c_void_p, c_int64, c_void_p, c_void_p, c_size_t, c_void_p]),
     "spa_pack_particles": (c_int, [POINTER(SpaDesign), c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_double,
                                    c_double, c_void_p, c_void_p]),

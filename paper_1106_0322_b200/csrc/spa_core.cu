@@ -21,6 +21,7 @@
 #include "philox.cuh"
 #include "resample.cuh"
 #include "tc_gemm.cuh"
+#include "tc_k1_i8.cuh"
 
 namespace spa {
 
@@ -76,6 +77,22 @@ static int make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t cols, uint
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(kDriverEntryPoint, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return 0;
+}
+
+// byte matrix [rows][cols] row-major (the int8 K1 planes); box = 64 columns
+// x 128 rows, 64B swizzle (one swizzle atom per row of the box)
+static int make_tmap_u8(CUtensorMap* map, const void* ptr, uint64_t cols, uint64_t rows, uint32_t box_rows = 128) {
+  auto enc = tmap_encoder();
+  if (!enc) return fail(kDriverEntryPoint, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols};
+  cuuint32_t box[2] = {(cuuint32_t)kI8BK, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(kDriverEntryPoint, "cuTensorMapEncodeTiled (u8) failed: " + std::to_string((int)r));
   return 0;
 }
 
@@ -230,6 +247,48 @@ __device__ __forceinline__ void offset_limbs(double o, __half* dst, double* ylin
   if (!(fabs(o) < (double)kOpMax)) *ylin_row = __longlong_as_double(0x7ff8000000000000ll);
 }
 
+// Integer-coded designs feed K1 on the int8 tensor cores (tc_k1_i8.cuh): the
+// row is a 22-bit fixed-point vector relative to its largest |alpha_j beta_j|,
+// Q = rint(alpha_j beta_j / s) with |Q| <= 2^21 - 1, stored as three byte
+// planes [hi | mid | lo] (Q = hi 2^14 + mid 2^6 + lo, hi signed), followed
+// after the m rows by {s, o} per row (o = sum_j gamma_j beta_j).  A row
+// whose maximum is not finite gets s = 0 and a NaN linear term.
+constexpr float kQMax = 2097151.0f;  // 2^21 - 1
+__device__ __forceinline__ void emit_i8_4(uint8_t* __restrict__ row8, int kp, int j0, const float (&bs)[4],
+                                          float inv) {
+  uint32_t hi = 0, mid = 0, lo = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int Q = __float2int_rn(bs[i] * inv);
+    Q = max(-2097151, min(2097151, Q));
+    const uint32_t r = (uint32_t)Q & 0x3FFFu;  // Q - hi 2^14, hi = floor(Q / 2^14)
+    hi |= ((uint32_t)(Q >> 14) & 0xFFu) << (8 * i);
+    mid |= (r >> 6) << (8 * i);
+    lo |= (r & 63u) << (8 * i);
+  }
+  __stcs(reinterpret_cast<uint32_t*>(row8 + j0), hi);
+  __stcs(reinterpret_cast<uint32_t*>(row8 + kp + j0), mid);
+  __stcs(reinterpret_cast<uint32_t*>(row8 + 2 * kp + j0), lo);
+}
+__device__ __forceinline__ void emit_f16_4(__half* __restrict__ row16, int kp, int j0, const float (&bs)[4]) {
+  __align__(8) __half h[4], l[4];
+  float unused = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) split_op(bs[i], h[i], l[i], unused);
+  __stcs(reinterpret_cast<uint2*>(row16 + j0), *reinterpret_cast<const uint2*>(h));
+  __stcs(reinterpret_cast<uint2*>(row16 + kp + j0), *reinterpret_cast<const uint2*>(l));
+}
+// {s, o} of the coded rows, after the m rows of byte planes
+__host__ __device__ inline float2* k1_rowc(void* A, int64_t m, int kp) {
+  return reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(A) + (size_t)m * 3 * kp);
+}
+__device__ __forceinline__ void emit_row_constants(float2* rowc, int64_t row, float amax, double off, double* ylin_row) {
+  const bool ok = amax < INFINITY;  // false for inf / NaN
+  rowc[row] = make_float2(ok ? amax / kQMax : 0.f, (float)off);
+  if (!ok || !(fabs(off) < 3.0e38)) *ylin_row = __longlong_as_double(0x7ff8000000000000ll);
+}
+__device__ __forceinline__ float i8_inv(float amax) { return (amax > 0.f && amax < INFINITY) ? kQMax / amax : 0.f; }
+
 // ---------------------------------------------------------------------------
 // Pack particle rows into the K1 A operand [m][2*kp] fp16 = [hi | lo] of the
 // scaled coefficients; coded designs carry the centring offset
@@ -240,21 +299,19 @@ __device__ __forceinline__ void offset_limbs(double o, __half* dst, double* ylin
 // off (coded) into the offset columns; lp = sum gt(prop) (float32 terms,
 // float64 accumulation).
 __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const __nv_bfloat16* __restrict__ eps, int64_t m,
-                            int ldb, __half* __restrict__ A, double* __restrict__ ylin, PriorConst pc,
+                            int ldb, void* __restrict__ A, double* __restrict__ ylin, PriorConst pc,
                             double* __restrict__ lp) {
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= m) return;
   const float* b = beta + row * ldb;
   const __nv_bfloat16* e = eps ? eps + row * ldb : nullptr;
-  __half* ah = A + row * (2 * (int64_t)d.kp);
-  __half* al = ah + d.kp;
   double yl = 0.0, off = 0.0;
   LpAcc la;
   const double K = pc.de ? 0.0 : 1.0 / (pc.a * pc.c);
   const bool vec = (ldb & 3) == 0;
-  for (int j0 = lane * 4; j0 < d.kp; j0 += 128) {
-    float p[4] = {0.f, 0.f, 0.f, 0.f};
+  auto load_p = [&](int j0, float (&p)[4]) {
+    p[0] = p[1] = p[2] = p[3] = 0.f;
     if (vec && j0 + 4 <= d.q) {
       const float4 x = *reinterpret_cast<const float4*>(b + j0);
       p[0] = x.x;
@@ -275,18 +332,25 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const 
       for (int i = 0; i < 4; ++i)
         if (j0 + i < d.q) p[i] = b[j0 + i] + (e ? __bfloat162float(e[j0 + i]) : 0.f);
     }
-    __align__(8) __half h[4], l[4];
+  };
+  // pass 1: linear term, offset, log-prior and the row maximum of |alpha p|
+  float amax = 0.f;
+  bool bad = false;
+  for (int j0 = lane * 4; j0 < d.kp; j0 += 128) {
+    float p[4];
+    load_p(j0, p);
     float fy = 0.f, fo = 0.f;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int j = j0 + i;
-      float bs = 0.f;
       if (j < d.q) {
-        bs = (float)d.alpha[j] * p[i];
+        const float bs = (float)d.alpha[j] * p[i];
+        amax = fmaxf(amax, fabsf(bs));
+        bad |= !(fabsf(bs) < INFINITY);
         fy = fmaf(p[i], (float)d.sy[j], fy);
         fo = fmaf(p[i], d.coded ? (float)d.gamma[j] : 0.f, fo);
+        if (!d.coded && !(fabsf(bs) < kOpMax)) fy = __int_as_float(0x7fc00000);
       }
-      split_op(bs, h[i], l[i], fy);
     }
     if (lp != nullptr) {
       float pen[4];
@@ -296,21 +360,31 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const 
     }
     yl += fy;
     off += fo;
-    *reinterpret_cast<uint2*>(ah + j0) = *reinterpret_cast<const uint2*>(h);
-    *reinterpret_cast<uint2*>(al + j0) = *reinterpret_cast<const uint2*>(l);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  if (__any_sync(0xffffffffu, bad)) amax = INFINITY;  // NaN / inf in the row
+  // pass 2: the K1 operand (int8 planes for coded designs, fp16 hi/lo otherwise)
+  const float inv = i8_inv(amax);
+  for (int j0 = lane * 4; j0 < d.kp; j0 += 128) {
+    float p[4], bs[4];
+    load_p(j0, p);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) bs[i] = j0 + i < d.q ? (float)d.alpha[j0 + i] * p[i] : 0.f;
+    if (d.coded)
+      emit_i8_4(reinterpret_cast<uint8_t*>(A) + row * 3 * (int64_t)d.kp, d.kp, j0, bs, inv);
+    else
+      emit_f16_4(reinterpret_cast<__half*>(A) + row * 2 * (int64_t)d.kp, d.kp, j0, bs);
   }
   yl = warp_sum(yl);
   off = warp_sum(off);
   double lps = 0.0;
   if (lp != nullptr) lps = warp_sum(la.value(pc));
-  __syncwarp();  // orders every lane's zero stores to columns q..q+2 before lane 0's offset limbs
   if (lane == 0) {
     ylin[row] = yl;
     if (lp != nullptr) lp[row] = lps;
-    if (d.coded) {
-      // eta = sum_j g_ij alpha_j beta_j + sum_j gamma_j beta_j
-      offset_limbs(off, ah + d.q, ylin + row);
-    }
+    // eta = sum_j g_ij alpha_j beta_j + sum_j gamma_j beta_j: the offset rides in the row constants
+    if (d.coded) emit_row_constants(k1_rowc(A, m, d.kp), row, amax, off, ylin + row);
   }
 }
 
@@ -323,6 +397,26 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const 
 constexpr int kPackWarps = 8;
 constexpr int kPackSlots = 2;  // rows in flight per warp (current + 1 ahead; 3 blocks per SM)
 
+// prop = beta + eps for 4 columns of a staged (shared-memory) row
+__device__ __forceinline__ void ring_prop4(const float* b, const __nv_bfloat16* e, int j0, int q, bool full,
+                                           float (&p)[4]) {
+  p[0] = p[1] = p[2] = p[3] = 0.f;
+  if (full && j0 + 4 <= q) {
+    const float4 xv = *reinterpret_cast<const float4*>(b + j0);
+    const uint2 ev = *reinterpret_cast<const uint2*>(e + j0);
+    const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&ev);
+    const float2 ya = __bfloat1622float2(y2[0]), yb = __bfloat1622float2(y2[1]);
+    p[0] = xv.x + ya.x;
+    p[1] = xv.y + ya.y;
+    p[2] = xv.z + yb.x;
+    p[3] = xv.w + yb.y;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (j0 + i < q) p[i] = b[j0 + i] + __bfloat162float(e[j0 + i]);
+  }
+}
+
 __host__ __device__ inline size_t pack_eps_smem_bytes(int kp, int ldb) {
   return (size_t)16 * kp + (size_t)kPackWarps * kPackSlots * ((size_t)ldb * 6);
 }
@@ -330,7 +424,7 @@ __host__ __device__ inline size_t pack_eps_smem_bytes(int kp, int ldb) {
 template <int IT>
 __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design d, const float* __restrict__ beta,
                                                                 const __nv_bfloat16* __restrict__ eps, int64_t m,
-                                                                int ldb, __half* __restrict__ A,
+                                                                int ldb, void* __restrict__ A,
                                                                 double* __restrict__ ylin, PriorConst pc,
                                                                 double* __restrict__ lp) {
   extern __shared__ float4 csm[];  // [kp] x {alpha, sy, gamma, pen}, then the row rings
@@ -374,9 +468,9 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
     phase ^= 1u << s;
     const float* b = reinterpret_cast<const float*>(ring + s * slotB);
     const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(ring + s * slotB + rowB);
-    __half* ah = A + row * (2 * (int64_t)d.kp);
-    __half* al = ah + d.kp;
     double yl = 0.0, off = 0.0;  // same grouping as pack_kernel => identical sums
+    float amax = 0.f;
+    bool bad = false;
     // log-prior: the LpAcc product order without its per-chunk overflow
     // branch (factors are >= 1, so the running product can only overflow
     // upwards; one check per lane below), the flag applied as a multiply
@@ -387,34 +481,22 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
       const int j0 = it * 128 + lane * 4;
       if (j0 >= d.kp) break;
       float fy = 0.f, fo = 0.f;
-      float p[4] = {0.f, 0.f, 0.f, 0.f};
-      if (full && j0 + 4 <= d.q) {
-        const float4 xv = *reinterpret_cast<const float4*>(b + j0);
-        const uint2 ev = *reinterpret_cast<const uint2*>(e + j0);
-        const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&ev);
-        const float2 ya = __bfloat1622float2(y2[0]), yb = __bfloat1622float2(y2[1]);
-        p[0] = xv.x + ya.x;
-        p[1] = xv.y + ya.y;
-        p[2] = xv.z + yb.x;
-        p[3] = xv.w + yb.y;
-      } else {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (j0 + i < d.q) p[i] = b[j0 + i] + __bfloat162float(e[j0 + i]);
-      }
+      float p[4];
+      ring_prop4(b, e, j0, d.q, full, p);
       const float4 va = *reinterpret_cast<const float4*>(ca + j0);
       const float4 vs = *reinterpret_cast<const float4*>(cs + j0);
       const float4 vg = *reinterpret_cast<const float4*>(cg + j0);
       const float4 vp = *reinterpret_cast<const float4*>(cp + j0);
       const float a4[4] = {va.x, va.y, va.z, va.w}, s4[4] = {vs.x, vs.y, vs.z, vs.w};
       const float g4[4] = {vg.x, vg.y, vg.z, vg.w}, p4[4] = {vp.x, vp.y, vp.z, vp.w};
-      __align__(8) __half h[4], l[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const float bs = a4[i] * p[i];
         fy = fmaf(p[i], s4[i], fy);
         fo = fmaf(p[i], g4[i], fo);
-        split_op(bs, h[i], l[i], fy);
+        amax = fmaxf(amax, fabsf(bs));
+        bad |= !(fabsf(bs) < INFINITY);
+        if (!d.coded && !(fabsf(bs) < kOpMax)) fy = __int_as_float(0x7fc00000);
       }
       {
         npen += (p4[0] + p4[1]) + (p4[2] + p4[3]);
@@ -427,8 +509,28 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
       }
       yl += fy;
       off += fo;
-      __stcs(reinterpret_cast<uint2*>(ah + j0), *reinterpret_cast<const uint2*>(h));
-      __stcs(reinterpret_cast<uint2*>(al + j0), *reinterpret_cast<const uint2*>(l));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if (__any_sync(0xffffffffu, bad)) amax = INFINITY;
+    {  // pass 2: the K1 operand from the staged row
+      const float inv = i8_inv(amax);
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const int j0 = it * 128 + lane * 4;
+        if (j0 >= d.kp) break;
+        float p[4], bs[4];
+        ring_prop4(b, e, j0, d.q, full, p);
+        const float4 va = *reinterpret_cast<const float4*>(ca + j0);
+        bs[0] = va.x * p[0];
+        bs[1] = va.y * p[1];
+        bs[2] = va.z * p[2];
+        bs[3] = va.w * p[3];
+        if (d.coded)
+          emit_i8_4(reinterpret_cast<uint8_t*>(A) + row * 3 * (int64_t)d.kp, d.kp, j0, bs, inv);
+        else
+          emit_f16_4(reinterpret_cast<__half*>(A) + row * 2 * (int64_t)d.kp, d.kp, j0, bs);
+      }
     }
     double lpl;
     if (pc.de) {
@@ -460,9 +562,7 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
     if (lane == 0) {
       ylin[row] = yl;
       if (lp != nullptr) lp[row] = lps;
-      if (d.coded) {
-        offset_limbs(off, ah + d.q, ylin + row);
-      }
+      if (d.coded) emit_row_constants(k1_rowc(A, m, d.kp), row, amax, off, ylin + row);
     }
   }
 }
@@ -476,7 +576,7 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
 template <int IT, int LPR>
 __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
     spa_design d, const float* __restrict__ beta, const __nv_bfloat16* __restrict__ eps, int64_t m, int ldb,
-    __half* __restrict__ A, double* __restrict__ ylin, PriorConst pc, double* __restrict__ lp) {
+    void* __restrict__ A, double* __restrict__ ylin, PriorConst pc, double* __restrict__ lp) {
   constexpr int R = 32 / LPR;
   extern __shared__ float4 csm[];  // [kp] x {alpha, sy, gamma, pen}, then the row rings
   __shared__ uint64_t bars[kPackWarps][kPackSlots];
@@ -527,45 +627,30 @@ __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
     const bool live = row < m;
     const float* b = reinterpret_cast<const float*>(ring + s * groupB + rsub * slotB);
     const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(ring + s * groupB + rsub * slotB + rowB);
-    __half* ah = A + (live ? row : 0) * (2 * (int64_t)d.kp);
-    __half* al = ah + d.kp;
     double yl = 0.0, off = 0.0, prod = 1.0, lin = 0.0;
-    float npen = 0.f;
+    float npen = 0.f, amax = 0.f;
+    bool bad = false;
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
       const int j0 = (it * LPR + sub) * 4;
       if (j0 >= d.kp) break;
       float fy = 0.f, fo = 0.f;
       float p[4] = {0.f, 0.f, 0.f, 0.f};
-      if (live) {
-        if (full && j0 + 4 <= d.q) {
-          const float4 xv = *reinterpret_cast<const float4*>(b + j0);
-          const uint2 ev = *reinterpret_cast<const uint2*>(e + j0);
-          const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&ev);
-          const float2 ya = __bfloat1622float2(y2[0]), yb = __bfloat1622float2(y2[1]);
-          p[0] = xv.x + ya.x;
-          p[1] = xv.y + ya.y;
-          p[2] = xv.z + yb.x;
-          p[3] = xv.w + yb.y;
-        } else {
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (j0 + i < d.q) p[i] = b[j0 + i] + __bfloat162float(e[j0 + i]);
-        }
-      }
+      if (live) ring_prop4(b, e, j0, d.q, full, p);
       const float4 va = *reinterpret_cast<const float4*>(ca + j0);
       const float4 vs = *reinterpret_cast<const float4*>(cs + j0);
       const float4 vg = *reinterpret_cast<const float4*>(cg + j0);
       const float4 vp = *reinterpret_cast<const float4*>(cp + j0);
       const float a4[4] = {va.x, va.y, va.z, va.w}, s4[4] = {vs.x, vs.y, vs.z, vs.w};
       const float g4[4] = {vg.x, vg.y, vg.z, vg.w}, p4[4] = {vp.x, vp.y, vp.z, vp.w};
-      __align__(8) __half h[4], l[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const float bs = a4[i] * p[i];
         fy = fmaf(p[i], s4[i], fy);
         fo = fmaf(p[i], g4[i], fo);
-        split_op(bs, h[i], l[i], fy);
+        amax = fmaxf(amax, fabsf(bs));
+        bad |= !(fabsf(bs) < INFINITY);
+        if (!d.coded && !(fabsf(bs) < kOpMax)) fy = __int_as_float(0x7fc00000);
       }
       npen += (p4[0] + p4[1]) + (p4[2] + p4[3]);
       const double x0 = (double)(fabsf(p[0]) * p4[0]), x1 = (double)(fabsf(p[1]) * p4[1]);
@@ -576,9 +661,31 @@ __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
         prod *= fma(x0, K, 1.0) * fma(x1, K, 1.0) * (fma(x2, K, 1.0) * fma(x3, K, 1.0));
       yl += fy;
       off += fo;
-      if (live) {
-        __stcs(reinterpret_cast<uint2*>(ah + j0), *reinterpret_cast<const uint2*>(h));
-        __stcs(reinterpret_cast<uint2*>(al + j0), *reinterpret_cast<const uint2*>(l));
+    }
+    // row maximum over the row's LPR lanes (aligned groups of the warp)
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) {
+      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      bad |= __shfl_xor_sync(0xffffffffu, (int)bad, o) != 0;
+    }
+    if (bad) amax = INFINITY;
+    if (live) {  // pass 2: the K1 operand from the staged row
+      const float inv = i8_inv(amax);
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const int j0 = (it * LPR + sub) * 4;
+        if (j0 >= d.kp) break;
+        float p[4], bs[4];
+        ring_prop4(b, e, j0, d.q, full, p);
+        const float4 va = *reinterpret_cast<const float4*>(ca + j0);
+        bs[0] = va.x * p[0];
+        bs[1] = va.y * p[1];
+        bs[2] = va.z * p[2];
+        bs[3] = va.w * p[3];
+        if (d.coded)
+          emit_i8_4(reinterpret_cast<uint8_t*>(A) + row * 3 * (int64_t)d.kp, d.kp, j0, bs, inv);
+        else
+          emit_f16_4(reinterpret_cast<__half*>(A) + row * 2 * (int64_t)d.kp, d.kp, j0, bs);
       }
     }
     double lpl;
@@ -614,9 +721,7 @@ __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
     if (live && sub == 0) {
       ylin[row] = yl;
       if (lp != nullptr) lp[row] = lpl;
-      if (d.coded) {
-        offset_limbs(off, ah + d.q, ylin + row);
-      }
+      if (d.coded) emit_row_constants(k1_rowc(A, m, d.kp), row, amax, off, ylin + row);
     }
   }
 }
@@ -2009,16 +2114,16 @@ static cudaError_t chol_graph_launch(float* S, int q, float* inv, int* info, cud
 static inline unsigned cdiv(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
 
 // Likelihood work split: units of BN tiles so the grid covers several waves.
-static void loglik_split(int64_t m, int n, int& m_tiles, int& n_tiles, int& tpu, int& units) {
+static void loglik_split(int64_t m, int n, int& m_tiles, int& n_tiles, int& tpu, int& units, int bn = 256,
+                         double item_cost = 0.1, int bm = kTcBM, int kSms = 148) {
   // persistent kernel: items = (particle tile, group of tpu subject tiles),
   // CTA b takes items b, b + 148, ...  The group size minimises the makespan
   // in subject-tile times, ceil(items / 148) * tpu, plus a small per-item
   // cost (epilogue drain, partial-sum write, pipeline ramp) -- e.g. C3
   // (512 x 20 tiles): tpu = 10, 7 rounds of 10 (the 4-tile groups of round 1
   // took 18 rounds of 4: 72 vs 70 tile times)
-  constexpr int kSms = 148;
-  m_tiles = (int)((m + kTcBM - 1) / kTcBM);
-  n_tiles = (n + 255) / 256;
+  m_tiles = (int)((m + bm - 1) / bm);
+  n_tiles = (n + bn - 1) / bn;
   double best = 1e300;
   tpu = 1;
   for (int g = 1; g <= n_tiles; ++g) {
@@ -2026,7 +2131,7 @@ static void loglik_split(int64_t m, int n, int& m_tiles, int& n_tiles, int& tpu,
     if (g > 1 && (u - 1) * g >= n_tiles) continue;  // same units as a smaller group
     const int64_t items = (int64_t)m_tiles * u;
     const int64_t rounds = (items + kSms - 1) / kSms;
-    const double cost = (double)rounds * g + 0.1 * (double)rounds;
+    const double cost = (double)rounds * g + item_cost * (double)rounds;
     if (cost < best - 1e-9) {
       best = cost;
       tpu = g;
@@ -2054,10 +2159,73 @@ int spa_philox_blocks(uint64_t k0, uint64_t k1, uint64_t first_block, int64_t co
   return 0;
 }
 
+size_t spa_k1_operand_bytes(const spa_design* d, int64_t m) {
+  if (!d || m < 0) return 0;
+  return d->coded ? (size_t)m * (3 * (size_t)d->kp + sizeof(float2)) : (size_t)m * 4 * (size_t)d->kp;
+}
+
 size_t spa_loglik_workspace_bytes(int64_t m, int32_t n) {
-  int mt, nt, tpu, units;
+  int mt, nt, tpu, units, units8;
   loglik_split(m, n, mt, nt, tpu, units);
-  return (size_t)units * (size_t)m * sizeof(double);
+  int units8r;  // int8 paths: kI8EpiGroups partial rows per unit
+  loglik_split(m, n, mt, nt, tpu, units8, kI8BN);
+  loglik_split(m, n, mt, nt, tpu, units8r, kI8BN, 0.3, 256, 74);
+  return (size_t)std::max(units, kI8EpiGroups * std::max(units8, units8r)) * (size_t)m * sizeof(double);
+}
+
+// K1 for coded designs on the int8 tensor cores (tc_k1_i8.cuh): the
+// CTA-pair kernel (resident particle tiles) for kp <= 512, the streaming one
+// above.  Work items are (particle tile, group of subject tiles) over 148
+// SMs (74 pairs).
+static bool k1_i8_use_pair(int kp) { return kp <= kI8MaxKb * kI8BK && k1_i8_pair_stages(kp) >= 2; }
+
+static int loglik_i8(const spa_design* d, const void* A, int64_t m, const double* ylin, double* out, void* ws,
+                     cudaStream_t st) {
+  const bool pair = k1_i8_use_pair(d->kp);
+  CUtensorMap ta, tb;
+  int rc = make_tmap_u8(&ta, A, 3ull * d->kp, (uint64_t)m);
+  if (rc) return rc;
+  rc = make_tmap_u8(&tb, d->gemm_b, 2ull * d->kp, (uint64_t)d->n, pair ? kI8PairB : 128);
+  if (rc) return rc;
+  K1I8Args args;
+  if (pair)  // the pair reloads its resident tiles per item: weight items more
+    loglik_split(m, d->n, args.m_tiles, args.n_tiles, args.tpu, args.units, kI8BN, 0.3, 256, 74);
+  else
+    loglik_split(m, d->n, args.m_tiles, args.n_tiles, args.tpu, args.units, kI8BN);
+  args.m = (int)m;
+  args.n = d->n;
+  args.kp = d->kp;
+  args.stages = pair ? k1_i8_pair_stages(d->kp) : kI8Stages;
+  args.rowc = k1_rowc(const_cast<void*>(A), m, d->kp);
+  args.partial = reinterpret_cast<double*>(ws);
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    SPA_CHECK_CUDA(cudaGetDevice(&dev));
+    SPA_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  if (pair) {
+    const int smem = k1_i8_pair_smem(d->kp);
+    static int attr = 0;  // largest size set so far
+    if (smem > attr) {
+      SPA_CHECK_CUDA(cudaFuncSetAttribute(k1_i8_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr = smem;
+    }
+    const int grid = 2 * std::min(args.m_tiles * args.units, sms / 2);
+    k1_i8_pair_kernel<<<grid, kI8Threads, smem, st>>>(ta, tb, args);
+  } else {
+    static bool attr_done = false;
+    if (!attr_done) {
+      SPA_CHECK_CUDA(cudaFuncSetAttribute(k1_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kI8Smem));
+      attr_done = true;
+    }
+    k1_i8_kernel<<<std::min(args.m_tiles * args.units, sms), kI8Threads, kI8Smem, st>>>(ta, tb, args);
+  }
+  SPA_CHECK_LAUNCH();
+  reduce_units_kernel<<<cdiv(m, 256), 256, 0, st>>>(reinterpret_cast<double*>(ws), kI8EpiGroups * args.units, m,
+                                                    ylin, out);
+  SPA_CHECK_LAUNCH();
+  return 0;
 }
 
 static int loglik_impl(const spa_design* d, const void* A, int64_t m, const double* ylin, double* out, void* ws,
@@ -2067,6 +2235,10 @@ static int loglik_impl(const spa_design* d, const void* A, int64_t m, const doub
   SPA_REQUIRE(m > 0 && m < (1ll << 31), kBadArgument, "spa_loglik: m out of range");
   SPA_REQUIRE(ws_bytes >= spa_loglik_workspace_bytes(m, d->n), kWorkspaceTooSmall, "spa_loglik: workspace too small");
   SPA_REQUIRE(d->terms == 1 || d->terms == 2, kBadArgument, "spa_loglik: terms must be 1 or 2");
+  if (d->coded) {
+    SPA_REQUIRE(d->kp <= 1024, kNotSupported, "spa_loglik: coded designs with q > 1024 not supported");
+    return loglik_i8(d, A, m, ylin, out, ws, st);
+  }
   TcArgs args;
   int units;
   loglik_split(m, d->n, args.m_tiles, args.n_tiles, args.tiles_per_unit, units);
@@ -2109,10 +2281,9 @@ static PriorConst make_prior(double a, double c, double c_prev) {
 int spa_pack_particles(const spa_design* d, const float* beta, int64_t m, int32_t ldb, void* A, double* ylin,
                        double a, double c, double* lp, void* stream) {
   SPA_REQUIRE(d && beta && A && ylin && m >= 0, kBadArgument, "spa_pack_particles: bad arguments");
-  SPA_REQUIRE(!d->coded || d->kp >= d->q + 3, kBadArgument, "spa_pack_particles: kp < q + 3");
+  SPA_REQUIRE(d->kp >= d->q && d->kp % 64 == 0, kBadArgument, "spa_pack_particles: kp must be >= q, a multiple of 64");
   if (m == 0) return 0;
-  pack_kernel<<<cdiv(m, 8), 256, 0, as_stream(stream)>>>(*d, beta, (const __nv_bfloat16*)nullptr, m, ldb,
-                                                        reinterpret_cast<__half*>(A), ylin,
+  pack_kernel<<<cdiv(m, 8), 256, 0, as_stream(stream)>>>(*d, beta, (const __nv_bfloat16*)nullptr, m, ldb, A, ylin,
                                                         make_prior(a, c, c), lp);
   SPA_CHECK_LAUNCH();
   return 0;
@@ -2482,7 +2653,7 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
                    double c, double* lp, void* stream) {
   SPA_REQUIRE(d && beta && Lb && zbuf && eps && A && ylin && m > 0, kBadArgument, "spa_rw_propose: bad arguments");
   SPA_REQUIRE((ldb & 3) == 0 && beta != eps, kBadArgument, "spa_rw_propose: ldb % 4 != 0 or beta aliases eps");
-  SPA_REQUIRE(!d->coded || d->kp >= d->q + 3, kBadArgument, "spa_rw_propose: kp < q + 3");
+  SPA_REQUIRE(d->kp >= d->q && d->kp % 64 == 0, kBadArgument, "spa_rw_propose: kp must be >= q, a multiple of 64");
   cudaStream_t st = as_stream(stream);
   const int q = d->q;
   const int kq = (q + 63) / 64 * 64;
@@ -2512,7 +2683,7 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
   rc = launch_tc<1, 1, kPropBN, EpiStoreT<__nv_bfloat16>>(Z, (uint64_t)kq, Lb, (uint64_t)kq, (uint64_t)q, args, 1,
                                                           epi, st);
   if (rc) return rc;
-  auto* Ab = reinterpret_cast<__half*>(A);
+  void* Ab = A;
   const PriorConst pc = make_prior(a, c, c);
   const size_t sm = pack_eps_smem_bytes(d->kp, ldb);
   auto run = [&](auto kern) -> int {

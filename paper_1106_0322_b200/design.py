@@ -7,9 +7,9 @@ of ones).  Two representations:
 * coded (the genotype case): every column takes at most 3 equally spaced
   values, x = alpha*g + gamma with g in {0,1,2} (standardised allele counts,
   reference data.py:131-140, are exactly this).  The tensor-core operand is
-  G itself (exact in bf16) and the MwG kernel reads 2-bit codes from two bit
-  planes.
-* general: arbitrary float columns; the tensor-core operand is the bf16
+  the byte planes [G | 64 G] for the int8 likelihood kernel and the MwG
+  kernel reads 2-bit codes from two bit planes.
+* general: arbitrary float columns; the tensor-core operand is the fp16
   hi/lo split [Xhi | Xlo] and the MwG kernel reads float32 columns.
 """
 
@@ -137,15 +137,16 @@ class DeviceDesign:
             p1 = np.packbits(b1, axis=1, bitorder="little").view("<u4")
             p2 = np.packbits(b2, axis=1, bitorder="little").view("<u4")
             planes = np.stack([p1, p2], axis=-1).astype(np.uint32)  # [q][n_words][2]
-            kp = _round_up(q + 3, K_ALIGN)
-            G = np.zeros((n, kp), np.float32)
+            # int8 K1 operand (csrc/tc_k1_i8.cuh): two byte planes [G | 64 G]
+            kp = _round_up(q, K_ALIGN)
+            G = np.zeros((n, 2 * kp), np.uint8)
             G[:, :q] = codes.T
-            G[:, q:q + 3] = 1.0
+            G[:, kp:kp + q] = 64 * codes.T
             t["planes"] = torch.from_numpy(planes.view(np.int32).copy()).to(dev)
             t["xlev"] = torch.from_numpy(lev).to(dev)
             t["alpha"] = torch.from_numpy(alpha).to(dev)
             t["gamma"] = torch.from_numpy(gamma).to(dev)
-            t["gemm_b"] = torch.from_numpy(G).to(dev).to(torch.float16).contiguous()  # 0/1/2 exact
+            t["gemm_b"] = torch.from_numpy(G).to(dev).contiguous()
             terms = 1
         else:
             kp = _round_up(q, K_ALIGN)

@@ -302,11 +302,11 @@ class ParticleSystem:
     def ll_workspace(self):
         if self._ll_ws is None:
             d = self.design
-            kq = _round_up(self.q, 64)
-            a_cols = max(2 * d.kp, kq)
-            nbytes = _lib.load().spa_loglik_workspace_bytes(self.N, d.n)
+            lib = _lib.load()
+            a_bytes = lib.spa_k1_operand_bytes(ctypes.byref(d.struct), self.N)
+            nbytes = lib.spa_loglik_workspace_bytes(self.N, d.n)
             self._ll_ws = dict(
-                A=torch.empty((self.N, a_cols), dtype=torch.float16, device=self.device),  # K1 operand (fp16 hi|lo)
+                A=torch.empty(max(a_bytes, 8), dtype=torch.uint8, device=self.device),  # K1 operand
                 ylin=torch.empty(self.N, dtype=torch.float64, device=self.device),
                 sp=torch.empty(self.N, dtype=torch.float64, device=self.device),
                 ws=torch.empty(max(nbytes, 8), dtype=torch.uint8, device=self.device),

@@ -67,10 +67,10 @@ def _system(name, N, seed=0):
 def test_loglik_guards(name, N):
     data, d, s = _system(name, N)
     nws = _lib.load().spa_loglik_workspace_bytes(N, d.n)
-    a_cols = 2 * d.kp
+    a_bytes = _lib.load().spa_k1_operand_bytes(ctypes.byref(d.struct), N)
     outs = []
     for poison in (False, True):
-        A = Guarded((N, a_cols), torch.float16, float("nan") if poison else 0.0)
+        A = Guarded((a_bytes,), torch.uint8, 0xFF if poison else 0)
         yl = Guarded((N,), torch.float64, float("nan") if poison else 0.0)
         out = Guarded((N,), torch.float64, float("nan"))
         ws = poisoned(nws) if poison else torch.zeros(nws, dtype=torch.uint8, device="cuda")
@@ -98,7 +98,8 @@ def test_rw_move_guards():
     for poison in (False, True):
         eps = Guarded((N, s.ldb), torch.bfloat16, float("nan") if poison else 0.0)
         eps.t[:, q:] = 0  # the padding columns are the caller's (zero) contract
-        A = Guarded((N, 2 * d.kp), torch.float16, float("nan") if poison else 0.0)
+        A = Guarded((_lib.load().spa_k1_operand_bytes(ctypes.byref(d.struct), N),), torch.uint8,
+                    0xFF if poison else 0)
         yl = Guarded((N,), torch.float64, float("nan"))
         lp = Guarded((N,), torch.float64, float("nan"))
         sp = Guarded((N,), torch.float64, float("nan"))

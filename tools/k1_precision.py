@@ -50,3 +50,19 @@ def fp16(x):
 
 print(f"bf16 hi/lo: max relative log-lik error {rel_err(bf16):.2e}")
 print(f"fp16 hi/lo: max relative log-lik error {rel_err(fp16):.2e}")
+
+
+def fixed_point_rel_err(bits):
+    """Per-row fixed point with `bits` significant bits relative to the row's
+    max |alpha_j beta_j| (the int8 three-product scheme: bits = 20 for s8
+    pieces hi*2^12 + mid*2^6 + lo), offset in float32, exact integer sums."""
+    amax = np.abs(bs).max(axis=1, keepdims=True).astype(np.float64)
+    scale = amax / (2.0 ** (bits - 1) - 1)
+    Q = np.rint(bs.astype(np.float64) / scale)
+    eta = G @ (Q * scale).T + off.astype(np.float32).astype(np.float64)[None, :]
+    ll = ylin - np.logaddexp(0, eta).sum(0)
+    return float(np.max(np.abs(ll - ref) / np.abs(ref)))
+
+
+for b in (16, 20, 22):
+    print(f"fixed point {b} bits (row max): max relative log-lik error {fixed_point_rel_err(b):.2e}")
