@@ -254,18 +254,23 @@ __device__ __forceinline__ void offset_limbs(double o, __half* dst, double* ylin
 // after the m rows by {s, o} per row (o = sum_j gamma_j beta_j).  A row
 // whose maximum is not finite gets s = 0 and a NaN linear term.
 constexpr float kQMax = 2097151.0f;  // 2^21 - 1
+__device__ __forceinline__ uint32_t pack_low_bytes(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
 __device__ __forceinline__ void emit_i8_4(uint8_t* __restrict__ row8, int kp, int j0, const float (&bs)[4],
                                           float inv) {
-  uint32_t hi = 0, mid = 0, lo = 0;
+  uint32_t Q[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    int Q = __float2int_rn(bs[i] * inv);
-    Q = max(-2097151, min(2097151, Q));
-    const uint32_t r = (uint32_t)Q & 0x3FFFu;  // Q - hi 2^14, hi = floor(Q / 2^14)
-    hi |= ((uint32_t)(Q >> 14) & 0xFFu) << (8 * i);
-    mid |= (r >> 6) << (8 * i);
-    lo |= (r & 63u) << (8 * i);
+    // rint(bs * inv) on the FMA/ALU pipes (|bs * inv| <= 2^21: exact
+    // round-to-nearest-even through the 1.5 * 2^23 magic constant)
+    const int q = __float_as_int(fmaf(bs[i], inv, 12582912.0f)) - 0x4B400000;
+    Q[i] = (uint32_t)max(-2097151, min(2097151, q));
   }
+  // hi = bits 14..21 (two's complement: floor(Q / 2^14)), mid = bits 6..13, lo = bits 0..5
+  const uint32_t hi = pack_low_bytes(Q[0] >> 14, Q[1] >> 14, Q[2] >> 14, Q[3] >> 14);
+  const uint32_t mid = pack_low_bytes(Q[0] >> 6, Q[1] >> 6, Q[2] >> 6, Q[3] >> 6);
+  const uint32_t lo = pack_low_bytes(Q[0], Q[1], Q[2], Q[3]) & 0x3F3F3F3Fu;
   __stcs(reinterpret_cast<uint32_t*>(row8 + j0), hi);
   __stcs(reinterpret_cast<uint32_t*>(row8 + kp + j0), mid);
   __stcs(reinterpret_cast<uint32_t*>(row8 + 2 * kp + j0), lo);
@@ -421,7 +426,7 @@ __host__ __device__ inline size_t pack_eps_smem_bytes(int kp, int ldb) {
   return (size_t)16 * kp + (size_t)kPackWarps * kPackSlots * ((size_t)ldb * 6);
 }
 
-template <int IT>
+template <int IT, bool CODED>
 __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design d, const float* __restrict__ beta,
                                                                 const __nv_bfloat16* __restrict__ eps, int64_t m,
                                                                 int ldb, void* __restrict__ A,
@@ -440,7 +445,7 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
     const bool v = j < d.q;
     ca[j] = v ? (float)d.alpha[j] : 0.f;
     cs[j] = v ? (float)d.sy[j] : 0.f;
-    cg[j] = (v && d.coded) ? (float)d.gamma[j] : 0.f;
+    cg[j] = (v && CODED) ? (float)d.gamma[j] : 0.f;
     cp[j] = (v && d.penalized[j]) ? 1.f : 0.f;
   }
   if (lane == 0) {
@@ -469,8 +474,8 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
     const float* b = reinterpret_cast<const float*>(ring + s * slotB);
     const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(ring + s * slotB + rowB);
     double yl = 0.0, off = 0.0;  // same grouping as pack_kernel => identical sums
-    float amax = 0.f;
-    bool bad = false;
+    float amax = 0.f, nanf = 0.f;  // nanf: sum of bs - bs (NaN iff some bs is NaN / inf)
+    float bsr[IT][4];  // alpha * prop, kept for the operand pass
     // log-prior: the LpAcc product order without its per-chunk overflow
     // branch (factors are >= 1, so the running product can only overflow
     // upwards; one check per lane below), the flag applied as a multiply
@@ -492,11 +497,15 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const float bs = a4[i] * p[i];
+        bsr[it][i] = bs;
         fy = fmaf(p[i], s4[i], fy);
         fo = fmaf(p[i], g4[i], fo);
-        amax = fmaxf(amax, fabsf(bs));
-        bad |= !(fabsf(bs) < INFINITY);
-        if (!d.coded && !(fabsf(bs) < kOpMax)) fy = __int_as_float(0x7fc00000);
+        if (CODED) {
+          amax = fmaxf(amax, fabsf(bs));
+          nanf += bs - bs;
+        } else if (!(fabsf(bs) < kOpMax)) {
+          fy = __int_as_float(0x7fc00000);
+        }
       }
       {
         npen += (p4[0] + p4[1]) + (p4[2] + p4[3]);
@@ -510,27 +519,10 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
       yl += fy;
       off += fo;
     }
+    if (CODED) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-    if (__any_sync(0xffffffffu, bad)) amax = INFINITY;
-    {  // pass 2: the K1 operand from the staged row
-      const float inv = i8_inv(amax);
-#pragma unroll
-      for (int it = 0; it < IT; ++it) {
-        const int j0 = it * 128 + lane * 4;
-        if (j0 >= d.kp) break;
-        float p[4], bs[4];
-        ring_prop4(b, e, j0, d.q, full, p);
-        const float4 va = *reinterpret_cast<const float4*>(ca + j0);
-        bs[0] = va.x * p[0];
-        bs[1] = va.y * p[1];
-        bs[2] = va.z * p[2];
-        bs[3] = va.w * p[3];
-        if (d.coded)
-          emit_i8_4(reinterpret_cast<uint8_t*>(A) + row * 3 * (int64_t)d.kp, d.kp, j0, bs, inv);
-        else
-          emit_f16_4(reinterpret_cast<__half*>(A) + row * 2 * (int64_t)d.kp, d.kp, j0, bs);
-      }
+      for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      if (__any_sync(0xffffffffu, nanf != 0.f)) amax = INFINITY;  // NaN / inf in the row
     }
     double lpl;
     if (pc.de) {
@@ -556,13 +548,25 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
       fence_proxy_async_smem();
       issue(row + kPackSlots * nwarps, s);
     }
+    {  // the K1 operand from the registers
+      const float inv = i8_inv(amax);
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const int j0 = it * 128 + lane * 4;
+        if (j0 >= d.kp) break;
+        if (CODED)
+          emit_i8_4(reinterpret_cast<uint8_t*>(A) + row * 3 * (int64_t)d.kp, d.kp, j0, bsr[it], inv);
+        else
+          emit_f16_4(reinterpret_cast<__half*>(A) + row * 2 * (int64_t)d.kp, d.kp, j0, bsr[it]);
+      }
+    }
     yl = warp_sum(yl);
     off = warp_sum(off);
     const double lps = warp_sum(lpl);
     if (lane == 0) {
       ylin[row] = yl;
       if (lp != nullptr) lp[row] = lps;
-      if (d.coded) emit_row_constants(k1_rowc(A, m, d.kp), row, amax, off, ylin + row);
+      if (CODED) emit_row_constants(k1_rowc(A, m, d.kp), row, amax, off, ylin + row);
     }
   }
 }
@@ -573,7 +577,7 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
 // stores -- is shared by R rows, which halves it at LPR = 16.  A hi/lo are
 // the same bits as pack_eps_kernel; ylin / lp / the offset are summed in a
 // different order (float64 rounding).
-template <int IT, int LPR>
+template <int IT, int LPR, bool CODED>
 __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
     spa_design d, const float* __restrict__ beta, const __nv_bfloat16* __restrict__ eps, int64_t m, int ldb,
     void* __restrict__ A, double* __restrict__ ylin, PriorConst pc, double* __restrict__ lp) {
@@ -591,7 +595,7 @@ __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
     const bool v = j < d.q;
     ca[j] = v ? (float)d.alpha[j] : 0.f;
     cs[j] = v ? (float)d.sy[j] : 0.f;
-    cg[j] = (v && d.coded) ? (float)d.gamma[j] : 0.f;
+    cg[j] = (v && CODED) ? (float)d.gamma[j] : 0.f;
     cp[j] = (v && d.penalized[j]) ? 1.f : 0.f;
   }
   if (lane == 0) {
@@ -628,8 +632,8 @@ __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
     const float* b = reinterpret_cast<const float*>(ring + s * groupB + rsub * slotB);
     const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(ring + s * groupB + rsub * slotB + rowB);
     double yl = 0.0, off = 0.0, prod = 1.0, lin = 0.0;
-    float npen = 0.f, amax = 0.f;
-    bool bad = false;
+    float npen = 0.f, amax = 0.f, nanf = 0.f;  // nanf: sum of bs - bs (NaN iff some bs is NaN / inf)
+    float bsr[IT][4];  // alpha * prop, kept for the operand pass
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
       const int j0 = (it * LPR + sub) * 4;
@@ -646,11 +650,15 @@ __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const float bs = a4[i] * p[i];
+        bsr[it][i] = bs;
         fy = fmaf(p[i], s4[i], fy);
         fo = fmaf(p[i], g4[i], fo);
-        amax = fmaxf(amax, fabsf(bs));
-        bad |= !(fabsf(bs) < INFINITY);
-        if (!d.coded && !(fabsf(bs) < kOpMax)) fy = __int_as_float(0x7fc00000);
+        if (CODED) {
+          amax = fmaxf(amax, fabsf(bs));
+          nanf += bs - bs;
+        } else if (!(fabsf(bs) < kOpMax)) {
+          fy = __int_as_float(0x7fc00000);
+        }
       }
       npen += (p4[0] + p4[1]) + (p4[2] + p4[3]);
       const double x0 = (double)(fabsf(p[0]) * p4[0]), x1 = (double)(fabsf(p[1]) * p4[1]);
@@ -663,30 +671,13 @@ __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
       off += fo;
     }
     // row maximum over the row's LPR lanes (aligned groups of the warp)
+    if (CODED) {
 #pragma unroll
-    for (int o = LPR / 2; o > 0; o >>= 1) {
-      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-      bad |= __shfl_xor_sync(0xffffffffu, (int)bad, o) != 0;
-    }
-    if (bad) amax = INFINITY;
-    if (live) {  // pass 2: the K1 operand from the staged row
-      const float inv = i8_inv(amax);
-#pragma unroll
-      for (int it = 0; it < IT; ++it) {
-        const int j0 = (it * LPR + sub) * 4;
-        if (j0 >= d.kp) break;
-        float p[4], bs[4];
-        ring_prop4(b, e, j0, d.q, full, p);
-        const float4 va = *reinterpret_cast<const float4*>(ca + j0);
-        bs[0] = va.x * p[0];
-        bs[1] = va.y * p[1];
-        bs[2] = va.z * p[2];
-        bs[3] = va.w * p[3];
-        if (d.coded)
-          emit_i8_4(reinterpret_cast<uint8_t*>(A) + row * 3 * (int64_t)d.kp, d.kp, j0, bs, inv);
-        else
-          emit_f16_4(reinterpret_cast<__half*>(A) + row * 2 * (int64_t)d.kp, d.kp, j0, bs);
+      for (int o = LPR / 2; o > 0; o >>= 1) {
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        nanf += __shfl_xor_sync(0xffffffffu, nanf, o);
       }
+      if (nanf != 0.f) amax = INFINITY;  // NaN / inf in the row
     }
     double lpl;
     if (pc.de) {
@@ -712,6 +703,18 @@ __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
       fence_proxy_async_smem();
       issue(g + kPackSlots * nwarps, s);
     }
+    if (live) {  // the K1 operand from the registers
+      const float inv = i8_inv(amax);
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const int j0 = (it * LPR + sub) * 4;
+        if (j0 >= d.kp) break;
+        if (CODED)
+          emit_i8_4(reinterpret_cast<uint8_t*>(A) + row * 3 * (int64_t)d.kp, d.kp, j0, bsr[it], inv);
+        else
+          emit_f16_4(reinterpret_cast<__half*>(A) + row * 2 * (int64_t)d.kp, d.kp, j0, bsr[it]);
+      }
+    }
 #pragma unroll
     for (int o = LPR / 2; o > 0; o >>= 1) {
       yl += __shfl_xor_sync(0xffffffffu, yl, o);
@@ -721,7 +724,7 @@ __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
     if (live && sub == 0) {
       ylin[row] = yl;
       if (lp != nullptr) lp[row] = lpl;
-      if (d.coded) emit_row_constants(k1_rowc(A, m, d.kp), row, amax, off, ylin + row);
+      if (CODED) emit_row_constants(k1_rowc(A, m, d.kp), row, amax, off, ylin + row);
     }
   }
 }
@@ -2165,37 +2168,34 @@ size_t spa_k1_operand_bytes(const spa_design* d, int64_t m) {
 }
 
 size_t spa_loglik_workspace_bytes(int64_t m, int32_t n) {
-  int mt, nt, tpu, units, units8;
-  loglik_split(m, n, mt, nt, tpu, units);
-  int units8r;  // int8 paths: kI8EpiGroups partial rows per unit
-  loglik_split(m, n, mt, nt, tpu, units8, kI8BN);
+  int mt, nt, tpu, units, units8r, units8s;
+  loglik_split(m, n, mt, nt, tpu, units);  // fp16 path (general designs)
+  // int8 paths (coded designs): kI8EpiGroups partial rows per unit
   loglik_split(m, n, mt, nt, tpu, units8r, kI8BN, 0.3, 256, 74);
-  return (size_t)std::max(units, kI8EpiGroups * std::max(units8, units8r)) * (size_t)m * sizeof(double);
+  loglik_split(m, n, mt, nt, tpu, units8s, kI8BN, 0.1, 256, 74);
+  return (size_t)std::max(units, kI8EpiGroups * std::max(units8r, units8s)) * (size_t)m * sizeof(double);
 }
 
-// K1 for coded designs on the int8 tensor cores (tc_k1_i8.cuh): the
-// CTA-pair kernel (resident particle tiles) for kp <= 512, the streaming one
-// above.  Work items are (particle tile, group of subject tiles) over 148
-// SMs (74 pairs).
-static bool k1_i8_use_pair(int kp) { return kp <= kI8MaxKb * kI8BK && k1_i8_pair_stages(kp) >= 2; }
+// K1 for coded designs on the int8 tensor cores (tc_k1_i8.cuh): CTA-pair
+// kernels -- resident particle tiles for kp <= 512, streamed above.  Work
+// items are (256-particle tile, group of subject tiles) over 74 pairs.
+static bool k1_i8_resident(int kp) { return kp <= kI8MaxKb * kI8BK && k1_i8_pair_stages(kp) >= 2; }
 
 static int loglik_i8(const spa_design* d, const void* A, int64_t m, const double* ylin, double* out, void* ws,
                      cudaStream_t st) {
-  const bool pair = k1_i8_use_pair(d->kp);
+  const bool res = k1_i8_resident(d->kp);
   CUtensorMap ta, tb;
   int rc = make_tmap_u8(&ta, A, 3ull * d->kp, (uint64_t)m);
   if (rc) return rc;
-  rc = make_tmap_u8(&tb, d->gemm_b, 2ull * d->kp, (uint64_t)d->n, pair ? kI8PairB : 128);
+  rc = make_tmap_u8(&tb, d->gemm_b, 2ull * d->kp, (uint64_t)d->n, kI8PairB);
   if (rc) return rc;
   K1I8Args args;
-  if (pair)  // the pair reloads its resident tiles per item: weight items more
-    loglik_split(m, d->n, args.m_tiles, args.n_tiles, args.tpu, args.units, kI8BN, 0.3, 256, 74);
-  else
-    loglik_split(m, d->n, args.m_tiles, args.n_tiles, args.tpu, args.units, kI8BN);
+  // a resident pair reloads its particle tiles per item: weight items more
+  loglik_split(m, d->n, args.m_tiles, args.n_tiles, args.tpu, args.units, kI8BN, res ? 0.3 : 0.1, 256, 74);
   args.m = (int)m;
   args.n = d->n;
   args.kp = d->kp;
-  args.stages = pair ? k1_i8_pair_stages(d->kp) : kI8Stages;
+  args.stages = res ? k1_i8_pair_stages(d->kp) : kI8PairStreamStages;
   args.rowc = k1_rowc(const_cast<void*>(A), m, d->kp);
   args.partial = reinterpret_cast<double*>(ws);
   static int sms = 0;
@@ -2204,22 +2204,26 @@ static int loglik_i8(const spa_design* d, const void* A, int64_t m, const double
     SPA_CHECK_CUDA(cudaGetDevice(&dev));
     SPA_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  if (pair) {
-    const int smem = k1_i8_pair_smem(d->kp);
-    static int attr = 0;  // largest size set so far
-    if (smem > attr) {
-      SPA_CHECK_CUDA(cudaFuncSetAttribute(k1_i8_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr = smem;
-    }
+  {
     const int grid = 2 * std::min(args.m_tiles * args.units, sms / 2);
-    k1_i8_pair_kernel<<<grid, kI8Threads, smem, st>>>(ta, tb, args);
-  } else {
-    static bool attr_done = false;
-    if (!attr_done) {
-      SPA_CHECK_CUDA(cudaFuncSetAttribute(k1_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kI8Smem));
-      attr_done = true;
+    if (res) {
+      const int smem = k1_i8_pair_smem(d->kp);
+      static int attr = 0;  // largest size set so far
+      if (smem > attr) {
+        SPA_CHECK_CUDA(
+            cudaFuncSetAttribute(k1_i8_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = smem;
+      }
+      k1_i8_pair_kernel<true><<<grid, kI8Threads, smem, st>>>(ta, tb, args);
+    } else {
+      static bool attr_done = false;
+      if (!attr_done) {
+        SPA_CHECK_CUDA(cudaFuncSetAttribute(k1_i8_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            kI8PairStreamSmem));
+        attr_done = true;
+      }
+      k1_i8_pair_kernel<false><<<grid, kI8Threads, kI8PairStreamSmem, st>>>(ta, tb, args);
     }
-    k1_i8_kernel<<<std::min(args.m_tiles * args.units, sms), kI8Threads, kI8Smem, st>>>(ta, tb, args);
   }
   SPA_CHECK_LAUNCH();
   reduce_units_kernel<<<cdiv(m, 256), 256, 0, st>>>(reinterpret_cast<double*>(ws), kI8EpiGroups * args.units, m,
@@ -2701,7 +2705,8 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
   // 2 rows per warp iteration where the doubled ring still fits 2 blocks per SM
   if (d->kp > 128 && d->kp <= 512) {
     const size_t sm2 = (size_t)16 * d->kp + (size_t)kPackWarps * kPackSlots * 2 * ((size_t)ldb * 6);
-    auto kern = d->kp <= 256 ? pack_eps_rows_kernel<4, 16> : pack_eps_rows_kernel<8, 16>;
+    auto kern = d->coded ? (d->kp <= 256 ? pack_eps_rows_kernel<4, 16, true> : pack_eps_rows_kernel<8, 16, true>)
+                         : (d->kp <= 256 ? pack_eps_rows_kernel<4, 16, false> : pack_eps_rows_kernel<8, 16, false>);
     // the attribute / occupancy queries once per (kernel, smem size): the
     // move loop calls this 5 times per step
     struct Geo {
@@ -2736,10 +2741,17 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
       return 0;
     }
   }
-  if (d->kp <= 128) return run(pack_eps_kernel<1>);
-  if (d->kp <= 256) return run(pack_eps_kernel<2>);
-  if (d->kp <= 512) return run(pack_eps_kernel<4>);
-  if (d->kp <= 1024 && sm <= 200 * 1024) return run(pack_eps_kernel<8>);
+  if (d->coded) {
+    if (d->kp <= 128) return run(pack_eps_kernel<1, true>);
+    if (d->kp <= 256) return run(pack_eps_kernel<2, true>);
+    if (d->kp <= 512) return run(pack_eps_kernel<4, true>);
+    if (d->kp <= 1024 && sm <= 200 * 1024) return run(pack_eps_kernel<8, true>);
+  } else {
+    if (d->kp <= 128) return run(pack_eps_kernel<1, false>);
+    if (d->kp <= 256) return run(pack_eps_kernel<2, false>);
+    if (d->kp <= 512) return run(pack_eps_kernel<4, false>);
+    if (d->kp <= 1024 && sm <= 200 * 1024) return run(pack_eps_kernel<8, false>);
+  }
   pack_kernel<<<cdiv(m, 8), 256, 0, st>>>(*d, beta, epsb, m, ldb, Ab, ylin, pc, lp);
   SPA_CHECK_LAUNCH();
   return 0;
@@ -2756,8 +2768,13 @@ int spa_prepare(void) {
       (const void*)tc_gemm_kernel<2, 2, 256, EpiSoftplusRowSum, 1, true>,
       (const void*)tc_gemm_kernel<1, 1, 256, EpiStoreT<__nv_bfloat16>>,
       (const void*)tc_gemm_kernel<2, 2, 256, EpiStoreT<float>>,
-      (const void*)pack_kernel, (const void*)pack_eps_kernel<1>, (const void*)pack_eps_kernel<2>,
-      (const void*)pack_eps_kernel<4>, (const void*)pack_eps_kernel<8>, (const void*)prior_kernel,
+      (const void*)pack_kernel, (const void*)pack_eps_kernel<1, true>, (const void*)pack_eps_kernel<2, true>,
+      (const void*)pack_eps_kernel<4, true>, (const void*)pack_eps_kernel<8, true>,
+      (const void*)pack_eps_kernel<1, false>, (const void*)pack_eps_kernel<2, false>,
+      (const void*)pack_eps_kernel<4, false>, (const void*)pack_eps_kernel<8, false>,
+      (const void*)pack_eps_rows_kernel<4, 16, true>, (const void*)pack_eps_rows_kernel<8, 16, true>,
+      (const void*)pack_eps_rows_kernel<4, 16, false>, (const void*)pack_eps_rows_kernel<8, 16, false>,
+      (const void*)k1_i8_pair_kernel<true>, (const void*)k1_i8_pair_kernel<false>, (const void*)prior_kernel,
       (const void*)prior_reweight_rows_kernel<8, 4>, (const void*)prior_reweight_rows_kernel<8, 8>,
       (const void*)prior_reweight_rows_kernel<16, 8>, (const void*)prior_reweight_rows_kernel<16, 16>,
       (const void*)prior_reweight_rows_kernel<32, 16>, (const void*)prior_reweight_kernel<32>, (const void*)lse_stats_kernel, (const void*)lse_combine_kernel,
