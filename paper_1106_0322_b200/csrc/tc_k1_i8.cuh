@@ -84,42 +84,35 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool a_signed) {
          | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-// exact int32 -> float32 for |x| < 2^22 without the XU pipe
-__device__ __forceinline__ float i2f_small(int x) { return __int_as_float(x + 0x4B400000) - 12582912.0f; }
-
-// Softplus sum of one 32-column accumulator chunk of a row:
-//   sum_i softplus(eta_i) = sum_i max(eta_i, 0) + ln 2 * log2 prod_i (1 + 2^(-|eta_i| log2 e))
-// with the product taken over four interleaved groups of eight factors in
-// [1, 2] (one lg2 per group instead of one per element: the XU pipe does
-// one exp2 per element and 1/8 lg2).  eta_i = 4 s (4096 acc1 + floor(acc2 / 4))
-// + off (off carries the mean dropped fraction, see the epilogue notes).
-// Columns >= nval (ragged last subject tile) contribute nothing.
-__device__ __forceinline__ float k1_i8_chunk_sum(const uint32_t (&r1)[32], const uint32_t (&r2)[32], float s4,
-                                                 float off, int nval) {
+// Softplus sum of one 32-column accumulator chunk of a row, in log2 units:
+//   sum_i softplus(eta_i) = ln 2 * [ sum_i max(y_i, 0) + log2 prod_i (1 + 2^-|y_i|) ],  y = eta log2 e
+// with the product over four interleaved groups of eight factors in [1, 2]
+// (one lg2 per group: the XU pipe does one exp2 per element and 1/8 lg2).
+// The accumulators combine into the integer T in one shift-add:
+//   WIDE = false (kp <= 512): T = 2^14 acc1 + acc2 = sum_j g_j Q_j exactly
+//     (|sum_j g_j Q_j| <= 2 * 512 * (2^21 - 1) < 2^31; the int32 arithmetic
+//     is modular, so the exact in-range value comes out);
+//   WIDE = true (kp <= 1024): T = 2^12 acc1 + floor(acc2 / 4) (|T| < 2^31),
+//     the dropped fraction's mean (3/8) carried by the caller's offset;
+// then y = sl * float(T) + ol (sl = s log2 e, ol = o log2 e, per row).
+// float(T) rounds to 24 bits: relative 6e-8 of eta's linear part.
+// Returns the chunk's sum of softplus / ln 2.  Columns >= nval (ragged last
+// subject tile) contribute nothing (y = -inf).
+template <bool WIDE>
+__device__ __forceinline__ float k1_i8_chunk_sum(const uint32_t (&r1)[32], const uint32_t (&r2)[32], float sl,
+                                                 float ol, int nval) {
   float P[4] = {1.f, 1.f, 1.f, 1.f}, R[2] = {0.f, 0.f};
-  if (nval >= 32) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const float f1 = i2f_small((int)r1[i]);
-      const float f2 = __int_as_float((r2[i] >> 2) | 0x4B000000u) - 8388608.0f;
-      const float x = fmaf(s4, fmaf(4096.0f, f1, f2), off);
-      const float e = fast_ex2(fabsf(x) * -1.4426950408889634f);
-      P[i & 3] = fmaf(P[i & 3], e, P[i & 3]);
-      R[i & 1] += fmaxf(x, 0.0f);
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const float f1 = i2f_small((int)r1[i]);
-      const float f2 = __int_as_float((r2[i] >> 2) | 0x4B000000u) - 8388608.0f;
-      const float x = i < nval ? fmaf(s4, fmaf(4096.0f, f1, f2), off) : -INFINITY;  // softplus(-inf) = 0
-      const float e = fast_ex2(fabsf(x) * -1.4426950408889634f);
-      P[i & 3] = fmaf(P[i & 3], i < nval ? e : 0.0f, P[i & 3]);
-      R[i & 1] += fmaxf(x, 0.0f);
-    }
+  for (int i = 0; i < 32; ++i) {
+    const int T = WIDE ? (int)((r1[i] << 12) + (r2[i] >> 2)) : (int)((r1[i] << 14) + r2[i]);
+    float y = fmaf(sl, __int2float_rn(T), ol);
+    if (nval < 32 && i >= nval) y = -INFINITY;
+    const float e = fast_ex2(-fabsf(y));
+    P[i & 3] = fmaf(P[i & 3], e, P[i & 3]);
+    R[i & 1] += fmaxf(y, 0.0f);
   }
   const float lg = (fast_lg2(P[0]) + fast_lg2(P[1])) + (fast_lg2(P[2]) + fast_lg2(P[3]));
-  return fmaf(0.6931471805599453f, lg, R[0] + R[1]);
+  return (R[0] + R[1]) + lg;
 }
 
 struct K1I8Args {
@@ -346,12 +339,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
     // set, two groups of four warps (one per TMEM lane quarter) take 64
     // columns each, in two 32-column chunks.  The buffer is released after
     // the second chunk is in registers.
-    // eta = s (2^14 acc1 + acc2) + o = 4 s (4096 acc1 + acc2 / 4) + o, with
-    // both accumulators converted without the XU pipe (which the softplus
-    // exp2 keeps busy): acc1 (|acc1| < 2^22) exactly, acc2 (0 <= acc2 <
-    // 2^25) as floor(acc2 / 4) exactly, the dropped fraction (mean 3/8)
-    // restored in the offset -- an absolute error below 1.5 s, under the
-    // 22-bit quantisation's own (tests: 1e-5 relative).
+    // eta = s (2^14 acc1 + acc2) + o (k1_i8_chunk_sum; the streamed kp > 512
+    // variant drops acc2's two low bits -- an absolute error below 1.5 s,
+    // under the 22-bit quantisation's own; tests: 1e-5 relative).
     const int quarter = warp & 3;
     const int set = (warp - 2) >> 3;
     const int grp = ((warp - 2) >> 2) & 1;
@@ -363,7 +353,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
       const int row = mt * 256 + (int)rank * 128 + quarter * 32 + lane;
       float2 rc = make_float2(0.f, 0.f);
       if (row < args.m) rc = args.rowc[row];
-      const float s4 = rc.x * 4.0f, off = fmaf(rc.x, 1.5f, rc.y);
+      // log2-unit row constants (see k1_i8_chunk_sum)
+      constexpr float kLog2e = 1.4426950408889634f;
+      const float sl = kResA ? rc.x * kLog2e : rc.x * (4.0f * kLog2e);
+      const float ol = kResA ? rc.y * kLog2e : fmaf(rc.x, 1.5f, rc.y) * kLog2e;
       double acc = 0.0;
       for (int nt = nt0; nt < nt1; ++nt, ++it) {
         if ((it & 1) != set) continue;
@@ -383,11 +376,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(tempty_c);  // the leader's barrier
           }
-          tile += k1_i8_chunk_sum(r1, r2, s4, off, args.n - (nt * kI8BN + grp * 64 + c * 32));
+          tile += k1_i8_chunk_sum<!kResA>(r1, r2, sl, ol, args.n - (nt * kI8BN + grp * 64 + c * 32));
         }
         acc += (double)tile;
       }
-      if (row < args.m) args.partial[(size_t)(kI8EpiGroups * unit + set * 2 + grp) * args.m + row] = acc;
+      if (row < args.m)
+        args.partial[(size_t)(kI8EpiGroups * unit + set * 2 + grp) * args.m + row] = acc * 0.6931471805599453;
     }
   }
 
