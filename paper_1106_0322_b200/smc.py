@@ -15,6 +15,8 @@ Extra SmcConfig fields (defaults keep the reference's behaviour):
     moves        RW moves per step
     rw_scale     RW proposal scale numerator (scale = rw_scale / sqrt(q))
     init_chains  parallel MwG chains for initialisation (0 = auto)
+    init_forks   thinning chains forked from each burned-in chain (0 = auto:
+                 1 when init_chains is pinned, else auto_chains' choice)
     summary_levels / summary_deltas
                  per-step weighted marginal summaries computed on the device
                  (StepRecord.summary; see marginal_summaries)
@@ -47,7 +49,7 @@ from ._philox_host import first_uniform
 from .design import DeviceDesign
 from .model import GtPrior
 
-TAG_INIT, TAG_MOVE, TAG_RESAMPLE, TAG_RWMOVE = 0, 1, 2, 3
+TAG_INIT, TAG_MOVE, TAG_RESAMPLE, TAG_RWMOVE, TAG_INIT_FORK = 0, 1, 2, 3, 4
 
 # Optional CUDA-event timer around the dominant kernel (bench.py sets it;
 # events are recorded on the launching stream).
@@ -119,6 +121,7 @@ class SmcConfig:
     moves: int = 5
     rw_scale: float = 2.38
     init_chains: int = 0
+    init_forks: int = 0
     summary_levels: tuple = ()
     summary_deltas: tuple = ()
     rw_factor_lag: int = 2
@@ -141,8 +144,8 @@ class SmcConfig:
             raise ValueError(f"move_kernel must be 'mwg' or 'rw', got {self.move_kernel!r}")
         if self.rw_factor_lag not in (0, 1, 2):
             raise ValueError(f"rw_factor_lag must be 0, 1 or 2, got {self.rw_factor_lag!r}")
-        if self.moves < 1 or self.init_chains < 0 or not self.rw_scale > 0:
-            raise ValueError("moves >= 1, init_chains >= 0, rw_scale > 0 required")
+        if self.moves < 1 or self.init_chains < 0 or self.init_forks < 0 or not self.rw_scale > 0:
+            raise ValueError("moves >= 1, init_chains >= 0, init_forks >= 0, rw_scale > 0 required")
         if len(self.summary_levels) > 4 or not all(0.0 < float(v) < 1.0 for v in self.summary_levels):
             raise ValueError("summary_levels: at most 4 quantile levels in (0, 1)")
         if len(self.summary_deltas) > 4 or not all(float(v) > 0.0 for v in self.summary_deltas):
@@ -721,21 +724,25 @@ def resident_chains(design: DeviceDesign) -> int:
 _CHAIN_SHARE_EXP = 0.52
 
 
-def auto_chains(design: DeviceDesign, N: int, burn: int, thin: int) -> int:
-    """Parallel initialisation chains per GPU: c chains per SM (up to the
-    resident wave) minimising the sequential sweeps per chain, burn +
-    N*thin/(SMs*c), times the sweep time at c chains per SM (~c^0.52).  C3
-    with 2000 burn sweeps: one chain per SM (1.32 s vs 1.39 s for two); with
-    200, two."""
+def auto_chains(design: DeviceDesign, N: int, burn: int, thin: int, forks: int = 0) -> tuple[int, int]:
+    """Parallel initialisation chains per GPU and thinning forks per chain:
+    c burn-in chains per SM, each forked into F thinning chains (c F per SM
+    within the resident wave), minimising the sequential sweep time
+        burn * c^0.52 + (N thin / (SMs c F)) * (c F)^0.52
+    (a sweep at k chains per SM takes ~k^0.52 of one chain's).  forks > 0
+    pins F.  C3 with 2000 burn sweeps: c = 1, F = 3 (init 1.37 -> 1.16 s vs
+    one unforked chain per SM); with 200: c = 1, F = 3."""
     resident = resident_chains(design)
     sms = torch.cuda.get_device_properties(design.tensors["sy"].device).multi_processor_count
     occ = max(1, resident // max(sms, 1))
-    best, best_c = None, 1
+    best, plan = None, (1, 1)
     for c in range(1, occ + 1):
-        cost = (burn + N * thin / (sms * c)) * c**_CHAIN_SHARE_EXP
-        if best is None or cost < best:
-            best, best_c = cost, c
-    return best_c * sms
+        for f in ([forks] if forks else range(1, occ // c + 1)):
+            k = c * f
+            cost = (burn * c**_CHAIN_SHARE_EXP if burn > 0 else 0.0) + (N * thin / (sms * k)) * k**_CHAIN_SHARE_EXP
+            if best is None or cost < best - 1e-9:
+                best, plan = cost, (c, f)
+    return plan[0] * sms, plan[1]
 
 
 def init_plan(N_total: int, init_chains: int, chains_auto: int) -> tuple[int, int]:
@@ -752,15 +759,20 @@ def init_particles(data, prior_at_b1: GtPrior, config: SmcConfig, intercept: boo
     """Seed the particles from MwG chains targeting the first posterior.
 
     The reference runs ONE chain (init_burn sweeps, then every init_thin-th
-    state; smc.py:202-245).  Here K independent chains run in parallel, chain
-    c keyed (seed, 0, 0, c): each burns init_burn sweeps, then its state after
-    every further init_thin sweeps fills its next slot of the contiguous block
-    [c R, (c+1) R).  Total chain-sweeps K*init_burn + N*init_thin; K defaults
-    to whole waves of chains per GPU (auto_chains x ranks: one or more chains
-    per SM, whichever minimises the wall time of these latency-bound sweeps).  A rank
-    simulates only the chains whose blocks meet its shard, so for a given K
-    the particles are identical for any number of GPUs.
-    Returns (system, acceptance_rate)."""
+    state; smc.py:202-245).  Here K1 independent chains run in parallel, chain
+    c keyed (seed, 0, 0, c), each burning init_burn sweeps; each burned-in
+    chain is then forked into F thinning chains (fork f of chain c is chain
+    k = c F + f, keyed (seed, TAG_INIT_FORK, 0, k); F = 1 keeps chain c's own
+    stream), and chain k's state after every further init_thin sweeps fills
+    its next slot of the contiguous block [k R, (k+1) R).  Every thinning
+    chain is a Markov chain started from a burned-in state, as in the
+    reference, and F only changes which chain a slot comes from.  K1 defaults
+    to whole waves of chains per GPU (auto_chains x ranks: one or more per
+    SM) and F jointly minimise the wall time of these latency-bound sweeps
+    (auto_chains).  A rank
+    simulates only the chains whose blocks meet its shard (and their
+    parents), so for given K1 and F the particles are identical for any
+    number of GPUs.  Returns (system, acceptance_rate)."""
     _require_cuda()
     if design is None:
         design = DeviceDesign.build(data.X, data.y, intercept)
@@ -768,23 +780,41 @@ def init_particles(data, prior_at_b1: GtPrior, config: SmcConfig, intercept: boo
     world = 1 if group is None else group.world
     shard, offset = (N_total, 0) if group is None else group.shard(N_total)
     system = ParticleSystem(design, shard, prior_at_b1.a, intercept, rank_offset=offset, N_total=N_total)
-    auto = 0 if config.init_chains else auto_chains(design, N_total // world, config.init_burn, config.init_thin) * world
-    K, R = init_plan(N_total, config.init_chains, auto)
+    auto, F = 0, 1
+    if not config.init_chains:
+        auto, F = auto_chains(design, N_total // world, config.init_burn, config.init_thin, config.init_forks)
+        auto *= world
+    elif config.init_forks:
+        F = config.init_forks
+    if config.init_burn <= 0:
+        F = 1
+    K1, _ = init_plan(N_total, config.init_chains, auto)  # burn-in chains
+    # thinning chains: fork f of burned chain c is chain c F + f (keyed (seed, TAG_INIT_FORK, 0, c F + f);
+    # F = 1 keeps the single-chain keys), each filling R slots
+    K, R = init_plan(N_total, K1 * F, 0)
     lo, hi = offset, offset + shard
-    c0, c1 = lo // R, min(K, -(-hi // R))  # chains whose slot blocks meet [lo, hi)
+    c0, c1 = lo // R, min(K, -(-hi // R))  # thinning chains whose slot blocks meet [lo, hi)
+    p0, p1 = c0 // F, -(-c1 // F)  # their burned-in parents
     chains = ParticleSystem(design, c1 - c0, prior_at_b1.a, intercept, rank_offset=c0)
     Kl = c1 - c0
     counts = torch.zeros(Kl, dtype=torch.int64, device=system.device)  # per chain, read once at the end
     d = chains.design
     if config.init_burn > 0:  # the burn-in: one chain-slot block of init_burn sweeps (the chains' layout)
-        bb = torch.empty((Kl, system.ldb), dtype=torch.float32, device=system.device)
-        bl = torch.empty(Kl, dtype=torch.float64, device=system.device)
-        bp = torch.empty(Kl, dtype=torch.float64, device=system.device)
-        _lib.call("spa_mwg_chain_slots", ctypes.byref(d.struct), _p(chains.beta), chains.N, chains.ldb,
+        parents = chains if F == 1 else ParticleSystem(design, p1 - p0, prior_at_b1.a, intercept, rank_offset=p0)
+        pcounts = counts if F == 1 else torch.zeros(p1 - p0, dtype=torch.int64, device=system.device)
+        bb = torch.empty((parents.N, system.ldb), dtype=torch.float32, device=system.device)
+        bl = torch.empty(parents.N, dtype=torch.float64, device=system.device)
+        bp = torch.empty(parents.N, dtype=torch.float64, device=system.device)
+        _lib.call("spa_mwg_chain_slots", ctypes.byref(d.struct), _p(parents.beta), parents.N, parents.ldb,
                   float(prior_at_b1.a), float(prior_at_b1.c), float(config.step_sd), int(config.init_burn), 1,
-                  int(config.seed), TAG_INIT, 0, int(chains.i0), 0, _p(chains.ll), _p(chains.lp), _p(bb), _p(bl),
-                  _p(bp), _p(counts), 1, _stream())
+                  int(config.seed), TAG_INIT, 0, int(parents.i0), 0, _p(parents.ll), _p(parents.lp), _p(bb), _p(bl),
+                  _p(bp), _p(pcounts), 1, _stream())
         del bb, bl, bp
+        if F > 1:  # fork: thinning chain k starts from its parent's burned-in state
+            par = torch.arange(c0, c1, device=system.device) // F - p0
+            chains.beta.copy_(parents.beta.index_select(0, par))
+            counts.copy_(pcounts.index_select(0, par) * (par * F + p0 * F == torch.arange(c0, c1, device=system.device)))
+            del parents, pcounts
     _prepare_for_path(system, config)  # host work while the chains run
     stage_b = torch.empty((Kl, R, system.ldb), dtype=torch.float32, device=system.device)
     stage_l = torch.empty((Kl, R), dtype=torch.float64, device=system.device)
@@ -793,8 +823,8 @@ def init_particles(data, prior_at_b1: GtPrior, config: SmcConfig, intercept: boo
     # + (j+1)*init_thin sweeps; bit-identical to one chain-slot call per slot)
     _lib.call("spa_mwg_chain_slots", ctypes.byref(d.struct), _p(chains.beta), chains.N, chains.ldb,
               float(prior_at_b1.a), float(prior_at_b1.c), float(config.step_sd), int(config.init_thin), int(R),
-              int(config.seed), TAG_INIT, 0, int(chains.i0), int(config.init_burn), _p(chains.ll), _p(chains.lp),
-              _p(stage_b), _p(stage_l), _p(stage_p), _p(counts), 1, _stream())
+              int(config.seed), TAG_INIT if F == 1 else TAG_INIT_FORK, 0, int(chains.i0), int(config.init_burn),
+              _p(chains.ll), _p(chains.lp), _p(stage_b), _p(stage_l), _p(stage_p), _p(counts), 1, _stream())
     a, b = lo - c0 * R, hi - c0 * R  # this shard inside the staged slots [c0 R, c1 R)
     system.beta.copy_(stage_b.view(Kl * R, system.ldb)[a:b])
     system.ll.copy_(stage_l.view(-1)[a:b])
@@ -803,7 +833,10 @@ def init_particles(data, prior_at_b1: GtPrior, config: SmcConfig, intercept: boo
     # acceptance over the chains this rank owns (first slot in its shard), so
     # every chain counts once for any number of ranks
     own = torch.arange(c0, c1, device=system.device) * R >= lo
-    tally = torch.stack([counts[own].sum(), own.sum() * (config.init_burn + R * config.init_thin) * design.q])
+    # (a fork's burn-in sweeps are its parent's: counted with the parent's first fork only)
+    first = torch.arange(c0, c1, device=system.device) % F == 0
+    tally = torch.stack([counts[own].sum(),
+                         (own.sum() * R * config.init_thin + (own & first).sum() * config.init_burn) * design.q])
     if group is not None:
         tally = group.all_reduce_sum(tally)
     acc, total = (int(v) for v in tally.tolist())
