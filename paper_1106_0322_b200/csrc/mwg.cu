@@ -217,6 +217,7 @@ __global__ void __launch_bounds__(S == 8 ? 1024 : (S == 16 ? 640 : 512)) mwg_ker
   const Key2 key = stream_key(P.seed, (uint32_t)P.tag, (uint64_t)P.t, (uint64_t)(P.i0 + row));
 
   for (int j = tid; j < q; j += nthr) bsh[j] = brow[j];
+  if (tid < 64) fred[tid] = 0.0f;  // warp-sum scratch: slots >= nw stay zero
   __syncthreads();
 
   float sig[S];
@@ -299,9 +300,18 @@ __global__ void __launch_bounds__(S == 8 ? 1024 : (S == 16 ? 640 : 512)) mwg_ker
         float* buf = fred + (j & 1) * 32;
         if (lane == 0) buf[wid] = tot;
         __syncthreads();
-        tot = lane < nw ? buf[lane] : 0.0f;
+        const float4* b4 = reinterpret_cast<const float4*>(buf);
+        float s8[8];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        for (int k = 0; k < 8; ++k) {
+          if (4 * k < nw) {
+            const float4 v = b4[k];
+            s8[k] = (v.x + v.y) + (v.z + v.w);
+          } else {
+            s8[k] = 0.0f;
+          }
+        }
+        tot = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
       }
       const double dll = cs.dsy - 0.6931471805599453 * (double)tot;
       const double d = dll + cs.dlp;
