@@ -57,6 +57,9 @@ def test_sass_contains_tcgen05_and_tma():
     sass = subprocess.run([exe, "-sass", so], capture_output=True, text=True, check=True).stdout
     assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass
     assert "HMMA" not in sass.replace("UTCHMMA", "")
+    # the int8 likelihood kernel: CTA-pair integer MMAs and pair-scoped TMA loads
+    assert "UTCIMMA.2CTA" in sass and "UTMALDG.2D.2CTA" in sass
+    assert "IMMA" not in sass.replace("UTCIMMA", "")
 
 
 class TestConfig:

@@ -97,6 +97,42 @@ def test_loglik_many_particles_ragged_vs_oracle(gold_loglik):
     np.testing.assert_allclose(gpu_loglik(X, y, B), orc.loglik_rows(X, y, B), rtol=LL_RTOL)
 
 
+@pytest.mark.parametrize("N", [1, 129, 255, 256, 257, 300, 513])
+def test_loglik_int8_ragged_pair_tiles(gold_loglik, N):
+    """The int8 CTA-pair kernel covers 256 particles per pair tile: particle
+    counts below, at and across the pair boundary (the second CTA's rows
+    partially or wholly beyond N), against the float64 oracle."""
+    X, y = gold_loglik["c1_X"], gold_loglik["c1_y"]
+    B = np.random.default_rng(N).normal(0, 0.3, size=(N, X.shape[1]))
+    np.testing.assert_allclose(gpu_loglik(X, y, B), orc.loglik_rows(X, y, B), rtol=LL_RTOL)
+
+
+def test_loglik_int8_row_scales():
+    """Per-row fixed point: all-zero rows, a row dominated by one huge
+    coefficient, rows far outside fp16's range (finite and correct here, the
+    fp16 operand gave NaN from |alpha beta| >= 65504), tiny rows, and
+    non-finite rows (NaN log-likelihood)."""
+    from paper_1106_0322_b200.data import named_spec, simulate_dataset
+
+    data, _ = simulate_dataset(named_spec("c2"))
+    X, y = data.X, data.y
+    q = X.shape[1]
+    rng = np.random.default_rng(11)
+    B = rng.normal(0, 0.05, size=(8, q))
+    B[0] = 0.0                          # beta = 0: n log(1/2)
+    B[1, 7] = 6.0                       # one dominant coefficient
+    B[2] *= 1e5                         # |alpha beta| ~ 1e5: beyond fp16
+    B[3] *= 1e-9                        # tiny but nonzero
+    B[4, :] = 0.0
+    B[4, q - 1] = -3.0                  # only the last (tail) column
+    B[6, 3] = np.nan
+    B[7, 5] = np.inf
+    got = gpu_loglik(X, y, B)
+    ref = orc.loglik_rows(X, y, np.nan_to_num(B[:6], posinf=0.0))
+    np.testing.assert_allclose(got[:6], ref, rtol=LL_RTOL)
+    assert np.isnan(got[6]) and np.isnan(got[7])
+
+
 def test_loglik_known_answers():
     # beta = 0 -> n log(1/2) (test_model.py:131-136)
     rng = np.random.default_rng(0)
