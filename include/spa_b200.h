@@ -54,6 +54,9 @@ typedef struct spa_design {
                                [n][2*kp], Xs = X/alpha                        */
   int32_t kp;               /* K per plane, multiple of 64, >= q (<= 1024 coded) */
   int32_t terms;            /* general designs: 2 B terms; coded: 1 (unused) */
+  const uint32_t* codes;    /* coded: [q][2*n_words] genotype codes for the MwG
+                               kernel, 16 subjects per word, subject s of the
+                               word in bits 2s..2s+1 (0,1,2; 3 = padding)    */
 } spa_design;
 
 /* Prior description: a > 0 (generalised t, model.py:78-81) or a = +inf
@@ -221,6 +224,16 @@ int spa_mwg_chain_slots(const spa_design* d, float* beta, int64_t m, int32_t ldb
                         int64_t t, int64_t i0, int64_t sweep0, double* ll, double* lp, float* slot_beta,
                         double* slot_ll, double* slot_lp, unsigned long long* accepted, int32_t per_particle,
                         void* stream);
+
+/* Coordinates per blocked MwG round (1, 2, 4 or 8) for spa_mwg_chain_slots
+ * (init_rounds) and spa_mwg_move (move_rounds), coded designs: a round
+ * evaluates the next `rounds` coordinates' log-likelihood differences
+ * against the current subject cache in one block reduction and decides them
+ * in order up to the first acceptance.  The chain states are bit-identical
+ * for every value (the same sums, reduction order and decisions as one
+ * coordinate at a time, reference smc.py:177-199); it trades reductions and
+ * barriers for discarded work after an acceptance.  Defaults: 4 / 4. */
+int spa_mwg_set_rounds(int32_t init_rounds, int32_t move_rounds);
 
 /* ---- K8: population random-walk moves (north-star kernel) --------------
  * Weighted moments into an int64 fixed-point (2^-48) accumulator

@@ -71,8 +71,8 @@ struct CoordSlot {
   double dsy;     // delta * (X^T y)_j (formed with the slot: off the per-coordinate critical path)
   double dlp;     // prior difference
   double logu;    // log of the MH uniform
-  float newv;     // beta_j' (float32 state)
-  float m0, m1, m2;  // expm1(delta * x) for codes 0, 1, 2
+  float m0, m1, m2;  // expm1(delta * x) for codes 0, 1, 2 (16-byte aligned: one vector load)
+  float newv;        // beta_j' (float32 state)
 };
 
 // Genotype code from the two bit planes: (0,0)->0, (1,0)->1, (0,1)->2.  A
@@ -197,16 +197,79 @@ __device__ __forceinline__ void coord_accept(float (&sig)[S], uint32_t p1, uint3
   }
 }
 
-// Thread limits per layout: S = 8 up to 1024 threads, S = 16 up to 640 (the
+// Pair-table form of coord_log2_sum / coord_accept (coded designs): cw holds
+// this thread's 2-bit genotype codes, subjects 2k and 2k+1 in nibble k (code
+// 3 = padding); tbl[nibble] = (m of the first subject, m of the second).
+// The factors, products and logs are those of coord_log2_sum (same values,
+// same order), so the sums are bit-identical to the bit-plane form.
+template <int S>
+__device__ __forceinline__ float coord_log2_sum_tbl(const float (&sig)[S], const uint32_t (&cw)[S >= 16 ? S / 16 : 1],
+                                                    const float2* tbl) {
+  float part = 0.0f;
+#pragma unroll
+  for (int c8 = 0; c8 < S / 8; ++c8) {
+    float fac[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int pk = 4 * c8 + k;  // subject pair
+      const float2 mm = tbl[(cw[pk >> 3] >> (4 * (pk & 7))) & 15u];
+      fac[2 * k] = fmaf(mm.x, sig[2 * pk], 1.0f);
+      fac[2 * k + 1] = fmaf(mm.y, sig[2 * pk + 1], 1.0f);
+    }
+    const float prod = ((fac[0] * fac[1]) * (fac[2] * fac[3])) * ((fac[4] * fac[5]) * (fac[6] * fac[7]));
+    if (prod >= 1e-30f && prod <= 1e30f) {
+      part += fast_lg2(prod);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) part += fast_lg2(fmaxf(fac[k], 1e-37f));
+    }
+  }
+  return part;
+}
+
+template <int S>
+__device__ __forceinline__ void coord_accept_tbl(float (&sig)[S], const uint32_t (&cw)[S >= 16 ? S / 16 : 1],
+                                                 const float2* tbl) {
+#pragma unroll
+  for (int pk = 0; pk < S / 2; ++pk) {
+    const float2 mm = tbl[(cw[pk >> 3] >> (4 * (pk & 7))) & 15u];
+    sig[2 * pk] = __fdividef(sig[2 * pk] * (1.0f + mm.x), fmaf(mm.x, sig[2 * pk], 1.0f));
+    sig[2 * pk + 1] = __fdividef(sig[2 * pk + 1] * (1.0f + mm.y), fmaf(mm.y, sig[2 * pk + 1], 1.0f));
+  }
+}
+
+// Blocked coordinate rounds (coded designs).  A coordinate's sum
+// sum_i log(1 + m_i sigma_i) depends on the state only through sigma, which
+// changes only when a coordinate is accepted (~8-30% of proposals).  A round
+// therefore evaluates the sums of the next D coordinates against the current
+// sigma, reduces all D in ONE block reduction (one barrier instead of D),
+// then decides them in order: the decisions up to and including the first
+// acceptance are exactly the sequential ones (same sigma, same per-thread
+// partials, same reduction tree), the sums after it are discarded and the
+// next round starts at the coordinate after it.  States are bit-identical to
+// D = 1.  The genotype codes and pair tables of the coordinates in flight
+// are staged in a shared-memory ring of 4D coordinates, refilled one round ahead
+// (coordinates [j + D, j + 2D) are loaded while round j computes, stored after
+// its reduction; 4D slots keep a slow warp's reads of round r clear of the
+// stores of round r + 1).
+template <int D>
+struct MwgRing {
+  static constexpr int kSlots = 4 * D;
+};
+
+// Thread limits per layout: S = 8 up to 640 threads, S = 16 up to 640 (the
 // initialisation layout up to n = 10240: <= 102 registers), S = 32 512
-template <int S, bool CODED>
-__global__ void __launch_bounds__(S == 8 ? 1024 : (S == 16 ? 640 : 512)) mwg_kernel(MwgParams P) {
+template <int S, bool CODED, int D = 1>
+__global__ void __launch_bounds__(S == 8 ? 640 : (S == 16 ? 640 : 512)) mwg_kernel(MwgParams P) {
+  static_assert(D == 1 || CODED, "blocked rounds are for coded designs");
   extern __shared__ __align__(16) uint8_t sm[];
   const int q = P.d.q;
   CoordSlot* slot = reinterpret_cast<CoordSlot*>(sm);
   float* bsh = reinterpret_cast<float*>(slot + q);
   double* red = reinterpret_cast<double*>(bsh + ((q + 1) & ~1));  // [2][32]
-  float* fred = reinterpret_cast<float*>(red + 64);               // [2][32]
+  float* fred = reinterpret_cast<float*>(red + 64);               // [2][D][32]
+  uint2* ring = reinterpret_cast<uint2*>(fred + 64 * D);          // coded: [4D][n_words] code words
+  float2* tring = reinterpret_cast<float2*>(ring + (size_t)MwgRing<D>::kSlots * P.d.n_words);  // coded: [4D][16]
 
   const int64_t row = blockIdx.x;
   if (row >= P.m) return;
@@ -217,7 +280,7 @@ __global__ void __launch_bounds__(S == 8 ? 1024 : (S == 16 ? 640 : 512)) mwg_ker
   const Key2 key = stream_key(P.seed, (uint32_t)P.tag, (uint64_t)P.t, (uint64_t)(P.i0 + row));
 
   for (int j = tid; j < q; j += nthr) bsh[j] = brow[j];
-  if (tid < 64) fred[tid] = 0.0f;  // warp-sum scratch: slots >= nw stay zero
+  for (int k = tid; k < 64 * D; k += nthr) fred[k] = 0.0f;  // warp-sum scratch: slots >= nw stay zero
   __syncthreads();
 
   float sig[S];
@@ -270,58 +333,195 @@ __global__ void __launch_bounds__(S == 8 ? 1024 : (S == 16 ? 640 : 512)) mwg_ker
     }
     __syncthreads();
 
-    // genotype bits are prefetched two coordinates ahead (the L2 load latency
-    // was the largest stall); the per-subject factors m are re-selected from
-    // the bits on acceptance instead of being kept (32 registers fewer, so
-    // more chains are resident per SM)
-    uint32_t nb1 = 0, nb2 = 0, nn1 = 0, nn2 = 0;
-    if (CODED) {
-      load_bits<S>(P.d, 0, tid, nb1, nb2);
-      if (q > 1) load_bits<S>(P.d, 1, tid, nn1, nn2);
-    }
-    for (int j = 0; j < q; ++j) {
-      const CoordSlot cs = slot[j];
-      const uint32_t p1 = nb1, p2 = nb2;
+    if constexpr (!CODED) {
+      // genotype bits are prefetched two coordinates ahead (the L2 load latency
+      // was the largest stall); the per-subject factors m are re-selected from
+      // the bits on acceptance instead of being kept (32 registers fewer, so
+      // more chains are resident per SM)
+      uint32_t nb1 = 0, nb2 = 0, nn1 = 0, nn2 = 0;
       if (CODED) {
-        nb1 = nn1;
-        nb2 = nn2;
-        if (j + 2 < q) load_bits<S>(P.d, j + 2, tid, nn1, nn2);
+        load_bits<S>(P.d, 0, tid, nb1, nb2);
+        if (q > 1) load_bits<S>(P.d, 1, tid, nn1, nn2);
       }
-      const float* xc = P.d.xcols + (size_t)j * P.d.n_words * 32 + sub0;
-      const float df = (float)cs.delta;
-      const float part = coord_log2_sum<S, CODED>(sig, p1, p2, cs, xc, df);
-      // block sum (double-buffered scratch: one barrier per coordinate)
-      float tot = part;
+      for (int j = 0; j < q; ++j) {
+        const CoordSlot cs = slot[j];
+        const uint32_t p1 = nb1, p2 = nb2;
+        if (CODED) {
+          nb1 = nn1;
+          nb2 = nn2;
+          if (j + 2 < q) load_bits<S>(P.d, j + 2, tid, nn1, nn2);
+        }
+        const float* xc = P.d.xcols + (size_t)j * P.d.n_words * 32 + sub0;
+        const float df = (float)cs.delta;
+        const float part = coord_log2_sum<S, CODED>(sig, p1, p2, cs, xc, df);
+        // block sum (double-buffered scratch: one barrier per coordinate)
+        float tot = part;
+  #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if (nw > 1) {
+          // second level: every warp reduces the nw warp sums with shuffles
+          // (one smem load per lane instead of nw serial loads and adds)
+          float* buf = fred + (j & 1) * 32;
+          if (lane == 0) buf[wid] = tot;
+          __syncthreads();
+          const float4* b4 = reinterpret_cast<const float4*>(buf);
+          float s8[8];
+  #pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            if (4 * k < nw) {
+              const float4 v = b4[k];
+              s8[k] = (v.x + v.y) + (v.z + v.w);
+            } else {
+              s8[k] = 0.0f;
+            }
+          }
+          tot = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
+        }
+        const double dll = cs.dsy - 0.6931471805599453 * (double)tot;
+        const double d = dll + cs.dlp;
+        const bool ok = (d >= 0.0) || (cs.logu < d);
+        if (ok) {
+          coord_accept<S, CODED>(sig, p1, p2, cs, xc, df);
+          ll += dll;
+          lp += cs.dlp;
+          ++acc;
+          if (tid == 0) bsh[j] = cs.newv;
+        }
+      }
+    } else {
+      // coded designs: blocked rounds over a shared-memory ring (MwgRing):
+      // round r evaluates coordinates j .. j+D-1 against the current sigma,
+      // one block reduction for all D, decisions in order up to the first
+      // acceptance.  Subject factors come from the coordinate's pair table
+      // (m of two subjects per 64-bit shared load, indexed by their 4-bit
+      // code nibble) instead of bit tests and selects.
+      constexpr int RS = MwgRing<D>::kSlots;
+      constexpr int kMaxL = (D * S + 31) / 32 + 1;  // staged uint2 per thread (host: D n_words <= kMaxL nthr)
+      constexpr int NCW = S >= 16 ? S / 16 : 1;     // code words per thread
+      const int nwd = P.d.n_words;                  // uint2 (= 32 subjects) per coordinate
+      const uint2* codes = reinterpret_cast<const uint2*>(P.d.codes);
+      const uint32_t* cr32 = reinterpret_cast<const uint32_t*>(ring);
+      const int cw0 = S >= 16 ? tid * NCW : tid >> 1;  // first code word of this thread
+      const int csh = S == 8 ? (tid & 1) * 16 : 0;
+      int coff[kMaxL], woff[kMaxL];  // round-invariant (coordinate, uint2) of this thread's staged loads
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-      if (nw > 1) {
-        // second level: every warp reduces the nw warp sums with shuffles
-        // (one smem load per lane instead of nw serial loads and adds)
-        float* buf = fred + (j & 1) * 32;
-        if (lane == 0) buf[wid] = tot;
-        __syncthreads();
-        const float4* b4 = reinterpret_cast<const float4*>(buf);
-        float s8[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          if (4 * k < nw) {
-            const float4 v = b4[k];
-            s8[k] = (v.x + v.y) + (v.z + v.w);
-          } else {
-            s8[k] = 0.0f;
+      for (int k = 0; k < kMaxL; ++k) {
+        const int e = tid + k * nthr;
+        coff[k] = e < D * nwd ? e / nwd : q;  // q: never loaded
+        woff[k] = e - (e / nwd) * nwd;
+      }
+      // the pair tables of coordinates [c0, c1) from their slots: entry e =
+      // (m[e & 3], m[e >> 2]), m = {m0, m1, m2, 0} (code 3 = padding, sigma 0)
+      auto build_tables = [&](int c0, int c1) {
+        for (int e = tid; e < 16 * (c1 - c0); e += nthr) {
+          const int c = c0 + (e >> 4);
+          if (c < q) {
+            const float4 mv = *reinterpret_cast<const float4*>(&slot[c].m0);  // m0, m1, m2, (newv)
+            const int a = e & 3, b = (e >> 2) & 3;
+            const float ma = a == 3 ? 0.0f : a == 2 ? mv.z : a == 1 ? mv.y : mv.x;
+            const float mb = b == 3 ? 0.0f : b == 2 ? mv.z : b == 1 ? mv.y : mv.x;
+            tring[(c & (RS - 1)) * 16 + (e & 15)] = make_float2(ma, mb);
           }
         }
-        tot = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
+      };
+      for (int e = tid; e < 2 * D * nwd; e += nthr) {  // coordinates [0, 2D)
+        const int c = e / nwd;
+        if (c < q) ring[(c & (RS - 1)) * nwd + (e - c * nwd)] = codes[(size_t)c * nwd + (e - c * nwd)];
       }
-      const double dll = cs.dsy - 0.6931471805599453 * (double)tot;
-      const double d = dll + cs.dlp;
-      const bool ok = (d >= 0.0) || (cs.logu < d);
-      if (ok) {
-        coord_accept<S, CODED>(sig, p1, p2, cs, xc, df);
-        ll += dll;
-        lp += cs.dlp;
-        ++acc;
-        if (tid == 0) bsh[j] = cs.newv;
+      build_tables(0, 2 * D);
+      __syncthreads();
+      int rnd = 0;
+      for (int j = 0; j < q; ++rnd) {
+        // coordinates [j + D, j + 2D): loaded now, stored after the reduction
+        uint2 lv[kMaxL];
+#pragma unroll
+        for (int k = 0; k < kMaxL; ++k) {
+          const int c = j + D + coff[k];
+          if (c < q) lv[k] = __ldg(&codes[(size_t)c * nwd + woff[k]]);
+        }
+        float part[D];
+#pragma unroll
+        for (int dd = 0; dd < D; ++dd) {
+          part[dd] = 0.0f;
+          if (j + dd < q) {
+            const int rs = (j + dd) & (RS - 1);
+            uint32_t cw[NCW];
+#pragma unroll
+            for (int w = 0; w < NCW; ++w) cw[w] = cr32[rs * 2 * nwd + cw0 + w] >> csh;
+            part[dd] = coord_log2_sum_tbl<S>(sig, cw, tring + rs * 16);
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int dd = 0; dd < D; ++dd) part[dd] += __shfl_xor_sync(0xffffffffu, part[dd], o);
+        float* buf = fred + (rnd & 1) * 32 * D;
+        if (nw > 1 && lane == 0)
+#pragma unroll
+          for (int dd = 0; dd < D; ++dd) buf[dd * 32 + wid] = part[dd];
+#pragma unroll
+        for (int k = 0; k < kMaxL; ++k) {
+          const int c = j + D + coff[k];
+          if (c < q) ring[(c & (RS - 1)) * nwd + woff[k]] = lv[k];
+        }
+        build_tables(j + D, j + 2 * D);
+        __syncthreads();
+        if (nw > 1) {
+          if (D >= 4 && nw <= 16) {
+            // D >= 4: the same tree as an xor butterfly over lanes (level k
+            // of the tree = shuffle distance 2^k; two coordinates per pass,
+            // lanes 16..31 take the second, whose top level adds only zeros)
+#pragma unroll
+            for (int p2 = 0; p2 < (D + 1) / 2; ++p2) {
+              const int dd = 2 * p2 + (lane >> 4);
+              float v = dd < D ? buf[dd * 32 + (lane & 15)] : 0.0f;
+#pragma unroll
+              for (int o = 1; o < 16; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+              part[2 * p2] = __shfl_sync(0xffffffffu, v, 0);
+              if (2 * p2 + 1 < D) part[2 * p2 + 1] = __shfl_sync(0xffffffffu, v, 16);
+            }
+          } else {
+            // the perfect binary tree over the 32 warp slots (zero beyond nw)
+#pragma unroll
+            for (int dd = 0; dd < D; ++dd) {
+              const float4* b4 = reinterpret_cast<const float4*>(buf + dd * 32);
+              float s8[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                if (4 * k < nw) {
+                  const float4 v = b4[k];
+                  s8[k] = (v.x + v.y) + (v.z + v.w);
+                } else {
+                  s8[k] = 0.0f;
+                }
+              }
+              part[dd] = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
+            }
+          }
+        }
+        // decisions in order; the first acceptance ends the round
+        int adv = min(D, q - j);
+#pragma unroll
+        for (int dd = 0; dd < D; ++dd) {
+          if (dd < adv) {
+            const CoordSlot cs = slot[j + dd];
+            const double dll = cs.dsy - 0.6931471805599453 * (double)part[dd];
+            const double d = dll + cs.dlp;
+            if ((d >= 0.0) || (cs.logu < d)) {
+              const int rs = (j + dd) & (RS - 1);
+              uint32_t cw[NCW];
+#pragma unroll
+              for (int w = 0; w < NCW; ++w) cw[w] = cr32[rs * 2 * nwd + cw0 + w] >> csh;
+              coord_accept_tbl<S>(sig, cw, tring + rs * 16);
+              ll += dll;
+              lp += cs.dlp;
+              ++acc;
+              if (tid == 0) bsh[j + dd] = cs.newv;
+              adv = dd + 1;
+            }
+          }
+        }
+        j += adv;
       }
     }
     __syncthreads();
@@ -356,16 +556,41 @@ __global__ void __launch_bounds__(S == 8 ? 1024 : (S == 16 ? 640 : 512)) mwg_ker
   }
 }
 
+template <int S, int D>
+static const void* mwg_fn_sd(bool coded) {
+  return coded ? (const void*)mwg_kernel<S, true, D> : (const void*)mwg_kernel<S, false, 1>;
+}
+
 template <int S>
-static const void* mwg_fn_s(bool coded) {
-  return coded ? (const void*)mwg_kernel<S, true> : (const void*)mwg_kernel<S, false>;
+static const void* mwg_fn_s(bool coded, int D) {
+  return D == 8 ? mwg_fn_sd<S, 8>(coded)
+                : D == 4 ? mwg_fn_sd<S, 4>(coded) : D == 2 ? mwg_fn_sd<S, 2>(coded) : mwg_fn_sd<S, 1>(coded);
 }
 
-static const void* mwg_fn(int S, bool coded) {
-  return S == 8 ? mwg_fn_s<8>(coded) : S == 16 ? mwg_fn_s<16>(coded) : mwg_fn_s<32>(coded);
+static const void* mwg_fn(int S, bool coded, int D = 1) {
+  return S == 8 ? mwg_fn_s<8>(coded, D) : S == 16 ? mwg_fn_s<16>(coded, D) : mwg_fn_s<32>(coded, D);
 }
 
-static int max_threads(int S) { return S == 8 ? 1024 : (S == 16 ? 640 : 512); }
+// Coordinates per blocked round (mwg_kernel's D) for the initialisation
+// chains and for the lambda-step move; spa_mwg_set_rounds changes them
+// (A/B and the bit-identity tests: every D gives the same states).
+static int g_rounds_init = 4, g_rounds_move = 4;
+
+static int rounds_for(const spa_design* d, int S, int nthr, bool init_layout) {
+  int D = init_layout ? g_rounds_init : g_rounds_move;
+  if (!d->coded) return 1;
+  // staged words per thread: D n_words <= kMaxL nthr with kMaxL = (D S + 31) / 32 + 1
+  while (D > 1 && D * d->n_words > ((D * S + 31) / 32 + 1) * nthr) D >>= 1;
+  return D;
+}
+
+static size_t mwg_smem(const spa_design* d, int D) {
+  return (size_t)d->q * sizeof(CoordSlot) + (size_t)((d->q + 1) & ~1) * sizeof(float) + 64 * sizeof(double) +
+         (size_t)64 * D * sizeof(float) +
+         (d->coded ? (size_t)MwgRing<1>::kSlots * D * (d->n_words * sizeof(uint2) + 16 * sizeof(float2)) : 0);
+}
+
+static int max_threads(int S) { return S == 8 ? 640 : (S == 16 ? 640 : 512); }
 
 // Layout of the initialisation chains (spa_mwg_chain_slots and the chain
 // count of spa_mwg_resident_chains): one resident wave of latency-bound
@@ -373,6 +598,13 @@ static int max_threads(int S) { return S == 8 ? 1024 : (S == 16 ? 640 : 512); }
 // with 2000 burn sweeps 1.58 -> 1.32 s, C2 0.51 -> 0.34 s against the
 // throughput layout of pick_s)
 static int pick_s_init(int n) {
+  // developer A/B knob: SPA_MWG_S_INIT=8|16|32
+  static const int forced = [] {
+    const char* e = getenv("SPA_MWG_S_INIT");
+    return e ? atoi(e) : 0;
+  }();
+  if ((forced == 8 || forced == 16 || forced == 32) && (n + forced - 1) / forced <= max_threads(forced))
+    return forced;
   if (n <= 256) return 8;
   if ((n + 15) / 16 <= 640) return 16;
   if (n <= 16384) return 32;
@@ -397,6 +629,17 @@ static int pick_s(int n) {
 
 using namespace spa;
 
+// Coordinates per blocked MwG round for the initialisation chains and the
+// lambda-step move (1, 2 or 4; coded designs; states are identical for any
+// value -- a tuning knob, used by the A/B tools and the bit-identity tests).
+extern "C" int spa_mwg_set_rounds(int32_t init_rounds, int32_t move_rounds) {
+  auto ok = [](int v) { return v == 1 || v == 2 || v == 4 || v == 8; };
+  SPA_REQUIRE(ok(init_rounds) && ok(move_rounds), kBadArgument, "spa_mwg_set_rounds: rounds must be 1, 2, 4 or 8");
+  g_rounds_init = init_rounds;
+  g_rounds_move = move_rounds;
+  return 0;
+}
+
 // internal (called by spa_prepare): load the MwG kernels
 extern "C" int spa_mwg_prepare_kernels(void) {
   const void* fns[] = {(const void*)mwg_kernel<8, true>,   (const void*)mwg_kernel<16, true>,
@@ -417,10 +660,10 @@ extern "C" int spa_mwg_resident_chains(const spa_design* d, int64_t* chains) {
   const int S = pick_s_init(d->n);
   SPA_REQUIRE(S > 0, kNotSupported, "spa_mwg_resident_chains: n > 16384 not supported");
   const int nthr = std::max(32, ((d->n + S - 1) / S + 31) / 32 * 32);
-  const size_t smem = (size_t)d->q * sizeof(CoordSlot) + (size_t)((d->q + 1) & ~1) * sizeof(float) +
-                      64 * sizeof(double) + 64 * sizeof(float);
+  const int D = rounds_for(d, S, nthr, true);
+  const size_t smem = mwg_smem(d, D);
   int per_sm = 0, dev = 0, nsm = 0;
-  const void* fn = mwg_fn(S, d->coded != 0);
+  const void* fn = mwg_fn(S, d->coded != 0, D);
   SPA_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   SPA_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nthr, smem));
   SPA_CHECK_CUDA(cudaGetDevice(&dev));
@@ -438,7 +681,7 @@ static int mwg_launch(const spa_design* d, float* beta, int64_t m, int32_t ldb, 
   SPA_REQUIRE(d->q >= 1 && d->q <= 2048, kNotSupported, "spa_mwg_move: q must lie in [1, 2048]");
   const int S = init_layout ? pick_s_init(d->n) : pick_s(d->n);
   SPA_REQUIRE(S > 0, kNotSupported, "spa_mwg_move: n > 16384 not supported");
-  SPA_REQUIRE(d->coded ? d->planes != nullptr : d->xcols != nullptr, kBadArgument, "spa_mwg_move: design arrays");
+  SPA_REQUIRE(d->coded ? d->codes != nullptr : d->xcols != nullptr, kBadArgument, "spa_mwg_move: design arrays");
   if (m == 0) return 0;
   MwgParams P;
   P.d = *d;
@@ -467,11 +710,11 @@ static int mwg_launch(const spa_design* d, float* beta, int64_t m, int32_t ldb, 
   const int nthr = std::max(32, (nthr_raw + 31) / 32 * 32);
   SPA_REQUIRE(nthr <= 1024, kNotSupported, "spa_mwg_move: too many subjects per particle");
   SPA_REQUIRE(nthr * S <= d->n_words * 32, kBadArgument, "spa_mwg_move: n_words does not cover the thread layout");
-  const size_t smem = (size_t)d->q * sizeof(CoordSlot) + (size_t)((d->q + 1) & ~1) * sizeof(float) +
-                      64 * sizeof(double) + 64 * sizeof(float);
+  const int D = rounds_for(d, S, nthr, init_layout);
+  const size_t smem = mwg_smem(d, D);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   SPA_REQUIRE(nthr <= max_threads(S), kNotSupported, "spa_mwg_move: too many threads for this layout");
-  const void* fn = mwg_fn(S, d->coded != 0);
+  const void* fn = mwg_fn(S, d->coded != 0, D);
   SPA_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   void* args[] = {&P};
   SPA_CHECK_CUDA(cudaLaunchKernel(fn, dim3((unsigned)m), dim3(nthr), args, smem, st));

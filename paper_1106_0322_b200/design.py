@@ -137,6 +137,11 @@ class DeviceDesign:
             p1 = np.packbits(b1, axis=1, bitorder="little").view("<u4")
             p2 = np.packbits(b2, axis=1, bitorder="little").view("<u4")
             planes = np.stack([p1, p2], axis=-1).astype(np.uint32)  # [q][n_words][2]
+            # MwG codes: 16 subjects per word, subject s in bits 2s..2s+1 (3 = padding)
+            cc = np.full((q, npad), 3, np.uint32)
+            cc[:, :n] = codes
+            words = (cc.reshape(q, npad // 16, 16) << (2 * np.arange(16, dtype=np.uint32))).sum(axis=2, dtype=np.uint64)
+            t["codes"] = torch.from_numpy(words.astype(np.uint32).view(np.int32)).to(dev)
             # int8 K1 operand (csrc/tc_k1_i8.cuh): two byte planes [G | 64 G]
             kp = _round_up(q, K_ALIGN)
             G = np.zeros((n, 2 * kp), np.uint8)
@@ -182,4 +187,5 @@ class DeviceDesign:
         s.penalized = t["penalized"].data_ptr()
         s.gemm_b = t["gemm_b"].data_ptr()
         s.kp, s.terms = kp, terms
+        s.codes = t["codes"].data_ptr() if coded else None
         return cls(n, q, coded, kp, pen.astype(bool), t, s)
