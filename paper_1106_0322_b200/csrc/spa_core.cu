@@ -9,6 +9,7 @@
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cmath>
 #include <mutex>
 #include <vector>
@@ -2170,16 +2171,30 @@ size_t spa_k1_operand_bytes(const spa_design* d, int64_t m) {
 size_t spa_loglik_workspace_bytes(int64_t m, int32_t n) {
   int mt, nt, tpu, units, units8r, units8s;
   loglik_split(m, n, mt, nt, tpu, units);  // fp16 path (general designs)
-  // int8 paths (coded designs): kI8EpiGroups partial rows per unit
+  // int8 paths (coded designs): kI8EpiGroups partial rows per segment slot
   loglik_split(m, n, mt, nt, tpu, units8r, kI8BN, 0.3, 256, 74);
   loglik_split(m, n, mt, nt, tpu, units8s, kI8BN, 0.1, 256, 74);
-  return (size_t)std::max(units, kI8EpiGroups * std::max(units8r, units8s)) * (size_t)m * sizeof(double);
+  return (size_t)std::max({units, kI8EpiGroups * k1_i8_max_slots(m, n), kI8EpiGroups * units8r,
+                           kI8EpiGroups * units8s}) * (size_t)m * sizeof(double);
 }
 
 // K1 for coded designs on the int8 tensor cores (tc_k1_i8.cuh): CTA-pair
-// kernels -- resident particle tiles for kp <= 512, streamed above.  Work
-// items are (256-particle tile, group of subject tiles) over 74 pairs.
+// kernels -- resident particle tiles for kp <= 512, streamed above.  The
+// (particle tile, subject tile) units are cut into equal contiguous ranges,
+// one per pair (K1Seg).
 static bool k1_i8_resident(int kp) { return kp <= kI8MaxKb * kI8BK && k1_i8_pair_stages(kp) >= 2; }
+
+// Per-row partial sums of the segments covering the row's particle tile
+// (k1_slots_of), summed in slot order, then ylin - sum.
+__global__ void reduce_k1_slots_kernel(const double* __restrict__ partial, int64_t m, int n_tiles, int U,
+                                       int nclus, const double* __restrict__ ylin, double* __restrict__ out) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const int units = kI8EpiGroups * k1_slots_of((int)(k >> 8), n_tiles, U, nclus);
+  double s = 0.0;
+  for (int u = 0; u < units; ++u) s += partial[(size_t)u * m + k];
+  out[k] = ylin ? ylin[k] - s : s;
+}
 
 static int loglik_i8(const spa_design* d, const void* A, int64_t m, const double* ylin, double* out, void* ws,
                      cudaStream_t st) {
@@ -2190,8 +2205,8 @@ static int loglik_i8(const spa_design* d, const void* A, int64_t m, const double
   rc = make_tmap_u8(&tb, d->gemm_b, 2ull * d->kp, (uint64_t)d->n, kI8PairB);
   if (rc) return rc;
   K1I8Args args;
-  // a resident pair reloads its particle tiles per item: weight items more
-  loglik_split(m, d->n, args.m_tiles, args.n_tiles, args.tpu, args.units, kI8BN, res ? 0.3 : 0.1, 256, 74);
+  args.m_tiles = (int)((m + 255) / 256);
+  args.n_tiles = (d->n + kI8BN - 1) / kI8BN;
   args.m = (int)m;
   args.n = d->n;
   args.kp = d->kp;
@@ -2204,8 +2219,23 @@ static int loglik_i8(const spa_design* d, const void* A, int64_t m, const double
     SPA_CHECK_CUDA(cudaGetDevice(&dev));
     SPA_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
+  // contiguous unit ranges for the resident kernel (its operand reloads then
+  // fall at different times per pair: C3 289 -> 283 us); the streamed kernel
+  // (kp > 512) re-reads each particle tile's operand per subject tile, so it
+  // keeps round-robin items, whose concurrently live particle tiles stay in
+  // L2 (contiguous ranges: C5 1.49 -> 1.72 ms).  SPA_K1_SCHED=0|1|2 overrides
+  // (developer A/B knob, K1Seg)
+  static const int forced = [] {
+    const char* e = getenv("SPA_K1_SCHED");
+    return e ? atoi(e) : -1;
+  }();
+  const int sched = (forced >= 0 && forced <= 2) ? forced : (res ? 0 : 1);
+  args.sched = sched;
+  loglik_split(m, d->n, args.m_tiles, args.n_tiles, args.tpu, args.units, kI8BN, res ? 0.3 : 0.1, 256, 74);
+  const int U = args.m_tiles * (sched == 0 ? args.n_tiles : args.units);  // < 2^31: m < 2^31, n_tiles <= 128
+  const int nclus = std::min(U, std::min(kI8MaxPairs, sms / 2));
   {
-    const int grid = 2 * std::min(args.m_tiles * args.units, sms / 2);
+    const int grid = 2 * nclus;
     if (res) {
       const int smem = k1_i8_pair_smem(d->kp);
       static int attr = 0;  // largest size set so far
@@ -2226,8 +2256,12 @@ static int loglik_i8(const spa_design* d, const void* A, int64_t m, const double
     }
   }
   SPA_CHECK_LAUNCH();
-  reduce_units_kernel<<<cdiv(m, 256), 256, 0, st>>>(reinterpret_cast<double*>(ws), kI8EpiGroups * args.units, m,
-                                                    ylin, out);
+  if (sched == 0)
+    reduce_k1_slots_kernel<<<cdiv(m, 256), 256, 0, st>>>(reinterpret_cast<double*>(ws), m, args.n_tiles, U, nclus,
+                                                         ylin, out);
+  else
+    reduce_units_kernel<<<cdiv(m, 256), 256, 0, st>>>(reinterpret_cast<double*>(ws), kI8EpiGroups * args.units, m,
+                                                      ylin, out);
   SPA_CHECK_LAUNCH();
   return 0;
 }

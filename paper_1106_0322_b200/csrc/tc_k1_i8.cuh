@@ -121,11 +121,92 @@ struct K1I8Args {
   int kp;        // K (bytes per plane), multiple of 64
   int m_tiles;   // ceil(m / 256): particle tiles of a CTA pair
   int n_tiles;   // ceil(n / 128)
-  int tpu;       // subject tiles per work item
-  int units;     // work items per particle tile
   int stages;    // stage ring depth
+  int sched;     // 0: contiguous unit ranges; 1: items (tpu tiles) round-robin; 2: items in contiguous blocks
+  int tpu;       // sched 1/2: subject tiles per item
+  int units;     // sched 1/2: items per particle tile
   const float2* rowc;  // [m] {s_k, o_k}
-  double* partial;     // [kI8EpiGroups * units][m] per-group, per-unit softplus sums
+  double* partial;     // [kI8EpiGroups * slots][m] per-group, per-segment softplus sums
+};
+
+// Work schedule: the m_tiles x n_tiles (particle tile, subject tile) units in
+// row-major order are cut into nclus contiguous ranges of equal length (+-1:
+// the first U % nclus ranges are one longer), one per CTA pair.  A pair walks
+// its range as segments -- maximal runs of one particle tile -- keeping the
+// tile's operand resident over a segment, so every pair does the same number
+// of tile products (no rounding to whole items) and the pairs reach their
+// segment boundaries (operand reloads) at different times instead of all at
+// once.  Particle tile mt is covered by pairs k1_pair_of(mt n_tiles) ..
+// k1_pair_of((mt + 1) n_tiles - 1); pair c writes its segment's partial sums
+// to slot c - k1_pair_of(mt n_tiles).  32-bit arithmetic throughout: the MMA
+// issuer's loop must stay in uniform registers (a 64-bit division is a
+// subroutine call whose results are not uniform, and the descriptor math then
+// moves to vector registers, ~10 instructions per MMA).
+__host__ __device__ __forceinline__ int k1_range_start(int c, int U, int nclus) {
+  const int base = U / nclus, rem = U % nclus;
+  return c * base + min(c, rem);
+}
+__host__ __device__ __forceinline__ int k1_pair_of(int u, int U, int nclus) {  // pair owning unit u
+  const int base = U / nclus, rem = U % nclus;
+  return u < rem * (base + 1) ? u / (base + 1) : rem + (u - rem * (base + 1)) / base;
+}
+__host__ __device__ __forceinline__ int k1_slots_of(int mt, int n_tiles, int U, int nclus) {
+  const int u0 = mt * n_tiles;
+  return k1_pair_of(u0 + n_tiles - 1, U, nclus) - k1_pair_of(u0, U, nclus) + 1;
+}
+// CTA pairs of the K1 launch (148 SMs on B200); the workspace bound below
+// holds for any pair count up to this
+constexpr int kI8MaxPairs = 74;
+// most segment slots of any particle tile for m particles and n subjects
+inline int k1_i8_max_slots(int64_t m, int n) {
+  const int64_t m_tiles = (m + 255) / 256, n_tiles = (n + kI8BN - 1) / kI8BN, U = m_tiles * n_tiles;
+  const int64_t L = std::max<int64_t>(1, U / std::min<int64_t>(U, kI8MaxPairs));  // shortest range
+  return (int)((n_tiles + L - 1) / L + 1);
+}
+// the segments of pair cid: (particle tile, subject tiles [nt0, nt1), slot)
+struct K1Seg {
+  int u, uend, U;
+  int n_tiles, nclus, cid, sched, tpu, units;
+  __device__ __forceinline__ K1Seg(const K1I8Args& a, int cid_, int nclus_)
+      : n_tiles(a.n_tiles), nclus(nclus_), cid(cid_), sched(a.sched), tpu(a.tpu), units(a.units) {
+    if (sched == 0) {
+      U = a.m_tiles * n_tiles;
+      u = k1_range_start(cid, U, nclus);
+      uend = k1_range_start(cid + 1, U, nclus);
+    } else {
+      U = a.m_tiles * units;  // items
+      u = sched == 1 ? cid : k1_range_start(cid, U, nclus);
+      uend = sched == 1 ? U : k1_range_start(cid + 1, U, nclus);
+    }
+  }
+  // odd pairs walk their range backwards, so the two pairs sharing a
+  // particle tile at a range boundary work on it at the same time (both at
+  // the start or both at the end of their walks: one DRAM read of its operand)
+  __device__ __forceinline__ bool next(int& mt, int& nt0, int& nt1, int& slot) {
+    if (u >= uend) return false;
+    if (sched != 0) {
+      mt = u / units;
+      slot = u - mt * units;
+      nt0 = slot * tpu;
+      nt1 = min(n_tiles, nt0 + tpu);
+      u += sched == 1 ? nclus : 1;
+      return true;
+    }
+    if (cid & 1) {
+      mt = (uend - 1) / n_tiles;
+      const int lo = max(u, mt * n_tiles);
+      nt0 = lo - mt * n_tiles;
+      nt1 = uend - mt * n_tiles;
+      uend = lo;
+    } else {
+      mt = u / n_tiles;
+      nt0 = u - mt * n_tiles;
+      nt1 = min(n_tiles, nt0 + (uend - u));
+      u += nt1 - nt0;
+    }
+    slot = cid - k1_pair_of(mt * n_tiles, U, nclus);
+    return true;
+  }
 };
 
 // ---------------------------------------------------------------------------
@@ -215,8 +296,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int cid = blockIdx.x >> 1, nclus = gridDim.x >> 1;
-  const int units = args.units;
-  const int items = args.m_tiles * units;  // m_tiles counts 256-row pair tiles here
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
@@ -251,9 +330,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
       prefetch_tmap(&tmb);
       int s = 0;
       uint32_t ph = 0, ic = 0;
-      for (int w = cid; w < items; w += nclus, ++ic) {
-        const int mt = w / units, unit = w % units;
-        const int nt0 = unit * args.tpu, nt1 = min(args.n_tiles, nt0 + args.tpu);
+      K1Seg seg(args, cid, nclus);
+      for (int mt, nt0, nt1, slot; seg.next(mt, nt0, nt1, slot); ++ic) {
         const int arow = mt * 256 + (int)rank * 128;
         for (int nt = nt0; nt < nt1; ++nt) {
           for (int kb = 0; kb < kblocks; ++kb) {
@@ -297,9 +375,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
       int s = 0;
       uint32_t ph = 0, ic = 0;
       int it = 0;
-      for (int w = cid; w < items; w += nclus, ++ic) {
-        const int unit = w % units;
-        const int nt0 = unit * args.tpu, nt1 = min(args.n_tiles, nt0 + args.tpu);
+      K1Seg seg(args, cid, nclus);
+      for (int mt, nt0, nt1, slot; seg.next(mt, nt0, nt1, slot); ++ic) {
         for (int nt = nt0; nt < nt1; ++nt, ++it) {
           const int buf = it & 1;
           const uint32_t bph = (it >> 1) & 1;
@@ -347,9 +424,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
     const int grp = ((warp - 2) >> 2) & 1;
     const uint32_t tempty_c = leader_addr(&tempty[set]);
     int it = 0;
-    for (int w = cid; w < items; w += nclus) {
-      const int mt = w / units, unit = w % units;
-      const int nt0 = unit * args.tpu, nt1 = min(args.n_tiles, nt0 + args.tpu);
+    K1Seg seg(args, cid, nclus);
+    for (int mt, nt0, nt1, slot; seg.next(mt, nt0, nt1, slot);) {
       const int row = mt * 256 + (int)rank * 128 + quarter * 32 + lane;
       float2 rc = make_float2(0.f, 0.f);
       if (row < args.m) rc = args.rowc[row];
@@ -381,7 +457,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
         acc += (double)tile;
       }
       if (row < args.m)
-        args.partial[(size_t)(kI8EpiGroups * unit + set * 2 + grp) * args.m + row] = acc * 0.6931471805599453;
+        args.partial[(size_t)(kI8EpiGroups * slot + set * 2 + grp) * args.m + row] = acc * 0.6931471805599453;
     }
   }
 
