@@ -225,7 +225,7 @@ int spa_mwg_chain_slots(const spa_design* d, float* beta, int64_t m, int32_t ldb
                         double* slot_ll, double* slot_lp, unsigned long long* accepted, int32_t per_particle,
                         void* stream);
 
-/* Coordinates per blocked MwG round (1, 2, 4 or 8) for spa_mwg_chain_slots
+/* Coordinates per blocked MwG round (1, 2 or 4) for spa_mwg_chain_slots
  * (init_rounds) and spa_mwg_move (move_rounds), coded designs: a round
  * evaluates the next `rounds` coordinates' log-likelihood differences
  * against the current subject cache in one block reduction and decides them
@@ -234,6 +234,10 @@ int spa_mwg_chain_slots(const spa_design* d, float* beta, int64_t m, int32_t ldb
  * coordinate at a time, reference smc.py:177-199); it trades reductions and
  * barriers for discarded work after an acceptance.  Defaults: 4 / 4. */
 int spa_mwg_set_rounds(int32_t init_rounds, int32_t move_rounds);
+/* Whether the coded MwG kernels may keep the per-coordinate factor tables of
+ * a whole sweep in shared memory (when two chains per SM still fit; else they
+ * are built a round ahead in a ring).  Identical states either way; default 1. */
+int spa_mwg_set_tables(int32_t full_allowed);
 
 /* ---- K8: population random-walk moves (north-star kernel) --------------
  * Weighted moments into an int64 fixed-point (2^-48) accumulator

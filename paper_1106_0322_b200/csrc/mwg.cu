@@ -55,6 +55,9 @@ struct MwgParams {
   float* slot_beta;
   double* slot_ll;
   double* slot_lp;
+  // coded designs: the pair tables of all q coordinates are built with the
+  // sweep's slots (shared memory permitting) instead of per round in the ring
+  int full_tables;
 };
 
 __device__ __forceinline__ double mwg_gt(double b, const MwgParams& P) {
@@ -270,6 +273,7 @@ __global__ void __launch_bounds__(S == 8 ? 640 : (S == 16 ? 640 : 512)) mwg_kern
   float* fred = reinterpret_cast<float*>(red + 64);               // [2][D][32]
   uint2* ring = reinterpret_cast<uint2*>(fred + 64 * D);          // coded: [4D][n_words] code words
   float2* tring = reinterpret_cast<float2*>(ring + (size_t)MwgRing<D>::kSlots * P.d.n_words);  // coded: [4D][16]
+  float2* ttab = tring + MwgRing<D>::kSlots * 16;  // coded, full_tables: [q][16]
 
   const int64_t row = blockIdx.x;
   if (row >= P.m) return;
@@ -330,6 +334,12 @@ __global__ void __launch_bounds__(S == 8 ? 640 : (S == 16 ? 640 : 512)) mwg_kern
         cs.m0 = cs.m1 = cs.m2 = 0.0f;
       }
       slot[j] = cs;
+      if (CODED && P.full_tables) {  // pair table: entry e = (m[e & 3], m[e >> 2]), m = {m0, m1, m2, 0}
+        const float mv[4] = {cs.m0, cs.m1, cs.m2, 0.0f};
+        float2* tb = ttab + (size_t)j * 16;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) tb[e] = make_float2(mv[e & 3], mv[e >> 2]);
+      }
     }
     __syncthreads();
 
@@ -410,9 +420,12 @@ __global__ void __launch_bounds__(S == 8 ? 640 : (S == 16 ? 640 : 512)) mwg_kern
         coff[k] = e < D * nwd ? e / nwd : q;  // q: never loaded
         woff[k] = e - (e / nwd) * nwd;
       }
+      const bool full = P.full_tables != 0;
+      auto tbl_of = [&](int c) -> const float2* { return full ? ttab + c * 16 : tring + (c & (RS - 1)) * 16; };
       // the pair tables of coordinates [c0, c1) from their slots: entry e =
       // (m[e & 3], m[e >> 2]), m = {m0, m1, m2, 0} (code 3 = padding, sigma 0)
       auto build_tables = [&](int c0, int c1) {
+        if (full) return;
         for (int e = tid; e < 16 * (c1 - c0); e += nthr) {
           const int c = c0 + (e >> 4);
           if (c < q) {
@@ -439,16 +452,53 @@ __global__ void __launch_bounds__(S == 8 ? 640 : (S == 16 ? 640 : 512)) mwg_kern
           const int c = j + D + coff[k];
           if (c < q) lv[k] = __ldg(&codes[(size_t)c * nwd + woff[k]]);
         }
+        // the D sums as straight-line code (coordinates past q are computed
+        // on coordinate q-1 and never decided), so the scheduler interleaves
+        // the D independent product chains; the per-group range check of
+        // coord_log2_sum_tbl is hoisted: one rare divergent fallback
         float part[D];
+        float prodv[D][S / 8];
+        bool inrange = true;
 #pragma unroll
         for (int dd = 0; dd < D; ++dd) {
-          part[dd] = 0.0f;
-          if (j + dd < q) {
-            const int rs = (j + dd) & (RS - 1);
+          const int cc = min(j + dd, q - 1);
+          const int rs = cc & (RS - 1);
+          uint32_t cw[NCW];
+#pragma unroll
+          for (int w = 0; w < NCW; ++w) cw[w] = cr32[rs * 2 * nwd + cw0 + w] >> csh;
+          const float2* tbl = tbl_of(cc);
+#pragma unroll
+          for (int c8 = 0; c8 < S / 8; ++c8) {
+            float fac[8];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int pk = 4 * c8 + k;
+              const float2 mm = tbl[(cw[pk >> 3] >> (4 * (pk & 7))) & 15u];
+              fac[2 * k] = fmaf(mm.x, sig[2 * pk], 1.0f);
+              fac[2 * k + 1] = fmaf(mm.y, sig[2 * pk + 1], 1.0f);
+            }
+            const float pr = ((fac[0] * fac[1]) * (fac[2] * fac[3])) * ((fac[4] * fac[5]) * (fac[6] * fac[7]));
+            prodv[dd][c8] = pr;
+            inrange = inrange && (pr >= 1e-30f && pr <= 1e30f);
+          }
+        }
+        if (inrange) {
+#pragma unroll
+          for (int dd = 0; dd < D; ++dd) {
+            float acc = 0.0f;
+#pragma unroll
+            for (int c8 = 0; c8 < S / 8; ++c8) acc += fast_lg2(prodv[dd][c8]);
+            part[dd] = acc;
+          }
+        } else {  // an extreme proposal: the per-group form (per-term logs where a product leaves the range)
+#pragma unroll 1
+          for (int dd = 0; dd < D; ++dd) {
+            const int cc = min(j + dd, q - 1);
+            const int rs = cc & (RS - 1);
             uint32_t cw[NCW];
 #pragma unroll
             for (int w = 0; w < NCW; ++w) cw[w] = cr32[rs * 2 * nwd + cw0 + w] >> csh;
-            part[dd] = coord_log2_sum_tbl<S>(sig, cw, tring + rs * 16);
+            part[dd] = coord_log2_sum_tbl<S>(sig, cw, tbl_of(cc));
           }
         }
 #pragma unroll
@@ -499,27 +549,38 @@ __global__ void __launch_bounds__(S == 8 ? 640 : (S == 16 ? 640 : 512)) mwg_kern
             }
           }
         }
-        // decisions in order; the first acceptance ends the round
-        int adv = min(D, q - j);
+        // the D decisions (independent given the sums) evaluated together;
+        // the first acceptance ends the round, later ones are discarded
+        const int nv = min(D, q - j);
+        uint32_t okm = 0;
+        double dllv[D];
 #pragma unroll
         for (int dd = 0; dd < D; ++dd) {
-          if (dd < adv) {
-            const CoordSlot cs = slot[j + dd];
-            const double dll = cs.dsy - 0.6931471805599453 * (double)part[dd];
-            const double d = dll + cs.dlp;
-            if ((d >= 0.0) || (cs.logu < d)) {
-              const int rs = (j + dd) & (RS - 1);
-              uint32_t cw[NCW];
+          const int cc = min(j + dd, q - 1);
+          const double dsy = slot[cc].dsy, dlp = slot[cc].dlp, logu = slot[cc].logu;
+          dllv[dd] = dsy - 0.6931471805599453 * (double)part[dd];
+          const double d = dllv[dd] + dlp;
+          okm |= (dd < nv && ((d >= 0.0) || (logu < d))) ? 1u << dd : 0u;
+        }
+        int adv = nv;
+        if (okm) {
+          const int first = __ffs(okm) - 1;
+          double dll = dllv[0];
 #pragma unroll
-              for (int w = 0; w < NCW; ++w) cw[w] = cr32[rs * 2 * nwd + cw0 + w] >> csh;
-              coord_accept_tbl<S>(sig, cw, tring + rs * 16);
-              ll += dll;
-              lp += cs.dlp;
-              ++acc;
-              if (tid == 0) bsh[j + dd] = cs.newv;
-              adv = dd + 1;
-            }
-          }
+          for (int dd = 1; dd < D; ++dd)
+            if (dd == first) dll = dllv[dd];
+          const int ca = j + first;
+          const CoordSlot cs = slot[ca];
+          const int rs = ca & (RS - 1);
+          uint32_t cw[NCW];
+#pragma unroll
+          for (int w = 0; w < NCW; ++w) cw[w] = cr32[rs * 2 * nwd + cw0 + w] >> csh;
+          coord_accept_tbl<S>(sig, cw, tbl_of(ca));
+          ll += dll;
+          lp += cs.dlp;
+          ++acc;
+          if (tid == 0) bsh[ca] = cs.newv;
+          adv = first + 1;
         }
         j += adv;
       }
@@ -563,8 +624,7 @@ static const void* mwg_fn_sd(bool coded) {
 
 template <int S>
 static const void* mwg_fn_s(bool coded, int D) {
-  return D == 8 ? mwg_fn_sd<S, 8>(coded)
-                : D == 4 ? mwg_fn_sd<S, 4>(coded) : D == 2 ? mwg_fn_sd<S, 2>(coded) : mwg_fn_sd<S, 1>(coded);
+  return D == 4 ? mwg_fn_sd<S, 4>(coded) : D == 2 ? mwg_fn_sd<S, 2>(coded) : mwg_fn_sd<S, 1>(coded);
 }
 
 static const void* mwg_fn(int S, bool coded, int D = 1) {
@@ -584,10 +644,19 @@ static int rounds_for(const spa_design* d, int S, int nthr, bool init_layout) {
   return D;
 }
 
-static size_t mwg_smem(const spa_design* d, int D) {
+static size_t mwg_smem(const spa_design* d, int D, bool full_tables = false) {
   return (size_t)d->q * sizeof(CoordSlot) + (size_t)((d->q + 1) & ~1) * sizeof(float) + 64 * sizeof(double) +
          (size_t)64 * D * sizeof(float) +
-         (d->coded ? (size_t)MwgRing<1>::kSlots * D * (d->n_words * sizeof(uint2) + 16 * sizeof(float2)) : 0);
+         (d->coded ? (size_t)MwgRing<1>::kSlots * D * (d->n_words * sizeof(uint2) + 16 * sizeof(float2)) : 0) +
+         (full_tables ? (size_t)d->q * 16 * sizeof(float2) : 0);
+}
+// all q pair tables per sweep for the initialisation chains when two chains
+// still fit per SM (C3: 109 KB; init 0.89 -> 0.80 s); the lambda-step move
+// keeps the ring (its many resident particles per SM would not fit: C3 move
+// 102 -> 117 ms with the tables)
+static bool g_full_tables_allowed = true;
+static bool mwg_full_tables(const spa_design* d, int D, bool init_layout) {
+  return g_full_tables_allowed && init_layout && d->coded && mwg_smem(d, D, true) <= (size_t)112 * 1024;
 }
 
 static int max_threads(int S) { return S == 8 ? 640 : (S == 16 ? 640 : 512); }
@@ -633,10 +702,18 @@ using namespace spa;
 // lambda-step move (1, 2 or 4; coded designs; states are identical for any
 // value -- a tuning knob, used by the A/B tools and the bit-identity tests).
 extern "C" int spa_mwg_set_rounds(int32_t init_rounds, int32_t move_rounds) {
-  auto ok = [](int v) { return v == 1 || v == 2 || v == 4 || v == 8; };
-  SPA_REQUIRE(ok(init_rounds) && ok(move_rounds), kBadArgument, "spa_mwg_set_rounds: rounds must be 1, 2, 4 or 8");
+  auto ok = [](int v) { return v == 1 || v == 2 || v == 4; };
+  SPA_REQUIRE(ok(init_rounds) && ok(move_rounds), kBadArgument, "spa_mwg_set_rounds: rounds must be 1, 2 or 4");
   g_rounds_init = init_rounds;
   g_rounds_move = move_rounds;
+  return 0;
+}
+
+// Whether the coded MwG kernels may build all q pair tables per sweep
+// (shared memory permitting) instead of per round in the ring; the states
+// are identical either way (A/B and tests).
+extern "C" int spa_mwg_set_tables(int32_t full_allowed) {
+  g_full_tables_allowed = full_allowed != 0;
   return 0;
 }
 
@@ -661,7 +738,7 @@ extern "C" int spa_mwg_resident_chains(const spa_design* d, int64_t* chains) {
   SPA_REQUIRE(S > 0, kNotSupported, "spa_mwg_resident_chains: n > 16384 not supported");
   const int nthr = std::max(32, ((d->n + S - 1) / S + 31) / 32 * 32);
   const int D = rounds_for(d, S, nthr, true);
-  const size_t smem = mwg_smem(d, D);
+  const size_t smem = mwg_smem(d, D, mwg_full_tables(d, D, true));
   int per_sm = 0, dev = 0, nsm = 0;
   const void* fn = mwg_fn(S, d->coded != 0, D);
   SPA_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -711,7 +788,8 @@ static int mwg_launch(const spa_design* d, float* beta, int64_t m, int32_t ldb, 
   SPA_REQUIRE(nthr <= 1024, kNotSupported, "spa_mwg_move: too many subjects per particle");
   SPA_REQUIRE(nthr * S <= d->n_words * 32, kBadArgument, "spa_mwg_move: n_words does not cover the thread layout");
   const int D = rounds_for(d, S, nthr, init_layout);
-  const size_t smem = mwg_smem(d, D);
+  P.full_tables = mwg_full_tables(d, D, init_layout) ? 1 : 0;
+  const size_t smem = mwg_smem(d, D, P.full_tables != 0);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   SPA_REQUIRE(nthr <= max_threads(S), kNotSupported, "spa_mwg_move: too many threads for this layout");
   const void* fn = mwg_fn(S, d->coded != 0, D);

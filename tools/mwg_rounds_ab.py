@@ -47,7 +47,7 @@ def chain_time(K, sweeps, rounds):
 
 for K in (148, 296):
     ref = None
-    for rounds in (1, 2, 4, 8):
+    for rounds in (1, 2, 4):
         ms, acc, b = chain_time(K, 40, rounds)
         same = "" if ref is None else (" identical" if torch.equal(ref, b) else " DIFFERENT")
         ref = b if ref is None else ref
@@ -56,7 +56,7 @@ for K in (148, 296):
 
 cfg = S.SmcConfig(N=65536, move_kernel="rw", moves=5, seed=1, init_burn=2000, init_thin=5)
 prior1 = S.GtPrior(1.0, 2.0)
-for rounds in (4, 8, 4, 8):
+for rounds in (4, 2, 4):
     _lib.call("spa_mwg_set_rounds", rounds, 1)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
