@@ -57,6 +57,9 @@ typedef struct spa_design {
   const uint32_t* codes;    /* coded: [q][2*n_words] genotype codes for the MwG
                                kernel, 16 subjects per word, subject s of the
                                word in bits 2s..2s+1 (0,1,2; 3 = padding)    */
+  const double* sx;         /* [q]     X^T 1 (coded K1: softplus(eta) =
+                               eta/2 + (|eta|/2 + log(1 + e^-|eta|)), the
+                               linear half summed by the pack)              */
 } spa_design;
 
 /* Prior description: a > 0 (generalised t, model.py:78-81) or a = +inf
@@ -77,7 +80,8 @@ int spa_philox_blocks(uint64_t k0, uint64_t k1, uint64_t first_block, int64_t co
  * spa_k1_operand_bytes(d, m) bytes:
  *   coded designs  -- int8 tensor cores: three byte planes [hi | mid | lo]
  *                     [m][3*kp] of the 22-bit per-row fixed point of
- *                     alpha*beta, then {scale, offset} float2 [m];
+ *                     alpha*beta, then {scale, offset} float2 [m], then
+ *                     (1/2) sum_i eta_ki = (1/2) beta_k . X^T 1 float64 [m];
  *   general        -- fp16 [m][2*kp] = [hi | lo] (22 significant bits).
  * out_sp[m] = sum_i softplus(eta_ki) (float64).
  * ws: workspace of spa_loglik_workspace_bytes(m, n) bytes. */

@@ -33,6 +33,7 @@ class SpaDesign(ctypes.Structure):
         ("kp", c_int32),
         ("terms", c_int32),
         ("codes", c_void_p),
+        ("sx", c_void_p),
     ]
 
 

@@ -288,9 +288,18 @@ __device__ __forceinline__ void emit_f16_4(__half* __restrict__ row16, int kp, i
 __host__ __device__ inline float2* k1_rowc(void* A, int64_t m, int kp) {
   return reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(A) + (size_t)m * 3 * kp);
 }
-__device__ __forceinline__ void emit_row_constants(float2* rowc, int64_t row, float amax, double off, double* ylin_row) {
+// (1/2) sum_i eta_ki = (1/2) prop_k . X^T 1 of the coded rows, after {s, o}:
+// K1 sums the symmetric part |eta|/2 + log(1 + e^-|eta|) of softplus(eta)
+// (one instruction per element fewer than max(eta, 0) + log(1 + e^-|eta|))
+// and adds this linear half in its row reduction
+__host__ __device__ inline double* k1_half(void* A, int64_t m, int kp) {
+  return reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(k1_rowc(A, m, kp)) + (size_t)m * sizeof(float2));
+}
+__device__ __forceinline__ void emit_row_constants(void* A, int64_t m, int kp, int64_t row, float amax, double off,
+                                                   double hx, double* ylin_row) {
   const bool ok = amax < INFINITY;  // false for inf / NaN
-  rowc[row] = make_float2(ok ? amax / kQMax : 0.f, (float)off);
+  k1_rowc(A, m, kp)[row] = make_float2(ok ? amax / kQMax : 0.f, (float)off);
+  k1_half(A, m, kp)[row] = 0.5 * hx;
   if (!ok || !(fabs(off) < 3.0e38)) *ylin_row = __longlong_as_double(0x7ff8000000000000ll);
 }
 __device__ __forceinline__ float i8_inv(float amax) { return (amax > 0.f && amax < INFINITY) ? kQMax / amax : 0.f; }
@@ -312,7 +321,7 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const 
   if (row >= m) return;
   const float* b = beta + row * ldb;
   const __nv_bfloat16* e = eps ? eps + row * ldb : nullptr;
-  double yl = 0.0, off = 0.0;
+  double yl = 0.0, off = 0.0, hx = 0.0;
   LpAcc la;
   const double K = pc.de ? 0.0 : 1.0 / (pc.a * pc.c);
   const bool vec = (ldb & 3) == 0;
@@ -345,7 +354,7 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const 
   for (int j0 = lane * 4; j0 < d.kp; j0 += 128) {
     float p[4];
     load_p(j0, p);
-    float fy = 0.f, fo = 0.f;
+    float fy = 0.f, fo = 0.f, fx = 0.f;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int j = j0 + i;
@@ -355,9 +364,11 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const 
         bad |= !(fabsf(bs) < INFINITY);
         fy = fmaf(p[i], (float)d.sy[j], fy);
         fo = fmaf(p[i], d.coded ? (float)d.gamma[j] : 0.f, fo);
+        fx = fmaf(p[i], d.coded ? (float)d.sx[j] : 0.f, fx);
         if (!d.coded && !(fabsf(bs) < kOpMax)) fy = __int_as_float(0x7fc00000);
       }
     }
+    hx += fx;
     if (lp != nullptr) {
       float pen[4];
 #pragma unroll
@@ -384,13 +395,14 @@ __global__ void pack_kernel(spa_design d, const float* __restrict__ beta, const 
   }
   yl = warp_sum(yl);
   off = warp_sum(off);
+  hx = warp_sum(hx);
   double lps = 0.0;
   if (lp != nullptr) lps = warp_sum(la.value(pc));
   if (lane == 0) {
     ylin[row] = yl;
     if (lp != nullptr) lp[row] = lps;
     // eta = sum_j g_ij alpha_j beta_j + sum_j gamma_j beta_j: the offset rides in the row constants
-    if (d.coded) emit_row_constants(k1_rowc(A, m, d.kp), row, amax, off, ylin + row);
+    if (d.coded) emit_row_constants(A, m, d.kp, row, amax, off, hx, ylin + row);
   }
 }
 
@@ -424,7 +436,7 @@ __device__ __forceinline__ void ring_prop4(const float* b, const __nv_bfloat16* 
 }
 
 __host__ __device__ inline size_t pack_eps_smem_bytes(int kp, int ldb) {
-  return (size_t)16 * kp + (size_t)kPackWarps * kPackSlots * ((size_t)ldb * 6);
+  return (size_t)20 * kp + (size_t)kPackWarps * kPackSlots * ((size_t)ldb * 6);
 }
 
 template <int IT, bool CODED>
@@ -439,15 +451,17 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
   float* cs = ca + d.kp;
   float* cg = cs + d.kp;
   float* cp = cg + d.kp;
+  float* cx = cp + d.kp;  // X^T 1 (coded: the linear half of softplus)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rowB = (uint32_t)ldb * 4, slotB = (uint32_t)ldb * 6;
-  uint8_t* ring = reinterpret_cast<uint8_t*>(cp + d.kp) + (size_t)warp * kPackSlots * slotB;
+  uint8_t* ring = reinterpret_cast<uint8_t*>(cx + d.kp) + (size_t)warp * kPackSlots * slotB;
   for (int j = threadIdx.x; j < d.kp; j += blockDim.x) {
     const bool v = j < d.q;
     ca[j] = v ? (float)d.alpha[j] : 0.f;
     cs[j] = v ? (float)d.sy[j] : 0.f;
     cg[j] = (v && CODED) ? (float)d.gamma[j] : 0.f;
     cp[j] = (v && d.penalized[j]) ? 1.f : 0.f;
+    cx[j] = (v && CODED) ? (float)d.sx[j] : 0.f;
   }
   if (lane == 0) {
     for (int sl = 0; sl < kPackSlots; ++sl) mbar_init(&bars[warp][sl], 1);
@@ -474,7 +488,7 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
     phase ^= 1u << s;
     const float* b = reinterpret_cast<const float*>(ring + s * slotB);
     const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(ring + s * slotB + rowB);
-    double yl = 0.0, off = 0.0;  // same grouping as pack_kernel => identical sums
+    double yl = 0.0, off = 0.0, hx = 0.0;  // same grouping as pack_kernel => identical sums
     float amax = 0.f, nanf = 0.f;  // nanf: sum of bs - bs (NaN iff some bs is NaN / inf)
     float bsr[IT][4];  // alpha * prop, kept for the operand pass
     // log-prior: the LpAcc product order without its per-chunk overflow
@@ -486,21 +500,24 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
     for (int it = 0; it < IT; ++it) {
       const int j0 = it * 128 + lane * 4;
       if (j0 >= d.kp) break;
-      float fy = 0.f, fo = 0.f;
+      float fy = 0.f, fo = 0.f, fx = 0.f;
       float p[4];
       ring_prop4(b, e, j0, d.q, full, p);
       const float4 va = *reinterpret_cast<const float4*>(ca + j0);
       const float4 vs = *reinterpret_cast<const float4*>(cs + j0);
       const float4 vg = *reinterpret_cast<const float4*>(cg + j0);
       const float4 vp = *reinterpret_cast<const float4*>(cp + j0);
+      const float4 vx = *reinterpret_cast<const float4*>(cx + j0);
       const float a4[4] = {va.x, va.y, va.z, va.w}, s4[4] = {vs.x, vs.y, vs.z, vs.w};
       const float g4[4] = {vg.x, vg.y, vg.z, vg.w}, p4[4] = {vp.x, vp.y, vp.z, vp.w};
+      const float x4[4] = {vx.x, vx.y, vx.z, vx.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const float bs = a4[i] * p[i];
         bsr[it][i] = bs;
         fy = fmaf(p[i], s4[i], fy);
         fo = fmaf(p[i], g4[i], fo);
+        if (CODED) fx = fmaf(p[i], x4[i], fx);
         if (CODED) {
           amax = fmaxf(amax, fabsf(bs));
           nanf += bs - bs;
@@ -519,6 +536,7 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
       }
       yl += fy;
       off += fo;
+      hx += fx;
     }
     if (CODED) {
 #pragma unroll
@@ -563,11 +581,12 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
     }
     yl = warp_sum(yl);
     off = warp_sum(off);
+    if (CODED) hx = warp_sum(hx);
     const double lps = warp_sum(lpl);
     if (lane == 0) {
       ylin[row] = yl;
       if (lp != nullptr) lp[row] = lps;
-      if (CODED) emit_row_constants(k1_rowc(A, m, d.kp), row, amax, off, ylin + row);
+      if (CODED) emit_row_constants(A, m, d.kp, row, amax, off, hx, ylin + row);
     }
   }
 }
@@ -589,15 +608,17 @@ __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
   float* cs = ca + d.kp;
   float* cg = cs + d.kp;
   float* cp = cg + d.kp;
+  float* cx = cp + d.kp;  // X^T 1 (coded: the linear half of softplus)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, sub = lane % LPR, rsub = lane / LPR;
   const uint32_t rowB = (uint32_t)ldb * 4, slotB = (uint32_t)ldb * 6, groupB = slotB * R;
-  uint8_t* ring = reinterpret_cast<uint8_t*>(cp + d.kp) + (size_t)warp * kPackSlots * groupB;
+  uint8_t* ring = reinterpret_cast<uint8_t*>(cx + d.kp) + (size_t)warp * kPackSlots * groupB;
   for (int j = threadIdx.x; j < d.kp; j += blockDim.x) {
     const bool v = j < d.q;
     ca[j] = v ? (float)d.alpha[j] : 0.f;
     cs[j] = v ? (float)d.sy[j] : 0.f;
     cg[j] = (v && CODED) ? (float)d.gamma[j] : 0.f;
     cp[j] = (v && d.penalized[j]) ? 1.f : 0.f;
+    cx[j] = (v && CODED) ? (float)d.sx[j] : 0.f;
   }
   if (lane == 0) {
     for (int sl = 0; sl < kPackSlots; ++sl) mbar_init(&bars[warp][sl], 1);
@@ -632,28 +653,31 @@ __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
     const bool live = row < m;
     const float* b = reinterpret_cast<const float*>(ring + s * groupB + rsub * slotB);
     const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(ring + s * groupB + rsub * slotB + rowB);
-    double yl = 0.0, off = 0.0, prod = 1.0, lin = 0.0;
+    double yl = 0.0, off = 0.0, hx = 0.0, prod = 1.0, lin = 0.0;
     float npen = 0.f, amax = 0.f, nanf = 0.f;  // nanf: sum of bs - bs (NaN iff some bs is NaN / inf)
     float bsr[IT][4];  // alpha * prop, kept for the operand pass
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
       const int j0 = (it * LPR + sub) * 4;
       if (j0 >= d.kp) break;
-      float fy = 0.f, fo = 0.f;
+      float fy = 0.f, fo = 0.f, fx = 0.f;
       float p[4] = {0.f, 0.f, 0.f, 0.f};
       if (live) ring_prop4(b, e, j0, d.q, full, p);
       const float4 va = *reinterpret_cast<const float4*>(ca + j0);
       const float4 vs = *reinterpret_cast<const float4*>(cs + j0);
       const float4 vg = *reinterpret_cast<const float4*>(cg + j0);
       const float4 vp = *reinterpret_cast<const float4*>(cp + j0);
+      const float4 vx = *reinterpret_cast<const float4*>(cx + j0);
       const float a4[4] = {va.x, va.y, va.z, va.w}, s4[4] = {vs.x, vs.y, vs.z, vs.w};
       const float g4[4] = {vg.x, vg.y, vg.z, vg.w}, p4[4] = {vp.x, vp.y, vp.z, vp.w};
+      const float x4[4] = {vx.x, vx.y, vx.z, vx.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const float bs = a4[i] * p[i];
         bsr[it][i] = bs;
         fy = fmaf(p[i], s4[i], fy);
         fo = fmaf(p[i], g4[i], fo);
+        if (CODED) fx = fmaf(p[i], x4[i], fx);
         if (CODED) {
           amax = fmaxf(amax, fabsf(bs));
           nanf += bs - bs;
@@ -670,6 +694,7 @@ __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
         prod *= fma(x0, K, 1.0) * fma(x1, K, 1.0) * (fma(x2, K, 1.0) * fma(x3, K, 1.0));
       yl += fy;
       off += fo;
+      hx += fx;
     }
     // row maximum over the row's LPR lanes (aligned groups of the warp)
     if (CODED) {
@@ -721,11 +746,12 @@ __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
       yl += __shfl_xor_sync(0xffffffffu, yl, o);
       off += __shfl_xor_sync(0xffffffffu, off, o);
       lpl += __shfl_xor_sync(0xffffffffu, lpl, o);
+      if (CODED) hx += __shfl_xor_sync(0xffffffffu, hx, o);
     }
     if (live && sub == 0) {
       ylin[row] = yl;
       if (lp != nullptr) lp[row] = lpl;
-      if (CODED) emit_row_constants(k1_rowc(A, m, d.kp), row, amax, off, ylin + row);
+      if (CODED) emit_row_constants(A, m, d.kp, row, amax, off, hx, ylin + row);
     }
   }
 }
@@ -1529,12 +1555,15 @@ __global__ void philox_blocks_kernel(Key2 k, uint64_t first, int64_t count, uint
   for (int j = 0; j < 4; ++j) out[4 * i + j] = w[j];
 }
 
+// hh (coded K1): the linear half (1/2) sum_i eta_ki added to the symmetric sums
 __global__ void reduce_units_kernel(const double* __restrict__ partial, int units, int64_t m,
-                                    const double* __restrict__ ylin, double* __restrict__ out) {
+                                    const double* __restrict__ ylin, double* __restrict__ out,
+                                    const double* __restrict__ hh = nullptr) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= m) return;
   double s = 0.0;
   for (int u = 0; u < units; ++u) s += partial[(size_t)u * m + k];
+  if (hh) s += hh[k];
   out[k] = ylin ? ylin[k] - s : s;
 }
 
@@ -2165,7 +2194,7 @@ int spa_philox_blocks(uint64_t k0, uint64_t k1, uint64_t first_block, int64_t co
 
 size_t spa_k1_operand_bytes(const spa_design* d, int64_t m) {
   if (!d || m < 0) return 0;
-  return d->coded ? (size_t)m * (3 * (size_t)d->kp + sizeof(float2)) : (size_t)m * 4 * (size_t)d->kp;
+  return d->coded ? (size_t)m * (3 * (size_t)d->kp + sizeof(float2) + sizeof(double)) : (size_t)m * 4 * (size_t)d->kp;
 }
 
 size_t spa_loglik_workspace_bytes(int64_t m, int32_t n) {
@@ -2187,12 +2216,14 @@ static bool k1_i8_resident(int kp) { return kp <= kI8MaxKb * kI8BK && k1_i8_pair
 // Per-row partial sums of the segments covering the row's particle tile
 // (k1_slots_of), summed in slot order, then ylin - sum.
 __global__ void reduce_k1_slots_kernel(const double* __restrict__ partial, int64_t m, int n_tiles, int U,
-                                       int nclus, const double* __restrict__ ylin, double* __restrict__ out) {
+                                       int nclus, const double* __restrict__ ylin, double* __restrict__ out,
+                                       const double* __restrict__ hh) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= m) return;
   const int units = kI8EpiGroups * k1_slots_of((int)(k >> 8), n_tiles, U, nclus);
   double s = 0.0;
   for (int u = 0; u < units; ++u) s += partial[(size_t)u * m + k];
+  s += hh[k];
   out[k] = ylin ? ylin[k] - s : s;
 }
 
@@ -2258,10 +2289,10 @@ static int loglik_i8(const spa_design* d, const void* A, int64_t m, const double
   SPA_CHECK_LAUNCH();
   if (sched == 0)
     reduce_k1_slots_kernel<<<cdiv(m, 256), 256, 0, st>>>(reinterpret_cast<double*>(ws), m, args.n_tiles, U, nclus,
-                                                         ylin, out);
+                                                         ylin, out, k1_half(const_cast<void*>(A), m, d->kp));
   else
     reduce_units_kernel<<<cdiv(m, 256), 256, 0, st>>>(reinterpret_cast<double*>(ws), kI8EpiGroups * args.units, m,
-                                                      ylin, out);
+                                                      ylin, out, k1_half(const_cast<void*>(A), m, d->kp));
   SPA_CHECK_LAUNCH();
   return 0;
 }
@@ -2738,7 +2769,7 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
   };
   // 2 rows per warp iteration where the doubled ring still fits 2 blocks per SM
   if (d->kp > 128 && d->kp <= 512) {
-    const size_t sm2 = (size_t)16 * d->kp + (size_t)kPackWarps * kPackSlots * 2 * ((size_t)ldb * 6);
+    const size_t sm2 = (size_t)20 * d->kp + (size_t)kPackWarps * kPackSlots * 2 * ((size_t)ldb * 6);
     auto kern = d->coded ? (d->kp <= 256 ? pack_eps_rows_kernel<4, 16, true> : pack_eps_rows_kernel<8, 16, true>)
                          : (d->kp <= 256 ? pack_eps_rows_kernel<4, 16, false> : pack_eps_rows_kernel<8, 16, false>);
     // the attribute / occupancy queries once per (kernel, smem size): the

@@ -84,8 +84,10 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool a_signed) {
          | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-// Softplus sum of one 32-column accumulator chunk of a row, in log2 units:
-//   sum_i softplus(eta_i) = ln 2 * [ sum_i max(y_i, 0) + log2 prod_i (1 + 2^-|y_i|) ],  y = eta log2 e
+// Symmetric softplus sum of one 32-column accumulator chunk of a row, in log2
+// units (softplus(eta) = eta / 2 + S(eta), the linear half added from the
+// pack's row constant (1/2) prop . X^T 1 by the row reduction):
+//   sum_i S(eta_i) = ln 2 * [ sum_i |y_i| / 2 + log2 prod_i (1 + 2^-|y_i|) ],  y = eta log2 e
 // with the product over four interleaved groups of eight factors in [1, 2]
 // (one lg2 per group: the XU pipe does one exp2 per element and 1/8 lg2).
 // The accumulators combine into the integer T in one shift-add:
@@ -113,13 +115,13 @@ __device__ __forceinline__ float k1_i8_chunk_sum(const uint32_t (&r1)[32], const
     const float e = fast_ex2(-fabsf(y));
 #endif
     P[i & 3] = fmaf(P[i & 3], e, P[i & 3]);
-    R[i & 1] += fmaxf(y, 0.0f);
+    R[i & 1] += RAGGED && i >= nval ? 0.0f : fabsf(y);
   }
   const float lg = (fast_lg2(P[0]) + fast_lg2(P[1])) + (fast_lg2(P[2]) + fast_lg2(P[3]));
 #if defined(K1_EPI_MODE) && K1_EPI_MODE == 1
   return __int_as_float(r1[0] ^ r2[31]);  // timing experiment only (TMEM loads, no softplus)
 #endif
-  return (R[0] + R[1]) + lg;
+  return 0.5f * (R[0] + R[1]) + lg;
 }
 
 struct K1I8Args {

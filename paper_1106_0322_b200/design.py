@@ -175,6 +175,7 @@ class DeviceDesign:
             t["gamma"] = torch.zeros(q, dtype=torch.float64, device=dev)
             terms = 2
         t["sy"] = torch.from_numpy(sy).to(dev)
+        t["sx"] = torch.from_numpy(X.sum(axis=0)).to(dev)  # X^T 1: the linear half of the coded K1 softplus
         t["penalized"] = torch.from_numpy(pen).to(dev)
         s = SpaDesign()
         s.n, s.q, s.coded, s.n_words = n, q, int(coded), n_words
@@ -182,6 +183,7 @@ class DeviceDesign:
         s.xcols = None if coded else t["xcols"].data_ptr()
         s.xlev = t["xlev"].data_ptr()
         s.sy = t["sy"].data_ptr()
+        s.sx = t["sx"].data_ptr()
         s.alpha = t["alpha"].data_ptr()
         s.gamma = t["gamma"].data_ptr()
         s.penalized = t["penalized"].data_ptr()
