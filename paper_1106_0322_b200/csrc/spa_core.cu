@@ -236,17 +236,6 @@ __device__ __forceinline__ void split_op(float x, __half& h, __half& l, float& f
   l = __float2half_rn(x - __half2float(h));
   if (!(fabsf(x) < kOpMax)) flag_into = __int_as_float(0x7fc00000);
 }
-// Coded designs: the centring offset o = sum_j gamma_j beta_j rides in three
-// fp16 limbs (B holds 1 in those columns); |o| >= 65504 -> NaN linear term.
-__device__ __forceinline__ void offset_limbs(double o, __half* dst, double* ylin_row) {
-  const __half o1 = __double2half(o);
-  const double r1 = o - (double)__half2float(o1);
-  const __half o2 = __double2half(r1);
-  dst[0] = o1;
-  dst[1] = o2;
-  dst[2] = __double2half(r1 - (double)__half2float(o2));
-  if (!(fabs(o) < (double)kOpMax)) *ylin_row = __longlong_as_double(0x7ff8000000000000ll);
-}
 
 // Integer-coded designs feed K1 on the int8 tensor cores (tc_k1_i8.cuh): the
 // row is a 22-bit fixed-point vector relative to its largest |alpha_j beta_j|,
