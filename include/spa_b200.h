@@ -203,10 +203,11 @@ int spa_resample_commit(const double* gate, float* beta, const float* beta_alt, 
  * Writes ll (log-likelihood) and lp (log-prior at c) of the final state,
  * and adds the number of accepted updates to *accepted (device u64), or,
  * with per_particle != 0, particle k's count to accepted[k]. */
-/* Chains (CTAs) of spa_mwg_chain_slots resident at once on the current
- * device for this design (occupancy x SMs); init_particles sizes its
- * parallel chains to one such wave (the reference's single init chain,
- * smc.py:202-245, is replaced by parallel chains). */
+/* Chains (CTAs) of spa_mwg_chain_slots (layout 1, the thinning chains)
+ * resident at once on the current device for this design (occupancy x SMs);
+ * init_particles sizes its parallel chains to one such wave (the
+ * reference's single init chain, smc.py:202-245, is replaced by parallel
+ * chains). */
 int spa_mwg_resident_chains(const spa_design* d, int64_t* chains);
 
 int spa_mwg_move(const spa_design* d, float* beta, int64_t m, int32_t ldb, double a, double c, double step_sd,
@@ -218,16 +219,16 @@ int spa_mwg_move(const spa_design* d, float* beta, int64_t m, int32_t ldb, doubl
  * beta/ll/lp end at the last slot's state.  Bit-identical to `slots` calls
  * of spa_mwg_chain_slots with slots = 1 and sweep0 advanced by
  * cycles_per_slot (one materialisation of the subject cache per slot
- * instead of two, one launch instead of `slots`).  Chains run the
- * latency layout (fewer subjects per thread, more threads per chain: one
- * resident wave of long sequential chains) where spa_mwg_move, the
- * throughput kernel of the lambda-step moves, keeps more subjects per
- * thread; the two therefore differ in float32 summation order. */
+ * instead of two, one launch instead of `slots`).  layout 0 (burn-in):
+ * the latency layout (fewer subjects per thread, more threads per chain,
+ * the factor tables of a whole sweep: one long chain per SM); layout 1
+ * (thinning): the throughput layout of spa_mwg_move (a resident wave of
+ * chains, several per SM).  Layouts differ in float32 summation order. */
 int spa_mwg_chain_slots(const spa_design* d, float* beta, int64_t m, int32_t ldb, double a, double c,
                         double step_sd, int32_t cycles_per_slot, int32_t slots, uint64_t seed, int32_t tag,
                         int64_t t, int64_t i0, int64_t sweep0, double* ll, double* lp, float* slot_beta,
                         double* slot_ll, double* slot_lp, unsigned long long* accepted, int32_t per_particle,
-                        void* stream);
+                        int32_t layout, void* stream);
 
 /* Coordinates per blocked MwG round (1, 2 or 4) for spa_mwg_chain_slots
  * (init_rounds) and spa_mwg_move (move_rounds), coded designs: a round

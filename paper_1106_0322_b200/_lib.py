@@ -92,7 +92,7 @@ _SIGNATURES = {
     "spa_mwg_set_tables": (c_int, [c_int32]),
     "spa_mwg_chain_slots": (c_int, [c_void_p, c_void_p, c_int64, c_int32, c_double, c_double, c_double, c_int32,
                                     c_int32, c_uint64, c_int32, c_int64, c_int64, c_int64, c_void_p, c_void_p,
-                                    c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
+                                    c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p]),
     "spa_mwg_move": (c_int, [POINTER(SpaDesign), c_void_p, c_int64, c_int32, c_double, c_double, c_double, c_int32,
                              c_uint64, c_int32, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_int32,
                              c_void_p]),

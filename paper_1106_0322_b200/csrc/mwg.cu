@@ -636,6 +636,12 @@ static const void* mwg_fn(int S, bool coded, int D = 1) {
 // (A/B and the bit-identity tests: every D gives the same states).
 static int g_rounds_init = 4, g_rounds_move = 4;
 
+// Thread layouts: the lambda-step move (many particles per SM), the
+// initialisation burn-in (one latency-bound chain per SM: fewer subjects per
+// thread, per-sweep factor tables) and the initialisation thinning chains
+// (a resident wave of chains: the move's throughput layout, the init rounds)
+enum class MwgLayout { kMove, kBurn, kThin };
+
 static int rounds_for(const spa_design* d, int S, int nthr, bool init_layout) {
   int D = init_layout ? g_rounds_init : g_rounds_move;
   if (!d->coded) return 1;
@@ -734,11 +740,11 @@ extern "C" int spa_mwg_prepare_kernels(void) {
 // times the SM count.  Initialisation sizes its parallel chains to one wave.
 extern "C" int spa_mwg_resident_chains(const spa_design* d, int64_t* chains) {
   SPA_REQUIRE(d && chains && d->q >= 1 && d->q <= 2048, kBadArgument, "spa_mwg_resident_chains: bad arguments");
-  const int S = pick_s_init(d->n);
+  const int S = pick_s(d->n);  // the thinning layout (spa_mwg_chain_slots, layout 1)
   SPA_REQUIRE(S > 0, kNotSupported, "spa_mwg_resident_chains: n > 16384 not supported");
   const int nthr = std::max(32, ((d->n + S - 1) / S + 31) / 32 * 32);
   const int D = rounds_for(d, S, nthr, true);
-  const size_t smem = mwg_smem(d, D, mwg_full_tables(d, D, true));
+  const size_t smem = mwg_smem(d, D, false);
   int per_sm = 0, dev = 0, nsm = 0;
   const void* fn = mwg_fn(S, d->coded != 0, D);
   SPA_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -752,11 +758,12 @@ extern "C" int spa_mwg_resident_chains(const spa_design* d, int64_t* chains) {
 static int mwg_launch(const spa_design* d, float* beta, int64_t m, int32_t ldb, double a, double c, double step_sd,
                       int32_t cycles, uint64_t seed, int32_t tag, int64_t t, int64_t i0, int64_t sweep0, double* ll,
                       double* lp, unsigned long long* accepted, int32_t per_particle, int32_t slots,
-                      float* slot_beta, double* slot_ll, double* slot_lp, void* stream, bool init_layout) {
+                      float* slot_beta, double* slot_ll, double* slot_lp, void* stream, MwgLayout layout) {
+  const bool init_layout = layout != MwgLayout::kMove;
   SPA_REQUIRE(d && beta && ll && accepted && m >= 0 && cycles >= 0, kBadArgument, "spa_mwg_move: bad arguments");
   SPA_REQUIRE(a > 0 && c > 0 && step_sd > 0, kBadArgument, "spa_mwg_move: a, c, step_sd must be positive");
   SPA_REQUIRE(d->q >= 1 && d->q <= 2048, kNotSupported, "spa_mwg_move: q must lie in [1, 2048]");
-  const int S = init_layout ? pick_s_init(d->n) : pick_s(d->n);
+  const int S = layout == MwgLayout::kBurn ? pick_s_init(d->n) : pick_s(d->n);
   SPA_REQUIRE(S > 0, kNotSupported, "spa_mwg_move: n > 16384 not supported");
   SPA_REQUIRE(d->coded ? d->codes != nullptr : d->xcols != nullptr, kBadArgument, "spa_mwg_move: design arrays");
   if (m == 0) return 0;
@@ -788,7 +795,7 @@ static int mwg_launch(const spa_design* d, float* beta, int64_t m, int32_t ldb, 
   SPA_REQUIRE(nthr <= 1024, kNotSupported, "spa_mwg_move: too many subjects per particle");
   SPA_REQUIRE(nthr * S <= d->n_words * 32, kBadArgument, "spa_mwg_move: n_words does not cover the thread layout");
   const int D = rounds_for(d, S, nthr, init_layout);
-  P.full_tables = mwg_full_tables(d, D, init_layout) ? 1 : 0;
+  P.full_tables = mwg_full_tables(d, D, layout == MwgLayout::kBurn) ? 1 : 0;
   const size_t smem = mwg_smem(d, D, P.full_tables != 0);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   SPA_REQUIRE(nthr <= max_threads(S), kNotSupported, "spa_mwg_move: too many threads for this layout");
@@ -805,16 +812,19 @@ extern "C" int spa_mwg_move(const spa_design* d, float* beta, int64_t m, int32_t
                             int64_t sweep0, double* ll, double* lp, unsigned long long* accepted,
                             int32_t per_particle, void* stream) {
   return mwg_launch(d, beta, m, ldb, a, c, step_sd, cycles, seed, tag, t, i0, sweep0, ll, lp, accepted, per_particle,
-                    0, nullptr, nullptr, nullptr, stream, false);
+                    0, nullptr, nullptr, nullptr, stream, MwgLayout::kMove);
 }
 
 extern "C" int spa_mwg_chain_slots(const spa_design* d, float* beta, int64_t m, int32_t ldb, double a, double c,
                                    double step_sd, int32_t cycles_per_slot, int32_t slots, uint64_t seed,
                                    int32_t tag, int64_t t, int64_t i0, int64_t sweep0, double* ll, double* lp,
                                    float* slot_beta, double* slot_ll, double* slot_lp,
-                                   unsigned long long* accepted, int32_t per_particle, void* stream) {
+                                   unsigned long long* accepted, int32_t per_particle, int32_t layout,
+                                   void* stream) {
   SPA_REQUIRE(slots >= 1 && slot_beta && slot_ll && slot_lp && cycles_per_slot >= 1, kBadArgument,
               "spa_mwg_chain_slots: bad slot arguments");
+  SPA_REQUIRE(layout == 0 || layout == 1, kBadArgument, "spa_mwg_chain_slots: layout must be 0 or 1");
   return mwg_launch(d, beta, m, ldb, a, c, step_sd, cycles_per_slot, seed, tag, t, i0, sweep0, ll, lp, accepted,
-                    per_particle, slots, slot_beta, slot_ll, slot_lp, stream, true);
+                    per_particle, slots, slot_beta, slot_ll, slot_lp, stream,
+                    layout ? MwgLayout::kThin : MwgLayout::kBurn);
 }

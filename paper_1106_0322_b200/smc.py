@@ -808,7 +808,7 @@ def init_particles(data, prior_at_b1: GtPrior, config: SmcConfig, intercept: boo
         _lib.call("spa_mwg_chain_slots", ctypes.byref(d.struct), _p(parents.beta), parents.N, parents.ldb,
                   float(prior_at_b1.a), float(prior_at_b1.c), float(config.step_sd), int(config.init_burn), 1,
                   int(config.seed), TAG_INIT, 0, int(parents.i0), 0, _p(parents.ll), _p(parents.lp), _p(bb), _p(bl),
-                  _p(bp), _p(pcounts), 1, _stream())
+                  _p(bp), _p(pcounts), 1, 0, _stream())  # layout 0: one latency-bound chain per SM
         del bb, bl, bp
         if F > 1:  # fork: thinning chain k starts from its parent's burned-in state
             par = torch.arange(c0, c1, device=system.device) // F - p0
@@ -824,7 +824,8 @@ def init_particles(data, prior_at_b1: GtPrior, config: SmcConfig, intercept: boo
     _lib.call("spa_mwg_chain_slots", ctypes.byref(d.struct), _p(chains.beta), chains.N, chains.ldb,
               float(prior_at_b1.a), float(prior_at_b1.c), float(config.step_sd), int(config.init_thin), int(R),
               int(config.seed), TAG_INIT if F == 1 else TAG_INIT_FORK, 0, int(chains.i0), int(config.init_burn),
-              _p(chains.ll), _p(chains.lp), _p(stage_b), _p(stage_l), _p(stage_p), _p(counts), 1, _stream())
+              _p(chains.ll), _p(chains.lp), _p(stage_b), _p(stage_l), _p(stage_p), _p(counts), 1, 1,
+              _stream())  # layout 1: the thinning chains' resident wave
     a, b = lo - c0 * R, hi - c0 * R  # this shard inside the staged slots [c0 R, c1 R)
     system.beta.copy_(stage_b.view(Kl * R, system.ldb)[a:b])
     system.ll.copy_(stage_l.view(-1)[a:b])

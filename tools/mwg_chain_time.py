@@ -27,7 +27,7 @@ cnt = torch.zeros(K, dtype=torch.int64, device="cuda")
 
 def run(n, sweep0):
     _lib.call("spa_mwg_chain_slots", ctypes.byref(d.struct), _p(s.beta), K, s.ldb, 1.0, 2.0, 0.5, n, 1, 7, 0, 0, 0,
-              sweep0, _p(s.ll), _p(s.lp), _p(bb), _p(bl), _p(bp), _p(cnt), 1, _stream())
+              sweep0, _p(s.ll), _p(s.lp), _p(bb), _p(bl), _p(bp), _p(cnt), 1, 0, _stream())
 
 
 run(20, 0)

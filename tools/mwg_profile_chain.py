@@ -24,6 +24,6 @@ bp = torch.empty(K, dtype=torch.float64, device="cuda")
 cnt = torch.zeros(K, dtype=torch.int64, device="cuda")
 for sw0 in (0, sweeps):
     _lib.call("spa_mwg_chain_slots", ctypes.byref(d.struct), _p(s.beta), K, s.ldb, 1.0, 2.0, 0.5, sweeps, 1, 7, 0, 0,
-              0, sw0, _p(s.ll), _p(s.lp), _p(bb), _p(bl), _p(bp), _p(cnt), 1, _stream())
+              0, sw0, _p(s.ll), _p(s.lp), _p(bb), _p(bl), _p(bp), _p(cnt), 1, 0, _stream())
 torch.cuda.synchronize()
 print("ok")

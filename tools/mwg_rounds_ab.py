@@ -31,7 +31,7 @@ def chain_time(K, sweeps, rounds):
 
     def run(n, sweep0):
         _lib.call("spa_mwg_chain_slots", ctypes.byref(d.struct), _p(s.beta), K, s.ldb, 1.0, 2.0, 0.5, n, 1, 7, 0, 0,
-                  0, sweep0, _p(s.ll), _p(s.lp), _p(bb), _p(bl), _p(bp), _p(cnt), 1, _stream())
+                  0, sweep0, _p(s.ll), _p(s.lp), _p(bb), _p(bl), _p(bp), _p(cnt), 1, 0, _stream())
 
     run(20, 0)
     torch.cuda.synchronize()
@@ -76,7 +76,7 @@ for mr in (1, 2, 4, 1, 2, 4):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     _lib.call("spa_mwg_move", ctypes.byref(d.struct), _p(s.beta), M, s.ldb, 1.0, 0.5, 0.5, 5, 3, 1, 2, 0, 0,
-              _p(s.ll), _p(s.lp), _p(cnt), 1, _stream())
+              _p(s.ll), _p(s.lp), _p(cnt), 1, 0, _stream())
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
