@@ -320,6 +320,11 @@ def main():
     import torch
 
     torch.cuda.set_device(local)
+    import paper_1106_0322_b200.smc as S
+
+    # the sampler's high-priority main stream (run_sampler uses it internally;
+    # the timed loop below calls smc_step directly, so it enters it here)
+    torch.cuda.set_stream(S.sampler_stream())
     group = None
     if ws > 1:
         import torch.distributed as dist
@@ -329,7 +334,6 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         group = ParticleGroup(dist.group.WORLD)
 
-    import paper_1106_0322_b200.smc as S
     from paper_1106_0322_b200 import _lib
     from paper_1106_0322_b200.data import named_spec, simulate_dataset
     from paper_1106_0322_b200.design import DeviceDesign
