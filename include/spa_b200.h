@@ -294,6 +294,16 @@ int spa_rw_normals(int64_t m, int32_t q, uint64_t seed, int64_t t, int64_t i0, i
 int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ldb, const void* Lb, uint64_t seed,
                    int64_t t, int64_t i0, int32_t move, void* zbuf, void* eps, void* A, double* ylin, double a,
                    double c, double* lp, void* stream);
+/* The two halves of spa_rw_propose.  spa_rw_increments: eps = L z for m rows
+ * (the tcgen05 GEMM; zbuf bf16 [m][roundup(q,64)], eps bf16 [m][ldb], q
+ * columns written) -- the increments do not depend on beta, so the sampler
+ * computes all moves of a lambda step in one call (m = moves x N) beside the
+ * step's reweighting.  spa_rw_pack: prop = beta + eps packed into the K1
+ * operand, ylin and the log-prior at c, as spa_rw_propose. */
+int spa_rw_increments(int64_t m, int32_t q, int32_t ldb, const void* Lb, const void* zbuf, void* eps,
+                      void* stream);
+int spa_rw_pack(const spa_design* d, const float* beta, int64_t m, int32_t ldb, const void* eps, void* A,
+                double* ylin, double a, double c, double* lp, void* stream);
 /* Metropolis accept: d = (ylin' - sp' + lp') - (ll + lp); u (53 bits) from
  * Philox4x32 counter (0xFFFFFFFF, i0+k, t, move | 3<<24); on accept beta <- beta + eps (the
  * proposal) and ll, lp are updated; adds the accepted count to *accepted. */

@@ -2706,20 +2706,13 @@ int spa_rw_normals(int64_t m, int32_t q, uint64_t seed, int64_t t, int64_t i0, i
   return 0;
 }
 
-int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ldb, const void* Lb, uint64_t seed,
-                   int64_t t, int64_t i0, int32_t move, void* zbuf, void* eps, void* A, double* ylin, double a,
-                   double c, double* lp, void* stream) {
-  SPA_REQUIRE(d && beta && Lb && zbuf && eps && A && ylin && m > 0, kBadArgument, "spa_rw_propose: bad arguments");
-  SPA_REQUIRE((ldb & 3) == 0 && beta != eps, kBadArgument, "spa_rw_propose: ldb % 4 != 0 or beta aliases eps");
-  SPA_REQUIRE(d->kp >= d->q && d->kp % 64 == 0, kBadArgument, "spa_rw_propose: kp must be >= q, a multiple of 64");
+int spa_rw_increments(int64_t m, int32_t q, int32_t ldb, const void* Lb, const void* zbuf, void* eps,
+                      void* stream) {
+  SPA_REQUIRE(Lb && zbuf && eps && m > 0 && q > 0 && ldb >= q, kBadArgument, "spa_rw_increments: bad arguments");
+  SPA_REQUIRE(m < (1ll << 31), kNotSupported, "spa_rw_increments: m >= 2^31 rows");
   cudaStream_t st = as_stream(stream);
-  const int q = d->q;
   const int kq = (q + 63) / 64 * 64;
-  __nv_bfloat16* Z = reinterpret_cast<__nv_bfloat16*>(zbuf);
-  (void)seed;
-  (void)t;
-  (void)i0;
-  (void)move;
+  const __nv_bfloat16* Z = reinterpret_cast<const __nv_bfloat16*>(zbuf);
   TcArgs args;
   args.m = (int)m;
   args.ncols = q;
@@ -2738,9 +2731,17 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
                                         (uint64_t)m * ldb);
   if (rc) return rc;
   epi.m = (int)m;
-  rc = launch_tc<1, 1, kPropBN, EpiStoreT<__nv_bfloat16>>(Z, (uint64_t)kq, Lb, (uint64_t)kq, (uint64_t)q, args, 1,
-                                                          epi, st);
-  if (rc) return rc;
+  return launch_tc<1, 1, kPropBN, EpiStoreT<__nv_bfloat16>>(Z, (uint64_t)kq, Lb, (uint64_t)kq, (uint64_t)q, args, 1,
+                                                            epi, st);
+}
+
+int spa_rw_pack(const spa_design* d, const float* beta, int64_t m, int32_t ldb, const void* eps, void* A,
+                double* ylin, double a, double c, double* lp, void* stream) {
+  SPA_REQUIRE(d && beta && eps && A && ylin && m > 0, kBadArgument, "spa_rw_pack: bad arguments");
+  SPA_REQUIRE((ldb & 3) == 0 && (const void*)beta != eps, kBadArgument, "spa_rw_pack: ldb % 4 != 0 or beta aliases eps");
+  SPA_REQUIRE(d->kp >= d->q && d->kp % 64 == 0, kBadArgument, "spa_rw_pack: kp must be >= q, a multiple of 64");
+  cudaStream_t st = as_stream(stream);
+  const __nv_bfloat16* epsb = reinterpret_cast<const __nv_bfloat16*>(eps);
   void* Ab = A;
   const PriorConst pc = make_prior(a, c, c);
   const size_t sm = pack_eps_smem_bytes(d->kp, ldb);
@@ -2809,6 +2810,21 @@ int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ld
   pack_kernel<<<cdiv(m, 8), 256, 0, st>>>(*d, beta, epsb, m, ldb, Ab, ylin, pc, lp);
   SPA_CHECK_LAUNCH();
   return 0;
+}
+
+int spa_rw_propose(const spa_design* d, const float* beta, int64_t m, int32_t ldb, const void* Lb, uint64_t seed,
+                   int64_t t, int64_t i0, int32_t move, void* zbuf, void* eps, void* A, double* ylin, double a,
+                   double c, double* lp, void* stream) {
+  SPA_REQUIRE(d && beta && Lb && zbuf && eps && A && ylin && m > 0, kBadArgument, "spa_rw_propose: bad arguments");
+  SPA_REQUIRE((ldb & 3) == 0 && (const void*)beta != eps, kBadArgument, "spa_rw_propose: ldb % 4 != 0 or beta aliases eps");
+  SPA_REQUIRE(d->kp >= d->q && d->kp % 64 == 0, kBadArgument, "spa_rw_propose: kp must be >= q, a multiple of 64");
+  (void)seed;
+  (void)t;
+  (void)i0;
+  (void)move;
+  const int rc = spa_rw_increments(m, d->q, ldb, Lb, zbuf, eps, stream);
+  if (rc) return rc;
+  return spa_rw_pack(d, beta, m, ldb, eps, A, ylin, a, c, lp, stream);
 }
 
 extern "C" int spa_mwg_prepare_kernels(void);  // mwg.cu

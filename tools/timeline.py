@@ -13,6 +13,7 @@ import paper_1106_0322_b200.smc as S  # noqa: E402
 from paper_1106_0322_b200.data import named_spec, simulate_dataset  # noqa: E402
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+torch.cuda.set_stream(S.sampler_stream())  # as run_sampler / bench.py
 data, _ = simulate_dataset(named_spec("c3"))
 cfg = S.SmcConfig(N=65536, move_kernel="rw", moves=5, seed=0, init_burn=20, init_thin=1, init_chains=1024)
 sched = S.make_schedule(2.0, 0.98, 100)
