@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-path", action="store_true", help="skip the full 99-step device-time path")
+    ap.add_argument("--no-c1", action="store_true", help="skip the whole-path C1 run_sampler timing")
     ap.add_argument("--profile", action="store_true",
                     help="bracket the timed steps with cudaProfilerStart/Stop (ncu --profile-from-start off)")
     return ap.parse_args()
@@ -250,6 +251,40 @@ def batched_loglik_rate(data, orc, n_sub=2048):
     return n_sub / (time.perf_counter() - t0)
 
 
+# C1 (BASELINE.json configs[0], the reference's own CPU-runnable case): the
+# whole run_sampler path with the reference's defaults (MwG kernel, N=1024,
+# 5 cycles, init_burn 2000 / thin 5, 50-step schedule b_t = 2 * 0.98^(t-1))
+C1 = dict(a=1.0, b1=2.0, rho=0.98, T=50, N=1024, cycles=5)
+
+
+def c1_reference_recorded():
+    """Walls of the reference package's own run_sampler at C1 (one thread),
+    recorded when its golden paths were generated in the build container
+    (tests/golden/make_golden.py gen_paths; 8 seeds)."""
+    import numpy as np
+
+    try:
+        g = np.load(os.path.join(ROOT, "tests", "golden", "path_c1.npz"), allow_pickle=True)
+        w = [float(v) for v in g["wall"]]
+        return {"wall_s_mean": sum(w) / len(w), "wall_s": w, "threads": 1,
+                "where": "build container, reference spa 0.1.0 (tests/golden/path_c1.npz)"}
+    except Exception as exc:  # pragma: no cover
+        return {"unavailable": str(exc)}
+
+
+def c1_port_run(orc, threads):
+    """The reference's run_sampler at C1 restated in numpy (oracle), timed on
+    this host with `threads` workers for the particle blocks (SmcConfig.threads)."""
+    from paper_1106_0322_b200.data import named_spec, simulate_dataset
+
+    data, _ = simulate_dataset(named_spec("c1"))
+    t0 = time.perf_counter()
+    lz = orc.run_sampler_port(data.X, data.y, C1["a"], C1["b1"], C1["rho"], C1["T"], C1["N"], C1["cycles"],
+                              threads=threads)
+    return {"wall_s": time.perf_counter() - t0, "threads": threads, "kind": "port", "log_z_T": lz,
+            "config": "C1: n=500 p=20 N=1024 a=1 b_t=2*0.98^(t-1) T=50, MwG 5 cycles, init_burn 2000 thin 5"}
+
+
 def cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -270,6 +305,7 @@ def reference_arm(args):
         run_cpu_baseline(data, 64, 1, orc, thr)
     val, dt = run_cpu_baseline(data, n_sub, args.steps, orc, thr)
     bl = batched_loglik_rate(data, orc)
+    c1 = None if args.no_c1 else dict(c1_port_run(orc, thr), reference_recorded=c1_reference_recorded())
     line = {
         "impl": "reference", "metric": "particle log-lik evals/s (SMC lambda-path, n x p)",
         "value": val, "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -284,6 +320,7 @@ def reference_arm(args):
                                    f"numpy restatement, particle blocks on {thr} threads (SmcConfig.threads)",
                          "batched_loglik_evals_per_s": bl},
         "e2e": {"value": val, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "c1_run_sampler": c1,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -484,6 +521,25 @@ def main():
                        "every 10th step; after an untimed 3-step warm-up run of the same shapes; mean of 2 runs"}
         del runs, out, out200
 
+    # C1 whole path through the public API with the reference's defaults
+    # (MwG kernel), beside the reference's own recorded walls at C1
+    c1 = None
+    if not args.no_c1 and ws == 1:
+        c1data, _ = simulate_dataset(named_spec("c1"))
+        c1cfg = dict(N=C1["N"], cycles=C1["cycles"], init_burn=2000, init_thin=5)
+        S.run_sampler(c1data, C1["a"], S.make_schedule(C1["b1"], C1["rho"], 3), S.SmcConfig(seed=9, **c1cfg))
+        walls = []
+        for seed_c1 in (1, 2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            S.run_sampler(c1data, C1["a"], S.make_schedule(C1["b1"], C1["rho"], C1["T"]),
+                          S.SmcConfig(seed=seed_c1, **c1cfg))
+            torch.cuda.synchronize()
+            walls.append(time.perf_counter() - t0)
+        c1 = {"wall_s": sum(walls) / len(walls), "wall_s_runs": walls, "move_kernel": "mwg",
+              "config": "C1: n=500 p=20 N=1024 a=1 b_t=2*0.98^(t-1) T=50, MwG 5 cycles, init_burn 2000 thin 5 "
+                        "(the reference's defaults); host Dataset in, host SmcOutput out",
+              "reference_recorded": c1_reference_recorded()}
     if rank != 0:
         return 0
     cpu = None
@@ -520,6 +576,7 @@ def main():
                      "algorithmic_flops_per_launch": flops_per_launch,
                      "k1_share_of_step": (k1_ms * MOVES) / step_ms},
         "full_path": full,
+        "c1_run_sampler": c1,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,

@@ -398,3 +398,68 @@ def em_map(X, y, a: float, c: float, beta_init, penalized, tol=1e-6, max_iter=50
     eta = X @ beta
     lp = float(eta @ y - np.logaddexp(0.0, eta).sum() + gt_log_density(beta[penalized], a, c).sum())
     return beta, lp, converged, inner_ok, it
+
+
+# ---------------------------------------------------------------------------
+# Whole-path timing baseline
+
+
+def run_sampler_port(X, y, a: float, b1: float, rho: float, T: int, N: int, cycles: int = 5, step_sd: float = 0.5,
+                     init_burn: int = 2000, init_thin: int = 5, seed: int = 0, threads: int = 1,
+                     ess_frac: float = 0.75):
+    """The reference's run_sampler (smc.py:427-449) restated for the CPU
+    timing baseline of bench.py: ONE Metropolis-within-Gibbs chain from the
+    origin, init_burn sweeps, then every init_thin-th state (init_particles /
+    _run_chain, smc.py:202-245); then T-1 lambda steps of reweight -> ESS ->
+    systematic resampling -> `cycles` MwG sweeps over particle blocks on
+    `threads` workers (smc_step, smc.py:397-424; _move_particles,
+    smc.py:335-359), with the vectorised arithmetic of _move_block
+    (smc.py:298-332).  NumPy's default generator replaces the reference's
+    Philox streams (same work, different draws).  Returns log Z_T / Z_1."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    X = np.asarray(X, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    rng = np.random.default_rng(seed)
+    q = X.shape[1]
+    bs = schedule_bs(b1, rho, T)
+    cs = bs / a if math.isfinite(a) else bs
+    beta = np.zeros((1, q))
+    eta = beta @ X.T
+    ll = loglik_rows(X, y, beta)
+
+    def sweep(b, e, l, c):
+        return mwg_move_rows(b, e, l, X, y, a, c, step_sd, rng.standard_normal((b.shape[0], 1, q)),
+                             rng.random((b.shape[0], 1, q)))[:3]
+
+    for _ in range(init_burn):
+        beta, eta, ll = sweep(beta, eta, ll, cs[0])
+    B = np.empty((N, q))
+    E = np.empty((N, X.shape[0]))
+    L = np.empty(N)
+    for k in range(N):
+        for _ in range(init_thin):
+            beta, eta, ll = sweep(beta, eta, ll, cs[0])
+        B[k], E[k], L[k] = beta[0], eta[0], ll[0]
+    logw = np.full(N, -math.log(N))
+    log_z = 0.0
+    bounds = np.linspace(0, N, threads + 1, dtype=int)
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        for t in range(1, T):
+            lw = reweight_increments(B, a, cs[t], cs[t - 1])
+            logw, inc = normalise_log_weights(logw, lw)
+            log_z += inc
+            w = weights_from_log(logw)
+            if ess(w) < ess_frac * N:
+                idx = systematic_ancestors(w, rng.random() / N)
+                B, E, L = B[idx], E[idx], L[idx]
+                logw = np.full(N, -math.log(N))
+            Z = rng.standard_normal((N, cycles, q))
+            U = rng.random((N, cycles, q))
+            parts = list(pool.map(lambda lh: mwg_move_rows(B[lh[0]:lh[1]], E[lh[0]:lh[1]], L[lh[0]:lh[1]], X, y, a,
+                                                           cs[t], step_sd, Z[lh[0]:lh[1]], U[lh[0]:lh[1]]),
+                                  [(lo, hi) for lo, hi in zip(bounds[:-1], bounds[1:]) if hi > lo]))
+            B = np.concatenate([p[0] for p in parts])
+            E = np.concatenate([p[1] for p in parts])
+            L = np.concatenate([p[2] for p in parts])
+    return log_z
