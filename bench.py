@@ -151,23 +151,34 @@ class ClockSampler:
 
 
 class EventTimer:
-    """CUDA events around one kernel, recorded on the launching stream."""
+    """CUDA events around one kernel, recorded on the launching stream (the
+    events are created and the stream looked up before the timed region, so
+    the timer adds little host time to launch-bound configurations)."""
 
     def __init__(self, torch):
         self.torch = torch
         self.pairs = {}
         self.enabled = False
+        self.pool = []
+        self.stream = None
+
+    def prepare(self, n):
+        self.pool = [self.torch.cuda.Event(enable_timing=True) for _ in range(2 * n)]
+        self.stream = self.torch.cuda.current_stream()
+
+    def _event(self):
+        return self.pool.pop() if self.pool else self.torch.cuda.Event(enable_timing=True)
 
     def start(self, name):
         if self.enabled:
-            e = self.torch.cuda.Event(enable_timing=True)
-            e.record(self.torch.cuda.current_stream())
+            e = self._event()
+            e.record(self.stream or self.torch.cuda.current_stream())
             self.pairs.setdefault(name, []).append([e, None])
 
     def stop(self, name):
         if self.enabled:
-            e = self.torch.cuda.Event(enable_timing=True)
-            e.record(self.torch.cuda.current_stream())
+            e = self._event()
+            e.record(self.stream or self.torch.cuda.current_stream())
             self.pairs[name][-1][1] = e
 
     def mean_ms(self, name):
@@ -390,6 +401,7 @@ def main():
         t += 1
     S.resolve_records(system, warm)
     timer = EventTimer(torch)
+    timer.prepare(args.steps * MOVES + 8)
     S.KERNEL_TIMER = timer
     torch.cuda.synchronize()
     if group is not None:

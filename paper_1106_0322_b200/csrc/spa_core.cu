@@ -64,37 +64,76 @@ static PFN_memGetAddressRange mem_range_fn() {
   return fn;
 }
 
+// cuTensorMapEncodeTiled through a small per-thread cache: a map depends only
+// on its arguments, and the sampler re-encodes the same few maps (the same
+// buffers) for every launch -- ~2 us of host time each in a launch-bound step.
+struct TmapKey {
+  int dev, dtype, rank, swizzle, l2;
+  const void* ptr;
+  cuuint64_t dims[3], strides[2];
+  cuuint32_t box[3];
+};
+static int encode_tmap_cached(CUtensorMap* map, CUtensorMapDataType dt, int rank, const void* ptr,
+                              const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box,
+                              CUtensorMapSwizzle sw, CUtensorMapL2promotion l2) {
+  struct Entry {
+    TmapKey key;
+    CUtensorMap map;
+    bool used;
+  };
+  static thread_local Entry cache[64];
+  static thread_local int next = 0;
+  TmapKey k;
+  std::memset(&k, 0, sizeof(k));
+  SPA_CHECK_CUDA(cudaGetDevice(&k.dev));
+  k.dtype = (int)dt;
+  k.rank = rank;
+  k.swizzle = (int)sw;
+  k.l2 = (int)l2;
+  k.ptr = ptr;
+  for (int i = 0; i < rank; ++i) {
+    k.dims[i] = dims[i];
+    k.box[i] = box[i];
+    if (i + 1 < rank) k.strides[i] = strides[i];
+  }
+  for (auto& e : cache)
+    if (e.used && std::memcmp(&e.key, &k, sizeof(k)) == 0) {
+      *map = e.map;
+      return 0;
+    }
+  auto enc = tmap_encoder();
+  if (!enc) return fail(kDriverEntryPoint, "cuTensorMapEncodeTiled unavailable");
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(map, dt, (cuuint32_t)rank, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, l2, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(kDriverEntryPoint, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  Entry& e = cache[next];
+  next = (next + 1) % 64;
+  e.key = k;
+  e.map = *map;
+  e.used = true;
+  return 0;
+}
+
 // 16-bit (bf16 / fp16) matrix [rows][cols] row-major; box = 64 columns x
 // box_rows rows, 128B swizzle.
 static int make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t cols, uint64_t rows, uint32_t box_rows,
                           bool f16 = false) {
-  auto enc = tmap_encoder();
-  if (!enc) return fail(kDriverEntryPoint, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
   cuuint32_t box[2] = {64, box_rows};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(map, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(kDriverEntryPoint, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-  return 0;
+  return encode_tmap_cached(map, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ptr, dims,
+                            strides, box, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
 }
 
 // byte matrix [rows][cols] row-major (the int8 K1 planes); box = 64 columns
 // x 128 rows, 64B swizzle (one swizzle atom per row of the box)
 static int make_tmap_u8(CUtensorMap* map, const void* ptr, uint64_t cols, uint64_t rows, uint32_t box_rows = 128) {
-  auto enc = tmap_encoder();
-  if (!enc) return fail(kDriverEntryPoint, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols};
   cuuint32_t box[2] = {(cuuint32_t)kI8BK, box_rows};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(kDriverEntryPoint, "cuTensorMapEncodeTiled (u8) failed: " + std::to_string((int)r));
-  return 0;
+  return encode_tmap_cached(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, ptr, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
 }
 
 // Output map for EpiStoreT: [units][rows][cols] (OutT = float / bf16), row
@@ -103,21 +142,15 @@ static int make_tmap_u8(CUtensorMap* map, const void* ptr, uint64_t cols, uint64
 template <class OutT>
 static int make_tmap_out(CUtensorMap* map, void* ptr, uint64_t cols, uint64_t rows, uint64_t units, uint64_t ld,
                          uint64_t unit_stride) {
-  auto enc = tmap_encoder();
-  if (!enc) return fail(kDriverEntryPoint, "cuTensorMapEncodeTiled unavailable");
   constexpr bool f32 = sizeof(OutT) == 4;
   if ((ld * sizeof(OutT)) % 16 || (unit_stride * sizeof(OutT)) % 16 || (reinterpret_cast<uintptr_t>(ptr) & 15))
     return fail(kBadArgument, "TMA store: output rows must be 16-byte aligned");
   cuuint64_t dims[3] = {cols, rows, units};
   cuuint64_t strides[2] = {ld * sizeof(OutT), unit_stride * sizeof(OutT)};
   cuuint32_t box[3] = {32, 32, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, ptr, dims,
-                   strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(kDriverEntryPoint, "cuTensorMapEncodeTiled (store) failed: " + std::to_string((int)r));
-  return 0;
+  return encode_tmap_cached(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, ptr, dims,
+                            strides, box, f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                            CU_TENSOR_MAP_L2_PROMOTION_NONE);
 }
 
 template <int TA, int TB, int BN, class Epi, int TM = 1, bool F16 = false>

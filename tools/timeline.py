@@ -14,8 +14,10 @@ from paper_1106_0322_b200.data import named_spec, simulate_dataset  # noqa: E402
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 torch.cuda.set_stream(S.sampler_stream())  # as run_sampler / bench.py
-data, _ = simulate_dataset(named_spec("c3"))
-cfg = S.SmcConfig(N=65536, move_kernel="rw", moves=5, seed=0, init_burn=20, init_thin=1, init_chains=1024)
+cfg_name = os.environ.get("TIMELINE_CONFIG", "c3")
+Nn = int(os.environ.get("TIMELINE_N", "65536"))
+data, _ = simulate_dataset(named_spec(cfg_name))
+cfg = S.SmcConfig(N=Nn, move_kernel="rw", moves=5, seed=0, init_burn=20, init_thin=1, init_chains=min(1024, Nn))
 sched = S.make_schedule(2.0, 0.98, 100)
 s, _ = S.init_particles(data, S.GtPrior(1.0, 2.0), cfg)
 for t in (2, 3, 4):
