@@ -310,6 +310,16 @@ int spa_rw_pack(const spa_design* d, const float* beta, int64_t m, int32_t ldb, 
 int spa_rw_accept(float* beta, int32_t ldb, const void* eps, int32_t q, int64_t m, const double* ylin_p,
                   const double* sp_p, const double* lp_p, double* ll, double* lp, uint64_t seed, int64_t t,
                   int64_t i0, int32_t move, unsigned long long* accepted, void* stream);
+/* Integer-coded designs: K1 without its row reduction (spa_loglik_partials
+ * leaves the partial row sums in ws), and the accept that reduces them itself
+ * (spa_rw_accept_k1: sp = the same fixed-order sum spa_loglik_softplus forms,
+ * so the decisions and states are bit-identical to spa_loglik_softplus +
+ * spa_rw_accept, one launch fewer per move).  ws and A as passed to
+ * spa_loglik_partials for the same design and m. */
+int spa_loglik_partials(const spa_design* d, const void* A, int64_t m, void* ws, size_t ws_bytes, void* stream);
+int spa_rw_accept_k1(float* beta, int32_t ldb, const void* eps, int32_t q, int64_t m, const spa_design* d,
+                     const void* A, const double* ylin_p, const void* ws, const double* lp_p, double* ll, double* lp,
+                     uint64_t seed, int64_t t, int64_t i0, int32_t move, unsigned long long* accepted, void* stream);
 
 /* ---- f1: per-step weighted marginal summaries (summary.py:36-61) --------
  * Weighted mean, weighted quantiles at nlev <= 4 levels ("smallest value whose

@@ -111,6 +111,10 @@ _SIGNATURES = {
     "spa_tc_gemm_f32": (c_int, [c_void_p, c_int64, c_int32, c_void_p, c_int32, c_int32, c_void_p, c_int32, c_void_p]),
     "spa_rw_accept": (c_int, [c_void_p, c_int32, c_void_p, c_int32, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
                               c_void_p, c_uint64, c_int64, c_int64, c_int32, c_void_p, c_void_p]),
+    "spa_loglik_partials": (c_int, [POINTER(SpaDesign), c_void_p, c_int64, c_void_p, c_size_t, c_void_p]),
+    "spa_rw_accept_k1": (c_int, [c_void_p, c_int32, c_void_p, c_int32, c_int64, POINTER(SpaDesign), c_void_p,
+                                 c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_int64, c_int64,
+                                 c_int32, c_void_p, c_void_p]),
 }
 
 _lib = None
@@ -151,7 +155,7 @@ KERNELS_PER_CALL = {
     "spa_prior_rows": 1, "spa_prior_reweight": 1, "spa_lse_chunk_stats": 1, "spa_lse_combine": 1, "spa_logw_apply": 1,
     "spa_systematic_ancestors": 4, "spa_exact_cumsum": 3, "spa_gather_rows": 1, "spa_mwg_move": 1, "spa_mwg_chain_slots": 1, "spa_rw_moments": 1,
     "spa_rw_factor": 0, "spa_mwg_resident_chains": 0, "spa_mwg_set_rounds": 0, "spa_mwg_set_tables": 0, "spa_step_record": 1, "spa_resample_gated": 6, "spa_resample_sharded": 5, "spa_resample_commit": 1, "spa_summary_pass": 1, "spa_summary_select": 1,
-    "spa_summary_finish": 1, "spa_em_map": 1, "spa_rw_propose": 2, "spa_rw_increments": 1, "spa_rw_pack": 1, "spa_rw_normals": 1, "spa_rw_accept": 1, "spa_tc_gemm_f32": 1,
+    "spa_summary_finish": 1, "spa_em_map": 1, "spa_rw_propose": 2, "spa_rw_increments": 1, "spa_rw_pack": 1, "spa_rw_normals": 1, "spa_rw_accept": 1, "spa_loglik_partials": 1, "spa_rw_accept_k1": 1, "spa_tc_gemm_f32": 1,
 }
 launch_count = 0
 

@@ -2029,11 +2029,15 @@ __global__ void __launch_bounds__(256) rw_center_kernel(const float* __restrict_
 
 constexpr int kAcceptThreads = 128;  // 4 warps x 32 particles: all blocks resident in one wave
 
-template <int kR>
+struct SpArray {  // the softplus sums as an array (spa_loglik_softplus)
+  const double* sp;
+  __device__ __forceinline__ double softplus_sum(int64_t k) const { return sp[k]; }
+};
+
+template <int kR, class SP>
 __global__ void __launch_bounds__(kAcceptThreads) rw_accept_kernel(float* __restrict__ beta, int ldb,
                                                          const __nv_bfloat16* __restrict__ eps, int q, int64_t m,
-                                                         const double* __restrict__ ylin_p,
-                                                         const double* __restrict__ sp_p,
+                                                         const double* __restrict__ ylin_p, const SP sp,
                                                          const double* __restrict__ lp_p, double* __restrict__ ll,
                                                          double* __restrict__ lp, uint64_t seed, int64_t t, int64_t i0,
                                                          int move, unsigned long long* accepted) {
@@ -2050,7 +2054,7 @@ __global__ void __launch_bounds__(kAcceptThreads) rw_accept_kernel(float* __rest
     uint32_t w[4] = {0xFFFFFFFFu, (uint32_t)(i0 + row), (uint32_t)t, (uint32_t)move | (3u << 24)};
     philox4x32_10(w, (uint32_t)seed, (uint32_t)(seed >> 32));
     const double u = (double)(((uint64_t)w[0] << 21) | (w[1] >> 11)) * 0x1.0p-53;
-    const double llp = ylin_p[row] - sp_p[row];
+    const double llp = ylin_p[row] - sp.softplus_sum(row);
     const double lpp = lp_p[row];
     const double d = (llp + lpp) - (ll[row] + lp[row]);
     ok = (d >= 0.0) || (log(u) < d);
@@ -2249,21 +2253,23 @@ __global__ void reduce_k1_slots_kernel(const double* __restrict__ partial, int64
   out[k] = ylin ? ylin[k] - s : s;
 }
 
-static int loglik_i8(const spa_design* d, const void* A, int64_t m, const double* ylin, double* out, void* ws,
-                     cudaStream_t st) {
-  const bool res = k1_i8_resident(d->kp);
-  CUtensorMap ta, tb;
-  int rc = make_tmap_u8(&ta, A, 3ull * d->kp, (uint64_t)m);
-  if (rc) return rc;
-  rc = make_tmap_u8(&tb, d->gemm_b, 2ull * d->kp, (uint64_t)d->n, kI8PairB);
-  if (rc) return rc;
+// How the int8 K1 launch for (design, m) lays out its partial row sums: the
+// schedule, and the (slot) count per row the reductions add up in fixed order.
+struct K1Plan {
   K1I8Args args;
+  bool res;
+  int sched, U, nclus;
+};
+
+static int k1_i8_plan(const spa_design* d, const void* A, int64_t m, void* ws, K1Plan& pl) {
+  pl.res = k1_i8_resident(d->kp);
+  K1I8Args& args = pl.args;
   args.m_tiles = (int)((m + 255) / 256);
   args.n_tiles = (d->n + kI8BN - 1) / kI8BN;
   args.m = (int)m;
   args.n = d->n;
   args.kp = d->kp;
-  args.stages = res ? k1_i8_pair_stages(d->kp) : kI8PairStreamStages;
+  args.stages = pl.res ? k1_i8_pair_stages(d->kp) : kI8PairStreamStages;
   args.rowc = k1_rowc(const_cast<void*>(A), m, d->kp);
   args.partial = reinterpret_cast<double*>(ws);
   static int sms = 0;
@@ -2282,38 +2288,82 @@ static int loglik_i8(const spa_design* d, const void* A, int64_t m, const double
     const char* e = getenv("SPA_K1_SCHED");
     return e ? atoi(e) : -1;
   }();
-  const int sched = (forced >= 0 && forced <= 2) ? forced : (res ? 0 : 1);
-  args.sched = sched;
-  loglik_split(m, d->n, args.m_tiles, args.n_tiles, args.tpu, args.units, kI8BN, res ? 0.3 : 0.1, 256, 74);
-  const int U = args.m_tiles * (sched == 0 ? args.n_tiles : args.units);  // < 2^31: m < 2^31, n_tiles <= 128
-  const int nclus = std::min(U, std::min(kI8MaxPairs, sms / 2));
-  {
-    const int grid = 2 * nclus;
-    if (res) {
-      const int smem = k1_i8_pair_smem(d->kp);
-      static int attr = 0;  // largest size set so far
-      if (smem > attr) {
-        SPA_CHECK_CUDA(
-            cudaFuncSetAttribute(k1_i8_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = smem;
-      }
-      k1_i8_pair_kernel<true><<<grid, kI8Threads, smem, st>>>(ta, tb, args);
-    } else {
-      static bool attr_done = false;
-      if (!attr_done) {
-        SPA_CHECK_CUDA(cudaFuncSetAttribute(k1_i8_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            kI8PairStreamSmem));
-        attr_done = true;
-      }
-      k1_i8_pair_kernel<false><<<grid, kI8Threads, kI8PairStreamSmem, st>>>(ta, tb, args);
+  pl.sched = (forced >= 0 && forced <= 2) ? forced : (pl.res ? 0 : 1);
+  args.sched = pl.sched;
+  loglik_split(m, d->n, args.m_tiles, args.n_tiles, args.tpu, args.units, kI8BN, pl.res ? 0.3 : 0.1, 256, 74);
+  pl.U = args.m_tiles * (pl.sched == 0 ? args.n_tiles : args.units);  // < 2^31: m < 2^31, n_tiles <= 128
+  pl.nclus = std::min(pl.U, std::min(kI8MaxPairs, sms / 2));
+  return 0;
+}
+
+// the K1 kernel alone: partial row sums in ws (see K1Plan)
+static int k1_i8_launch(const spa_design* d, const void* A, int64_t m, const K1Plan& pl, cudaStream_t st) {
+  CUtensorMap ta, tb;
+  int rc = make_tmap_u8(&ta, A, 3ull * d->kp, (uint64_t)m);
+  if (rc) return rc;
+  rc = make_tmap_u8(&tb, d->gemm_b, 2ull * d->kp, (uint64_t)d->n, kI8PairB);
+  if (rc) return rc;
+  const int grid = 2 * pl.nclus;
+  if (pl.res) {
+    const int smem = k1_i8_pair_smem(d->kp);
+    static int attr = 0;  // largest size set so far
+    if (smem > attr) {
+      SPA_CHECK_CUDA(cudaFuncSetAttribute(k1_i8_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr = smem;
     }
+    k1_i8_pair_kernel<true><<<grid, kI8Threads, smem, st>>>(ta, tb, pl.args);
+  } else {
+    static bool attr_done = false;
+    if (!attr_done) {
+      SPA_CHECK_CUDA(cudaFuncSetAttribute(k1_i8_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          kI8PairStreamSmem));
+      attr_done = true;
+    }
+    k1_i8_pair_kernel<false><<<grid, kI8Threads, kI8PairStreamSmem, st>>>(ta, tb, pl.args);
   }
   SPA_CHECK_LAUNCH();
-  if (sched == 0)
-    reduce_k1_slots_kernel<<<cdiv(m, 256), 256, 0, st>>>(reinterpret_cast<double*>(ws), m, args.n_tiles, U, nclus,
-                                                         ylin, out, k1_half(const_cast<void*>(A), m, d->kp));
+  return 0;
+}
+
+// The row reduction of a K1Plan's partial sums (the order of the reduction
+// kernels below), for kernels that consume the log-likelihood directly.
+struct K1Reduce {
+  const double* partial;
+  const double* hh;
+  int64_t m;
+  int sched, n_tiles, U, nclus, units;
+  __device__ __forceinline__ double softplus_sum(int64_t k) const {
+    const int n = kI8EpiGroups * (sched == 0 ? k1_slots_of((int)(k >> 8), n_tiles, U, nclus) : units);
+    double s = 0.0;
+    for (int u = 0; u < n; ++u) s += partial[(size_t)u * m + k];
+    return s + hh[k];
+  }
+};
+static K1Reduce k1_reduce_of(const spa_design* d, const void* A, int64_t m, const void* ws, const K1Plan& pl) {
+  K1Reduce r;
+  r.partial = reinterpret_cast<const double*>(ws);
+  r.hh = k1_half(const_cast<void*>(A), m, d->kp);
+  r.m = m;
+  r.sched = pl.sched;
+  r.n_tiles = pl.args.n_tiles;
+  r.U = pl.U;
+  r.nclus = pl.nclus;
+  r.units = pl.args.units;
+  return r;
+}
+
+static int loglik_i8(const spa_design* d, const void* A, int64_t m, const double* ylin, double* out, void* ws,
+                     cudaStream_t st) {
+  K1Plan pl;
+  int rc = k1_i8_plan(d, A, m, ws, pl);
+  if (rc) return rc;
+  rc = k1_i8_launch(d, A, m, pl, st);
+  if (rc) return rc;
+  if (pl.sched == 0)
+    reduce_k1_slots_kernel<<<cdiv(m, 256), 256, 0, st>>>(reinterpret_cast<double*>(ws), m, pl.args.n_tiles, pl.U,
+                                                         pl.nclus, ylin, out, k1_half(const_cast<void*>(A), m, d->kp));
   else
-    reduce_units_kernel<<<cdiv(m, 256), 256, 0, st>>>(reinterpret_cast<double*>(ws), kI8EpiGroups * args.units, m,
+    reduce_units_kernel<<<cdiv(m, 256), 256, 0, st>>>(reinterpret_cast<double*>(ws), kI8EpiGroups * pl.args.units, m,
                                                       ylin, out, k1_half(const_cast<void*>(A), m, d->kp));
   SPA_CHECK_LAUNCH();
   return 0;
@@ -2886,7 +2936,7 @@ int spa_prepare(void) {
       (const void*)peer_gather_kernel,
       (const void*)reduce_units_kernel, (const void*)rw_mean_kernel<4>, (const void*)rw_cov_kernel,
       (const void*)rw_chol_panel_kernel, (const void*)rw_emit_kernel,
-      (const void*)rw_normals_kernel, (const void*)rw_center_kernel, (const void*)rw_accept_kernel<2>,
+      (const void*)rw_normals_kernel, (const void*)rw_center_kernel, (const void*)rw_accept_kernel<2, SpArray>, (const void*)rw_accept_kernel<2, K1Reduce>,
       (const void*)syrk_reduce_kernel, (const void*)summary_hist_kernel, (const void*)summary_select_kernel,
       (const void*)summary_finish_kernel};
   for (const void* f : fns) {
@@ -2968,10 +3018,37 @@ int spa_rw_accept(float* beta, int32_t ldb, const void* eps, int32_t q, int64_t 
                   int64_t i0, int32_t move, unsigned long long* accepted, void* stream) {
   SPA_REQUIRE(beta && eps && ylin_p && sp_p && lp_p && ll && lp && accepted && m > 0, kBadArgument,
               "spa_rw_accept: bad arguments");
-  rw_accept_kernel<2><<<cdiv(m, kAcceptThreads), kAcceptThreads, 0, as_stream(stream)>>>(
-      beta, ldb, reinterpret_cast<const __nv_bfloat16*>(eps),
-                                                               q, m, ylin_p, sp_p, lp_p, ll, lp, seed, t, i0, move,
-                                                               accepted);
+  rw_accept_kernel<2, SpArray><<<cdiv(m, kAcceptThreads), kAcceptThreads, 0, as_stream(stream)>>>(
+      beta, ldb, reinterpret_cast<const __nv_bfloat16*>(eps), q, m, ylin_p, SpArray{sp_p}, lp_p, ll, lp, seed, t, i0,
+      move, accepted);
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+int spa_loglik_partials(const spa_design* d, const void* A, int64_t m, void* ws, size_t ws_bytes, void* stream) {
+  SPA_REQUIRE(d && A && ws && m > 0 && m < (1ll << 31), kBadArgument, "spa_loglik_partials: bad arguments");
+  SPA_REQUIRE(d->coded && d->kp <= 1024, kNotSupported, "spa_loglik_partials: integer-coded designs only");
+  SPA_REQUIRE(ws_bytes >= spa_loglik_workspace_bytes(m, d->n), kWorkspaceTooSmall,
+              "spa_loglik_partials: workspace too small");
+  K1Plan pl;
+  int rc = k1_i8_plan(d, A, m, ws, pl);
+  if (rc) return rc;
+  return k1_i8_launch(d, A, m, pl, as_stream(stream));
+}
+
+int spa_rw_accept_k1(float* beta, int32_t ldb, const void* eps, int32_t q, int64_t m, const spa_design* d,
+                     const void* A, const double* ylin_p, const void* ws, const double* lp_p, double* ll, double* lp,
+                     uint64_t seed, int64_t t, int64_t i0, int32_t move, unsigned long long* accepted, void* stream) {
+  SPA_REQUIRE(beta && eps && d && A && ylin_p && ws && lp_p && ll && lp && accepted && m > 0, kBadArgument,
+              "spa_rw_accept_k1: bad arguments");
+  SPA_REQUIRE(d->coded && d->kp <= 1024, kNotSupported, "spa_rw_accept_k1: integer-coded designs only");
+  K1Plan pl;
+  int rc = k1_i8_plan(d, A, m, const_cast<void*>(ws), pl);
+  if (rc) return rc;
+  const K1Reduce red = k1_reduce_of(d, A, m, ws, pl);
+  rw_accept_kernel<2, K1Reduce><<<cdiv(m, kAcceptThreads), kAcceptThreads, 0, as_stream(stream)>>>(
+      beta, ldb, reinterpret_cast<const __nv_bfloat16*>(eps), q, m, ylin_p, red, lp_p, ll, lp, seed, t, i0, move,
+      accepted);
   SPA_CHECK_LAUNCH();
   return 0;
 }

@@ -676,17 +676,28 @@ def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int,
             pend = system._z_pending = getattr(system, "_z_pending", None) or {}
             if _normals_key(system, config, t, 1) not in pend:
                 pend[_normals_key(system, config, t, 1)] = _launch_normals(system, config, t, 1)
+        fused = d.coded  # K1 without its row reduction; the accept sums the partial rows itself
         if KERNEL_TIMER is not None:
             KERNEL_TIMER.start("loglik")
-        _lib.call("spa_loglik_softplus", ctypes.byref(d.struct), _p(ws["A"]), system.N, _p(ws["sp"]), _p(ws["ws"]),
-                  ws["ws"].numel(), _stream())
+        if fused:
+            _lib.call("spa_loglik_partials", ctypes.byref(d.struct), _p(ws["A"]), system.N, _p(ws["ws"]),
+                      ws["ws"].numel(), _stream())
+        else:
+            _lib.call("spa_loglik_softplus", ctypes.byref(d.struct), _p(ws["A"]), system.N, _p(ws["sp"]),
+                      _p(ws["ws"]), ws["ws"].numel(), _stream())
         if KERNEL_TIMER is not None:
             KERNEL_TIMER.stop("loglik")
         if lag and mv == 0:
             main.wait_event(centred)  # the factor stream has read the particles
-        _lib.call("spa_rw_accept", _p(system.beta), system.ldb, _p(rw["prop"]), system.q, system.N, _p(ws["ylin"]),
-                  _p(ws["sp"]), _p(rw["lp_p"]), _p(system.ll), _p(system.lp), int(config.seed), int(t),
-                  int(system.i0), mv, _p(system.counter), _stream())
+        if fused:
+            _lib.call("spa_rw_accept_k1", _p(system.beta), system.ldb, _p(rw["prop"]), system.q, system.N,
+                      ctypes.byref(d.struct), _p(ws["A"]), _p(ws["ylin"]), _p(ws["ws"]), _p(rw["lp_p"]),
+                      _p(system.ll), _p(system.lp), int(config.seed), int(t), int(system.i0), mv,
+                      _p(system.counter), _stream())
+        else:
+            _lib.call("spa_rw_accept", _p(system.beta), system.ldb, _p(rw["prop"]), system.q, system.N,
+                      _p(ws["ylin"]), _p(ws["sp"]), _p(rw["lp_p"]), _p(system.ll), _p(system.lp), int(config.seed),
+                      int(t), int(system.i0), mv, _p(system.counter), _stream())
         _normals_ahead(system, config, t, mv)
     if lag == 2:
         system._factored = factored

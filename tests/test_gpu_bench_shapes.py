@@ -251,3 +251,44 @@ def test_device_decided_resampling_every_step_large_n(small_data, kernel):
     assert torch.equal(s1.beta[:, :q], s2.beta[:, :q])
     for name in ("logw", "ll", "lp"):
         assert torch.equal(getattr(s1, name), getattr(s2, name)), name
+
+
+@pytest.mark.parametrize("name,N", [("c3", 65536), ("c5", 131072), ("c2", 8192 + 77)])
+def test_accept_reducing_k1_partials_matches_two_step_path(name, N):
+    """spa_loglik_partials + spa_rw_accept_k1 (the accept sums K1's partial
+    rows itself) against spa_loglik_softplus + spa_rw_accept, bit for bit:
+    the resident (contiguous ranges) and streamed (C5, round-robin items) K1
+    schedules and a ragged N."""
+    from paper_1106_0322_b200.smc import _rw_factor
+
+    data, d, s = random_system(name, N, seed=3)
+    s.log_weights = np.full(s.N, -math.log(s.N))
+    _rw_factor(s, 2.38)
+    rw, ws = s.rw_workspace(), s.ll_workspace()
+    _lib.call("spa_loglik_rows", ctypes.byref(d.struct), _p(s.beta), s.N, s.ldb, _p(ws["A"]), _p(ws["ylin"]),
+              _p(s.ll), _p(ws["ws"]), ws["ws"].numel(), _stream())
+    _lib.call("spa_prior_rows", ctypes.byref(d.struct), _p(s.beta), s.N, s.ldb, 1.0, 0.9, 0.9, 2, _p(s.lp), _stream())
+    zb = s.z_buffers(1)[0]
+    _lib.call("spa_rw_normals", s.N, s.q, 3, 5, 0, 1, _p(zb), _stream())
+    _lib.call("spa_rw_propose", ctypes.byref(d.struct), _p(s.beta), s.N, s.ldb, s.factor_operand(), 3, 5, 0, 1,
+              _p(zb), _p(rw["prop"]), _p(ws["A"]), _p(ws["ylin"]), 1.0, 0.9, _p(rw["lp_p"]), _stream())
+    outs = []
+    for fused in (False, True):
+        beta, ll, lp = s.beta.clone(), s.ll.clone(), s.lp.clone()
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        if fused:
+            _lib.call("spa_loglik_partials", ctypes.byref(d.struct), _p(ws["A"]), s.N, _p(ws["ws"]),
+                      ws["ws"].numel(), _stream())
+            _lib.call("spa_rw_accept_k1", _p(beta), s.ldb, _p(rw["prop"]), s.q, s.N, ctypes.byref(d.struct),
+                      _p(ws["A"]), _p(ws["ylin"]), _p(ws["ws"]), _p(rw["lp_p"]), _p(ll), _p(lp), 3, 5, 0, 1, _p(cnt),
+                      _stream())
+        else:
+            _lib.call("spa_loglik_softplus", ctypes.byref(d.struct), _p(ws["A"]), s.N, _p(ws["sp"]), _p(ws["ws"]),
+                      ws["ws"].numel(), _stream())
+            _lib.call("spa_rw_accept", _p(beta), s.ldb, _p(rw["prop"]), s.q, s.N, _p(ws["ylin"]), _p(ws["sp"]),
+                      _p(rw["lp_p"]), _p(ll), _p(lp), 3, 5, 0, 1, _p(cnt), _stream())
+        outs.append((beta, ll, lp, cnt))
+    torch.cuda.synchronize()
+    assert 0 < int(outs[0][3].item()) < s.N
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
