@@ -163,6 +163,15 @@ int spa_gather_rows(const float* src, int32_t ld_src, float* dst, int32_t ld_dst
  * kernel returning immediately when *gate (rec[t][2]) is 0.  w = normalised
  * weights, u = the step's uniform / N. */
 int spa_step_record(const double* res, double* rec, int64_t t, double ess_threshold, void* stream);
+/* The weight update of an unsharded device-decided lambda step in one
+ * cooperative launch: spa_lse_chunk_stats(logw, lw) -> spa_lse_combine ->
+ * spa_step_record(t) -> spa_logw_apply(logw, lw) -> the statistics and
+ * combine of the new logw -> w = exp(logw - lse) (stats / res end as after
+ * that last combine); bit-identical to those calls (reference smc.py:151-157,
+ * 171-174, 248-262).  m <= spa_reweight_finish_max_particles(). */
+int spa_reweight_finish(double* logw, const double* lw, int64_t m, double* stats, double* res, double* rec, int64_t t,
+                        double ess_threshold, double* w, void* stream);
+int spa_reweight_finish_max_particles(void);
 int spa_resample_gated(const double* gate, const double* w, int64_t N, double u, float* beta, float* beta_alt,
                        int32_t ldb, int32_t q, double* ll, double* ll_alt, double* lp, double* lp_alt, double* logw,
                        int64_t* anc, void* ws, size_t ws_bytes, void* stream);

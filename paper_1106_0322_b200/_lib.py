@@ -84,6 +84,9 @@ _SIGNATURES = {
                            c_double, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "spa_prepare": (c_int, []),
     "spa_step_record": (c_int, [c_void_p, c_void_p, c_int64, c_double, c_void_p]),
+    "spa_reweight_finish": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int64, c_double,
+                                    c_void_p, c_void_p]),
+    "spa_reweight_finish_max_particles": (c_int, []),
     "spa_resample_gated": (c_int, [c_void_p, c_void_p, c_int64, c_double, c_void_p, c_void_p, c_int32, c_int32,
                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
                                    c_void_p]),
@@ -154,7 +157,7 @@ KERNELS_PER_CALL = {
     "spa_philox_blocks": 1, "spa_loglik_softplus": 2, "spa_pack_particles": 1, "spa_loglik_rows": 3,
     "spa_prior_rows": 1, "spa_prior_reweight": 1, "spa_lse_chunk_stats": 1, "spa_lse_combine": 1, "spa_logw_apply": 1,
     "spa_systematic_ancestors": 4, "spa_exact_cumsum": 3, "spa_gather_rows": 1, "spa_mwg_move": 1, "spa_mwg_chain_slots": 1, "spa_rw_moments": 1,
-    "spa_rw_factor": 0, "spa_mwg_resident_chains": 0, "spa_mwg_set_rounds": 0, "spa_mwg_set_tables": 0, "spa_step_record": 1, "spa_resample_gated": 6, "spa_resample_sharded": 5, "spa_resample_commit": 1, "spa_summary_pass": 1, "spa_summary_select": 1,
+    "spa_rw_factor": 0, "spa_mwg_resident_chains": 0, "spa_mwg_set_rounds": 0, "spa_mwg_set_tables": 0, "spa_step_record": 1, "spa_reweight_finish": 1, "spa_reweight_finish_max_particles": 0, "spa_resample_gated": 6, "spa_resample_sharded": 5, "spa_resample_commit": 1, "spa_summary_pass": 1, "spa_summary_select": 1,
     "spa_summary_finish": 1, "spa_em_map": 1, "spa_rw_propose": 2, "spa_rw_increments": 1, "spa_rw_pack": 1, "spa_rw_normals": 1, "spa_rw_accept": 1, "spa_loglik_partials": 1, "spa_rw_accept_k1": 1, "spa_tc_gemm_f32": 1,
 }
 launch_count = 0

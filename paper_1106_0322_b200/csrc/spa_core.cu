@@ -7,6 +7,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <cooperative_groups.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -1348,12 +1349,10 @@ __device__ __forceinline__ double block_reduce_1024(double v, double* red, bool 
   return v;
 }
 
-__global__ void __launch_bounds__(kLseThreads) lse_stats_kernel(const double* __restrict__ logw,
-                                                                const double* __restrict__ lw, int64_t m,
-                                                                double* __restrict__ stats) {
-  __shared__ double red[32];
+__device__ __forceinline__ void lse_chunk_stats(const double* __restrict__ logw, const double* __restrict__ lw,
+                                                int64_t m, double* __restrict__ stats, int64_t chunk, double* red) {
   constexpr int kPer = kChunk / kLseThreads;
-  const int64_t c0 = (int64_t)blockIdx.x * kChunk;
+  const int64_t c0 = chunk * kChunk;
   double x[kPer];
   double mx = -INFINITY;
   bool nan = false;
@@ -1378,34 +1377,48 @@ __global__ void __launch_bounds__(kLseThreads) lse_stats_kernel(const double* __
   s1 = block_reduce_1024(s1, red, false);
   s2 = block_reduce_1024(s2, red, false);
   if (threadIdx.x == 0) {
-    stats[3 * blockIdx.x + 0] = nan ? NAN : mx;
-    stats[3 * blockIdx.x + 1] = s1;
-    stats[3 * blockIdx.x + 2] = s2;
+    stats[3 * chunk + 0] = nan ? NAN : mx;
+    stats[3 * chunk + 1] = s1;
+    stats[3 * chunk + 2] = s2;
   }
 }
 
-__global__ void lse_combine_kernel(const double* __restrict__ stats, int64_t nchunks, double* __restrict__ res) {
-  if (threadIdx.x != 0) return;
+__global__ void __launch_bounds__(kLseThreads) lse_stats_kernel(const double* __restrict__ logw,
+                                                                const double* __restrict__ lw, int64_t m,
+                                                                double* __restrict__ stats) {
+  __shared__ double red[32];
+  lse_chunk_stats(logw, lw, m, stats, blockIdx.x, red);
+}
+
+// one thread: the fixed-order combine of the chunk statistics (L2 loads: in
+// reweight_finish_kernel other blocks wrote them, and L1 is not coherent)
+__device__ __forceinline__ void lse_combine_body(const double* __restrict__ stats, int64_t nchunks,
+                                                 double* __restrict__ res) {
   double M = -INFINITY;
   bool nan = false;
   for (int64_t c = 0; c < nchunks; ++c) {
-    const double v = stats[3 * c];
+    const double v = __ldcg(&stats[3 * c]);
     if (v != v) nan = true;
     M = fmax(M, v);
   }
   double s1 = 0.0, s2 = 0.0;
   if (M > -INFINITY && !nan) {
     for (int64_t c = 0; c < nchunks; ++c) {
-      const double mc = stats[3 * c];
+      const double mc = __ldcg(&stats[3 * c]);
       if (mc == -INFINITY) continue;
       const double f = exp(mc - M);
-      s1 += stats[3 * c + 1] * f;
-      s2 += stats[3 * c + 2] * f * f;
+      s1 += __ldcg(&stats[3 * c + 1]) * f;
+      s2 += __ldcg(&stats[3 * c + 2]) * f * f;
     }
   }
   res[0] = nan ? NAN : (M > -INFINITY ? M + log(s1) : -INFINITY);
   res[1] = nan ? NAN : s1 * s1 / s2;
   res[2] = M;
+}
+
+__global__ void lse_combine_kernel(const double* __restrict__ stats, int64_t nchunks, double* __restrict__ res) {
+  if (threadIdx.x != 0) return;
+  lse_combine_body(stats, nchunks, res);
 }
 
 __global__ void logw_apply_kernel(double* __restrict__ logw, const double* __restrict__ lw, int64_t m,
@@ -1501,14 +1514,61 @@ __global__ void gather_kernel(const float* __restrict__ src, int ld_src, float* 
 // Step record (device-decided resampling): rec[t] = {inc, ESS, resampled,
 // log Z_t/Z_1}, the running log-evidence accumulated in step order (the same
 // float64 additions as the host loop).
-__global__ void step_record_kernel(const double* __restrict__ res, double* __restrict__ rec, int64_t t,
-                                   double ess_threshold) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ __forceinline__ void step_record_body(const double* __restrict__ res, double* __restrict__ rec, int64_t t,
+                                                 double ess_threshold) {
   const double inc = res[0], e = res[1];
   rec[4 * t + 0] = inc;
   rec[4 * t + 1] = e;
   rec[4 * t + 2] = (e < ess_threshold) ? 1.0 : 0.0;
   rec[4 * t + 3] = rec[4 * (t - 1) + 3] + inc;
+}
+
+__global__ void step_record_kernel(const double* __restrict__ res, double* __restrict__ rec, int64_t t,
+                                   double ess_threshold) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  step_record_body(res, rec, t, ess_threshold);
+}
+
+// The whole weight update of an unsharded lambda step in one cooperative
+// launch (one 1024-thread block per 4096-particle chunk): the chunk
+// statistics of logw + lw, their combine (log Z_t / Z_t-1, ESS) and the step
+// record, logw <- logw + lw - lse, the statistics of the new logw, their
+// combine and the normalised weights w = exp(logw - lse) -- the arithmetic of
+// lse_stats / lse_combine / logw_apply / step_record / logw_apply(w), in the
+// same order (bit-identical), with grid barriers instead of seven launches.
+__global__ void __launch_bounds__(kLseThreads) reweight_finish_kernel(double* logw, const double* __restrict__ lw,
+                                                                      int64_t m, double* stats, int64_t nchunks,
+                                                                      double* res, double* rec, int64_t t,
+                                                                      double ess_threshold, double* __restrict__ w) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[32];
+  const int64_t c = blockIdx.x;
+  lse_chunk_stats(logw, lw, m, stats, c, red);
+  grid.sync();
+  if (c == 0 && threadIdx.x == 0) {
+    lse_combine_body(stats, nchunks, res);
+    step_record_body(res, rec, t, ess_threshold);
+  }
+  grid.sync();
+  constexpr int kPer = kChunk / kLseThreads;
+  const double r0 = __ldcg(&res[0]);  // written by block 0 (L2: L1 is not coherent across SMs)
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int64_t k = c * kChunk + threadIdx.x + i * kLseThreads;
+    if (k < m) logw[k] = logw[k] + lw[k] - r0;
+  }
+  __syncthreads();
+  lse_chunk_stats(logw, nullptr, m, stats, c, red);  // this block's own updated chunk
+  grid.sync();
+  if (c == 0 && threadIdx.x == 0) lse_combine_body(stats, nchunks, res);
+  grid.sync();
+  const double r1 = __ldcg(&res[0]);
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int64_t k = c * kChunk + threadIdx.x + i * kLseThreads;
+    if (k < m) w[k] = exp(logw[k] - r1);
+  }
 }
 
 // Gated copy-back of the gathered rows (alt -> main) and log-weight reset to
@@ -2626,6 +2686,36 @@ int spa_gather_rows(const float* src, int32_t ld_src, float* dst, int32_t ld_dst
                                                           v1_out, nullptr);
   SPA_CHECK_LAUNCH();
   return 0;
+}
+
+int spa_reweight_finish(double* logw, const double* lw, int64_t m, double* stats, double* res, double* rec, int64_t t,
+                        double ess_threshold, double* w, void* stream) {
+  SPA_REQUIRE(logw && lw && stats && res && rec && w && m > 0 && t >= 1, kBadArgument,
+              "spa_reweight_finish: bad arguments");
+  const int64_t nchunks = cdiv(m, kChunk);
+  static int max_blocks = 0;
+  if (max_blocks == 0) {
+    int dev = 0, nsm = 0, per_sm = 0;
+    SPA_CHECK_CUDA(cudaGetDevice(&dev));
+    SPA_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    SPA_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reweight_finish_kernel, kLseThreads, 0));
+    max_blocks = std::max(1, per_sm * nsm);
+  }
+  SPA_REQUIRE(nchunks <= max_blocks, kNotSupported, "spa_reweight_finish: more chunks than co-resident blocks");
+  void* args[] = {&logw, (void*)&lw, &m, &stats, (void*)&nchunks, &res, &rec, &t, &ess_threshold, &w};
+  SPA_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)reweight_finish_kernel, dim3((unsigned)nchunks),
+                                             dim3(kLseThreads), args, 0, as_stream(stream)));
+  SPA_CHECK_LAUNCH();
+  return 0;
+}
+
+int spa_reweight_finish_max_particles(void) {
+  int dev = 0, nsm = 0, per_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reweight_finish_kernel, kLseThreads, 0) != cudaSuccess)
+    return 0;
+  return per_sm * nsm * kChunk;
 }
 
 int spa_step_record(const double* res, double* rec, int64_t t, double ess_threshold, void* stream) {

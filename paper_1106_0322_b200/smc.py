@@ -382,6 +382,17 @@ class ParticleSystem:
         return self._fstream
 
 
+_REWEIGHT_FINISH_LIMIT = None
+
+
+def _reweight_finish_limit() -> int:
+    """Particles spa_reweight_finish handles (its chunks must be co-resident)."""
+    global _REWEIGHT_FINISH_LIMIT
+    if _REWEIGHT_FINISH_LIMIT is None:
+        _REWEIGHT_FINISH_LIMIT = int(_lib.load().spa_reweight_finish_max_particles())
+    return _REWEIGHT_FINISH_LIMIT
+
+
 def _lse(system: ParticleSystem, lw):
     _lib.call("spa_lse_chunk_stats", _p(system.logw), _p(lw), system.N, _p(system.stats), _stream())
     _lib.call("spa_lse_combine", _p(system.stats), system.nchunks, _p(system.res), _stream())
@@ -927,17 +938,22 @@ def _smc_step_async(system: ParticleSystem, schedule: Schedule, t: int, config: 
     _nvtx_push("reweight")
     _lib.call("spa_prior_reweight", ctypes.byref(d.struct), _p(system.beta), system.N, system.ldb,
               float(prior_t.a), float(prior_t.c), float(prior_prev.c), _p(system.lw), _p(system.lp), _stream())
-    _lib.call("spa_lse_chunk_stats", _p(system.logw), _p(system.lw), system.N, _p(system.stats), _stream())
-    stats = system.stats if group is None else group.all_gather_cat(system.stats)
-    _lib.call("spa_lse_combine", _p(stats), stats.shape[0], _p(system.res), _stream())
-    _lib.call("spa_logw_apply", _p(system.logw), _p(system.lw), system.N, _p(system.res), None, _stream())
-    _lib.call("spa_step_record", _p(system.res), _p(rec), t, float(config.ess_threshold_frac * N), _stream())
+    fused = group is None and system.N <= _reweight_finish_limit()
+    if fused:  # the weight update, step record and normalised weights in one cooperative launch
+        _lib.call("spa_reweight_finish", _p(system.logw), _p(system.lw), system.N, _p(system.stats), _p(system.res),
+                  _p(rec), t, float(config.ess_threshold_frac * N), _p(system.w), _stream())
+    else:
+        _lib.call("spa_lse_chunk_stats", _p(system.logw), _p(system.lw), system.N, _p(system.stats), _stream())
+        stats = system.stats if group is None else group.all_gather_cat(system.stats)
+        _lib.call("spa_lse_combine", _p(stats), stats.shape[0], _p(system.res), _stream())
+        _lib.call("spa_logw_apply", _p(system.logw), _p(system.lw), system.N, _p(system.res), None, _stream())
+        _lib.call("spa_step_record", _p(system.res), _p(rec), t, float(config.ess_threshold_frac * N), _stream())
     _nvtx_pop()
     _nvtx_push("resample")
     u = first_uniform(config.seed, TAG_RESAMPLE, t) / N
     gate = ctypes.c_void_p(rec.data_ptr() + (4 * t + 2) * 8)
     if group is None:
-        w = system.device_weights()
+        w = system.w if fused else system.device_weights()
         _lib.call("spa_resample_gated", gate, _p(w), system.N, u, _p(system.beta), _p(system.beta_alt), system.ldb,
                   system.q, _p(system.ll), _p(system.ll_alt), _p(system.lp), _p(system.lp_alt), _p(system.logw),
                   _p(anc), _p(ws), ws.numel(), _stream())

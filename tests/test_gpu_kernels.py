@@ -612,3 +612,42 @@ def test_code_columns_on_device_match_host():
         assert (h is None) == (d is None)
         if h is not None:
             assert np.array_equal(h[0], d[0]) and h[1] == d[1] and h[2] == d[2] and np.array_equal(h[3], d[3])
+
+
+@pytest.mark.parametrize("m", [1000, 8192, 65536 + 77])
+def test_reweight_finish_matches_kernel_sequence(m):
+    """spa_reweight_finish (one cooperative launch) against the sequence it
+    replaces -- chunk statistics of logw + lw, combine, apply, step record,
+    statistics and combine of the new logw, normalised weights -- bit for bit
+    in every output (logw, chunk statistics, lse / ESS, step record, w)."""
+    from paper_1106_0322_b200.smc import _p, _stream
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(m)
+    logw0 = torch.randn(m, device="cuda", dtype=torch.float64, generator=g) * 2
+    lw = torch.randn(m, device="cuda", dtype=torch.float64, generator=g) * 3
+    nch = -(-m // 4096)
+    outs = []
+    for fused in (False, True):
+        logw = logw0.clone()
+        stats = torch.zeros((nch, 3), dtype=torch.float64, device="cuda")
+        res = torch.zeros(3, dtype=torch.float64, device="cuda")
+        rec = torch.zeros((10, 4), dtype=torch.float64, device="cuda")
+        rec[2, 3] = 1.25
+        w = torch.zeros(m, dtype=torch.float64, device="cuda")
+        if fused:
+            _lib.call("spa_reweight_finish", _p(logw), _p(lw), m, _p(stats), _p(res), _p(rec), 3, 0.75 * m, _p(w),
+                      _stream())
+        else:
+            _lib.call("spa_lse_chunk_stats", _p(logw), _p(lw), m, _p(stats), _stream())
+            _lib.call("spa_lse_combine", _p(stats), nch, _p(res), _stream())
+            _lib.call("spa_logw_apply", _p(logw), _p(lw), m, _p(res), None, _stream())
+            _lib.call("spa_step_record", _p(res), _p(rec), 3, 0.75 * m, _stream())
+            _lib.call("spa_lse_chunk_stats", _p(logw), None, m, _p(stats), _stream())
+            _lib.call("spa_lse_combine", _p(stats), nch, _p(res), _stream())
+            _lib.call("spa_logw_apply", _p(logw), None, m, _p(res), _p(w), _stream())
+        outs.append((logw, stats, res, rec, w))
+    torch.cuda.synchronize()
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    assert abs(float(outs[1][4].sum()) - 1.0) < 1e-12
