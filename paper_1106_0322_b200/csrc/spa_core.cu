@@ -283,18 +283,22 @@ __device__ __forceinline__ uint32_t pack_low_bytes(uint32_t a, uint32_t b, uint3
 }
 __device__ __forceinline__ void emit_i8_4(uint8_t* __restrict__ row8, int kp, int j0, const float (&bs)[4],
                                           float inv) {
-  uint32_t Q[4];
+  // rint(bs * inv) through the 1.5 * 2^23 magic constant: the float's low 22
+  // bits are Q mod 2^22 (|bs * inv| <= 2^21 - 1 + 1/4 for a finite row, so no
+  // clamp: a non-finite row has inv = 0 and s = 0, its bytes are never used).
+  // r << 2 puts Q's bits 6..13 in byte 1 and bits 14..21 (hi, two's
+  // complement) in byte 2; lo = the low 6 bits of byte 0.
+  uint32_t r[4], r4[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    // rint(bs * inv) on the FMA/ALU pipes (|bs * inv| <= 2^21: exact
-    // round-to-nearest-even through the 1.5 * 2^23 magic constant)
-    const int q = __float_as_int(fmaf(bs[i], inv, 12582912.0f)) - 0x4B400000;
-    Q[i] = (uint32_t)max(-2097151, min(2097151, q));
+    r[i] = __float_as_uint(fmaf(bs[i], inv, 12582912.0f));
+    r4[i] = r[i] << 2;
   }
-  // hi = bits 14..21 (two's complement: floor(Q / 2^14)), mid = bits 6..13, lo = bits 0..5
-  const uint32_t hi = pack_low_bytes(Q[0] >> 14, Q[1] >> 14, Q[2] >> 14, Q[3] >> 14);
-  const uint32_t mid = pack_low_bytes(Q[0] >> 6, Q[1] >> 6, Q[2] >> 6, Q[3] >> 6);
-  const uint32_t lo = pack_low_bytes(Q[0], Q[1], Q[2], Q[3]) & 0x3F3F3F3Fu;
+  const uint32_t p01 = __byte_perm(r4[0], r4[1], 0x6521);  // {mid0, hi0, mid1, hi1}
+  const uint32_t p23 = __byte_perm(r4[2], r4[3], 0x6521);
+  const uint32_t hi = __byte_perm(p01, p23, 0x7531);
+  const uint32_t mid = __byte_perm(p01, p23, 0x6420);
+  const uint32_t lo = pack_low_bytes(r[0], r[1], r[2], r[3]) & 0x3F3F3F3Fu;
   __stcs(reinterpret_cast<uint32_t*>(row8 + j0), hi);
   __stcs(reinterpret_cast<uint32_t*>(row8 + kp + j0), mid);
   __stcs(reinterpret_cast<uint32_t*>(row8 + 2 * kp + j0), lo);
@@ -324,6 +328,12 @@ __device__ __forceinline__ void emit_row_constants(void* A, int64_t m, int kp, i
   k1_rowc(A, m, kp)[row] = make_float2(ok ? amax / kQMax : 0.f, (float)off);
   k1_half(A, m, kp)[row] = 0.5 * hx;
   if (!ok || !(fabs(off) < 3.0e38)) *ylin_row = __longlong_as_double(0x7ff8000000000000ll);
+}
+// max that propagates NaN (PTX max.NaN): the row maximum flags a NaN / inf row by itself
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
 }
 __device__ __forceinline__ float i8_inv(float amax) { return (amax > 0.f && amax < INFINITY) ? kQMax / amax : 0.f; }
 
@@ -677,15 +687,28 @@ __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
     const float* b = reinterpret_cast<const float*>(ring + s * groupB + rsub * slotB);
     const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(ring + s * groupB + rsub * slotB + rowB);
     double yl = 0.0, off = 0.0, hx = 0.0, prod = 1.0, lin = 0.0;
-    float npen = 0.f, amax = 0.f, nanf = 0.f;  // nanf: sum of bs - bs (NaN iff some bs is NaN / inf)
+    float npen = 0.f, amax = 0.f;  // amax: NaN-propagating, so a NaN / inf row ends non-finite
     float bsr[IT][4];  // alpha * prop, kept for the operand pass
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
+      if (it * LPR * 4 >= d.kp) break;  // kp % (4 LPR) == 0 (host-checked): warp-uniform
       const int j0 = (it * LPR + sub) * 4;
-      if (j0 >= d.kp) break;
       float fy = 0.f, fo = 0.f, fx = 0.f;
       float p[4] = {0.f, 0.f, 0.f, 0.f};
-      if (live) ring_prop4(b, e, j0, d.q, full, p);
+      if (full) {  // q % 4 == 0: the 4 columns are all valid or all padding; selects, no branch
+        const bool v = live && j0 < d.q;
+        const int jj = v ? j0 : 0;
+        const float4 xv = *reinterpret_cast<const float4*>(b + jj);
+        const uint2 ev = *reinterpret_cast<const uint2*>(e + jj);
+        const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&ev);
+        const float2 ya = __bfloat1622float2(y2[0]), yb = __bfloat1622float2(y2[1]);
+        p[0] = v ? xv.x + ya.x : 0.f;
+        p[1] = v ? xv.y + ya.y : 0.f;
+        p[2] = v ? xv.z + yb.x : 0.f;
+        p[3] = v ? xv.w + yb.y : 0.f;
+      } else if (live) {
+        ring_prop4(b, e, j0, d.q, false, p);
+      }
       const float4 va = *reinterpret_cast<const float4*>(ca + j0);
       const float4 vs = *reinterpret_cast<const float4*>(cs + j0);
       const float4 vg = *reinterpret_cast<const float4*>(cg + j0);
@@ -702,8 +725,7 @@ __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
         fo = fmaf(p[i], g4[i], fo);
         if (CODED) fx = fmaf(p[i], x4[i], fx);
         if (CODED) {
-          amax = fmaxf(amax, fabsf(bs));
-          nanf += bs - bs;
+          amax = fmax_nan(amax, fabsf(bs));
         } else if (!(fabsf(bs) < kOpMax)) {
           fy = __int_as_float(0x7fc00000);
         }
@@ -722,11 +744,8 @@ __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
     // row maximum over the row's LPR lanes (aligned groups of the warp)
     if (CODED) {
 #pragma unroll
-      for (int o = LPR / 2; o > 0; o >>= 1) {
-        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-        nanf += __shfl_xor_sync(0xffffffffu, nanf, o);
-      }
-      if (nanf != 0.f) amax = INFINITY;  // NaN / inf in the row
+      for (int o = LPR / 2; o > 0; o >>= 1) amax = fmax_nan(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      if (!(amax < INFINITY)) amax = INFINITY;  // NaN / inf in the row
     }
     double lpl;
     if (pc.de) {
@@ -756,8 +775,8 @@ __global__ void __launch_bounds__(32 * kPackWarps, 2) pack_eps_rows_kernel(
       const float inv = i8_inv(amax);
 #pragma unroll
       for (int it = 0; it < IT; ++it) {
+        if (it * LPR * 4 >= d.kp) break;
         const int j0 = (it * LPR + sub) * 4;
-        if (j0 >= d.kp) break;
         if (CODED)
           emit_i8_4(reinterpret_cast<uint8_t*>(A) + row * 3 * (int64_t)d.kp, d.kp, j0, bsr[it], inv);
         else
