@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
     const float* b = reinterpret_cast<const float*>(ring + s * slotB);
     const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(ring + s * slotB + rowB);
     double yl = 0.0, off = 0.0, hx = 0.0;  // same grouping as pack_kernel => identical sums
-    float amax = 0.f, nanf = 0.f;  // nanf: sum of bs - bs (NaN iff some bs is NaN / inf)
+    float amax = 0.f;  // NaN-propagating: a NaN / inf row ends non-finite
     float bsr[IT][4];  // alpha * prop, kept for the operand pass
     // log-prior: the LpAcc product order without its per-chunk overflow
     // branch (factors are >= 1, so the running product can only overflow
@@ -552,8 +552,7 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
         fo = fmaf(p[i], g4[i], fo);
         if (CODED) fx = fmaf(p[i], x4[i], fx);
         if (CODED) {
-          amax = fmaxf(amax, fabsf(bs));
-          nanf += bs - bs;
+          amax = fmax_nan(amax, fabsf(bs));
         } else if (!(fabsf(bs) < kOpMax)) {
           fy = __int_as_float(0x7fc00000);
         }
@@ -573,8 +572,8 @@ __global__ void __launch_bounds__(32 * kPackWarps, 3) pack_eps_kernel(spa_design
     }
     if (CODED) {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-      if (__any_sync(0xffffffffu, nanf != 0.f)) amax = INFINITY;  // NaN / inf in the row
+      for (int o = 16; o > 0; o >>= 1) amax = fmax_nan(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      if (!(amax < INFINITY)) amax = INFINITY;  // NaN / inf in the row
     }
     double lpl;
     if (pc.de) {

@@ -39,6 +39,7 @@ from __future__ import annotations
 import ctypes
 import math
 import os
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -1121,10 +1122,15 @@ class _SnapshotWriter:
     def __init__(self):
         from concurrent.futures import ThreadPoolExecutor
 
-        self.pool = ThreadPoolExecutor(max_workers=1)
+        import threading
+
+        # two host workers, each with its own side stream and pinned staging
+        # buffer: a snapshot's float64 widening (page-faulting a fresh 262 MB
+        # array at C3) can take longer than the 10 steps between snapshots
+        self.pool = ThreadPoolExecutor(max_workers=2)
         self.jobs = []
-        self.stream = None
-        self.stage = None
+        self.local = threading.local()
+        self.wait_s = 0.0
 
     def submit(self, system: ParticleSystem, record: StepRecord, group=None):
         if group is None:
@@ -1138,25 +1144,30 @@ class _SnapshotWriter:
         ev = torch.cuda.Event()
         ev.record()
         dev = system.device
-        if len(self.jobs) >= 4:  # bound the device memory held by pending clones
+        while len(self.jobs) > 16 or (self.jobs and self.jobs[0].done()):
+            # bound the device memory held by pending clones (16 x 131 MB at C3)
+            t = time.perf_counter()
             self.jobs.pop(0).result()
+            self.wait_s += time.perf_counter() - t
         self.jobs.append(self.pool.submit(self._finish, record, clones, ev, dev))
         return record
 
     def _finish(self, record, clones, ev, dev):
         w, beta, ll = clones
         with torch.cuda.device(dev):
-            if self.stream is None:
-                self.stream = torch.cuda.Stream(dev)
-            if self.stage is None or self.stage.numel() < beta.numel():
-                self.stage = torch.empty(beta.numel(), dtype=torch.float32, pin_memory=True)
-            st = self.stage[: beta.numel()].view(beta.shape)
-            self.stream.wait_event(ev)
-            with torch.cuda.stream(self.stream):
+            loc = self.local
+            if getattr(loc, "stream", None) is None:
+                loc.stream = torch.cuda.Stream(dev)
+                loc.stage = None
+            if loc.stage is None or loc.stage.numel() < beta.numel():
+                loc.stage = torch.empty(beta.numel(), dtype=torch.float32, pin_memory=True)
+            st = loc.stage[: beta.numel()].view(beta.shape)
+            loc.stream.wait_event(ev)
+            with torch.cuda.stream(loc.stream):
                 st.copy_(beta, non_blocking=True)
                 wh = w.to("cpu", non_blocking=False)
                 llh = ll.to("cpu", non_blocking=False)
-            self.stream.synchronize()
+            loc.stream.synchronize()
         part = torch.empty(beta.shape, dtype=torch.float64)
         part.copy_(st)  # float32 -> float64 on host threads
         weights = wh.numpy().copy()
@@ -1216,11 +1227,10 @@ def run_sampler(data, a: float, schedule: Schedule, config: SmcConfig, intercept
 
 
 def _run_sampler(data, a: float, schedule: Schedule, config: SmcConfig, intercept: bool, group) -> SmcOutput:
-    import time
-
     timings = {}
     t0 = time.perf_counter()
     design = DeviceDesign.build(data.X, data.y, intercept)
+    timings["design_s"] = time.perf_counter() - t0
     prior1 = GtPrior(a, prior_scale(a, schedule.bs[0]))
     system, init_acc = init_particles(data, prior1, config, intercept, design=design, group=group)
     torch.cuda.synchronize()
@@ -1279,6 +1289,7 @@ def _run_sampler(data, a: float, schedule: Schedule, config: SmcConfig, intercep
     finally:
         writer.close()
     timings["snapshot_drain_s"] = time.perf_counter() - ts
+    timings["snapshot_wait_s"] = writer.wait_s
     timings["resampling_steps"] = sum(1 for s in steps if s.resampled)
     return SmcOutput(float(a), schedule, config, intercept, names, steps, init_acc, timings, pooled)
 
