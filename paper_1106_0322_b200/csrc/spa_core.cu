@@ -1410,33 +1410,60 @@ __global__ void __launch_bounds__(kLseThreads) lse_stats_kernel(const double* __
 
 // one thread: the fixed-order combine of the chunk statistics (L2 loads: in
 // reweight_finish_kernel other blocks wrote them, and L1 is not coherent)
-__device__ __forceinline__ void lse_combine_body(const double* __restrict__ stats, int64_t nchunks,
+// The chunk statistics' combine, one warp: lanes load and exponentiate the
+// chunks in parallel; lane 0 then accumulates s1, s2 in chunk order with the
+// sequential loop's exact arithmetic (fma(a, f, s1), fma(b f, f, s2)).  A
+// single thread doing the loads and exp()s one chunk after another spent
+// ~0.5 us per chunk on L2 latency (C3: 16 chunks, twice per lambda step).
+__device__ __forceinline__ void lse_combine_warp(const double* __restrict__ stats, int64_t nchunks,
                                                  double* __restrict__ res) {
+  const int lane = threadIdx.x & 31;
   double M = -INFINITY;
   bool nan = false;
-  for (int64_t c = 0; c < nchunks; ++c) {
+  for (int64_t c = lane; c < nchunks; c += 32) {
     const double v = __ldcg(&stats[3 * c]);
     if (v != v) nan = true;
     M = fmax(M, v);
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
+  nan = __any_sync(0xffffffffu, nan);
   double s1 = 0.0, s2 = 0.0;
   if (M > -INFINITY && !nan) {
-    for (int64_t c = 0; c < nchunks; ++c) {
-      const double mc = __ldcg(&stats[3 * c]);
-      if (mc == -INFINITY) continue;
-      const double f = exp(mc - M);
-      s1 += __ldcg(&stats[3 * c + 1]) * f;
-      s2 += __ldcg(&stats[3 * c + 2]) * f * f;
+    for (int64_t base = 0; base < nchunks; base += 32) {
+      const int64_t c = base + lane;
+      double av = 0.0, bv = 0.0, f = 0.0;
+      int live = 0;
+      if (c < nchunks) {
+        const double mc = __ldcg(&stats[3 * c]);
+        if (mc != -INFINITY) {
+          live = 1;
+          f = exp(mc - M);
+          av = __ldcg(&stats[3 * c + 1]);
+          bv = __ldcg(&stats[3 * c + 2]);
+        }
+      }
+      const int cnt = nchunks - base < 32 ? (int)(nchunks - base) : 32;
+      for (int l = 0; l < cnt; ++l) {
+        const double al = __shfl_sync(0xffffffffu, av, l), bl = __shfl_sync(0xffffffffu, bv, l);
+        const double fl = __shfl_sync(0xffffffffu, f, l);
+        if (__shfl_sync(0xffffffffu, live, l)) {
+          s1 = fma(al, fl, s1);
+          s2 = fma(bl * fl, fl, s2);
+        }
+      }
     }
   }
-  res[0] = nan ? NAN : (M > -INFINITY ? M + log(s1) : -INFINITY);
-  res[1] = nan ? NAN : s1 * s1 / s2;
-  res[2] = M;
+  if (lane == 0) {
+    res[0] = nan ? NAN : (M > -INFINITY ? M + log(s1) : -INFINITY);
+    res[1] = nan ? NAN : s1 * s1 / s2;
+    res[2] = M;
+  }
 }
 
 __global__ void lse_combine_kernel(const double* __restrict__ stats, int64_t nchunks, double* __restrict__ res) {
-  if (threadIdx.x != 0) return;
-  lse_combine_body(stats, nchunks, res);
+  if (threadIdx.x >= 32) return;
+  lse_combine_warp(stats, nchunks, res);
 }
 
 __global__ void logw_apply_kernel(double* __restrict__ logw, const double* __restrict__ lw, int64_t m,
@@ -1564,9 +1591,9 @@ __global__ void __launch_bounds__(kLseThreads) reweight_finish_kernel(double* lo
   const int64_t c = blockIdx.x;
   lse_chunk_stats(logw, lw, m, stats, c, red);
   grid.sync();
-  if (c == 0 && threadIdx.x == 0) {
-    lse_combine_body(stats, nchunks, res);
-    step_record_body(res, rec, t, ess_threshold);
+  if (c == 0 && threadIdx.x < 32) {
+    lse_combine_warp(stats, nchunks, res);
+    if (threadIdx.x == 0) step_record_body(res, rec, t, ess_threshold);
   }
   grid.sync();
   constexpr int kPer = kChunk / kLseThreads;
@@ -1579,7 +1606,7 @@ __global__ void __launch_bounds__(kLseThreads) reweight_finish_kernel(double* lo
   __syncthreads();
   lse_chunk_stats(logw, nullptr, m, stats, c, red);  // this block's own updated chunk
   grid.sync();
-  if (c == 0 && threadIdx.x == 0) lse_combine_body(stats, nchunks, res);
+  if (c == 0 && threadIdx.x < 32) lse_combine_warp(stats, nchunks, res);
   grid.sync();
   const double r1 = __ldcg(&res[0]);
 #pragma unroll
