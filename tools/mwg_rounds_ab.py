@@ -1,6 +1,6 @@
 """A/B of blocked MwG rounds (spa_mwg_set_rounds): per-coordinate latency of
 the initialisation chains (K chains x sweeps, chain layout) and the whole
-C3 init_particles (2000 burn sweeps), for rounds 1 / 2 / 4.
+C3 init_particles (2000 burn sweeps), for the rounds in ROUNDS (default 1,2,4).
     python tools/mwg_rounds_ab.py [name=c3]"""
 import ctypes
 import os
@@ -17,6 +17,7 @@ from paper_1106_0322_b200.design import DeviceDesign  # noqa: E402
 from paper_1106_0322_b200.smc import _p, _stream  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
+R = [int(v) for v in os.environ.get("ROUNDS", "1,2,4").split(",")]  # rounds to compare
 data, _ = simulate_dataset(named_spec(name))
 d = DeviceDesign.build(data.X, data.y)
 
@@ -47,7 +48,7 @@ def chain_time(K, sweeps, rounds):
 
 for K in (148, 296):
     ref = None
-    for rounds in (1, 2, 4):
+    for rounds in R:
         ms, acc, b = chain_time(K, 40, rounds)
         same = "" if ref is None else (" identical" if torch.equal(ref, b) else " DIFFERENT")
         ref = b if ref is None else ref
@@ -56,7 +57,7 @@ for K in (148, 296):
 
 cfg = S.SmcConfig(N=65536, move_kernel="rw", moves=5, seed=1, init_burn=2000, init_thin=5)
 prior1 = S.GtPrior(1.0, 2.0)
-for rounds in (4, 2, 4):
+for rounds in R + R[:1]:
     _lib.call("spa_mwg_set_rounds", rounds, 1)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -67,7 +68,7 @@ for rounds in (4, 2, 4):
     del sysm
 # the lambda-step move (throughput layout): one call of 5 sweeps over M particles
 M = 16384
-for mr in (1, 2, 4, 1, 2, 4):
+for mr in R + R:
     _lib.call("spa_mwg_set_rounds", 4, mr)
     s = S.ParticleSystem(d, M, 1.0)
     s.beta.normal_(0.0, 0.05)
