@@ -2946,7 +2946,16 @@ int spa_rw_increments(int64_t m, int32_t q, int32_t ldb, const void* Lb, const v
   // column tile per item were measured no faster: DESIGN.md section 9)
   constexpr int kPropBN = 256;
   args.n_tiles = (q + kPropBN - 1) / kPropBN;
-  args.tiles_per_unit = args.n_tiles;
+  // q <= 512: the two column tiles (4 and 8 k-blocks under the triangle) are
+  // separate work items, alternating between rounds per CTA (tc_gemm.cuh
+  // item_range): 1024 items balance over 148 CTAs better than 512 whole
+  // m-tiles (3 or 4 per CTA); propose 103.4 -> 101.2 us at C3
+  static const int lz_units = [] {
+    const char* e = getenv("SPA_LZ_UNITS");  // developer A/B knob
+    return e ? atoi(e) : 2;
+  }();
+  const int units = (lz_units == 2 && args.n_tiles == 2) ? 2 : 1;
+  args.tiles_per_unit = units == 1 ? args.n_tiles : 1;
   args.kb_per_unit = 0;
   args.tri_b = 1;  // L is lower triangular: column tile nt needs k < (nt + 1) BN only
   auto* epsb = reinterpret_cast<__nv_bfloat16*>(eps);
@@ -2955,8 +2964,9 @@ int spa_rw_increments(int64_t m, int32_t q, int32_t ldb, const void* Lb, const v
                                         (uint64_t)m * ldb);
   if (rc) return rc;
   epi.m = (int)m;
-  return launch_tc<1, 1, kPropBN, EpiStoreT<__nv_bfloat16>>(Z, (uint64_t)kq, Lb, (uint64_t)kq, (uint64_t)q, args, 1,
-                                                            epi, st);
+  epi.slabs = 0;
+  return launch_tc<1, 1, kPropBN, EpiStoreT<__nv_bfloat16>>(Z, (uint64_t)kq, Lb, (uint64_t)kq, (uint64_t)q, args,
+                                                            units, epi, st);
 }
 
 int spa_rw_pack(const spa_design* d, const float* beta, int64_t m, int32_t ldb, const void* eps, void* A,

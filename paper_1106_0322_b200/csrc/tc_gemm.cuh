@@ -103,6 +103,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   auto item_range = [&](int w, int& mt, int& unit, int& nt0, int& nt1, int& kb0, int& kb1) {
     mt = w / units * TM;
     unit = w % units;
+    // triangular B with two column units: unit 1 costs twice unit 0 (8 vs 4
+    // k-blocks at q = 512), and with an even grid CTA b would always draw the
+    // same unit (odd CTAs twice the work: SMs 26% idle in the L z GEMM), so
+    // the unit alternates between rounds (a bijection: an m-tile's two items
+    // never straddle a round when the grid is even)
+    if (args.tri_b && units == 2 && (gridDim.x & 1) == 0) unit ^= (w / gridDim.x) & 1;
     if (args.kb_per_unit > 0) {
       nt0 = 0;
       nt1 = args.n_tiles;
@@ -326,6 +332,7 @@ struct EpiStoreT {
   static constexpr int kSmemBytes = 4 * 2 * kBoxBytes;
   CUtensorMap tmc;
   int m;
+  int slabs = 1;  // 1: unit u stores into slab u (split-K partials); 0: column units share one output
   struct State {
     uint8_t* scratch;
     int unit;
@@ -337,7 +344,7 @@ struct EpiStoreT {
     s.nbuf = 0;
     if ((threadIdx.x & 31) == 0) prefetch_tmap(&tmc);
   }
-  __device__ __forceinline__ void begin_unit(State& s, int, int unit, int, int) const { s.unit = unit; }
+  __device__ __forceinline__ void begin_unit(State& s, int, int unit, int, int) const { s.unit = slabs ? unit : 0; }
   __device__ __forceinline__ void consume(State& s, int row, int col0, const float (&v)[32], int) const {
     const int lane = threadIdx.x & 31;
     const int row0 = row - lane;  // warp-uniform
