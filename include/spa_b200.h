@@ -168,7 +168,9 @@ int spa_step_record(const double* res, double* rec, int64_t t, double ess_thresh
  * spa_step_record(t) -> spa_logw_apply(logw, lw) -> the statistics and
  * combine of the new logw -> w = exp(logw - lse) (stats / res end as after
  * that last combine); bit-identical to those calls (reference smc.py:151-157,
- * 171-174, 248-262).  m <= spa_reweight_finish_max_particles(). */
+ * 171-174, 248-262).  m <= spa_reweight_finish_max_particles().  stats holds
+ * 6 ceil(m / 4096) doubles: the first half ends as the chunk statistics of the
+ * new logw, the second half is scratch. */
 int spa_reweight_finish(double* logw, const double* lw, int64_t m, double* stats, double* res, double* rec, int64_t t,
                         double ess_threshold, double* w, void* stream);
 int spa_reweight_finish_max_particles(void);

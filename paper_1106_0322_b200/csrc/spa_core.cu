@@ -1580,7 +1580,10 @@ __global__ void step_record_kernel(const double* __restrict__ res, double* __res
 // record, logw <- logw + lw - lse, the statistics of the new logw, their
 // combine and the normalised weights w = exp(logw - lse) -- the arithmetic of
 // lse_stats / lse_combine / logw_apply / step_record / logw_apply(w), in the
-// same order (bit-identical), with grid barriers instead of seven launches.
+// same order (bit-identical).  Every block runs the (deterministic) combine
+// itself, so two grid barriers suffice (one per set of chunk statistics);
+// the second set goes to stats[nchunks..2 nchunks) and each block copies its
+// own entry down at the end (stats ends as after the last combine).
 __global__ void __launch_bounds__(kLseThreads) reweight_finish_kernel(double* logw, const double* __restrict__ lw,
                                                                       int64_t m, double* stats, int64_t nchunks,
                                                                       double* res, double* rec, int64_t t,
@@ -1588,27 +1591,36 @@ __global__ void __launch_bounds__(kLseThreads) reweight_finish_kernel(double* lo
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ double red[32];
+  __shared__ double rs[3];
   const int64_t c = blockIdx.x;
+  double* stats2 = stats + 3 * nchunks;
   lse_chunk_stats(logw, lw, m, stats, c, red);
   grid.sync();
-  if (c == 0 && threadIdx.x < 32) {
-    lse_combine_warp(stats, nchunks, res);
-    if (threadIdx.x == 0) step_record_body(res, rec, t, ess_threshold);
+  if (threadIdx.x < 32) {
+    lse_combine_warp(stats, nchunks, rs);
+    if (c == 0 && threadIdx.x == 0) {
+      res[0] = rs[0];
+      res[1] = rs[1];
+      res[2] = rs[2];
+      step_record_body(rs, rec, t, ess_threshold);
+    }
   }
-  grid.sync();
+  __syncthreads();
   constexpr int kPer = kChunk / kLseThreads;
-  const double r0 = __ldcg(&res[0]);  // written by block 0 (L2: L1 is not coherent across SMs)
+  const double r0 = rs[0];
 #pragma unroll
   for (int i = 0; i < kPer; ++i) {
     const int64_t k = c * kChunk + threadIdx.x + i * kLseThreads;
     if (k < m) logw[k] = logw[k] + lw[k] - r0;
   }
   __syncthreads();
-  lse_chunk_stats(logw, nullptr, m, stats, c, red);  // this block's own updated chunk
+  lse_chunk_stats(logw, nullptr, m, stats2, c, red);  // this block's own updated chunk
   grid.sync();
-  if (c == 0 && threadIdx.x < 32) lse_combine_warp(stats, nchunks, res);
-  grid.sync();
-  const double r1 = __ldcg(&res[0]);
+  if (threadIdx.x < 32) lse_combine_warp(stats2, nchunks, rs);
+  __syncthreads();
+  const double r1 = rs[0];
+  if (c == 0 && threadIdx.x < 3) res[threadIdx.x] = rs[threadIdx.x];
+  if (threadIdx.x < 3) stats[3 * c + threadIdx.x] = __ldcg(&stats2[3 * c + threadIdx.x]);
 #pragma unroll
   for (int i = 0; i < kPer; ++i) {
     const int64_t k = c * kChunk + threadIdx.x + i * kLseThreads;

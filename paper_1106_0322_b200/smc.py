@@ -265,6 +265,7 @@ class ParticleSystem:
         self.w = torch.empty(self.N, **f64)
         self.nchunks = -(-self.N // _CHUNK)
         self.stats = torch.empty((self.nchunks, 3), **f64)
+        self.stats_rwf = torch.empty((2 * self.nchunks, 3), **f64)  # spa_reweight_finish: two sets
         self.res = torch.empty(3, **f64)
         self.counter = torch.zeros(1, dtype=torch.int64, device=dev)
         self._rw = None
@@ -941,7 +942,7 @@ def _smc_step_async(system: ParticleSystem, schedule: Schedule, t: int, config: 
               float(prior_t.a), float(prior_t.c), float(prior_prev.c), _p(system.lw), _p(system.lp), _stream())
     fused = group is None and system.N <= _reweight_finish_limit()
     if fused:  # the weight update, step record and normalised weights in one cooperative launch
-        _lib.call("spa_reweight_finish", _p(system.logw), _p(system.lw), system.N, _p(system.stats), _p(system.res),
+        _lib.call("spa_reweight_finish", _p(system.logw), _p(system.lw), system.N, _p(system.stats_rwf), _p(system.res),
                   _p(rec), t, float(config.ess_threshold_frac * N), _p(system.w), _stream())
     else:
         _lib.call("spa_lse_chunk_stats", _p(system.logw), _p(system.lw), system.N, _p(system.stats), _stream())

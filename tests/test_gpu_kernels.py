@@ -630,14 +630,15 @@ def test_reweight_finish_matches_kernel_sequence(m):
     outs = []
     for fused in (False, True):
         logw = logw0.clone()
-        stats = torch.zeros((nch, 3), dtype=torch.float64, device="cuda")
+        stats = torch.zeros((2 * nch if fused else nch, 3), dtype=torch.float64, device="cuda")
         res = torch.zeros(3, dtype=torch.float64, device="cuda")
         rec = torch.zeros((10, 4), dtype=torch.float64, device="cuda")
         rec[2, 3] = 1.25
         w = torch.zeros(m, dtype=torch.float64, device="cuda")
-        if fused:
+        if fused:  # stats: the final chunk statistics, then a scratch set
             _lib.call("spa_reweight_finish", _p(logw), _p(lw), m, _p(stats), _p(res), _p(rec), 3, 0.75 * m, _p(w),
                       _stream())
+            stats = stats[:nch]
         else:
             _lib.call("spa_lse_chunk_stats", _p(logw), _p(lw), m, _p(stats), _stream())
             _lib.call("spa_lse_combine", _p(stats), nch, _p(res), _stream())
