@@ -24,6 +24,7 @@
 #include "resample.cuh"
 #include "tc_gemm.cuh"
 #include "tc_k1_i8.cuh"
+#include "tc_lz_pair.cuh"
 
 namespace spa {
 
@@ -2977,6 +2978,33 @@ int spa_rw_increments(int64_t m, int32_t q, int32_t ldb, const void* Lb, const v
   if (rc) return rc;
   epi.m = (int)m;
   epi.slabs = 0;
+  static const bool pair = [] {
+    const char* e = getenv("SPA_LZ_PAIR");  // developer A/B knob: 0 = the single-CTA engine
+    return !(e && atoi(e) == 0);
+  }();
+  if (pair) {  // CTA pairs (tc_lz_pair.cuh)
+    CUtensorMap tz, tl;
+    rc = make_tmap_bf16(&tz, Z, (uint64_t)kq, (uint64_t)m, 128);
+    if (rc) return rc;
+    rc = make_tmap_bf16(&tl, Lb, (uint64_t)kq, (uint64_t)q, 128);
+    if (rc) return rc;
+    static int nsm = 0;
+    if (nsm == 0) {
+      int dev = 0;
+      SPA_CHECK_CUDA(cudaGetDevice(&dev));
+      SPA_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+      SPA_CHECK_CUDA(cudaFuncSetAttribute(lz_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLzSmem));
+    }
+    LzArgs la;
+    la.m = (int)m;
+    la.kq = kq;
+    la.mtp = (int)((m + 255) / 256);
+    la.n_tiles = (q + kLzBN - 1) / kLzBN;
+    const int nclus = std::min(la.mtp * la.n_tiles, nsm / 2);
+    lz_pair_kernel<<<2 * nclus, kLzThreads, kLzSmem, st>>>(tz, tl, la, epi);
+    SPA_CHECK_LAUNCH();
+    return 0;
+  }
   return launch_tc<1, 1, kPropBN, EpiStoreT<__nv_bfloat16>>(Z, (uint64_t)kq, Lb, (uint64_t)kq, (uint64_t)q, args,
                                                             units, epi, st);
 }
@@ -3090,7 +3118,7 @@ int spa_prepare(void) {
       (const void*)pack_eps_kernel<4, false>, (const void*)pack_eps_kernel<8, false>,
       (const void*)pack_eps_rows_kernel<4, 16, true>, (const void*)pack_eps_rows_kernel<8, 16, true>,
       (const void*)pack_eps_rows_kernel<4, 16, false>, (const void*)pack_eps_rows_kernel<8, 16, false>,
-      (const void*)k1_i8_pair_kernel<true>, (const void*)k1_i8_pair_kernel<false>, (const void*)prior_kernel,
+      (const void*)k1_i8_pair_kernel<true>, (const void*)k1_i8_pair_kernel<false>, (const void*)lz_pair_kernel, (const void*)prior_kernel,
       (const void*)prior_reweight_rows_kernel<8, 4>, (const void*)prior_reweight_rows_kernel<8, 8>,
       (const void*)prior_reweight_rows_kernel<16, 8>, (const void*)prior_reweight_rows_kernel<16, 16>,
       (const void*)prior_reweight_rows_kernel<32, 16>, (const void*)prior_reweight_kernel<32>, (const void*)lse_stats_kernel, (const void*)lse_combine_kernel,
