@@ -15,7 +15,7 @@ full() {  # name regex
 }
 full k1 k1_i8_pair
 full pack pack_eps_rows
-full lz 'tc_gemm_kernel.*EpiStoreT<__nv_bfloat16>'
+full lz lz_pair
 full accept rw_accept_kernel
 $NCU --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base demangled \
   -k regex:reweight_finish --launch-count 1 -o gpurun_out/prof2d/rwf $B > gpurun_out/prof2d/ncu_rwf.log 2>&1
