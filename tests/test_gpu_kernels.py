@@ -520,14 +520,15 @@ def test_rw_factor_under_contention():
         assert torch.equal(L.cpu(), ref)
 
 
-@pytest.mark.parametrize("name", ["c2", "c3"])
-def test_rw_propose_eps_multi_tile(name):
-    """eps = L z of spa_rw_propose at q = 200 / 500 (several K blocks and
-    column tiles of the tcgen05 GEMM) equals the float32 product of the same
-    bf16 operands to bf16 output rounding."""
+@pytest.mark.parametrize("name,N", [("c1", 1536 + 77), ("c2", 1536), ("c3", 1536), ("c5", 1536 + 77)])
+def test_rw_propose_eps_multi_tile(name, N):
+    """eps = L z of spa_rw_propose at q = 20 / 200 / 500 / 1000 (one to four
+    256-coordinate tiles of the CTA-pair kernel, several K blocks, a ragged
+    last pair of particle tiles) equals the float32 product of the same bf16
+    operands to bf16 output rounding."""
     from paper_1106_0322_b200.smc import _round_up
 
-    data, d, s, B = _rw_setup(name, N=1536)
+    data, d, s, B = _rw_setup(name, N=N)
     from paper_1106_0322_b200.smc import _rw_factor
 
     _rw_factor(s, 2.38)
