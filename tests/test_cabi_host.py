@@ -60,6 +60,10 @@ def test_sass_contains_tcgen05_and_tma():
     # the int8 likelihood kernel: CTA-pair integer MMAs and pair-scoped TMA loads
     assert "UTCIMMA.2CTA" in sass and "UTMALDG.2D.2CTA" in sass
     assert "IMMA" not in sass.replace("UTCIMMA", "")
+    # the proposal increments L z: CTA-pair bf16 MMAs in lz_pair_kernel
+    i = sass.index("lz_pair_kernel")
+    body = sass[i: sass.find("Function :", i + 1)]
+    assert "UTCHMMA.2CTA" in body and "UTMALDG.2D.2CTA" in body and "UTMASTG" in body
 
 
 class TestConfig:
