@@ -600,6 +600,7 @@ def _launch_normals(system: ParticleSystem, config: SmcConfig, t: int, mv: int):
 
 
 _NORMALS_AHEAD = 2  # moves between a move's normals being drawn and used
+_NORMALS_AFTER_K1 = os.environ.get("SPA_NORMALS_AFTER_K1", "0") == "1"  # A/B knob
 
 
 def _normals_key(system: ParticleSystem, config: SmcConfig, t: int, mv: int):
@@ -700,6 +701,8 @@ def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int,
                       _p(ws["ws"]), ws["ws"].numel(), _stream())
         if KERNEL_TIMER is not None:
             KERNEL_TIMER.stop("loglik")
+        if _NORMALS_AFTER_K1:
+            _normals_ahead(system, config, t, mv)
         if lag and mv == 0:
             main.wait_event(centred)  # the factor stream has read the particles
         if fused:
@@ -711,7 +714,8 @@ def _rw_moves(system: ParticleSystem, prior: GtPrior, config: SmcConfig, t: int,
             _lib.call("spa_rw_accept", _p(system.beta), system.ldb, _p(rw["prop"]), system.q, system.N,
                       _p(ws["ylin"]), _p(ws["sp"]), _p(rw["lp_p"]), _p(system.ll), _p(system.lp), int(config.seed),
                       int(t), int(system.i0), mv, _p(system.counter), _stream())
-        _normals_ahead(system, config, t, mv)
+        if not _NORMALS_AFTER_K1:
+            _normals_ahead(system, config, t, mv)
     if lag == 2:
         system._factored = factored
     system._fcur = nxt
